@@ -1,0 +1,1062 @@
+// lmra_oracle.cpp -- CPU restatement of the reference's randomized Tucker hot path.
+//
+// TEST INFRASTRUCTURE ONLY (see lmra_oracle.h).  Compiled with -ffp-contract=off so
+// every a*b+c the reference writes is two roundings, exactly as in the reference
+// sources; the only fused operations are the explicit std::fma in the canonical
+// column-norm order.
+#include "lmra_oracle.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <functional>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+// ---------------------------------------------------------------- BLAS/LAPACK
+using i64 = long long;
+typedef void (*dgemm_t)(const char*, const char*, const i64*, const i64*, const i64*,
+                        const double*, const double*, const i64*, const double*, const i64*,
+                        const double*, double*, const i64*, size_t, size_t);
+typedef void (*dgesdd_t)(const char*, const i64*, const i64*, double*, const i64*, double*,
+                         double*, const i64*, double*, const i64*, double*, const i64*, i64*,
+                         i64*, size_t);
+typedef void (*dgeqrf_t)(const i64*, const i64*, double*, const i64*, double*, double*,
+                         const i64*, i64*);
+typedef void (*dorgqr_t)(const i64*, const i64*, const i64*, double*, const i64*,
+                         const double*, double*, const i64*, i64*);
+typedef void (*setthreads_t)(int);
+
+struct Blas {
+  dgemm_t dgemm = nullptr;
+  dgesdd_t dgesdd = nullptr;
+  dgeqrf_t dgeqrf = nullptr;
+  dorgqr_t dorgqr = nullptr;
+  setthreads_t set_threads = nullptr;
+} g_blas;
+
+void need_blas() {
+  if (!g_blas.dgemm) throw std::runtime_error("oracle: BLAS not initialised (orc_init_blas)");
+}
+
+// ---------------------------------------------------------------- RNG, rng.hpp:20-66
+struct Rng {
+  uint64_t state = 0, inc = 1;
+  double cached = 0.0;
+  bool has_cached = false;
+  Rng(uint64_t seed, uint64_t stream) {  // rng.hpp:22-28
+    inc = (stream << 1u) | 1u;
+    state = 0;
+    next_u32();
+    state += seed;
+    next_u32();
+  }
+  uint32_t next_u32() {  // rng.hpp:30-36
+    uint64_t old = state;
+    state = old * 6364136223846793005ULL + inc;
+    uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (xs >> rot) | (xs << ((32u - rot) & 31u));
+  }
+  double next_double() {  // rng.hpp:39-44
+    uint64_t hi = next_u32();
+    uint64_t lo = next_u32();
+    uint64_t x = (hi << 32) | lo;
+    return static_cast<double>(x >> 11) * 0x1.0p-53;
+  }
+  double next_normal() {  // rng.hpp:47-59
+    if (has_cached) {
+      has_cached = false;
+      return cached;
+    }
+    double u1 = 1.0 - next_double();
+    double u2 = next_double();
+    double r = std::sqrt(-2.0 * std::log(u1));
+    double a = 6.283185307179586476925286766559 * u2;
+    cached = r * std::sin(a);
+    has_cached = true;
+    return r * std::cos(a);
+  }
+  // LCG jump-ahead by `delta` u32 draws (O(log delta)); used only to split long
+  // normal sequences across threads, bit-identical to sequential generation.
+  void advance(uint64_t delta) {
+    uint64_t cur_mult = 6364136223846793005ULL, cur_plus = inc;
+    uint64_t acc_mult = 1, acc_plus = 0;
+    while (delta > 0) {
+      if (delta & 1) {
+        acc_mult *= cur_mult;
+        acc_plus = acc_plus * cur_mult + cur_plus;
+      }
+      cur_plus = (cur_mult + 1) * cur_plus;
+      cur_mult *= cur_mult;
+      delta >>= 1;
+    }
+    state = acc_mult * state + acc_plus;
+  }
+};
+
+// Fills out[0..n) with normals n0, n0+1, ... of stream (seed, stream): element e is the
+// cos (e even) or sin (e odd) half of Box-Muller pair e/2, which consumes draws 4(e/2)..+3.
+void fill_normals(uint64_t seed, uint64_t stream, double* out, size_t n, int threads) {
+  auto work = [&](size_t b, size_t e) {
+    if (b >= e) return;
+    Rng g(seed, stream);
+    size_t pair = b / 2;
+    g.advance(4 * pair);
+    size_t i = b;
+    if (i & 1) {  // start on the sin half
+      g.next_normal();
+      out[i++] = g.next_normal();
+    }
+    for (; i < e; ++i) out[i] = g.next_normal();
+  };
+  if (threads <= 1 || n < (1u << 20)) {
+    work(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  size_t chunk = ((n + threads - 1) / threads + 1) & ~size_t(1);
+  for (int t = 0; t < threads; ++t) {
+    size_t b = std::min(n, t * chunk), e = std::min(n, b + chunk);
+    pool.emplace_back(work, b, e);
+  }
+  for (auto& t : pool) t.join();
+}
+
+int default_threads() {
+  unsigned h = std::thread::hardware_concurrency();
+  return h ? static_cast<int>(h) : 1;
+}
+
+// ---------------------------------------------------------------- dense types
+struct Mat {  // column-major
+  size_t r = 0, c = 0;
+  std::vector<double> d;
+  Mat() = default;
+  Mat(size_t r_, size_t c_) : r(r_), c(c_), d(r_ * c_, 0.0) {}
+  double& operator()(size_t i, size_t j) { return d[i + r * j]; }
+  double operator()(size_t i, size_t j) const { return d[i + r * j]; }
+};
+
+struct Tensor {
+  std::vector<size_t> dims;
+  std::vector<double> v;
+  Tensor() = default;
+  explicit Tensor(std::vector<size_t> d) : dims(std::move(d)) {
+    size_t n = 1;
+    for (size_t x : dims) n *= x;
+    v.assign(n, 0.0);
+  }
+  size_t size() const { return v.size(); }
+};
+
+// C = op(A) * op(B), all column-major
+void gemm(bool ta, bool tb, size_t m, size_t n, size_t k, const double* a, size_t lda,
+          const double* b, size_t ldb, double* c, size_t ldc, double beta = 0.0) {
+  need_blas();
+  if (m == 0 || n == 0) return;
+  i64 M = (i64)m, N = (i64)n, K = (i64)k, LA = (i64)std::max<size_t>(lda, 1),
+      LB = (i64)std::max<size_t>(ldb, 1), LC = (i64)std::max<size_t>(ldc, 1);
+  double one = 1.0;
+  g_blas.dgemm(ta ? "T" : "N", tb ? "T" : "N", &M, &N, &K, &one, a, &LA, b, &LB, &beta, c, &LC,
+               1, 1);
+}
+
+Mat matmul(const Mat& a, bool ta, const Mat& b, bool tb) {
+  size_t m = ta ? a.c : a.r, k = ta ? a.r : a.c, n = tb ? b.r : b.c;
+  size_t k2 = tb ? b.c : b.r;
+  if (k != k2) throw std::invalid_argument("matmul: inner dimensions differ");
+  Mat out(m, n);
+  gemm(ta, tb, m, n, k, a.d.data(), a.r, b.d.data(), b.r, out.d.data(), m);
+  return out;
+}
+
+// ---------------------------------------------------------------- tensor.cpp:60-139
+void inner_outer(const std::vector<size_t>& dims, size_t mode, size_t& inner, size_t& outer) {
+  inner = 1;
+  for (size_t k = 0; k < mode; ++k) inner *= dims[k];
+  outer = 1;
+  for (size_t k = mode + 1; k < dims.size(); ++k) outer *= dims[k];
+}
+
+Mat unfold(const Tensor& t, size_t mode) {  // tensor.cpp:60-86
+  size_t rows = t.dims[mode], inner, outer;
+  inner_outer(t.dims, mode, inner, outer);
+  Mat m(rows, inner * outer);
+  if (mode == 0) {
+    std::memcpy(m.d.data(), t.v.data(), sizeof(double) * t.size());
+    return m;
+  }
+  const double* src = t.v.data();
+  double* dst = m.d.data();
+  for (size_t o = 0; o < outer; ++o)
+    for (size_t r = 0; r < rows; ++r) {
+      const double* s = src + (o * rows + r) * inner;
+      double* d = dst + r + o * inner * rows;
+      for (size_t i = 0; i < inner; ++i) d[i * rows] = s[i];
+    }
+  return m;
+}
+
+Tensor fold(const Mat& m, size_t mode, const std::vector<size_t>& dims) {  // tensor.cpp:88-116
+  size_t rows = dims[mode], inner, outer;
+  inner_outer(dims, mode, inner, outer);
+  if (m.r != rows || m.c != inner * outer)
+    throw std::invalid_argument("fold: matrix shape does not match target dims");
+  Tensor t(dims);
+  if (mode == 0) {
+    std::memcpy(t.v.data(), m.d.data(), sizeof(double) * t.size());
+    return t;
+  }
+  const double* src = m.d.data();
+  double* dst = t.v.data();
+  for (size_t o = 0; o < outer; ++o)
+    for (size_t r = 0; r < rows; ++r) {
+      const double* s = src + r + o * inner * rows;
+      double* d = dst + (o * rows + r) * inner;
+      for (size_t i = 0; i < inner; ++i) d[i] = s[i * rows];
+    }
+  return t;
+}
+
+Tensor mode_n_product(const Tensor& t, const Mat& b, size_t mode) {  // tensor.cpp:118-139
+  if (mode >= t.dims.size()) throw std::out_of_range("mode_n_product: mode out of range");
+  if (b.c != t.dims[mode])
+    throw std::invalid_argument(
+        "mode_n_product: matrix columns must match tensor mode dimension");
+  std::vector<size_t> od = t.dims;
+  od[mode] = b.r;
+  if (mode == 0) {
+    size_t cols = t.size() / t.dims[0];
+    Tensor out(od);
+    gemm(false, false, b.r, cols, t.dims[0], b.d.data(), b.r, t.v.data(), t.dims[0],
+         out.v.data(), b.r);
+    return out;
+  }
+  Mat m = unfold(t, mode);
+  Mat r = matmul(b, false, m, false);
+  return fold(r, mode, od);
+}
+
+Mat transpose(const Mat& a) {
+  Mat t(a.c, a.r);
+  for (size_t j = 0; j < a.c; ++j)
+    for (size_t i = 0; i < a.r; ++i) t(j, i) = a(i, j);
+  return t;
+}
+
+// ---------------------------------------------------------------- linalg.cpp:12-99
+void fix_signs(Mat& u, Mat& v) {  // linalg.cpp:13-29
+  for (size_t k = 0; k < u.c; ++k) {
+    size_t imax = 0;
+    double best = 0.0;
+    for (size_t i = 0; i < u.r; ++i) {
+      double a = std::abs(u(i, k));
+      if (a > best) {
+        best = a;
+        imax = i;
+      }
+    }
+    if (u(imax, k) < 0.0) {
+      for (size_t i = 0; i < u.r; ++i) u(i, k) = -u(i, k);
+      if (k < v.c)
+        for (size_t i = 0; i < v.r; ++i) v(i, k) = -v(i, k);
+    }
+  }
+}
+
+struct Svd {
+  Mat U;
+  std::vector<double> S;
+  Mat V;
+};
+
+Svd thin_svd(const Mat& m) {  // linalg.cpp:33-43 (BDCSVD -> LAPACK dgesdd)
+  need_blas();
+  i64 M = (i64)m.r, N = (i64)m.c, mn = std::min(M, N);
+  Svd out;
+  out.U = Mat(m.r, (size_t)mn);
+  out.S.assign((size_t)mn, 0.0);
+  Mat vt((size_t)mn, m.c);
+  if (mn == 0) return out;
+  std::vector<double> a = m.d;
+  std::vector<i64> iwork(8 * (size_t)mn);
+  i64 lwork = -1, info = 0;
+  double wq = 0;
+  i64 ldu = std::max<i64>(M, 1), ldvt = std::max<i64>(mn, 1), lda = std::max<i64>(M, 1);
+  g_blas.dgesdd("S", &M, &N, a.data(), &lda, out.S.data(), out.U.d.data(), &ldu, vt.d.data(),
+                &ldvt, &wq, &lwork, iwork.data(), &info, 1);
+  lwork = (i64)wq + 1;
+  std::vector<double> work((size_t)lwork);
+  g_blas.dgesdd("S", &M, &N, a.data(), &lda, out.S.data(), out.U.d.data(), &ldu, vt.d.data(),
+                &ldvt, work.data(), &lwork, iwork.data(), &info, 1);
+  if (info != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  out.V = transpose(vt);
+  fix_signs(out.U, out.V);
+  return out;
+}
+
+Mat thin_qr_q(const Mat& m) {  // linalg.cpp:52-60 (HouseholderQR -> dgeqrf/dorgqr)
+  need_blas();
+  if (m.r < m.c) throw std::invalid_argument("thin_qr: requires rows >= cols");
+  i64 M = (i64)m.r, N = (i64)m.c, lda = std::max<i64>(M, 1), info = 0, lwork = -1;
+  Mat q = m;
+  std::vector<double> tau((size_t)std::max<i64>(N, 1));
+  double wq = 0;
+  g_blas.dgeqrf(&M, &N, q.d.data(), &lda, tau.data(), &wq, &lwork, &info);
+  lwork = (i64)wq + 1;
+  std::vector<double> work((size_t)lwork);
+  g_blas.dgeqrf(&M, &N, q.d.data(), &lda, tau.data(), work.data(), &lwork, &info);
+  lwork = -1;
+  g_blas.dorgqr(&M, &N, &N, q.d.data(), &lda, tau.data(), &wq, &lwork, &info);
+  lwork = (i64)wq + 1;
+  work.assign((size_t)lwork, 0.0);
+  g_blas.dorgqr(&M, &N, &N, q.d.data(), &lda, tau.data(), work.data(), &lwork, &info);
+  if (info != 0) throw std::runtime_error("thin_qr: LAPACK failure");
+  return q;
+}
+
+Mat gram_power_apply(const Mat& a, const Mat& g, int q, int strategy) {  // linalg.cpp:62-80
+  if (g.r != a.r) throw std::invalid_argument("gram_power_apply: G must have as many rows as A");
+  if (q < 1) throw std::invalid_argument("gram_power_apply: q must be >= 1");
+  Mat c = g;
+  if (strategy == 0) {
+    for (int k = 0; k < q; ++k) {
+      Mat half = matmul(a, true, c, false);
+      c = matmul(a, false, half, false);
+    }
+  } else {
+    Mat gram = matmul(a, false, a, true);
+    for (int k = 0; k < q; ++k) c = matmul(gram, false, c, false);
+  }
+  return c;
+}
+
+Mat leading_left_singular_vectors(const Mat& c, size_t mu) {  // linalg.cpp:82-87
+  size_t maxrank = std::min(c.r, c.c);
+  if (mu < 1 || mu > maxrank)
+    throw std::invalid_argument("leading_left_singular_vectors: mu out of range");
+  Svd s = thin_svd(c);
+  Mat u(c.r, mu);
+  std::memcpy(u.d.data(), s.U.d.data(), sizeof(double) * c.r * mu);
+  return u;
+}
+
+// ---------------------------------------------------------------- sketching.cpp
+double stable_sum(const double* v, size_t n) {  // sketching.cpp:13-24
+  double s = 0.0, c = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    double x = v[i];
+    double t = s + x;
+    if (std::abs(s) >= std::abs(x))
+      c += (s - t) + x;
+    else
+      c += (x - t) + s;
+    s = t;
+  }
+  return s + c;
+}
+
+void check_distribution(const std::vector<double>& w) {  // sketching.cpp:28-38
+  if (w.empty()) throw std::invalid_argument("probability distribution must be nonempty");
+  for (double x : w)
+    if (!(x >= 0.0)) throw std::invalid_argument("probability weights must be nonnegative");
+  double s = stable_sum(w.data(), w.size());
+  if (std::abs(s - 1.0) > 1e-12) throw std::invalid_argument("probability weights must sum to one");
+}
+
+std::vector<double> normalized(std::vector<double> raw) {  // sketching.cpp:40-48
+  for (double w : raw)
+    if (!(w >= 0.0)) throw std::invalid_argument("probability weights must be nonnegative");
+  double s = stable_sum(raw.data(), raw.size());
+  if (s <= 0.0) throw std::invalid_argument("cannot normalize an all-zero distribution");
+  for (double& w : raw) w /= s;
+  check_distribution(raw);
+  return raw;
+}
+
+std::vector<double> uniform(size_t n) {  // sketching.cpp:50-53
+  if (n == 0) throw std::invalid_argument("probability distribution must be nonempty");
+  std::vector<double> w(n, 1.0 / static_cast<double>(n));
+  check_distribution(w);
+  return w;
+}
+
+struct Samples {
+  std::vector<int64_t> idx;
+  std::vector<double> scales;
+};
+
+Samples randsample(size_t L, const std::vector<double>& p, uint64_t seed, uint64_t stream) {
+  // sketching.cpp:96-131
+  if (L < 1) throw std::invalid_argument("randsample: L must be positive");
+  std::vector<double> cum(p.size());
+  double acc = 0.0;
+  for (size_t i = 0; i < p.size(); ++i) {
+    acc += p[i];
+    cum[i] = acc;
+  }
+  if (!(acc > 0.0)) throw std::invalid_argument("randsample: all-zero distribution");
+  size_t last = p.size();
+  while (last > 0 && p[last - 1] == 0.0) --last;
+  --last;
+  Samples s;
+  s.idx.resize(L);
+  s.scales.resize(L);
+  Rng gen(seed, stream);
+  const double scale_base = 1.0 / std::sqrt(static_cast<double>(L));
+  for (size_t j = 0; j < L; ++j) {
+    double u = gen.next_double() * acc;
+    auto it = std::upper_bound(cum.begin(), cum.end(), u);
+    size_t idx = (it == cum.end()) ? last : static_cast<size_t>(it - cum.begin());
+    if (p[idx] == 0.0) idx = last;
+    s.idx[j] = static_cast<int64_t>(idx);
+    s.scales[j] = scale_base / std::sqrt(p[idx]);
+  }
+  return s;
+}
+
+Mat sample_columns(const Mat& a, const Samples& s) {  // sketching.cpp:133-141
+  Mat c(a.r, s.idx.size());
+  for (size_t j = 0; j < s.idx.size(); ++j) {
+    const double* src = a.d.data() + a.r * (size_t)s.idx[j];
+    double* dst = c.d.data() + a.r * j;
+    for (size_t i = 0; i < a.r; ++i) dst[i] = src[i] * s.scales[j];
+  }
+  return c;
+}
+
+Mat gaussian_matrix(size_t rows, size_t cols, uint64_t seed, uint64_t stream) {
+  // sketching.cpp:164-173
+  if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_matrix: shape must be positive");
+  Mat g(rows, cols);
+  fill_normals(seed, stream, g.d.data(), rows * cols, default_threads());
+  return g;
+}
+
+// Canonical squared norm of a fiber (shared with the GPU kernels): chunks of 32
+// consecutive entries accumulated with fma, chunk partials added in order.
+double canonical_sqnorm(const double* x, size_t len, size_t stride) {
+  double total = 0.0;
+  for (size_t c0 = 0; c0 < len; c0 += 32) {
+    double p = 0.0;
+    size_t c1 = std::min(len, c0 + 32);
+    for (size_t r = c0; r < c1; ++r) {
+      double v = x[r * stride];
+      p = std::fma(v, v, p);
+    }
+    total = total + p;
+  }
+  return total;
+}
+
+std::vector<double> probabilities_from_norms(std::vector<double> w, int regime, double beta) {
+  // tucker.cpp:110-130 (after the squaredNorm loop)
+  const size_t n = w.size();
+  if (regime == ORC_UNIFORM) return uniform(n);
+  double total = 0.0;
+  for (size_t i = 0; i < n; ++i) total += w[i];
+  if (total <= 0.0) return uniform(n);
+  for (auto& x : w) x /= total;
+  if (regime == ORC_OPTIMAL) return normalized(std::move(w));
+  if (!(beta > 0.0 && beta <= 1.0))
+    throw std::invalid_argument("nearly-optimal mixture weight must lie in (0, 1]");
+  for (auto& x : w) x = beta * x + (1.0 - beta) / static_cast<double>(n);
+  return normalized(std::move(w));
+}
+
+std::vector<double> gram_sampling_norms(const Mat& a) {  // tucker.cpp:117-120 (norm half)
+  std::vector<double> w(a.c);
+  for (size_t j = 0; j < a.c; ++j) w[j] = canonical_sqnorm(a.d.data() + a.r * j, a.r, 1);
+  return w;
+}
+
+// ---------------------------------------------------------------- tucker.cpp
+struct Config {
+  std::vector<size_t> mu;
+  size_t oversampling = 10;
+  int power = 1;
+  double alpha = 0.2;
+  int regime = ORC_UNIFORM;
+  double beta = 0.5;
+  std::vector<size_t> t_samples;
+  std::vector<size_t> order;
+  uint64_t seed = 0;
+  int strategy = 0;
+  int mode_threads = 1;
+  bool keep_trace = false;
+};
+
+Config to_config(const orc_config* c, int order) {
+  Config k;
+  k.mu.assign(c->rank, c->rank + order);
+  k.oversampling = c->oversampling;
+  k.power = c->power;
+  k.alpha = c->alpha;
+  k.regime = c->regime;
+  k.beta = c->regime_beta;
+  if (c->t_samples) k.t_samples.assign(c->t_samples, c->t_samples + order);
+  if (c->order) k.order.assign(c->order, c->order + order);
+  k.seed = c->seed;
+  k.strategy = c->strategy;
+  k.mode_threads = std::max(1, c->mode_threads);
+  k.keep_trace = c->keep_trace != 0;
+  return k;
+}
+
+std::vector<size_t> clamped_for(const std::vector<size_t>& mu, const std::vector<size_t>& dims) {
+  // tucker.cpp:174-188
+  if (mu.size() != dims.size())
+    throw std::invalid_argument("rank vector length must equal tensor order");
+  std::vector<size_t> out(mu.size());
+  for (size_t n = 0; n < mu.size(); ++n) {
+    if (mu[n] < 1) throw std::invalid_argument("rank entries must be positive");
+    out[n] = std::min(mu[n], dims[n]);
+  }
+  return out;
+}
+
+struct Resolved {
+  std::vector<size_t> mu, sketch, order;
+};
+
+Resolved resolve(const Tensor& a, const Config& cfg) {  // tucker.cpp:24-52
+  const size_t nm = a.dims.size();
+  if (nm == 0) throw std::invalid_argument("cannot decompose an order-0 tensor");
+  if (cfg.mu.size() != nm) throw std::invalid_argument("rank vector length must equal tensor order");
+  if (cfg.power < 1) throw std::invalid_argument("power exponent must be >= 1");
+  Resolved r;
+  r.mu = clamped_for(cfg.mu, a.dims);
+  r.sketch.resize(nm);
+  for (size_t n = 0; n < nm; ++n) r.sketch[n] = std::min(r.mu[n] + cfg.oversampling, a.dims[n]);
+  if (cfg.order.empty()) {
+    r.order.resize(nm);
+    std::iota(r.order.begin(), r.order.end(), size_t{0});
+  } else {
+    if (cfg.order.size() != nm)
+      throw std::invalid_argument("processing order length must equal tensor order");
+    std::vector<bool> seen(nm, false);
+    for (size_t m : cfg.order) {
+      if (m >= nm || seen[m])
+        throw std::invalid_argument("processing order must be a permutation of the modes");
+      seen[m] = true;
+    }
+    r.order = cfg.order;
+  }
+  return r;
+}
+
+Mat top_left_vectors_clamped(const Mat& m, size_t mu) {  // tucker.cpp:65-77
+  return leading_left_singular_vectors(m, std::min(mu, std::min(m.r, m.c)));
+}
+
+Tensor core_from_factors(const Tensor& a, const std::vector<Mat>& f) {  // tucker.cpp:81-92
+  std::vector<size_t> idx(f.size());
+  std::iota(idx.begin(), idx.end(), size_t{0});
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t i, size_t j) { return f[i].c < f[j].c; });
+  Tensor t = a;
+  for (size_t n : idx) t = mode_n_product(t, transpose(f[n]), n);
+  return t;
+}
+
+size_t other_dims_product(const std::vector<size_t>& dims, size_t mode) {
+  size_t p = 1;
+  for (size_t k = 0; k < dims.size(); ++k)
+    if (k != mode) p *= dims[k];
+  return p;
+}
+
+size_t samples_from_alpha(double alpha, size_t cols) {  // tucker.cpp:101-106
+  if (!(alpha > 0.0 && alpha < 1.0))
+    throw std::invalid_argument("sampling fraction alpha must lie in (0, 1)");
+  auto t = static_cast<size_t>(std::ceil(alpha * static_cast<double>(cols)));
+  return std::max<size_t>(t, 1);
+}
+
+std::vector<size_t> amm_sample_counts(const std::vector<size_t>& dims, const Config& cfg,
+                                      bool sequential) {  // tucker.cpp:348-376
+  const size_t nm = dims.size();
+  if (!cfg.t_samples.empty()) {
+    if (cfg.t_samples.size() != nm)
+      throw std::invalid_argument("sample count override length must equal tensor order");
+    for (size_t t : cfg.t_samples)
+      if (t < 1) throw std::invalid_argument("sample counts must be positive");
+    return cfg.t_samples;
+  }
+  std::vector<size_t> counts(nm);
+  if (!sequential) {
+    for (size_t n = 0; n < nm; ++n) counts[n] = samples_from_alpha(cfg.alpha, other_dims_product(dims, n));
+    return counts;
+  }
+  std::vector<size_t> cur = dims;
+  std::vector<size_t> mu = clamped_for(cfg.mu, dims);
+  std::vector<size_t> order = cfg.order;
+  if (order.empty()) {
+    order.resize(nm);
+    std::iota(order.begin(), order.end(), size_t{0});
+  }
+  for (size_t n : order) {
+    counts[n] = samples_from_alpha(cfg.alpha, other_dims_product(cur, n));
+    cur[n] = mu[n];
+  }
+  return counts;
+}
+
+void run_modes(size_t nm, int cap, const std::function<void(size_t)>& body) {  // tucker.cpp:134-160
+  if (cap <= 1 || nm <= 1) {
+    for (size_t n = 0; n < nm; ++n) body(n);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::exception_ptr> errors(nm);
+  auto worker = [&] {
+    for (;;) {
+      size_t n = next.fetch_add(1);
+      if (n >= nm) return;
+      try {
+        body(n);
+      } catch (...) {
+        errors[n] = std::current_exception();
+      }
+    }
+  };
+  size_t workers = std::min<size_t>((size_t)cap, nm);
+  std::vector<std::thread> pool;
+  for (size_t i = 0; i + 1 < workers; ++i) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  for (auto& e : errors)
+    if (e) std::rethrow_exception(e);
+}
+
+struct Trace {
+  Mat omega;
+  Samples samples;
+  std::vector<double> norms;
+};
+
+}  // namespace
+
+struct orc_result {
+  Tensor core;
+  std::vector<Mat> factors;
+  std::vector<Trace> trace;
+  double seconds = 0.0;
+};
+
+namespace {
+
+// tucker.cpp:110-130 on an unfolding, with the trace hook
+std::vector<double> mode_probabilities(const Mat& a_n, const Config& cfg, Trace* tr) {
+  if (cfg.regime == ORC_UNIFORM) return uniform(a_n.c);
+  std::vector<double> w = gram_sampling_norms(a_n);
+  if (tr && cfg.keep_trace) tr->norms = w;
+  return probabilities_from_norms(std::move(w), cfg.regime, cfg.beta);
+}
+
+void alg_power(const Tensor& a, const Config& cfg, bool sequential, orc_result& res) {
+  // tucker.cpp:318-346
+  Resolved r = resolve(a, cfg);
+  const size_t nm = a.dims.size();
+  res.factors.assign(nm, Mat());
+  res.trace.assign(nm, Trace());
+  if (!sequential) {
+    run_modes(nm, cfg.mode_threads, [&](size_t n) {
+      Mat a_n = unfold(a, n);
+      Mat g = gaussian_matrix(a.dims[n], r.sketch[n], cfg.seed, n + 1);
+      Mat c = gram_power_apply(a_n, g, cfg.power, cfg.strategy);
+      res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+      if (cfg.keep_trace) res.trace[n].omega = std::move(g);
+    });
+    res.core = core_from_factors(a, res.factors);
+    return;
+  }
+  Tensor work = a;
+  for (size_t n : r.order) {
+    Mat a_n = unfold(work, n);
+    Mat g = gaussian_matrix(work.dims[n], r.sketch[n], cfg.seed, n + 1);
+    Mat c = gram_power_apply(a_n, g, cfg.power, cfg.strategy);
+    res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+    if (cfg.keep_trace) res.trace[n].omega = std::move(g);
+    work = mode_n_product(work, transpose(res.factors[n]), n);
+  }
+  res.core = std::move(work);
+}
+
+void alg_amm(const Tensor& a, const Config& cfg, bool sequential, orc_result& res) {
+  // tucker.cpp:378-420
+  Resolved r = resolve(a, cfg);
+  const size_t nm = a.dims.size();
+  res.factors.assign(nm, Mat());
+  res.trace.assign(nm, Trace());
+  if (!sequential) {
+    std::vector<size_t> t_n = amm_sample_counts(a.dims, cfg, false);
+    run_modes(nm, cfg.mode_threads, [&](size_t n) {
+      Mat a_n = unfold(a, n);
+      std::vector<double> p = mode_probabilities(a_n, cfg, &res.trace[n]);
+      Samples s = randsample(t_n[n], p, cfg.seed, nm + n + 1);
+      Mat sampled = sample_columns(a_n, s);
+      Mat g = gaussian_matrix(a.dims[n], r.sketch[n], cfg.seed, n + 1);
+      Mat c = gram_power_apply(sampled, g, cfg.power, cfg.strategy);
+      res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+      if (cfg.keep_trace) {
+        res.trace[n].omega = std::move(g);
+        res.trace[n].samples = std::move(s);
+      }
+    });
+    res.core = core_from_factors(a, res.factors);
+    return;
+  }
+  if (!cfg.t_samples.empty() && cfg.t_samples.size() != nm)
+    throw std::invalid_argument("sample count override length must equal tensor order");
+  Tensor work = a;
+  for (size_t n : r.order) {
+    Mat a_n = unfold(work, n);
+    size_t t_n = cfg.t_samples.empty() ? samples_from_alpha(cfg.alpha, a_n.c) : cfg.t_samples[n];
+    if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
+    std::vector<double> p = mode_probabilities(a_n, cfg, &res.trace[n]);
+    Samples s = randsample(t_n, p, cfg.seed, nm + n + 1);
+    Mat sampled = sample_columns(a_n, s);
+    Mat g = gaussian_matrix(work.dims[n], r.sketch[n], cfg.seed, n + 1);
+    Mat c = gram_power_apply(sampled, g, cfg.power, cfg.strategy);
+    res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+    if (cfg.keep_trace) {
+      res.trace[n].omega = std::move(g);
+      res.trace[n].samples = std::move(s);
+    }
+    work = mode_n_product(work, transpose(res.factors[n]), n);
+  }
+  res.core = std::move(work);
+}
+
+Tensor make_tensor(const double* x, const uint64_t* dims, int order) {
+  std::vector<size_t> d(dims, dims + order);
+  for (size_t v : d)
+    if (v == 0) throw std::invalid_argument("tensor dimension must be positive");
+  Tensor t(d);
+  std::memcpy(t.v.data(), x, sizeof(double) * t.size());
+  return t;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = std::string("runtime_error: ") + e.what();
+    return 2;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+int orc_init_blas(const char* path) {
+  return guard([&] {
+    void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) throw std::runtime_error(std::string("dlopen failed: ") + dlerror());
+    g_blas.dgemm = (dgemm_t)dlsym(h, "scipy_dgemm_64_");
+    g_blas.dgesdd = (dgesdd_t)dlsym(h, "scipy_dgesdd_64_");
+    g_blas.dgeqrf = (dgeqrf_t)dlsym(h, "scipy_dgeqrf_64_");
+    g_blas.dorgqr = (dorgqr_t)dlsym(h, "scipy_dorgqr_64_");
+    g_blas.set_threads = (setthreads_t)dlsym(h, "scipy_openblas_set_num_threads64_");
+    if (!g_blas.dgemm || !g_blas.dgesdd || !g_blas.dgeqrf || !g_blas.dorgqr)
+      throw std::runtime_error("BLAS/LAPACK symbols missing");
+  });
+}
+
+void orc_set_blas_threads(int n) {
+  if (g_blas.set_threads) g_blas.set_threads(n);
+}
+
+void orc_rng_u32(uint64_t seed, uint64_t stream, uint64_t skip, uint32_t* out, size_t n) {
+  Rng g(seed, stream);
+  g.advance(skip);
+  for (size_t i = 0; i < n; ++i) out[i] = g.next_u32();
+}
+
+void orc_rng_double(uint64_t seed, uint64_t stream, double* out, size_t n) {
+  Rng g(seed, stream);
+  for (size_t i = 0; i < n; ++i) out[i] = g.next_double();
+}
+
+void orc_rng_normal(uint64_t seed, uint64_t stream, double* out, size_t n) {
+  Rng g(seed, stream);  // strictly sequential, the reference's own loop
+  for (size_t i = 0; i < n; ++i) out[i] = g.next_normal();
+}
+
+int orc_gaussian_matrix(uint64_t rows, uint64_t cols, uint64_t seed, uint64_t stream, double* out) {
+  return guard([&] {
+    Mat g = gaussian_matrix(rows, cols, seed, stream);
+    std::memcpy(out, g.d.data(), sizeof(double) * rows * cols);
+  });
+}
+
+double orc_stable_sum(const double* v, size_t n) { return stable_sum(v, n); }
+
+int orc_column_sqnorms(const double* x, const uint64_t* dims, int order, int mode, double* w) {
+  return guard([&] {
+    std::vector<size_t> d(dims, dims + order);
+    size_t inner, outer;
+    inner_outer(d, (size_t)mode, inner, outer);
+    size_t L = d[mode];
+    for (size_t o = 0; o < outer; ++o)
+      for (size_t i = 0; i < inner; ++i)
+        w[i + inner * o] = canonical_sqnorm(x + i + inner * L * o, L, inner);
+  });
+}
+
+int orc_probabilities(const double* w, uint64_t n, int regime, double beta, double* p) {
+  return guard([&] {
+    std::vector<double> v(w, w + n);
+    std::vector<double> out = probabilities_from_norms(std::move(v), regime, beta);
+    std::memcpy(p, out.data(), sizeof(double) * n);
+  });
+}
+
+int orc_randsample(uint64_t L, const double* p, uint64_t n, uint64_t seed, uint64_t stream,
+                   int64_t* idx, double* scales) {
+  return guard([&] {
+    std::vector<double> pv(p, p + n);
+    check_distribution(pv);
+    Samples s = randsample(L, pv, seed, stream);
+    std::memcpy(idx, s.idx.data(), sizeof(int64_t) * L);
+    std::memcpy(scales, s.scales.data(), sizeof(double) * L);
+  });
+}
+
+int orc_amm_sample_counts(const uint64_t* dims, int order, const orc_config* cfg, int sequential,
+                          uint64_t* out) {
+  return guard([&] {
+    Config k = to_config(cfg, order);
+    std::vector<size_t> d(dims, dims + order);
+    std::vector<size_t> c = amm_sample_counts(d, k, sequential != 0);
+    for (int n = 0; n < order; ++n) out[n] = c[n];
+  });
+}
+
+int orc_mode_n_product(const double* x, const uint64_t* dims, int order, int mode,
+                       const double* b, uint64_t b_rows, double* y) {
+  return guard([&] {
+    Tensor t = make_tensor(x, dims, order);
+    Mat bm(b_rows, dims[mode]);
+    std::memcpy(bm.d.data(), b, sizeof(double) * bm.d.size());
+    Tensor o = mode_n_product(t, bm, (size_t)mode);
+    std::memcpy(y, o.v.data(), sizeof(double) * o.size());
+  });
+}
+
+int orc_gram_power_apply(const double* a, uint64_t rows, uint64_t cols, const double* g,
+                         uint64_t s, int q, int strategy, double* c) {
+  return guard([&] {
+    Mat am(rows, cols), gm(rows, s);
+    std::memcpy(am.d.data(), a, sizeof(double) * rows * cols);
+    std::memcpy(gm.d.data(), g, sizeof(double) * rows * s);
+    Mat out = gram_power_apply(am, gm, q, strategy);
+    std::memcpy(c, out.d.data(), sizeof(double) * rows * s);
+  });
+}
+
+int orc_leading_left_singular_vectors(const double* c, uint64_t rows, uint64_t cols, uint64_t mu,
+                                      double* u) {
+  return guard([&] {
+    Mat cm(rows, cols);
+    std::memcpy(cm.d.data(), c, sizeof(double) * rows * cols);
+    Mat out = leading_left_singular_vectors(cm, mu);
+    std::memcpy(u, out.d.data(), sizeof(double) * rows * mu);
+  });
+}
+
+int orc_thin_qr_q(const double* m, uint64_t rows, uint64_t cols, double* q) {
+  return guard([&] {
+    Mat mm(rows, cols);
+    std::memcpy(mm.d.data(), m, sizeof(double) * rows * cols);
+    Mat out = thin_qr_q(mm);
+    std::memcpy(q, out.d.data(), sizeof(double) * rows * cols);
+  });
+}
+
+int orc_run(int alg, const double* x, const uint64_t* dims, int order, const orc_config* cfg,
+            orc_result** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (order < 1) throw std::invalid_argument("cannot decompose an order-0 tensor");
+    Tensor a = make_tensor(x, dims, order);
+    Config k = to_config(cfg, order);
+    auto res = new orc_result();
+    try {
+      auto t0 = std::chrono::steady_clock::now();  // bench.cpp:247-249 timed span
+      switch (alg) {
+        case ORC_ALG1: alg_power(a, k, false, *res); break;
+        case ORC_ALG2: alg_power(a, k, true, *res); break;
+        case ORC_ALG4: alg_amm(a, k, false, *res); break;
+        case ORC_ALG5: alg_amm(a, k, true, *res); break;
+        default: throw std::invalid_argument("unknown algorithm");
+      }
+      auto t1 = std::chrono::steady_clock::now();
+      res->seconds = std::chrono::duration<double>(t1 - t0).count();
+    } catch (...) {
+      delete res;
+      throw;
+    }
+    *out = res;
+  });
+}
+
+int orc_result_order(const orc_result* r) { return (int)r->factors.size(); }
+void orc_result_core_dims(const orc_result* r, uint64_t* dims) {
+  for (size_t n = 0; n < r->core.dims.size(); ++n) dims[n] = r->core.dims[n];
+}
+void orc_result_factor_dims(const orc_result* r, int n, uint64_t* rows, uint64_t* cols) {
+  *rows = r->factors[n].r;
+  *cols = r->factors[n].c;
+}
+void orc_result_core(const orc_result* r, double* out) {
+  std::memcpy(out, r->core.v.data(), sizeof(double) * r->core.size());
+}
+void orc_result_factor(const orc_result* r, int n, double* out) {
+  std::memcpy(out, r->factors[n].d.data(), sizeof(double) * r->factors[n].d.size());
+}
+double orc_result_seconds(const orc_result* r) { return r->seconds; }
+void orc_result_omega_dims(const orc_result* r, int n, uint64_t* rows, uint64_t* cols) {
+  *rows = r->trace[n].omega.r;
+  *cols = r->trace[n].omega.c;
+}
+void orc_result_omega(const orc_result* r, int n, double* out) {
+  std::memcpy(out, r->trace[n].omega.d.data(), sizeof(double) * r->trace[n].omega.d.size());
+}
+uint64_t orc_result_num_samples(const orc_result* r, int n) { return r->trace[n].samples.idx.size(); }
+void orc_result_samples(const orc_result* r, int n, int64_t* idx, double* scales) {
+  const Samples& s = r->trace[n].samples;
+  std::memcpy(idx, s.idx.data(), sizeof(int64_t) * s.idx.size());
+  std::memcpy(scales, s.scales.data(), sizeof(double) * s.scales.size());
+}
+uint64_t orc_result_num_norms(const orc_result* r, int n) { return r->trace[n].norms.size(); }
+void orc_result_norms(const orc_result* r, int n, double* w) {
+  std::memcpy(w, r->trace[n].norms.data(), sizeof(double) * r->trace[n].norms.size());
+}
+void orc_result_free(orc_result* r) { delete r; }
+
+double orc_relative_error(const double* x, const uint64_t* dims, int order, const orc_result* r) {
+  // tucker.cpp:222-240: reconstruct (core x_n Q_n for n = 0..N-1), then the RE loop
+  double re = -1.0;
+  guard([&] {
+    Tensor a = make_tensor(x, dims, order);
+    Tensor t = r->core;
+    for (size_t n = 0; n < r->factors.size(); ++n) t = mode_n_product(t, r->factors[n], n);
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) {
+      double d = a.v[i] - t.v[i];
+      num += d * d;
+      den += a.v[i] * a.v[i];
+    }
+    if (den == 0.0) throw std::invalid_argument("relative_error: zero reference tensor");
+    re = std::sqrt(num / den);
+  });
+  return re;
+}
+
+// ---------------------------------------------------------------- BASELINE generators
+// Definitions: RandomStream stream ids follow the
+// reference's datagen.cpp:20-23 (core 100, factor 101+n, noise 200).
+int orc_gen_tucker_noise(const uint64_t* dims, const uint64_t* core_dims, int order, double gamma,
+                         uint64_t seed, double* out) {
+  return guard([&] {
+    std::vector<size_t> cd(core_dims, core_dims + order), d(dims, dims + order);
+    Tensor b(cd);
+    fill_normals(seed, 100, b.v.data(), b.size(), default_threads());
+    for (int n = 0; n < order; ++n) {
+      Mat u = thin_qr_q(gaussian_matrix(d[n], cd[n], seed, 101 + n));
+      b = mode_n_product(b, u, (size_t)n);
+    }
+    std::vector<double> e(b.size());
+    fill_normals(seed, 200, e.data(), e.size(), default_threads());
+    double nb = 0.0, ne = 0.0;
+    for (size_t i = 0; i < b.size(); ++i) {
+      nb += b.v[i] * b.v[i];
+      ne += e[i] * e[i];
+    }
+    double coef = gamma * std::sqrt(nb) / std::sqrt(ne);
+    for (size_t i = 0; i < b.size(); ++i) out[i] = b.v[i] + coef * e[i];
+  });
+}
+
+int orc_gen_hilbert(const uint64_t* dims, int order, double* out) {
+  return guard([&] {
+    size_t total = 1;
+    for (int n = 0; n < order; ++n) total *= dims[n];
+    std::vector<size_t> idx(order, 0);
+    for (size_t e = 0; e < total; ++e) {
+      size_t s = 0;
+      for (int n = 0; n < order; ++n) s += idx[n];
+      out[e] = 1.0 / static_cast<double>(s + 1);
+      for (int n = 0; n < order; ++n) {
+        if (++idx[n] < dims[n]) break;
+        idx[n] = 0;
+      }
+    }
+  });
+}
+
+int orc_gen_video(const uint64_t* dims, int order, uint64_t n_terms, double noise, uint64_t seed,
+                  double* out) {
+  return guard([&] {
+    std::vector<size_t> d(dims, dims + order);
+    size_t total = 1;
+    for (size_t v : d) total *= v;
+    // profiles P_n (I_n x R) and weights
+    std::vector<Mat> P(order);
+    for (int n = 0; n < order; ++n) P[n] = Mat(d[n], n_terms);
+    std::vector<double> w(n_terms);
+    for (size_t t = 0; t < n_terms; ++t) {
+      Rng g(seed, 300 + t);
+      w[t] = g.next_double();
+      for (int n = 0; n < order; ++n) {
+        double f = 0.5 + 7.5 * g.next_double();
+        double ph = 6.283185307179586476925286766559 * g.next_double();
+        for (size_t i = 0; i < d[n]; ++i) {
+          double x = static_cast<double>(i) / static_cast<double>(d[n]);
+          P[n](i, t) = std::cos(6.283185307179586476925286766559 * f * x + ph);
+        }
+      }
+    }
+    // Khatri-Rao of modes 1..N-1 (J x R), then X_(0) = P_0 diag(w) KR^T
+    size_t J = total / d[0];
+    Mat kr(J, n_terms);
+    for (size_t t = 0; t < n_terms; ++t) {
+      for (size_t j = 0; j < J; ++j) {
+        size_t rem = j;
+        double v = w[t];
+        for (int n = 1; n < order; ++n) {
+          v *= P[n](rem % d[n], t);
+          rem /= d[n];
+        }
+        kr(j, t) = v;
+      }
+    }
+    gemm(false, true, d[0], J, n_terms, P[0].d.data(), d[0], kr.d.data(), J, out, d[0]);
+    Rng g(seed, 400);
+    for (size_t e = 0; e < total; ++e) out[e] += noise * g.next_double();
+  });
+}
+
+}  // extern "C"
