@@ -1,0 +1,172 @@
+/* lmra_b200.h -- C ABI of the B200-native randomized Tucker hot path.
+ *
+ * Drop-in boundary for the reference's C++ entry points (namespace lmra,
+ * /root/reference/proj/include/lmra/tucker.hpp).  Plain pointers and sizes only;
+ * no torch, Eigen or CUDA types in the signatures (streams are `void*`).
+ *
+ *   reference (tucker.hpp)                              this ABI
+ *   rand_thosvd_power   (tucker.hpp:91)       alg1  ->  lmra_run_algorithm(LMRA_ALG1, ...)
+ *   rand_sthosvd_power  (tucker.hpp:95)       alg2  ->  lmra_run_algorithm(LMRA_ALG2, ...)
+ *   rand_thosvd_amm     (tucker.hpp:99)       alg4  ->  lmra_run_algorithm(LMRA_ALG4, ...)
+ *   rand_sthosvd_amm    (tucker.hpp:102)      alg5  ->  lmra_run_algorithm(LMRA_ALG5, ...)
+ *   run_algorithm       (tucker.hpp:110-111)        ->  lmra_run_algorithm
+ *   amm_sample_counts   (tucker.hpp:116-117)        ->  lmra_amm_sample_counts
+ *   thread_cap          (tucker.hpp:121)            ->  (device count knob: env LMRA_NUM_GPUS)
+ *   AlgoConfig          (tucker.hpp:32-45)          ->  lmra_algo_config
+ *   TuckerDecomposition (tucker.hpp:27-30)          ->  lmra_result (core + factors)
+ *   mode_n_product      (tensor.hpp:56-57)          ->  lmra_mode_n_product
+ *   gram_power_apply    (linalg.hpp:37-38)          ->  lmra_gram_power_apply
+ *   leading_left_singular_vectors (linalg.hpp:41)   ->  lmra_leading_left_singular_vectors
+ *   gaussian_matrix     (sketching.hpp:69)          ->  lmra_gaussian_matrix
+ *   randsample          (sketching.hpp:56)          ->  lmra_randsample
+ *   gram_sampling_probabilities (tucker.cpp:110-130)->  lmra_column_sqnorms + lmra_probabilities
+ *
+ * Tensors are dense fp64 with the reference's linearisation: first index fastest
+ * (tensor.hpp:9-12).  Matrices are column-major (Eigen default).
+ *
+ * Errors (tucker.cpp / linalg.cpp exception surface): every int-returning call
+ * returns LMRA_OK or an error code; lmra_last_error() gives the thread's message.
+ *   LMRA_EINVAL   <-> std::invalid_argument  (bad rank length, power < 1, bad order,
+ *                                             alpha outside (0,1), t < 1, ...)
+ *   LMRA_ERUNTIME <-> std::runtime_error     (SVD did not converge)
+ *   LMRA_ECUDA    CUDA / NCCL failure
+ * Rank clamping is a warning on stderr, as in the reference (tucker.cpp:65-72,185-186).
+ */
+#ifndef LMRA_B200_H
+#define LMRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum lmra_status { LMRA_OK = 0, LMRA_EINVAL = 1, LMRA_ERUNTIME = 2, LMRA_ECUDA = 3 };
+/* Algorithm ids (tucker.hpp:47-57). Only the randomized power/AMM family is on this path. */
+enum lmra_algorithm { LMRA_ALG1 = 1, LMRA_ALG2 = 2, LMRA_ALG4 = 4, LMRA_ALG5 = 5 };
+/* ProbRegime (sketching.hpp:31) */
+enum lmra_regime { LMRA_OPTIMAL = 0, LMRA_NEARLY_OPTIMAL = 1, LMRA_UNIFORM = 2 };
+/* GramStrategy (linalg.hpp:26) */
+enum lmra_strategy { LMRA_STRATEGY_A = 0, LMRA_STRATEGY_B = 1 };
+/* where a buffer lives */
+enum lmra_location { LMRA_HOST = 0, LMRA_DEVICE = 1 };
+
+/* AlgoConfig (tucker.hpp:32-45); arrays may be NULL with length 0 = "empty vector". */
+typedef struct {
+  const uint64_t* rank;       /* MultilinearRank::mu */
+  uint64_t n_rank;
+  uint64_t oversampling;      /* default 10 */
+  int32_t power;              /* q, default 1 */
+  double alpha;               /* default 0.2 */
+  int32_t regime;             /* lmra_regime, default LMRA_UNIFORM */
+  double regime_beta;         /* default 0.5 */
+  const uint64_t* t_samples;  /* per-mode sample counts or NULL */
+  uint64_t n_t_samples;
+  const uint64_t* order;      /* processing order (0-based) or NULL */
+  uint64_t n_order;
+  uint64_t seed;              /* default 0 */
+  int32_t strategy;           /* lmra_strategy, default A */
+} lmra_algo_config;
+
+/* Fills the reference's defaults (tucker.hpp:32-45). */
+void lmra_algo_config_init(lmra_algo_config* cfg);
+
+/* Parity overrides: per-mode Omega (I_n x s, column-major, host) and per-mode sampled
+ * columns (indices + scales, host).  NULL arrays / NULL entries mean "draw them from
+ * the seeded host RNG as the reference does".  Sample indices are columns of the mode-n
+ * unfolding of the tensor as it is when that mode is processed. */
+typedef struct {
+  const double* const* omega;        /* [order] or NULL */
+  const int64_t* const* sample_idx;  /* [order] or NULL */
+  const double* const* sample_scale; /* [order] or NULL */
+  const uint64_t* n_samples;         /* [order] or NULL */
+} lmra_overrides;
+
+typedef struct lmra_context lmra_context;
+typedef struct lmra_result lmra_result;
+
+const char* lmra_last_error(void);
+const char* lmra_version(void);
+
+/* One context per (process, device).  stream == NULL -> the context creates its own. */
+int lmra_context_create(int device, void* stream, lmra_context** out);
+void lmra_context_destroy(lmra_context* ctx);
+int lmra_context_set_stream(lmra_context* ctx, void* stream);
+int lmra_context_synchronize(lmra_context* ctx);
+
+/* Multi-GPU (one process per GPU).  The tensor passed to lmra_run_algorithm is then
+ * this rank's slab along the LAST mode (rows [start, start+count) of that mode, see
+ * lmra_shard_range); dims[] are the GLOBAL dims.  Small sketch / Gram / norm partials
+ * are combined with NCCL all-reduce / all-gather over NVLink. */
+int lmra_nccl_unique_id(void* out128);
+int lmra_context_set_comm(lmra_context* ctx, const void* unique_id128, int nranks, int rank);
+/* Shard plan: contiguous balanced slabs, rank r owns [start, start + count). */
+int lmra_shard_range(uint64_t extent, int nranks, int rank, uint64_t* start, uint64_t* count);
+
+/* run_algorithm (tucker.cpp:456-470) for alg1/alg2/alg4/alg5. x: dense tensor on the host
+ * (x_location = LMRA_HOST, copied in) or device (LMRA_DEVICE, read in place, never
+ * mutated).  The call returns once the result is complete on the device. */
+int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const uint64_t* dims,
+                       int order, int x_location, const lmra_algo_config* cfg,
+                       const lmra_overrides* overrides, lmra_result** out);
+
+int lmra_result_order(const lmra_result* r);
+void lmra_result_core_dims(const lmra_result* r, uint64_t* dims);
+int lmra_result_copy_core(const lmra_result* r, double* dst, int dst_location);
+void lmra_result_factor_dims(const lmra_result* r, int mode, uint64_t* rows, uint64_t* cols);
+int lmra_result_copy_factor(const lmra_result* r, int mode, double* dst, int dst_location);
+const double* lmra_result_core_device(const lmra_result* r);
+const double* lmra_result_factor_device(const lmra_result* r, int mode);
+/* trace of the draws this run used (host copies) */
+void lmra_result_omega_dims(const lmra_result* r, int mode, uint64_t* rows, uint64_t* cols);
+int lmra_result_copy_omega(const lmra_result* r, int mode, double* dst);
+uint64_t lmra_result_num_samples(const lmra_result* r, int mode);
+int lmra_result_copy_samples(const lmra_result* r, int mode, int64_t* idx, double* scales);
+uint64_t lmra_result_num_norms(const lmra_result* r, int mode);
+int lmra_result_copy_norms(const lmra_result* r, int mode, double* w);
+/* phase timings of the run (milliseconds): [0] total wall, [1] host RNG (Omega),
+ * [2] host sampling chains, [3] device time of the run (events), [4] kernel launches */
+int lmra_result_timings(const lmra_result* r, double* out5);
+void lmra_result_free(lmra_result* r);
+
+/* ---- primitives (device pointers unless stated; all on the context's stream) ---- */
+/* y = x x_mode b, b is b_rows x dims[mode] column-major (tensor.cpp:118-139) */
+int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
+                        int mode, const double* b, uint64_t b_rows, double* y);
+/* c = (A A^T)^q G  (linalg.cpp:62-80), A rows x cols, G rows x s */
+int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uint64_t cols,
+                          const double* g, uint64_t s, int q, int strategy, double* c);
+/* u = top-mu left singular vectors of c with the reference's sign rule (linalg.cpp:82-87) */
+int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint64_t rows,
+                                       uint64_t cols, uint64_t mu, double* u);
+/* canonical column squared norms of the mode-n unfolding (tucker.cpp:117-119) */
+int lmra_column_sqnorms(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
+                        int mode, double* w);
+
+/* ---- host-side reference restatements used on the path (host pointers) ---- */
+int lmra_gaussian_matrix(uint64_t rows, uint64_t cols, uint64_t seed, uint64_t stream,
+                         double* out);
+int lmra_probabilities(const double* w, uint64_t n, int regime, double beta, double* p);
+int lmra_randsample(uint64_t L, const double* p, uint64_t n, uint64_t seed, uint64_t stream,
+                    int64_t* idx, double* scales);
+int lmra_amm_sample_counts(const uint64_t* dims, int order, const lmra_algo_config* cfg,
+                           int sequential, uint64_t* out);
+
+/* ---- synthetic BASELINE inputs, generated on the device (x is a device buffer) ---- */
+int lmra_gen_tucker_noise(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims,
+                          int order, double gamma, uint64_t seed, double* x);
+int lmra_gen_hilbert(lmra_context* ctx, const uint64_t* dims, int order, double* x);
+int lmra_gen_video(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms,
+                   double noise, uint64_t seed, double* x);
+
+/* device memory helpers (so callers without a CUDA runtime can stage data) */
+int lmra_device_alloc(lmra_context* ctx, size_t bytes, void** out);
+int lmra_device_free(lmra_context* ctx, void* p);
+int lmra_memcpy(lmra_context* ctx, void* dst, const void* src, size_t bytes, int dst_location,
+                int src_location);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -643,6 +643,7 @@ void run_modes(size_t nm, int cap, const std::function<void(size_t)>& body) {  /
 
 struct Trace {
   Mat omega;
+  Mat sketch;  // C = (A A^T)^q G, the matrix whose top left singular vectors are the factor
   Samples samples;
   std::vector<double> norms;
 };
@@ -678,6 +679,8 @@ void alg_power(const Tensor& a, const Config& cfg, bool sequential, orc_result& 
       Mat g = gaussian_matrix(a.dims[n], r.sketch[n], cfg.seed, n + 1);
       Mat c = gram_power_apply(a_n, g, cfg.power, cfg.strategy);
       res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+      if (cfg.keep_trace) res.trace[n].sketch = c;
+    if (cfg.keep_trace) res.trace[n].sketch = c;
       if (cfg.keep_trace) res.trace[n].omega = std::move(g);
     });
     res.core = core_from_factors(a, res.factors);
@@ -689,6 +692,7 @@ void alg_power(const Tensor& a, const Config& cfg, bool sequential, orc_result& 
     Mat g = gaussian_matrix(work.dims[n], r.sketch[n], cfg.seed, n + 1);
     Mat c = gram_power_apply(a_n, g, cfg.power, cfg.strategy);
     res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+    if (cfg.keep_trace) res.trace[n].sketch = c;
     if (cfg.keep_trace) res.trace[n].omega = std::move(g);
     work = mode_n_product(work, transpose(res.factors[n]), n);
   }
@@ -711,6 +715,8 @@ void alg_amm(const Tensor& a, const Config& cfg, bool sequential, orc_result& re
       Mat g = gaussian_matrix(a.dims[n], r.sketch[n], cfg.seed, n + 1);
       Mat c = gram_power_apply(sampled, g, cfg.power, cfg.strategy);
       res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+      if (cfg.keep_trace) res.trace[n].sketch = c;
+    if (cfg.keep_trace) res.trace[n].sketch = c;
       if (cfg.keep_trace) {
         res.trace[n].omega = std::move(g);
         res.trace[n].samples = std::move(s);
@@ -732,6 +738,7 @@ void alg_amm(const Tensor& a, const Config& cfg, bool sequential, orc_result& re
     Mat g = gaussian_matrix(work.dims[n], r.sketch[n], cfg.seed, n + 1);
     Mat c = gram_power_apply(sampled, g, cfg.power, cfg.strategy);
     res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
+    if (cfg.keep_trace) res.trace[n].sketch = c;
     if (cfg.keep_trace) {
       res.trace[n].omega = std::move(g);
       res.trace[n].samples = std::move(s);
@@ -943,6 +950,9 @@ void orc_result_omega_dims(const orc_result* r, int n, uint64_t* rows, uint64_t*
 }
 void orc_result_omega(const orc_result* r, int n, double* out) {
   std::memcpy(out, r->trace[n].omega.d.data(), sizeof(double) * r->trace[n].omega.d.size());
+}
+void orc_result_sketch(const orc_result* r, int n, double* out) {
+  std::memcpy(out, r->trace[n].sketch.d.data(), sizeof(double) * r->trace[n].sketch.d.size());
 }
 uint64_t orc_result_num_samples(const orc_result* r, int n) { return r->trace[n].samples.idx.size(); }
 void orc_result_samples(const orc_result* r, int n, int64_t* idx, double* scales) {

@@ -98,6 +98,7 @@ double orc_result_seconds(const orc_result* r);
 /* trace (keep_trace != 0) */
 void orc_result_omega_dims(const orc_result* r, int n, uint64_t* rows, uint64_t* cols);
 void orc_result_omega(const orc_result* r, int n, double* out);
+void orc_result_sketch(const orc_result* r, int n, double* out); /* same dims as omega */
 uint64_t orc_result_num_samples(const orc_result* r, int n);
 void orc_result_samples(const orc_result* r, int n, int64_t* idx, double* scales);
 uint64_t orc_result_num_norms(const orc_result* r, int n);

@@ -62,8 +62,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            build()
+        try:
+            build()  # make: no-op when up to date
+        except (OSError, subprocess.CalledProcessError):
+            if not os.path.exists(LIB_PATH):
+                raise
         L = C.CDLL(LIB_PATH)
         L.orc_last_error.restype = C.c_char_p
         L.orc_stable_sum.restype = C.c_double
@@ -204,6 +207,7 @@ class Decomposition:
     omega: list                 # per mode (I_n x s) or None
     samples: list               # per mode (idx, scales) or None
     norms: list                 # per mode w or None
+    sketches: list = field(default_factory=list)  # per mode C (I_n x s)
 
 
 def amm_sample_counts(dims: Sequence[int], cfg: AlgoConfig, sequential: bool) -> list:
@@ -228,7 +232,7 @@ def run(alg: str, x: np.ndarray, dims: Sequence[int], cfg: AlgoConfig) -> Decomp
         L.orc_result_core_dims(h, _p(cd, u64p))
         core = np.empty(int(np.prod(cd)))
         L.orc_result_core(h, _p(core, dblp))
-        factors, omegas, samples, norms = [], [], [], []
+        factors, omegas, samples, norms, sketches = [], [], [], [], []
         for n in range(N):
             r, k = C.c_uint64(), C.c_uint64()
             L.orc_result_factor_dims(h, n, C.byref(r), C.byref(k))
@@ -241,6 +245,10 @@ def run(alg: str, x: np.ndarray, dims: Sequence[int], cfg: AlgoConfig) -> Decomp
                 if g.size:
                     L.orc_result_omega(h, n, _p(g, dblp))
                 omegas.append(g.reshape((r.value, k.value), order="F"))
+                c = np.empty(r.value * k.value)
+                if c.size:
+                    L.orc_result_sketch(h, n, _p(c, dblp))
+                sketches.append(c.reshape((r.value, k.value), order="F"))
                 T = L.orc_result_num_samples(h, n)
                 if T:
                     idx = np.empty(T, dtype=np.int64)
@@ -258,7 +266,7 @@ def run(alg: str, x: np.ndarray, dims: Sequence[int], cfg: AlgoConfig) -> Decomp
                     norms.append(None)
         seconds = L.orc_result_seconds(h)
         re_core = core.reshape(tuple(int(v) for v in cd), order="F")
-        return Decomposition(re_core, factors, seconds, omegas, samples, norms)
+        return Decomposition(re_core, factors, seconds, omegas, samples, norms, sketches)
     finally:
         L.orc_result_free(h)
 

@@ -1,0 +1,73 @@
+// common.cuh -- shared device helpers for the sm_100a fp64 kernels.
+//
+// fp64 on Blackwell: tcgen05.mma has no f64 kind, so fp64 tensor work is the
+// warp-level mma.sync ... f64 family, which lowers to DMMA.8x8x4 in SASS
+// (measured peak 37.0 TFLOP/s on B200, profiles/fp64_peaks_r01.json, vs 33.9 for
+// a DFMA loop).  Tiles are staged global->shared with cp.async (LDGSTS) in a
+// multi-stage ring so HBM streaming overlaps the DMMA issue.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace lmra_dev {
+
+__device__ __forceinline__ long long col_base(long long j, long long inner, long long I) {
+  if (inner == 1) return j * I;
+  long long o = j / inner;
+  long long i = j - o * inner;
+  return i + inner * I * o;
+}
+
+// D(16x8) += A(16x4) * B(4x8), fp64, fragments per PTX ISA m16n8k4 .f64:
+//   a0 = A[g][t], a1 = A[g+8][t]; b = B[t][g]; d0,d1 = D[g][2t..2t+1], d2,d3 = D[g+8][2t..2t+1]
+// with g = lane / 4, t = lane % 4.
+__device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async copy; src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(valid ? 8 : 0));
+}
+
+// 16-byte async copy (L2 only, bypass L1); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Leading dimension (in doubles) >= n with ld % 16 == 4: a 64-bit fragment read of
+// rows t = 0..3 x cols g = 0..3 per half-warp then hits 16 distinct even banks.
+__host__ __device__ constexpr int conflict_free_ld(int n) { return ((n + 11) / 16) * 16 + 4; }
+
+// Opt a kernel into > 48 KB dynamic shared memory once per device (bitmask of devices).
+inline cudaError_t ensure_smem_attr(const void* fn, size_t bytes, unsigned long long& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  unsigned long long bit = 1ull << (dev & 63);
+  if (done & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done |= bit;
+  return e;
+}
+
+}  // namespace lmra_dev

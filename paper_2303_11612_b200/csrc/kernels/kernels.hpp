@@ -1,0 +1,63 @@
+// kernels.hpp -- host-side launchers for the sm_100a kernels (no torch types).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lmra_dev {
+
+// Tensor viewed around one mode: X3[i, r, o] = x[i + inner * (r + I * o)].
+// Column j of the mode unfolding is (i, o) with j = i + inner * o (tensor.cpp:60-86).
+struct ModeView {
+  long long inner, I, outer;
+};
+
+// widest factor / sketch the DMMA tiles take (N of m16n8k4 padded to 8)
+constexpr int kMaxWidth = 64;
+
+// Y = X x_mode B, with B given transposed: bt[r + I*k] = B[k, r] (I x m column-major).
+cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
+                       cudaStream_t st);
+
+struct GramPlan {
+  int nsplit = 1;
+  long long jper = 0;
+};
+GramPlan plan_gram(ModeView v, int num_sms);
+// z (I x s, column-major) = sum_j X(:, j) H(:, j)^T; zpart holds nsplit * I * s doubles.
+cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, double* zpart,
+                        const GramPlan& plan, double* z, cudaStream_t st);
+
+// C' = A_(n)(:, idx) * diag(scale), I x T column-major.
+cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, const double* scale,
+                          long long T, double* out, cudaStream_t st);
+
+// Canonical column squared norms of the mode-n unfolding (chunks of 32 along the fiber,
+// fma within a chunk, chunk partials added in order) -- bit-identical to the oracle.
+cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaStream_t st);
+
+// Top-mu left singular vectors of C (I x s, column-major) with the reference's sign
+// convention (linalg.cpp:13-43,82-87), written to U (I x mu).  Workspace: orth_workspace().
+size_t orth_workspace_doubles(long long I, int s);
+cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, double* work,
+                        int* status, cudaStream_t st);
+
+// ---- synthetic generators (device) ----
+// element e of the normal sequence of PCG32 stream (seed, stream), Box-Muller pairs as in rng.hpp
+cudaError_t launch_gen_normals(double* out, long long n, uint64_t seed, uint64_t stream,
+                               cudaStream_t st);
+cudaError_t launch_gen_uniform_add(double* out, long long n, double scale, uint64_t seed,
+                                   uint64_t stream, cudaStream_t st);
+cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, cudaStream_t st);
+cudaError_t launch_gen_cp(double* out, const long long* dims, int order, const double* profiles,
+                          const double* weights, int n_terms, cudaStream_t st);
+// at (cols x rows) = a^T
+cudaError_t launch_transpose(const double* a, long long rows, long long cols, double* at,
+                             cudaStream_t st);
+// out = a + coef * b
+cudaError_t launch_axpby(const double* a, const double* b, double coef, double* out, long long n,
+                         cudaStream_t st);
+// partial sums of squares (deterministic, fixed grid) -> host reduces
+cudaError_t launch_sumsq(const double* a, long long n, double* partials, int nparts,
+                         cudaStream_t st);
+
+}  // namespace lmra_dev

@@ -1,0 +1,483 @@
+// ttm.cu -- in-place mode-n TTM and Gram contraction on the fp64 DMMA pipe.
+//
+// Replaces the Eigen GEMMs the reference runs on explicit unfoldings:
+//   mode_n_product  tensor.cpp:118-139  (unfold -> b * m -> fold)      -> ttm_kernel
+//   gram_power_apply linalg.cpp:70-74   (half = A^T c ; c = A * half)  -> ttm_kernel + gram_kernel
+//   sample_columns  sketching.cpp:133-141                              -> gather_columns_kernel
+// No unfolding is materialised: a column j = (i, o) of A_(n) is addressed in place
+// through ModeView (common.cuh).  Both contractions run as a DMMA GEMM whose long
+// dimension is j; the short dimension (factor / sketch width, <= 64) lives in
+// the N of m16n8k4 and is padded to a multiple of 8.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace lmra_dev {
+
+constexpr int kThreads = 256;
+
+// ----------------------------------------------------------------------------
+// TTM: Y(k, j) = sum_r Bt[r + I*k] * X(r, j), k < m.  Y has X's layout with I -> m.
+// CTA tile: 128 columns j x all k; 8 warps x 16 j.  K (= I) in chunks of 16.
+// ----------------------------------------------------------------------------
+template <int M8, bool RCONTIG>
+struct TtmCfg {
+  static constexpr int JT = 128, KC = 16, STAGES = 3;
+  static constexpr int LDA = RCONTIG ? conflict_free_ld(KC) : conflict_free_ld(JT);
+  static constexpr int A_ELEMS = RCONTIG ? JT * LDA : KC * LDA;
+  static constexpr int LDB = conflict_free_ld(M8);
+  static constexpr int B_ELEMS = KC * LDB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES;
+};
+
+template <int M8, bool RCONTIG>
+__global__ void __launch_bounds__(kThreads, 2)
+    ttm_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ bt, int m,
+               int mtot, int koff, double* __restrict__ y) {
+  using C = TtmCfg<M8, RCONTIG>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const long long J = v.inner * v.outer, I = v.I;
+  const long long j0 = (long long)blockIdx.x * C::JT;
+  const int nk = (int)((I + C::KC - 1) / C::KC);
+  const bool vec16 = RCONTIG ? (I % 2 == 0) : (v.inner % 2 == 0);
+
+  // per-thread fixed column(s) for the JCONTIG loader
+  long long jbase = 0;
+  bool jvalid = false;
+  int jl = 0, rsub = 0;
+  if (!RCONTIG) {
+    if (vec16) {
+      jl = (tid % 64) * 2;
+      rsub = tid / 64;  // 0..3
+    } else {
+      jl = tid % 128;
+      rsub = tid / 128;  // 0..1
+    }
+    long long j = j0 + jl;
+    jvalid = j < J;
+    jbase = jvalid ? col_base(j, v.inner, I) : 0;
+  }
+
+  auto load = [&](int stage, int kt) {
+    double* As = smem + stage * C::STAGE_ELEMS;
+    double* Bs = As + C::A_ELEMS;
+    const long long k0 = (long long)kt * C::KC;
+    // B^T chunk: Bs[r][k] = bt[(k0 + r) + I*k]
+    for (int e = tid; e < C::KC * M8; e += kThreads) {
+      int r = e % C::KC, k = e / C::KC;
+      bool ok = (k0 + r < I) && (k < m);
+      cp_async8(Bs + r * C::LDB + k, ok ? bt + (k0 + r) + I * k : bt, ok);
+    }
+    if (RCONTIG) {  // X(r, j) = x[I*j + r]  ->  As[j][r]
+      if (vec16) {
+#pragma unroll
+        for (int q = 0; q < (C::JT * C::KC / 2) / kThreads; ++q) {
+          int e = tid + q * kThreads;
+          int rp = e % (C::KC / 2), jj = e / (C::KC / 2);
+          long long j = j0 + jj, r = k0 + 2 * rp;
+          bool ok = (j < J) && (r < I);
+          cp_async16(As + jj * C::LDA + 2 * rp, ok ? x + I * j + r : x, ok);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < (C::JT * C::KC) / kThreads; ++q) {
+          int e = tid + q * kThreads;
+          int rl = e % C::KC, jj = e / C::KC;
+          long long j = j0 + jj, r = k0 + rl;
+          bool ok = (j < J) && (r < I);
+          cp_async8(As + jj * C::LDA + rl, ok ? x + I * j + r : x, ok);
+        }
+      }
+    } else {  // X(r, j) = x[base_j + inner*r]  ->  As[r][j]
+      if (vec16) {
+#pragma unroll
+        for (int q = 0; q < C::KC / 4; ++q) {
+          int rl = rsub + 4 * q;
+          long long r = k0 + rl;
+          bool ok = jvalid && (r < I);
+          cp_async16(As + rl * C::LDA + jl, ok ? x + jbase + v.inner * r : x, ok);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < C::KC / 2; ++q) {
+          int rl = rsub + 2 * q;
+          long long r = k0 + rl;
+          bool ok = jvalid && (r < I);
+          cp_async8(As + rl * C::LDA + jl, ok ? x + jbase + v.inner * r : x, ok);
+        }
+      }
+    }
+  };
+
+  constexpr int NF = M8 / 8;
+  double acc[NF][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[f][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < nk) load(s, s);
+    cp_async_commit();
+  }
+  const int jw = warp * 16;
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    const double* As = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
+    const double* Bs = As + C::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < C::KC / 4; ++kk) {
+      const int r = kk * 4 + t;
+      double a0, a1;
+      if (RCONTIG) {
+        a0 = As[(jw + g) * C::LDA + r];
+        a1 = As[(jw + g + 8) * C::LDA + r];
+      } else {
+        a0 = As[r * C::LDA + jw + g];
+        a1 = As[r * C::LDA + jw + g + 8];
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) dmma16x8x4(acc[f], a0, a1, Bs[r * C::LDB + f * 8 + g]);
+    }
+    const int nt = kt + C::STAGES - 1;
+    if (nt < nk) load(nt % C::STAGES, nt);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const long long j = j0 + jw + g + 8 * half;
+    if (j >= J) continue;
+    long long ybase;
+    long long ystride;
+    if (RCONTIG) {
+      ybase = j * mtot + koff;
+      ystride = 1;
+    } else {
+      long long o = j / v.inner, i = j - o * v.inner;
+      ybase = i + v.inner * ((long long)mtot * o + koff);
+      ystride = v.inner;
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int k = f * 8 + 2 * t;
+      if (k < m) y[ybase + ystride * k] = acc[f][2 * half];
+      if (k + 1 < m) y[ybase + ystride * (k + 1)] = acc[f][2 * half + 1];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Gram: Zpart[split](r, k) = sum_{j in split} X(r, j) * H(k, j);  H has the TTM output
+// layout with width s.  CTA tile: 64 rows r (4 warps x 16) x all k, K = j in chunks of 16.
+// ----------------------------------------------------------------------------
+constexpr int kGramThreads = 128;
+
+template <int M8, bool RCONTIG>
+struct GramCfg {
+  static constexpr int RT = 64, JC = 16, STAGES = 4;
+  static constexpr int LDA = RCONTIG ? conflict_free_ld(RT) : conflict_free_ld(JC);
+  static constexpr int A_ELEMS = RCONTIG ? JC * LDA : RT * LDA;
+  static constexpr int LDH = conflict_free_ld(M8);
+  static constexpr int H_ELEMS = JC * LDH;
+  static constexpr int STAGE_ELEMS = A_ELEMS + H_ELEMS;
+  static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES;
+};
+
+template <int M8, bool RCONTIG>
+__global__ void __launch_bounds__(kGramThreads)
+    gram_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ h, int s,
+                int stot, int koff, double* __restrict__ zpart, long long jper) {
+  using C = GramCfg<M8, RCONTIG>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const long long J = v.inner * v.outer, I = v.I;
+  const long long r0 = (long long)blockIdx.x * C::RT;
+  const long long jbeg = (long long)blockIdx.y * jper;
+  const long long jend = min(J, jbeg + jper);
+  const int nk = (int)((jend - jbeg + C::JC - 1) / C::JC);
+
+  auto load = [&](int stage, int kt) {
+    double* As = smem + stage * C::STAGE_ELEMS;
+    double* Hs = As + C::A_ELEMS;
+    const long long jc0 = jbeg + (long long)kt * C::JC;
+    if (RCONTIG) {  // X(r, j) = x[I*j + r] -> As[j][r]
+#pragma unroll
+      for (int q = 0; q < (C::RT * C::JC) / kGramThreads; ++q) {
+        int e = tid + q * kGramThreads;
+        int rl = e % C::RT, jl = e / C::RT;
+        long long j = jc0 + jl, r = r0 + rl;
+        bool ok = (j < jend) && (r < I);
+        cp_async8(As + jl * C::LDA + rl, ok ? x + I * j + r : x, ok);
+      }
+      for (int e = tid; e < C::JC * M8; e += kGramThreads) {
+        int k = e % M8, jl = e / M8;
+        long long j = jc0 + jl;
+        bool ok = (j < jend) && (k < s);
+        cp_async8(Hs + jl * C::LDH + k, ok ? h + j * stot + koff + k : h, ok);
+      }
+    } else {  // X(r, j) = x[base_j + inner*r] -> As[r][j]
+      const int jl = tid % C::JC, rs = tid / C::JC;  // rs 0..7
+      const long long j = jc0 + jl;
+      const bool jok = j < jend;
+      long long base = 0, hbase = 0;
+      if (jok) {
+        long long o = j / v.inner, i = j - o * v.inner;
+        base = i + v.inner * I * o;
+        hbase = i + v.inner * ((long long)stot * o + koff);
+      }
+#pragma unroll
+      for (int q = 0; q < C::RT / 8; ++q) {
+        int rl = rs + 8 * q;
+        long long r = r0 + rl;
+        bool ok = jok && (r < I);
+        cp_async8(As + rl * C::LDA + jl, ok ? x + base + v.inner * r : x, ok);
+      }
+      for (int k = rs; k < M8; k += 8) {
+        bool ok = jok && (k < s);
+        cp_async8(Hs + jl * C::LDH + k, ok ? h + hbase + v.inner * k : h, ok);
+      }
+    }
+  };
+
+  constexpr int NF = M8 / 8;
+  double acc[NF][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[f][e] = 0.0;
+
+#pragma unroll
+  for (int st = 0; st < C::STAGES - 1; ++st) {
+    if (st < nk) load(st, st);
+    cp_async_commit();
+  }
+  const int rw = warp * 16;
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    const double* As = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
+    const double* Hs = As + C::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < C::JC / 4; ++kk) {
+      const int jj = kk * 4 + t;
+      double a0, a1;
+      if (RCONTIG) {
+        a0 = As[jj * C::LDA + rw + g];
+        a1 = As[jj * C::LDA + rw + g + 8];
+      } else {
+        a0 = As[(rw + g) * C::LDA + jj];
+        a1 = As[(rw + g + 8) * C::LDA + jj];
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) dmma16x8x4(acc[f], a0, a1, Hs[jj * C::LDH + f * 8 + g]);
+    }
+    const int nt = kt + C::STAGES - 1;
+    if (nt < nk) load(nt % C::STAGES, nt);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+
+  double* zp = zpart + (size_t)blockIdx.y * I * stot + (size_t)I * koff;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const long long r = r0 + rw + g + 8 * half;
+    if (r >= I) continue;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int k = f * 8 + 2 * t;
+      if (k < s) zp[r + I * k] = acc[f][2 * half];
+      if (k + 1 < s) zp[r + I * (k + 1)] = acc[f][2 * half + 1];
+    }
+  }
+}
+
+// z[e] = sum_{p < nsplit} zpart[p][e], fixed order (deterministic).
+__global__ void reduce_splits_kernel(const double* __restrict__ zpart, int nsplit, long long n,
+                                     double* __restrict__ z) {
+  long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double acc = zpart[e];
+  for (int p = 1; p < nsplit; ++p) acc += zpart[(size_t)p * n + e];
+  z[e] = acc;
+}
+
+// C'(:, t) = X(:, idx[t]) * scale[t]  (sketching.cpp:133-141), C' is I x T column-major.
+// One warp per sampled column for contiguous fibers; a 32x32 staged transpose otherwise.
+__global__ void gather_contig_kernel(const double* __restrict__ x, long long I,
+                                     const long long* __restrict__ idx,
+                                     const double* __restrict__ scale, long long T,
+                                     double* __restrict__ out) {
+  long long tcol = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (tcol >= T) return;
+  const int lane = threadIdx.x & 31;
+  const double* src = x + idx[tcol] * I;
+  const double sc = scale[tcol];
+  double* dst = out + tcol * I;
+  for (long long r = lane; r < I; r += 32) dst[r] = src[r] * sc;
+}
+
+__global__ void gather_strided_kernel(const double* __restrict__ x, ModeView v,
+                                      const long long* __restrict__ idx,
+                                      const double* __restrict__ scale, long long T,
+                                      double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const long long t0 = (long long)blockIdx.x * 32;
+  const long long tcol = t0 + tx;
+  long long base = 0;
+  double sc = 0.0;
+  const bool ok = tcol < T;
+  if (ok) {
+    base = col_base(idx[tcol], v.inner, v.I);
+    sc = scale[tcol];
+  }
+  for (long long r0 = 0; r0 < v.I; r0 += 32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int rl = ty + 8 * q;
+      long long r = r0 + rl;
+      tile[rl][tx] = (ok && r < v.I) ? x[base + v.inner * r] * sc : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int tl = ty + 8 * q;
+      long long tc = t0 + tl, r = r0 + tx;
+      if (tc < T && r < v.I) out[tc * v.I + r] = tile[tx][tl];
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// launchers
+// ----------------------------------------------------------------------------
+template <int M8, bool RC>
+static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt, int m, int mtot,
+                                int koff, double* y, cudaStream_t st) {
+  using C = TtmCfg<M8, RC>;
+  static unsigned long long attr_done = 0;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_kernel<M8, RC>), C::SMEM,
+                                   attr_done);
+  if (e != cudaSuccess) return e;
+  long long J = v.inner * v.outer;
+  dim3 grid((unsigned)((J + C::JT - 1) / C::JT));
+  ttm_kernel<M8, RC><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y);
+  return cudaGetLastError();
+}
+
+template <bool RC>
+static cudaError_t launch_ttm_rc(const double* x, ModeView v, const double* bt, int m, int mtot,
+                                 int koff, double* y, cudaStream_t st) {
+  switch ((m + 7) / 8) {
+    case 1: return launch_ttm_t<8, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 2: return launch_ttm_t<16, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 3: return launch_ttm_t<24, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 4: return launch_ttm_t<32, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 5: return launch_ttm_t<40, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 6: return launch_ttm_t<48, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 7: return launch_ttm_t<56, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 8: return launch_ttm_t<64, RC>(x, v, bt, m, mtot, koff, y, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
+                       cudaStream_t st) {
+  if (m < 1) return cudaErrorInvalidValue;
+  if (v.inner * v.outer == 0) return cudaSuccess;
+  // widths above one DMMA tile are done as column blocks of <= kMaxWidth output rows
+  for (int k0 = 0; k0 < m; k0 += kMaxWidth) {
+    int mb = std::min(kMaxWidth, m - k0);
+    const double* btb = bt + (size_t)v.I * k0;
+    cudaError_t e = v.inner == 1 ? launch_ttm_rc<true>(x, v, btb, mb, m, k0, y, st)
+                                 : launch_ttm_rc<false>(x, v, btb, mb, m, k0, y, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <int M8, bool RC>
+static cudaError_t launch_gram_t(const double* x, ModeView v, const double* h, int s, int stot,
+                                 int koff, double* zpart, int nsplit, long long jper,
+                                 cudaStream_t st) {
+  using C = GramCfg<M8, RC>;
+  static unsigned long long attr_done = 0;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_kernel<M8, RC>), C::SMEM,
+                                   attr_done);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((v.I + C::RT - 1) / C::RT), (unsigned)nsplit);
+  gram_kernel<M8, RC><<<grid, kGramThreads, C::SMEM, st>>>(x, v, h, s, stot, koff, zpart, jper);
+  return cudaGetLastError();
+}
+
+template <bool RC>
+static cudaError_t launch_gram_rc(const double* x, ModeView v, const double* h, int s, int stot,
+                                  int koff, double* zpart, int nsplit, long long jper,
+                                  cudaStream_t st) {
+  switch ((s + 7) / 8) {
+    case 1: return launch_gram_t<8, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 2: return launch_gram_t<16, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 3: return launch_gram_t<24, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 4: return launch_gram_t<32, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 5: return launch_gram_t<40, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 6: return launch_gram_t<48, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 7: return launch_gram_t<56, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 8: return launch_gram_t<64, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+GramPlan plan_gram(ModeView v, int num_sms) {
+  GramPlan p;
+  const long long J = v.inner * v.outer;
+  const long long rtiles = (v.I + 63) / 64;
+  long long target = (long long)num_sms * 4;
+  long long ns = std::max<long long>(1, target / std::max<long long>(1, rtiles));
+  // at least 256 columns per split so each CTA amortises its prologue
+  ns = std::min<long long>(ns, std::max<long long>(1, J / 256));
+  ns = std::min<long long>(ns, 1024);
+  long long jper = (J + ns - 1) / ns;
+  jper = ((jper + 15) / 16) * 16;
+  ns = (J + jper - 1) / jper;
+  p.nsplit = (int)std::max<long long>(1, ns);
+  p.jper = jper;
+  return p;
+}
+
+cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, double* zpart,
+                        const GramPlan& plan, double* z, cudaStream_t st) {
+  if (s < 1) return cudaErrorInvalidValue;
+  for (int k0 = 0; k0 < s; k0 += kMaxWidth) {
+    int sb = std::min(kMaxWidth, s - k0);
+    cudaError_t e =
+        v.inner == 1
+            ? launch_gram_rc<true>(x, v, h, sb, s, k0, zpart, plan.nsplit, plan.jper, st)
+            : launch_gram_rc<false>(x, v, h, sb, s, k0, zpart, plan.nsplit, plan.jper, st);
+    if (e != cudaSuccess) return e;
+  }
+  long long n = v.I * s;
+  reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(zpart, plan.nsplit, n, z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, const double* scale,
+                          long long T, double* out, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  if (v.inner == 1) {
+    gather_contig_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(x, v.I, idx, scale, T, out);
+  } else {
+    gather_strided_kernel<<<(unsigned)((T + 31) / 32), 256, 0, st>>>(x, v, idx, scale, T, out);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace lmra_dev

@@ -1,0 +1,877 @@
+// lmra_b200.cpp -- host orchestration of the randomized Tucker hot path + the C ABI.
+//
+// Mirrors the control flow of the reference's four entry points
+//   rand_thosvd_power  tucker.cpp:318-330   (alg1)
+//   rand_sthosvd_power tucker.cpp:332-346   (alg2)
+//   rand_thosvd_amm    tucker.cpp:378-395   (alg4)
+//   rand_sthosvd_amm   tucker.cpp:397-420   (alg5)
+// with every flop on the device (kernels/*.cu) and the tensor read in place (no unfold).
+// The only host work is what must be bit-exact with the reference's seeded host RNG:
+// Omega (gaussian_matrix) and the sampling chain (probabilities -> randsample).
+#include "../../include/lmra_b200.h"
+
+#include <cuda_runtime.h>
+#include "host/nccl_dyn.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "host/host_chain.hpp"
+#include "kernels/kernels.hpp"
+
+using lmra_dev::ModeView;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ckn(ncclResult_t e, const char* what) {
+  if (e != ncclSuccess) throw CudaError(std::string(what) + ": " + lmra_host::nccl().GetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return LMRA_OK;
+  } catch (const std::logic_error& e) {  // invalid_argument, out_of_range
+    g_err = e.what();
+    return LMRA_EINVAL;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return LMRA_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LMRA_ERUNTIME;
+  }
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct lmra_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  std::mutex mu;
+  long long launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Stream-ordered device buffer from the device's (retained) memory pool.
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t st) : st_(st), n_(n) {
+    if (n) ck(cudaMallocAsync(reinterpret_cast<void**>(&p_), std::max<size_t>(n, 2) * sizeof(double), st), "cudaMallocAsync");
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p_ = o.p_;
+    st_ = o.st_;
+    n_ = o.n_;
+    o.p_ = nullptr;
+    o.n_ = 0;
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  double* get() const { return p_; }
+  size_t size() const { return n_; }
+  double* detach() {
+    double* p = p_;
+    p_ = nullptr;
+    n_ = 0;
+    return p;
+  }
+
+ private:
+  void release() {
+    if (p_) cudaFreeAsync(p_, st_);
+    p_ = nullptr;
+  }
+  double* p_ = nullptr;
+  cudaStream_t st_ = nullptr;
+  size_t n_ = 0;
+};
+
+ModeView view_of(const std::vector<size_t>& dims, size_t mode) {
+  ModeView v;
+  v.inner = 1;
+  for (size_t k = 0; k < mode; ++k) v.inner *= (long long)dims[k];
+  v.I = (long long)dims[mode];
+  v.outer = 1;
+  for (size_t k = mode + 1; k < dims.size(); ++k) v.outer *= (long long)dims[k];
+  return v;
+}
+
+size_t prod(const std::vector<size_t>& d) {
+  size_t p = 1;
+  for (size_t x : d) p *= x;
+  return p;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ result
+struct lmra_result {
+  int device = 0;
+  std::vector<size_t> core_dims;
+  double* core = nullptr;
+  std::vector<size_t> f_rows, f_cols;
+  std::vector<double*> factors;
+  std::vector<size_t> om_rows, om_cols;
+  std::vector<std::vector<double>> omega;
+  std::vector<std::vector<int64_t>> idx;
+  std::vector<std::vector<double>> scales;
+  std::vector<std::vector<double>> norms;
+  double t_total = 0, t_rng = 0, t_sampling = 0, t_device = 0, launches = 0;
+  ~lmra_result() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != device) cudaSetDevice(device);
+    if (core) cudaFree(core);
+    for (double* f : factors)
+      if (f) cudaFree(f);
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ the engine
+class Engine {
+ public:
+  Engine(lmra_context* ctx) : ctx_(ctx), st_(ctx->stream) {}
+
+  void launched(cudaError_t e, const char* what) {
+    ck(e, what);
+    ++ctx_->launches;
+  }
+
+  // Y = X x_mode Q^T, Q is I x m column-major (already "bt" format)
+  DevBuf ttm(const double* x, const std::vector<size_t>& dims, size_t mode, const double* q,
+             size_t m) {
+    std::vector<size_t> od = dims;
+    od[mode] = m;
+    DevBuf y(prod(od), st_);
+    launched(lmra_dev::launch_ttm(x, view_of(dims, mode), q, (int)m, y.get(), st_), "ttm");
+    return y;
+  }
+
+  // c = (A A^T)^q G on the mode-`mode` unfolding view of a; c (I x s) in/out
+  void gram_power(const double* a, ModeView v, DevBuf& c, size_t s, int q, int strategy) {
+    const size_t I = (size_t)v.I, J = (size_t)(v.inner * v.outer);
+    lmra_dev::GramPlan plan = lmra_dev::plan_gram(v, ctx_->num_sms);
+    if (strategy == 0) {  // linalg.cpp:70-74, Strategy A
+      DevBuf h(J * s, st_);
+      DevBuf zpart((size_t)plan.nsplit * I * s, st_);
+      for (int k = 0; k < q; ++k) {
+        launched(lmra_dev::launch_ttm(a, v, c.get(), (int)s, h.get(), st_), "ttm(half)");
+        launched(lmra_dev::launch_gram(a, v, h.get(), (int)s, zpart.get(), plan, c.get(), st_),
+                 "gram");
+      }
+    } else {  // linalg.cpp:76-77, Strategy B: gram = A A^T once, then c = gram * c
+      DevBuf gram(I * I, st_), gramt(I * I, st_);
+      DevBuf zpart((size_t)plan.nsplit * I * I, st_);
+      launched(lmra_dev::launch_gram(a, v, a, (int)I, zpart.get(), plan, gram.get(), st_),
+               "gram(AA^T)");
+      launched(lmra_dev::launch_transpose(gram.get(), (long long)I, (long long)I, gramt.get(), st_),
+               "transpose");
+      ModeView cv{1, (long long)I, (long long)s};
+      for (int k = 0; k < q; ++k) {
+        DevBuf nc(I * s, st_);
+        launched(lmra_dev::launch_ttm(c.get(), cv, gramt.get(), (int)I, nc.get(), st_),
+                 "ttm(gram*c)");
+        c = std::move(nc);
+      }
+    }
+  }
+
+  DevBuf orth(const double* c, size_t I, size_t s, size_t mu, int* status) {
+    DevBuf u(I * mu, st_);
+    DevBuf work(lmra_dev::orth_workspace_doubles((long long)I, (int)s), st_);
+    launched(lmra_dev::launch_orth(c, (long long)I, (int)s, (int)mu, u.get(), work.get(), status,
+                                   st_),
+             "orth");
+    return u;
+  }
+
+  DevBuf upload(const double* h, size_t n) {
+    DevBuf d(n, st_);
+    ck(cudaMemcpyAsync(d.get(), h, n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D");
+    return d;
+  }
+
+  lmra_context* ctx_;
+  cudaStream_t st_;
+};
+
+struct RunInputs {
+  int alg;
+  const double* x;  // device
+  std::vector<size_t> dims;
+  lmra_host::Config cfg;
+  const lmra_overrides* ov;
+};
+
+// Per-mode factor: Omega -> (optional AMM sampling) -> power scheme -> orthonormalise.
+struct ModeFactor {
+  DevBuf q;
+};
+
+void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) {
+  using namespace lmra_host;
+  const double t0 = now_ms();
+  Engine eng(ctx);
+  cudaStream_t st = ctx->stream;
+  const auto& cfg = in.cfg;
+  const size_t N = in.dims.size();
+  for (size_t d : in.dims)
+    if (d == 0) throw std::invalid_argument("tensor dimension must be positive");
+  Resolved r = resolve(in.dims, cfg);
+  const bool amm = in.alg == LMRA_ALG4 || in.alg == LMRA_ALG5;
+  const bool sequential = in.alg == LMRA_ALG2 || in.alg == LMRA_ALG5;
+  std::vector<size_t> t_flat;
+  if (amm && !sequential) t_flat = amm_sample_counts(in.dims, cfg, false);
+  if (amm && sequential && !cfg.t_samples.empty() && cfg.t_samples.size() != N)
+    throw std::invalid_argument("sample count override length must equal tensor order");
+  for (size_t n = 0; n < N; ++n)
+    if (r.sketch[n] > (size_t)lmra_dev::kMaxWidth)
+      throw std::invalid_argument("sketch width mu_n + oversampling above 64 is not supported");
+
+  res->omega.assign(N, {});
+  res->om_rows.assign(N, 0);
+  res->om_cols.assign(N, 0);
+  res->idx.assign(N, {});
+  res->scales.assign(N, {});
+  res->norms.assign(N, {});
+  res->factors.assign(N, nullptr);
+  res->f_rows.assign(N, 0);
+  res->f_cols.assign(N, 0);
+
+  cudaEvent_t ev0, ev1;
+  ck(cudaEventCreate(&ev0), "event");
+  ck(cudaEventCreate(&ev1), "event");
+  ck(cudaEventRecord(ev0, st), "event");
+  const long long launches0 = ctx->launches;
+
+  // Omega for every mode up front (data independent; the GPU is idle anyway on the
+  // first mode only for the duration of the copy). gaussian_stream = {seed, n+1}.
+  const double tr0 = now_ms();
+  for (size_t n = 0; n < N; ++n) {
+    const size_t I = in.dims[n], s = r.sketch[n];
+    res->om_rows[n] = I;
+    res->om_cols[n] = s;
+    res->omega[n].resize(I * s);
+    if (in.ov && in.ov->omega && in.ov->omega[n]) {
+      std::memcpy(res->omega[n].data(), in.ov->omega[n], sizeof(double) * I * s);
+    } else {
+      fill_normals(cfg.seed, n + 1, res->omega[n].data(), I * s, host_threads());
+    }
+  }
+  res->t_rng = now_ms() - tr0;
+
+  std::vector<DevBuf> status_buf;
+  DevBuf status(N, st);  // int status per mode (stored in double slots)
+  ck(cudaMemsetAsync(status.get(), 0, N * sizeof(double), st), "memset");
+  int* status_i = reinterpret_cast<int*>(status.get());
+
+  auto mode_factor = [&](const double* x, const std::vector<size_t>& dims, size_t n,
+                         size_t t_n) -> DevBuf {
+    const ModeView v = view_of(dims, n);
+    const size_t I = dims[n], s = r.sketch[n], J = (size_t)(v.inner * v.outer);
+    DevBuf c = eng.upload(res->omega[n].data(), I * s);
+    if (!amm) {
+      eng.gram_power(x, v, c, s, cfg.power, cfg.strategy);
+    } else {
+      // sampling (tucker.cpp:110-130 + sketching.cpp:96-131); stream {seed, N+n+1}
+      const double ts0 = now_ms();
+      Samples smp;
+      if (in.ov && in.ov->sample_idx && in.ov->sample_idx[n]) {
+        const size_t T = in.ov->n_samples[n];
+        smp.idx.assign(in.ov->sample_idx[n], in.ov->sample_idx[n] + T);
+        smp.scales.assign(in.ov->sample_scale[n], in.ov->sample_scale[n] + T);
+        for (int64_t j : smp.idx)
+          if (j < 0 || (size_t)j >= J) throw std::invalid_argument("sample index out of range");
+      } else {
+        std::vector<double> p;
+        if (cfg.regime == kUniform) {
+          p = uniform_distribution(J);
+        } else {
+          DevBuf w(J, st);
+          eng.launched(lmra_dev::launch_column_sqnorms(x, v, w.get(), st), "sqnorms");
+          std::vector<double> wh(J);
+          ck(cudaMemcpyAsync(wh.data(), w.get(), J * sizeof(double), cudaMemcpyDeviceToHost, st),
+             "D2H norms");
+          ck(cudaStreamSynchronize(st), "sync");
+          res->norms[n] = wh;
+          p = probabilities_from_norms(std::move(wh), cfg.regime, cfg.beta);
+        }
+        smp = randsample(t_n, p, cfg.seed, N + n + 1);
+      }
+      res->t_sampling += now_ms() - ts0;
+      const size_t T = smp.idx.size();
+      DevBuf didx((T + 1), st), dsc(T, st);
+      ck(cudaMemcpyAsync(didx.get(), smp.idx.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice,
+                         st),
+         "H2D idx");
+      ck(cudaMemcpyAsync(dsc.get(), smp.scales.data(), T * sizeof(double), cudaMemcpyHostToDevice,
+                         st),
+         "H2D scales");
+      DevBuf cp(I * T, st);
+      eng.launched(lmra_dev::launch_gather(x, v, reinterpret_cast<const long long*>(didx.get()),
+                                           dsc.get(), (long long)T, cp.get(), st),
+                   "gather");
+      const ModeView cv{1, (long long)I, (long long)T};
+      eng.gram_power(cp.get(), cv, c, s, cfg.power, cfg.strategy);
+      // keep the host copies alive until the async copies have consumed them
+      ck(cudaStreamSynchronize(st), "sync");
+      res->idx[n] = std::move(smp.idx);
+      res->scales[n] = std::move(smp.scales);
+    }
+    const size_t mu = std::min(r.mu[n], std::min(I, s));  // top_left_vectors_clamped
+    if (mu < r.mu[n])
+      fprintf(stderr, "lmra: requested rank %zu exceeds matrix rank limit %zu, clamping\n",
+              r.mu[n], mu);
+    res->f_rows[n] = I;
+    res->f_cols[n] = mu;
+    return eng.orth(c.get(), I, s, mu, status_i + n);
+  };
+
+  std::vector<DevBuf> factors(N);
+  if (!sequential) {
+    for (size_t n = 0; n < N; ++n)
+      factors[n] = mode_factor(in.x, in.dims, n, amm ? t_flat[n] : 0);
+    // core_from_factors (tucker.cpp:81-92): ascending factor width, stable
+    std::vector<size_t> idx(N);
+    std::iota(idx.begin(), idx.end(), size_t{0});
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](size_t a, size_t b) { return res->f_cols[a] < res->f_cols[b]; });
+    std::vector<size_t> cur = in.dims;
+    DevBuf t;
+    const double* src = in.x;
+    for (size_t n : idx) {
+      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n]);
+      cur[n] = res->f_cols[n];
+      t = std::move(y);
+      src = t.get();
+    }
+    res->core_dims = cur;
+    res->core = t.detach();
+  } else {
+    std::vector<size_t> cur = in.dims;
+    DevBuf work;
+    const double* src = in.x;
+    for (size_t n : r.order) {
+      size_t t_n = 0;
+      if (amm) {
+        const size_t cols = prod(cur) / cur[n];
+        t_n = cfg.t_samples.empty() ? samples_from_alpha(cfg.alpha, cols) : cfg.t_samples[n];
+        if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
+      }
+      factors[n] = mode_factor(src, cur, n, t_n);
+      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n]);
+      cur[n] = res->f_cols[n];
+      work = std::move(y);
+      src = work.get();
+    }
+    res->core_dims = cur;
+    res->core = work.detach();
+  }
+  for (size_t n = 0; n < N; ++n) res->factors[n] = factors[n].detach();
+
+  ck(cudaEventRecord(ev1, st), "event");
+  std::vector<int> stat(2 * N);
+  ck(cudaMemcpyAsync(stat.data(), status.get(), N * sizeof(int), cudaMemcpyDeviceToHost, st),
+     "D2H status");
+  ck(cudaStreamSynchronize(st), "sync");
+  float dev_ms = 0;
+  ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event time");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  for (size_t n = 0; n < N; ++n)
+    if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  res->t_device = dev_ms;
+  res->launches = (double)(ctx->launches - launches0);
+  res->t_total = now_ms() - t0;
+}
+
+lmra_host::Config to_config(const lmra_algo_config* c) {
+  lmra_host::Config k;
+  if (!c) throw std::invalid_argument("null config");
+  if (c->n_rank && !c->rank) throw std::invalid_argument("null rank array");
+  k.mu.assign(c->rank, c->rank + c->n_rank);
+  k.oversampling = c->oversampling;
+  k.power = c->power;
+  k.alpha = c->alpha;
+  k.regime = c->regime;
+  k.beta = c->regime_beta;
+  if (c->n_t_samples) k.t_samples.assign(c->t_samples, c->t_samples + c->n_t_samples);
+  if (c->n_order) k.order.assign(c->order, c->order + c->n_order);
+  k.seed = c->seed;
+  k.strategy = c->strategy;
+  if (k.regime < 0 || k.regime > 2) throw std::invalid_argument("unknown probability regime");
+  if (k.strategy != 0 && k.strategy != 1) throw std::invalid_argument("unknown Gram strategy");
+  return k;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* lmra_last_error(void) { return g_err.c_str(); }
+const char* lmra_version(void) { return "lmra-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+void lmra_algo_config_init(lmra_algo_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->oversampling = 10;
+  cfg->power = 1;
+  cfg->alpha = 0.2;
+  cfg->regime = LMRA_UNIFORM;
+  cfg->regime_beta = 0.5;
+  cfg->strategy = LMRA_STRATEGY_A;
+}
+
+int lmra_context_create(int device, void* stream, lmra_context** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto c = std::make_unique<lmra_context>();
+    c->device = device;
+    DeviceGuard dg(device);
+    ck(cudaFree(nullptr), "cuda init");
+    ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+      c->own_stream = true;
+    }
+    cudaMemPool_t pool;
+    ck(cudaDeviceGetDefaultMemPool(&pool, device), "mempool");
+    uint64_t thresh = UINT64_MAX;
+    ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh), "mempool attr");
+    *out = c.release();
+  });
+}
+
+void lmra_context_destroy(lmra_context* ctx) {
+  if (!ctx) return;
+  {
+    DeviceGuard dg(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) lmra_host::nccl().CommDestroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+}
+
+int lmra_context_set_stream(lmra_context* ctx, void* stream) {
+  return guard([&] {
+    if (!stream) throw std::invalid_argument("null stream");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int lmra_context_synchronize(lmra_context* ctx) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_nccl_unique_id(void* out128) {
+  return guard([&] {
+    ncclUniqueId id;
+    ckn(lmra_host::nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int lmra_context_set_comm(lmra_context* ctx, const void* uid, int nranks, int rank) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank layout");
+    DeviceGuard dg(ctx->device);
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    if (ctx->comm) lmra_host::nccl().CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+    ckn(lmra_host::nccl().CommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+int lmra_shard_range(uint64_t extent, int nranks, int rank, uint64_t* start, uint64_t* count) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank layout");
+    uint64_t b = (extent * (uint64_t)rank) / (uint64_t)nranks;
+    uint64_t e = (extent * (uint64_t)(rank + 1)) / (uint64_t)nranks;
+    *start = b;
+    *count = e - b;
+  });
+}
+
+int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const uint64_t* dims,
+                       int order, int x_location, const lmra_algo_config* cfg,
+                       const lmra_overrides* overrides, lmra_result** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (algorithm != LMRA_ALG1 && algorithm != LMRA_ALG2 && algorithm != LMRA_ALG4 &&
+        algorithm != LMRA_ALG5)
+      throw std::invalid_argument("unknown algorithm");
+    if (order < 1) throw std::invalid_argument("cannot decompose an order-0 tensor");
+    if (ctx->nranks > 1)
+      throw std::invalid_argument("multi-GPU sharded run not available in this build");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    RunInputs in;
+    in.alg = algorithm;
+    in.dims.assign(dims, dims + order);
+    in.cfg = to_config(cfg);
+    in.ov = overrides;
+    auto res = std::make_unique<lmra_result>();
+    res->device = ctx->device;
+    DevBuf staged;
+    if (x_location == LMRA_HOST) {
+      size_t n = prod(in.dims);
+      staged = DevBuf(n, ctx->stream);
+      ck(cudaMemcpyAsync(staged.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
+         "H2D tensor");
+      in.x = staged.get();
+    } else {
+      in.x = x;
+    }
+    run_algorithm_impl(ctx, in, res.get());
+    *out = res.release();
+  });
+}
+
+int lmra_result_order(const lmra_result* r) { return (int)r->factors.size(); }
+void lmra_result_core_dims(const lmra_result* r, uint64_t* dims) {
+  for (size_t n = 0; n < r->core_dims.size(); ++n) dims[n] = r->core_dims[n];
+}
+static int copy_out(int device, double* dst, const double* src, size_t n, int loc) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    ck(cudaMemcpy(dst, src, n * sizeof(double),
+                  loc == LMRA_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice),
+       "copy out");
+  });
+}
+int lmra_result_copy_core(const lmra_result* r, double* dst, int dst_location) {
+  return copy_out(r->device, dst, r->core, prod(r->core_dims), dst_location);
+}
+void lmra_result_factor_dims(const lmra_result* r, int mode, uint64_t* rows, uint64_t* cols) {
+  *rows = r->f_rows[mode];
+  *cols = r->f_cols[mode];
+}
+int lmra_result_copy_factor(const lmra_result* r, int mode, double* dst, int dst_location) {
+  return copy_out(r->device, dst, r->factors[mode], r->f_rows[mode] * r->f_cols[mode],
+                  dst_location);
+}
+const double* lmra_result_core_device(const lmra_result* r) { return r->core; }
+const double* lmra_result_factor_device(const lmra_result* r, int mode) {
+  return r->factors[mode];
+}
+void lmra_result_omega_dims(const lmra_result* r, int mode, uint64_t* rows, uint64_t* cols) {
+  *rows = r->om_rows[mode];
+  *cols = r->om_cols[mode];
+}
+int lmra_result_copy_omega(const lmra_result* r, int mode, double* dst) {
+  std::memcpy(dst, r->omega[mode].data(), sizeof(double) * r->omega[mode].size());
+  return LMRA_OK;
+}
+uint64_t lmra_result_num_samples(const lmra_result* r, int mode) { return r->idx[mode].size(); }
+int lmra_result_copy_samples(const lmra_result* r, int mode, int64_t* idx, double* scales) {
+  std::memcpy(idx, r->idx[mode].data(), sizeof(int64_t) * r->idx[mode].size());
+  std::memcpy(scales, r->scales[mode].data(), sizeof(double) * r->scales[mode].size());
+  return LMRA_OK;
+}
+uint64_t lmra_result_num_norms(const lmra_result* r, int mode) { return r->norms[mode].size(); }
+int lmra_result_copy_norms(const lmra_result* r, int mode, double* w) {
+  std::memcpy(w, r->norms[mode].data(), sizeof(double) * r->norms[mode].size());
+  return LMRA_OK;
+}
+int lmra_result_timings(const lmra_result* r, double* out5) {
+  out5[0] = r->t_total;
+  out5[1] = r->t_rng;
+  out5[2] = r->t_sampling;
+  out5[3] = r->t_device;
+  out5[4] = r->launches;
+  return LMRA_OK;
+}
+void lmra_result_free(lmra_result* r) { delete r; }
+
+// ------------------------------------------------------------------ primitives
+int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
+                        int mode, const double* b, uint64_t b_rows, double* y) {
+  return guard([&] {
+    if (mode < 0 || mode >= order) throw std::out_of_range("mode_n_product: mode out of range");
+    if (b_rows < 1) throw std::invalid_argument("mode_n_product: empty matrix");
+    DeviceGuard dg(ctx->device);
+    std::vector<size_t> d(dims, dims + order);
+    const size_t I = d[mode];
+    Engine eng(ctx);
+    DevBuf bt(I * b_rows, ctx->stream);
+    eng.launched(lmra_dev::launch_transpose(b, (long long)b_rows, (long long)I, bt.get(), ctx->stream),
+                 "transpose");
+    eng.launched(lmra_dev::launch_ttm(x, view_of(d, (size_t)mode), bt.get(), (int)b_rows, y,
+                                      ctx->stream),
+                 "ttm");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uint64_t cols,
+                          const double* g, uint64_t s, int q, int strategy, double* c) {
+  return guard([&] {
+    if (q < 1) throw std::invalid_argument("gram_power_apply: q must be >= 1");
+    DeviceGuard dg(ctx->device);
+    Engine eng(ctx);
+    DevBuf cb(rows * s, ctx->stream);
+    ck(cudaMemcpyAsync(cb.get(), g, rows * s * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream),
+       "copy");
+    eng.gram_power(a, ModeView{1, (long long)rows, (long long)cols}, cb, s, q, strategy);
+    ck(cudaMemcpyAsync(c, cb.get(), rows * s * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream),
+       "copy");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint64_t rows,
+                                       uint64_t cols, uint64_t mu, double* u) {
+  return guard([&] {
+    if (mu < 1 || mu > std::min(rows, cols))
+      throw std::invalid_argument("leading_left_singular_vectors: mu out of range");
+    if (rows < cols) throw std::invalid_argument("leading_left_singular_vectors: needs rows >= cols");
+    if (cols > (uint64_t)lmra_dev::kMaxWidth)
+      throw std::invalid_argument("leading_left_singular_vectors: more than 64 columns");
+    DeviceGuard dg(ctx->device);
+    Engine eng(ctx);
+    DevBuf status(1, ctx->stream);
+    ck(cudaMemsetAsync(status.get(), 0, sizeof(double), ctx->stream), "memset");
+    DevBuf out = eng.orth(c, rows, cols, mu, reinterpret_cast<int*>(status.get()));
+    ck(cudaMemcpyAsync(u, out.get(), rows * mu * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream),
+       "copy");
+    int st = 0;
+    ck(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    if (st) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  });
+}
+
+int lmra_column_sqnorms(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
+                        int mode, double* w) {
+  return guard([&] {
+    if (mode < 0 || mode >= order) throw std::out_of_range("mode out of range");
+    DeviceGuard dg(ctx->device);
+    std::vector<size_t> d(dims, dims + order);
+    Engine eng(ctx);
+    eng.launched(lmra_dev::launch_column_sqnorms(x, view_of(d, (size_t)mode), w, ctx->stream),
+                 "sqnorms");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_gaussian_matrix(uint64_t rows, uint64_t cols, uint64_t seed, uint64_t stream,
+                         double* out) {
+  return guard([&] {
+    if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_matrix: shape must be positive");
+    lmra_host::fill_normals(seed, stream, out, rows * cols, lmra_host::host_threads());
+  });
+}
+
+int lmra_probabilities(const double* w, uint64_t n, int regime, double beta, double* p) {
+  return guard([&] {
+    std::vector<double> v(w, w + n);
+    auto out = lmra_host::probabilities_from_norms(std::move(v), regime, beta);
+    std::memcpy(p, out.data(), sizeof(double) * n);
+  });
+}
+
+int lmra_randsample(uint64_t L, const double* p, uint64_t n, uint64_t seed, uint64_t stream,
+                    int64_t* idx, double* scales) {
+  return guard([&] {
+    std::vector<double> pv(p, p + n);
+    lmra_host::check_distribution(pv);
+    auto s = lmra_host::randsample(L, pv, seed, stream);
+    std::memcpy(idx, s.idx.data(), sizeof(int64_t) * L);
+    std::memcpy(scales, s.scales.data(), sizeof(double) * L);
+  });
+}
+
+int lmra_amm_sample_counts(const uint64_t* dims, int order, const lmra_algo_config* cfg,
+                           int sequential, uint64_t* out) {
+  return guard([&] {
+    std::vector<size_t> d(dims, dims + order);
+    auto c = lmra_host::amm_sample_counts(d, to_config(cfg), sequential != 0);
+    for (int n = 0; n < order; ++n) out[n] = c[n];
+  });
+}
+
+// ------------------------------------------------------------------ generators
+int lmra_gen_hilbert(lmra_context* ctx, const uint64_t* dims, int order, double* x) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    std::vector<long long> d(dims, dims + order);
+    ck(lmra_dev::launch_gen_hilbert(x, d.data(), order, ctx->stream), "gen_hilbert");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_gen_tucker_noise(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims,
+                          int order, double gamma, uint64_t seed, double* x) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    cudaStream_t st = ctx->stream;
+    Engine eng(ctx);
+    std::vector<size_t> d(dims, dims + order), cd(core_dims, core_dims + order);
+    for (int n = 0; n < order; ++n)
+      if (cd[n] > d[n] || cd[n] < 1 || cd[n] > (size_t)lmra_dev::kMaxWidth)
+        throw std::invalid_argument("core dimensions must lie in [1, min(I_n, 64)]");
+    // G ~ N(0,1) (stream 100), U_n = orthonormal basis of N(0,1) I_n x mu_n (stream 101+n)
+    DevBuf b(prod(cd), st);
+    ck(lmra_dev::launch_gen_normals(b.get(), (long long)prod(cd), seed, 100, st), "normals");
+    std::vector<size_t> cur = cd;
+    for (int n = 0; n < order; ++n) {
+      DevBuf m(d[n] * cd[n], st), u(d[n] * cd[n], st), ut(d[n] * cd[n], st);
+      ck(lmra_dev::launch_gen_normals(m.get(), (long long)(d[n] * cd[n]), seed, 101 + n, st), "normals");
+      DevBuf status(1, st);
+      DevBuf uu = eng.orth(m.get(), d[n], cd[n], cd[n], reinterpret_cast<int*>(status.get()));
+      // B <- B x_n U  (U is I_n x mu_n; bt = U^T, mu_n x I_n)
+      ck(lmra_dev::launch_transpose(uu.get(), (long long)d[n], (long long)cd[n], ut.get(), st),
+         "transpose");
+      std::vector<size_t> od = cur;
+      od[n] = d[n];
+      DevBuf y(prod(od), st);
+      ck(lmra_dev::launch_ttm(b.get(), view_of(cur, n), ut.get(), (int)d[n], y.get(), st), "ttm");
+      b = std::move(y);
+      cur = od;
+    }
+    const size_t total = prod(d);
+    DevBuf e(total, st);
+    ck(lmra_dev::launch_gen_normals(e.get(), (long long)total, seed, 200, st), "normals");
+    const int parts = 1024;
+    DevBuf pb(parts, st), pe(parts, st);
+    ck(lmra_dev::launch_sumsq(b.get(), (long long)total, pb.get(), parts, st), "sumsq");
+    ck(lmra_dev::launch_sumsq(e.get(), (long long)total, pe.get(), parts, st), "sumsq");
+    std::vector<double> hb(parts), he(parts);
+    ck(cudaMemcpyAsync(hb.data(), pb.get(), parts * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(he.data(), pe.get(), parts * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    double nb = 0, ne = 0;
+    for (int i = 0; i < parts; ++i) {
+      nb += hb[i];
+      ne += he[i];
+    }
+    const double coef = gamma * std::sqrt(nb) / std::sqrt(ne);
+    ck(lmra_dev::launch_axpby(b.get(), e.get(), coef, x, (long long)total, st), "axpby");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int lmra_gen_video(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms,
+                   double noise, uint64_t seed, double* x) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    cudaStream_t st = ctx->stream;
+    std::vector<size_t> d(dims, dims + order);
+    // profiles on the host with glibc cos (bit-identical to the oracle's), packed per mode
+    size_t tot = 0;
+    for (size_t v : d) tot += v * n_terms;
+    std::vector<double> prof(tot), w(n_terms);
+    for (size_t t = 0; t < n_terms; ++t) {
+      lmra_host::Rng g(seed, 300 + t);
+      w[t] = g.next_double();
+      size_t off = 0;
+      for (int n = 0; n < order; ++n) {
+        double f = 0.5 + 7.5 * g.next_double();
+        double ph = 6.283185307179586476925286766559 * g.next_double();
+        for (size_t i = 0; i < d[n]; ++i) {
+          double xx = static_cast<double>(i) / static_cast<double>(d[n]);
+          prof[off + i + d[n] * t] = std::cos(6.283185307179586476925286766559 * f * xx + ph);
+        }
+        off += d[n] * n_terms;
+      }
+    }
+    Engine eng(ctx);
+    DevBuf dp = eng.upload(prof.data(), tot), dw = eng.upload(w.data(), n_terms);
+    std::vector<long long> dl(d.begin(), d.end());
+    ck(lmra_dev::launch_gen_cp(x, dl.data(), order, dp.get(), dw.get(), (int)n_terms, st), "gen_cp");
+    ck(lmra_dev::launch_gen_uniform_add(x, (long long)prod(d), noise, seed, 400, st), "uniform");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int lmra_device_alloc(lmra_context* ctx, size_t bytes, void** out) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    ck(cudaMalloc(out, std::max<size_t>(bytes, 16)), "cudaMalloc");
+  });
+}
+
+int lmra_device_free(lmra_context* ctx, void* p) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    ck(cudaFree(p), "cudaFree");
+  });
+}
+
+int lmra_memcpy(lmra_context* ctx, void* dst, const void* src, size_t bytes, int dst_location,
+                int src_location) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    cudaMemcpyKind k = src_location == LMRA_HOST
+                           ? (dst_location == LMRA_HOST ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice)
+                           : (dst_location == LMRA_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+    ck(cudaMemcpyAsync(dst, src, bytes, k, ctx->stream), "memcpy");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+}  // extern "C"

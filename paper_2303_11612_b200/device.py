@@ -1,0 +1,109 @@
+"""Device-side helpers over the C ABI, with torch as the allocator (plumbing only).
+
+Primitives on device buffers (mode_n_product, gram_power_apply,
+leading_left_singular_vectors, column_sqnorms) and the BASELINE input generators.
+All tensors here are flat float64 CUDA tensors in the reference's layout (first
+index fastest) together with explicit dims.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .tucker import Context, default_context
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _u64(v):
+    return np.ascontiguousarray(np.asarray(v, dtype=np.uint64))
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+def empty(n: int, device: int = 0):
+    torch = _torch()
+    return torch.empty(int(n), dtype=torch.float64, device=f"cuda:{device}")
+
+
+def mode_n_product(x, dims: Sequence[int], mode: int, b, ctx: Context = None):
+    """y = x x_mode b  (tensor.cpp:118-139); b: torch (rows x I_mode) row-major -> passed
+    column-major as the reference's Eigen matrix."""
+    ctx = ctx or default_context()
+    torch = _torch()
+    bc = b.t().contiguous().view(-1) if b.dim() == 2 else b  # column-major flat
+    rows = b.shape[0]
+    out_dims = list(dims)
+    out_dims[mode] = rows
+    y = empty(int(np.prod(out_dims)), ctx.device)
+    d = _u64(dims)
+    torch.cuda.current_stream().synchronize()
+    check(lib.lmra_mode_n_product(ctx.handle, _ptr(x), d.ctypes.data_as(_lib.u64p), len(dims), mode,
+                                  _ptr(bc), rows, _ptr(y)))
+    return y, out_dims
+
+
+def gram_power_apply(a_colmajor, rows: int, cols: int, g_colmajor, s: int, q: int,
+                     strategy: str = "A", ctx: Context = None):
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    c = empty(rows * s, ctx.device)
+    check(lib.lmra_gram_power_apply(ctx.handle, _ptr(a_colmajor), rows, cols, _ptr(g_colmajor), s, q,
+                                    0 if strategy == "A" else 1, _ptr(c)))
+    return c
+
+
+def leading_left_singular_vectors(c_colmajor, rows: int, cols: int, mu: int, ctx: Context = None):
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    u = empty(rows * mu, ctx.device)
+    check(lib.lmra_leading_left_singular_vectors(ctx.handle, _ptr(c_colmajor), rows, cols, mu, _ptr(u)))
+    return u
+
+
+def column_sqnorms(x, dims: Sequence[int], mode: int, ctx: Context = None):
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    J = int(np.prod(dims)) // int(dims[mode])
+    w = empty(J, ctx.device)
+    d = _u64(dims)
+    check(lib.lmra_column_sqnorms(ctx.handle, _ptr(x), d.ctypes.data_as(_lib.u64p), len(dims), mode,
+                                  _ptr(w)))
+    return w
+
+
+# ---------------------------------------------------------------- BASELINE generators
+def gen_tucker_noise(dims, core_dims, gamma: float, seed: int, ctx: Context = None):
+    ctx = ctx or default_context()
+    x = empty(int(np.prod(dims)), ctx.device)
+    _torch().cuda.current_stream().synchronize()
+    check(lib.lmra_gen_tucker_noise(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p),
+                                    _u64(core_dims).ctypes.data_as(_lib.u64p), len(dims),
+                                    C.c_double(gamma), C.c_uint64(seed), _ptr(x)))
+    return x
+
+
+def gen_hilbert(dims, ctx: Context = None):
+    ctx = ctx or default_context()
+    x = empty(int(np.prod(dims)), ctx.device)
+    _torch().cuda.current_stream().synchronize()
+    check(lib.lmra_gen_hilbert(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims), _ptr(x)))
+    return x
+
+
+def gen_video(dims, n_terms: int = 30, noise: float = 0.05, seed: int = 1, ctx: Context = None):
+    ctx = ctx or default_context()
+    x = empty(int(np.prod(dims)), ctx.device)
+    _torch().cuda.current_stream().synchronize()
+    check(lib.lmra_gen_video(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims),
+                             C.c_uint64(n_terms), C.c_double(noise), C.c_uint64(seed), _ptr(x)))
+    return x

@@ -1,0 +1,415 @@
+"""Host-side mirror of the reference's Tucker interface (proj/include/lmra/tucker.hpp).
+
+Same names, argument meaning and error behaviour as the reference's C++ API:
+
+    reference (namespace lmra)                       here
+    struct AlgoConfig          tucker.hpp:32-45      AlgoConfig
+    struct TuckerDecomposition tucker.hpp:27-30      TuckerDecomposition
+    rand_thosvd_power          tucker.hpp:91         rand_thosvd_power   (alg1)
+    rand_sthosvd_power         tucker.hpp:95         rand_sthosvd_power  (alg2)
+    rand_thosvd_amm            tucker.hpp:99         rand_thosvd_amm     (alg4)
+    rand_sthosvd_amm           tucker.hpp:102        rand_sthosvd_amm    (alg5)
+    run_algorithm              tucker.hpp:110        run_algorithm
+    amm_sample_counts          tucker.hpp:116        amm_sample_counts
+    parse_algorithm / algorithm_id / all_algorithm_ids (tucker.hpp:59-61)
+
+std::invalid_argument surfaces as LmraInvalidArgument (a ValueError), runtime_error
+as LmraError.  Every call goes through the C ABI (include/lmra_b200.h) into the
+sm_100a kernels -- there is no CPU path.
+
+Tensor convention: the reference's linearisation, first index fastest
+(tensor.hpp:9-12).  A numpy ndarray `a` is read as a[i0, i1, ...] (Fortran-order
+flattening); device data is passed as DenseTensor.on_device(ptr_or_torch, dims).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import LmraError, LmraInvalidArgument, check, lib
+
+ALGORITHM_IDS = ["thosvd", "sthosvd", "hooi", "alg1", "alg2", "alg4", "alg5", "alg6", "alg7"]
+_ALG_CODE = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5}
+_REGIME = {"optimal": 0, "nearly_optimal": 1, "uniform": 2}
+_STRATEGY = {"A": 0, "B": 1}
+
+
+def parse_algorithm(name: str) -> Optional[str]:
+    """tucker.cpp:190-201: returns the id if known, else None."""
+    return name if name in ALGORITHM_IDS else None
+
+
+def algorithm_id(a: str) -> str:
+    return a
+
+
+def all_algorithm_ids() -> List[str]:
+    return list(ALGORITHM_IDS)
+
+
+@dataclass
+class AlgoConfig:
+    """lmra::AlgoConfig (tucker.hpp:32-45) with the reference's defaults."""
+    rank: Sequence[int]
+    oversampling: int = 10
+    power: int = 1
+    alpha: float = 0.2
+    regime: str = "uniform"          # "optimal" | "nearly_optimal" | "uniform"
+    regime_beta: float = 0.5
+    t_samples: Optional[Sequence[int]] = None
+    order: Optional[Sequence[int]] = None
+    seed: int = 0
+    strategy: str = "A"              # GramStrategy
+
+    def _to_c(self):
+        if self.regime not in _REGIME:
+            raise LmraInvalidArgument(f"unknown probability regime {self.regime!r}")
+        if self.strategy not in _STRATEGY:
+            raise LmraInvalidArgument(f"unknown Gram strategy {self.strategy!r}")
+        keep = []
+
+        def arr(v):
+            if v is None:
+                return None, 0
+            a = np.ascontiguousarray(np.asarray(v, dtype=np.uint64))
+            keep.append(a)
+            return a.ctypes.data_as(_lib.u64p), a.size
+
+        for name, v in (("rank", self.rank), ("t_samples", self.t_samples), ("order", self.order)):
+            if v is not None and any(int(x) < 0 for x in v):
+                raise LmraInvalidArgument(f"{name} entries must be non-negative")
+        c = _lib.LmraAlgoConfig()
+        lib.lmra_algo_config_init(C.byref(c))
+        c.rank, c.n_rank = arr(self.rank)
+        c.oversampling = int(self.oversampling)
+        c.power = int(self.power)
+        c.alpha = float(self.alpha)
+        c.regime = _REGIME[self.regime]
+        c.regime_beta = float(self.regime_beta)
+        c.t_samples, c.n_t_samples = arr(self.t_samples)
+        c.order, c.n_order = arr(self.order)
+        c.seed = int(self.seed)
+        c.strategy = _STRATEGY[self.strategy]
+        return c, keep
+
+
+class DenseTensor:
+    """Dense fp64 tensor in the reference's layout (first index fastest).
+
+    Host: `data` is a flat numpy float64 array.  Device: `ptr` is a device address
+    (int), optionally with the owning torch tensor kept alive in `owner`.
+    """
+
+    def __init__(self, dims: Sequence[int], data: Optional[np.ndarray] = None, ptr: int = 0,
+                 owner=None):
+        self.dims = [int(d) for d in dims]
+        self.data = data
+        self.ptr = int(ptr)
+        self.owner = owner
+
+    @property
+    def on_device(self) -> bool:
+        return self.data is None
+
+    @staticmethod
+    def from_array(a: np.ndarray) -> "DenseTensor":
+        a = np.asarray(a, dtype=np.float64)
+        return DenseTensor(list(a.shape), np.ascontiguousarray(a.ravel(order="F")))
+
+    @staticmethod
+    def from_flat(flat: np.ndarray, dims: Sequence[int]) -> "DenseTensor":
+        flat = np.ascontiguousarray(np.asarray(flat, dtype=np.float64).ravel())
+        if flat.size != int(np.prod(dims)):
+            raise LmraInvalidArgument("value count does not match tensor shape")
+        return DenseTensor(dims, flat)
+
+    @staticmethod
+    def device(t, dims: Sequence[int]) -> "DenseTensor":
+        """t: a contiguous float64 CUDA torch tensor (any shape; read flat) or a raw pointer."""
+        if isinstance(t, int):
+            return DenseTensor(dims, None, t)
+        if t.dtype.__repr__() != "torch.float64" or not t.is_cuda or not t.is_contiguous():
+            raise LmraInvalidArgument("device tensors must be contiguous float64 CUDA tensors")
+        if t.numel() != int(np.prod(dims)):
+            raise LmraInvalidArgument("value count does not match tensor shape")
+        return DenseTensor(dims, None, t.data_ptr(), owner=t)
+
+    def size(self) -> int:
+        return int(np.prod(self.dims))
+
+    def to_array(self) -> np.ndarray:
+        if self.on_device:
+            raise LmraError("device tensor: copy it to the host first")
+        return self.data.reshape(self.dims, order="F")
+
+
+@dataclass
+class TuckerDecomposition:
+    """lmra::TuckerDecomposition (tucker.hpp:27-30) plus the run's trace."""
+    core: np.ndarray                     # shape = core dims (a[i0, i1, ...] indexing)
+    factors: List[np.ndarray]            # I_n x mu_n, orthonormal columns
+    omega: List[np.ndarray] = field(default_factory=list)
+    samples: List[Optional[tuple]] = field(default_factory=list)
+    norms: List[Optional[np.ndarray]] = field(default_factory=list)
+    timings_ms: dict = field(default_factory=dict)
+
+
+class Context:
+    """One lmra_context (device + stream [+ NCCL communicator])."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        h = C.c_void_p()
+        check(lib.lmra_context_create(int(device), C.c_void_p(stream or 0), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def set_stream(self, stream: int):
+        check(lib.lmra_context_set_stream(self.handle, C.c_void_p(stream)))
+
+    def synchronize(self):
+        check(lib.lmra_context_synchronize(self.handle))
+
+    def set_comm(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib.lmra_context_set_comm(self.handle, buf, int(nranks), int(rank)))
+
+    def close(self):
+        if self.handle:
+            lib.lmra_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib.lmra_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_range(extent: int, nranks: int, rank: int):
+    s, c = C.c_uint64(), C.c_uint64()
+    check(lib.lmra_shard_range(C.c_uint64(extent), int(nranks), int(rank), C.byref(s), C.byref(c)))
+    return s.value, c.value
+
+
+_default = {}
+_default_lock = threading.Lock()
+
+
+def default_context(device: int = 0) -> Context:
+    with _default_lock:
+        if device not in _default:
+            _default[device] = Context(device)
+        return _default[device]
+
+
+def _overrides(n_modes: int, omega=None, samples=None):
+    if omega is None and samples is None:
+        return None, []
+    keep = []
+    ov = _lib.LmraOverrides()
+    if omega is not None:
+        arr = (_lib.dblp * n_modes)()
+        for n, g in enumerate(omega):
+            if g is None:
+                continue
+            gf = np.asfortranarray(np.asarray(g, dtype=np.float64))
+            keep.append(gf)
+            arr[n] = gf.ctypes.data_as(_lib.dblp)
+        keep.append(arr)
+        ov.omega = C.cast(arr, C.POINTER(_lib.dblp))
+    if samples is not None:
+        ia = (_lib.i64p * n_modes)()
+        sa = (_lib.dblp * n_modes)()
+        na = np.zeros(n_modes, dtype=np.uint64)
+        for n, sm in enumerate(samples):
+            if sm is None:
+                continue
+            idx = np.ascontiguousarray(np.asarray(sm[0], dtype=np.int64))
+            sc = np.ascontiguousarray(np.asarray(sm[1], dtype=np.float64))
+            keep += [idx, sc]
+            ia[n] = idx.ctypes.data_as(_lib.i64p)
+            sa[n] = sc.ctypes.data_as(_lib.dblp)
+            na[n] = idx.size
+        keep += [ia, sa, na]
+        ov.sample_idx = C.cast(ia, C.POINTER(_lib.i64p))
+        ov.sample_scale = C.cast(sa, C.POINTER(_lib.dblp))
+        ov.n_samples = na.ctypes.data_as(_lib.u64p)
+    return ov, keep
+
+
+class _Result:
+    """Owning wrapper of an lmra_result handle (device-resident core and factors)."""
+
+    def __init__(self, handle, order: int):
+        self.handle = handle
+        self.order = order
+
+    def core_dims(self):
+        d = np.zeros(self.order, dtype=np.uint64)
+        lib.lmra_result_core_dims(self.handle, d.ctypes.data_as(_lib.u64p))
+        return [int(v) for v in d]
+
+    def factor_dims(self, n):
+        r, c = C.c_uint64(), C.c_uint64()
+        lib.lmra_result_factor_dims(self.handle, n, C.byref(r), C.byref(c))
+        return r.value, c.value
+
+    def core_device_ptr(self) -> int:
+        return lib.lmra_result_core_device(self.handle) or 0
+
+    def factor_device_ptr(self, n) -> int:
+        return lib.lmra_result_factor_device(self.handle, n) or 0
+
+    def to_host(self, with_trace: bool = True) -> TuckerDecomposition:
+        cd = self.core_dims()
+        core = np.empty(int(np.prod(cd)))
+        check(lib.lmra_result_copy_core(self.handle, C.c_void_p(core.ctypes.data), _lib.LMRA_HOST))
+        factors, omega, samples, norms = [], [], [], []
+        for n in range(self.order):
+            r, c = self.factor_dims(n)
+            f = np.empty(r * c)
+            check(lib.lmra_result_copy_factor(self.handle, n, C.c_void_p(f.ctypes.data), _lib.LMRA_HOST))
+            factors.append(f.reshape((r, c), order="F"))
+            if with_trace:
+                orow, ocol = C.c_uint64(), C.c_uint64()
+                lib.lmra_result_omega_dims(self.handle, n, C.byref(orow), C.byref(ocol))
+                g = np.empty(orow.value * ocol.value)
+                if g.size:
+                    lib.lmra_result_copy_omega(self.handle, n, g.ctypes.data_as(_lib.dblp))
+                omega.append(g.reshape((orow.value, ocol.value), order="F"))
+                T = lib.lmra_result_num_samples(self.handle, n)
+                if T:
+                    idx = np.empty(T, dtype=np.int64)
+                    sc = np.empty(T)
+                    lib.lmra_result_copy_samples(self.handle, n, idx.ctypes.data_as(_lib.i64p),
+                                                 sc.ctypes.data_as(_lib.dblp))
+                    samples.append((idx, sc))
+                else:
+                    samples.append(None)
+                W = lib.lmra_result_num_norms(self.handle, n)
+                if W:
+                    w = np.empty(W)
+                    lib.lmra_result_copy_norms(self.handle, n, w.ctypes.data_as(_lib.dblp))
+                    norms.append(w)
+                else:
+                    norms.append(None)
+        return TuckerDecomposition(core.reshape(cd, order="F"), factors, omega, samples, norms,
+                                   self.timings())
+
+    def timings(self) -> dict:
+        t = np.zeros(5)
+        lib.lmra_result_timings(self.handle, t.ctypes.data_as(_lib.dblp))
+        return {"total_ms": t[0], "host_rng_ms": t[1], "host_sampling_ms": t[2],
+                "device_ms": t[3], "launches": int(t[4])}
+
+    def free(self):
+        if self.handle:
+            lib.lmra_result_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _as_tensor(a) -> DenseTensor:
+    if isinstance(a, DenseTensor):
+        return a
+    return DenseTensor.from_array(np.asarray(a))
+
+
+def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omega=None,
+            samples=None) -> _Result:
+    """run_algorithm returning the device-resident result handle (no copy-out)."""
+    if alg not in _ALG_CODE:
+        if alg in ALGORITHM_IDS:
+            raise LmraInvalidArgument(f"{alg} is outside the B200 hot path (alg1/alg2/alg4/alg5)")
+        raise LmraInvalidArgument("unknown algorithm")
+    t = _as_tensor(a)
+    ctx = ctx or default_context()
+    dims = np.asarray(t.dims, dtype=np.uint64)
+    c, keep = cfg._to_c()
+    ov, keep2 = _overrides(len(t.dims), omega, samples)
+    h = C.c_void_p()
+    if t.on_device:
+        xp, loc = C.c_void_p(t.ptr), _lib.LMRA_DEVICE
+    else:
+        xp, loc = C.c_void_p(t.data.ctypes.data), _lib.LMRA_HOST
+    rc = lib.lmra_run_algorithm(ctx.handle, _ALG_CODE[alg], xp, dims.ctypes.data_as(_lib.u64p),
+                                len(t.dims), loc, C.byref(c), C.byref(ov) if ov is not None else None,
+                                C.byref(h))
+    del keep, keep2
+    check(rc)
+    return _Result(h, len(t.dims))
+
+
+def run_algorithm(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omega=None,
+                  samples=None) -> TuckerDecomposition:
+    """tucker.cpp:456-470.  omega / samples: per-mode parity overrides (None = seeded RNG)."""
+    r = run_raw(alg, a, cfg, ctx=ctx, omega=omega, samples=samples)
+    try:
+        return r.to_host()
+    finally:
+        r.free()
+
+
+def rand_thosvd_power(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    return run_algorithm("alg1", a, cfg, **kw)
+
+
+def rand_sthosvd_power(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    return run_algorithm("alg2", a, cfg, **kw)
+
+
+def rand_thosvd_amm(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    return run_algorithm("alg4", a, cfg, **kw)
+
+
+def rand_sthosvd_amm(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    return run_algorithm("alg5", a, cfg, **kw)
+
+
+def amm_sample_counts(dims: Sequence[int], cfg: AlgoConfig, sequential: bool) -> List[int]:
+    d = np.asarray(dims, dtype=np.uint64)
+    out = np.zeros(len(dims), dtype=np.uint64)
+    c, keep = cfg._to_c()
+    check(lib.lmra_amm_sample_counts(d.ctypes.data_as(_lib.u64p), len(dims), C.byref(c),
+                                     int(bool(sequential)), out.ctypes.data_as(_lib.u64p)))
+    return [int(v) for v in out]
+
+
+# ---------------------------------------------------------------- host restatements on the path
+def gaussian_matrix(rows: int, cols: int, seed: int, stream: int) -> np.ndarray:
+    out = np.empty(rows * cols)
+    check(lib.lmra_gaussian_matrix(rows, cols, seed, stream, out.ctypes.data_as(_lib.dblp)))
+    return out.reshape((rows, cols), order="F")
+
+
+def probabilities(w, regime: str, beta: float = 0.5) -> np.ndarray:
+    w = np.ascontiguousarray(np.asarray(w, dtype=np.float64))
+    p = np.empty_like(w)
+    check(lib.lmra_probabilities(w.ctypes.data_as(_lib.dblp), w.size, _REGIME[regime], beta,
+                                 p.ctypes.data_as(_lib.dblp)))
+    return p
+
+
+def randsample(L: int, p, seed: int, stream: int):
+    p = np.ascontiguousarray(np.asarray(p, dtype=np.float64))
+    idx = np.empty(L, dtype=np.int64)
+    sc = np.empty(L)
+    check(lib.lmra_randsample(L, p.ctypes.data_as(_lib.dblp), p.size, seed, stream,
+                              idx.ctypes.data_as(_lib.i64p), sc.ctypes.data_as(_lib.dblp)))
+    return idx, sc
