@@ -128,6 +128,13 @@ int lmra_result_copy_norms(const lmra_result* r, int mode, double* w);
 /* phase timings of the run (milliseconds): [0] total wall, [1] host RNG (Omega),
  * [2] host sampling chains, [3] device time of the run (events), [4] kernel launches */
 int lmra_result_timings(const lmra_result* r, double* out5);
+/* per-phase device time (CUDA events around each launch on the context's stream), only
+ * recorded when lmra_context_set_profiling(ctx, 1).  Phases: norms, gather, power_half,
+ * power_gram, orth, core_ttm<k> (k-th contraction of core_from_factors), shrink_ttm_m<n>. */
+int lmra_context_set_profiling(lmra_context* ctx, int on);
+int lmra_result_num_phases(const lmra_result* r);
+int lmra_result_phase(const lmra_result* r, int i, char* name, size_t name_len, double* ms,
+                      int* launches);
 void lmra_result_free(lmra_result* r);
 
 /* ---- primitives (device pointers unless stated; all on the context's stream) ---- */

@@ -79,6 +79,10 @@ def _load():
         "lmra_result_copy_norms": (C.c_int, [vp, C.c_int, dblp]),
         "lmra_result_timings": (C.c_int, [vp, dblp]),
         "lmra_result_free": (None, [vp]),
+        "lmra_context_set_profiling": (C.c_int, [vp, C.c_int]),
+        "lmra_result_num_phases": (C.c_int, [vp]),
+        "lmra_result_phase": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, dblp,
+                                        C.POINTER(C.c_int)]),
         "lmra_mode_n_product": (C.c_int, [vp, vp, u64p, C.c_int, C.c_int, vp, C.c_uint64, vp]),
         "lmra_gram_power_apply": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp, C.c_uint64,
                                             C.c_int, C.c_int, vp]),
@@ -116,7 +120,9 @@ EXPORTED = [
     "lmra_result_factor_dims", "lmra_result_copy_factor", "lmra_result_core_device",
     "lmra_result_factor_device", "lmra_result_omega_dims", "lmra_result_copy_omega",
     "lmra_result_num_samples", "lmra_result_copy_samples", "lmra_result_num_norms",
-    "lmra_result_copy_norms", "lmra_result_timings", "lmra_result_free", "lmra_mode_n_product",
+    "lmra_result_copy_norms", "lmra_result_timings", "lmra_result_free",
+    "lmra_context_set_profiling", "lmra_result_num_phases", "lmra_result_phase",
+    "lmra_mode_n_product",
     "lmra_gram_power_apply", "lmra_leading_left_singular_vectors", "lmra_column_sqnorms",
     "lmra_gaussian_matrix", "lmra_probabilities", "lmra_randsample", "lmra_amm_sample_counts",
     "lmra_gen_tucker_noise", "lmra_gen_hilbert", "lmra_gen_video", "lmra_device_alloc",

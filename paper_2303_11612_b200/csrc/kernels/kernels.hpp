@@ -61,3 +61,7 @@ cudaError_t launch_sumsq(const double* a, long long n, double* partials, int npa
                          cudaStream_t st);
 
 }  // namespace lmra_dev
+
+namespace lmra_dev {
+int last_jacobi_sweeps();  // diagnostics: sweeps of the most recent converged Jacobi
+}

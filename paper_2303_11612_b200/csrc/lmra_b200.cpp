@@ -81,6 +81,17 @@ struct lmra_context {
   int nranks = 1, rank = 0;
   std::mutex mu;
   long long launches = 0;
+  bool profile = false;  // per-launch CUDA events (lmra_context_set_profiling)
+  std::vector<cudaEvent_t> events;
+  size_t next_event = 0;
+  cudaEvent_t event() {  // pooled timing events, recycled every run
+    if (next_event == events.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) throw std::runtime_error("cudaEventCreate failed");
+      events.push_back(e);
+    }
+    return events[next_event++];
+  }
 };
 
 namespace {
@@ -168,6 +179,12 @@ struct lmra_result {
   std::vector<std::vector<double>> scales;
   std::vector<std::vector<double>> norms;
   double t_total = 0, t_rng = 0, t_sampling = 0, t_device = 0, launches = 0;
+  struct Phase {
+    std::string name;
+    double ms;
+    int count;
+  };
+  std::vector<Phase> phases;  // device time per launch category (profiling contexts only)
   ~lmra_result() {
     int prev = -1;
     cudaGetDevice(&prev);
@@ -182,22 +199,40 @@ struct lmra_result {
 namespace {
 
 // ------------------------------------------------------------------ the engine
+// One launch (or launch group) bracketed by CUDA events on the launching stream.
+struct PhaseRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
 class Engine {
  public:
-  Engine(lmra_context* ctx) : ctx_(ctx), st_(ctx->stream) {}
+  Engine(lmra_context* ctx, std::vector<PhaseRec>* prof = nullptr)
+      : ctx_(ctx), st_(ctx->stream), prof_(prof) {}
 
-  void launched(cudaError_t e, const char* what) {
-    ck(e, what);
+  template <class F>
+  void launch(const std::string& phase, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (prof_) {
+      a = ctx_->event();
+      ck(cudaEventRecord(a, st_), "event");
+    }
+    ck(f(), phase.c_str());
     ++ctx_->launches;
+    if (prof_) {
+      b = ctx_->event();
+      ck(cudaEventRecord(b, st_), "event");
+      prof_->push_back({phase, a, b});
+    }
   }
 
   // Y = X x_mode Q^T, Q is I x m column-major (already "bt" format)
   DevBuf ttm(const double* x, const std::vector<size_t>& dims, size_t mode, const double* q,
-             size_t m) {
+             size_t m, const std::string& phase = "ttm") {
     std::vector<size_t> od = dims;
     od[mode] = m;
     DevBuf y(prod(od), st_);
-    launched(lmra_dev::launch_ttm(x, view_of(dims, mode), q, (int)m, y.get(), st_), "ttm");
+    launch(phase, [&] { return lmra_dev::launch_ttm(x, view_of(dims, mode), q, (int)m, y.get(), st_); });
     return y;
   }
 
@@ -209,22 +244,26 @@ class Engine {
       DevBuf h(J * s, st_);
       DevBuf zpart((size_t)plan.nsplit * I * s, st_);
       for (int k = 0; k < q; ++k) {
-        launched(lmra_dev::launch_ttm(a, v, c.get(), (int)s, h.get(), st_), "ttm(half)");
-        launched(lmra_dev::launch_gram(a, v, h.get(), (int)s, zpart.get(), plan, c.get(), st_),
-                 "gram");
+        launch("power_half", [&] { return lmra_dev::launch_ttm(a, v, c.get(), (int)s, h.get(), st_); });
+        launch("power_gram", [&] {
+          return lmra_dev::launch_gram(a, v, h.get(), (int)s, zpart.get(), plan, c.get(), st_);
+        });
       }
     } else {  // linalg.cpp:76-77, Strategy B: gram = A A^T once, then c = gram * c
       DevBuf gram(I * I, st_), gramt(I * I, st_);
       DevBuf zpart((size_t)plan.nsplit * I * I, st_);
-      launched(lmra_dev::launch_gram(a, v, a, (int)I, zpart.get(), plan, gram.get(), st_),
-               "gram(AA^T)");
-      launched(lmra_dev::launch_transpose(gram.get(), (long long)I, (long long)I, gramt.get(), st_),
-               "transpose");
+      launch("power_gram", [&] {
+        return lmra_dev::launch_gram(a, v, a, (int)I, zpart.get(), plan, gram.get(), st_);
+      });
+      launch("transpose", [&] {
+        return lmra_dev::launch_transpose(gram.get(), (long long)I, (long long)I, gramt.get(), st_);
+      });
       ModeView cv{1, (long long)I, (long long)s};
       for (int k = 0; k < q; ++k) {
         DevBuf nc(I * s, st_);
-        launched(lmra_dev::launch_ttm(c.get(), cv, gramt.get(), (int)I, nc.get(), st_),
-                 "ttm(gram*c)");
+        launch("power_half", [&] {
+          return lmra_dev::launch_ttm(c.get(), cv, gramt.get(), (int)I, nc.get(), st_);
+        });
         c = std::move(nc);
       }
     }
@@ -233,9 +272,9 @@ class Engine {
   DevBuf orth(const double* c, size_t I, size_t s, size_t mu, int* status) {
     DevBuf u(I * mu, st_);
     DevBuf work(lmra_dev::orth_workspace_doubles((long long)I, (int)s), st_);
-    launched(lmra_dev::launch_orth(c, (long long)I, (int)s, (int)mu, u.get(), work.get(), status,
-                                   st_),
-             "orth");
+    launch("orth", [&] {
+      return lmra_dev::launch_orth(c, (long long)I, (int)s, (int)mu, u.get(), work.get(), status, st_);
+    });
     return u;
   }
 
@@ -247,6 +286,7 @@ class Engine {
 
   lmra_context* ctx_;
   cudaStream_t st_;
+  std::vector<PhaseRec>* prof_;
 };
 
 struct RunInputs {
@@ -265,7 +305,9 @@ struct ModeFactor {
 void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) {
   using namespace lmra_host;
   const double t0 = now_ms();
-  Engine eng(ctx);
+  std::vector<PhaseRec> prof;
+  ctx->next_event = 0;
+  Engine eng(ctx, ctx->profile ? &prof : nullptr);
   cudaStream_t st = ctx->stream;
   const auto& cfg = in.cfg;
   const size_t N = in.dims.size();
@@ -342,7 +384,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
           p = uniform_distribution(J);
         } else {
           DevBuf w(J, st);
-          eng.launched(lmra_dev::launch_column_sqnorms(x, v, w.get(), st), "sqnorms");
+          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(x, v, w.get(), st); });
           std::vector<double> wh(J);
           ck(cudaMemcpyAsync(wh.data(), w.get(), J * sizeof(double), cudaMemcpyDeviceToHost, st),
              "D2H norms");
@@ -362,9 +404,10 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
                          st),
          "H2D scales");
       DevBuf cp(I * T, st);
-      eng.launched(lmra_dev::launch_gather(x, v, reinterpret_cast<const long long*>(didx.get()),
-                                           dsc.get(), (long long)T, cp.get(), st),
-                   "gather");
+      eng.launch("gather", [&] {
+        return lmra_dev::launch_gather(x, v, reinterpret_cast<const long long*>(didx.get()),
+                                       dsc.get(), (long long)T, cp.get(), st);
+      });
       const ModeView cv{1, (long long)I, (long long)T};
       eng.gram_power(cp.get(), cv, c, s, cfg.power, cfg.strategy);
       // keep the host copies alive until the async copies have consumed them
@@ -393,8 +436,10 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     std::vector<size_t> cur = in.dims;
     DevBuf t;
     const double* src = in.x;
+    int step = 0;
     for (size_t n : idx) {
-      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n]);
+      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n],
+                         "core_ttm" + std::to_string(step++));
       cur[n] = res->f_cols[n];
       t = std::move(y);
       src = t.get();
@@ -413,7 +458,8 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
         if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
       }
       factors[n] = mode_factor(src, cur, n, t_n);
-      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n]);
+      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n],
+                         "shrink_ttm_m" + std::to_string(n));
       cur[n] = res->f_cols[n];
       work = std::move(y);
       src = work.get();
@@ -436,6 +482,18 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
   res->t_device = dev_ms;
   res->launches = (double)(ctx->launches - launches0);
+  for (const PhaseRec& p : prof) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, p.a, p.b), "event time");
+    auto it = std::find_if(res->phases.begin(), res->phases.end(),
+                           [&](const lmra_result::Phase& q) { return q.name == p.name; });
+    if (it == res->phases.end()) {
+      res->phases.push_back({p.name, 0.0, 0});
+      it = res->phases.end() - 1;
+    }
+    it->ms += ms;
+    it->count += 1;
+  }
   res->t_total = now_ms() - t0;
 }
 
@@ -647,6 +705,25 @@ int lmra_result_timings(const lmra_result* r, double* out5) {
 }
 void lmra_result_free(lmra_result* r) { delete r; }
 
+int lmra_result_num_phases(const lmra_result* r) { return (int)r->phases.size(); }
+int lmra_result_phase(const lmra_result* r, int i, char* name, size_t name_len, double* ms,
+                      int* launches) {
+  return guard([&] {
+    if (i < 0 || i >= (int)r->phases.size()) throw std::out_of_range("phase index");
+    const auto& p = r->phases[i];
+    if (name && name_len) {
+      std::strncpy(name, p.name.c_str(), name_len - 1);
+      name[name_len - 1] = 0;
+    }
+    *ms = p.ms;
+    *launches = p.count;
+  });
+}
+
+int lmra_context_set_profiling(lmra_context* ctx, int on) {
+  return guard([&] { ctx->profile = on != 0; });
+}
+
 // ------------------------------------------------------------------ primitives
 int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
                         int mode, const double* b, uint64_t b_rows, double* y) {
@@ -658,11 +735,12 @@ int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims
     const size_t I = d[mode];
     Engine eng(ctx);
     DevBuf bt(I * b_rows, ctx->stream);
-    eng.launched(lmra_dev::launch_transpose(b, (long long)b_rows, (long long)I, bt.get(), ctx->stream),
-                 "transpose");
-    eng.launched(lmra_dev::launch_ttm(x, view_of(d, (size_t)mode), bt.get(), (int)b_rows, y,
-                                      ctx->stream),
-                 "ttm");
+    eng.launch("transpose", [&] {
+      return lmra_dev::launch_transpose(b, (long long)b_rows, (long long)I, bt.get(), ctx->stream);
+    });
+    eng.launch("ttm", [&] {
+      return lmra_dev::launch_ttm(x, view_of(d, (size_t)mode), bt.get(), (int)b_rows, y, ctx->stream);
+    });
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }
@@ -712,8 +790,9 @@ int lmra_column_sqnorms(lmra_context* ctx, const double* x, const uint64_t* dims
     DeviceGuard dg(ctx->device);
     std::vector<size_t> d(dims, dims + order);
     Engine eng(ctx);
-    eng.launched(lmra_dev::launch_column_sqnorms(x, view_of(d, (size_t)mode), w, ctx->stream),
-                 "sqnorms");
+    eng.launch("norms", [&] {
+      return lmra_dev::launch_column_sqnorms(x, view_of(d, (size_t)mode), w, ctx->stream);
+    });
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }
@@ -875,3 +954,5 @@ int lmra_memcpy(lmra_context* ctx, void* dst, const void* src, size_t bytes, int
 }
 
 }  // extern "C"
+
+extern "C" int lmra_debug_jacobi_sweeps(void) { return lmra_dev::last_jacobi_sweeps(); }

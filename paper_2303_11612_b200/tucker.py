@@ -174,6 +174,10 @@ class Context:
     def synchronize(self):
         check(lib.lmra_context_synchronize(self.handle))
 
+    def set_profiling(self, on: bool):
+        """Per-launch CUDA events on the context stream -> _Result.phases()."""
+        check(lib.lmra_context_set_profiling(self.handle, int(bool(on))))
+
     def set_comm(self, unique_id: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib.lmra_context_set_comm(self.handle, buf, int(nranks), int(rank)))
@@ -306,6 +310,16 @@ class _Result:
                     norms.append(None)
         return TuckerDecomposition(core.reshape(cd, order="F"), factors, omega, samples, norms,
                                    self.timings())
+
+    def phases(self) -> dict:
+        """{phase: (device ms, launches)} for profiling contexts."""
+        out = {}
+        buf = C.create_string_buffer(64)
+        for i in range(lib.lmra_result_num_phases(self.handle)):
+            ms, cnt = C.c_double(), C.c_int()
+            check(lib.lmra_result_phase(self.handle, i, buf, 64, C.byref(ms), C.byref(cnt)))
+            out[buf.value.decode()] = (ms.value, cnt.value)
+        return out
 
     def timings(self) -> dict:
         t = np.zeros(5)
