@@ -261,7 +261,7 @@ def bench_gpu(args, rank, world, local_rank):
 
     phases = {}
     launches = 0
-    host_split = {"host_rng_ms": 0.0, "host_sampling_ms": 0.0}
+    host_split = {"host_rng_ms": 0.0, "host_sampling_ms": 0.0, "total_ms": 0.0, "device_ms": 0.0}
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:

@@ -132,6 +132,8 @@ int lmra_result_timings(const lmra_result* r, double* out5);
  * recorded when lmra_context_set_profiling(ctx, 1).  Phases: norms, gather, power_half,
  * power_gram, orth, core_ttm<k> (k-th contraction of core_from_factors), shrink_ttm_m<n>. */
 int lmra_context_set_profiling(lmra_context* ctx, int on);
+/* keep host copies of the drawn samples / column norms in the result (default on) */
+int lmra_context_set_trace(lmra_context* ctx, int on);
 int lmra_result_num_phases(const lmra_result* r);
 int lmra_result_phase(const lmra_result* r, int i, char* name, size_t name_len, double* ms,
                       int* launches);
@@ -147,6 +149,12 @@ int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uin
 /* u = top-mu left singular vectors of c with the reference's sign rule (linalg.cpp:82-87) */
 int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint64_t rows,
                                        uint64_t cols, uint64_t mu, double* u);
+/* the sampling chain on the device, bit-exact with the reference's host loops:
+ * p = gram_sampling_probabilities from squared norms w (tucker.cpp:110-130), then
+ * randsample(L, p, {seed, stream}) (sketching.cpp:96-131).  w, idx, scales, p: device. */
+int lmra_sample_columns_device(lmra_context* ctx, const double* w, uint64_t n, int regime,
+                               double beta, uint64_t L, uint64_t seed, uint64_t stream,
+                               int64_t* idx, double* scales, double* p);
 /* canonical column squared norms of the mode-n unfolding (tucker.cpp:117-119) */
 int lmra_column_sqnorms(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
                         int mode, double* w);

@@ -80,6 +80,9 @@ def _load():
         "lmra_result_timings": (C.c_int, [vp, dblp]),
         "lmra_result_free": (None, [vp]),
         "lmra_context_set_profiling": (C.c_int, [vp, C.c_int]),
+        "lmra_context_set_trace": (C.c_int, [vp, C.c_int]),
+        "lmra_sample_columns_device": (C.c_int, [vp, vp, C.c_uint64, C.c_int, C.c_double, C.c_uint64,
+                                                 C.c_uint64, C.c_uint64, vp, vp, vp]),
         "lmra_result_num_phases": (C.c_int, [vp]),
         "lmra_result_phase": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, dblp,
                                         C.POINTER(C.c_int)]),
@@ -122,6 +125,7 @@ EXPORTED = [
     "lmra_result_num_samples", "lmra_result_copy_samples", "lmra_result_num_norms",
     "lmra_result_copy_norms", "lmra_result_timings", "lmra_result_free",
     "lmra_context_set_profiling", "lmra_result_num_phases", "lmra_result_phase",
+    "lmra_context_set_trace", "lmra_sample_columns_device",
     "lmra_mode_n_product",
     "lmra_gram_power_apply", "lmra_leading_left_singular_vectors", "lmra_column_sqnorms",
     "lmra_gaussian_matrix", "lmra_probabilities", "lmra_randsample", "lmra_amm_sample_counts",

@@ -35,6 +35,17 @@ cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, con
 // fma within a chunk, chunk partials added in order) -- bit-identical to the oracle.
 cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaStream_t st);
 
+// The reference's sampling chain on the device, bit-exact (sampler.cu):
+// probabilities from squared column norms w (regime 0 optimal, 1 nearly-optimal, 2 uniform)
+// then L multinomial draws from PCG32 stream (seed, stream): idx (int64), scales, p (n).
+// status bits: 1 bad weight, 2 zero normaliser, 4 sum != 1, 8 zero total, 16 fallback,
+// 32 bad beta.
+size_t sampler_workspace_doubles(long long n);
+void sampler_walk_stats(unsigned long long* out2, bool reset);  // diagnostics
+cudaError_t launch_sampler(const double* w, long long n, int regime, double beta, long long L,
+                           uint64_t seed, uint64_t stream, long long* idx, double* scales,
+                           double* p_out, double* work, int* status, cudaStream_t st);
+
 // Top-mu left singular vectors of C (I x s, column-major) with the reference's sign
 // convention (linalg.cpp:13-43,82-87), written to U (I x mu).  Workspace: orth_workspace().
 size_t orth_workspace_doubles(long long I, int s);

@@ -82,8 +82,31 @@ struct lmra_context {
   std::mutex mu;
   long long launches = 0;
   bool profile = false;  // per-launch CUDA events (lmra_context_set_profiling)
+  bool keep_trace = true;  // copy drawn samples / norms back to the host (lmra_context_set_trace)
   std::vector<cudaEvent_t> events;
   size_t next_event = 0;
+  std::vector<cudaStream_t> aux;   // per-mode streams (T-HOSVD modes run concurrently)
+  double* pinned = nullptr;        // pinned staging for Omega (async H2D, no pageable sync)
+  size_t pinned_doubles = 0;
+  cudaStream_t aux_stream(size_t i) {
+    while (aux.size() <= i) {
+      cudaStream_t s;
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+        throw std::runtime_error("cudaStreamCreate failed");
+      aux.push_back(s);
+    }
+    return aux[i];
+  }
+  double* pinned_buffer(size_t n) {
+    if (n > pinned_doubles) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      if (cudaMallocHost(reinterpret_cast<void**>(&pinned), n * sizeof(double)) != cudaSuccess)
+        throw std::runtime_error("cudaMallocHost failed");
+      pinned_doubles = n;
+    }
+    return pinned;
+  }
   cudaEvent_t event() {  // pooled timing events, recycled every run
     if (next_event == events.size()) {
       cudaEvent_t e;
@@ -179,6 +202,7 @@ struct lmra_result {
   std::vector<std::vector<double>> scales;
   std::vector<std::vector<double>> norms;
   double t_total = 0, t_rng = 0, t_sampling = 0, t_device = 0, launches = 0;
+  int sampler_fallbacks = 0;  // uncertified Neumaier roundings resolved sequentially
   struct Phase {
     std::string name;
     double ms;
@@ -209,6 +233,8 @@ class Engine {
  public:
   Engine(lmra_context* ctx, std::vector<PhaseRec>* prof = nullptr)
       : ctx_(ctx), st_(ctx->stream), prof_(prof) {}
+  Engine(lmra_context* ctx, cudaStream_t st, std::vector<PhaseRec>* prof)
+      : ctx_(ctx), st_(st), prof_(prof) {}
 
   template <class F>
   void launch(const std::string& phase, F&& f) {
@@ -340,80 +366,105 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   ck(cudaEventRecord(ev0, st), "event");
   const long long launches0 = ctx->launches;
 
-  // Omega for every mode up front (data independent; the GPU is idle anyway on the
-  // first mode only for the duration of the copy). gaussian_stream = {seed, n+1}.
-  const double tr0 = now_ms();
+  // Omega for every mode (gaussian_stream = {seed, n+1}, sketching.cpp:164-173) is data
+  // independent: a host thread draws it into pinned memory while the GPU already runs
+  // the column norms / sampling chains.
+  std::vector<size_t> om_off(N + 1, 0);
   for (size_t n = 0; n < N; ++n) {
-    const size_t I = in.dims[n], s = r.sketch[n];
-    res->om_rows[n] = I;
-    res->om_cols[n] = s;
-    res->omega[n].resize(I * s);
-    if (in.ov && in.ov->omega && in.ov->omega[n]) {
-      std::memcpy(res->omega[n].data(), in.ov->omega[n], sizeof(double) * I * s);
-    } else {
-      fill_normals(cfg.seed, n + 1, res->omega[n].data(), I * s, host_threads());
-    }
+    res->om_rows[n] = in.dims[n];
+    res->om_cols[n] = r.sketch[n];
+    om_off[n + 1] = om_off[n] + in.dims[n] * r.sketch[n];
   }
-  res->t_rng = now_ms() - tr0;
+  double* om_pin = ctx->pinned_buffer(om_off[N]);
+  std::thread omega_thread([&] {
+    const double tr0 = now_ms();
+    for (size_t n = 0; n < N; ++n) {
+      const size_t cnt = om_off[n + 1] - om_off[n];
+      if (in.ov && in.ov->omega && in.ov->omega[n])
+        std::memcpy(om_pin + om_off[n], in.ov->omega[n], sizeof(double) * cnt);
+      else
+        fill_normals(cfg.seed, n + 1, om_pin + om_off[n], cnt, host_threads());
+    }
+    res->t_rng = now_ms() - tr0;
+  });
+  struct JoinGuard {
+    std::thread& t;
+    ~JoinGuard() {
+      if (t.joinable()) t.join();
+    }
+  } join_guard{omega_thread};
 
-  std::vector<DevBuf> status_buf;
-  DevBuf status(N, st);  // int status per mode (stored in double slots)
+  // per-mode device status words: [0, N) orth convergence, [N, 2N) sampler flags
+  DevBuf status(N, st);
   ck(cudaMemsetAsync(status.get(), 0, N * sizeof(double), st), "memset");
   int* status_i = reinterpret_cast<int*>(status.get());
+  // device-drawn samples / norms kept until the end of the run for the trace
+  std::vector<DevBuf> d_idx(N), d_sc(N), d_w(N);
+  std::vector<size_t> n_draws(N, 0);
 
-  auto mode_factor = [&](const double* x, const std::vector<size_t>& dims, size_t n,
-                         size_t t_n) -> DevBuf {
+  // phase 1 of a mode: the sampled columns (AMM only) -- norms + exact sampling chain
+  auto sample_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims, size_t n,
+                         size_t t_n) {
+    if (!amm) return;
+    cudaStream_t s_ = e.st_;
     const ModeView v = view_of(dims, n);
-    const size_t I = dims[n], s = r.sketch[n], J = (size_t)(v.inner * v.outer);
-    DevBuf c = eng.upload(res->omega[n].data(), I * s);
-    if (!amm) {
-      eng.gram_power(x, v, c, s, cfg.power, cfg.strategy);
-    } else {
-      // sampling (tucker.cpp:110-130 + sketching.cpp:96-131); stream {seed, N+n+1}
-      const double ts0 = now_ms();
-      Samples smp;
-      if (in.ov && in.ov->sample_idx && in.ov->sample_idx[n]) {
-        const size_t T = in.ov->n_samples[n];
-        smp.idx.assign(in.ov->sample_idx[n], in.ov->sample_idx[n] + T);
-        smp.scales.assign(in.ov->sample_scale[n], in.ov->sample_scale[n] + T);
-        for (int64_t j : smp.idx)
-          if (j < 0 || (size_t)j >= J) throw std::invalid_argument("sample index out of range");
-      } else {
-        std::vector<double> p;
-        if (cfg.regime == kUniform) {
-          p = uniform_distribution(J);
-        } else {
-          DevBuf w(J, st);
-          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(x, v, w.get(), st); });
-          std::vector<double> wh(J);
-          ck(cudaMemcpyAsync(wh.data(), w.get(), J * sizeof(double), cudaMemcpyDeviceToHost, st),
-             "D2H norms");
-          ck(cudaStreamSynchronize(st), "sync");
-          res->norms[n] = wh;
-          p = probabilities_from_norms(std::move(wh), cfg.regime, cfg.beta);
-        }
-        smp = randsample(t_n, p, cfg.seed, N + n + 1);
-      }
-      res->t_sampling += now_ms() - ts0;
-      const size_t T = smp.idx.size();
-      DevBuf didx((T + 1), st), dsc(T, st);
-      ck(cudaMemcpyAsync(didx.get(), smp.idx.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice,
-                         st),
+    const size_t J = (size_t)(v.inner * v.outer);
+    const double ts0 = now_ms();
+    size_t T;
+    if (in.ov && in.ov->sample_idx && in.ov->sample_idx[n]) {  // parity overrides
+      T = in.ov->n_samples[n];
+      const int64_t* oi = in.ov->sample_idx[n];
+      for (size_t j = 0; j < T; ++j)
+        if (oi[j] < 0 || (size_t)oi[j] >= J) throw std::invalid_argument("sample index out of range");
+      d_idx[n] = DevBuf(T + 1, s_);
+      d_sc[n] = DevBuf(T, s_);
+      ck(cudaMemcpyAsync(d_idx[n].get(), oi, T * sizeof(int64_t), cudaMemcpyHostToDevice, s_),
          "H2D idx");
-      ck(cudaMemcpyAsync(dsc.get(), smp.scales.data(), T * sizeof(double), cudaMemcpyHostToDevice,
-                         st),
+      ck(cudaMemcpyAsync(d_sc[n].get(), in.ov->sample_scale[n], T * sizeof(double),
+                         cudaMemcpyHostToDevice, s_),
          "H2D scales");
-      DevBuf cp(I * T, st);
-      eng.launch("gather", [&] {
-        return lmra_dev::launch_gather(x, v, reinterpret_cast<const long long*>(didx.get()),
-                                       dsc.get(), (long long)T, cp.get(), st);
+      ck(cudaStreamSynchronize(s_), "sync");  // caller's host arrays are only borrowed
+    } else {
+      T = t_n;
+      if (T < 1) throw std::invalid_argument("randsample: L must be positive");
+      d_idx[n] = DevBuf(T + 1, s_);
+      d_sc[n] = DevBuf(T, s_);
+      DevBuf p(J, s_), work(lmra_dev::sampler_workspace_doubles((long long)J), s_);
+      d_w[n] = DevBuf(J, s_);
+      if (cfg.regime != kUniform)
+        e.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(x, v, d_w[n].get(), s_); });
+      e.launch("sampler", [&] {
+        return lmra_dev::launch_sampler(
+            d_w[n].get(), (long long)J, cfg.regime, cfg.beta, (long long)T, cfg.seed, N + n + 1,
+            reinterpret_cast<long long*>(d_idx[n].get()), d_sc[n].get(), p.get(), work.get(),
+            status_i + N + n, s_);
+      });
+    }
+    n_draws[n] = T;
+    res->t_sampling += now_ms() - ts0;
+  };
+
+  // phase 2 of a mode: Omega -> power scheme (on the unfolding or the sampled columns)
+  // -> orthonormalised factor.  Omega must be drawn (omega_thread joined) before this.
+  auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
+                         size_t n) -> DevBuf {
+    cudaStream_t s_ = e.st_;
+    const ModeView v = view_of(dims, n);
+    const size_t I = dims[n], s = r.sketch[n];
+    DevBuf c(I * s, s_);
+    ck(cudaMemcpyAsync(c.get(), om_pin + om_off[n], I * s * sizeof(double), cudaMemcpyHostToDevice, s_),
+       "H2D omega");
+    if (!amm) {
+      e.gram_power(x, v, c, s, cfg.power, cfg.strategy);
+    } else {
+      const size_t T = n_draws[n];
+      DevBuf cp(I * T, s_);
+      e.launch("gather", [&] {
+        return lmra_dev::launch_gather(x, v, reinterpret_cast<const long long*>(d_idx[n].get()),
+                                       d_sc[n].get(), (long long)T, cp.get(), s_);
       });
       const ModeView cv{1, (long long)I, (long long)T};
-      eng.gram_power(cp.get(), cv, c, s, cfg.power, cfg.strategy);
-      // keep the host copies alive until the async copies have consumed them
-      ck(cudaStreamSynchronize(st), "sync");
-      res->idx[n] = std::move(smp.idx);
-      res->scales[n] = std::move(smp.scales);
+      e.gram_power(cp.get(), cv, c, s, cfg.power, cfg.strategy);
     }
     const size_t mu = std::min(r.mu[n], std::min(I, s));  // top_left_vectors_clamped
     if (mu < r.mu[n])
@@ -421,13 +472,35 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
               r.mu[n], mu);
     res->f_rows[n] = I;
     res->f_cols[n] = mu;
-    return eng.orth(c.get(), I, s, mu, status_i + n);
+    return e.orth(c.get(), I, s, mu, status_i + n);
   };
 
   std::vector<DevBuf> factors(N);
   if (!sequential) {
-    for (size_t n = 0; n < N; ++n)
-      factors[n] = mode_factor(in.x, in.dims, n, amm ? t_flat[n] : 0);
+    // modes are independent (run_modes, tucker.cpp:134-160): one stream per mode, so the
+    // latency-bound sampling / power / orthonormalisation kernels of different modes
+    // overlap; the core contraction joins them on the main stream
+    cudaEvent_t fork;
+    ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(fork, st), "event");
+    std::vector<Engine> engs;
+    engs.reserve(N);
+    for (size_t n = 0; n < N; ++n) {
+      cudaStream_t sn = ctx->aux_stream(n);
+      ck(cudaStreamWaitEvent(sn, fork, 0), "wait");
+      engs.emplace_back(ctx, sn, ctx->profile ? &prof : nullptr);
+    }
+    for (size_t n = 0; n < N; ++n) sample_mode(engs[n], in.x, in.dims, n, amm ? t_flat[n] : 0);
+    omega_thread.join();
+    for (size_t n = 0; n < N; ++n) factors[n] = factor_mode(engs[n], in.x, in.dims, n);
+    for (size_t n = 0; n < N; ++n) {
+      cudaEvent_t done;
+      ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(done, ctx->aux_stream(n)), "event");
+      ck(cudaStreamWaitEvent(st, done, 0), "wait");
+      cudaEventDestroy(done);
+    }
+    cudaEventDestroy(fork);
     // core_from_factors (tucker.cpp:81-92): ascending factor width, stable
     std::vector<size_t> idx(N);
     std::iota(idx.begin(), idx.end(), size_t{0});
@@ -457,7 +530,9 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
         t_n = cfg.t_samples.empty() ? samples_from_alpha(cfg.alpha, cols) : cfg.t_samples[n];
         if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
       }
-      factors[n] = mode_factor(src, cur, n, t_n);
+      sample_mode(eng, src, cur, n, t_n);
+      if (omega_thread.joinable()) omega_thread.join();
+      factors[n] = factor_mode(eng, src, cur, n);
       DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n],
                          "shrink_ttm_m" + std::to_string(n));
       cur[n] = res->f_cols[n];
@@ -471,13 +546,45 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
 
   ck(cudaEventRecord(ev1, st), "event");
   std::vector<int> stat(2 * N);
-  ck(cudaMemcpyAsync(stat.data(), status.get(), N * sizeof(int), cudaMemcpyDeviceToHost, st),
+  ck(cudaMemcpyAsync(stat.data(), status.get(), 2 * N * sizeof(int), cudaMemcpyDeviceToHost, st),
      "D2H status");
+  // trace of the draws (host copies) -- off for throughput runs (lmra_context_set_trace)
+  if (ctx->keep_trace) {
+    for (size_t n = 0; n < N; ++n) res->omega[n].assign(om_pin + om_off[n], om_pin + om_off[n + 1]);
+    for (size_t n = 0; n < N; ++n) {
+      if (n_draws[n] && d_idx[n].get()) {
+        res->idx[n].resize(n_draws[n]);
+        res->scales[n].resize(n_draws[n]);
+        ck(cudaMemcpyAsync(res->idx[n].data(), d_idx[n].get(), n_draws[n] * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, st),
+           "D2H idx");
+        ck(cudaMemcpyAsync(res->scales[n].data(), d_sc[n].get(), n_draws[n] * sizeof(double),
+                           cudaMemcpyDeviceToHost, st),
+           "D2H scales");
+      }
+      if (d_w[n].get() && cfg.regime != kUniform) {
+        res->norms[n].resize(d_w[n].size());
+        ck(cudaMemcpyAsync(res->norms[n].data(), d_w[n].get(), d_w[n].size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, st),
+           "D2H norms");
+      }
+    }
+  }
   ck(cudaStreamSynchronize(st), "sync");
   float dev_ms = 0;
   ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event time");
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
+  // the reference's exception surface, in its order of checks (sketching.cpp / tucker.cpp)
+  for (size_t n = 0; n < N; ++n) {
+    const int f = stat[N + n];
+    if (f & 1) throw std::invalid_argument("probability weights must be nonnegative");
+    if (f & 32) throw std::invalid_argument("nearly-optimal mixture weight must lie in (0, 1]");
+    if (f & 2) throw std::invalid_argument("cannot normalize an all-zero distribution");
+    if (f & 4) throw std::invalid_argument("probability weights must sum to one");
+    if (f & 8) throw std::invalid_argument("randsample: all-zero distribution");
+    if (f & 16) ++res->sampler_fallbacks;
+  }
   for (size_t n = 0; n < N; ++n)
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
   res->t_device = dev_ms;
@@ -724,6 +831,10 @@ int lmra_context_set_profiling(lmra_context* ctx, int on) {
   return guard([&] { ctx->profile = on != 0; });
 }
 
+int lmra_context_set_trace(lmra_context* ctx, int on) {
+  return guard([&] { ctx->keep_trace = on != 0; });
+}
+
 // ------------------------------------------------------------------ primitives
 int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
                         int mode, const double* b, uint64_t b_rows, double* y) {
@@ -794,6 +905,46 @@ int lmra_column_sqnorms(lmra_context* ctx, const double* x, const uint64_t* dims
       return lmra_dev::launch_column_sqnorms(x, view_of(d, (size_t)mode), w, ctx->stream);
     });
     ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+// diagnostics: [certified chunks, element-exact chunks] of the exact scans since last reset
+int lmra_debug_sampler_stats(unsigned long long* out2, int reset) {
+  lmra_dev::sampler_walk_stats(out2, reset != 0);
+  return LMRA_OK;
+}
+
+int lmra_sample_columns_device(lmra_context* ctx, const double* w, uint64_t n, int regime,
+                               double beta, uint64_t L, uint64_t seed, uint64_t stream,
+                               int64_t* idx, double* scales, double* p) {
+  return guard([&] {
+    if (n < 1) throw std::invalid_argument("probability distribution must be nonempty");
+    if (L < 1) throw std::invalid_argument("randsample: L must be positive");
+    if (regime < 0 || regime > 2) throw std::invalid_argument("unknown probability regime");
+    DeviceGuard dg(ctx->device);
+    Engine eng(ctx);
+    DevBuf work(lmra_dev::sampler_workspace_doubles((long long)n), ctx->stream);
+    DevBuf status(1, ctx->stream);
+    ck(cudaMemsetAsync(status.get(), 0, sizeof(double), ctx->stream), "memset");
+    const double* wv = w;
+    DevBuf dummy;
+    if (regime == 2) {  // uniform never reads w
+      dummy = DevBuf(n, ctx->stream);
+      wv = dummy.get();
+    }
+    eng.launch("sampler", [&] {
+      return lmra_dev::launch_sampler(wv, (long long)n, regime, beta, (long long)L, seed, stream,
+                                      reinterpret_cast<long long*>(idx), scales, p, work.get(),
+                                      reinterpret_cast<int*>(status.get()), ctx->stream);
+    });
+    int f = 0;
+    ck(cudaMemcpyAsync(&f, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    if (f & 1) throw std::invalid_argument("probability weights must be nonnegative");
+    if (f & 32) throw std::invalid_argument("nearly-optimal mixture weight must lie in (0, 1]");
+    if (f & 2) throw std::invalid_argument("cannot normalize an all-zero distribution");
+    if (f & 4) throw std::invalid_argument("probability weights must sum to one");
+    if (f & 8) throw std::invalid_argument("randsample: all-zero distribution");
   });
 }
 

@@ -81,6 +81,23 @@ def column_sqnorms(x, dims: Sequence[int], mode: int, ctx: Context = None):
     return w
 
 
+def sample_columns(w, regime: str, beta: float, L: int, seed: int, stream: int, ctx: Context = None):
+    """Device sampling chain (tucker.cpp:110-130 + sketching.cpp:96-131) on norms w.
+    Returns (idx int64, scales, p) as CUDA tensors."""
+    ctx = ctx or default_context()
+    torch = _torch()
+    torch.cuda.current_stream().synchronize()
+    n = int(w.numel())
+    idx = torch.empty(L, dtype=torch.int64, device=w.device)
+    sc = empty(L, ctx.device)
+    p = empty(n, ctx.device)
+    regime_code = {"optimal": 0, "nearly_optimal": 1, "uniform": 2}[regime]
+    check(lib.lmra_sample_columns_device(ctx.handle, _ptr(w), n, regime_code, C.c_double(beta), L,
+                                         C.c_uint64(seed), C.c_uint64(stream), _ptr(idx), _ptr(sc),
+                                         _ptr(p)))
+    return idx, sc, p
+
+
 # ---------------------------------------------------------------- BASELINE generators
 def gen_tucker_noise(dims, core_dims, gamma: float, seed: int, ctx: Context = None):
     ctx = ctx or default_context()

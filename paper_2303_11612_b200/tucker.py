@@ -174,6 +174,10 @@ class Context:
     def synchronize(self):
         check(lib.lmra_context_synchronize(self.handle))
 
+    def set_trace(self, on: bool):
+        """Keep host copies of drawn samples / column norms in results (default on)."""
+        check(lib.lmra_context_set_trace(self.handle, int(bool(on))))
+
     def set_profiling(self, on: bool):
         """Per-launch CUDA events on the context stream -> _Result.phases()."""
         check(lib.lmra_context_set_profiling(self.handle, int(bool(on))))
@@ -346,14 +350,16 @@ def _as_tensor(a) -> DenseTensor:
 
 
 def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omega=None,
-            samples=None) -> _Result:
-    """run_algorithm returning the device-resident result handle (no copy-out)."""
+            samples=None, trace: bool = False) -> _Result:
+    """run_algorithm returning the device-resident result handle (no copy-out).
+    trace=True also keeps host copies of the drawn samples and column norms."""
     if alg not in _ALG_CODE:
         if alg in ALGORITHM_IDS:
             raise LmraInvalidArgument(f"{alg} is outside the B200 hot path (alg1/alg2/alg4/alg5)")
         raise LmraInvalidArgument("unknown algorithm")
     t = _as_tensor(a)
     ctx = ctx or default_context()
+    ctx.set_trace(trace)
     dims = np.asarray(t.dims, dtype=np.uint64)
     c, keep = cfg._to_c()
     ov, keep2 = _overrides(len(t.dims), omega, samples)
@@ -371,9 +377,10 @@ def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omeg
 
 
 def run_algorithm(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omega=None,
-                  samples=None) -> TuckerDecomposition:
-    """tucker.cpp:456-470.  omega / samples: per-mode parity overrides (None = seeded RNG)."""
-    r = run_raw(alg, a, cfg, ctx=ctx, omega=omega, samples=samples)
+                  samples=None, trace: bool = True) -> TuckerDecomposition:
+    """tucker.cpp:456-470.  omega / samples: per-mode parity overrides (None = seeded RNG).
+    trace: also return the drawn samples / column norms (host copies)."""
+    r = run_raw(alg, a, cfg, ctx=ctx, omega=omega, samples=samples, trace=trace)
     try:
         return r.to_host()
     finally:

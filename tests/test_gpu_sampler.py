@@ -1,0 +1,67 @@
+"""The device sampling chain (sampler.cu) against the oracle's sequential restatement of
+tucker.cpp:110-130 + sketching.cpp:28-53,96-131: probabilities, indices and scales must be
+bit-identical, including inputs built to stress the exact emulation of the reference's
+sequential fp64 sums (ties to even everywhere, zeros, binade-boundary values, wide ranges).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases():
+    rng = np.random.default_rng(11)
+    out = {
+        "gauss_sq_1e5": rng.standard_normal(100_000) ** 2,
+        "gauss_sq_1e6": rng.standard_normal(1_000_000) ** 2,
+        "uniform01_333k": rng.random(333_333),
+        "constant_ones_70k": np.ones(70_000),
+        "constant_third_50k": np.full(50_000, 1.0 / 3.0),
+        "powers_of_two_20k": 2.0 ** rng.integers(-30, 30, 20_000).astype(np.float64),
+        "with_zeros_40k": np.where(rng.random(40_000) < 0.3, 0.0, rng.random(40_000)),
+        "leading_zeros_9000": np.concatenate([np.zeros(5000), rng.random(4000)]),
+        "wide_range_60k": rng.random(60_000) * 10.0 ** rng.integers(-200, 200, 60_000),
+        "tiny_values_30k": rng.random(30_000) * 1e-300,
+        "single": np.array([2.5]),
+        "small_7": np.array([1.0, 2.0, 3.0, 2.0, 1.0, 0.0, 5.0]),
+        "half_ulp_ties_10k": np.tile([1.0, 2.0 ** -53, 2.0 ** -53, 3 * 2.0 ** -53], 2500),
+    }
+    return out
+
+
+CASES = _cases()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("regime", ["optimal", "nearly_optimal", "uniform"])
+def test_sampler_bit_exact(gpu_ctx, orc, name, regime):
+    import torch
+    from paper_2303_11612_b200 import device
+    w = np.ascontiguousarray(CASES[name], dtype=np.float64)
+    L = 4099 if w.size > 10 else 17
+    p_ref = orc.probabilities(w, regime, 0.5)
+    idx_ref, sc_ref = orc.randsample(L, p_ref, 7, 13)
+    wd = torch.from_numpy(w).cuda()
+    idx, sc, p = device.sample_columns(wd, regime, 0.5, L, 7, 13, ctx=gpu_ctx)
+    p = p.cpu().numpy()
+    assert np.array_equal(p, p_ref), f"p differs at {np.flatnonzero(p != p_ref)[:5]}"
+    assert np.array_equal(idx.cpu().numpy(), idx_ref)
+    assert np.array_equal(sc.cpu().numpy(), sc_ref)
+
+
+def test_sampler_error_surface(gpu_ctx, lmra):
+    import torch
+    from paper_2303_11612_b200 import device
+    bad = torch.tensor([1.0, float("nan"), 2.0], dtype=torch.float64, device="cuda")
+    with pytest.raises(lmra.LmraInvalidArgument, match="nonnegative"):
+        device.sample_columns(bad, "optimal", 0.5, 4, 1, 1, ctx=gpu_ctx)
+    neg = torch.tensor([1.0, -1.0, 2.0], dtype=torch.float64, device="cuda")
+    with pytest.raises(lmra.LmraInvalidArgument):
+        device.sample_columns(neg, "nearly_optimal", 0.5, 4, 1, 1, ctx=gpu_ctx)
+    ok = torch.tensor([1.0, 1.0, 2.0], dtype=torch.float64, device="cuda")
+    with pytest.raises(lmra.LmraInvalidArgument, match="mixture"):
+        device.sample_columns(ok, "nearly_optimal", 1.5, 4, 1, 1, ctx=gpu_ctx)
+    # all-zero norms fall back to uniform (tucker.cpp:121), like the reference
+    z = torch.zeros(10, dtype=torch.float64, device="cuda")
+    idx, sc, p = device.sample_columns(z, "optimal", 0.5, 5, 1, 1, ctx=gpu_ctx)
+    assert np.all(p.cpu().numpy() == 0.1)
