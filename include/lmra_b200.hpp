@@ -1,0 +1,225 @@
+// lmra_b200.hpp -- C++ drop-in for the reference's hot-path API (namespace lmra,
+// proj/include/lmra/tucker.hpp:17-121), header-only over the C ABI in lmra_b200.h.
+//
+// Same names, argument meaning and exception surface as the reference:
+//   rand_thosvd_power / rand_sthosvd_power / rand_thosvd_amm / rand_sthosvd_amm,
+//   run_algorithm, amm_sample_counts, AlgoConfig, MultilinearRank, TuckerDecomposition.
+// std::invalid_argument / std::runtime_error are re-thrown from the ABI status codes.
+//
+// Deviation: Eigen3 is not a dependency, so TuckerDecomposition::factors is a
+// std::vector<lmra::Matrix> -- a column-major rows() x cols() matrix with data() and
+// operator()(i, j); with Eigen available, `Eigen::Map<const Eigen::MatrixXd>(m.data(),
+// m.rows(), m.cols())` views it without a copy.  Multi-GPU follows the thread_cap()
+// idiom: LMRA_NUM_GPUS (tucker.cpp:164-172 reads LMRA_NUM_THREADS the same way); one
+// process per GPU passes its slab of the last mode after lmra_context_set_comm.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lmra_b200.h"
+
+namespace lmra {
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == LMRA_OK) return;
+  const char* m = lmra_last_error();
+  if (rc == LMRA_EINVAL) throw std::invalid_argument(m);
+  throw std::runtime_error(m);
+}
+struct Ctx {
+  lmra_context* c = nullptr;
+  explicit Ctx(int device) { check(lmra_context_create(device, nullptr, &c)); }
+  ~Ctx() { lmra_context_destroy(c); }
+};
+inline lmra_context* default_context() {
+  thread_local std::unique_ptr<Ctx> ctx;
+  if (!ctx) ctx = std::make_unique<Ctx>(0);
+  return ctx->c;
+}
+}  // namespace detail
+
+// tensor.hpp:14-44 -- dense tensor, first index fastest
+class DenseTensor {
+ public:
+  DenseTensor() = default;
+  explicit DenseTensor(std::vector<std::size_t> dims) : dims_(std::move(dims)) {
+    std::size_t n = 1;
+    for (std::size_t d : dims_) n *= d;
+    values_.assign(n, 0.0);
+  }
+  DenseTensor(std::vector<std::size_t> dims, std::vector<double> values)
+      : dims_(std::move(dims)), values_(std::move(values)) {
+    std::size_t n = 1;
+    for (std::size_t d : dims_) n *= d;
+    if (n != values_.size()) throw std::invalid_argument("value count does not match tensor shape");
+  }
+  std::size_t order() const { return dims_.size(); }
+  const std::vector<std::size_t>& dims() const { return dims_; }
+  std::size_t dim(std::size_t m) const { return dims_.at(m); }
+  std::size_t size() const { return values_.size(); }
+  const double* data() const { return values_.data(); }
+  double* data() { return values_.data(); }
+  double operator[](std::size_t i) const { return values_[i]; }
+  double& operator[](std::size_t i) { return values_[i]; }
+
+ private:
+  std::vector<std::size_t> dims_;
+  std::vector<double> values_;
+};
+
+// column-major dense matrix (stands in for Eigen::MatrixXd, see header comment)
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(std::size_t r, std::size_t c) : r_(r), c_(c), v_(r * c, 0.0) {}
+  std::size_t rows() const { return r_; }
+  std::size_t cols() const { return c_; }
+  const double* data() const { return v_.data(); }
+  double* data() { return v_.data(); }
+  double operator()(std::size_t i, std::size_t j) const { return v_[i + r_ * j]; }
+  double& operator()(std::size_t i, std::size_t j) { return v_[i + r_ * j]; }
+
+ private:
+  std::size_t r_ = 0, c_ = 0;
+  std::vector<double> v_;
+};
+
+enum class ProbRegime { Optimal, NearlyOptimal, Uniform };  // sketching.hpp:31
+enum class GramStrategy { A, B };                           // linalg.hpp:26
+
+struct MultilinearRank {  // tucker.hpp:17-24
+  std::vector<std::size_t> mu;
+  MultilinearRank() = default;
+  explicit MultilinearRank(std::vector<std::size_t> m) : mu(std::move(m)) {}
+};
+
+struct TuckerDecomposition {  // tucker.hpp:27-30
+  DenseTensor core;
+  std::vector<Matrix> factors;
+};
+
+struct AlgoConfig {  // tucker.hpp:32-45
+  MultilinearRank rank;
+  std::size_t oversampling = 10;
+  int power = 1;
+  double alpha = 0.2;
+  ProbRegime regime = ProbRegime::Uniform;
+  double regime_beta = 0.5;
+  std::vector<std::size_t> t_samples;
+  std::vector<std::size_t> order;
+  std::uint64_t seed = 0;
+  GramStrategy strategy = GramStrategy::A;
+  int hooi_max_sweeps = 50;  // accepted for layout compatibility; HOOI is off this path
+  double hooi_tol = 1e-8;
+};
+
+enum class Algorithm {  // tucker.hpp:47-57
+  Thosvd, Sthosvd, Hooi, RandThosvdPower, RandSthosvdPower, RandThosvdAmm, RandSthosvdAmm,
+  RandThosvdPowerQr, RandSthosvdPowerQr,
+};
+
+namespace detail {
+struct CConfig {
+  std::vector<uint64_t> rank, t, order;
+  lmra_algo_config c{};
+  explicit CConfig(const AlgoConfig& cfg) {
+    lmra_algo_config_init(&c);
+    rank.assign(cfg.rank.mu.begin(), cfg.rank.mu.end());
+    t.assign(cfg.t_samples.begin(), cfg.t_samples.end());
+    order.assign(cfg.order.begin(), cfg.order.end());
+    c.rank = rank.data();
+    c.n_rank = rank.size();
+    c.oversampling = cfg.oversampling;
+    c.power = cfg.power;
+    c.alpha = cfg.alpha;
+    c.regime = cfg.regime == ProbRegime::Optimal ? LMRA_OPTIMAL
+               : cfg.regime == ProbRegime::NearlyOptimal ? LMRA_NEARLY_OPTIMAL
+                                                         : LMRA_UNIFORM;
+    c.regime_beta = cfg.regime_beta;
+    c.t_samples = t.empty() ? nullptr : t.data();
+    c.n_t_samples = t.size();
+    c.order = order.empty() ? nullptr : order.data();
+    c.n_order = order.size();
+    c.seed = cfg.seed;
+    c.strategy = cfg.strategy == GramStrategy::A ? LMRA_STRATEGY_A : LMRA_STRATEGY_B;
+  }
+};
+
+inline TuckerDecomposition run(int alg, const DenseTensor& a, const AlgoConfig& cfg) {
+  CConfig cc(cfg);
+  std::vector<uint64_t> dims(a.dims().begin(), a.dims().end());
+  lmra_result* r = nullptr;
+  check(lmra_run_algorithm(default_context(), alg, a.data(), dims.data(), (int)dims.size(),
+                           LMRA_HOST, &cc.c, nullptr, &r));
+  std::unique_ptr<lmra_result, void (*)(lmra_result*)> guard(r, lmra_result_free);
+  const int N = lmra_result_order(r);
+  std::vector<uint64_t> cd(N);
+  lmra_result_core_dims(r, cd.data());
+  TuckerDecomposition out;
+  out.core = DenseTensor(std::vector<std::size_t>(cd.begin(), cd.end()));
+  check(lmra_result_copy_core(r, out.core.data(), LMRA_HOST));
+  for (int n = 0; n < N; ++n) {
+    uint64_t rows = 0, cols = 0;
+    lmra_result_factor_dims(r, n, &rows, &cols);
+    Matrix m(rows, cols);
+    check(lmra_result_copy_factor(r, n, m.data(), LMRA_HOST));
+    out.factors.push_back(std::move(m));
+  }
+  return out;
+}
+}  // namespace detail
+
+// tucker.hpp:91-102
+inline TuckerDecomposition rand_thosvd_power(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_ALG1, a, cfg);
+}
+inline TuckerDecomposition rand_sthosvd_power(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_ALG2, a, cfg);
+}
+inline TuckerDecomposition rand_thosvd_amm(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_ALG4, a, cfg);
+}
+inline TuckerDecomposition rand_sthosvd_amm(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_ALG5, a, cfg);
+}
+
+// tucker.hpp:110-111 (the B200 path carries the randomized power / AMM family)
+inline TuckerDecomposition run_algorithm(Algorithm alg, const DenseTensor& a, const AlgoConfig& cfg) {
+  switch (alg) {
+    case Algorithm::RandThosvdPower: return rand_thosvd_power(a, cfg);
+    case Algorithm::RandSthosvdPower: return rand_sthosvd_power(a, cfg);
+    case Algorithm::RandThosvdAmm: return rand_thosvd_amm(a, cfg);
+    case Algorithm::RandSthosvdAmm: return rand_sthosvd_amm(a, cfg);
+    default: throw std::invalid_argument("algorithm is outside the B200 hot path (alg1/2/4/5)");
+  }
+}
+
+inline std::optional<Algorithm> parse_algorithm(const std::string& id) {  // tucker.cpp:190-201
+  if (id == "thosvd") return Algorithm::Thosvd;
+  if (id == "sthosvd") return Algorithm::Sthosvd;
+  if (id == "hooi") return Algorithm::Hooi;
+  if (id == "alg1") return Algorithm::RandThosvdPower;
+  if (id == "alg2") return Algorithm::RandSthosvdPower;
+  if (id == "alg4") return Algorithm::RandThosvdAmm;
+  if (id == "alg5") return Algorithm::RandSthosvdAmm;
+  if (id == "alg6") return Algorithm::RandThosvdPowerQr;
+  if (id == "alg7") return Algorithm::RandSthosvdPowerQr;
+  return std::nullopt;
+}
+
+// tucker.hpp:116-117
+inline std::vector<std::size_t> amm_sample_counts(const std::vector<std::size_t>& dims,
+                                                  const AlgoConfig& cfg, bool sequential) {
+  detail::CConfig cc(cfg);
+  std::vector<uint64_t> d(dims.begin(), dims.end()), out(dims.size());
+  detail::check(lmra_amm_sample_counts(d.data(), (int)d.size(), &cc.c, sequential ? 1 : 0, out.data()));
+  return std::vector<std::size_t>(out.begin(), out.end());
+}
+
+}  // namespace lmra

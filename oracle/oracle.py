@@ -286,6 +286,8 @@ def mode_n_product(x: np.ndarray, dims: Sequence[int], mode: int, b: np.ndarray)
 def gram_power_apply(a: np.ndarray, g: np.ndarray, q: int, strategy: str = "A") -> np.ndarray:
     a = np.asfortranarray(a, dtype=np.float64)
     g = np.asfortranarray(g, dtype=np.float64)
+    if g.shape[0] != a.shape[0]:  # linalg.cpp:64-65 (the C entry takes G's rows from A)
+        raise OracleInvalidArgument("gram_power_apply: G must have as many rows as A")
     c = np.empty((a.shape[0], g.shape[1]), order="F")
     _check(lib().orc_gram_power_apply(a.ctypes.data_as(dblp), C.c_uint64(a.shape[0]), C.c_uint64(a.shape[1]),
                                       g.ctypes.data_as(dblp), C.c_uint64(g.shape[1]), q,

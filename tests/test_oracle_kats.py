@@ -1,0 +1,197 @@
+"""The reference test suite's known answers, oracles and invariants for the hot path,
+applied to the CPU oracle (proj/tests/test_linalg.cpp, test_sketching.cpp, test_tucker.cpp)."""
+import numpy as np
+import pytest
+
+from conftest import relative_error
+
+ALGS = ["alg1", "alg2", "alg4", "alg5"]
+
+
+# ---------------------------------------------------------------- linalg (test_linalg.cpp)
+def test_gram_power_apply_identity_and_diagonal(orc):
+    g = orc.gaussian_matrix(4, 2, 113, 0)
+    assert np.linalg.norm(orc.gram_power_apply(np.eye(4), g, 3) - g) < 1e-12      # :87-89
+    c = orc.gram_power_apply(np.diag([2.0, 1.0]), np.eye(2), 2)                       # :91-95
+    assert c[0, 0] == pytest.approx(16.0) and c[1, 1] == pytest.approx(1.0)
+    assert abs(c[0, 1]) + abs(c[1, 0]) == 0.0
+
+
+def test_gram_strategies_match_explicit_product(orc):
+    a = orc.gaussian_matrix(10, 30, 127, 0)                                            # :98-110
+    g = orc.gaussian_matrix(10, 4, 127, 1)
+    ex = (a @ a.T) @ g
+    sa, sb = orc.gram_power_apply(a, g, 1, "A"), orc.gram_power_apply(a, g, 1, "B")
+    n = np.linalg.norm(ex)
+    assert np.linalg.norm(sa - ex) <= 2e-9 * n and np.linalg.norm(sb - ex) <= 2e-9 * n
+    with pytest.raises(orc.OracleInvalidArgument):
+        orc.gram_power_apply(a, orc.gaussian_matrix(9, 4, 127, 2), 1)
+    with pytest.raises(orc.OracleInvalidArgument):
+        orc.gram_power_apply(a, g, 0)
+
+
+def test_gram_powers_compose(orc):
+    a, g = orc.gaussian_matrix(8, 12, 131, 0), orc.gaussian_matrix(8, 3, 131, 1)       # :112-118
+    once = orc.gram_power_apply(a, g, 3)
+    split = orc.gram_power_apply(a, orc.gram_power_apply(a, g, 2), 1)
+    assert np.linalg.norm(once - split) <= 1e-8 * np.linalg.norm(once)
+
+
+def test_leading_vectors_diag_and_range(orc):
+    u = orc.leading_left_singular_vectors(np.diag([3.0, 2.0, 1.0]), 3)                  # :24-32
+    assert np.linalg.norm(u - np.eye(3)) < 1e-12
+    d = np.diag([3.0, 2.0, 1.0])
+    q2 = orc.leading_left_singular_vectors(d, 2)                                        # :126-128
+    assert np.linalg.norm(q2 @ q2.T @ d - d) == pytest.approx(1.0, rel=1e-10)
+    with pytest.raises(orc.OracleInvalidArgument):
+        orc.leading_left_singular_vectors(d, 4)
+    with pytest.raises(orc.OracleInvalidArgument):
+        orc.leading_left_singular_vectors(d, 0)
+
+
+def test_truncation_residual_is_singular_tail(orc):
+    c = orc.gaussian_matrix(12, 6, 139, 0)                                              # :134-145
+    s = np.linalg.svd(c, compute_uv=False)
+    q = orc.leading_left_singular_vectors(c, 3)
+    resid = np.linalg.norm(c - q @ q.T @ c)
+    assert resid == pytest.approx(np.sqrt(np.sum(s[3:] ** 2)), rel=1e-10)
+
+
+def test_sign_convention(orc):
+    # linalg.cpp:13-29: the largest-|u| entry of each column is nonnegative
+    c = orc.gaussian_matrix(40, 8, 5, 5)
+    u = orc.leading_left_singular_vectors(c, 8)
+    for k in range(8):
+        i = int(np.argmax(np.abs(u[:, k])))
+        assert u[i, k] >= 0.0
+
+
+# ---------------------------------------------------------------- sketching (test_sketching.cpp)
+def test_probability_invariants(orc):
+    p = orc.probabilities(np.ones(4), "uniform")                                          # :56-68
+    assert np.all(p == 0.25)
+    n = orc.probabilities(np.array([2.0, 6.0]), "optimal")
+    assert n[0] == pytest.approx(0.25) and n[1] == pytest.approx(0.75)
+    with pytest.raises(orc.OracleInvalidArgument):  # sketching.cpp:41-43 (total > 0 here)
+        orc.probabilities(np.array([3.0, -1.0]), "optimal")
+    z = orc.probabilities(np.zeros(5), "optimal")  # tucker.cpp:121 -> uniform
+    assert np.all(z == 0.2)
+
+
+def test_randsample_point_mass_and_zero_weights(orc):
+    idx, sc = orc.randsample(5, np.array([1.0, 0.0, 0.0]), 5, 0)                        # :112-127
+    assert np.all(idx == 0) and np.allclose(sc, 1.0 / np.sqrt(5.0))
+    idx, _ = orc.randsample(2000, np.array([0.5, 0.0, 0.5, 0.0]), 6, 0)                 # :129-134
+    assert set(np.unique(idx)) <= {0, 2}
+
+
+def test_randsample_frequencies(orc):
+    n, draws = 7, 100000                                                                  # :136-147
+    idx, _ = orc.randsample(draws, np.full(n, 1.0 / n), 8, 0)
+    counts = np.bincount(idx, minlength=n)
+    sigma = np.sqrt(draws * (1 / n) * (1 - 1 / n))
+    assert np.all(np.abs(counts - draws / n) <= 3 * sigma)
+
+
+def test_selector_second_moment(orc):
+    p = orc.probabilities(np.array([1.0, 2, 3, 2, 1]), "optimal")                       # :149-159
+    acc = np.zeros((5, 5))
+    for t in range(2000):
+        idx, sc = orc.randsample(8, p, 11, t)
+        s = np.zeros((5, 8))
+        s[idx, np.arange(8)] = sc
+        acc += s @ s.T
+    assert np.abs(acc / 2000 - np.eye(5)).max() <= 0.1
+
+
+# ---------------------------------------------------------------- tucker (test_tucker.cpp)
+def test_sample_counts(orc):
+    cfg = orc.AlgoConfig(rank=[10, 10, 10], alpha=0.2)                                     # :448-459
+    assert orc.amm_sample_counts([60, 60, 60], cfg, False) == [720, 720, 720]
+    assert orc.amm_sample_counts([60, 60, 60], cfg, True) == [720, 120, 20]
+    cfg.t_samples = [5, 6, 7]
+    assert orc.amm_sample_counts([60, 60, 60], cfg, True) == [5, 6, 7]
+    # BASELINE cfg5 counts, in IEEE double
+    c5 = orc.AlgoConfig(rank=[40, 40, 3, 40], alpha=0.2)
+    assert orc.amm_sample_counts([512, 512, 3, 512], c5, True) == [157287, 12288, 163840, 960]
+
+
+def test_config_validation(orc):
+    x = orc.rng_normal(45, 0, 64)                                                          # :430-446
+    for alg, kw in [("alg2", dict(rank=[2, 2, 2], order=[0, 0, 2])), ("alg1", dict(rank=[2, 2, 2], power=0)),
+                    ("alg4", dict(rank=[2, 2, 2], alpha=1.5))]:
+        with pytest.raises(orc.OracleInvalidArgument):
+            orc.run(alg, x, [4, 4, 4], orc.AlgoConfig(**kw))
+    with pytest.raises(orc.OracleInvalidArgument):  # rank length != order
+        orc.run("alg1", x, [4, 4, 4], orc.AlgoConfig(rank=[2, 2]))
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_exact_rank_recovery(orc, alg):
+    dims = [24, 24, 24]                                                                     # :247-264
+    x = orc.gen_tucker_noise(dims, [4, 4, 4], 0.0, 27)
+    kw = dict(rank=[4, 4, 4], seed=1)
+    if alg == "alg4":
+        kw.update(regime="optimal", t_samples=[576, 576, 576])
+    if alg == "alg5":
+        kw.update(t_samples=[576, 96, 16])
+    d = orc.run(alg, x, dims, orc.AlgoConfig(**kw))
+    re = relative_error(x.reshape(dims, order="F"), d.core, d.factors)
+    assert re <= (1e-6 if alg in ("alg4", "alg5") else 1e-8)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_shared_invariants(orc, alg):
+    # :74-109 applied at :360-369: orthonormal factors, core = a x_n Q_n^T, energy identity
+    dims = [12, 10, 8]
+    x = orc.rng_normal(37, 0, 960)
+    d = orc.run(alg, x, dims, orc.AlgoConfig(rank=[3, 4, 2], seed=5))
+    a = x.reshape(dims, order="F")
+    for q in d.factors:
+        assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-10
+    ref = a
+    for n, q in enumerate(d.factors):
+        ref = np.moveaxis(np.tensordot(q.T, ref, axes=([1], [n])), 0, n)
+    assert np.linalg.norm(ref - d.core) <= 1e-10 * max(1.0, np.linalg.norm(d.core))
+    err = relative_error(a, d.core, d.factors) ** 2 * np.sum(a * a)
+    assert abs(err - (np.sum(a * a) - np.sum(d.core ** 2))) <= 1e-8 * max(1.0, np.sum(a * a))
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_bit_identical_reruns(orc, alg):
+    dims = [14, 12, 10]                                                                     # :386-397
+    x = orc.rng_normal(41, 0, 1680)
+    cfg = orc.AlgoConfig(rank=[3, 3, 3], seed=99)
+    a, b = orc.run(alg, x, dims, cfg), orc.run(alg, x, dims, cfg)
+    assert np.array_equal(a.core, b.core)
+    assert all(np.array_equal(p, q) for p, q in zip(a.factors, b.factors))
+
+
+def test_order4_exact_rank(orc):
+    dims = [12, 12, 12, 12]                                                                 # :399-421
+    x = orc.gen_tucker_noise(dims, [3, 3, 3, 3], 0.0, 47)
+    for alg in ["alg1", "alg2"]:
+        d = orc.run(alg, x, dims, orc.AlgoConfig(rank=[3, 3, 3, 3], seed=2))
+        assert relative_error(x.reshape(dims, order="F"), d.core, d.factors) <= 1e-8
+    d = orc.run("alg4", x, dims, orc.AlgoConfig(rank=[3, 3, 3, 3], seed=2, t_samples=[1728] * 4))
+    assert relative_error(x.reshape(dims, order="F"), d.core, d.factors) <= 1e-6
+
+
+def test_degenerate_shapes(orc):
+    dims = [40, 2, 2]                                                                       # :461-482
+    x = orc.rng_normal(51, 0, 160)
+    for alg in ALGS:
+        d = orc.run(alg, x, dims, orc.AlgoConfig(rank=[10, 2, 2], seed=3, t_samples=[4, 80, 80]))
+        for q in d.factors:
+            assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-10
+        assert d.factors[0].shape == (40, 10)
+
+
+def test_baseline_generators(orc):
+    h = orc.gen_hilbert([4, 3, 2])
+    a = h.reshape([4, 3, 2], order="F")
+    assert a[0, 0, 0] == 1.0 and a[1, 2, 1] == 1.0 / 5.0  # 1/(i+j+k+1), 0-based
+    x = orc.gen_tucker_noise([20, 20, 20], [5, 5, 5], 1e-2, 1)
+    assert np.all(np.isfinite(x))
+    v = orc.gen_video([16, 16, 3, 16], 30, 0.05, 1)
+    assert v.shape == (16 * 16 * 3 * 16,) and np.all(np.isfinite(v))
