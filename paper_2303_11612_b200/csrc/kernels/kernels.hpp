@@ -34,6 +34,10 @@ cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, con
 // Canonical column squared norms of the mode-n unfolding (chunks of 32 along the fiber,
 // fma within a chunk, chunk partials added in order) -- bit-identical to the oracle.
 cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaStream_t st);
+// The same canonical norms for all three modes of a 3-way tensor from one read (norms3.cu).
+size_t norms3_workspace_doubles(long long I0, long long I1, long long I2);
+cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long I2, double* w0,
+                          double* w1, double* w2, double* work, cudaStream_t st);
 
 // The reference's sampling chain on the device, bit-exact (sampler.cu):
 // probabilities from squared column norms w (regime 0 optimal, 1 nearly-optimal, 2 uniform)

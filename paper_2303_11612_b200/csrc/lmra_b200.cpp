@@ -430,9 +430,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       d_idx[n] = DevBuf(T + 1, s_);
       d_sc[n] = DevBuf(T, s_);
       DevBuf p(J, s_), work(lmra_dev::sampler_workspace_doubles((long long)J), s_);
-      d_w[n] = DevBuf(J, s_);
-      if (cfg.regime != kUniform)
-        e.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(x, v, d_w[n].get(), s_); });
+      if (!d_w[n].get()) {  // not already produced by the fused all-modes pass
+        d_w[n] = DevBuf(J, s_);
+        if (cfg.regime != kUniform)
+          e.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(x, v, d_w[n].get(), s_); });
+      }
       e.launch("sampler", [&] {
         return lmra_dev::launch_sampler(
             d_w[n].get(), (long long)J, cfg.regime, cfg.beta, (long long)T, cfg.seed, N + n + 1,
@@ -480,6 +482,17 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     // modes are independent (run_modes, tucker.cpp:134-160): one stream per mode, so the
     // latency-bound sampling / power / orthonormalisation kernels of different modes
     // overlap; the core contraction joins them on the main stream
+    const bool any_override = in.ov && in.ov->sample_idx;
+    if (amm && cfg.regime != kUniform && N == 3 && !any_override) {
+      // every mode samples from the same input: one read of X for all three norm vectors
+      const long long I0 = in.dims[0], I1 = in.dims[1], I2 = in.dims[2];
+      for (size_t n = 0; n < 3; ++n) d_w[n] = DevBuf(prod(in.dims) / in.dims[n], st);
+      DevBuf nwork(lmra_dev::norms3_workspace_doubles(I0, I1, I2), st);
+      eng.launch("norms", [&] {
+        return lmra_dev::launch_norms3(in.x, I0, I1, I2, d_w[0].get(), d_w[1].get(), d_w[2].get(),
+                                       nwork.get(), st);
+      });
+    }
     cudaEvent_t fork;
     ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
     ck(cudaEventRecord(fork, st), "event");
