@@ -113,6 +113,8 @@ def phase_cost(bc, phase: str, dims_local=None):
     mu = [min(m, d) for m, d in zip(cfg.rank, dims)]
     size = float(np.prod(dims))
     if phase == "norms":
+        if bc.alg == "alg4" and len(dims) == 3:  # fused all-modes pass: one read, N outputs
+            return 2.0 * size * 3, (size + sum(size / d for d in dims)) * 8
         return 2.0 * size, size * 8 + size / dims[0] * 8
     if phase.startswith("core_ttm"):
         k = int(phase[len("core_ttm"):])
@@ -135,8 +137,13 @@ def phase_cost(bc, phase: str, dims_local=None):
 
 def roofline(bc, phases, steps, dims_local=None):
     hbm, src = measured_peaks()
-    # dominant kernel = the phase with the largest device time whose cost we model
-    cands = [(ms, name, cnt) for name, (ms, cnt) in phases.items() if phase_cost(bc, name, dims_local)]
+    # dominant kernel = the phase with the largest device time among the launches that run
+    # alone on the main stream (core / shrink contractions, the fused norms pass); the
+    # per-mode phases of T-HOSVD overlap on their own streams, so their event times
+    # include contention and are not a per-kernel duration
+    cands = [(ms, name, cnt) for name, (ms, cnt) in phases.items()
+             if phase_cost(bc, name, dims_local)
+             and (name != "norms" or bc.alg in ("alg2", "alg5") or len(bc.dims) == 3)]
     if not cands:
         return None
     ms, name, cnt = max(cands)

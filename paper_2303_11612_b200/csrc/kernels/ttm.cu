@@ -9,6 +9,8 @@
 // dimension is j; the short dimension (factor / sketch width, <= 64) lives in
 // the N of m16n8k4 and is padded to a multiple of 8.
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -21,9 +23,9 @@ constexpr int kThreads = 256;
 // TTM: Y(k, j) = sum_r Bt[r + I*k] * X(r, j), k < m.  Y has X's layout with I -> m.
 // CTA tile: 128 columns j x all k; 8 warps x 16 j.  K (= I) in chunks of 16.
 // ----------------------------------------------------------------------------
-template <int M8, bool RCONTIG>
+template <int M8, bool RCONTIG, int KC_ = 16, int ST_ = 3>
 struct TtmCfg {
-  static constexpr int JT = 128, KC = 16, STAGES = 3;
+  static constexpr int JT = 128, KC = KC_, STAGES = ST_;
   static constexpr int LDA = RCONTIG ? conflict_free_ld(KC) : conflict_free_ld(JT);
   static constexpr int A_ELEMS = RCONTIG ? JT * LDA : KC * LDA;
   static constexpr int LDB = conflict_free_ld(M8);
@@ -32,11 +34,11 @@ struct TtmCfg {
   static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES;
 };
 
-template <int M8, bool RCONTIG>
+template <int M8, bool RCONTIG, int KC_, int ST_>
 __global__ void __launch_bounds__(kThreads, 2)
     ttm_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ bt, int m,
                int mtot, int koff, double* __restrict__ y) {
-  using C = TtmCfg<M8, RCONTIG>;
+  using C = TtmCfg<M8, RCONTIG, KC_, ST_>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const long long J = v.inner * v.outer, I = v.I;
@@ -65,11 +67,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     double* As = smem + stage * C::STAGE_ELEMS;
     double* Bs = As + C::A_ELEMS;
     const long long k0 = (long long)kt * C::KC;
-    // B^T chunk: Bs[r][k] = bt[(k0 + r) + I*k]
-    for (int e = tid; e < C::KC * M8; e += kThreads) {
-      int r = e % C::KC, k = e / C::KC;
-      bool ok = (k0 + r < I) && (k < m);
-      cp_async8(Bs + r * C::LDB + k, ok ? bt + (k0 + r) + I * k : bt, ok);
+    // B chunk from the packed row-major bk[r][M8] (zero padded): rows r0..r0+15 are
+    // contiguous, 16-byte copies, conflict-free row-major stores
+    for (int e = tid; e < C::KC * (M8 / 2); e += kThreads) {
+      int r = e / (M8 / 2), c2 = e % (M8 / 2);
+      bool ok = k0 + r < I;
+      cp_async16(Bs + r * C::LDB + 2 * c2, ok ? bt + (k0 + r) * M8 + 2 * c2 : bt, ok);
     }
     if (RCONTIG) {  // X(r, j) = x[I*j + r]  ->  As[j][r]
       if (vec16) {
@@ -360,18 +363,43 @@ __global__ void gather_strided_kernel(const double* __restrict__ x, ModeView v,
 // ----------------------------------------------------------------------------
 // launchers
 // ----------------------------------------------------------------------------
+// bk[r * M8 + k] = bt[r + I * k] for k < m, 0 for m <= k < M8 (row-major, zero padded)
+__global__ void pack_b_kernel(const double* __restrict__ bt, long long I, int m, int M8,
+                              double* __restrict__ bk) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * M8) return;
+  const long long r = e / M8;
+  const int k = (int)(e - r * M8);
+  bk[e] = k < m ? bt[r + I * k] : 0.0;
+}
+
 template <int M8, bool RC>
-static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt, int m, int mtot,
-                                int koff, double* y, cudaStream_t st) {
-  using C = TtmCfg<M8, RC>;
-  static unsigned long long attr_done = 0;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_kernel<M8, RC>), C::SMEM,
-                                   attr_done);
-  if (e != cudaSuccess) return e;
-  long long J = v.inner * v.outer;
-  dim3 grid((unsigned)((J + C::JT - 1) / C::JT));
-  ttm_kernel<M8, RC><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y);
-  return cudaGetLastError();
+static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_colmajor, int m,
+                                int mtot, int koff, double* y, cudaStream_t st) {
+  double* bt = nullptr;  // packed copy, stream-ordered scratch
+  cudaError_t pe = cudaMallocAsync(reinterpret_cast<void**>(&bt), sizeof(double) * v.I * M8, st);
+  if (pe != cudaSuccess) return pe;
+  pack_b_kernel<<<(unsigned)((v.I * M8 + 255) / 256), 256, 0, st>>>(bt_colmajor, v.I, m, M8, bt);
+  struct FreeGuard {
+    double* p;
+    cudaStream_t s;
+    ~FreeGuard() { cudaFreeAsync(p, s); }
+  } free_guard{bt, st};
+  // K chunk 16 x 3 stages: measured best overall against (32,2), (16,4), (32,3) on the
+  // BASELINE widths (tools/ttm_variants.sh, round 1)
+  auto go = [&](auto kc, auto stg) -> cudaError_t {
+    constexpr int KC = decltype(kc)::value, ST = decltype(stg)::value;
+    using C = TtmCfg<M8, RC, KC, ST>;
+    static unsigned long long attr_done = 0;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_kernel<M8, RC, KC, ST>),
+                                     C::SMEM, attr_done);
+    if (e != cudaSuccess) return e;
+    long long J = v.inner * v.outer;
+    dim3 grid((unsigned)((J + C::JT - 1) / C::JT));
+    ttm_kernel<M8, RC, KC, ST><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y);
+    return cudaGetLastError();
+  };
+  return go(std::integral_constant<int, 16>{}, std::integral_constant<int, 3>{});
 }
 
 template <bool RC>
