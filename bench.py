@@ -247,12 +247,15 @@ def bench_gpu(args, rank, world, local_rank):
 
     x = generate_device(bc, ctx=ctx)
     dims = list(bc.dims)
-    if world > 1:
+    local_dims = list(dims)
+    if world > 1:  # this rank's slab of the last mode (lmra_shard_range)
         start, count = P.shard_range(dims[-1], world, rank)
         slab = int(np.prod(dims[:-1]))
         x = x[start * slab:(start + count) * slab].clone()
+        local_dims[-1] = count
+        torch.cuda.synchronize()
         torch.cuda.empty_cache()
-    t = P.DenseTensor.device(x, dims)
+    t = P.DenseTensor.device(x, local_dims)
     cost = algorithmic_cost(bc)
 
     def barrier():
@@ -260,7 +263,7 @@ def bench_gpu(args, rank, world, local_rank):
             dist.barrier()
 
     for _ in range(args.warmup):
-        r = P.run_raw(bc.alg, t, bc.cfg, ctx=ctx)
+        r = P.run_raw(bc.alg, t, bc.cfg, ctx=ctx, global_dims=dims)
         r.free()
     torch.cuda.synchronize()
     barrier()
@@ -274,7 +277,7 @@ def bench_gpu(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            r = P.run_raw(bc.alg, t, bc.cfg, ctx=ctx)
+            r = P.run_raw(bc.alg, t, bc.cfg, ctx=ctx, global_dims=dims)
             for k, (ms, cnt) in r.phases().items():
                 a = phases.get(k, (0.0, 0))
                 phases[k] = (a[0] + ms, a[1] + cnt)
@@ -300,8 +303,8 @@ def bench_gpu(args, rank, world, local_rank):
     if args.e2e_steps > 0:
         host = torch.empty(x.numel(), dtype=torch.float64, pin_memory=True)
         host.copy_(x)
-        th = P.DenseTensor(dims, host.numpy())  # host buffer (pinned): H2D inside every step
-        r = P.run_raw(bc.alg, th, bc.cfg, ctx=ctx)
+        th = P.DenseTensor(local_dims, host.numpy())  # host buffer (pinned): H2D inside every step
+        r = P.run_raw(bc.alg, th, bc.cfg, ctx=ctx, global_dims=dims)
         dec = r.to_host(with_trace=False)
         r.free()
         d2h = (dec.core.size + sum(f.size for f in dec.factors)) * 8
@@ -311,7 +314,7 @@ def bench_gpu(args, rank, world, local_rank):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            r = P.run_raw(bc.alg, th, bc.cfg, ctx=ctx)
+            r = P.run_raw(bc.alg, th, bc.cfg, ctx=ctx, global_dims=dims)
             dec = r.to_host(with_trace=False)
             r.free()
         e1.record(stream)
@@ -321,17 +324,16 @@ def bench_gpu(args, rank, world, local_rank):
             tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
+        # whole job: every rank copies its slab in (together the full tensor) and reads back
+        # the (replicated) core + factors
         e2e = {"value": round(cost["bytes"] * args.e2e_steps / (ems / 1e3) / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": int(host.numel() * 8), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(np.prod(dims)) * 8, "d2h_bytes_per_step": int(d2h) * world,
                "ms_per_step": round(ems / args.e2e_steps, 3), "steps": args.e2e_steps}
         del host
 
     if rank != 0:
         return 0
-    dims_local = None
-    if world > 1:
-        dims_local = dims[:-1] + [P.shard_range(dims[-1], world, rank)[1]]
-    roof = roofline(bc, phases, args.steps, dims_local)
+    roof = roofline(bc, phases, args.steps, local_dims if world > 1 else None)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         sbc = cpu_sample_workload()

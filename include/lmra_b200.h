@@ -101,6 +101,12 @@ int lmra_context_synchronize(lmra_context* ctx);
  * are combined with NCCL all-reduce / all-gather over NVLink. */
 int lmra_nccl_unique_id(void* out128);
 int lmra_context_set_comm(lmra_context* ctx, const void* unique_id128, int nranks, int rank);
+/* In-process rank group: each rank is a host thread with its own context (any devices);
+ * collectives are device copies + host barriers.  Used to check the sharded path with
+ * several ranks on one GPU; NCCL (lmra_context_set_comm) is the multi-GPU product path. */
+int lmra_thread_group_create(int nranks, void** group);
+void lmra_thread_group_destroy(void* group);
+int lmra_context_set_thread_comm(lmra_context* ctx, void* group, int rank);
 /* Shard plan: contiguous balanced slabs, rank r owns [start, start + count). */
 int lmra_shard_range(uint64_t extent, int nranks, int rank, uint64_t* start, uint64_t* count);
 

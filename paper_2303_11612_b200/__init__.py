@@ -4,7 +4,7 @@ from .tucker import (  # noqa: F401
     AlgoConfig, Context, DenseTensor, TuckerDecomposition, all_algorithm_ids, algorithm_id,
     amm_sample_counts, default_context, gaussian_matrix, nccl_unique_id, parse_algorithm,
     probabilities, rand_sthosvd_amm, rand_sthosvd_power, rand_thosvd_amm, rand_thosvd_power,
-    randsample, run_algorithm, run_raw, shard_range,
+    randsample, run_algorithm, run_raw, shard_range, ThreadGroup,
 )
 from ._lib import LmraError, LmraInvalidArgument, LIB_PATH  # noqa: F401
 from . import device  # noqa: F401

@@ -61,6 +61,9 @@ def _load():
         "lmra_nccl_unique_id": (C.c_int, [vp]),
         "lmra_context_set_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "lmra_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, u64p, u64p]),
+        "lmra_thread_group_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "lmra_thread_group_destroy": (None, [vp]),
+        "lmra_context_set_thread_comm": (C.c_int, [vp, vp, C.c_int]),
         "lmra_run_algorithm": (C.c_int, [vp, C.c_int, vp, u64p, C.c_int, C.c_int,
                                          C.POINTER(LmraAlgoConfig), C.POINTER(LmraOverrides),
                                          C.POINTER(vp)]),
@@ -119,6 +122,7 @@ EXPORTED = [
     "lmra_last_error", "lmra_version", "lmra_algo_config_init", "lmra_context_create",
     "lmra_context_destroy", "lmra_context_set_stream", "lmra_context_synchronize",
     "lmra_nccl_unique_id", "lmra_context_set_comm", "lmra_shard_range", "lmra_run_algorithm",
+    "lmra_thread_group_create", "lmra_thread_group_destroy", "lmra_context_set_thread_comm",
     "lmra_result_order", "lmra_result_core_dims", "lmra_result_copy_core",
     "lmra_result_factor_dims", "lmra_result_copy_factor", "lmra_result_core_device",
     "lmra_result_factor_device", "lmra_result_omega_dims", "lmra_result_copy_omega",

@@ -162,6 +162,40 @@ cudaError_t launch_transpose(const double* a, long long rows, long long cols, do
   return cudaGetLastError();
 }
 
+// sharded runs: global sampled column -> this rank's local column, or -1 if another rank's
+__global__ void localize_idx_kernel(const long long* __restrict__ g, long long T, long long off,
+                                    long long cnt, long long* __restrict__ l) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const long long j = g[t] - off;
+  l[t] = (j >= 0 && j < cnt) ? j : -1;
+}
+
+cudaError_t launch_localize_idx(const long long* g, long long T, long long off, long long cnt,
+                                long long* l, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  localize_idx_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(g, T, off, cnt, l);
+  return cudaGetLastError();
+}
+
+// out[i] = sum_r in[r][i], ranks in order (deterministic in-process all-reduce)
+__global__ void sum_ranks_kernel(const double* const* __restrict__ in, int nranks, long long n,
+                                 double* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = in[0][i];
+    for (int r = 1; r < nranks; ++r) s += in[r][i];
+    out[i] = s;
+  }
+}
+
+cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long n, double* out,
+                             cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  sum_ranks_kernel<<<148 * 4, 256, 0, st>>>(in_dev, nranks, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gen_normals(double* out, long long n, uint64_t seed, uint64_t stream,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

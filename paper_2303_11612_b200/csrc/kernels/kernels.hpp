@@ -65,6 +65,12 @@ cudaError_t launch_gen_uniform_add(double* out, long long n, double scale, uint6
 cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, cudaStream_t st);
 cudaError_t launch_gen_cp(double* out, const long long* dims, int order, const double* profiles,
                           const double* weights, int n_terms, cudaStream_t st);
+// sharded runs: l[t] = g[t] - off if in [0, cnt) else -1
+cudaError_t launch_localize_idx(const long long* g, long long T, long long off, long long cnt,
+                                long long* l, cudaStream_t st);
+// out[i] = sum over ranks in order of in_dev[r][i] (in_dev: device array of device pointers)
+cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long n, double* out,
+                             cudaStream_t st);
 // at (cols x rows) = a^T
 cudaError_t launch_transpose(const double* a, long long rows, long long cols, double* at,
                              cudaStream_t st);

@@ -321,9 +321,14 @@ __global__ void gather_contig_kernel(const double* __restrict__ x, long long I,
   long long tcol = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (tcol >= T) return;
   const int lane = threadIdx.x & 31;
-  const double* src = x + idx[tcol] * I;
-  const double sc = scale[tcol];
   double* dst = out + tcol * I;
+  const long long id = idx[tcol];
+  if (id < 0) {  // column owned by another rank (sharded runs): zero
+    for (long long r = lane; r < I; r += 32) dst[r] = 0.0;
+    return;
+  }
+  const double* src = x + id * I;
+  const double sc = scale[tcol];
   for (long long r = lane; r < I; r += 32) dst[r] = src[r] * sc;
 }
 
@@ -337,7 +342,7 @@ __global__ void gather_strided_kernel(const double* __restrict__ x, ModeView v,
   const long long tcol = t0 + tx;
   long long base = 0;
   double sc = 0.0;
-  const bool ok = tcol < T;
+  const bool ok = tcol < T && idx[tcol] >= 0;  // negative index: another rank's column -> 0
   if (ok) {
     base = col_base(idx[tcol], v.inner, v.I);
     sc = scale[tcol];

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -69,6 +70,98 @@ double now_ms() {
       .count();
 }
 
+// ------------------------------------------------------------------ collectives
+// The sharded path needs two collectives on small device buffers: an in-place sum
+// all-reduce and an equal-count all-gather.  NcclComm is the product (one process per GPU,
+// NVLink); ThreadComm runs several ranks as host threads of one process (each with its own
+// context/stream, possibly on one GPU) with device-side copies and host barriers -- no
+// kernel ever waits on another rank -- so the sharded code can be checked rank-for-rank on
+// a single GPU.
+struct Comm {
+  int nranks = 1, rank = 0;
+  virtual ~Comm() = default;
+  virtual void allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
+  virtual void allgather(const double* send, double* recv, size_t n_per_rank, cudaStream_t st) = 0;
+  virtual void abort() {}  // a rank failed mid-run: release peers blocked in a collective
+};
+
+struct NcclComm : Comm {
+  ncclComm_t c = nullptr;
+  ~NcclComm() override {
+    if (c) lmra_host::nccl().CommDestroy(c);
+  }
+  void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
+    ckn(lmra_host::nccl().AllReduce(buf, buf, n, ncclDouble, ncclSum, c, st), "ncclAllReduce");
+  }
+  void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    ckn(lmra_host::nccl().AllGather(send, recv, n, ncclDouble, c, st), "ncclAllGather");
+  }
+};
+
+struct ThreadGroup {
+  int n = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  bool aborted = false;  // sticky: a group whose run failed on some rank is not reusable
+  std::vector<const double*> ptrs;
+  explicit ThreadGroup(int nr) : n(nr), ptrs(nr, nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    if (aborted) throw std::runtime_error("thread group: a peer rank failed");
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g || aborted; });
+      if (gen == g) throw std::runtime_error("thread group: a peer rank failed");
+    }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+struct ThreadComm : Comm {
+  std::shared_ptr<ThreadGroup> g;
+  void allreduce_sum(double* buf, size_t n, cudaStream_t st) override;
+  void abort() override { g->abort(); }
+  void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    ck(cudaStreamSynchronize(st), "sync");
+    g->ptrs[rank] = send;
+    g->barrier();
+    for (int r = 0; r < nranks; ++r)
+      ck(cudaMemcpyAsync(recv + (size_t)r * n, g->ptrs[r], n * sizeof(double),
+                         cudaMemcpyDeviceToDevice, st),
+         "allgather copy");
+    ck(cudaStreamSynchronize(st), "sync");
+    g->barrier();
+  }
+};
+
+void ThreadComm::allreduce_sum(double* buf, size_t n, cudaStream_t st) {
+  ck(cudaStreamSynchronize(st), "sync");
+  g->ptrs[rank] = buf;
+  g->barrier();
+  double* tmp = nullptr;
+  const double** dptrs = nullptr;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<size_t>(n, 1) * sizeof(double), st), "alloc");
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&dptrs), nranks * sizeof(double*), st), "alloc");
+  ck(cudaMemcpyAsync(dptrs, g->ptrs.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice, st), "H2D");
+  ck(lmra_dev::launch_sum_ranks(dptrs, nranks, (long long)n, tmp, st), "sum_ranks");
+  ck(cudaStreamSynchronize(st), "sync");
+  g->barrier();  // every rank has read every buffer
+  ck(cudaMemcpyAsync(buf, tmp, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(dptrs, st);
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ context
@@ -77,7 +170,7 @@ struct lmra_context {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int num_sms = 148;
-  ncclComm_t comm = nullptr;
+  std::shared_ptr<Comm> comm;  // set: sharded runs (tensor = this rank's slab of the last mode)
   int nranks = 1, rank = 0;
   std::mutex mu;
   long long launches = 0;
@@ -617,6 +710,366 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   res->t_total = now_ms() - t0;
 }
 
+// ------------------------------------------------------------------ sharded (multi-GPU) run
+// The tensor is sharded along its LAST mode: rank R holds the contiguous slab
+// i_{N-1} in [start_R, start_R + count_R) (lmra_shard_range), dims[] are global.
+//  * modes n < N-1: an unfolding column j = (i, o) has i_{N-1} inside o, so each rank owns a
+//    contiguous range of columns: norms are local and exact (canonical order) and are
+//    all-gathered, so every rank runs the identical sampling chain; sampled fibres are
+//    gathered by their owner (others contribute zero columns); the power scheme's Gram
+//    partials (I_n x s) are all-reduced; the contraction stays local (still sharded).
+//  * mode N-1: fibres are split by rows: local norm partials are all-reduced, half-products
+//    (T x s or J x s) are all-reduced, the sketch's row blocks are all-gathered; the
+//    contraction of this mode produces a partial that is all-reduced, after which the tensor
+//    is replicated and the remaining work is identical on every rank.
+// Every rank computes bitwise-identical factors (identical reduced inputs, deterministic
+// kernels), so no broadcast is needed.
+void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) {
+  using namespace lmra_host;
+  const double t0 = now_ms();
+  std::vector<PhaseRec> prof;
+  ctx->next_event = 0;
+  Engine eng(ctx, ctx->profile ? &prof : nullptr);
+  cudaStream_t st = ctx->stream;
+  Comm& comm = *ctx->comm;
+  const int P = comm.nranks, R = comm.rank;
+  const auto& cfg = in.cfg;
+  const size_t N = in.dims.size();
+  for (size_t d : in.dims)
+    if (d == 0) throw std::invalid_argument("tensor dimension must be positive");
+  Resolved r = resolve(in.dims, cfg);
+  const bool amm = in.alg == LMRA_ALG4 || in.alg == LMRA_ALG5;
+  const bool sequential = in.alg == LMRA_ALG2 || in.alg == LMRA_ALG5;
+  std::vector<size_t> t_flat;
+  if (amm && !sequential) t_flat = amm_sample_counts(in.dims, cfg, false);
+  if (amm && sequential && !cfg.t_samples.empty() && cfg.t_samples.size() != N)
+    throw std::invalid_argument("sample count override length must equal tensor order");
+  for (size_t n = 0; n < N; ++n)
+    if (r.sketch[n] > (size_t)lmra_dev::kMaxWidth)
+      throw std::invalid_argument("sketch width mu_n + oversampling above 64 is not supported");
+  const size_t L = in.dims[N - 1];
+  if (L < (size_t)P) throw std::invalid_argument("last mode extent is smaller than the rank count");
+  std::vector<size_t> sh0(P), shc(P);
+  for (int q = 0; q < P; ++q) {
+    sh0[q] = (L * q) / P;
+    shc[q] = (L * (q + 1)) / P - sh0[q];
+  }
+  const size_t s0 = sh0[R], c0 = shc[R], cmax = *std::max_element(shc.begin(), shc.end());
+
+  res->omega.assign(N, {});
+  res->om_rows.assign(N, 0);
+  res->om_cols.assign(N, 0);
+  res->idx.assign(N, {});
+  res->scales.assign(N, {});
+  res->norms.assign(N, {});
+  res->factors.assign(N, nullptr);
+  res->f_rows.assign(N, 0);
+  res->f_cols.assign(N, 0);
+
+  cudaEvent_t ev0, ev1;
+  ck(cudaEventCreate(&ev0), "event");
+  ck(cudaEventCreate(&ev1), "event");
+  ck(cudaEventRecord(ev0, st), "event");
+  const long long launches0 = ctx->launches;
+
+  std::vector<size_t> om_off(N + 1, 0);
+  for (size_t n = 0; n < N; ++n) {
+    res->om_rows[n] = in.dims[n];
+    res->om_cols[n] = r.sketch[n];
+    om_off[n + 1] = om_off[n] + in.dims[n] * r.sketch[n];
+  }
+  double* om_pin = ctx->pinned_buffer(om_off[N]);
+  {
+    const double tr0 = now_ms();
+    for (size_t n = 0; n < N; ++n) {
+      const size_t cnt = om_off[n + 1] - om_off[n];
+      if (in.ov && in.ov->omega && in.ov->omega[n])
+        std::memcpy(om_pin + om_off[n], in.ov->omega[n], sizeof(double) * cnt);
+      else
+        fill_normals(cfg.seed, n + 1, om_pin + om_off[n], cnt, host_threads());
+    }
+    res->t_rng = now_ms() - tr0;
+  }
+  DevBuf status(N, st);
+  ck(cudaMemsetAsync(status.get(), 0, N * sizeof(double), st), "memset");
+  int* status_i = reinterpret_cast<int*>(status.get());
+  std::vector<DevBuf> d_idx(N), d_sc(N), d_w(N);
+  std::vector<size_t> n_draws(N, 0);
+
+  std::vector<size_t> gdims = in.dims;  // global dims of the current tensor
+  bool sharded = true;                  // current tensor = this rank's slab of mode N-1
+  const double* cur = in.x;
+  DevBuf curbuf;
+  auto ldims = [&]() {
+    std::vector<size_t> d = gdims;
+    if (sharded) d[N - 1] = c0;
+    return d;
+  };
+  auto rows_of = [&](const double* m, size_t I, size_t cols, size_t start, size_t cnt) {
+    DevBuf out(cnt * cols, st);  // rows [start, start+cnt) of an I x cols column-major matrix
+    ck(cudaMemcpy2DAsync(out.get(), cnt * sizeof(double), m + start, I * sizeof(double),
+                         cnt * sizeof(double), cols, cudaMemcpyDeviceToDevice, st),
+       "rows");
+    return out;
+  };
+  auto gather_rows = [&](const double* local, size_t cols, double* full, size_t I) {
+    // all-gather row blocks (c_q x cols each, padded to cmax) into full (I x cols)
+    DevBuf send(cmax * cols, st), recv((size_t)P * cmax * cols, st);
+    ck(cudaMemsetAsync(send.get(), 0, cmax * cols * sizeof(double), st), "memset");
+    ck(cudaMemcpy2DAsync(send.get(), cmax * sizeof(double), local, c0 * sizeof(double),
+                         c0 * sizeof(double), cols, cudaMemcpyDeviceToDevice, st),
+       "pack");
+    comm.allgather(send.get(), recv.get(), cmax * cols, st);
+    for (int q = 0; q < P; ++q)
+      ck(cudaMemcpy2DAsync(full + sh0[q], I * sizeof(double), recv.get() + (size_t)q * cmax * cols,
+                           cmax * sizeof(double), shc[q] * sizeof(double), cols,
+                           cudaMemcpyDeviceToDevice, st),
+         "unpack");
+  };
+  auto run_sampler = [&](size_t n, const double* w, size_t J, size_t T) -> size_t {
+    if (in.ov && in.ov->sample_idx && in.ov->sample_idx[n]) {  // parity overrides (global idx)
+      T = in.ov->n_samples[n];
+      const int64_t* oi = in.ov->sample_idx[n];
+      for (size_t j = 0; j < T; ++j)
+        if (oi[j] < 0 || (size_t)oi[j] >= J) throw std::invalid_argument("sample index out of range");
+      d_idx[n] = DevBuf(T + 1, st);
+      d_sc[n] = DevBuf(T, st);
+      ck(cudaMemcpyAsync(d_idx[n].get(), oi, T * sizeof(int64_t), cudaMemcpyHostToDevice, st), "H2D idx");
+      ck(cudaMemcpyAsync(d_sc[n].get(), in.ov->sample_scale[n], T * sizeof(double),
+                         cudaMemcpyHostToDevice, st), "H2D scales");
+      ck(cudaStreamSynchronize(st), "sync");
+      n_draws[n] = T;
+      return T;
+    }
+    if (T < 1) throw std::invalid_argument("randsample: L must be positive");
+    d_idx[n] = DevBuf(T + 1, st);
+    d_sc[n] = DevBuf(T, st);
+    DevBuf p(J, st), work(lmra_dev::sampler_workspace_doubles((long long)J), st);
+    DevBuf dummy;
+    if (!w) {  // uniform regime never reads w
+      dummy = DevBuf(J, st);
+      w = dummy.get();
+    }
+    eng.launch("sampler", [&] {
+      return lmra_dev::launch_sampler(w, (long long)J, cfg.regime, cfg.beta, (long long)T,
+                                      cfg.seed, N + n + 1,
+                                      reinterpret_cast<long long*>(d_idx[n].get()), d_sc[n].get(),
+                                      p.get(), work.get(), status_i + N + n, st);
+    });
+    n_draws[n] = T;
+    return T;
+  };
+
+  auto factor = [&](size_t n, size_t t_n) -> DevBuf {
+    const size_t I = gdims[n], s = r.sketch[n];
+    const std::vector<size_t> ld = ldims();
+    const ModeView v = view_of(ld, n);
+    DevBuf c(I * s, st);
+    ck(cudaMemcpyAsync(c.get(), om_pin + om_off[n], I * s * sizeof(double), cudaMemcpyHostToDevice, st),
+       "H2D omega");
+    const bool rows_split = sharded && n == N - 1;
+    if (!sharded) {  // replicated tensor: the single-GPU computation, identical on every rank
+      if (!amm) {
+        eng.gram_power(cur, v, c, s, cfg.power, cfg.strategy);
+      } else {
+        const size_t J = (size_t)(v.inner * v.outer);
+        if (cfg.regime != kUniform) {
+          d_w[n] = DevBuf(J, st);
+          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+        }
+        t_n = run_sampler(n, d_w[n].get(), J, t_n);
+        DevBuf cp(I * t_n, st);
+        eng.launch("gather", [&] {
+          return lmra_dev::launch_gather(cur, v, reinterpret_cast<const long long*>(d_idx[n].get()),
+                                         d_sc[n].get(), (long long)t_n, cp.get(), st);
+        });
+        eng.gram_power(cp.get(), ModeView{1, (long long)I, (long long)t_n}, c, s, cfg.power, cfg.strategy);
+      }
+    } else if (!rows_split) {  // n < N-1: rank-local column range
+      const size_t Jl = (size_t)(v.inner * v.outer), per = Jl / c0, Jg = per * L;
+      const lmra_dev::GramPlan plan = lmra_dev::plan_gram(v, ctx->num_sms);
+      if (!amm) {
+        DevBuf h(Jl * s, st), zpart((size_t)plan.nsplit * I * s, st);
+        for (int k = 0; k < cfg.power; ++k) {
+          eng.launch("power_half", [&] { return lmra_dev::launch_ttm(cur, v, c.get(), (int)s, h.get(), st); });
+          eng.launch("power_gram", [&] {
+            return lmra_dev::launch_gram(cur, v, h.get(), (int)s, zpart.get(), plan, c.get(), st);
+          });
+          comm.allreduce_sum(c.get(), I * s, st);
+        }
+      } else {
+        if (cfg.regime != kUniform) {
+          DevBuf wl(per * cmax, st), all((size_t)P * per * cmax, st);
+          ck(cudaMemsetAsync(wl.get(), 0, per * cmax * sizeof(double), st), "memset");
+          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, wl.get(), st); });
+          comm.allgather(wl.get(), all.get(), per * cmax, st);
+          d_w[n] = DevBuf(Jg, st);
+          for (int q = 0; q < P; ++q)
+            ck(cudaMemcpyAsync(d_w[n].get() + per * sh0[q], all.get() + (size_t)q * per * cmax,
+                               per * shc[q] * sizeof(double), cudaMemcpyDeviceToDevice, st),
+               "unpack norms");
+        }
+        t_n = run_sampler(n, d_w[n].get(), Jg, t_n);
+        DevBuf lidx(t_n + 1, st), cp(I * t_n, st);
+        ck(lmra_dev::launch_localize_idx(reinterpret_cast<const long long*>(d_idx[n].get()),
+                                         (long long)t_n, (long long)(per * s0), (long long)Jl,
+                                         reinterpret_cast<long long*>(lidx.get()), st),
+           "localize");
+        eng.launch("gather", [&] {
+          return lmra_dev::launch_gather(cur, v, reinterpret_cast<const long long*>(lidx.get()),
+                                         d_sc[n].get(), (long long)t_n, cp.get(), st);
+        });
+        const ModeView cv{1, (long long)I, (long long)t_n};
+        const lmra_dev::GramPlan cplan = lmra_dev::plan_gram(cv, ctx->num_sms);
+        DevBuf h(t_n * s, st), zpart((size_t)cplan.nsplit * I * s, st);
+        for (int k = 0; k < cfg.power; ++k) {
+          eng.launch("power_half", [&] { return lmra_dev::launch_ttm(cp.get(), cv, c.get(), (int)s, h.get(), st); });
+          eng.launch("power_gram", [&] {
+            return lmra_dev::launch_gram(cp.get(), cv, h.get(), (int)s, zpart.get(), cplan, c.get(), st);
+          });
+          comm.allreduce_sum(c.get(), I * s, st);
+        }
+      }
+    } else {  // n == N-1 on the slab: fibres split by rows [s0, s0 + c0)
+      const size_t J = (size_t)(v.inner * v.outer);  // all columns are local
+      DevBuf cr = rows_of(c.get(), I, s, s0, c0);
+      if (!amm) {
+        const lmra_dev::GramPlan plan = lmra_dev::plan_gram(v, ctx->num_sms);
+        DevBuf h(J * s, st), zpart((size_t)plan.nsplit * c0 * s, st);
+        for (int k = 0; k < cfg.power; ++k) {
+          eng.launch("power_half", [&] { return lmra_dev::launch_ttm(cur, v, cr.get(), (int)s, h.get(), st); });
+          comm.allreduce_sum(h.get(), J * s, st);
+          eng.launch("power_gram", [&] {
+            return lmra_dev::launch_gram(cur, v, h.get(), (int)s, zpart.get(), plan, cr.get(), st);
+          });
+        }
+      } else {
+        if (cfg.regime != kUniform) {
+          d_w[n] = DevBuf(J, st);
+          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+          comm.allreduce_sum(d_w[n].get(), J, st);
+        }
+        t_n = run_sampler(n, d_w[n].get(), J, t_n);
+        DevBuf cp(c0 * t_n, st);
+        eng.launch("gather", [&] {
+          return lmra_dev::launch_gather(cur, v, reinterpret_cast<const long long*>(d_idx[n].get()),
+                                         d_sc[n].get(), (long long)t_n, cp.get(), st);
+        });
+        const ModeView cv{1, (long long)c0, (long long)t_n};
+        const lmra_dev::GramPlan cplan = lmra_dev::plan_gram(cv, ctx->num_sms);
+        DevBuf h(t_n * s, st), zpart((size_t)cplan.nsplit * c0 * s, st);
+        for (int k = 0; k < cfg.power; ++k) {
+          eng.launch("power_half", [&] { return lmra_dev::launch_ttm(cp.get(), cv, cr.get(), (int)s, h.get(), st); });
+          comm.allreduce_sum(h.get(), t_n * s, st);
+          eng.launch("power_gram", [&] {
+            return lmra_dev::launch_gram(cp.get(), cv, h.get(), (int)s, zpart.get(), cplan, cr.get(), st);
+          });
+        }
+      }
+      gather_rows(cr.get(), s, c.get(), I);
+    }
+    const size_t mu = std::min(r.mu[n], std::min(I, s));  // top_left_vectors_clamped
+    if (mu < r.mu[n] && R == 0)
+      fprintf(stderr, "lmra: requested rank %zu exceeds matrix rank limit %zu, clamping\n",
+              r.mu[n], mu);
+    res->f_rows[n] = I;
+    res->f_cols[n] = mu;
+    return eng.orth(c.get(), I, s, mu, status_i + n);
+  };
+
+  auto contract = [&](size_t n, const double* q, size_t mu, const std::string& phase) {
+    const std::vector<size_t> ld = ldims();
+    if (!sharded || n != N - 1) {
+      DevBuf y = eng.ttm(cur, ld, n, q, mu, phase);
+      curbuf = std::move(y);
+    } else {  // contraction over the sharded mode: local partial + all-reduce -> replicated
+      DevBuf qr = rows_of(q, gdims[n], mu, s0, c0);
+      DevBuf y = eng.ttm(cur, ld, n, qr.get(), mu, phase);
+      std::vector<size_t> od = ld;
+      od[n] = mu;
+      comm.allreduce_sum(y.get(), prod(od), st);
+      curbuf = std::move(y);
+      sharded = false;
+    }
+    cur = curbuf.get();
+    gdims[n] = mu;
+  };
+
+  std::vector<DevBuf> factors(N);
+  if (!sequential) {
+    for (size_t n = 0; n < N; ++n) factors[n] = factor(n, amm ? t_flat[n] : 0);
+    std::vector<size_t> idx(N);
+    std::iota(idx.begin(), idx.end(), size_t{0});
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](size_t a, size_t b) { return res->f_cols[a] < res->f_cols[b]; });
+    int step = 0;
+    for (size_t n : idx) contract(n, factors[n].get(), res->f_cols[n], "core_ttm" + std::to_string(step++));
+  } else {
+    for (size_t n : r.order) {
+      size_t t_n = 0;
+      if (amm) {
+        const size_t cols = prod(gdims) / gdims[n];
+        t_n = cfg.t_samples.empty() ? samples_from_alpha(cfg.alpha, cols) : cfg.t_samples[n];
+        if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
+      }
+      factors[n] = factor(n, t_n);
+      contract(n, factors[n].get(), res->f_cols[n], "shrink_ttm_m" + std::to_string(n));
+    }
+  }
+  res->core_dims = gdims;
+  if (curbuf.get() == nullptr) throw std::runtime_error("sharded run produced no core");
+  res->core = curbuf.detach();
+  for (size_t n = 0; n < N; ++n) res->factors[n] = factors[n].detach();
+
+  ck(cudaEventRecord(ev1, st), "event");
+  std::vector<int> stat(2 * N);
+  ck(cudaMemcpyAsync(stat.data(), status.get(), 2 * N * sizeof(int), cudaMemcpyDeviceToHost, st),
+     "D2H status");
+  if (ctx->keep_trace) {
+    for (size_t n = 0; n < N; ++n) res->omega[n].assign(om_pin + om_off[n], om_pin + om_off[n + 1]);
+    for (size_t n = 0; n < N; ++n)
+      if (n_draws[n]) {
+        res->idx[n].resize(n_draws[n]);
+        res->scales[n].resize(n_draws[n]);
+        ck(cudaMemcpyAsync(res->idx[n].data(), d_idx[n].get(), n_draws[n] * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, st), "D2H idx");
+        ck(cudaMemcpyAsync(res->scales[n].data(), d_sc[n].get(), n_draws[n] * sizeof(double),
+                           cudaMemcpyDeviceToHost, st), "D2H scales");
+      }
+  }
+  ck(cudaStreamSynchronize(st), "sync");
+  float dev_ms = 0;
+  ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event time");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  for (size_t n = 0; n < N; ++n) {
+    const int f = stat[N + n];
+    if (f & 1) throw std::invalid_argument("probability weights must be nonnegative");
+    if (f & 32) throw std::invalid_argument("nearly-optimal mixture weight must lie in (0, 1]");
+    if (f & 2) throw std::invalid_argument("cannot normalize an all-zero distribution");
+    if (f & 4) throw std::invalid_argument("probability weights must sum to one");
+    if (f & 8) throw std::invalid_argument("randsample: all-zero distribution");
+    if (f & 16) ++res->sampler_fallbacks;
+  }
+  for (size_t n = 0; n < N; ++n)
+    if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  res->t_device = dev_ms;
+  res->launches = (double)(ctx->launches - launches0);
+  for (const PhaseRec& p : prof) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, p.a, p.b), "event time");
+    auto it = std::find_if(res->phases.begin(), res->phases.end(),
+                           [&](const lmra_result::Phase& q2) { return q2.name == p.name; });
+    if (it == res->phases.end()) {
+      res->phases.push_back({p.name, 0.0, 0});
+      it = res->phases.end() - 1;
+    }
+    it->ms += ms;
+    it->count += 1;
+  }
+  res->t_total = now_ms() - t0;
+}
+
 lmra_host::Config to_config(const lmra_algo_config* c) {
   lmra_host::Config k;
   if (!c) throw std::invalid_argument("null config");
@@ -681,7 +1134,10 @@ void lmra_context_destroy(lmra_context* ctx) {
   {
     DeviceGuard dg(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->comm) lmra_host::nccl().CommDestroy(ctx->comm);
+    ctx->comm.reset();
+    for (cudaStream_t s : ctx->aux) cudaStreamDestroy(s);
+    for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   }
   delete ctx;
@@ -715,10 +1171,38 @@ int lmra_context_set_comm(lmra_context* ctx, const void* uid, int nranks, int ra
     DeviceGuard dg(ctx->device);
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
-    if (ctx->comm) lmra_host::nccl().CommDestroy(ctx->comm);
-    ctx->comm = nullptr;
-    ckn(lmra_host::nccl().CommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+    ctx->comm.reset();
+    auto c = std::make_shared<NcclComm>();
+    ckn(lmra_host::nccl().CommInitRank(&c->c, nranks, id, rank), "ncclCommInitRank");
+    c->nranks = nranks;
+    c->rank = rank;
+    ctx->comm = c;
     ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+int lmra_thread_group_create(int nranks, void** group) {
+  return guard([&] {
+    if (nranks < 1) throw std::invalid_argument("bad rank count");
+    *group = new std::shared_ptr<ThreadGroup>(std::make_shared<ThreadGroup>(nranks));
+  });
+}
+
+void lmra_thread_group_destroy(void* group) {
+  delete static_cast<std::shared_ptr<ThreadGroup>*>(group);
+}
+
+int lmra_context_set_thread_comm(lmra_context* ctx, void* group, int rank) {
+  return guard([&] {
+    auto g = *static_cast<std::shared_ptr<ThreadGroup>*>(group);
+    if (rank < 0 || rank >= g->n) throw std::invalid_argument("bad rank");
+    auto c = std::make_shared<ThreadComm>();
+    c->g = g;
+    c->nranks = g->n;
+    c->rank = rank;
+    ctx->comm = c;
+    ctx->nranks = g->n;
     ctx->rank = rank;
   });
 }
@@ -743,8 +1227,7 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
         algorithm != LMRA_ALG5)
       throw std::invalid_argument("unknown algorithm");
     if (order < 1) throw std::invalid_argument("cannot decompose an order-0 tensor");
-    if (ctx->nranks > 1)
-      throw std::invalid_argument("multi-GPU sharded run not available in this build");
+    const bool sharded = ctx->comm && ctx->nranks > 1;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard dg(ctx->device);
     RunInputs in;
@@ -757,6 +1240,13 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
     DevBuf staged;
     if (x_location == LMRA_HOST) {
       size_t n = prod(in.dims);
+      if (sharded) {  // x is this rank's slab of the last mode
+        const size_t L = in.dims.back();
+        if (L == 0) throw std::invalid_argument("tensor dimension must be positive");
+        const size_t b = (L * (size_t)ctx->rank) / (size_t)ctx->nranks;
+        const size_t e = (L * (size_t)(ctx->rank + 1)) / (size_t)ctx->nranks;
+        n = n / L * (e - b);
+      }
       staged = DevBuf(n, ctx->stream);
       ck(cudaMemcpyAsync(staged.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),
          "H2D tensor");
@@ -764,7 +1254,15 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
     } else {
       in.x = x;
     }
-    run_algorithm_impl(ctx, in, res.get());
+    if (sharded) {
+      try {
+        run_sharded_impl(ctx, in, res.get());
+      } catch (...) {
+        ctx->comm->abort();
+        throw;
+      }
+    } else
+      run_algorithm_impl(ctx, in, res.get());
     *out = res.release();
   });
 }

@@ -183,8 +183,17 @@ class Context:
         check(lib.lmra_context_set_profiling(self.handle, int(bool(on))))
 
     def set_comm(self, unique_id: bytes, nranks: int, rank: int):
+        """NCCL communicator (one process per GPU): later runs on this context are sharded
+        along the last mode (this rank's slab = shard_range(dims[-1], nranks, rank))."""
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib.lmra_context_set_comm(self.handle, buf, int(nranks), int(rank)))
+
+    def set_thread_comm(self, group: "ThreadGroup", rank: int):
+        """In-process communicator: several ranks as host threads of one process (each with
+        its own Context), exchanging through device copies -- the sharded run checked
+        rank-for-rank on one GPU."""
+        check(lib.lmra_context_set_thread_comm(self.handle, group.handle, int(rank)))
+        self._group = group
 
     def close(self):
         if self.handle:
@@ -202,6 +211,24 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib.lmra_nccl_unique_id(buf))
     return buf.raw
+
+
+class ThreadGroup:
+    """Rendezvous for Context.set_thread_comm (lmra_thread_group_create)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        check(lib.lmra_thread_group_create(int(nranks), C.byref(h)))
+        self.handle = h
+        self.nranks = int(nranks)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.lmra_thread_group_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
 
 
 def shard_range(extent: int, nranks: int, rank: int):
@@ -350,9 +377,12 @@ def _as_tensor(a) -> DenseTensor:
 
 
 def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omega=None,
-            samples=None, trace: bool = False) -> _Result:
+            samples=None, trace: bool = False,
+            global_dims: Optional[Sequence[int]] = None) -> _Result:
     """run_algorithm returning the device-resident result handle (no copy-out).
-    trace=True also keeps host copies of the drawn samples and column norms."""
+    trace=True also keeps host copies of the drawn samples and column norms.
+    global_dims: on a sharded context `a` is this rank's slab of the last mode and
+    global_dims the whole tensor's dims (default: a's own dims, i.e. unsharded)."""
     if alg not in _ALG_CODE:
         if alg in ALGORITHM_IDS:
             raise LmraInvalidArgument(f"{alg} is outside the B200 hot path (alg1/alg2/alg4/alg5)")
@@ -360,7 +390,10 @@ def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omeg
     t = _as_tensor(a)
     ctx = ctx or default_context()
     ctx.set_trace(trace)
-    dims = np.asarray(t.dims, dtype=np.uint64)
+    dims = np.asarray(t.dims if global_dims is None else list(global_dims), dtype=np.uint64)
+    if global_dims is not None:
+        if len(global_dims) != len(t.dims) or list(global_dims[:-1]) != list(t.dims[:-1]):
+            raise LmraInvalidArgument("slab dims must equal the global dims except the last")
     c, keep = cfg._to_c()
     ov, keep2 = _overrides(len(t.dims), omega, samples)
     h = C.c_void_p()
@@ -377,10 +410,13 @@ def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omeg
 
 
 def run_algorithm(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omega=None,
-                  samples=None, trace: bool = True) -> TuckerDecomposition:
+                  samples=None, trace: bool = True,
+                  global_dims: Optional[Sequence[int]] = None) -> TuckerDecomposition:
     """tucker.cpp:456-470.  omega / samples: per-mode parity overrides (None = seeded RNG).
-    trace: also return the drawn samples / column norms (host copies)."""
-    r = run_raw(alg, a, cfg, ctx=ctx, omega=omega, samples=samples, trace=trace)
+    trace: also return the drawn samples / column norms (host copies).
+    global_dims: sharded contexts only (see run_raw)."""
+    r = run_raw(alg, a, cfg, ctx=ctx, omega=omega, samples=samples, trace=trace,
+                global_dims=global_dims)
     try:
         return r.to_host()
     finally:
