@@ -38,7 +38,7 @@ P64_MEASURED_TFLOPS = 37.0   # DMMA m16n8k4 loop, profiles/fp64_peaks_r01.json (
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -57,36 +57,88 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region (NVML every 5 ms from a
+    host thread, so even a ~100 ms region gets samples; nvidia-smi -lms 200 as fallback)."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4), ("hw_power_brake", 0x80))
 
-    def __init__(self, index: int):
-        self.index = index
-        self.rows = []
-        self.proc = None
+    def __init__(self, cuda_index: int, period_s: float = 0.005):
+        self.cuda_index = cuda_index
+        self.period = period_s
+        self.rows = []  # (sm_mhz, max_mhz, reason_bits)
+        self.src = None
+        self._stop = threading.Event()
+        self.t = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:  # map the CUDA device to its NVML handle by PCI bus id
+            import torch
+            pr = torch.cuda.get_device_properties(self.cuda_index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.cuda_index)
+
+    def _sample(self):
+        nv, h = self.nv, self.h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.rows.append((float(sm), float(mx), int(bits)))
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                return
+            self._stop.wait(self.period)
 
     def __enter__(self):
         try:
+            self.nv, self.h = self._handle()
+            self._sample()
+            self.src = "nvml"
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.src = None
+            self._smi_start()
+        return self
+
+    def _smi_start(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(self.cuda_index), f"--query-gpu={fields}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.src = "nvidia-smi"
+
+            def rd():
+                for line in self.proc.stdout:
+                    p = [x.strip() for x in line.split(",")]
+                    if len(p) == 6 and p[0].replace(".", "").isdigit():
+                        bits = sum(b for (_, b), v in zip(self.REASONS, p[2:]) if v == "Active")
+                        self.rows.append((float(p[0]), float(p[1]), bits))
+            self.t = threading.Thread(target=rd, daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
-        return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
 
     def __exit__(self, *a):
-        if self.proc:
+        if self.src == "nvml":
+            self._stop.set()
+            self.t.join(1.0)
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
+        elif self.src == "nvidia-smi" and self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -95,14 +147,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        reasons = sorted({n for r in self.rows for n, b in self.REASONS if r[2] & b})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": self.src}
 
 
 def phase_cost(bc, phase: str, dims_local=None):

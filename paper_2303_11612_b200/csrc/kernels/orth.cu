@@ -2,18 +2,27 @@
 //
 // Replaces thin_svd (linalg.cpp:33-43, Eigen BDCSVD) + fix_signs (linalg.cpp:13-29)
 // as used by leading_left_singular_vectors (linalg.cpp:82-87):
-//   C = Q R            blocked Householder TSQR: phase A per row block (recursive levels),
-//                      phase B column-pivoted Householder on the stacked R factors
+//   C = Q R            Householder TSQR: leaves of <= 256 rows factored in parallel CTAs,
+//                      their stacked R factors reduced level by level; the last block gets
+//                      a column-pivoted Householder QR
 //   R = U_R S V^T      one-sided (Hestenes) Jacobi on R^T with the rotations accumulated:
 //                      R^T J = W  =>  R = J diag(|W_j|) (W/|W|)^T, so U_R = J (orthogonal even
 //                      for zero singular values).  The pivoted R is graded, which makes
 //                      Jacobi on R^T converge in a few sweeps (de Rijk / Drmac).
-//   U = Q [U_R ; 0]    reflectors applied in reverse (phase C per row block, staged in smem)
+//   U = Q [U_R ; 0]    reflectors applied in reverse, level by level back down the tree
 //   fix_signs          largest-|u| entry (first index on ties) made >= 0
 // All reductions run in a fixed order, so the result is deterministic run to run.
 // Householder QR is used instead of CholeskyQR2 because the sketches of the
 // BASELINE configs reach kappa(C) ~ 1e16, far past CholeskyQR2's
 // u^{-1/2} limit.
+//
+// Register-resident panels.  A block of <= 16*RPW rows x <= 64 columns lives in registers:
+// warp w holds rows [w*RPW, (w+1)*RPW), lane l holds columns l and l+32.  A Householder
+// step then costs one pass over the registers: the column dot products are per-thread
+// partial sums over the warp's rows, combined across the 16 warps through a 16 x 64
+// shared buffer in warp order.  (The first version kept the panel in shared memory and
+// re-read the whole trailing matrix twice per step: ncu showed it bound on shared-memory
+// bandwidth, ~3.7 us per step for a 334 x 60 block.)
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -22,11 +31,10 @@
 
 namespace lmra_dev {
 
-constexpr int kOrthThreads = 1024;
-constexpr int kOrthWarps = kOrthThreads / 32;
-constexpr size_t kOrthSmemBudget = 200 * 1024;
+constexpr int kQThreads = 512;
+constexpr int kQWarps = kQThreads / 32;
+constexpr int kMaxBlockRows = kQWarps * 16;  // 256 rows per CTA (RPW <= 16)
 constexpr int kOrthMaxS = 64;
-constexpr int kApplyChunk = 8;  // reflectors staged per smem chunk in phase C
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -34,414 +42,682 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Lane-strided dot product over rows [lo, m) with stride 32 and four independent
-// accumulators (ILP: the loads of four rows are in flight together).
-__device__ __forceinline__ double lane_dot(const double* __restrict__ a,
-                                           const double* __restrict__ b, int lo, int m) {
-  double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-  int i = lo;
-  for (; i + 96 < m; i += 128) {
-    d0 += a[i] * b[i];
-    d1 += a[i + 32] * b[i + 32];
-    d2 += a[i + 64] * b[i + 64];
-    d3 += a[i + 96] * b[i + 96];
-  }
-  for (; i < m; i += 32) d0 += a[i] * b[i];
-  return (d0 + d1) + (d2 + d3);
+// ---------------------------------------------------------------------------
+// shared scratch of the register-resident QR / apply
+// ---------------------------------------------------------------------------
+struct QSmem {
+  double* part;   // kQWarps x 64 per-warp partial sums (column c at [w * 64 + c])
+  double* vbuf;   // kMaxBlockRows: the current reflector, broadcast to every lane
+  double* fval;   // 64: tau * (v^T a_c) per column
+  double* rowk;   // 64: row k of the panel (pivoted QR)
+  double* red;    // 64: reduced sums below row k (pivoted QR)
+  double* cn;     // 64: column norms from row k (pivot choice)
+  double* tau;    // 64
+  double* normp;  // kQWarps: partial norms of column k (unpivoted QR)
+  double* pval;   // kQWarps x 64 argmax partials (value), sign fix
+  int* pidx;      // kQWarps x 64 argmax partials (row)
+  int* piv;       // 64
+};
+constexpr size_t kQScratchDoubles = kQWarps * 64 + kMaxBlockRows + 64 * 6 + kQWarps + kQWarps * 64;
+constexpr size_t kQScratchBytes = kQScratchDoubles * 8 + (kQWarps * 64 + 64) * 4 + 64;
+
+__device__ __forceinline__ QSmem carve_q(double* base) {
+  QSmem q;
+  q.part = base;
+  q.vbuf = q.part + kQWarps * 64;
+  q.fval = q.vbuf + kMaxBlockRows;
+  q.rowk = q.fval + 64;
+  q.red = q.rowk + 64;
+  q.cn = q.red + 64;
+  q.tau = q.cn + 64;
+  q.normp = q.tau + 64;
+  q.pval = q.normp + kQWarps;
+  q.pidx = reinterpret_cast<int*>(q.pval + kQWarps * 64);
+  q.piv = q.pidx + kQWarps * 64;
+  return q;
 }
 
-// Householder QR in place on A (m x s, column-major, leading dim lda, in shared memory).
-// On exit: R in the upper triangle, v_k (unit leading entry implicit) below the
-// diagonal, tau[k].  LAPACK dlarfg convention: H_k = I - tau v v^T, beta = -sign(a)*||x||.
-// Column c is owned by warp c % 32.  With piv != nullptr, columns are pivoted
-// (largest remaining norm first, first index on ties; norms recomputed exactly each
-// step in the update pass) and piv[] receives the permutation; cn is s doubles scratch.
-__device__ void block_householder_qr(double* A, int m, int s, int lda, double* tau, int* piv,
-                                     double* cn) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Column helpers.  lo = k - row0 is the position of row k inside this warp's rows: lo < 0
+// means every row is below row k ("full"), lo >= RPW that every row is above it ("done");
+// only the one warp holding row k takes the per-element predicated path.
+template <int RPW>
+__device__ __forceinline__ double col_norm_below(const double (&col)[RPW], int lo) {
+  double t = 0.0;
+  if (lo < 0) {
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) t = fma(col[i], col[i], t);
+  } else if (lo < RPW - 1) {
+#pragma unroll
+    for (int i = 0; i < RPW; ++i)
+      if (i > lo) t = fma(col[i], col[i], t);
+  }
+  return t;
+}
+
+template <int RPW>
+__device__ __forceinline__ double col_at(const double (&col)[RPW], int lo) {
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i)
+    if (i == lo) v = col[i];
+  return v;
+}
+
+// v = x(k+1:) * scale in place below the diagonal, beta on it; publish v (v_k = 1, zeros
+// above) to the warp's rows of vb
+template <int RPW>
+__device__ __forceinline__ void make_reflector(double (&col)[RPW], int lo, double scale,
+                                               double beta, double* vb) {
+  if (lo < 0) {
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const double nv = col[i] * scale;
+      col[i] = nv;
+      vb[i] = nv;
+    }
+  } else if (lo < RPW) {
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      if (i > lo) {
+        const double nv = col[i] * scale;
+        col[i] = nv;
+        vb[i] = nv;
+      } else if (i == lo) {
+        col[i] = beta;
+        vb[i] = 1.0;
+      } else {
+        vb[i] = 0.0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) vb[i] = 0.0;
+  }
+}
+
+template <int RPW>
+__device__ __forceinline__ void swap_cols(double (&a)[2][RPW], int k, int p) {
+  const int l = threadIdx.x & 31, ol = k & 31, os = k >> 5, pl = p & 31, ps = p >> 5;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const double vk = __shfl_sync(0xffffffffu, os ? a[1][i] : a[0][i], ol);
+    const double vp = __shfl_sync(0xffffffffu, ps ? a[1][i] : a[0][i], pl);
+    if (l == ol) {
+      if (os)
+        a[1][i] = vp;
+      else
+        a[0][i] = vp;
+    }
+    if (l == pl) {
+      if (ps)
+        a[1][i] = vk;
+      else
+        a[0][i] = vk;
+    }
+  }
+}
+
+// Householder QR of the register panel a (m x s; rows >= m are zero).  LAPACK dlarfg
+// convention: H_k = I - tau v v^T, v_k = 1, beta = -sign(alpha) ||x||.  On exit a holds R on
+// and above the diagonal and v below it; q.tau[k] the scalars.  With pivot, columns are
+// exchanged (largest norm below row k first, first index on ties; norms recomputed exactly
+// every step) and q.piv receives the permutation (pivoting only permutes R's columns, so
+// the left singular vectors are unaffected).
+template <int RPW>
+__device__ void reg_qr(double (&a)[2][RPW], int m, int s, const QSmem& q, bool pivot) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
   const int kmax = min(m, s);
-  auto make_reflector = [&](int k) {  // executed by the owner warp of column k
-    if (piv) {  // pick the pivot among columns k..s-1 and swap it into k
+  if (pivot && threadIdx.x < 64) q.piv[threadIdx.x] = threadIdx.x;
+  for (int k = 0; k < kmax; ++k) {
+    const int ol = k & 31, os = k >> 5, lo = k - row0;
+    double alpha, ss;
+    if (pivot) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = l + 32 * j;
+        if (c >= k && c < s) {
+          q.part[w * 64 + c] = col_norm_below(a[j], lo);
+          if (lo >= 0 && lo < RPW) q.rowk[c] = col_at(a[j], lo);
+        }
+      }
+      __syncthreads();
+      if ((int)threadIdx.x >= k && (int)threadIdx.x < s) {
+        const int c = threadIdx.x;
+        double t = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kQWarps; ++w2) t += q.part[w2 * 64 + c];
+        q.red[c] = t;
+        q.cn[c] = fma(q.rowk[c], q.rowk[c], t);
+      }
+      __syncthreads();
       double best = -1.0;
       int p = k;
-      for (int c = k + lane; c < s; c += 32) {
-        if (cn[c] > best) {
-          best = cn[c];
+      for (int c = k + l; c < s; c += 32) {
+        const double v = q.cn[c];
+        if (v > best) {
+          best = v;
           p = c;
         }
       }
 #pragma unroll
       for (int msk = 16; msk >= 1; msk >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, msk);
-        int op = __shfl_xor_sync(0xffffffffu, p, msk);
+        const double ob = __shfl_xor_sync(0xffffffffu, best, msk);
+        const int op = __shfl_xor_sync(0xffffffffu, p, msk);
         if (ob > best || (ob == best && op < p)) {
           best = ob;
           p = op;
         }
       }
-      if (p != k) {
-        double* ck = A + (size_t)lda * k;
-        double* cp = A + (size_t)lda * p;
-        for (int i = lane; i < m; i += 32) {
-          double t = ck[i];
-          ck[i] = cp[i];
-          cp[i] = t;
+      if (p != k) {  // exchange columns k and p in every warp's rows
+        swap_cols(a, k, p);
+        if (threadIdx.x == 0) {
+          const int t = q.piv[k];
+          q.piv[k] = q.piv[p];
+          q.piv[p] = t;
         }
-        if (lane == 0) {
-          double t = cn[k];
-          cn[k] = cn[p];
-          cn[p] = t;
-          int ti = piv[k];
-          piv[k] = piv[p];
-          piv[p] = ti;
-        }
-        __syncwarp();
       }
-    }
-    double* col = A + (size_t)lda * k;
-    double ss = warp_sum(lane_dot(col, col, k + 1 + lane, m));
-    const double alpha = col[k];
-    double t = 0.0;
-    if (ss != 0.0) {
-      const double beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-      t = (beta - alpha) / beta;
-      const double scale = 1.0 / (alpha - beta);
-      for (int i = k + 1 + lane; i < m; i += 32) col[i] *= scale;
-      __syncwarp();
-      if (lane == 0) col[k] = beta;
-    }
-    if (lane == 0) tau[k] = t;
-    __syncwarp();
-  };
-  if (piv) {
-    for (int c = warp; c < s; c += kOrthWarps) {
-      const double* col = A + (size_t)lda * c;
-      double a = warp_sum(lane_dot(col, col, lane, m));
-      if (lane == 0) {
-        cn[c] = a;
-        piv[c] = c;
+      alpha = q.rowk[p];
+      ss = q.red[p];
+    } else {
+      if (l == ol) {
+        const double t = os ? col_norm_below(a[1], lo) : col_norm_below(a[0], lo);
+        if (lo >= 0 && lo < RPW) q.rowk[0] = os ? col_at(a[1], lo) : col_at(a[0], lo);
+        q.normp[w] = t;
       }
-    }
-    __syncthreads();
-  }
-  if (kmax > 0 && warp == 0) make_reflector(0);
-  __syncthreads();
-  for (int k = 0; k < kmax; ++k) {
-    const double* v = A + (size_t)lda * k;
-    const double tk = tau[k];
-    for (int c = warp; c < s; c += 32) {
-      if (c <= k) continue;
-      double* col = A + (size_t)lda * c;
-      if (tk != 0.0) {
-        double d = warp_sum(lane_dot(v, col, k + 1 + lane, m));
-        d += col[k];
-        const double f = tk * d;
-        double nn = 0.0;
-#pragma unroll 4
-        for (int i = k + 1 + lane; i < m; i += 32) {
-          double val = col[i] - f * v[i];
-          col[i] = val;
-          nn += val * val;
-        }
-        __syncwarp();
-        if (lane == 0) col[k] -= f;
-        if (piv) {
-          nn = warp_sum(nn);
-          if (lane == 0) cn[c] = nn;
-        }
-        __syncwarp();
-      } else if (piv) {
-        double nn = warp_sum(lane_dot(col, col, k + 1 + lane, m));
-        if (lane == 0) cn[c] = nn;
-        __syncwarp();
-      }
-      if (c == k + 1 && k + 1 < kmax && !piv) make_reflector(k + 1);
-    }
-    __syncthreads();
-    if (piv && k + 1 < kmax) {  // the pivot needs every column's updated norm
-      if (warp == (k + 1) % 32) make_reflector(k + 1);
       __syncthreads();
+      // fixed-order tree over the 16 warp partials, identical in every warp
+      double t = l < kQWarps ? q.normp[l] : 0.0;
+      t += __shfl_xor_sync(0xffffffffu, t, 8);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      ss = __shfl_sync(0xffffffffu, t, 0);
+      alpha = q.rowk[0];
     }
-  }
-}
-
-// Y (m x mu, ld ldy, shared) <- Q Y with Q = H_0 H_1 ... H_{kmax-1} from (V, tau) in shared
-// memory.  Each warp owns whole columns of Y, so no block barrier between reflectors.
-__device__ void apply_q(const double* V, int ldv, const double* tau, int m, int s, double* Y,
-                        int ldy, int mu, int k_hi, int k_lo) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = warp; c < mu; c += kOrthWarps) {
-    double* y = Y + (size_t)ldy * c;
-    for (int k = k_hi - 1; k >= k_lo; --k) {
-      const double tk = tau[k];
-      if (tk == 0.0) continue;
-      const double* v = V + (size_t)ldv * (k - k_lo);
-      double d = warp_sum(lane_dot(v, y, k + 1 + lane, m));
-      d += y[k];
-      const double f = tk * d;
-#pragma unroll 4
-      for (int i = k + 1 + lane; i < m; i += 32) y[i] -= f * v[i];
-      __syncwarp();
-      if (lane == 0) y[k] -= f;
-      __syncwarp();
+    double beta = alpha, tk = 0.0, scale = 0.0;
+    if (ss != 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+      tk = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
     }
-  }
-}
-
-// argmax |y| with the reference's scan semantics (strict >, first index wins);
-// all-zero column -> index 0 with value 0.
-__device__ void warp_argmax(const double* y, int m, double& best, int& imax) {
-  const int lane = threadIdx.x & 31;
-  best = 0.0;
-  imax = 0;
-  bool found = false;
-  for (int i = lane; i < m; i += 32) {
-    double a = fabs(y[i]);
-    if (a > best) {
-      best = a;
-      imax = i;
-      found = true;
+    if (l == ol) {  // the owner lane forms v (in place below the diagonal) and publishes it
+      if (os)
+        make_reflector(a[1], lo, scale, beta, q.vbuf + row0);
+      else
+        make_reflector(a[0], lo, scale, beta, q.vbuf + row0);
     }
-  }
-  if (!found) imax = 0x7fffffff;
+    if (threadIdx.x == 0) q.tau[k] = tk;
+    __syncthreads();
+    if (tk != 0.0) {
+      const bool done = lo >= RPW;  // all of this warp's rows are above row k: v is zero here
+      double vr[RPW];
+      if (!done) {
 #pragma unroll
-  for (int msk = 16; msk >= 1; msk >>= 1) {
-    double ob = __shfl_xor_sync(0xffffffffu, best, msk);
-    int oi = __shfl_xor_sync(0xffffffffu, imax, msk);
-    if (ob > best || (ob == best && oi < imax)) {
-      best = ob;
-      imax = oi;
+        for (int i = 0; i < RPW; ++i) vr[i] = q.vbuf[row0 + i];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = l + 32 * j;
+        if (c > k && c < s) {
+          double t = 0.0;
+          if (!done) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) t = fma(vr[i], a[j][i], t);
+          }
+          q.part[w * 64 + c] = t;
+        }
+      }
+      __syncthreads();
+      if ((int)threadIdx.x > k && (int)threadIdx.x < s) {
+        const int c = threadIdx.x;
+        double t = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kQWarps; ++w2) t += q.part[w2 * 64 + c];
+        q.fval[c] = tk * t;
+      }
+      __syncthreads();
+      if (!done) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = l + 32 * j;
+          if (c > k && c < s) {
+            const double f = q.fval[c];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) a[j][i] = fma(-f, vr[i], a[j][i]);
+          }
+        }
+      }
     }
   }
-  if (best == 0.0) imax = 0;
 }
 
-// One-sided Jacobi on G (s x n, ld s; n even, column n-1 may be a zero pad); the same
-// rotations are applied to the columns of J (n x n, ld n).  Round-robin (circle)
-// ordering: n/2 disjoint pairs per round.  A quad of 4 lanes owns one pair (8 pairs per
-// warp, rows strided by 4): the rotation math is done once per pair instead of once per
-// warp lane-replicated, which keeps the SM's issue slots free (ncu: the warp-per-pair
-// version was issue-bound at 58% slot use on instruction count, not latency).
+// y <- H_{k_lo} H_{k_lo+1} ... H_{k_hi-1} y  (reflectors applied last to first).
+// Vs: the block's reflectors (v_k below row k of column k, ld ldv), rows >= m of Vs zero,
+// ldv >= 16 * RPW; tau in smem.
+template <int RPW>
+__device__ void reg_apply(double (&y)[2][RPW], int mu, const double* Vs, int ldv,
+                          const double* tau, int k_hi, int k_lo, const QSmem& q) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+  for (int k = k_hi - 1; k >= k_lo; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const int lo = k - row0;
+    const bool done = lo >= RPW;
+    double vr[RPW];
+    if (lo < 0) {
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) vr[i] = Vs[row0 + i + (size_t)ldv * k];
+    } else if (!done) {
+#pragma unroll
+      for (int i = 0; i < RPW; ++i)
+        vr[i] = i > lo ? Vs[row0 + i + (size_t)ldv * k] : (i == lo ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = l + 32 * j;
+      if (c < mu) {
+        double t = 0.0;
+        if (!done) {
+#pragma unroll
+          for (int i = 0; i < RPW; ++i) t = fma(vr[i], y[j][i], t);
+        }
+        q.part[w * 64 + c] = t;
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < mu) {
+      const int c = threadIdx.x;
+      double t = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < kQWarps; ++w2) t += q.part[w2 * 64 + c];
+      q.fval[c] = tk * t;
+    }
+    __syncthreads();
+    if (!done) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = l + 32 * j;
+        if (c < mu) {
+          const double f = q.fval[c];
+#pragma unroll
+          for (int i = 0; i < RPW; ++i) y[j][i] = fma(-f, vr[i], y[j][i]);
+        }
+      }
+    }
+  }
+}
+
+// Per-column argmax |y| over this CTA's rows with the reference's scan semantics (strict >,
+// first index wins): thread partials over its rows, combined in warp (= row) order by
+// threads c < mu into best[c] / bidx[c] (bidx = -1 if the column is all zero here).
+template <int RPW>
+__device__ void reg_argmax(const double (&y)[2][RPW], int m, int mu, const QSmem& q,
+                           double* best, int* bidx) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = l + 32 * j;
+    if (c < mu) {
+      double b = 0.0;
+      int bi = -1;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const double v = fabs(y[j][i]);
+        if (row0 + i < m && v > b) {
+          b = v;
+          bi = row0 + i;
+        }
+      }
+      q.pval[w * 64 + c] = b;
+      q.pidx[w * 64 + c] = bi;
+    }
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < mu) {
+    const int c = threadIdx.x;
+    double b = 0.0;
+    int bi = -1;
+    for (int w2 = 0; w2 < kQWarps; ++w2) {
+      const double v = q.pval[w2 * 64 + c];
+      if (v > b) {
+        b = v;
+        bi = q.pidx[w2 * 64 + c];
+      }
+    }
+    best[c] = b;
+    bidx[c] = bi;
+  }
+  __syncthreads();
+}
+
+// coalesced global (rows x cols, ld lda) -> shared tile (ld ldt), rows [rows, prow) zeroed
+__device__ __forceinline__ void load_tile(const double* __restrict__ g, long long lda, int rows,
+                                          int cols, double* t, int ldt, int prow) {
+  for (int e = threadIdx.x; e < rows * cols; e += kQThreads) {
+    const int i = e % rows, c = e / rows;
+    t[i + ldt * c] = g[i + (size_t)lda * c];
+  }
+  const int pad = prow - rows;
+  for (int e = threadIdx.x; e < pad * cols; e += kQThreads) {
+    const int i = e % pad, c = e / pad;
+    t[rows + i + ldt * c] = 0.0;
+  }
+}
+
+template <int RPW>
+__device__ __forceinline__ void tile_to_regs(const double* t, int ldt, int rows, int cols,
+                                             double (&a)[2][RPW]) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = l + 32 * j;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = row0 + i;
+      a[j][i] = (r < rows && c < cols) ? t[r + ldt * c] : 0.0;
+    }
+  }
+}
+
+template <int RPW>
+__device__ __forceinline__ void regs_to_tile(const double (&a)[2][RPW], int rows, int cols,
+                                             double* t, int ldt) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = l + 32 * j;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = row0 + i;
+      if (r < rows && c < cols) t[r + ldt * c] = a[j][i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One-sided Jacobi on G = R^T (s x 64, zero columns >= s), rotations accumulated in J.
+//
+// Register-resident with a recursive pair ordering.  The 64 column slots are the (top,
+// bottom) registers of the 32 lanes; lane j rotates the pair (top_j, bottom_j).  Warps 0-7
+// hold 8 rows each of G, warps 8-15 8 rows each of J, so a rotation is lane-local and the
+// pair's dot products are per-warp partials combined by warp 0 (fixed warp order).  The
+// schedule: within groups of g lanes (g = 32, 16, ..., 1) the bottoms shift cyclically by
+// one lane per round for g rounds (every top meets every bottom of its group), then each
+// group splits in halves whose tops pair with tops and bottoms with bottoms (one XOR
+// shuffle).  63 rounds cover all 2016 slot pairs; each round moves one register column
+// per lane by a shuffle instead of reloading both columns of every pair from shared memory
+// (the previous round-robin version was bound on shared-memory bandwidth at ~1900 cycles a
+// round).  Offline simulation on the cfg4 sketches: 7-8 sweeps, as with round-robin.
+// ---------------------------------------------------------------------------
 __device__ int g_jacobi_sweeps;
 #ifdef LMRA_JACOBI_CLOCKS
-__device__ unsigned long long g_jclk[8];
+__device__ unsigned long long g_jclk[8];  // microbenchmark only: per-phase cycles, warp 0
 #endif
 
-// One round of the parallel one-sided Jacobi: LPP lanes own one column pair, each lane
-// holds R = ceil(s / LPP) rows of both columns (and of the two J columns) in registers;
-// the loops are fully unrolled so a lane's loads issue together (the runtime-trip-count
-// smem loops of the first version serialised on load latency: ~3000 cycles per round).
-template <int LPP, int R>
-__device__ void jacobi_round(double* G, int s, int n, double* J, int* flag, double tol2,
-                             const unsigned char* pairs) {
-  const int lane = threadIdx.x & 31, sub = lane & (LPP - 1);
-  const int pair = threadIdx.x / LPP;
-  if (pair >= n / 2) return;
-  const unsigned gmask = LPP == 32 ? 0xffffffffu : (((1u << LPP) - 1u) << (lane & ~(LPP - 1)));
-  const int p = pairs[2 * pair], q = pairs[2 * pair + 1];
-  double* gp = G + (size_t)s * p;
-  double* gq = G + (size_t)s * q;
-  double x[R], y[R];
-#ifdef LMRA_JACOBI_CLOCKS
-  long long tc0 = clock64();
-#endif
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = sub + r * LPP;
-    x[r] = i < s ? gp[i] : 0.0;
-    y[r] = i < s ? gq[i] : 0.0;
-  }
-  double a = 0.0, b = 0.0, c = 0.0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    a = fma(x[r], x[r], a);
-    b = fma(y[r], y[r], b);
-    c = fma(x[r], y[r], c);
-  }
-#pragma unroll
-  for (int m = 1; m < LPP; m <<= 1) {
-    a += __shfl_xor_sync(gmask, a, m);
-    b += __shfl_xor_sync(gmask, b, m);
-    c += __shfl_xor_sync(gmask, c, m);
-  }
-#ifdef LMRA_JACOBI_CLOCKS
-  long long tc1 = clock64();
-#endif
-  // rotate while c^2 > tol^2 a b (no sqrt); huge norms take an exponent-scaled path
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Rotation for the pair (top, bottom) with squared norms a, b and inner product c: the
+// smaller root t of t^2 + 2 zeta t - 1 = 0 (zeta = (b - a) / 2c), written without forming
+// t: with d = b - a, r = sqrt(d^2 + 4c^2), u = |d| + r:  1 + t^2 = 2r / u, so
+//   cos = u / sqrt(2 r u),  sin = sign(d) 2c / sqrt(2 r u)
+// (one sqrt and one rsqrt on the chain instead of sqrt, reciprocal and rsqrt).
+__device__ __forceinline__ bool jacobi_angle(double a, double b, double c, double tol2,
+                                             double& cs, double& sn) {
   bool rot;
   double sa = a, sb = b, sc = c;
   if (fmax(a, b) < 1e150) {
     rot = c != 0.0 && c * c > tol2 * (a * b);
-  } else {
+  } else {  // huge norms: exponent-scaled
     const int ea = ilogb(fmax(fmax(a, b), fabs(c)));
     sa = ldexp(a, -ea);
     sb = ldexp(b, -ea);
     sc = ldexp(c, -ea);
     rot = c != 0.0 && sc * sc > tol2 * (sa * sb);
   }
-  if (!rot) return;
-  // smaller root of t^2 + 2 zeta t - 1 = 0, zeta = (b - a) / (2c):
-  //   t = sign(d) 2c / (|d| + sqrt(d^2 + 4c^2)),  d = b - a;
-  // sqrt, reciprocal and rsqrt on the critical path (~100 + 80 + 75 cycles, measured).
-  const double d = sb - sa;
-  const double t = (d >= 0.0 ? 2.0 * sc : -2.0 * sc) * __drcp_rn(fabs(d) + sqrt(fma(d, d, 4.0 * sc * sc)));
-  const double cs = rsqrt(fma(t, t, 1.0));
-  const double sn = cs * t;
-#ifdef LMRA_JACOBI_CLOCKS
-  long long tc2 = clock64();
-#endif
-  double* jp = J + (size_t)n * p;
-  double* jq = J + (size_t)n * q;
-  double u[R], w[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = sub + r * LPP;
-    u[r] = i < n ? jp[i] : 0.0;
-    w[r] = i < n ? jq[i] : 0.0;
+  cs = 1.0;
+  sn = 0.0;
+  if (rot) {
+    const double d = sb - sa;
+    const double r = sqrt(fma(d, d, 4.0 * sc * sc));
+    const double u = fabs(d) + r;
+    const double qn = rsqrt(2.0 * r * u);
+    cs = u * qn;
+    sn = (d >= 0.0 ? 2.0 * sc : -2.0 * sc) * qn;
   }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = sub + r * LPP;
-    if (i < s) {
-      gp[i] = cs * x[r] - sn * y[r];
-      gq[i] = sn * x[r] + cs * y[r];
-    }
-    if (i < n) {
-      jp[i] = cs * u[r] - sn * w[r];
-      jq[i] = sn * u[r] + cs * w[r];
-    }
-  }
-  if (sub == 0) *flag = 1;
-#ifdef LMRA_JACOBI_CLOCKS
-  if (pair == 0 && sub == 0) {
-    long long tc3 = clock64();
-    g_jclk[0] += tc1 - tc0;
-    g_jclk[1] += tc2 - tc1;
-    g_jclk[2] += tc3 - tc2;
-    g_jclk[3] += 1;
-  }
-#endif
+  return rot;
 }
 
-// One-sided Jacobi on G (s x n, ld s; n even, column n-1 may be a zero pad); the same
-// rotations are applied to the columns of J (n x n, ld n).  Round-robin (circle)
-// ordering, n/2 disjoint pairs per round; `pairs` is smem scratch of n*(n-1) bytes.
-__device__ bool one_sided_jacobi(double* G, int s, int n, double* J, int* flag, double tol,
-                                 unsigned char* pairs) {
-  const double tol2 = tol * tol;
-  for (int e = threadIdx.x; e < (n - 1) * (n / 2); e += blockDim.x) {
-    const int round = e / (n / 2), k = e % (n / 2);
-    int p, q;
-    if (k == 0) {
-      p = n - 1;
-      q = round;
+__device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem& q) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const bool isG = w < 8;
+  const int row0 = (w & 7) * 8;
+  double* part = q.part;  // [3][8 warps][32 lanes]
+  double* csn = q.fval;   // [round parity][cos 32 | sin 32]: q.fval and q.rowk (128 doubles)
+  int* flags = q.pidx;    // per-sweep "rotated" flags
+  double T[8], B[8];
+  int cT = l, cB = l + 32;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = row0 + i;
+    if (isG) {
+      T[i] = (r < s && cT < s) ? G[r + (size_t)s * cT] : 0.0;
+      B[i] = (r < s && cB < s) ? G[r + (size_t)s * cB] : 0.0;
     } else {
-      p = (round + k) % (n - 1);
-      q = (round - k + (n - 1)) % (n - 1);
+      T[i] = r == cT ? 1.0 : 0.0;
+      B[i] = r == cB ? 1.0 : 0.0;
     }
-    pairs[2 * e] = (unsigned char)min(p, q);
-    pairs[2 * e + 1] = (unsigned char)max(p, q);
   }
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (threadIdx.x == 0) *flag = 0;
-    __syncthreads();
-    for (int round = 0; round < n - 1; ++round) {
-      const unsigned char* pr = pairs + (size_t)round * n;
-      if (s <= 16)
-        jacobi_round<4, 4>(G, s, n, J, flag, tol2, pr);
-      else if (s <= 32)
-        jacobi_round<8, 4>(G, s, n, J, flag, tol2, pr);
+  if (threadIdx.x < 64) flags[threadIdx.x] = 0;
+  __syncthreads();
+  const double tol2 = tol * tol;
+  bool converged = false;
+  int round = 0;  // global round counter (csn parity)
+  // G warps: [rotate with round r-1 | shift | partials r] -> bar A (G warps) -> warp 0 angles
+  // -> bar B (all).  J warps only wait at bar B and apply round r while the G warps and
+  // warp 0 work on round r + 1, so the J rotations are off the critical path.
+  for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
+    for (int group = 32;; group >>= 1) {
+      const int src = (l & ~(group - 1)) | ((l + 1) & (group - 1));
+      for (int r = 0; r < group; ++r, ++round) {
+        double* cs_r = csn + 64 * (round & 1);
+#ifdef LMRA_JACOBI_CLOCKS
+        const long long k0 = clock64();
+        long long k1 = k0, k2 = k0;
+#endif
+        if (isG) {
+          double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            a = fma(T[i], T[i], a);
+            b = fma(B[i], B[i], b);
+            c = fma(T[i], B[i], c);
+          }
+          part[(0 * 8 + w) * 32 + l] = a;
+          part[(1 * 8 + w) * 32 + l] = b;
+          part[(2 * 8 + w) * 32 + l] = c;
+          named_bar(1, 256);
+#ifdef LMRA_JACOBI_CLOCKS
+          k1 = clock64();
+#endif
+          if (w == 0) {
+            double pa[8], pb[8], pc[8];
+#pragma unroll
+            for (int w2 = 0; w2 < 8; ++w2) {
+              pa[w2] = part[(0 * 8 + w2) * 32 + l];
+              pb[w2] = part[(1 * 8 + w2) * 32 + l];
+              pc[w2] = part[(2 * 8 + w2) * 32 + l];
+            }
+            const double sa = ((pa[0] + pa[1]) + (pa[2] + pa[3])) + ((pa[4] + pa[5]) + (pa[6] + pa[7]));
+            const double sb = ((pb[0] + pb[1]) + (pb[2] + pb[3])) + ((pb[4] + pb[5]) + (pb[6] + pb[7]));
+            const double sc = ((pc[0] + pc[1]) + (pc[2] + pc[3])) + ((pc[4] + pc[5]) + (pc[6] + pc[7]));
+            double cs, sn;
+            if (jacobi_angle(sa, sb, sc, tol2, cs, sn)) flags[sweep] = 1;
+            cs_r[l] = cs;
+            cs_r[32 + l] = sn;
+          }
+#ifdef LMRA_JACOBI_CLOCKS
+          k2 = clock64();
+#endif
+        }
+        __syncthreads();  // bar B: angles of this round visible to every warp
+#ifdef LMRA_JACOBI_CLOCKS
+        const long long k3 = clock64();
+#endif
+        const double cs = cs_r[l], sn = cs_r[32 + l];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double x = T[i], y = B[i];
+          T[i] = cs * x - sn * y;
+          B[i] = sn * x + cs * y;
+        }
+        // bottoms move one lane down their group (cyclically)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) B[i] = __shfl_sync(0xffffffffu, B[i], src);
+        cB = __shfl_sync(0xffffffffu, cB, src);
+#ifdef LMRA_JACOBI_CLOCKS
+        if (threadIdx.x == 0) {  // k0->k1 partials + bar A, k1->k2 angles, k2->k3 bar B, k3->k4 rotate
+          const long long k4 = clock64();
+          g_jclk[0] += k1 - k0;
+          g_jclk[1] += k2 - k1;
+          g_jclk[2] += k3 - k2;
+          g_jclk[3] += k4 - k3;
+          g_jclk[4] += 1;
+        }
+        if (threadIdx.x == 256) {  // a J warp: bar B wait and its rotation
+          const long long k4 = clock64();
+          g_jclk[5] += k3 - k0;
+          g_jclk[6] += k4 - k3;
+        }
+#endif
+      }
+      if (group == 1) break;
+      // split: first-half tops pair with second-half tops, bottoms with bottoms
+      const int h = group >> 1;
+      const bool second = (l & h) != 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double tp = __shfl_xor_sync(0xffffffffu, T[i], h);
+        const double bp = __shfl_xor_sync(0xffffffffu, B[i], h);
+        if (second)
+          T[i] = bp;
+        else
+          B[i] = tp;
+      }
+      const int ctp = __shfl_xor_sync(0xffffffffu, cT, h);
+      const int cbp = __shfl_xor_sync(0xffffffffu, cB, h);
+      if (second)
+        cT = cbp;
       else
-        jacobi_round<16, 4>(G, s, n, J, flag, tol2, pr);
-      __syncthreads();
+        cB = ctp;
     }
-    const int f = *flag;
-    __syncthreads();
-    if (!f) {
+    // flags[sweep] was written before the sweep's last bar B
+    if (!flags[sweep]) {
+      converged = true;
       if (threadIdx.x == 0) g_jacobi_sweeps = sweep + 1;
-      return true;
     }
   }
-  return false;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = row0 + i;
+    if (isG) {
+      if (r < s) {
+        if (cT < s) G[r + (size_t)s * cT] = T[i];
+        if (cB < s) G[r + (size_t)s * cB] = B[i];
+      }
+    } else {
+      J[r + 64 * cT] = T[i];
+      J[r + 64 * cB] = B[i];
+    }
+  }
+  __syncthreads();
+  return converged;
 }
 
 // ---------------------------------------------------------------------------
-// Phase A: QR of row block b of A (m x s, lda) -> reflectors into V (same rows),
-// tau[b*s + k], R_b into rows [b*s, b*s+s) of S (ld lds), zeros below the diagonal.
+// Leaf QR: block b of A (m x s, lda) -> reflectors into V (same rows), tau[b*s + k],
+// R_b into rows [b*s, b*s+s) of S (ld lds), zeros below the diagonal.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kOrthThreads) orth_block_qr_kernel(
+template <int RPW>
+__global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
     const double* __restrict__ A, long long m, int s, int lda, int nb, double* __restrict__ V,
     double* __restrict__ tau, double* __restrict__ S, int lds) {
   extern __shared__ __align__(16) double sm[];
+  const QSmem q = carve_q(sm);
+  double* tile = sm + kQScratchBytes / 8;
   const int b = blockIdx.x;
   const long long r0 = (m * b) / nb, r1 = (m * (b + 1)) / nb;
-  const int rows = (int)(r1 - r0);
-  double* W = sm;                      // rows x s
-  double* t = sm + (size_t)rows * s;   // s
-  for (int e = threadIdx.x; e < rows * s; e += kOrthThreads) {
-    int i = e % rows, c = e / rows;
-    W[e] = A[r0 + i + (size_t)lda * c];
-  }
+  const int rows = (int)(r1 - r0), ldt = rows | 1;
+  load_tile(A + r0, lda, rows, s, tile, ldt, rows);
   __syncthreads();
-  block_householder_qr(W, rows, s, rows, t, nullptr, nullptr);
+  double a[2][RPW];
+  tile_to_regs(tile, ldt, rows, s, a);
+  reg_qr(a, rows, s, q, false);
+  regs_to_tile(a, rows, s, tile, ldt);
   __syncthreads();
-  for (int e = threadIdx.x; e < rows * s; e += kOrthThreads) {
-    int i = e % rows, c = e / rows;
-    V[r0 + i + (size_t)lda * c] = W[e];
+  for (int e = threadIdx.x; e < rows * s; e += kQThreads) {
+    const int i = e % rows, c = e / rows;
+    V[r0 + i + (size_t)lda * c] = tile[i + ldt * c];
   }
-  for (int e = threadIdx.x; e < s * s; e += kOrthThreads) {
-    int i = e % s, c = e / s;
-    S[(size_t)b * s + i + (size_t)lds * c] = (i <= c && i < rows) ? W[i + (size_t)rows * c] : 0.0;
+  for (int e = threadIdx.x; e < s * s; e += kQThreads) {
+    const int i = e % s, c = e / s;
+    S[(size_t)b * s + i + (size_t)lds * c] = (i <= c && i < rows) ? tile[i + ldt * c] : 0.0;
   }
-  for (int k = threadIdx.x; k < s; k += kOrthThreads) tau[(size_t)b * s + k] = k < rows ? t[k] : 0.0;
+  for (int k = threadIdx.x; k < s; k += kQThreads) tau[(size_t)b * s + k] = k < min(rows, s) ? q.tau[k] : 0.0;
 }
 
 // ---------------------------------------------------------------------------
-// Phase B: one CTA. S (m x s, lds) -> pivoted QR -> Jacobi on R^T -> Y = Q [U_R(:, :mu); 0].
+// Core: one CTA.  S (m x s, lds) -> pivoted QR -> Jacobi on R^T -> Y = Q [U_R(:, :mu); 0].
 // final != 0: sign-fix Y and write it to out (ld ldo); else write Y to out unsigned.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kOrthThreads) orth_core_kernel(
+template <int RPW>
+__global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
     int ldo, int final_level, int* status, double jacobi_tol) {
   extern __shared__ __align__(16) double sm[];
-  const int n = s + (s & 1);  // even column count for the tournament
-  double* A = sm;                                   // m x s
-  double* Y = A + (size_t)m * s;                    // m x mu
-  double* G = Y + (size_t)m * mu;                   // s x n   (R^T, padded)
-  double* J = G + (size_t)s * n;                    // n x n   (accumulated rotations)
-  double* tau = J + (size_t)n * n;                  // s
-  double* cn = tau + s;                             // s
-  double* sig = cn + s;                             // n
-  int* piv = reinterpret_cast<int*>(sig + n);       // s
-  int* perm = piv + s;                              // n
-  int* flag = perm + n;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const QSmem q = carve_q(sm);
+  const int n = 64;  // Jacobi column slots (zero columns beyond s)
+  const int ldv = (kQWarps * RPW) | 1;
+  double* Vs = sm + kQScratchBytes / 8;        // m x s (ld ldv): input, then reflectors, then Y
+  double* G = Vs + (size_t)ldv * s;            // s x s   (R^T)
+  double* J = G + (size_t)s * s;               // n x n   (accumulated rotations)
+  double* sig = J + (size_t)n * n;             // n
+  int* perm = reinterpret_cast<int*>(sig + n); // n
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 
-  for (int e = threadIdx.x; e < m * s; e += kOrthThreads) {
-    int i = e % m, c = e / m;
-    A[e] = S[i + (size_t)lds * c];
+  load_tile(S, lds, m, s, Vs, ldv, kQWarps * RPW);
+  __syncthreads();
+  double a[2][RPW];
+  tile_to_regs(Vs, ldv, m, s, a);
+  reg_qr(a, m, s, q, true);
+  // G = R^T (lower triangle) with a zero pad column, reflectors back to Vs, J = I
+  {
+    const int row0 = w * RPW;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = l + 32 * j;
+      if (c >= s) continue;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int r = row0 + i;
+        if (r < s) G[c + (size_t)s * r] = r <= c && r < m ? a[j][i] : 0.0;
+        if (r > c && r < m) Vs[r + (size_t)ldv * c] = a[j][i];
+      }
+    }
   }
   __syncthreads();
-  block_householder_qr(A, m, s, m, tau, piv, cn);
-  __syncthreads();
-  // G = R^T (s x s lower triangle), zero pad column; J = I
-  for (int e = threadIdx.x; e < s * n; e += kOrthThreads) {
-    int i = e % s, j = e / s;  // G[i, j] = R[j, i]
-    G[e] = (j < s && j <= i && j < m) ? A[j + (size_t)m * i] : 0.0;
-  }
-  for (int e = threadIdx.x; e < n * n; e += kOrthThreads) J[e] = (e % n == e / n) ? 1.0 : 0.0;
-  __syncthreads();
-  const bool converged =
-      one_sided_jacobi(G, s, n, J, flag, jacobi_tol, reinterpret_cast<unsigned char*>(flag + 1));
+  const bool converged = reg_jacobi(G, s, J, jacobi_tol, q);
   // singular values = column norms of G, fixed order
-  for (int c = warp; c < n; c += kOrthWarps) {
-    double a = 0.0;
-    for (int i = lane; i < s; i += 32) a += G[i + (size_t)s * c] * G[i + (size_t)s * c];
-    a = warp_sum(a);
-    if (lane == 0) sig[c] = sqrt(a);
+  for (int c = w; c < s; c += kQWarps) {
+    double t = 0.0;
+    for (int i = l; i < s; i += 32) t += G[i + (size_t)s * c] * G[i + (size_t)s * c];
+    t = warp_sum(t);
+    if (l == 0) sig[c] = sqrt(t);
   }
   __syncthreads();
-  if (threadIdx.x < s) {  // stable descending order of the s real columns (pad excluded)
+  if ((int)threadIdx.x < s) {  // stable descending order of the s real columns (pad excluded)
     const int c = threadIdx.x;
     const double v = sig[c];
     int rank = 0;
@@ -449,87 +725,94 @@ __global__ void __launch_bounds__(kOrthThreads) orth_core_kernel(
     perm[rank] = c;
   }
   __syncthreads();
-  // Y = [U_R(:, :mu) ; 0] with U_R = J(0:s, perm)
-  for (int e = threadIdx.x; e < m * mu; e += kOrthThreads) {
-    int i = e % m, c = e / m;
-    Y[e] = i < s ? J[i + (size_t)n * perm[c]] : 0.0;
-  }
-  __syncthreads();
-  apply_q(A, m, tau, m, s, Y, m, mu, min(m, s), 0);
-  __syncthreads();
-  if (final_level) {
-    for (int c = warp; c < mu; c += kOrthWarps) {
-      double best;
-      int imax;
-      warp_argmax(Y + (size_t)m * c, m, best, imax);
-      const bool flip = Y[imax + (size_t)m * c] < 0.0;
-      __syncwarp();
-      for (int i = lane; i < m; i += 32) {
-        double val = Y[i + (size_t)m * c];
-        out[i + (size_t)ldo * c] = flip ? -val : val;
+  // Y = [U_R(:, :mu) ; 0] with U_R = J(0:s, perm), then the reflectors
+  double y[2][RPW];
+  {
+    const int row0 = w * RPW;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = l + 32 * j;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int r = row0 + i;
+        y[j][i] = (c < mu && r < s && r < m) ? J[r + (size_t)n * perm[c]] : 0.0;
       }
     }
+  }
+  reg_apply(y, mu, Vs, ldv, q.tau, min(m, s), 0, q);
+  __syncthreads();
+  if (final_level) {
+    reg_argmax(y, m, mu, q, q.red, q.piv);  // best |.| per column in q.red, row in q.piv
+    regs_to_tile(y, m, mu, Vs, ldv);
+    __syncthreads();
+    if ((int)threadIdx.x < mu) {
+      const int c = threadIdx.x, im = q.piv[c];
+      q.fval[c] = (im >= 0 && Vs[im + (size_t)ldv * c] < 0.0) ? -1.0 : 1.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * mu; e += kQThreads) {
+      const int i = e % m, c = e / m;
+      out[i + (size_t)ldo * c] = q.fval[c] * Vs[i + (size_t)ldv * c];
+    }
   } else {
-    for (int e = threadIdx.x; e < m * mu; e += kOrthThreads) {
-      int i = e % m, c = e / m;
-      out[i + (size_t)ldo * c] = Y[e];
+    regs_to_tile(y, m, mu, Vs, ldv);
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * mu; e += kQThreads) {
+      const int i = e % m, c = e / m;
+      out[i + (size_t)ldo * c] = Vs[i + (size_t)ldv * c];
     }
   }
   if (threadIdx.x == 0 && status) *status = converged ? 0 : 1;
 }
 
 // ---------------------------------------------------------------------------
-// Phase C: block b: Y_b = Q_b [W(b*s : b*s+s, :) ; 0] -> out rows [r0, r1) (ld ldo).
-// Reflectors are staged through shared memory kApplyChunk at a time.  With pbest also
-// records per-block column argmax partials for the sign fix.
+// Leaf apply: block b: Y_b = Q_b [W(b*s : b*s+s, :) ; 0] -> out rows [r0, r1) (ld ldo).
+// With pbest also records per-block column argmax partials for the sign fix.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kOrthThreads) orth_block_apply_kernel(
+template <int RPW>
+__global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
     const double* __restrict__ V, long long m, int s, int ldv, int nb,
     const double* __restrict__ tau, const double* __restrict__ W, int ldw, int mu,
     double* __restrict__ out, int ldo, double* __restrict__ pbest, int* __restrict__ pidx) {
   extern __shared__ __align__(16) double sm[];
+  const QSmem q = carve_q(sm);
+  double* tile = sm + kQScratchBytes / 8;
   const int b = blockIdx.x;
   const long long r0 = (m * b) / nb, r1 = (m * (b + 1)) / nb;
-  const int rows = (int)(r1 - r0);
-  double* Y = sm;                                  // rows x mu
-  double* Vs = Y + (size_t)rows * mu;              // rows x kApplyChunk
-  double* ts = Vs + (size_t)rows * kApplyChunk;    // s
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < rows * mu; e += kOrthThreads) {
-    int i = e % rows, c = e / rows;
-    Y[e] = i < s ? W[(size_t)b * s + i + (size_t)ldw * c] : 0.0;
-  }
-  for (int k = threadIdx.x; k < s; k += kOrthThreads) ts[k] = tau[(size_t)b * s + k];
-  const int kmax = min(rows, s);
-  for (int k_hi = kmax; k_hi > 0; k_hi -= kApplyChunk) {
-    const int k_lo = max(0, k_hi - kApplyChunk);
-    __syncthreads();
-    for (int e = threadIdx.x; e < rows * (k_hi - k_lo); e += kOrthThreads) {
-      int i = e % rows, kk = e / rows;
-      Vs[e] = V[r0 + i + (size_t)ldv * (k_lo + kk)];
+  const int rows = (int)(r1 - r0), ldt = (kQWarps * RPW) | 1;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+  load_tile(V + r0, ldv, rows, s, tile, ldt, kQWarps * RPW);
+  for (int k = threadIdx.x; k < s; k += kQThreads) q.tau[k] = tau[(size_t)b * s + k];
+  double y[2][RPW];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = l + 32 * j;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = row0 + i;
+      y[j][i] = (c < mu && r < s && r < rows) ? W[(size_t)b * s + r + (size_t)ldw * c] : 0.0;
     }
-    __syncthreads();
-    apply_q(Vs, rows, ts, rows, s, Y, rows, mu, k_hi, k_lo);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < rows * mu; e += kOrthThreads) {
-    int i = e % rows, c = e / rows;
-    out[r0 + i + (size_t)ldo * c] = Y[e];
-  }
+  reg_apply(y, mu, tile, ldt, q.tau, min(rows, s), 0, q);
+  __syncthreads();
   if (pbest) {
-    for (int c = warp; c < mu; c += kOrthWarps) {
-      double best;
-      int imax;
-      warp_argmax(Y + (size_t)rows * c, rows, best, imax);
-      if (lane == 0) {
-        pbest[(size_t)b * mu + c] = best;
-        pidx[(size_t)b * mu + c] = (int)(r0 + imax);
-      }
+    reg_argmax(y, rows, mu, q, q.red, q.piv);
+    if ((int)threadIdx.x < mu) {
+      const int c = threadIdx.x, im = q.piv[c];
+      pbest[(size_t)b * mu + c] = q.red[c];
+      pidx[(size_t)b * mu + c] = im >= 0 ? (int)(r0 + im) : 0;
     }
+  }
+  regs_to_tile(y, rows, mu, tile, ldt);
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * mu; e += kQThreads) {
+    const int i = e % rows, c = e / rows;
+    out[r0 + i + (size_t)ldo * c] = tile[i + ldt * c];
   }
 }
 
-// Phase D: per column, combine block partials in block order; flip if negative.
+// Sign fix: per column, combine block partials in block order; flip if negative.
 __global__ void orth_signfix_kernel(double* __restrict__ U, long long m, int ldu, int mu, int nb,
                                     const double* __restrict__ pbest,
                                     const int* __restrict__ pidx) {
@@ -557,55 +840,55 @@ __global__ void orth_signfix_kernel(double* __restrict__ U, long long m, int ldu
 // ---------------------------------------------------------------------------
 struct OrthLevel {
   long long m;  // rows of this level's input
-  int nb;       // row blocks
+  int nb;       // row blocks (leaves)
   size_t v_off, tau_off, w_off;  // workspace offsets (doubles)
 };
 
-static size_t core_smem(long long m, int s, int mu) {
-  int n = s + (s & 1);
-  return sizeof(double) * ((size_t)m * s + (size_t)m * mu + (size_t)s * n + (size_t)n * n + 2 * s + n) +
-         sizeof(int) * (s + n + 1) + (size_t)n * n + 64;
+static int rpw_for(long long rows) {
+  const long long r = (rows + kQWarps - 1) / kQWarps;
+  return r <= 4 ? 4 : r <= 8 ? 8 : r <= 12 ? 12 : 16;
 }
 
-static long long block_rows(int s, int mu) {
-  // phase A: rows x s ; phase C: rows x (mu + kApplyChunk)
-  return (long long)(kOrthSmemBudget / (sizeof(double) * (size_t)std::max(s, mu + kApplyChunk))) - 8;
+// shared tiles hold 16 * RPW rows (ld (16 * RPW) | 1) so reflector columns can be read
+// without row guards
+static size_t leaf_smem(long long rows, int s) {
+  return kQScratchBytes + sizeof(double) * (size_t)((kQWarps * rpw_for(rows)) | 1) * s + 64;
 }
 
-static std::vector<OrthLevel> plan_levels(long long I, int s, int mu, size_t* total) {
+static size_t core_smem(long long m, int s) {
+  const int n = 64;
+  return kQScratchBytes +
+         sizeof(double) * ((size_t)((kQWarps * rpw_for(m)) | 1) * s + (size_t)s * s + (size_t)n * n + n) +
+         sizeof(int) * n + 64;
+}
+
+static std::vector<OrthLevel> plan_levels(long long I, int s, size_t* total) {
   std::vector<OrthLevel> lv;
   size_t off = 0;
   long long m = I;
-  while (core_smem(m, s, mu) > kOrthSmemBudget) {
-    long long per = block_rows(s, mu);
-    int nb = std::max(2, (int)((m + per - 1) / per));
+  while (m > kMaxBlockRows) {
     OrthLevel L;
     L.m = m;
-    L.nb = nb;
+    L.nb = (int)((m + kMaxBlockRows - 1) / kMaxBlockRows);
     L.v_off = off;
     off += (size_t)m * s;
     L.tau_off = off;
-    off += (size_t)nb * s;
+    off += (size_t)L.nb * s;
     L.w_off = off;  // stacked R of this level = next level's input (nb*s x s)
-    off += (size_t)nb * s * s;
+    off += (size_t)L.nb * s * s;
     lv.push_back(L);
-    m = (long long)nb * s;
+    m = (long long)L.nb * s;
   }
   *total = off;
   return lv;
 }
 
 size_t orth_workspace_doubles(long long I, int s) {
-  // upper bound over mu <= s
-  size_t best = 64;
-  for (int mu = 1; mu <= s; ++mu) {
-    size_t used = 0;
-    std::vector<OrthLevel> lv = plan_levels(I, s, mu, &used);
-    for (auto& L : lv) used += (size_t)L.nb * s * mu;
-    if (!lv.empty()) used += (size_t)lv[0].nb * mu * 2;
-    best = std::max(best, used + 64);
-  }
-  return best;
+  size_t used = 0;
+  std::vector<OrthLevel> lv = plan_levels(I, s, &used);
+  for (auto& L : lv) used += (size_t)L.nb * s * s;  // W per level (mu <= s)
+  if (!lv.empty()) used += (size_t)lv[0].nb * s * 2;
+  return used + 64;
 }
 
 // sweeps taken by the most recent converged Jacobi (diagnostics only)
@@ -615,26 +898,66 @@ int last_jacobi_sweeps() {
   return v;
 }
 
+namespace {
+
+// the attribute is set once per kernel (and device) to the largest size any call can use
+constexpr size_t kOrthSmemMax = 227 * 1024;
+
+template <int RPW>
+cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, double* tau,
+                    double* S, int lds, cudaStream_t st) {
+  static unsigned long long done = 0;
+  const long long rows = (m + nb - 1) / nb;
+  const size_t smem = leaf_smem(rows, s);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_qr_kernel<RPW>), kOrthSmemMax, done);
+  if (e != cudaSuccess) return e;
+  orth_leaf_qr_kernel<RPW><<<nb, kQThreads, smem, st>>>(A, m, s, (int)m, nb, V, tau, S, lds);
+  return cudaGetLastError();
+}
+
+template <int RPW>
+cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, int final_level,
+                 int* status, double tol, cudaStream_t st) {
+  static unsigned long long done = 0;
+  const size_t smem = core_smem(m, s);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPW>), kOrthSmemMax, done);
+  if (e != cudaSuccess) return e;
+  orth_core_kernel<RPW><<<1, kQThreads, smem, st>>>(S, m, s, m, mu, out, ldo, final_level, status, tol);
+  return cudaGetLastError();
+}
+
+template <int RPW>
+cudaError_t leaf_apply(const double* V, long long m, int s, int nb, const double* tau,
+                       const double* W, int ldw, int mu, double* out, double* pbest, int* pidx,
+                       cudaStream_t st) {
+  static unsigned long long done = 0;
+  const long long rows = (m + nb - 1) / nb;
+  const size_t smem = leaf_smem(rows, s);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_apply_kernel<RPW>), kOrthSmemMax, done);
+  if (e != cudaSuccess) return e;
+  orth_leaf_apply_kernel<RPW><<<nb, kQThreads, smem, st>>>(V, m, s, (int)m, nb, tau, W, ldw, mu,
+                                                          out, (int)m, pbest, pidx);
+  return cudaGetLastError();
+}
+
+#define LMRA_RPW_DISPATCH(rpw, call) \
+  ((rpw) == 4 ? call<4> : (rpw) == 8 ? call<8> : (rpw) == 12 ? call<12> : call<16>)
+
+}  // namespace
+
 cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, double* work,
                         int* status, cudaStream_t st) {
   if (s < 1 || s > kOrthMaxS || mu < 1 || mu > s || I < s) return cudaErrorInvalidValue;
-  static unsigned long long a1 = 0, a2 = 0, a3 = 0;
-  cudaError_t e;
-  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel), kOrthSmemBudget + 16384, a1)) != cudaSuccess) return e;
-  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(orth_block_qr_kernel), kOrthSmemBudget + 16384, a2)) != cudaSuccess) return e;
-  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(orth_block_apply_kernel), kOrthSmemBudget + 16384, a3)) != cudaSuccess) return e;
-
+  if (core_smem(kMaxBlockRows, kOrthMaxS) > kOrthSmemMax) return cudaErrorInvalidConfiguration;
   // Jacobi stopping rule: rotate while |g_p.g_q| > tol |g_p| |g_q|; below ~s*eps the inner
   // product is rounding noise and further rotations cannot reduce it.
   double tol = 8.0 * s * 0x1.0p-53;
   if (const char* env = getenv("LMRA_JACOBI_TOL")) tol = atof(env);
   size_t used = 0;
-  std::vector<OrthLevel> lv = plan_levels(I, s, mu, &used);
-  if (lv.empty()) {
-    orth_core_kernel<<<1, kOrthThreads, core_smem(I, s, mu), st>>>(c, (int)I, s, (int)I, mu, u,
-                                                                    (int)I, 1, status, tol);
-    return cudaGetLastError();
-  }
+  std::vector<OrthLevel> lv = plan_levels(I, s, &used);
+  cudaError_t e;
+  if (lv.empty())
+    return LMRA_RPW_DISPATCH(rpw_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st);
   std::vector<size_t> wbuf(lv.size());
   for (size_t l = 0; l < lv.size(); ++l) {
     wbuf[l] = used;
@@ -642,36 +965,30 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   }
   double* pbest = work + used;
   int* pidx = reinterpret_cast<int*>(pbest + (size_t)lv[0].nb * mu);
-  // phase A, level by level
+  // leaves, level by level
   for (size_t l = 0; l < lv.size(); ++l) {
     const OrthLevel& L = lv[l];
     const double* A = l == 0 ? c : work + lv[l - 1].w_off;
-    long long per = (L.m + L.nb - 1) / L.nb;
-    size_t smem = sizeof(double) * ((size_t)per * s + s) + 64;
-    orth_block_qr_kernel<<<L.nb, kOrthThreads, smem, st>>>(A, L.m, s, (int)L.m, L.nb,
-                                                          work + L.v_off, work + L.tau_off,
-                                                          work + L.w_off, L.nb * s);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int rpw = rpw_for((L.m + L.nb - 1) / L.nb);
+    e = LMRA_RPW_DISPATCH(rpw, leaf_qr)(A, L.m, s, L.nb, work + L.v_off, work + L.tau_off,
+                                        work + L.w_off, L.nb * s, st);
+    if (e != cudaSuccess) return e;
   }
-  // phase B on the last stacked R
+  // core on the last stacked R
   const OrthLevel& last = lv.back();
   const int mB = last.nb * s;
-  orth_core_kernel<<<1, kOrthThreads, core_smem(mB, s, mu), st>>>(
-      work + last.w_off, mB, s, mB, mu, work + wbuf.back(), mB, 0, status, tol);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  // phase C, back down
+  e = LMRA_RPW_DISPATCH(rpw_for(mB), core)(work + last.w_off, mB, s, mu, work + wbuf.back(), mB, 0,
+                                          status, tol, st);
+  if (e != cudaSuccess) return e;
+  // back down
   for (int l = (int)lv.size() - 1; l >= 0; --l) {
     const OrthLevel& L = lv[l];
-    const double* W = work + wbuf[l];
-    const int ldw = L.nb * s;
     double* out = l == 0 ? u : work + wbuf[l - 1];
-    const int ldo = (int)L.m;
-    long long per = (L.m + L.nb - 1) / L.nb;
-    size_t smem = sizeof(double) * ((size_t)per * (mu + kApplyChunk) + s) + 64;
-    orth_block_apply_kernel<<<L.nb, kOrthThreads, smem, st>>>(
-        work + L.v_off, L.m, s, (int)L.m, L.nb, work + L.tau_off, W, ldw, mu, out, ldo,
-        l == 0 ? pbest : nullptr, l == 0 ? pidx : nullptr);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int rpw = rpw_for((L.m + L.nb - 1) / L.nb);
+    e = LMRA_RPW_DISPATCH(rpw, leaf_apply)(work + L.v_off, L.m, s, L.nb, work + L.tau_off,
+                                           work + wbuf[l], L.nb * s, mu, out,
+                                           l == 0 ? pbest : nullptr, l == 0 ? pidx : nullptr, st);
+    if (e != cudaSuccess) return e;
   }
   orth_signfix_kernel<<<mu, 256, 0, st>>>(u, I, (int)I, mu, lv[0].nb, pbest, pidx);
   return cudaGetLastError();

@@ -342,10 +342,15 @@ void sampler_walk_stats(unsigned long long* out2, bool reset) {
 __device__ double exact_segment(const double* __restrict__ x, long long c0, long long c1, double S,
                                 double* __restrict__ out, double* smd, int* smi, long long* sml) {
   constexpr long long kSeq = 256;  // sequential batch when crossings come fast
+  constexpr long long kDense = 64;  // a crossing this close to the last one: go sequential
   __shared__ double s_seq;
   long long i0 = c0;
-  bool sequential = true;  // chunks start sequentially: early crossings are dense
+  // only the start of the whole sum has dense crossings (each early element can double
+  // S); a later chunk is here because the approximate prefix could not place it in one
+  // binade, i.e. it holds one (rarely a few) crossing at an unknown position
+  bool sequential = S == 0.0;
   while (i0 < c1) {
+    const long long tb0 = clock64();
     if (sequential || S == 0.0) {
       // one thread steps the recurrence itself (plain IEEE adds, the reference's loop);
       // cheaper than a block iteration when the next binade crossing is only a few
@@ -357,7 +362,21 @@ __device__ double exact_segment(const double* __restrict__ x, long long c0, long
       __syncthreads();
       if (threadIdx.x == 0) {
         double s = S;
-        for (int j = 0; j < (int)(e - i0); ++j) {
+        const int cnt = (int)(e - i0);
+        int j = 0;
+        for (; j + 8 <= cnt; j += 8) {  // loads batched ahead of the dependent adds
+          double v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = s_buf[j + k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            s = __dadd_rn(s, v[k]);
+            v[k] = s;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s_buf[j + k] = v[k];
+        }
+        for (; j < cnt; ++j) {
           s = __dadd_rn(s, s_buf[j]);
           s_buf[j] = s;
         }
@@ -369,9 +388,11 @@ __device__ double exact_segment(const double* __restrict__ x, long long c0, long
       S = s_seq;
       i0 = e;
       sequential = false;
+      if (threadIdx.x == 0) g_walk_stats[6] += (unsigned long long)(clock64() - tb0);
       __syncthreads();
       continue;
     }
+    if (threadIdx.x == 0) g_walk_stats[7] += 1;
     int ue, be;
     binade_of(S, ue, be);
     const double M = ldexp(S, -ue);                  // exact integer < 2^53
@@ -428,7 +449,7 @@ __device__ double exact_segment(const double* __restrict__ x, long long c0, long
       }
       __syncthreads();
       S = s_next;
-      sequential = cross - i0 < kSeq;  // crossings are dense here: step sequentially
+      sequential = cross - i0 < kDense;  // crossings are dense here: step sequentially
       i0 = cross + 1;
     } else {
       S = ldexp(M + tot, ue);

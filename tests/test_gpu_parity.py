@@ -159,7 +159,8 @@ def check_own_draws(alg, own, ref, regime, order=None):
     probabilities are computed from the input tensor itself (T-HOSVD, the first mode of
     ST-HOSVD, or uniform sampling) -- the column norms use the canonical order shared with
     the oracle.  Later ST-HOSVD modes sample the shrunk tensor, whose last bits depend on
-    the GEMM summation order: indices must still agree, scales to 1e-13 relative."""
+    the GEMM summation order (and on the factors' last bits): indices must still agree,
+    scales to 1e-12 relative."""
     N = len(ref.factors)
     order = order or list(range(N))
     for n in range(N):
@@ -172,7 +173,7 @@ def check_own_draws(alg, own, ref, regime, order=None):
             assert np.array_equal(own.samples[n][1], ref.samples[n][1]), f"scales mode {n}"
         else:
             d = np.abs(own.samples[n][1] / ref.samples[n][1] - 1).max()
-            assert d <= 1e-13, f"scales mode {n}: {d:.3g}"
+            assert d <= 1e-12, f"scales mode {n}: {d:.3g}"
 
 
 @pytest.mark.parametrize("alg", ALGS)
