@@ -16,10 +16,13 @@
 //    A step whose exact sum reaches the next binade is evaluated directly (one IEEE add).
 //    Parallel structure: chunks of 4096; each chunk's aggregate (R for start parity 0/1,
 //    parity map, crossing margin) is computed assuming the binade that an approximate
-//    prefix predicts (pass B); one CTA walks the chunks in order with the exact state
-//    (pass C), taking the O(1) aggregate when it is certified and processing the chunk
-//    element-exactly otherwise (chunk 0 and the few chunks holding binade crossings);
-//    pass D writes every S_i of the certified chunks.
+//    prefix predicts (pass B).  A chunk the prediction places across exactly one binade
+//    boundary is "split": pass B gives it 16 sub-chunk aggregates (256 elements) under
+//    both binades.  One CTA walks the chunks in order with the exact state (pass C): runs
+//    of certified chunks are taken at once (a block scan of the 2-state parity transducer
+//    M -> M + R_parity(M)); a split chunk is walked sub-chunk by sub-chunk, stepping only
+//    the sub-chunk that holds the crossing; chunk 0 (dense crossings from S = 0) is
+//    processed element-exactly.  Pass D writes every S_i of the certified (sub-)chunks.
 //  * Neumaier's stable_sum (sketching.cpp:13-24) = fl(S + c): S is the naive sum (above);
 //    c is the naive sum of the exact two-sum errors e_i (computable from S_{i-1}, x_i,
 //    S_i).  c is accumulated exactly (double-double, fixed tree) and the final rounding
@@ -38,6 +41,9 @@ constexpr int kThr = 256;                 // grid passes: 16 items per thread
 constexpr int kItems = kChunk / kThr;
 constexpr int kCThr = 1024;               // pass C (single CTA): 4 items per thread
 constexpr int kCItems = kChunk / kCThr;
+constexpr int kSub = 256;                 // sub-chunk of a split chunk
+constexpr int kNSub = kChunk / kSub;      // 16 sub-chunks
+constexpr int kSubThr = kSub / kItems;    // 16 threads (a half-warp) per sub-chunk in passes B/D
 constexpr double kTwo53 = 9007199254740992.0;
 
 enum SamplerStatus {
@@ -197,7 +203,7 @@ struct ChunkAgg {
   int map;          // parity map of the whole chunk
   int ulp_exp;      // assumed binade (ulp exponent); kNoBinade if ambiguous
   int bad;          // negative / NaN input seen
-  int pad;
+  int split;        // chunk-level: sub-chunk aggregates exist (two binade hypotheses)
 };
 constexpr int kNoBinade = 1 << 30;
 
@@ -205,20 +211,105 @@ struct ChunkStart {  // exact state at a certified chunk's start (pass C -> pass
   double M;          // S / u (integer < 2^53)
   int parity;
   int ulp_exp;
-  int fast;          // 1: pass D writes the chunk, 0: pass C already wrote it
+  int fast;          // 1: pass D writes the chunk, 0: pass C already wrote it, 2: split
   int pad;
 };
+
+// ---------------------------------------------------------------- half-warp segments
+// A split chunk's sub-chunk is 16 consecutive threads (16 items each) in passes B and D:
+// scans and reductions stay inside the 16-lane segment.
+__device__ __forceinline__ unsigned seg_mask() {
+  return 0xffffu << (threadIdx.x & 16);
+}
+__device__ __forceinline__ int seg_excl_map(int m, unsigned mask, int& total) {
+  const int sl = threadIdx.x & 15;
+  int inc = m;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const int t = __shfl_up_sync(mask, inc, o, 16);
+    if (sl >= o) inc = map_compose(t, inc);
+  }
+  total = __shfl_sync(mask, inc, 15, 16);
+  int prev = __shfl_up_sync(mask, inc, 1, 16);
+  return sl == 0 ? 0 : prev;
+}
+__device__ __forceinline__ double seg_incl_sum(double v, unsigned mask, double& total) {
+  const int sl = threadIdx.x & 15;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const double t = __shfl_up_sync(mask, v, o, 16);
+    if (sl >= o) v += t;
+  }
+  total = __shfl_sync(mask, v, 15, 16);
+  return v;
+}
+__device__ __forceinline__ double seg_max(double v, unsigned mask) {
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(mask, v, o, 16));
+  return v;
+}
+
+// r of one element given the running parity (updated), from its classification
+__device__ __forceinline__ double step_r(const Elem& e, int& par) {
+  const double r = e.tie ? tie_r(e.q, par) : e.q;
+  par = map_apply(e.map, par);
+  return r;
+}
+
+// Per-thread pass over its items for BOTH start parities at once (classifications are
+// recomputed instead of kept: the earlier version held 16 Elem + 16 prefixes per thread
+// in registers, 200 registers and one CTA per SM, latency-bound).  Returns the thread's
+// ulp totals run_p and zl_p = max_j (ulps before j + y_j), saturated past 2^53.
+__device__ __forceinline__ void two_parity_pass(const double (&xv)[kItems], int ue, int excl,
+                                                double& run0, double& run1, double& zl0,
+                                                double& zl1) {
+  int par0 = map_apply(excl, 0), par1 = map_apply(excl, 1);
+  run0 = run1 = zl0 = zl1 = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j) {
+    const Elem e = classify(xv[j] >= 0.0 ? xv[j] : 0.0, ue);
+    zl0 = fmax(zl0, run0 + e.y);
+    zl1 = fmax(zl1, run1 + e.y);
+    run0 = fmin(run0 + step_r(e, par0), 2.0 * kTwo53);  // saturate: past 2^53 is a crossing
+    run1 = fmin(run1 + step_r(e, par1), 2.0 * kTwo53);
+  }
+}
+
+__device__ __forceinline__ int thread_map(const double (&xv)[kItems], int ue) {
+  int tmap = 0;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j)
+    tmap = map_compose(tmap, classify(xv[j] >= 0.0 ? xv[j] : 0.0, ue).map);
+  return tmap;
+}
+
+// this thread's kItems consecutive elements (16-byte vector loads when fully in range;
+// rows past n read as 0)
+__device__ __forceinline__ void load_items(const double* __restrict__ x, long long n,
+                                           long long base, double (&v)[kItems]) {
+  if (base + kItems <= n) {
+    const double2* p = reinterpret_cast<const double2*>(x + base);
+#pragma unroll
+    for (int j = 0; j < kItems / 2; ++j) {
+      const double2 t = p[j];
+      v[2 * j] = t.x;
+      v[2 * j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) v[j] = base + j < n ? x[base + j] : 0.0;
+  }
+}
 
 // ---------------------------------------------------------------- pass A: chunk sums
 __global__ void __launch_bounds__(kThr) chunk_sums_kernel(const double* __restrict__ x, long long n,
                                                           double* __restrict__ csum) {
   __shared__ double sm[32];
-  const long long base = (long long)blockIdx.x * kChunk;
+  double xv[kItems];
+  load_items(x, n, (long long)blockIdx.x * kChunk + threadIdx.x * kItems, xv);
   double v = 0.0;
-  for (int k = 0; k < kItems; ++k) {
-    long long i = base + threadIdx.x * kItems + k;
-    if (i < n) v += x[i];
-  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) v += xv[k];
   double tot;
   block_incl<kThr>(v, sm, tot);
   if (threadIdx.x == 0) csum[blockIdx.x] = tot;
@@ -228,7 +319,8 @@ __global__ void __launch_bounds__(kThr) chunk_sums_kernel(const double* __restri
 // scan over tiles of 1024 chunks; the prediction only needs |approx - exact| <= delta)
 __global__ void __launch_bounds__(1024) chunk_plan_kernel(const double* __restrict__ csum,
                                                           int nchunks, long long n,
-                                                          int* __restrict__ assumed) {
+                                                          int* __restrict__ assumed,
+                                                          int* __restrict__ assumed2) {
   __shared__ double smd[32];
   const double delta = 4.0 * ((double)n + 64.0) * 0x1.0p-53 + 1e-15;
   double carry = 0.0;
@@ -240,32 +332,121 @@ __global__ void __launch_bounds__(1024) chunk_plan_kernel(const double* __restri
     const double acc = carry + (incl - v);  // approximate exclusive prefix
     if (k < nchunks) {
       const double lo = acc * (1.0 - delta), hi = (acc + v) * (1.0 + delta) + 1e-300;
-      int ue = kNoBinade;
+      int ue = kNoBinade, ue2 = kNoBinade;
       if (k > 0 && lo >= 0x1.0p-1022) {
         const int e_lo = ilogb(lo), e_hi = ilogb(hi);
-        if (e_lo == e_hi) ue = e_lo - 52;
+        if (e_lo == e_hi) {
+          ue = e_lo - 52;
+        } else if (e_hi == e_lo + 1) {  // one boundary inside: split chunk, both binades
+          ue = e_lo - 52;
+          ue2 = e_hi - 52;
+        }
       }
       assumed[k] = ue;
+      assumed2[k] = ue2;
     }
     carry += tot;
   }
 }
 
 // ---------------------------------------------------------------- pass B: aggregates
+// sub-chunk aggregates of a split chunk under binade ue (this thread's 16 items)
+__device__ void sub_aggregate(const double (&xv)[kItems], int ue, ChunkAgg* __restrict__ out) {
+  const unsigned mask = seg_mask();
+  int smap;
+  const int excl = seg_excl_map(thread_map(xv, ue), mask, smap);
+  double run0, run1, zl0, zl1;
+  two_parity_pass(xv, ue, excl, run0, run1, zl0, zl1);
+  double tot0, tot1;
+  const double ex0 = seg_incl_sum(run0, mask, tot0) - run0;
+  const double ex1 = seg_incl_sum(run1, mask, tot1) - run1;
+  const double Z0 = seg_max(zl0 + ex0, mask) + 2.0;  // margin for the rounded additions
+  const double Z1 = seg_max(zl1 + ex1, mask) + 2.0;
+  if ((threadIdx.x & 15) == 0) {
+    ChunkAgg a;
+    a.R0 = fmin(tot0, 2.0 * kTwo53);
+    a.R1 = fmin(tot1, 2.0 * kTwo53);
+    a.Z0 = Z0;
+    a.Z1 = Z1;
+    a.map = smap;
+    a.ulp_exp = ue;
+    a.bad = 0;
+    a.split = 0;
+    *out = a;
+  }
+}
+
 __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restrict__ x, long long n,
                                                          const int* __restrict__ assumed,
-                                                         ChunkAgg* __restrict__ agg) {
+                                                         const int* __restrict__ assumed2,
+                                                         ChunkAgg* __restrict__ agg,
+                                                         ChunkAgg* __restrict__ subagg) {
   __shared__ double smd[32];
   __shared__ int smi[32];
   const int k = blockIdx.x;
   const long long base = (long long)k * kChunk + threadIdx.x * kItems;
   const int ue = assumed[k];
+  double xv[kItems];
+  load_items(x, n, base, xv);
   int bad = 0;
-  if (ue == kNoBinade) {
-    for (int j = 0; j < kItems; ++j) {
-      long long i = base + j;
-      if (i < n && !(x[i] >= 0.0)) bad = 1;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j)
+    if (!(xv[j] >= 0.0)) bad = 1;
+  const int g = threadIdx.x / kSubThr;
+  if (k == 0) {
+    // chunk 0 holds the dense crossings of the sum's start (S grows from 0): sub-chunks get
+    // their own binade prediction from an approximate prefix inside the chunk; the walk
+    // steps sub-chunk 0 and any sub-chunk the prediction cannot place in one binade
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) v += xv[j] >= 0.0 ? xv[j] : 0.0;
+    __shared__ double subsum[kNSub];
+    double tot;
+    seg_incl_sum(v, seg_mask(), tot);
+    if ((threadIdx.x & 15) == 0) subsum[g] = tot;
+    __syncthreads();
+    double pre = 0.0;
+    for (int h = 0; h < g; ++h) pre += subsum[h];
+    const double delta = 4.0 * ((double)n + 64.0) * 0x1.0p-53 + 1e-15;
+    const double lo = pre * (1.0 - delta), hi = (pre + subsum[g]) * (1.0 + delta) + 1e-300;
+    int ug = kNoBinade;
+    if (g > 0 && lo >= 0x1.0p-1022 && ilogb(lo) == ilogb(hi)) ug = ilogb(lo) - 52;
+    if (ug != kNoBinade) {
+      sub_aggregate(xv, ug, subagg + g);
+    } else if ((threadIdx.x & 15) == 0) {
+      ChunkAgg a{};
+      a.ulp_exp = kNoBinade;
+      subagg[g] = a;
     }
+    if ((threadIdx.x & 15) == 0) {
+      ChunkAgg a{};
+      a.ulp_exp = kNoBinade;
+      subagg[kNSub + g] = a;  // no second hypothesis
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+      ChunkAgg a{};
+      a.ulp_exp = kNoBinade;
+      a.bad = bad;
+      a.split = 1;
+      agg[k] = a;
+    }
+    return;
+  }
+  if (assumed2[k] != kNoBinade) {  // split: [k][hypothesis][sub-chunk]
+    sub_aggregate(xv, ue, subagg + ((size_t)k * 2 + 0) * kNSub + g);
+    sub_aggregate(xv, assumed2[k], subagg + ((size_t)k * 2 + 1) * kNSub + g);
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+      ChunkAgg a{};
+      a.ulp_exp = kNoBinade;
+      a.bad = bad;
+      a.split = 1;
+      agg[k] = a;
+    }
+    return;
+  }
+  if (ue == kNoBinade) {
     bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
       ChunkAgg a{};
@@ -275,51 +456,26 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
     }
     return;
   }
-  Elem el[kItems];
-  int tmap = 0;  // thread-local composition
-  for (int j = 0; j < kItems; ++j) {
-    long long i = base + j;
-    double xv = i < n ? x[i] : 0.0;
-    if (!(xv >= 0.0)) bad = 1;
-    el[j] = classify(xv >= 0.0 ? xv : 0.0, ue);
-    tmap = map_compose(tmap, el[j].map);
-  }
   int excl;
-  const int bmap = BlockScan<kThr>::excl_map(tmap, excl, smi);
-  // two passes: start parity 0 and 1
-  double R[2], Z[2];
-  for (int p0 = 0; p0 < 2; ++p0) {
-    int par = map_apply(excl, p0);
-    double local[kItems];
-    double run = 0.0;
-    for (int j = 0; j < kItems; ++j) {
-      double r = el[j].tie ? tie_r(el[j].q, par) : el[j].q;
-      par = map_apply(el[j].map, par);
-      run = fmin(run + r, 2.0 * kTwo53);  // saturate: anything past 2^53 is a crossing
-      local[j] = run;
-    }
-    double tot;
-    const double incl = block_incl<kThr>(run, smd, tot);
-    const double excl_sum = incl - run;
-    double z = 0.0;
-    for (int j = 0; j < kItems; ++j) {
-      const double rprev = excl_sum + (j > 0 ? local[j - 1] : 0.0);
-      z = fmax(z, rprev + el[j].y);
-    }
-    Z[p0] = block_max<kThr>(z, smd) + 2.0;  // margin for the rounded additions
-    R[p0] = fmin(tot, 2.0 * kTwo53);
-  }
+  const int bmap = BlockScan<kThr>::excl_map(thread_map(xv, ue), excl, smi);
+  double run0, run1, zl0, zl1;
+  two_parity_pass(xv, ue, excl, run0, run1, zl0, zl1);
+  double tot0, tot1;
+  const double ex0 = block_incl<kThr>(run0, smd, tot0) - run0;
+  const double ex1 = block_incl<kThr>(run1, smd, tot1) - run1;
+  const double Z0 = block_max<kThr>(zl0 + ex0, smd) + 2.0;  // margin for the rounded additions
+  const double Z1 = block_max<kThr>(zl1 + ex1, smd) + 2.0;
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     ChunkAgg a;
-    a.R0 = R[0];
-    a.R1 = R[1];
-    a.Z0 = Z[0];
-    a.Z1 = Z[1];
+    a.R0 = fmin(tot0, 2.0 * kTwo53);
+    a.R1 = fmin(tot1, 2.0 * kTwo53);
+    a.Z0 = Z0;
+    a.Z1 = Z1;
     a.map = bmap;
     a.ulp_exp = ue;
     a.bad = bad;
-    a.pad = 0;
+    a.split = 0;
     agg[k] = a;
   }
 }
@@ -340,7 +496,8 @@ void sampler_walk_stats(unsigned long long* out2, bool reset) {
 // Exact element-wise processing of [c0, c1) starting from state S (one CTA, kCThr threads).
 // Writes out[i] = S_i when out != nullptr.  Returns the final S.
 __device__ double exact_segment(const double* __restrict__ x, long long c0, long long c1, double S,
-                                double* __restrict__ out, double* smd, int* smi, long long* sml) {
+                                double* __restrict__ out, double* smd, int* smi, long long* sml,
+                                unsigned long long* st, bool force_seq = false) {
   constexpr long long kSeq = 256;  // sequential batch when crossings come fast
   constexpr long long kDense = 64;  // a crossing this close to the last one: go sequential
   __shared__ double s_seq;
@@ -348,7 +505,7 @@ __device__ double exact_segment(const double* __restrict__ x, long long c0, long
   // only the start of the whole sum has dense crossings (each early element can double
   // S); a later chunk is here because the approximate prefix could not place it in one
   // binade, i.e. it holds one (rarely a few) crossing at an unknown position
-  bool sequential = S == 0.0;
+  bool sequential = force_seq || S == 0.0;
   while (i0 < c1) {
     const long long tb0 = clock64();
     if (sequential || S == 0.0) {
@@ -388,11 +545,11 @@ __device__ double exact_segment(const double* __restrict__ x, long long c0, long
       S = s_seq;
       i0 = e;
       sequential = false;
-      if (threadIdx.x == 0) g_walk_stats[6] += (unsigned long long)(clock64() - tb0);
+      (void)tb0;
       __syncthreads();
       continue;
     }
-    if (threadIdx.x == 0) g_walk_stats[7] += 1;
+    if (threadIdx.x == 0) st[7] += 1;
     int ue, be;
     binade_of(S, ue, be);
     const double M = ldexp(S, -ue);                  // exact integer < 2^53
@@ -460,133 +617,311 @@ __device__ double exact_segment(const double* __restrict__ x, long long c0, long
   return S;
 }
 
-__global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restrict__ x, long long n,
-                                                           int nchunks,
-                                                           const ChunkAgg* __restrict__ agg,
-                                                           ChunkStart* __restrict__ starts,
-                                                           double* __restrict__ out,
-                                                           double* __restrict__ total,
-                                                           int* __restrict__ status, int bad_flag) {
-  constexpr int kTile = 256;  // aggregates staged in smem per tile (12 KB)
-  __shared__ ChunkAgg tile[kTile];
-  __shared__ double smd[32];
-  __shared__ int smi[32];
-  __shared__ long long sml[32];
+// Parity transducer of a certified chunk: starting with parity p the chunk adds d_p ulps
+// and leaves parity q_p.  Composition (a then b) is associative, so a run of chunks in one
+// binade is a block scan; sums of the integer d stay exact below 2^53 in any order and
+// only certified states (M + Z < 2^53) are used.
+struct Tx {
+  double d0, d1;
+  int q0, q1;
+};
+__device__ __forceinline__ Tx tx_identity() { return Tx{0.0, 0.0, 0, 1}; }
+__device__ __forceinline__ Tx tx_compose(const Tx& a, const Tx& b) {
+  Tx r;
+  r.d0 = a.d0 + (a.q0 ? b.d1 : b.d0);
+  r.q0 = a.q0 ? b.q1 : b.q0;
+  r.d1 = a.d1 + (a.q1 ? b.d1 : b.d0);
+  r.q1 = a.q1 ? b.q1 : b.q0;
+  return r;
+}
+__device__ __forceinline__ Tx tx_shfl_up(const Tx& t, int o) {
+  Tx r;
+  r.d0 = __shfl_up_sync(0xffffffffu, t.d0, o);
+  r.d1 = __shfl_up_sync(0xffffffffu, t.d1, o);
+  r.q0 = __shfl_up_sync(0xffffffffu, t.q0, o);
+  r.q1 = __shfl_up_sync(0xffffffffu, t.q1, o);
+  return r;
+}
+
+constexpr int kTile = 256;            // chunks per walk tile (= threads taking part in runs)
+constexpr int kTileWarps = kTile / 32;
+
+// exclusive scan of transducers over threads [0, kTile) (others must pass the identity)
+__device__ Tx block_excl_tx(Tx t, Tx* sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Tx inc = t;
+  if (w < kTileWarps) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const Tx u = tx_shfl_up(inc, o);
+      if (lane >= o) inc = tx_compose(u, inc);
+    }
+    if (lane == 31) sm[w] = inc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Tx run = tx_identity();
+    for (int k = 0; k < kTileWarps; ++k) {
+      const Tx v = sm[k];
+      sm[k] = run;  // exclusive warp prefix
+      run = tx_compose(run, v);
+    }
+  }
+  __syncthreads();
+  Tx ex = tx_identity();
+  if (w < kTileWarps) {
+    Tx prev = tx_shfl_up(inc, 1);
+    if (lane == 0) prev = tx_identity();
+    ex = tx_compose(sm[w], prev);
+  }
+  __syncthreads();
+  return ex;
+}
+
+__device__ __forceinline__ int block_min_int(int v, int* sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < kCThr / 32 ? sm[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) t = min(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) sm[32] = t;
+  }
+  __syncthreads();
+  const int r = sm[32];
+  __syncthreads();
+  return r;
+}
+
+// A split chunk: thread 0 takes certified sub-chunks (under whichever hypothesis matches the
+// current binade); the sub-chunk that is not certified (the crossing) is stepped exactly.
+__device__ double split_walk(const double* __restrict__ x, long long n, int k, double S,
+                             const ChunkAgg* __restrict__ subagg, ChunkStart* __restrict__ substarts,
+                             double* __restrict__ out, double* smd, int* smi, long long* sml,
+                             unsigned long long* st) {
   __shared__ double s_S;
-  __shared__ int s_k;
-  double S = 0.0;
-  int bad = 0;
-  for (int t0 = 0; t0 < nchunks; t0 += kTile) {
-    const int t1 = min(nchunks, t0 + kTile);
-    __syncthreads();
-    for (int k = t0 + (int)threadIdx.x; k < t1; k += kCThr) tile[k - t0] = agg[k];
-    __syncthreads();
-    int k = t0;
-    while (k < t1) {
-      // thread 0 takes the certified O(1) aggregates until the first chunk that is not
-      const long long tf0 = clock64();
-      if (threadIdx.x == 0) {
-        double s = S;
-        int kk = k;
-        // exact state in ulps of the current binade, carried across certified chunks
-        // (a certified chunk never leaves the binade, so M, ue, capU stay valid)
-        int ue = kNoBinade, be = 0;
-        double M = 0.0, capU = 0.0;
-        if (s > 0.0) {
-          binade_of(s, ue, be);
-          M = ldexp(s, -ue);
-          capU = ldexp(1.0, be - ue);
-        }
-        for (; kk < t1; ++kk) {
-          const ChunkAgg& a = tile[kk - t0];
-          bad |= a.bad;
-          if (a.ulp_exp == kNoBinade || !(s > 0.0)) {
-            g_walk_stats[2] += 1;
-            break;
-          }
-          if (ue != a.ulp_exp) {
-            g_walk_stats[3] += 1;
-            break;
-          }
+  __shared__ int s_g;
+  __shared__ ChunkAgg sub[2 * kNSub];  // this chunk's sub-aggregates, both hypotheses
+  if (threadIdx.x < 2 * kNSub) sub[threadIdx.x] = subagg[(size_t)k * 2 * kNSub + threadIdx.x];
+  __syncthreads();
+  int g = 0;
+  while (g < kNSub) {
+    if (threadIdx.x == 0) {
+      double s = S;
+      int gg = g;
+      if (s > 0.0) {
+        int ue, be;
+        binade_of(s, ue, be);
+        double M = ldexp(s, -ue);
+        const double capU = ldexp(1.0, be - ue);
+        for (; gg < kNSub; ++gg) {
+          const ChunkAgg* h0 = sub + gg;
+          const ChunkAgg* h1 = sub + kNSub + gg;
+          const ChunkAgg* a = h0->ulp_exp == ue ? h0 : (h1->ulp_exp == ue ? h1 : nullptr);
+          if (!a) break;
           const int P = parity_of(M);
-          if (!(M + (P ? a.Z1 : a.Z0) < capU - 1.0)) break;
+          if (!(M + (P ? a->Z1 : a->Z0) < capU - 1.0)) break;
           ChunkStart cs;
           cs.M = M;
           cs.parity = P;
           cs.ulp_exp = ue;
           cs.fast = 1;
           cs.pad = 0;
-          starts[kk] = cs;
-          M += P ? a.R1 : a.R0;
+          substarts[(size_t)k * kNSub + gg] = cs;
+          M += P ? a->R1 : a->R0;
         }
-        if (s > 0.0) s = ldexp(M, ue);
-        s_S = s;
-        s_k = kk;
-        if (kk < t1) {
-          ChunkStart cs{};
-          cs.fast = 0;
-          starts[kk] = cs;
-        }
+        s = ldexp(M, ue);
       }
-      __syncthreads();
+      s_S = s;
+      s_g = gg;
+    }
+    __syncthreads();
+    S = s_S;
+    g = s_g;
+    __syncthreads();
+    if (g < kNSub) {  // the crossing sub-chunk, element-exact (one sequential batch)
+      const long long c0 = (long long)k * kChunk + (long long)g * kSub, c1 = min(n, c0 + kSub);
       if (threadIdx.x == 0) {
-        g_walk_stats[4] += (unsigned long long)(clock64() - tf0);
-        g_walk_stats[0] += (unsigned long long)(s_k - k);  // certified chunks
-        g_walk_stats[1] += s_k < t1 ? 1ull : 0ull;        // element-exact chunks
+        ChunkStart cs{};
+        cs.fast = 0;
+        substarts[(size_t)k * kNSub + g] = cs;
+        st[3] += 1;
       }
-      S = s_S;
-      k = s_k;
-      __syncthreads();
-      if (k < t1) {  // element-exact processing of chunk k (binade crossings / unknown binade)
-        const long long c0 = (long long)k * kChunk, c1 = min(n, c0 + kChunk);
-        const long long tq0 = clock64();
-        S = exact_segment(x, c0, c1, S, out, smd, smi, sml);
-        if (threadIdx.x == 0) g_walk_stats[5] += (unsigned long long)(clock64() - tq0);
-        ++k;
-      }
+      if (c0 < n) S = exact_segment(x, c0, c1, S, out, smd, smi, sml, st, true);
+      ++g;
     }
   }
+  return S;
+}
+
+__global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restrict__ x, long long n,
+                                                           int nchunks,
+                                                           const ChunkAgg* __restrict__ agg,
+                                                           const ChunkAgg* __restrict__ subagg,
+                                                           ChunkStart* __restrict__ starts,
+                                                           ChunkStart* __restrict__ substarts,
+                                                           double* __restrict__ out,
+                                                           double* __restrict__ total,
+                                                           int* __restrict__ status, int bad_flag) {
+  __shared__ ChunkAgg tile[kTile];
+  __shared__ Tx stx[kTileWarps];
+  __shared__ double smd[32];
+  __shared__ int smi[33];
+  __shared__ long long sml[32];
+  __shared__ double s_S;
+  double S = 0.0;
+  int bad = 0;
+  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // diagnostics (thread 0), flushed once
+  for (int t0 = 0; t0 < nchunks; t0 += kTile) {
+    const int t1 = min(nchunks, t0 + kTile);
+    __syncthreads();
+    for (int k = t0 + (int)threadIdx.x; k < t1; k += kCThr) {
+      tile[k - t0] = agg[k];
+      bad |= agg[k].bad;
+    }
+    __syncthreads();
+    int k = t0;
+    while (k < t1) {
+      if (S > 0.0) {
+        // run of certified chunks from k: thread i takes chunk k + i
+        const long long tr0 = clock64();
+        int ue, be;
+        binade_of(S, ue, be);
+        const double M = ldexp(S, -ue);
+        const double capU = ldexp(1.0, be - ue);
+        const int P0 = parity_of(M);
+        const int i = threadIdx.x;
+        const int kk = k + i;
+        bool valid = i < kTile && kk < t1;
+        ChunkAgg a{};
+        Tx t = tx_identity();
+        if (valid) {
+          a = tile[kk - t0];
+          valid = !a.split && a.ulp_exp == ue;
+        }
+        if (valid) {
+          t.d0 = a.R0;
+          t.q0 = parity_of(a.R0);
+          t.d1 = a.R1;
+          t.q1 = 1 ^ parity_of(a.R1);
+        }
+        const Tx ex = block_excl_tx(t, stx);
+        const double Mi = M + (P0 ? ex.d1 : ex.d0);
+        const int Pi = P0 ? ex.q1 : ex.q0;
+        const bool cert = valid && (Mi + (Pi ? a.Z1 : a.Z0) < capU - 1.0);
+        const int f = block_min_int(cert ? 0x7fffffff : i, smi);  // first chunk not certified
+        const int run = min(f, t1 - k);
+        if (i < run) {
+          ChunkStart cs;
+          cs.M = Mi;
+          cs.parity = Pi;
+          cs.ulp_exp = ue;
+          cs.fast = 1;
+          cs.pad = 0;
+          starts[kk] = cs;
+        }
+        if (run > 0 && i == run - 1) s_S = ldexp(Mi + (Pi ? a.R1 : a.R0), ue);  // state after the run
+        __syncthreads();
+        if (run > 0) S = s_S;
+        k += run;
+        if (threadIdx.x == 0) {
+          st[0] += (unsigned long long)run;
+          st[4] += (unsigned long long)(clock64() - tr0);
+        }
+        __syncthreads();
+        if (k >= t1) break;
+      }
+      // chunk k is not certified: a split chunk, or element-exact processing
+      const long long tq0 = clock64();
+      const long long c0 = (long long)k * kChunk, c1 = min(n, c0 + kChunk);
+      if (tile[k - t0].split) {  // (chunk 0 is split: its first sub-chunk starts at S = 0)
+        if (threadIdx.x == 0) {
+          ChunkStart cs{};
+          cs.fast = 2;
+          starts[k] = cs;
+          st[2] += 1;
+        }
+        S = split_walk(x, n, k, S, subagg, substarts, out, smd, smi, sml, st);
+        if (threadIdx.x == 0) st[6] += (unsigned long long)(clock64() - tq0);
+      } else {
+        if (threadIdx.x == 0) {
+          ChunkStart cs{};
+          cs.fast = 0;
+          starts[k] = cs;
+          st[1] += 1;
+        }
+        S = exact_segment(x, c0, c1, S, out, smd, smi, sml, st);
+        if (threadIdx.x == 0) st[5] += (unsigned long long)(clock64() - tq0);
+      }
+      ++k;
+    }
+  }
+  bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     *total = S;
     if (bad) atomicOr(status, bad_flag);
+    for (int i = 0; i < 8; ++i)
+      if (st[i]) atomicAdd(&g_walk_stats[i], st[i]);
   }
 }
 
 // ---------------------------------------------------------------- pass D: write S_i
+// S_i = (M + ulps before i) * u for this thread's items, given the exclusive map of the
+// items before them (recomputing the classifications: see two_parity_pass)
+__device__ __forceinline__ double items_run(const double (&xv)[kItems], int ue, int par) {
+  double run = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j) run += step_r(classify(xv[j], ue), par);
+  return run;
+}
+__device__ __forceinline__ void items_write(const double (&xv)[kItems], int ue, int par, double M,
+                                            double ex, long long base, long long n,
+                                            double* __restrict__ out) {
+  double local = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j) {
+    local += step_r(classify(xv[j], ue), par);
+    if (base + j < n) out[base + j] = ldexp(M + ex + local, ue);
+  }
+}
+
 __global__ void __launch_bounds__(kThr) chunk_write_kernel(const double* __restrict__ x, long long n,
                                                            const ChunkStart* __restrict__ starts,
+                                                           const ChunkStart* __restrict__ substarts,
                                                            double* __restrict__ out) {
   __shared__ double smd[32];
   __shared__ int smi[32];
   const int k = blockIdx.x;
-  const ChunkStart cs = starts[k];
-  if (!cs.fast) return;
+  const ChunkStart cs0 = starts[k];
+  if (cs0.fast == 0) return;
   const long long base = (long long)k * kChunk + threadIdx.x * kItems;
-  Elem el[kItems];
-  int tmap = 0;
-  for (int j = 0; j < kItems; ++j) {
-    long long i = base + j;
-    el[j] = classify(i < n ? x[i] : 0.0, cs.ulp_exp);
-    tmap = map_compose(tmap, el[j].map);
+  double xv[kItems];
+  if (cs0.fast == 2) {  // split chunk: one 16-lane segment per sub-chunk, own start state
+    const ChunkStart cs = substarts[(size_t)k * kNSub + threadIdx.x / kSubThr];
+    if (!cs.fast) return;  // stepped by the walk (whole segment leaves together)
+    const unsigned mask = seg_mask();
+    load_items(x, n, base, xv);
+    int smap;
+    const int excl = seg_excl_map(thread_map(xv, cs.ulp_exp), mask, smap);
+    const int par = map_apply(excl, cs.parity);
+    const double run = items_run(xv, cs.ulp_exp, par);
+    double tot;
+    const double ex = seg_incl_sum(run, mask, tot) - run;
+    items_write(xv, cs.ulp_exp, par, cs.M, ex, base, n, out);
+    return;
   }
+  const ChunkStart cs = cs0;
+  load_items(x, n, base, xv);
   int excl;
-  BlockScan<kThr>::excl_map(tmap, excl, smi);
-  int par = map_apply(excl, cs.parity);
-  double local[kItems];
-  double run = 0.0;
-  for (int j = 0; j < kItems; ++j) {
-    const double r = el[j].tie ? tie_r(el[j].q, par) : el[j].q;
-    par = map_apply(el[j].map, par);
-    run += r;
-    local[j] = run;
-  }
+  BlockScan<kThr>::excl_map(thread_map(xv, cs.ulp_exp), excl, smi);
+  const int par = map_apply(excl, cs.parity);
+  const double run = items_run(xv, cs.ulp_exp, par);
   double tot;
-  const double incl = block_incl<kThr>(run, smd, tot);
-  const double ex = incl - run;
-  for (int j = 0; j < kItems; ++j) {
-    long long i = base + j;
-    if (i < n) out[i] = ldexp(cs.M + ex + local[j], cs.ulp_exp);
-  }
+  const double ex = block_incl<kThr>(run, smd, tot) - run;
+  items_write(xv, cs.ulp_exp, par, cs.M, ex, base, n, out);
 }
 
 // ---------------------------------------------------------------- Neumaier terms
@@ -652,22 +987,48 @@ __device__ double neumaier_sequential(const double* __restrict__ v, long long n)
   return __dadd_rn(s, c);
 }
 
-// s_out = stable_sum(x) given S_final and the chunk partials (1 thread)
-__global__ void neumaier_final_kernel(const double* __restrict__ x, long long n,
-                                      const double* __restrict__ Sfinal,
-                                      const double* __restrict__ part, int nchunks,
-                                      double* __restrict__ s_out, int* __restrict__ status,
-                                      const int* __restrict__ skip) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (skip && *skip) return;
+// double-double accumulation of per-chunk (hi, lo[, abs]) partials: thread t takes chunks
+// t, t + 256, ... in order, then a fixed tree over the threads (deterministic).
+constexpr int kRedThr = 256;
+__device__ void dd_block_sum(const double* __restrict__ part, int stride, int nchunks,
+                             double& hi_out, double& lo_out, double& ab_out) {
+  __shared__ double hi_s[kRedThr], lo_s[kRedThr], ab_s[kRedThr];
   double hi = 0.0, lo = 0.0, ab = 0.0;
-  for (int k = 0; k < nchunks; ++k) {
+  for (int k = threadIdx.x; k < nchunks; k += kRedThr) {
     double s2, e2;
-    two_sum(hi, part[3 * k], s2, e2);
+    two_sum(hi, part[stride * k], s2, e2);
     hi = s2;
-    lo = __dadd_rn(__dadd_rn(lo, part[3 * k + 1]), e2);
-    ab = __dadd_rn(ab, part[3 * k + 2]);
+    lo = __dadd_rn(__dadd_rn(lo, part[stride * k + 1]), e2);
+    if (stride == 3) ab = __dadd_rn(ab, part[stride * k + 2]);
   }
+  hi_s[threadIdx.x] = hi;
+  lo_s[threadIdx.x] = lo;
+  ab_s[threadIdx.x] = ab;
+  __syncthreads();
+  for (int w = kRedThr / 2; w >= 1; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      double s2, e2;
+      two_sum(hi_s[threadIdx.x], hi_s[threadIdx.x + w], s2, e2);
+      hi_s[threadIdx.x] = s2;
+      lo_s[threadIdx.x] = __dadd_rn(__dadd_rn(lo_s[threadIdx.x], lo_s[threadIdx.x + w]), e2);
+      ab_s[threadIdx.x] = __dadd_rn(ab_s[threadIdx.x], ab_s[threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  hi_out = hi_s[0];
+  lo_out = lo_s[0];
+  ab_out = ab_s[0];
+}
+
+// s_out = stable_sum(x) given S_final and the chunk partials (one CTA of kRedThr)
+__global__ void __launch_bounds__(kRedThr) neumaier_final_kernel(
+    const double* __restrict__ x, long long n, const double* __restrict__ Sfinal,
+    const double* __restrict__ part, int nchunks, double* __restrict__ s_out,
+    int* __restrict__ status, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  double hi, lo, ab;
+  dd_block_sum(part, 3, nchunks, hi, lo, ab);
+  if (threadIdx.x != 0) return;
   // exact c (double-double) and the drift bound of the sequential c: <= u * sum_k |c_k|,
   // |c_k| <= sum |e|  =>  B <= n u sum|e| (with slack)
   const double S = *Sfinal;
@@ -770,18 +1131,17 @@ __global__ void __launch_bounds__(kThr) check_last_kernel(const double* __restri
   }
 }
 
-__global__ void check_final_kernel(const double* __restrict__ part, const long long* __restrict__ lastpos,
-                                   int nchunks, long long* __restrict__ last, int* __restrict__ status) {
-  if (threadIdx.x != 0) return;
-  double hi = 0.0, lo = 0.0;
+__global__ void __launch_bounds__(kRedThr) check_final_kernel(const double* __restrict__ part,
+                                                               const long long* __restrict__ lastpos,
+                                                               int nchunks, long long* __restrict__ last,
+                                                               int* __restrict__ status) {
+  __shared__ long long sml[32];
   long long lp = -1;
-  for (int k = 0; k < nchunks; ++k) {
-    double s2, e2;
-    two_sum(hi, part[2 * k], s2, e2);
-    hi = s2;
-    lo = __dadd_rn(__dadd_rn(lo, part[2 * k + 1]), e2);
-    lp = max(lp, lastpos[k]);
-  }
+  for (int k = threadIdx.x; k < nchunks; k += kRedThr) lp = max(lp, lastpos[k]);
+  lp = -block_min_ll<kRedThr>(-lp, sml);
+  double hi, lo, ab;
+  dd_block_sum(part, 2, nchunks, hi, lo, ab);
+  if (threadIdx.x != 0) return;
   const double sum = __dadd_rn(hi, lo);
   if (fabs(sum - 1.0) > 1e-12) atomicOr(status, kNotOne);
   *last = lp;
@@ -864,25 +1224,30 @@ static int nchunks_of(long long n) { return (int)((n + kChunk - 1) / kChunk); }
 size_t sampler_workspace_doubles(long long n) {
   const size_t nc = (size_t)nchunks_of(n);
   // p / x1 (n), S (n), csum (nc), assumed (nc ints), agg (nc * 6), starts (nc * 3),
-  // neumaier partials (3 nc), check partials (2 nc), lastpos (nc), scalars (16)
-  return 2 * (size_t)n + nc * (1 + 1 + 6 + 3 + 3 + 2 + 1) + 64;
+  // neumaier partials (3 nc), check partials (2 nc), lastpos (nc), scalars (16),
+  // assumed2 (nc ints), subagg (nc * 2 * 16 * 6), substarts (nc * 16 * 3)
+  return 2 * (size_t)n + nc * (1 + 1 + 6 + 3 + 3 + 2 + 1) + 64 + nc * (1 + 192 + 48);
 }
 
 struct ScanBufs {
   double* csum;
   int* assumed;
+  int* assumed2;
   ChunkAgg* agg;
   ChunkStart* starts;
+  ChunkAgg* subagg;
+  ChunkStart* substarts;
 };
 
 static cudaError_t exact_scan(const double* x, long long n, double* out, double* total,
                               int* status, int bad_flag, const ScanBufs& b, cudaStream_t st) {
   const int nc = nchunks_of(n);
   chunk_sums_kernel<<<nc, kThr, 0, st>>>(x, n, b.csum);
-  chunk_plan_kernel<<<1, 1024, 0, st>>>(b.csum, nc, n, b.assumed);
-  chunk_agg_kernel<<<nc, kThr, 0, st>>>(x, n, b.assumed, b.agg);
-  chunk_walk_kernel<<<1, kCThr, 0, st>>>(x, n, nc, b.agg, b.starts, out, total, status, bad_flag);
-  if (out) chunk_write_kernel<<<nc, kThr, 0, st>>>(x, n, b.starts, out);
+  chunk_plan_kernel<<<1, 1024, 0, st>>>(b.csum, nc, n, b.assumed, b.assumed2);
+  chunk_agg_kernel<<<nc, kThr, 0, st>>>(x, n, b.assumed, b.assumed2, b.agg, b.subagg);
+  chunk_walk_kernel<<<1, kCThr, 0, st>>>(x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
+                                         total, status, bad_flag);
+  if (out) chunk_write_kernel<<<nc, kThr, 0, st>>>(x, n, b.starts, b.substarts, out);
   return cudaGetLastError();
 }
 
@@ -903,7 +1268,11 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   double* scal = csum + 17 * nc;  // [0] total [1] s [2] acc ; ints after
   int* uni = reinterpret_cast<int*>(scal + 8);
   long long* last = reinterpret_cast<long long*>(scal + 10);
-  ScanBufs b{csum, assumed, agg, starts};
+  double* ext = scal + 64;  // split-chunk buffers
+  int* assumed2 = reinterpret_cast<int*>(ext);
+  ChunkAgg* subagg = reinterpret_cast<ChunkAgg*>(ext + nc);
+  ChunkStart* substarts = reinterpret_cast<ChunkStart*>(ext + nc + (size_t)nc * 192);
+  ScanBufs b{csum, assumed, assumed2, agg, starts, subagg, substarts};
   const int eg = 148 * 8;
   cudaError_t e;
   if (regime == 2) {  // uniform(n): p = 1/n each (sketching.cpp:50-53)
@@ -914,11 +1283,11 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
     normalize_mix_kernel<<<eg, 256, 0, st>>>(w, n, scal + 0, regime, beta, p, uni, status);
     if ((e = exact_scan(p, n, S, scal + 1, status, kBadWeight, b, st)) != cudaSuccess) return e;
     neumaier_terms_kernel<<<nc, kThr, 0, st>>>(p, S, n, npart);
-    neumaier_final_kernel<<<1, 32, 0, st>>>(p, n, scal + 1, npart, nc, scal + 1, status, uni);
+    neumaier_final_kernel<<<1, kRedThr, 0, st>>>(p, n, scal + 1, npart, nc, scal + 1, status, uni);
     divide_kernel<<<eg, 256, 0, st>>>(p, n, scal + 1, uni, status);
   }
   check_last_kernel<<<nc, kThr, 0, st>>>(p, n, cpart, lastpos);
-  check_final_kernel<<<1, 32, 0, st>>>(cpart, lastpos, nc, last, status);
+  check_final_kernel<<<1, kRedThr, 0, st>>>(cpart, lastpos, nc, last, status);
   // cum = naive prefix of p; acc = cum[n-1]
   if ((e = exact_scan(p, n, S, scal + 2, status, kBadWeight, b, st)) != cudaSuccess) return e;
   const long long threads = (L + kDrawsPerThread - 1) / kDrawsPerThread;

@@ -24,5 +24,5 @@ for regime in ["nearly_optimal", "uniform"]:
     b.synchronize()
     _lib.lib.lmra_debug_sampler_stats(st, 1)
     print(regime, n, "ms %.3f" % a.elapsed_time(b),
-          "| walk: certified %d exact %d (nobinade %d, ulp mismatch %d), fast-loop cycles %d, exact cycles %d, seq cycles %d, block iters %d"
+          "| walk: certified %d exact %d split %d (stepped subs %d), run cycles %d, exact cycles %d, split cycles %d, block iters %d"
           % tuple(st[:8]))
