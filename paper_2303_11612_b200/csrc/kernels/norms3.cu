@@ -6,66 +6,256 @@
 // in-order sum of chunk partials, a chunk partial being the fma-sequential sum over 32
 // consecutive fiber entries.  Each element belongs to exactly one chunk per mode, so a
 // 32 x 32 x 32 brick holds complete chunks of all three modes:
-//   pass 1 (this kernel, one read of X): every chunk partial of every mode -> P0, P1, P2
-//          (|X|/32 doubles each)
+//   pass 1 (this kernel, one read of X): chunk partials of modes 0 and 1 -> P0, P1
+//          (|X|/32 doubles each); mode 2 combined in registers (see below)
 //   pass 2 (combine): per column, the chunk partials added in chunk order.
-// Traffic: |X| read + 3 |X|/32 written and read back, vs 3 |X| for three mode passes.
+// Traffic: |X| read + 2 |X|/32 written and read back, vs 3 |X| for three mode passes.
+#include <cmath>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace lmra_dev {
 
 constexpr int kB = 32;          // brick edge = canonical chunk length
 constexpr int kN3Threads = 256;
+constexpr int kN3Stages = 3;    // cp.async ring of 32 x 32 slices
 
-// X[i0, i1, i2], i0 fastest.  Grid: (ceil(I1/32), ceil(I2/32), ceil(I0/32)).
-// P0[c0][i1 + I1*i2]  chunk c0 of mode-0 fibers (over i0)
-// P1[c1][i0 + I0*i2]  chunk c1 of mode-1 fibers (over i1)
-// P2[c2][i0 + I0*i1]  chunk c2 of mode-2 fibers (over i2)
+// X[i0, i1, i2], i0 fastest.  Grid: (ceil(I0/32), ceil(I1/32)); each CTA walks the whole i2
+// extent of its 32 x 32 (i0, i1) column of bricks, one (i0, i1) slice at a time:
+//   mode 0 chunk partial of fibre (i1, i2) over its 32 i0  -> P0[c0][i1 + I1*i2]
+//   mode 1 chunk partial of fibre (i0, i2) over its 32 i1  -> P1[c1][i0 + I0*i2]
+//   mode 2 fibres (i0, i1) lie entirely in the CTA: chunk partials over 32 consecutive i2
+//   are combined in chunk order in registers and written as the final w2 (no P2 round
+//   trip through HBM).
+// Slices stream through a 3-stage cp.async ring so loads stay in flight while the
+// previous slice's partials are formed (the first version loaded synchronously and sat
+// at ~60% of HBM bandwidth).
+// Grids with too few (i0, i1) columns to fill the GPU also split i2 into gridDim.z segments
+// of whole chunks; mode 2 then writes its chunk partials to P2 (combined by pass 2) instead
+// of the in-register total.
 __global__ void __launch_bounds__(kN3Threads) norms3_chunks_kernel(
     const double* __restrict__ x, long long I0, long long I1, long long I2,
-    double* __restrict__ P0, double* __restrict__ P1, double* __restrict__ P2) {
-  __shared__ double slice[kB][kB + 1];  // [i1][i0] of one i2
+    double* __restrict__ P0, double* __restrict__ P1, double* __restrict__ w2,
+    double* __restrict__ P2, long long seg) {
+  __shared__ __align__(16) double ring[kN3Stages][kB][kB + 1];  // [stage][i1][i0]
   const int tid = threadIdx.x;
-  const long long c1 = blockIdx.x, c2 = blockIdx.y, c0 = blockIdx.z;
-  const long long i0b = c0 * kB, i1b = c1 * kB, i2b = c2 * kB;
-  const int n0 = (int)(I0 - i0b < kB ? I0 - i0b : kB), n1 = (int)(I1 - i1b < kB ? I1 - i1b : kB),
-            n2 = (int)(I2 - i2b < kB ? I2 - i2b : kB);
-  // mode-2 accumulators: thread owns (i0 = tid % 32, i1 = tid / 32 + 8k), k < 4
+  const long long c0 = blockIdx.x, c1 = blockIdx.y;
+  const long long i0b = c0 * kB, i1b = c1 * kB;
+  const int n0 = (int)(I0 - i0b < kB ? I0 - i0b : kB), n1 = (int)(I1 - i1b < kB ? I1 - i1b : kB);
+  // loads / mode-2 fibres: thread owns (i0 = tid % 32, i1 = tid / 32 + 8k), k < 4
   const int a0 = tid & 31, a1 = tid >> 5;
-  double acc2[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int k2 = 0; k2 < n2; ++k2) {
-    const long long i2 = i2b + k2;
-    // load the 32 x 32 (i0, i1) slice: rows of 32 contiguous i0 (256 B) per warp
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r1 = a1 + 8 * k;
-      double v = 0.0;
-      if (r1 < n1 && a0 < n0) v = __ldcs(x + (i0b + a0) + I0 * ((i1b + r1) + I1 * i2));
-      slice[r1][a0] = v;
-      acc2[k] = fma(v, v, acc2[k]);  // mode 2: over i2, in order
-    }
-    __syncthreads();
-    if (tid < 32) {  // mode 0 chunk partial of fiber (i1 = tid, i2): over i0 in order
-      if (tid < n1) {
-        double p = 0.0;
-        for (int q = 0; q < n0; ++q) p = fma(slice[tid][q], slice[tid][q], p);
-        P0[c0 * (I1 * I2) + (i1b + tid) + I1 * i2] = p;
-      }
-    } else if (tid < 64) {  // mode 1 chunk partial of fiber (i0 = tid-32, i2): over i1
-      const int r0 = tid - 32;
-      if (r0 < n0) {
-        double p = 0.0;
-        for (int q = 0; q < n1; ++q) p = fma(slice[q][r0], slice[q][r0], p);
-        P1[c1 * (I0 * I2) + (i0b + r0) + I0 * i2] = p;
-      }
-    }
-    __syncthreads();
-  }
+  const double* src[4];
+  bool ok[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r1 = a1 + 8 * k;
-    if (r1 < n1 && a0 < n0) P2[c2 * (I0 * I1) + (i0b + a0) + I0 * (i1b + r1)] = acc2[k];
+    ok[k] = r1 < n1 && a0 < n0;
+    src[k] = x + (ok[k] ? (i0b + a0) + I0 * (i1b + r1) : 0);
   }
+  const long long slab = I0 * I1;
+  const long long z0 = blockIdx.z * seg, z1 = z0 + seg < I2 ? z0 + seg : I2;  // i2 range
+  auto issue = [&](long long i2) {
+    if (i2 < z1) {
+      const int st = (int)(i2 % kN3Stages);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        cp_async8(&ring[st][a1 + 8 * k][a0], ok[k] ? src[k] + slab * i2 : x, ok[k]);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < kN3Stages - 1; ++s) issue(z0 + s);
+  double part2[4] = {0.0, 0.0, 0.0, 0.0}, tot2[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long long i2 = z0; i2 < z1; ++i2) {
+    issue(i2 + kN3Stages - 1);
+    cp_async_wait<kN3Stages - 1>();
+    __syncthreads();
+    const double (*slice)[kB + 1] = ring[i2 % kN3Stages];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double v = slice[a1 + 8 * k][a0];
+      part2[k] = fma(v, v, part2[k]);  // mode 2: over i2, in order within the chunk
+    }
+    if ((i2 & (kB - 1)) == kB - 1 || i2 == I2 - 1) {  // chunk of 32 i2 complete
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (P2) {
+          if (ok[k]) P2[(i2 / kB) * slab + (i0b + a0) + I0 * (i1b + a1 + 8 * k)] = part2[k];
+        } else {
+          tot2[k] = tot2[k] + part2[k];
+        }
+        part2[k] = 0.0;
+      }
+    }
+    // modes 0 / 1: the 32 values first (independent loads), then the in-order fma chain;
+    // entries past the tensor edge were zero-filled, and fma(0, 0, p) = p exactly
+    if (tid < 64) {
+      const int f = tid & 31;
+      double v[kB];
+      if (tid < 32) {
+#pragma unroll
+        for (int q = 0; q < kB; ++q) v[q] = slice[f][q];  // fibre (i1 = f, i2) over i0
+      } else {
+#pragma unroll
+        for (int q = 0; q < kB; ++q) v[q] = slice[q][f];  // fibre (i0 = f, i2) over i1
+      }
+      double p = 0.0;
+#pragma unroll
+      for (int q = 0; q < kB; ++q) p = fma(v[q], v[q], p);
+      if (tid < 32) {
+        if (f < n1) P0[c0 * (I1 * I2) + (i1b + f) + I1 * i2] = p;
+      } else {
+        if (f < n0) P1[c1 * (I0 * I2) + (i0b + f) + I0 * i2] = p;
+      }
+    }
+    __syncthreads();  // the slot is refilled by the next iteration's issue
+  }
+  if (!P2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (ok[k]) w2[(i0b + a0) + I0 * (i1b + a1 + 8 * k)] = tot2[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA version (I0 even: the tensor map needs 16-byte row strides).  One producer warp
+// streams each (i0, i1) slice of the CTA's 32 x 32 column as two 16 x 32 boxes (128-byte
+// swizzle) into a ring of shared-memory stages guarded by mbarriers; eight consumer warps
+// form the chunk partials exactly as above.  One TMA instruction per box replaces 1024
+// per-element cp.async (whose issue cost, ~8 cycles per warp instruction, would itself
+// approach the per-SM share of HBM bandwidth).
+// ---------------------------------------------------------------------------
+constexpr int kTStages = 6;
+constexpr int kTCons = 256;                 // consumer threads (8 warps)
+constexpr int kTThreads = kTCons + 32;      // + producer warp
+constexpr int kTStageBytes = 2 * 32 * 128;  // two boxes of 32 rows x 16 doubles
+
+// element (row r = i1 - i1b, column c = i0 - i0b) of a stage, 128-byte swizzle: the 16-byte
+// chunk j of a 128-byte row r sits at chunk j ^ (r & 7)
+__device__ __forceinline__ int sw_idx(int r, int c) {
+  return (c >> 4) * 512 + r * 16 + ((((c & 15) >> 1) ^ (r & 7)) << 1) + (c & 1);
+}
+
+__global__ void __launch_bounds__(kTThreads, 3) norms3_tma_kernel(
+    const __grid_constant__ CUtensorMap tmap, long long I0, long long I1, long long I2,
+    double* __restrict__ P0, double* __restrict__ P1, double* __restrict__ w2,
+    double* __restrict__ P2, long long seg) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  // 1024-byte alignment for the 128-byte swizzle, kept as an offset into the shared array
+  // so the compiler still emits shared-memory loads (not generic ones)
+  unsigned char* base = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+  double* ring = reinterpret_cast<double*>(base);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kTStages * kTStageBytes);
+  uint64_t* empty = full + kTStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long c0 = blockIdx.x, c1 = blockIdx.y;
+  const long long i0b = c0 * kB, i1b = c1 * kB;
+  const int n0 = (int)(I0 - i0b < kB ? I0 - i0b : kB), n1 = (int)(I1 - i1b < kB ? I1 - i1b : kB);
+  const long long z0 = blockIdx.z * seg, z1 = z0 + seg < I2 ? z0 + seg : I2;
+  if (tid == 0) {
+    for (int s = 0; s < kTStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTCons / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kTCons / 32) {  // producer
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (long long i2 = z0; i2 < z1; ++i2) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], kTStageBytes);
+        double* dst = ring + stage * (kTStageBytes / 8);
+        tma_load_3d(dst, &tmap, &full[stage], (int)i0b, (int)i1b, (int)i2);
+        tma_load_3d(dst + 512, &tmap, &full[stage], (int)i0b + 16, (int)i1b, (int)i2);
+        if (++stage == kTStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int a0 = tid & 31, a1 = tid >> 5;  // mode-2 fibres (i0 = a0, i1 = a1 + 8k)
+  double part2[4] = {0.0, 0.0, 0.0, 0.0}, tot2[4] = {0.0, 0.0, 0.0, 0.0};
+  int stage = 0;
+  unsigned phase = 0;
+  for (long long i2 = z0; i2 < z1; ++i2) {
+    mbar_wait(&full[stage], phase);
+    const double* sl = ring + stage * (kTStageBytes / 8);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double v = sl[sw_idx(a1 + 8 * k, a0)];
+      part2[k] = fma(v, v, part2[k]);  // mode 2: over i2, in order within the chunk
+    }
+    if ((i2 & (kB - 1)) == kB - 1 || i2 == I2 - 1) {  // chunk of 32 i2 complete
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (P2) {
+          if (a0 < n0 && a1 + 8 * k < n1)
+            P2[(i2 / kB) * (I0 * I1) + (i0b + a0) + I0 * (i1b + a1 + 8 * k)] = part2[k];
+        } else {
+          tot2[k] = tot2[k] + part2[k];
+        }
+        part2[k] = 0.0;
+      }
+    }
+    if (tid < 64) {  // modes 0 / 1: the in-order fma chain over 32 entries (zero past the edge)
+      const int f = tid & 31;
+      double p = 0.0;
+      if (tid < 32) {
+#pragma unroll
+        for (int q = 0; q < kB; q += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = sl[sw_idx(f, q + u)];  // fibre (i1 = f) over i0
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p = fma(v[u], v[u], p);
+        }
+        if (f < n1) P0[c0 * (I1 * I2) + (i1b + f) + I1 * i2] = p;
+      } else {
+#pragma unroll
+        for (int q = 0; q < kB; q += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = sl[sw_idx(q + u, f)];  // fibre (i0 = f) over i1
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p = fma(v[u], v[u], p);
+        }
+        if (f < n0) P1[c1 * (I0 * I2) + (i0b + f) + I0 * i2] = p;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == kTStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  if (!P2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (a0 < n0 && a1 + 8 * k < n1) w2[(i0b + a0) + I0 * (i1b + a1 + 8 * k)] = tot2[k];
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
 }
 
 // w[j] = sum_c P[c][j] in chunk order (c = 0, 1, ...): the canonical combine
@@ -78,9 +268,17 @@ __global__ void chunk_combine_kernel(const double* __restrict__ P, long long J, 
   w[j] = total;
 }
 
+// i2 segments (whole chunks) so that the grid has >= 4 CTAs per SM
+static long long norms3_segments(long long I0, long long I1, long long I2) {
+  const long long cols = ((I0 + kB - 1) / kB) * ((I1 + kB - 1) / kB);
+  const long long c2 = (I2 + kB - 1) / kB;
+  long long z = (4 * 148 + cols - 1) / cols;
+  return z < 1 ? 1 : (z > c2 ? c2 : z);
+}
+
 size_t norms3_workspace_doubles(long long I0, long long I1, long long I2) {
   const long long c0 = (I0 + kB - 1) / kB, c1 = (I1 + kB - 1) / kB, c2 = (I2 + kB - 1) / kB;
-  return (size_t)(c0 * I1 * I2 + c1 * I0 * I2 + c2 * I0 * I1);
+  return (size_t)(c0 * I1 * I2 + c1 * I0 * I2 + c2 * I0 * I1);  // P2 when i2 is split
 }
 
 cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long I2, double* w0,
@@ -88,14 +286,60 @@ cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long
   const long long c0 = (I0 + kB - 1) / kB, c1 = (I1 + kB - 1) / kB, c2 = (I2 + kB - 1) / kB;
   double* P0 = work;
   double* P1 = P0 + c0 * I1 * I2;
-  double* P2 = P1 + c1 * I0 * I2;
-  dim3 grid((unsigned)c1, (unsigned)c2, (unsigned)c0);
-  norms3_chunks_kernel<<<grid, kN3Threads, 0, st>>>(x, I0, I1, I2, P0, P1, P2);
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  const bool tma_ok = enc && I0 % 2 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                      I0 < (1ll << 31) && I1 < (1ll << 31) && I2 < (1ll << 31);
+  long long zs = norms3_segments(I0, I1, I2);
+  if (tma_ok) {
+    // wave quantisation: the memory-bound kernel runs at full bandwidth only while every
+    // SM holds its full set of CTAs, so choose the number of i2 segments whose CTA count
+    // best fills whole waves (a split costs the mode-2 chunk partials' round trip, ~6% of
+    // the tensor read)
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = kTStages * kTStageBytes + 2 * kTStages * sizeof(uint64_t) + 1024;
+    static unsigned long long attr_done0 = 0;  // the occupancy query needs the smem attribute
+    cudaError_t ea = ensure_smem_attr(reinterpret_cast<const void*>(norms3_tma_kernel), smem, attr_done0);
+    if (ea != cudaSuccess) return ea;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, norms3_tma_kernel, kTThreads, smem);
+    const double slots = (double)sms * (per_sm > 0 ? per_sm : 1);
+    const long long cols = c0 * c1;
+    auto fill = [&](long long z) {
+      const double n = (double)(cols * z);
+      return n / (std::ceil(n / slots) * slots) - (z > 1 ? 0.06 : 0.0);
+    };
+    long long best = 1;
+    for (long long z = 2; z <= 8 && z <= c2; ++z)
+      if (fill(z) > fill(best) + 1e-9) best = z;
+    zs = best;
+  }
+  double* P2 = zs > 1 ? P1 + c1 * I0 * I2 : nullptr;
+  const long long seg = ((c2 + zs - 1) / zs) * kB;
+  dim3 grid((unsigned)c0, (unsigned)c1, (unsigned)((I2 + seg - 1) / seg));
+  CUtensorMap tmap;
+  if (tma_ok) {
+    const cuuint64_t gdim[3] = {(cuuint64_t)I0, (cuuint64_t)I1, (cuuint64_t)I2};
+    const cuuint64_t gstride[2] = {(cuuint64_t)I0 * 8, (cuuint64_t)(I0 * I1) * 8};
+    const cuuint32_t box[3] = {16, 32, 1}, estride[3] = {1, 1, 1};
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), gdim, gstride, box,
+            estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    static unsigned long long attr_done = 0;
+    const size_t smem = kTStages * kTStageBytes + 2 * kTStages * sizeof(uint64_t) + 1024;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(norms3_tma_kernel), smem, attr_done);
+    if (e != cudaSuccess) return e;
+    norms3_tma_kernel<<<grid, kTThreads, smem, st>>>(tmap, I0, I1, I2, P0, P1, w2, P2, seg);
+  } else {
+    norms3_chunks_kernel<<<grid, kN3Threads, 0, st>>>(x, I0, I1, I2, P0, P1, w2, P2, seg);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   chunk_combine_kernel<<<(unsigned)((I1 * I2 + 255) / 256), 256, 0, st>>>(P0, I1 * I2, (int)c0, w0);
   chunk_combine_kernel<<<(unsigned)((I0 * I2 + 255) / 256), 256, 0, st>>>(P1, I0 * I2, (int)c1, w1);
-  chunk_combine_kernel<<<(unsigned)((I0 * I1 + 255) / 256), 256, 0, st>>>(P2, I0 * I1, (int)c2, w2);
+  if (P2)
+    chunk_combine_kernel<<<(unsigned)((I0 * I1 + 255) / 256), 256, 0, st>>>(P2, I0 * I1, (int)c2, w2);
   return cudaGetLastError();
 }
 
