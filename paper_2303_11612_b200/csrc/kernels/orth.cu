@@ -448,6 +448,7 @@ __device__ __forceinline__ void regs_to_tile(const double (&a)[2][RPW], int rows
 // per lane by a shuffle instead of reloading both columns of every pair from shared memory
 // (the previous round-robin version was bound on shared-memory bandwidth at ~1900 cycles a
 // round).  Offline simulation on the cfg4 sketches: 7-8 sweeps, as with round-robin.
+// Sketches with s <= 16 / 32 use 16 / 32 slots (15 / 31 rounds a sweep).
 // ---------------------------------------------------------------------------
 __device__ int g_jacobi_sweeps;
 #ifdef LMRA_JACOBI_CLOCKS
@@ -458,46 +459,61 @@ __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// 1/sqrt(x) for normal positive x: the hardware approximation plus two Newton steps
+// (full double precision within an ulp or two) -- a short dependent chain, where the
+// library rsqrt/sqrt carry special-case branches on the Jacobi's critical path.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
 // Rotation for the pair (top, bottom) with squared norms a, b and inner product c: the
 // smaller root t of t^2 + 2 zeta t - 1 = 0 (zeta = (b - a) / 2c), written without forming
 // t: with d = b - a, r = sqrt(d^2 + 4c^2), u = |d| + r:  1 + t^2 = 2r / u, so
-//   cos = u / sqrt(2 r u),  sin = sign(d) 2c / sqrt(2 r u)
-// (one sqrt and one rsqrt on the chain instead of sqrt, reciprocal and rsqrt).
+//   cos = u / sqrt(2 r u),  sin = sign(d) 2c / sqrt(2 r u).
+// G is pre-scaled by a power of two (max |g| in [1, 2)), so a, b, c neither overflow nor
+// need the exponent-scaled path; the rotation is orthogonal to an ulp or two regardless of
+// the accuracy of t.
 __device__ __forceinline__ bool jacobi_angle(double a, double b, double c, double tol2,
                                              double& cs, double& sn) {
-  bool rot;
-  double sa = a, sb = b, sc = c;
-  if (fmax(a, b) < 1e150) {
-    rot = c != 0.0 && c * c > tol2 * (a * b);
-  } else {  // huge norms: exponent-scaled
-    const int ea = ilogb(fmax(fmax(a, b), fabs(c)));
-    sa = ldexp(a, -ea);
-    sb = ldexp(b, -ea);
-    sc = ldexp(c, -ea);
-    rot = c != 0.0 && sc * sc > tol2 * (sa * sb);
-  }
   cs = 1.0;
   sn = 0.0;
-  if (rot) {
-    const double d = sb - sa;
-    const double r = sqrt(fma(d, d, 4.0 * sc * sc));
-    const double u = fabs(d) + r;
-    const double qn = rsqrt(2.0 * r * u);
-    cs = u * qn;
-    sn = (d >= 0.0 ? 2.0 * sc : -2.0 * sc) * qn;
-  }
-  return rot;
+  if (!(c != 0.0 && c * c > tol2 * (a * b))) return false;
+  const double d = b - a;
+  const double q = fma(d, d, 4.0 * c * c);
+  const double r = q * rsqrt_nr(q);
+  const double u = fabs(d) + r;
+  const double qn = rsqrt_nr(2.0 * r * u);
+  cs = u * qn;
+  sn = (d >= 0.0 ? 2.0 * c : -2.0 * c) * qn;
+  return true;
 }
 
+// Per round: every G warp writes its partial (a, b, c) of each lane's pair; after a named
+// barrier among the G warps, warp 0 sums them (fixed order) and forms the angles; a second
+// barrier (G and J warps) releases the rotation.  (Measured alternatives -- every G warp
+// forming all angles itself, or J warps consuming the angles asynchronously from an
+// mbarrier ring -- were slower: the angle chain is issue-bound when replicated, and the
+// ring's extra synchronisation costs more than the J rotation it takes off the barrier.)
 __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem& q) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const bool isG = w < 8;
   const int row0 = (w & 7) * 8;
   double* part = q.part;  // [3][8 warps][32 lanes]
   double* csn = q.fval;   // [round parity][cos 32 | sin 32]: q.fval and q.rowk (128 doubles)
-  int* flags = q.pidx;    // per-sweep "rotated" flags
+  int* flags = q.pidx;    // [0, 60) per-sweep "rotated", [63] result
+  // slots: the next power of two >= s (16, 32 or 64); lanes >= nh hold nothing
+  const int nh = s <= 16 ? 8 : (s <= 32 ? 16 : 32);
+  // rows: warps 0 .. gw-1 hold G (8 rows each), warps 8 .. 8+gw-1 the same rows of J (rows
+  // >= s of J stay zero for every real column); the other warps sit the Jacobi out
+  const int gw = (s + 7) / 8;
+  const bool active = (w & 7) < gw;
   double T[8], B[8];
-  int cT = l, cB = l + 32;
+  int cT = l < nh ? l : 1 << 20, cB = l < nh ? l + nh : 1 << 20;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = row0 + i;
@@ -514,11 +530,12 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
   const double tol2 = tol * tol;
   bool converged = false;
   int round = 0;  // global round counter (csn parity)
-  // G warps: [rotate with round r-1 | shift | partials r] -> bar A (G warps) -> warp 0 angles
-  // -> bar B (all).  J warps only wait at bar B and apply round r while the G warps and
-  // warp 0 work on round r + 1, so the J rotations are off the critical path.
+#ifdef LMRA_JACOBI_CLOCKS
+  long long jc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  if (!active) goto done;
   for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
-    for (int group = 32;; group >>= 1) {
+    for (int group = nh;; group >>= 1) {
       const int src = (l & ~(group - 1)) | ((l + 1) & (group - 1));
       for (int r = 0; r < group; ++r, ++round) {
         double* cs_r = csn + 64 * (round & 1);
@@ -537,7 +554,7 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
           part[(0 * 8 + w) * 32 + l] = a;
           part[(1 * 8 + w) * 32 + l] = b;
           part[(2 * 8 + w) * 32 + l] = c;
-          named_bar(1, 256);
+          named_bar(1, 32 * gw);
 #ifdef LMRA_JACOBI_CLOCKS
           k1 = clock64();
 #endif
@@ -545,9 +562,9 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
             double pa[8], pb[8], pc[8];
 #pragma unroll
             for (int w2 = 0; w2 < 8; ++w2) {
-              pa[w2] = part[(0 * 8 + w2) * 32 + l];
-              pb[w2] = part[(1 * 8 + w2) * 32 + l];
-              pc[w2] = part[(2 * 8 + w2) * 32 + l];
+              pa[w2] = w2 < gw ? part[(0 * 8 + w2) * 32 + l] : 0.0;
+              pb[w2] = w2 < gw ? part[(1 * 8 + w2) * 32 + l] : 0.0;
+              pc[w2] = w2 < gw ? part[(2 * 8 + w2) * 32 + l] : 0.0;
             }
             const double sa = ((pa[0] + pa[1]) + (pa[2] + pa[3])) + ((pa[4] + pa[5]) + (pa[6] + pa[7]));
             const double sb = ((pb[0] + pb[1]) + (pb[2] + pb[3])) + ((pb[4] + pb[5]) + (pb[6] + pb[7]));
@@ -561,7 +578,7 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
           k2 = clock64();
 #endif
         }
-        __syncthreads();  // bar B: angles of this round visible to every warp
+        named_bar(2, 64 * gw);  // bar B: angles of this round visible to every active warp
 #ifdef LMRA_JACOBI_CLOCKS
         const long long k3 = clock64();
 #endif
@@ -577,18 +594,15 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
         for (int i = 0; i < 8; ++i) B[i] = __shfl_sync(0xffffffffu, B[i], src);
         cB = __shfl_sync(0xffffffffu, cB, src);
 #ifdef LMRA_JACOBI_CLOCKS
-        if (threadIdx.x == 0) {  // k0->k1 partials + bar A, k1->k2 angles, k2->k3 bar B, k3->k4 rotate
+        {  // k0->k1 partials + bar A, k1->k2 angles, k2->k3 bar B, k3->k4 rotate (registers)
           const long long k4 = clock64();
-          g_jclk[0] += k1 - k0;
-          g_jclk[1] += k2 - k1;
-          g_jclk[2] += k3 - k2;
-          g_jclk[3] += k4 - k3;
-          g_jclk[4] += 1;
-        }
-        if (threadIdx.x == 256) {  // a J warp: bar B wait and its rotation
-          const long long k4 = clock64();
-          g_jclk[5] += k3 - k0;
-          g_jclk[6] += k4 - k3;
+          jc[0] += k1 - k0;
+          jc[1] += k2 - k1;
+          jc[2] += k3 - k2;
+          jc[3] += k4 - k3;
+          jc[4] += 1;
+          jc[5] += k3 - k0;
+          jc[6] += k4 - k3;
         }
 #endif
       }
@@ -618,22 +632,34 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
       if (threadIdx.x == 0) g_jacobi_sweeps = sweep + 1;
     }
   }
+done:
+#ifdef LMRA_JACOBI_CLOCKS
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 5; ++i) g_jclk[i] = jc[i];
+  if (threadIdx.x == 256)
+    for (int i = 5; i < 7; ++i) g_jclk[i] = jc[i];
+#endif
   __syncthreads();
+  if (active) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = row0 + i;
-    if (isG) {
-      if (r < s) {
-        if (cT < s) G[r + (size_t)s * cT] = T[i];
-        if (cB < s) G[r + (size_t)s * cB] = B[i];
+    for (int i = 0; i < 8; ++i) {
+      const int r = row0 + i;
+      if (isG) {
+        if (r < s) {
+          if (cT < s) G[r + (size_t)s * cT] = T[i];
+          if (cB < s) G[r + (size_t)s * cB] = B[i];
+        }
+      } else if (cT < 64) {  // (inactive lanes hold no column)
+        J[r + 64 * cT] = T[i];
+        J[r + 64 * cB] = B[i];
       }
-    } else {
-      J[r + 64 * cT] = T[i];
-      J[r + 64 * cB] = B[i];
     }
   }
   __syncthreads();
-  return converged;
+  // converged is only known to the active warps: publish it
+  if (threadIdx.x == 0) flags[63] = converged ? 1 : 0;
+  __syncthreads();
+  return flags[63] != 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -708,6 +734,24 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     }
   }
   __syncthreads();
+  {  // G *= 2^-e with max |G| in [1, 2) (exact; only J and the singular values' order are used)
+    double mx = 0.0;
+    for (int e = threadIdx.x; e < s * s; e += kQThreads) mx = fmax(mx, fabs(G[e]));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    if (l == 0) q.normp[w] = mx;
+    __syncthreads();
+    double gm = 0.0;
+    for (int k = 0; k < kQWarps; ++k) gm = fmax(gm, q.normp[k]);
+    if (gm > 0.0 && isfinite(gm)) {
+      const int ex = ilogb(gm);
+      for (int e = threadIdx.x; e < s * s; e += kQThreads) G[e] = ldexp(G[e], -ex);
+    }
+    __syncthreads();
+  }
   const bool converged = reg_jacobi(G, s, J, jacobi_tol, q);
   // singular values = column norms of G, fixed order
   for (int c = w; c < s; c += kQWarps) {

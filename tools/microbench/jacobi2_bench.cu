@@ -29,7 +29,7 @@ int main() {
     srand(1);
     for (int i = 0; i < s; ++i)
       for (int j = i; j < s; ++j)  // R upper, graded rows; G = R^T
-        h[j + s * i] = ((rand() / (double)RAND_MAX) - 0.5) * pow(10.0, -10.0 * i / s) * (i == j ? 4.0 : 1.0);
+        h[j + s * i] = ((rand() / (double)RAND_MAX) - 0.5) * pow(10.0, -10.0 * i / s) * (i == j ? 4.0 : 1.0) * 0.5;
     double* d;
     cudaMalloc(&d, s * s * 8);
     cudaMemcpy(d, h.data(), s * s * 8, cudaMemcpyHostToDevice);
