@@ -155,7 +155,10 @@ class ClockSampler:
 
 
 def phase_cost(bc, phase: str, dims_local=None):
-    """Algorithmic (flops, bytes) of ONE launch of a phase, for the roofline."""
+    """Algorithmic (flops, bytes) of ONE launch of a phase, for the roofline.  A "_i8" suffix
+    marks a contraction run on the int8 tensor cores (same algorithmic cost)."""
+    if phase.endswith("_i8"):
+        phase = phase[:-3]
     dims = list(dims_local or bc.dims)
     cfg = bc.cfg
     N = len(dims)
@@ -190,16 +193,26 @@ def roofline(bc, phases, steps, dims_local=None):
     # alone on the main stream (core / shrink contractions, the fused norms pass); the
     # per-mode phases of T-HOSVD overlap on their own streams, so their event times
     # include contention and are not a per-kernel duration
+    # ("norms" only as the single fused 3-mode pass: ST-HOSVD's per-mode norms read shrinking
+    # tensors of different sizes under one phase name)
     cands = [(ms, name, cnt) for name, (ms, cnt) in phases.items()
-             if phase_cost(bc, name, dims_local)
-             and (name != "norms" or bc.alg in ("alg2", "alg5") or len(bc.dims) == 3)]
+             if phase_cost(bc, name, dims_local) and (name != "norms" or cnt == steps)]
     if not cands:
         return None
     ms, name, cnt = max(cands)
     flops, byts = phase_cost(bc, name, dims_local)
     per_launch_ms = ms / cnt
     ridge = P64_MEASURED_TFLOPS * 1e12 / (hbm * 1e9)
-    if flops / byts > ridge:
+    if name.endswith("_i8"):
+        # fp64 contraction emulated with exact int8 digit products on tcgen05 (ttm_i8.cu): it
+        # streams the tensor once, so its roofline is HBM; the fp64-equivalent rate is reported
+        # beside it (above the 37 TF DMMA peak by construction)
+        achieved = byts / (per_launch_ms / 1e3) / 1e9
+        out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+               "frac": round(achieved / hbm, 4), "peak_source": src,
+               "fp64_equiv_tflops": round(flops / (per_launch_ms / 1e3) / 1e12, 2),
+               "impl": "int8 tcgen05 digit products (ttm_i8.cu)"}
+    elif flops / byts > ridge:
         achieved = flops / (per_launch_ms / 1e3) / 1e12
         out = {"bound": "tensor", "achieved": round(achieved, 3), "peak": P64_MEASURED_TFLOPS,
                "unit": "TFLOP/s", "frac": round(achieved / P64_MEASURED_TFLOPS, 4),

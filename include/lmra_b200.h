@@ -150,6 +150,14 @@ void lmra_result_free(lmra_result* r);
 int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
                         int mode, const double* b, uint64_t b_rows, double* y);
 /* c = (A A^T)^q G  (linalg.cpp:62-80), A rows x cols, G rows x s */
+/* y (mu x J) = q^T x for the mode-0 view of a tensor (x: K x J, column j contiguous; q: K x mu
+ * column-major; w[j] = canonical squared norm of column j), computed on the int8 tensor cores
+ * with exact digit products (~1e-13 relative).  Replaces, for the core's first contraction,
+ * mode_n_product (tensor.hpp:56-57) as called by core_from_factors (tucker.cpp:81-92) and the
+ * ST-HOSVD shrink (tucker.cpp:397-420).  Device pointers; K even <= 4096, mu <= 64. */
+int lmra_mode0_product_i8(lmra_context* ctx, const double* x, uint64_t K, uint64_t J, const double* q,
+                          int mu, const double* w, double* y);
+
 int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uint64_t cols,
                           const double* g, uint64_t s, int q, int strategy, double* c);
 /* u = top-mu left singular vectors of c with the reference's sign rule (linalg.cpp:82-87) */

@@ -69,6 +69,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef LMRA_MBAR_SUSPEND_NS
+#define LMRA_MBAR_SUSPEND_NS 0x989680
+#endif
+constexpr unsigned kMbarSuspendNs = LMRA_MBAR_SUSPEND_NS;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred P1;\n"
@@ -76,7 +80,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       " @!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680)  // suspend-time hint: the warp sleeps in hardware instead of spinning
+      "r"(parity), "r"(kMbarSuspendNs)  // suspend-time hint: the warp sleeps in hardware instead of spinning
       : "memory");
 }
 // 3-D tiled TMA load of one box into shared memory, completion counted on `bar`

@@ -56,6 +56,15 @@ size_t orth_workspace_doubles(long long I, int s);
 cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, double* work,
                         int* status, cudaStream_t st);
 
+// Mode-0 contraction on the int8 tensor cores (ttm_i8.cu): y (mu x J) = q^T x with x K x J
+// (column j contiguous), q K x mu column-major, w[j] the canonical squared norm of column j
+// (sets the column's fixed-point scale).  ~1e-13 relative accuracy; supported for K even,
+// K <= 4096, mu <= 64, x 16-byte aligned.
+bool ttm_i8_supported(long long K, long long J, int mu, const double* x);
+size_t ttm_i8_workspace_bytes(long long K, int mu);
+cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const double* q, int mu,
+                          const double* w, double* y, void* work, cudaStream_t st);
+
 // ---- synthetic generators (device) ----
 // element e of the normal sequence of PCG32 stream (seed, stream), Box-Muller pairs as in rng.hpp
 cudaError_t launch_gen_normals(double* out, long long n, uint64_t seed, uint64_t stream,

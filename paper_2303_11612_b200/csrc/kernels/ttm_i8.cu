@@ -1,0 +1,463 @@
+// ttm_i8.cu -- the fp64 mode-0 contraction Y = Q^T X on the int8 tensor cores (tcgen05).
+//
+// fp64 has no tcgen05 kind; DMMA (mma.sync f64) peaks at 37 TF/s, which makes the core
+// contraction of cfg4 (2 * 50 * 1000 * 10^6 flop) compute-bound at ~2.7 ms.  This kernel
+// emulates it exactly enough (~1e-13 relative, far inside the 1e-10 parity tolerance) with
+// integer tensor-core products (the Ozaki idea: split into fixed-point digits, multiply
+// digits exactly, recombine):
+//   x_kj = 2^(ex_j - 47) V_kj,  V = round(x 2^(47-ex_j)),  |V| < 2^46  (ex_j from the
+//          canonical column norm: 2^ex_j >= 2 ||x_j|| >= 2 max_k |x_kj|)
+//   q_km = 2^(eq_m - 47) U_km   (eq_m from max_k |q_km|)
+//   V = sum_t d_t 2^(8t) with balanced signed digits d_t in [-128, 128): the bytes of V + C,
+//   C = 128 sum_t 2^(8t), each XOR 0x80 -- one fma (V + C lands in the low bits of
+//   fma(x, 2^(47-ex), 1.5 2^52 + C)) and one LOP3 per 4 digits.
+//   y_mj = 2^(ex_j + eq_m - 94) sum_{t,s} 2^(8(t+s)) sum_k d_t[k,j] e_s[k,m]
+// Each digit product is an exact int8 x int8 -> int32 MMA; products with t + s >= 5 are kept
+// (21 of 36) and summed per level L = t + s in TMEM (int32, exact for K <= 4096).  The
+// dropped products are zero-mean (balanced digits), ~2^-46 relative to |x||q| per term,
+// growing like sqrt(K): ~1e-13 relative on the BASELINE shapes.
+//
+// Tile: 128 columns of X (the MMA's M) x all of K, N = mu rounded up to 16 (<= 64).  Warp roles
+// (one CTA per SM, persistent over tiles):
+//   warp 8 (2 lanes) TMA: X K-steps (32 k x 128 j, two 16 x 128 boxes, 128 B swizzle) into a
+//                    5-stage ring freed by the slicers; the K-step's pre-split Q digits (bulk
+//                    copy) into a 2-stage ring freed by the MMA
+//   warps 0-7        digit split, two groups of 4 warps taking alternate K-steps (one A buffer
+//                    each): thread j converts its column's 32 doubles to 6 x 32 digit
+//                    bytes and writes them to TMEM with tcgen05.st (the A operand is read from
+//                    TMEM, so shared memory only feeds the small B operand); after the last
+//                    K-step group 0 drains the 7 level accumulators, recombines in fp64, stores Y
+//   warp 9 (1 lane)  tcgen05.mma.kind::i8: 26 MMAs per K-step (A = TMEM digits, B = smem Q
+//                    digits), commits to the ring / A-buffer / accumulator mbarriers
+// TMEM: 6 levels x N columns of accumulators + 2 buffers x 48 columns of A digits (<= 480).
+// MMA grouping: the Q digits are stored as consecutive N-row blocks, so digits s..s+g-1 form
+// one B operand of g N rows and one MMA computes (t, s), ..., (t, s+g-1) into the adjacent
+// level accumulators t+s-5, ... (levels are adjacent N-column blocks).  int8 MMAs with N <= 64
+// cost ~45 cycles regardless of N (measured, tools/microbench/umma_rate.cu) while N >= 128 runs
+// at the full 8192 MAC/clk, so 9 grouped MMAs (~690 cycles per K-step) replace 21 (~955).
+// Accumulators are zeroed by the epilogue warps (every MMA accumulates).
+#include <cmath>
+#include <cstdlib>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace lmra_dev {
+
+namespace {
+
+constexpr int kI8Stages = 4;   // X ring (released by the slicers)
+constexpr int kI8QStages = 5;  // Q-digit ring (released by the MMA; the L2 -> smem copy needs
+                               // several K-steps of lead)
+constexpr int kI8Tile = 128;                 // columns of X per tile (MMA M)
+constexpr int kI8Kstep = 32;                 // k per MMA (int8)
+constexpr int kI8XBytes = kI8Kstep * kI8Tile * 8;  // 32 KB per X stage
+constexpr int kI8Digits = 6;
+constexpr int kI8Levels = 6;                 // L = t + s in 5..10
+constexpr int kI8MinLevel = 5;
+constexpr unsigned long long kI8Balance = 0x808080808080ull;  // 128 in each of the 6 digits
+constexpr int kI8Threads = 320;              // 2 x 4 slicer warps, TMA warp, MMA warp
+constexpr int kI8ProdWarp = 8, kI8MmaWarp = 9;
+constexpr int kI8MaxN = 64;  // N = mu rounded up to 16 (M = 128 needs N % 16 == 0)
+constexpr int kI8ABufs = 2;
+constexpr int kI8TmemDigits = 6;  // all A digits in TMEM (the smem-digit path is compiled out)
+constexpr int kI8ABytes = kI8Tile * kI8Kstep;  // one digit of one K-step in smem, 4 KB
+
+__device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr) {
+  // K-major, no swizzle: 8-row x 16-byte core matrices, LBO 128 B (K chunk), SBO 256 B (rows)
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(256 >> 4) << 32) | ((uint64_t)1 << 46);
+}
+
+__host__ __device__ constexpr uint32_t umma_idesc_i8(int M, int N, bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// Q digits: qd[ks][s][canonical N x 32 B] (K-major core matrices), eq[m]
+__global__ void q_digits_kernel(const double* __restrict__ q, int K, int mu, int N,
+                                uint8_t* __restrict__ qd, int* __restrict__ eq) {
+  __shared__ double red[32];
+  const int m = blockIdx.x;
+  double mx = 0.0;
+  if (m < mu)
+    for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmax(mx, fabs(q[k + (size_t)K * m]));
+  for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+  const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
+  if (threadIdx.x == 0 && m < mu) eq[m] = e;
+  const int nks = (K + kI8Kstep - 1) / kI8Kstep;
+  const size_t blk = (size_t)kI8Digits * N * kI8Kstep;
+  for (int k = threadIdx.x; k < nks * kI8Kstep; k += blockDim.x) {
+    long long U = 0;
+    if (m < mu && k < K) U = __double2ll_rn(ldexp(q[k + (size_t)K * m], 47 - e));
+    const unsigned long long W = (unsigned long long)U + kI8Balance;  // balanced digits: bytes ^ 0x80
+    const int ks = k / kI8Kstep, kk = k % kI8Kstep;
+    const size_t off = (size_t)ks * blk + (m / 8) * 256 + (kk / 16) * 128 + (m % 8) * 16 + (kk % 16);
+#pragma unroll
+    for (int s = 0; s < kI8Digits; ++s)
+      qd[off + (size_t)s * N * kI8Kstep] = (uint8_t)(((W >> (8 * s)) & 0xFF) ^ 0x80);
+  }
+}
+
+// X stage layout: two boxes (k 0-15, 16-31) of 128 rows (j) x 128 B, 128-byte swizzle
+__device__ __forceinline__ const double* xs_elem(const double* stage, int j, int k) {
+  const int h = k >> 4, kk = k & 15;
+  return stage + h * (kI8Tile * 16) + j * 16 + ((((kk >> 1) ^ (j & 7)) << 1) | (kk & 1));
+}
+
+
+template <int N>
+__global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
+    const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ qd, const int* __restrict__ eqg,
+    const double* __restrict__ w, long long J, int K, int mu, double* __restrict__ y, int dbg) {
+  constexpr int kQBytes = kI8Digits * N * kI8Kstep;
+  constexpr uint32_t kAccCols = kI8Levels * N;
+  constexpr uint32_t kACols = kI8TmemDigits * 8;  // TMEM digits x 32 bytes per lane
+  constexpr int kAB = kI8ABufs;
+  static_assert(kAccCols + kAB * kACols <= 512, "TMEM budget");
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned char* base = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+  double* xs = reinterpret_cast<double*>(base);                          // stages x 32 KB
+  uint8_t* qs = base + kI8Stages * kI8XBytes;                            // qstages x kQBytes
+  uint8_t* as = qs + kI8QStages * kQBytes;  // [buffer][digit 4..5] x 4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(as + kAB * 2 * kI8ABytes);
+  uint64_t* full = bars;                       // [stages] X landed
+  uint64_t* empty = full + kI8Stages;          // [stages] X converted (4 slicer warps)
+  uint64_t* qfull = empty + kI8Stages;         // [qstages] Q digits landed
+  uint64_t* qempty = qfull + kI8QStages;       // [qstages] Q digits consumed (MMA commit)
+  uint64_t* afull = qempty + kI8QStages;       // [kAB]
+  uint64_t* aempty = afull + kAB;              // [kAB]
+  uint64_t* accfull = aempty + kAB;            // [1]
+  uint64_t* accempty = accfull + 1;            // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+  int* eq = reinterpret_cast<int*>(tmem_slot + 4);  // [N]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nks = (K + kI8Kstep - 1) / kI8Kstep;
+  const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
+  if (tid == 0) {
+    for (int s = 0; s < kI8Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    for (int s = 0; s < kI8QStages; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], 1);
+    }
+    for (int b = 0; b < kAB; ++b) {
+      mbar_init(&afull[b], 4);
+      mbar_init(&aempty[b], 1);
+    }
+    mbar_init(accfull, 1);
+    mbar_init(accempty, 4);
+    mbar_fence_init();
+  }
+  if (tid < N) eq[tid] = tid < mu ? eqg[tid] : 0;
+  if (warp == kI8MmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kI8ProdWarp) {  // ---------------- producers: lane 0 X tiles, lane 1 Q digits
+    if (lane == 0) {
+      long long g = 0;
+      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int ks = 0; ks < nks; ++ks, ++g) {
+          const int st = (int)(g % kI8Stages);
+          mbar_wait(&empty[st], (unsigned)((g / kI8Stages) & 1) ^ 1u);
+          mbar_arrive_expect_tx(&full[st], kI8XBytes);
+          double* dst = xs + (size_t)st * (kI8XBytes / 8);
+          tma_load_2d(dst, &xmap, &full[st], ks * kI8Kstep, (int)(t * kI8Tile));
+          tma_load_2d(dst + kI8Tile * 16, &xmap, &full[st], ks * kI8Kstep + 16, (int)(t * kI8Tile));
+        }
+      }
+    } else if (lane == 1 && !(dbg & 8)) {
+      long long g = 0;
+      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int ks = 0; ks < nks; ++ks, ++g) {
+          const int qsi = (int)(g % kI8QStages);
+          mbar_wait(&qempty[qsi], (unsigned)((g / kI8QStages) & 1) ^ 1u);
+          mbar_arrive_expect_tx(&qfull[qsi], kQBytes);
+          bulk_load(qs + (size_t)qsi * kQBytes, qd + (size_t)ks * kQBytes, kQBytes, &qfull[qsi]);
+        }
+      }
+    }
+  } else if (warp == kI8MmaWarp) {  // ---------------- MMA issuer
+    if (lane == 0 && !(dbg & 8)) {
+      long long g = 0, tcount = 0;
+      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+        mbar_wait(accempty, (unsigned)(tcount & 1));  // zeroed for this tile
+        tc_fence_after();
+        for (int ks = 0; ks < nks; ++ks, ++g) {
+          const int qsi = (int)(g % kI8QStages), b = (int)(g % kAB);
+          if (!(dbg & 4)) mbar_wait(&afull[b], (unsigned)((g / kAB) & 1));
+          mbar_wait(&qfull[qsi], (unsigned)((g / kI8QStages) & 1));
+          tc_fence_after();
+          const uint32_t qbase = smem_u32(qs + (size_t)qsi * kQBytes);
+          const uint32_t abase = tmem + kAccCols + (uint32_t)b * kACols;
+          const uint32_t asbase = smem_u32(as + (size_t)b * 2 * kI8ABytes);
+          // (t, first s, number of s) groups covering s in [max(0, 5 - t), 5]
+          constexpr int kSched[9][3] = {{5, 0, 3}, {5, 3, 3}, {4, 1, 2}, {4, 3, 3}, {3, 2, 2},
+                                        {3, 4, 2}, {2, 3, 3}, {1, 4, 2}, {0, 5, 1}};
+#pragma unroll
+          for (int gi = 0; gi < 9; ++gi) {
+            if (dbg & 2) break;
+            const int dt = kSched[gi][0], s0 = kSched[gi][1], gl = kSched[gi][2];
+            const int L = dt + s0 - kI8MinLevel;
+            const uint32_t idesc = umma_idesc_i8(kI8Tile, gl * N, true, true);
+            const uint64_t bdesc = umma_smem_desc(qbase + (uint32_t)(s0 * N * kI8Kstep));
+            if (dt < kI8TmemDigits) {
+              asm volatile(
+                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                  " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
+                  "r"(abase + (uint32_t)dt * 8), "l"(bdesc), "r"(idesc), "r"(1u));
+            } else {
+              const uint64_t adesc = umma_smem_desc(asbase + (uint32_t)((dt - kI8TmemDigits) * kI8ABytes));
+              asm volatile(
+                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                  " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
+                  "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1u));
+            }
+          }
+          tc_commit(&qempty[qsi]);  // the Q digits are consumed
+          tc_commit(&aempty[b]);  // the A digit buffer is consumed
+        }
+        tc_commit(accfull);
+      }
+    }
+  } else {  // ---------------- warps 0-7: digit split (group = K-step parity) + epilogue (group 0)
+    const int grp = warp >> 2;
+    const int jl = tid & (kI8Tile - 1);  // column within the tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    long long g = 0, tcount = 0;
+    // zero this lane's level accumulators (every MMA accumulates); group 0 owns them
+    auto zero_levels = [&]() {
+#pragma unroll
+      for (int c0 = 0; c0 < (int)kAccCols; c0 += 8)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
+                         tmem + lane_base + (uint32_t)c0),
+                     "r"(0u));
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty);
+    };
+    if (grp == 0) zero_levels();
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+      const long long j = t * kI8Tile + jl;
+      int ex = 0;
+      double scale = 0.0;
+      if (j < J) {
+        const double nrm = sqrt(w[j]);
+        ex = nrm > 0.0 ? ilogb(nrm) + 2 : 0;
+        scale = nrm > 0.0 ? ldexp(1.0, 47 - ex) : 0.0;
+      }
+      // V = round(x 2^(47-ex)) read off the bits of fma(x, 2^(47-ex), 1.5 2^52): for |V| < 2^51
+      // the sum is exact up to the final rounding (= round-to-nearest-even of x 2^(47-ex)) and
+      // its low 51 bits are V's two's complement bits, i.e. bytes 0..5 are V's digits
+      constexpr double kMagic = 6755399441055744.0 + (double)kI8Balance;  // 1.5 * 2^52 + C (exact)
+      for (int ks = 0; ks < nks; ++ks, ++g) {
+        if ((int)(g & 1) != grp) continue;  // the other group's K-step
+        const int st = (int)(g % kI8Stages), b = (int)(g % kAB);
+        mbar_wait(&full[st], (unsigned)((g / kI8Stages) & 1));
+        const double* stage = xs + (size_t)st * (kI8XBytes / 8);
+        uint32_t dw[kI8Digits][8];
+        if (dbg & 1) {
+#pragma unroll
+          for (int s2 = 0; s2 < kI8Digits; ++s2)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dw[s2][c] = 0;
+        } else
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // k = 4c .. 4c+3: two 16-byte chunks of one swizzled row
+          const double* rowp = stage + (c >> 2) * (kI8Tile * 16) + jl * 16;
+          const int c2 = 2 * (c & 3);
+          const double2 p0 = *reinterpret_cast<const double2*>(rowp + ((c2 ^ (jl & 7)) << 1));
+          const double2 p1 = *reinterpret_cast<const double2*>(rowp + (((c2 + 1) ^ (jl & 7)) << 1));
+          const double xv[4] = {p0.x, p0.y, p1.x, p1.y};
+          uint32_t lo[4], hi[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double d = fma(xv[u], scale, kMagic);
+            lo[u] = (uint32_t)__double2loint(d);
+            hi[u] = (uint32_t)__double2hiint(d);
+          }
+          // digit s of the 4 values = byte s of each V, packed little-endian
+          const uint32_t l01 = __byte_perm(lo[0], lo[1], 0x5140), l23 = __byte_perm(lo[2], lo[3], 0x5140);
+          const uint32_t l01b = __byte_perm(lo[0], lo[1], 0x7362), l23b = __byte_perm(lo[2], lo[3], 0x7362);
+          dw[0][c] = __byte_perm(l01, l23, 0x5410) ^ 0x80808080u;    // bytes 0
+          dw[1][c] = __byte_perm(l01, l23, 0x7632) ^ 0x80808080u;    // bytes 1
+          dw[2][c] = __byte_perm(l01b, l23b, 0x5410) ^ 0x80808080u;  // bytes 2
+          dw[3][c] = __byte_perm(l01b, l23b, 0x7632) ^ 0x80808080u;  // bytes 3
+          const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
+          dw[4][c] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;    // bytes 4
+          dw[5][c] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;    // bytes 5
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the X stage
+        if (dbg & 12) continue;
+        mbar_wait(&aempty[b], (unsigned)((g / kAB) & 1) ^ 1u);
+        tc_fence_after();
+        const uint32_t abase = tmem + lane_base + kAccCols + (uint32_t)b * kACols;
+#pragma unroll
+        for (int s = 0; s < kI8TmemDigits; ++s)
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(
+                           abase + (uint32_t)s * 8),
+                       "r"(dw[s][0]), "r"(dw[s][1]), "r"(dw[s][2]), "r"(dw[s][3]), "r"(dw[s][4]),
+                       "r"(dw[s][5]), "r"(dw[s][6]), "r"(dw[s][7]));
+#pragma unroll
+        for (int s = kI8TmemDigits; s < kI8Digits; ++s) {  // canonical K-major rows in smem
+          uint8_t* row = as + (size_t)b * 2 * kI8ABytes + (size_t)(s - kI8TmemDigits) * kI8ABytes +
+                         (jl >> 3) * 256 + (jl & 7) * 16;
+          *reinterpret_cast<uint4*>(row) = make_uint4(dw[s][0], dw[s][1], dw[s][2], dw[s][3]);
+          *reinterpret_cast<uint4*>(row + 128) = make_uint4(dw[s][4], dw[s][5], dw[s][6], dw[s][7]);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem digits -> tensor core
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[b]);
+      }
+      // epilogue (group 0): recombine the 7 level accumulators of column j
+      if (grp != 0 || (dbg & 8)) continue;
+      mbar_wait(accfull, (unsigned)(tcount & 1));
+      tc_fence_after();
+#pragma unroll 1
+      for (int m0 = 0; m0 < N; m0 += 8) {
+        uint32_t v[kI8Levels][8];
+#pragma unroll
+        for (int L = 0; L < kI8Levels; ++L)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
+                         "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
+                       : "r"(tmem + lane_base + (uint32_t)(L * N + m0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (j < J) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int m = m0 + u;
+            if (m >= mu) break;
+            double s = 0.0;
+#pragma unroll
+            for (int L = kI8Levels - 1; L >= 0; --L) s = fma((double)(int)v[L][u], ldexp(1.0, 8 * L), s);
+            y[m + (size_t)mu * j] = ldexp(s, ex + eq[m] - 94 + 8 * kI8MinLevel);
+          }
+        }
+      }
+      zero_levels();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kI8MmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 i8_tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int N>
+cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, const double* w, long long J,
+                     int K, int mu, double* y, cudaStream_t st) {
+  static unsigned long long done = 0;
+  const size_t smem = kI8Stages * (size_t)kI8XBytes + kI8QStages * (size_t)kI8Digits * N * kI8Kstep +
+                      kI8ABufs * 2 * (size_t)kI8ABytes + 512 + 1024 + 4 * N;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_i8_kernel<N>), smem, done);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
+  const int grid = (int)(ntiles < sms ? ntiles : sms);
+  static const int dbg = getenv("LMRA_I8_DEBUG") ? atoi(getenv("LMRA_I8_DEBUG")) : 0;
+  ttm_i8_kernel<N><<<grid, kI8Threads, smem, st>>>(map, qd, eq, w, J, K, mu, y, dbg);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool ttm_i8_supported(long long K, long long J, int mu, const double* x) {
+  return i8_tensor_map_encoder() != nullptr && K % 2 == 0 && K >= 2 && K <= 4096 && mu >= 1 &&
+         mu <= kI8MaxN && J >= 1 && J < (1ll << 31) && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+}
+
+size_t ttm_i8_workspace_bytes(long long K, int mu) {
+  const int N = ((mu + 15) / 16) * 16;
+  const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
+  return (size_t)nks * kI8Digits * N * kI8Kstep + 4 * 64 + 256;
+}
+
+cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const double* q, int mu,
+                          const double* w, double* y, void* work, cudaStream_t st) {
+  if (!ttm_i8_supported(K, J, mu, x)) return cudaErrorInvalidValue;
+  const int N = ((mu + 15) / 16) * 16;
+  const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
+  uint8_t* qd = static_cast<uint8_t*>(work);
+  int* eq = reinterpret_cast<int*>(qd + ((size_t)nks * kI8Digits * N * kI8Kstep + 255) / 256 * 256);
+  q_digits_kernel<<<N, 256, 0, st>>>(q, (int)K, mu, N, qd, eq);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {(cuuint64_t)K, (cuuint64_t)J};
+  const cuuint64_t gstride[1] = {(cuuint64_t)K * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)kI8Tile}, estride[2] = {1, 1};
+  if (i8_tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), gdim, gstride,
+                              box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  switch (N) {
+    case 16: return launch_n<16>(map, qd, eq, w, J, (int)K, mu, y, st);
+    case 32: return launch_n<32>(map, qd, eq, w, J, (int)K, mu, y, st);
+    case 48: return launch_n<48>(map, qd, eq, w, J, (int)K, mu, y, st);
+    default: return launch_n<64>(map, qd, eq, w, J, (int)K, mu, y, st);
+  }
+}
+
+}  // namespace lmra_dev

@@ -355,6 +355,25 @@ class Engine {
     return y;
   }
 
+  // Mode-0 contraction of a tensor whose canonical mode-0 column norms w are known: on the
+  // int8 tensor cores (ttm_i8.cu, ~1e-13 relative) when the shape allows, else the DMMA TTM.
+  // LMRA_TTM_I8=0 forces the DMMA path.
+  DevBuf ttm_mode0(const double* x, const std::vector<size_t>& dims, size_t mode, const double* q,
+                   size_t m, const double* w, const std::string& phase) {
+    static const bool enabled = !(getenv("LMRA_TTM_I8") && std::string(getenv("LMRA_TTM_I8")) == "0");
+    const size_t K = dims[0], J = prod(dims) / K;
+    if (mode != 0 || !w || !enabled || !lmra_dev::ttm_i8_supported((long long)K, (long long)J, (int)m, x))
+      return ttm(x, dims, mode, q, m, phase);
+    std::vector<size_t> od = dims;
+    od[0] = m;
+    DevBuf y(prod(od), st_);
+    DevBuf work((lmra_dev::ttm_i8_workspace_bytes((long long)K, (int)m) + 7) / 8, st_);
+    launch(phase + "_i8", [&] {
+      return lmra_dev::launch_ttm_i8(x, (long long)K, (long long)J, q, (int)m, w, y.get(), work.get(), st_);
+    });
+    return y;
+  }
+
   // c = (A A^T)^q G on the mode-`mode` unfolding view of a; c (I x s) in/out
   void gram_power(const double* a, ModeView v, DevBuf& c, size_t s, int q, int strategy) {
     const size_t I = (size_t)v.I, J = (size_t)(v.inner * v.outer);
@@ -616,9 +635,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     DevBuf t;
     const double* src = in.x;
     int step = 0;
+    // the first contraction reads the input, whose mode-0 norms the sampler already has
+    const double* w0 = (amm && cfg.regime != kUniform && d_w[0].get()) ? d_w[0].get() : nullptr;
     for (size_t n : idx) {
-      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n],
-                         "core_ttm" + std::to_string(step++));
+      DevBuf y = eng.ttm_mode0(src, cur, n, factors[n].get(), res->f_cols[n], src == in.x ? w0 : nullptr,
+                               "core_ttm" + std::to_string(step++));
       cur[n] = res->f_cols[n];
       t = std::move(y);
       src = t.get();
@@ -639,8 +660,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       sample_mode(eng, src, cur, n, t_n);
       if (omega_thread.joinable()) omega_thread.join();
       factors[n] = factor_mode(eng, src, cur, n);
-      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), res->f_cols[n],
-                         "shrink_ttm_m" + std::to_string(n));
+      const double* w0 =
+          (amm && cfg.regime != kUniform && src == in.x && d_w[n].get() && !(in.ov && in.ov->sample_idx))
+              ? d_w[n].get() : nullptr;
+      DevBuf y = eng.ttm_mode0(src, cur, n, factors[n].get(), res->f_cols[n], w0,
+                               "shrink_ttm_m" + std::to_string(n));
       cur[n] = res->f_cols[n];
       work = std::move(y);
       src = work.get();
@@ -1362,6 +1386,21 @@ int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims
     });
     eng.launch("ttm", [&] {
       return lmra_dev::launch_ttm(x, view_of(d, (size_t)mode), bt.get(), (int)b_rows, y, ctx->stream);
+    });
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_mode0_product_i8(lmra_context* ctx, const double* x, uint64_t K, uint64_t J, const double* q,
+                          int mu, const double* w, double* y) {
+  return guard([&] {
+    if (!lmra_dev::ttm_i8_supported((long long)K, (long long)J, mu, x))
+      throw std::invalid_argument("mode0_product_i8: shape not supported (K even <= 4096, mu <= 64)");
+    DeviceGuard dg(ctx->device);
+    DevBuf work((lmra_dev::ttm_i8_workspace_bytes((long long)K, mu) + 7) / 8, ctx->stream);
+    Engine eng(ctx);
+    eng.launch("ttm_i8", [&] {
+      return lmra_dev::launch_ttm_i8(x, (long long)K, (long long)J, q, mu, w, y, work.get(), ctx->stream);
     });
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });

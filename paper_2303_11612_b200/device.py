@@ -52,6 +52,16 @@ def mode_n_product(x, dims: Sequence[int], mode: int, b, ctx: Context = None):
     return y, out_dims
 
 
+def mode0_product_i8(x, K: int, J: int, q, mu: int, w, ctx: Context = None):
+    """y (mu x J, column-major) = q^T x on the int8 tensor cores (lmra_mode0_product_i8);
+    x: K x J (columns contiguous), q: K x mu column-major, w: squared column norms of x."""
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    y = empty(mu * J, ctx.device)
+    check(lib.lmra_mode0_product_i8(ctx.handle, _ptr(x), K, J, _ptr(q), mu, _ptr(w), _ptr(y)))
+    return y
+
+
 def gram_power_apply(a_colmajor, rows: int, cols: int, g_colmajor, s: int, q: int,
                      strategy: str = "A", ctx: Context = None):
     ctx = ctx or default_context()
