@@ -37,6 +37,7 @@
 // at the full 8192 MAC/clk, so 9 grouped MMAs (~690 cycles per K-step) replace 21 (~955).
 // Accumulators are zeroed by the epilogue warps (every MMA accumulates).
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -48,8 +49,10 @@ namespace lmra_dev {
 
 namespace {
 
-constexpr int kI8Stages = 4;   // X ring (released by the slicers)
-constexpr int kI8QStages = 5;  // Q-digit ring (released by the MMA; the L2 -> smem copy needs
+constexpr int kI8Stages = 4;   // X ring (released by the slicers); even: the two slicer groups
+                               // then own disjoint stages (with an odd count a group could wait
+                               // on a stage one phase ahead and pass on the stale parity)
+constexpr int kI8QStages = 6;  // Q-digit ring (released by the MMA; the L2 -> smem copy needs
                                // several K-steps of lead)
 constexpr int kI8Tile = 128;                 // columns of X per tile (MMA M)
 constexpr int kI8Kstep = 32;                 // k per MMA (int8)
@@ -58,8 +61,9 @@ constexpr int kI8Digits = 6;
 constexpr int kI8Levels = 6;                 // L = t + s in 5..10
 constexpr int kI8MinLevel = 5;
 constexpr unsigned long long kI8Balance = 0x808080808080ull;  // 128 in each of the 6 digits
-constexpr int kI8Threads = 320;              // 2 x 4 slicer warps, TMA warp, MMA warp
-constexpr int kI8ProdWarp = 8, kI8MmaWarp = 9;
+constexpr int kI8Threads = 608;  // 2 x 4 slicer warps, X TMA warp, MMA warp, Q warp, 8 epilogue warps
+constexpr int kI8ProdWarp = 8, kI8MmaWarp = 9, kI8QWarp = 10, kI8EpiWarp0 = 11;
+constexpr int kI8EpiWarps = 8;
 constexpr int kI8MaxN = 64;  // N = mu rounded up to 16 (M = 128 needs N % 16 == 0)
 constexpr int kI8ABufs = 2;
 constexpr int kI8TmemDigits = 6;  // all A digits in TMEM (the smem-digit path is compiled out)
@@ -131,6 +135,10 @@ __global__ void q_digits_kernel(const double* __restrict__ q, int K, int mu, int
   }
 }
 
+__device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
 // X stage layout: two boxes (k 0-15, 16-31) of 128 rows (j) x 128 B, 128-byte swizzle
 __device__ __forceinline__ const double* xs_elem(const double* stage, int j, int k) {
   const int h = k >> 4, kk = k & 15;
@@ -141,11 +149,12 @@ __device__ __forceinline__ const double* xs_elem(const double* stage, int j, int
 template <int N>
 __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ qd, const int* __restrict__ eqg,
-    const double* __restrict__ w, long long J, int K, int mu, double* __restrict__ y, int dbg) {
+    const double* __restrict__ w, long long J, int K, int mu, double* __restrict__ y) {
   constexpr int kQBytes = kI8Digits * N * kI8Kstep;
   constexpr uint32_t kAccCols = kI8Levels * N;
   constexpr uint32_t kACols = kI8TmemDigits * 8;  // TMEM digits x 32 bytes per lane
   constexpr int kAB = kI8ABufs;
+  static_assert(kI8Stages % 2 == 0 && kAB == 2, "stages and A buffers are partitioned by slicer group");
   static_assert(kAccCols + kAB * kACols <= 512, "TMEM budget");
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* base = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       mbar_init(&aempty[b], 1);
     }
     mbar_init(accfull, 1);
-    mbar_init(accempty, 4);
+    mbar_init(accempty, kI8EpiWarps);
     mbar_fence_init();
   }
   if (tid < N) eq[tid] = tid < mu ? eqg[tid] : 0;
@@ -208,7 +217,10 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
           tma_load_2d(dst + kI8Tile * 16, &xmap, &full[st], ks * kI8Kstep + 16, (int)(t * kI8Tile));
         }
       }
-    } else if (lane == 1 && !(dbg & 8)) {
+    }
+  } else if (warp == kI8QWarp) {  // ---------------- Q-digit producer (own warp: a blocked wait of
+                                  // the X producer must not hold it up)
+    if (lane == 0) {
       long long g = 0;
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int ks = 0; ks < nks; ++ks, ++g) {
@@ -220,14 +232,14 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       }
     }
   } else if (warp == kI8MmaWarp) {  // ---------------- MMA issuer
-    if (lane == 0 && !(dbg & 8)) {
+    if (lane == 0) {
       long long g = 0, tcount = 0;
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
-        mbar_wait(accempty, (unsigned)(tcount & 1));  // zeroed for this tile
+        mbar_wait(accempty, (unsigned)(tcount & 1) ^ 1u);  // previous tile drained
         tc_fence_after();
         for (int ks = 0; ks < nks; ++ks, ++g) {
           const int qsi = (int)(g % kI8QStages), b = (int)(g % kAB);
-          if (!(dbg & 4)) mbar_wait(&afull[b], (unsigned)((g / kAB) & 1));
+          mbar_wait(&afull[b], (unsigned)((g / kAB) & 1));
           mbar_wait(&qfull[qsi], (unsigned)((g / kI8QStages) & 1));
           tc_fence_after();
           const uint32_t qbase = smem_u32(qs + (size_t)qsi * kQBytes);
@@ -238,22 +250,24 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
                                         {3, 4, 2}, {2, 3, 3}, {1, 4, 2}, {0, 5, 1}};
 #pragma unroll
           for (int gi = 0; gi < 9; ++gi) {
-            if (dbg & 2) break;
             const int dt = kSched[gi][0], s0 = kSched[gi][1], gl = kSched[gi][2];
             const int L = dt + s0 - kI8MinLevel;
             const uint32_t idesc = umma_idesc_i8(kI8Tile, gl * N, true, true);
             const uint64_t bdesc = umma_smem_desc(qbase + (uint32_t)(s0 * N * kI8Kstep));
+            // the first two groups (t = 5) cover all six levels: at a tile's first K-step they
+            // overwrite, everything after accumulates (no zeroing pass)
+            const uint32_t acc = (ks == 0 && gi < 2) ? 0u : 1u;
             if (dt < kI8TmemDigits) {
               asm volatile(
                   "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                   " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
-                  "r"(abase + (uint32_t)dt * 8), "l"(bdesc), "r"(idesc), "r"(1u));
+                  "r"(abase + (uint32_t)dt * 8), "l"(bdesc), "r"(idesc), "r"(acc));
             } else {
               const uint64_t adesc = umma_smem_desc(asbase + (uint32_t)((dt - kI8TmemDigits) * kI8ABytes));
               asm volatile(
                   "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                   " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
-                  "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1u));
+                  "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
             }
           }
           tc_commit(&qempty[qsi]);  // the Q digits are consumed
@@ -262,24 +276,61 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
         tc_commit(accfull);
       }
     }
-  } else {  // ---------------- warps 0-7: digit split (group = K-step parity) + epilogue (group 0)
+  } else if (warp >= kI8EpiWarp0) {  // ---------------- epilogue warps: drain + recombine
+    // a warp reaches only the TMEM sub-partition (32 lanes) of its warp index mod 4
+    const int jl = 32 * (warp & 3) + lane;  // column within the tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    long long tcount = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+      const long long j = t * kI8Tile + jl;
+      int ex = 0;
+      if (j < J) {
+        const double nrm = sqrt(w[j]);
+        ex = nrm > 0.0 ? ilogb(nrm) + 2 : 0;
+      }
+      mbar_wait(accfull, (unsigned)(tcount & 1));
+      tc_fence_after();
+      // recombine the 6 level accumulators of column j, scale by 2^(ex + eq_m - 94 + 40); the
+      // accumulators are released as soon as the last chunk is in registers
+      const int half = (warp - kI8EpiWarp0) >> 2;  // two warps per sub-partition split the chunks
+#pragma unroll 1
+      for (int m0 = 8 * half; m0 < N; m0 += 16) {
+        uint32_t v[kI8Levels][8];
+#pragma unroll
+        for (int L = 0; L < kI8Levels; ++L)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
+                         "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
+                       : "r"(tmem + lane_base + (uint32_t)(L * N + m0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (m0 + 16 >= N) {  // this warp's last chunk is in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(accempty);
+        }
+        if (j < J) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int m = m0 + u;
+            if (m >= mu) break;
+            // sum_L S_L 2^(8L) < 2^71: levels 0-3 and 4-5 combined exactly in int64, then two
+            // conversions (the fp64 conversion throughput, not the arithmetic, bounds this loop)
+            const long long lo = (long long)(int)v[0][u] + ((long long)(int)v[1][u] << 8) +
+                                 ((long long)(int)v[2][u] << 16) + ((long long)(int)v[3][u] << 24);
+            const long long hi = (long long)(int)v[4][u] + ((long long)(int)v[5][u] << 8);
+            const double sacc = fma((double)hi, 4294967296.0, (double)lo);
+            const int e = ex + eq[m] - 94 + 8 * kI8MinLevel;
+            y[m + (size_t)mu * j] =
+                (e > -1000 && e < 1000) ? sacc * pow2(e) : ldexp(sacc, e);  // pow2: exact 2^e
+          }
+        }
+      }
+    }
+  } else {  // ---------------- warps 0-7: digit split (group = K-step parity)
     const int grp = warp >> 2;
     const int jl = tid & (kI8Tile - 1);  // column within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     long long g = 0, tcount = 0;
-    // zero this lane's level accumulators (every MMA accumulates); group 0 owns them
-    auto zero_levels = [&]() {
-#pragma unroll
-      for (int c0 = 0; c0 < (int)kAccCols; c0 += 8)
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
-                         tmem + lane_base + (uint32_t)c0),
-                     "r"(0u));
-      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(accempty);
-    };
-    if (grp == 0) zero_levels();
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
       const long long j = t * kI8Tile + jl;
       int ex = 0;
@@ -299,12 +350,6 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
         mbar_wait(&full[st], (unsigned)((g / kI8Stages) & 1));
         const double* stage = xs + (size_t)st * (kI8XBytes / 8);
         uint32_t dw[kI8Digits][8];
-        if (dbg & 1) {
-#pragma unroll
-          for (int s2 = 0; s2 < kI8Digits; ++s2)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) dw[s2][c] = 0;
-        } else
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // k = 4c .. 4c+3: two 16-byte chunks of one swizzled row
           const double* rowp = stage + (c >> 2) * (kI8Tile * 16) + jl * 16;
@@ -332,7 +377,6 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the X stage
-        if (dbg & 12) continue;
         mbar_wait(&aempty[b], (unsigned)((g / kAB) & 1) ^ 1u);
         tc_fence_after();
         const uint32_t abase = tmem + lane_base + kAccCols + (uint32_t)b * kACols;
@@ -355,33 +399,6 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[b]);
       }
-      // epilogue (group 0): recombine the 7 level accumulators of column j
-      if (grp != 0 || (dbg & 8)) continue;
-      mbar_wait(accfull, (unsigned)(tcount & 1));
-      tc_fence_after();
-#pragma unroll 1
-      for (int m0 = 0; m0 < N; m0 += 8) {
-        uint32_t v[kI8Levels][8];
-#pragma unroll
-        for (int L = 0; L < kI8Levels; ++L)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
-                         "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
-                       : "r"(tmem + lane_base + (uint32_t)(L * N + m0)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (j < J) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int m = m0 + u;
-            if (m >= mu) break;
-            double s = 0.0;
-#pragma unroll
-            for (int L = kI8Levels - 1; L >= 0; --L) s = fma((double)(int)v[L][u], ldexp(1.0, 8 * L), s);
-            y[m + (size_t)mu * j] = ldexp(s, ex + eq[m] - 94 + 8 * kI8MinLevel);
-          }
-        }
-      }
-      zero_levels();
     }
   }
   tc_fence_before();
@@ -416,8 +433,7 @@ cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, c
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
   const int grid = (int)(ntiles < sms ? ntiles : sms);
-  static const int dbg = getenv("LMRA_I8_DEBUG") ? atoi(getenv("LMRA_I8_DEBUG")) : 0;
-  ttm_i8_kernel<N><<<grid, kI8Threads, smem, st>>>(map, qd, eq, w, J, K, mu, y, dbg);
+  ttm_i8_kernel<N><<<grid, kI8Threads, smem, st>>>(map, qd, eq, w, J, K, mu, y);
   return cudaGetLastError();
 }
 
