@@ -143,6 +143,10 @@ int lmra_context_set_trace(lmra_context* ctx, int on);
 int lmra_result_num_phases(const lmra_result* r);
 int lmra_result_phase(const lmra_result* r, int i, char* name, size_t name_len, double* ms,
                       int* launches);
+/* Releases the result.  Its device core / factor buffers go back to the context's block
+ * cache and are reused by later runs: device work still reading them (on another stream)
+ * must be complete first -- the same contract as cudaFree, minus cudaFree's implicit
+ * device synchronisation. */
 void lmra_result_free(lmra_result* r);
 
 /* ---- primitives (device pointers unless stated; all on the context's stream) ---- */

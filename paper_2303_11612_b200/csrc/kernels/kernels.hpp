@@ -14,6 +14,11 @@ struct ModeView {
 // widest factor / sketch the DMMA tiles take (N of m16n8k4 padded to 8)
 constexpr int kMaxWidth = 64;
 
+// Stream-ordered scratch for the launchers: served from the run's device arena when the host
+// has one installed (lmra_b200.cpp ArenaScope), else from the stream-ordered pool.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+void scratch_free(void* p, cudaStream_t st);
+
 // Y = X x_mode B, with B given transposed: bt[r + I*k] = B[k, r] (I x m column-major).
 cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
                        cudaStream_t st);

@@ -16,13 +16,15 @@
 // BASELINE configs reach kappa(C) ~ 1e16, far past CholeskyQR2's
 // u^{-1/2} limit.
 //
-// Register-resident panels.  A block of <= 16*RPW rows x <= 64 columns lives in registers:
-// warp w holds rows [w*RPW, (w+1)*RPW), lane l holds columns l and l+32.  A Householder
-// step then costs one pass over the registers: the column dot products are per-thread
-// partial sums over the warp's rows, combined across the 16 warps through a 16 x 64
-// shared buffer in warp order.  (The first version kept the panel in shared memory and
-// re-read the whole trailing matrix twice per step: ncu showed it bound on shared-memory
-// bandwidth, ~3.7 us per step for a 334 x 60 block.)
+// Register-resident panels, columns by warp.  A block of <= 256 rows x <= 64 columns lives
+// in registers: warp w holds columns w, w + 16, w + 32, w + 48 (four slots), lane l holds
+// rows l, l + 32, ... (RPL rows per lane).  Every column reduction (norm, v^T a) is then a
+// warp butterfly, and a Householder step needs ONE block barrier: the warp owning the step's
+// column forms the reflector and publishes v (double-buffered by step parity), every warp
+// updates its own remaining columns.  Applying stored reflectors needs no barrier at all.
+// (Round-1 history: rows-by-warp panels needed four barriers and two cross-warp partial
+// reductions per step -- 4350 cycles a step measured with tools/microbench/qr_bench.cu; the
+// first version kept the panel in shared memory and was bound on shared-memory bandwidth.)
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -33,8 +35,9 @@ namespace lmra_dev {
 
 constexpr int kQThreads = 512;
 constexpr int kQWarps = kQThreads / 32;
-constexpr int kMaxBlockRows = kQWarps * 16;  // 256 rows per CTA (RPW <= 16)
+constexpr int kMaxBlockRows = 256;            // rows per CTA: 32 lanes x RPL (<= 8)
 constexpr int kOrthMaxS = 64;
+constexpr int kCW = kOrthMaxS / kQWarps;      // column slots per warp
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -42,354 +45,92 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Butterfly sums of the four slots at once (independent chains).  Every lane ends with the
+// same bits: at each level a lane and its partner add the same two values.
+__device__ __forceinline__ void warp_sum_cw(double (&t)[kCW]) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1)
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) t[j] += __shfl_xor_sync(0xffffffffu, t[j], m);
+}
+
 // ---------------------------------------------------------------------------
-// shared scratch of the register-resident QR / apply
+// shared scratch of the register-resident QR / apply / Jacobi
 // ---------------------------------------------------------------------------
 struct QSmem {
-  double* part;   // kQWarps x 64 per-warp partial sums (column c at [w * 64 + c])
-  double* vbuf;   // kMaxBlockRows: the current reflector, broadcast to every lane
-  double* fval;   // 64: tau * (v^T a_c) per column
-  double* rowk;   // 64: row k of the panel (pivoted QR)
-  double* red;    // 64: reduced sums below row k (pivoted QR)
-  double* cn;     // 64: column norms from row k (pivot choice)
+  double* part;   // kQWarps x 64: Jacobi per-warp partials
+  double* vbuf;   // 2 x kMaxBlockRows: the current reflector (by step parity)
+  double* fval;   // 64 } Jacobi: cos / sin of the round (128 contiguous doubles)
+  double* rowk;   // 64 }
+  double* red;    // 64: per-column best |y| (sign fix)
+  double* cn;     // 64: squared column norms over the remaining rows (pivoted QR)
   double* tau;    // 64
-  double* normp;  // kQWarps: partial norms of column k (unpivoted QR)
-  double* pval;   // kQWarps x 64 argmax partials (value), sign fix
-  int* pidx;      // kQWarps x 64 argmax partials (row)
-  int* piv;       // 64
+  double* normp;  // kQWarps
+  int* pidx;      // 64: Jacobi flags
+  int* piv;       // 64: logical position -> physical column (QR); argmax row (sign fix)
+  int* ipiv;      // 64: physical column -> logical position
 };
-constexpr size_t kQScratchDoubles = kQWarps * 64 + kMaxBlockRows + 64 * 6 + kQWarps + kQWarps * 64;
-constexpr size_t kQScratchBytes = kQScratchDoubles * 8 + (kQWarps * 64 + 64) * 4 + 64;
+constexpr size_t kQScratchDoubles = kQWarps * 64 + 2 * kMaxBlockRows + 64 * 5 + kQWarps;
+constexpr size_t kQScratchBytes = kQScratchDoubles * 8 + 3 * 64 * 4 + 64;
 
 __device__ __forceinline__ QSmem carve_q(double* base) {
   QSmem q;
   q.part = base;
   q.vbuf = q.part + kQWarps * 64;
-  q.fval = q.vbuf + kMaxBlockRows;
+  q.fval = q.vbuf + 2 * kMaxBlockRows;
   q.rowk = q.fval + 64;
   q.red = q.rowk + 64;
   q.cn = q.red + 64;
   q.tau = q.cn + 64;
   q.normp = q.tau + 64;
-  q.pval = q.normp + kQWarps;
-  q.pidx = reinterpret_cast<int*>(q.pval + kQWarps * 64);
-  q.piv = q.pidx + kQWarps * 64;
+  q.pidx = reinterpret_cast<int*>(q.normp + kQWarps);
+  q.piv = q.pidx + 64;
+  q.ipiv = q.piv + 64;
   return q;
 }
 
-// Column helpers.  lo = k - row0 is the position of row k inside this warp's rows: lo < 0
-// means every row is below row k ("full"), lo >= RPW that every row is above it ("done");
-// only the one warp holding row k takes the per-element predicated path.
-template <int RPW>
-__device__ __forceinline__ double col_norm_below(const double (&col)[RPW], int lo) {
-  double t = 0.0;
-  if (lo < 0) {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) t = fma(col[i], col[i], t);
-  } else if (lo < RPW - 1) {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i)
-      if (i > lo) t = fma(col[i], col[i], t);
-  }
-  return t;
+// 1/sqrt(x), 1/x for normal positive x: hardware approximation plus two Newton steps (full
+// double precision within an ulp or two) -- short dependent chains, where the IEEE library
+// sqrt / division carry special-case branches on the critical path.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
 }
 
-template <int RPW>
-__device__ __forceinline__ double col_at(const double (&col)[RPW], int lo) {
-  double v = 0.0;
-#pragma unroll
-  for (int i = 0; i < RPW; ++i)
-    if (i == lo) v = col[i];
-  return v;
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
 }
 
-// v = x(k+1:) * scale in place below the diagonal, beta on it; publish v (v_k = 1, zeros
-// above) to the warp's rows of vb
-template <int RPW>
-__device__ __forceinline__ void make_reflector(double (&col)[RPW], int lo, double scale,
-                                               double beta, double* vb) {
-  if (lo < 0) {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const double nv = col[i] * scale;
-      col[i] = nv;
-      vb[i] = nv;
-    }
-  } else if (lo < RPW) {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      if (i > lo) {
-        const double nv = col[i] * scale;
-        col[i] = nv;
-        vb[i] = nv;
-      } else if (i == lo) {
-        col[i] = beta;
-        vb[i] = 1.0;
-      } else {
-        vb[i] = 0.0;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) vb[i] = 0.0;
+// dlarfg scalars for the column (alpha; ||x(below)||^2 = ss > 0): beta = -sign(alpha) n,
+// tau = (beta - alpha) / beta = 1 + |alpha| / n, scale = 1 / (alpha - beta).
+__device__ __forceinline__ void householder_scalars(double alpha, double ss, double& beta,
+                                                    double& tk, double& scale) {
+  const double n2 = fma(alpha, alpha, ss);
+  if (n2 > 0x1.0p-1000 && n2 < 0x1.0p+1000) {
+    const double rn = rsqrt_nr(n2);
+    const double n = n2 * rn;
+    beta = -copysign(n, alpha);
+    tk = fma(fabs(alpha), rn, 1.0);
+    scale = copysign(rcp_nr(fabs(alpha) + n), alpha);
+  } else {  // far from 1: the IEEE path (no flush, no overflow in the approximations)
+    beta = -copysign(sqrt(n2), alpha);
+    tk = (beta - alpha) / beta;
+    scale = 1.0 / (alpha - beta);
   }
 }
 
-template <int RPW>
-__device__ __forceinline__ void swap_cols(double (&a)[2][RPW], int k, int p) {
-  const int l = threadIdx.x & 31, ol = k & 31, os = k >> 5, pl = p & 31, ps = p >> 5;
-#pragma unroll
-  for (int i = 0; i < RPW; ++i) {
-    const double vk = __shfl_sync(0xffffffffu, os ? a[1][i] : a[0][i], ol);
-    const double vp = __shfl_sync(0xffffffffu, ps ? a[1][i] : a[0][i], pl);
-    if (l == ol) {
-      if (os)
-        a[1][i] = vp;
-      else
-        a[0][i] = vp;
-    }
-    if (l == pl) {
-      if (ps)
-        a[1][i] = vk;
-      else
-        a[0][i] = vk;
-    }
-  }
-}
-
-// Householder QR of the register panel a (m x s; rows >= m are zero).  LAPACK dlarfg
-// convention: H_k = I - tau v v^T, v_k = 1, beta = -sign(alpha) ||x||.  On exit a holds R on
-// and above the diagonal and v below it; q.tau[k] the scalars.  With pivot, columns are
-// exchanged (largest norm below row k first, first index on ties; norms recomputed exactly
-// every step) and q.piv receives the permutation (pivoting only permutes R's columns, so
-// the left singular vectors are unaffected).
-template <int RPW>
-__device__ void reg_qr(double (&a)[2][RPW], int m, int s, const QSmem& q, bool pivot) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
-  const int kmax = min(m, s);
-  if (pivot && threadIdx.x < 64) q.piv[threadIdx.x] = threadIdx.x;
-  for (int k = 0; k < kmax; ++k) {
-    const int ol = k & 31, os = k >> 5, lo = k - row0;
-    double alpha, ss;
-    if (pivot) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = l + 32 * j;
-        if (c >= k && c < s) {
-          q.part[w * 64 + c] = col_norm_below(a[j], lo);
-          if (lo >= 0 && lo < RPW) q.rowk[c] = col_at(a[j], lo);
-        }
-      }
-      __syncthreads();
-      if ((int)threadIdx.x >= k && (int)threadIdx.x < s) {
-        const int c = threadIdx.x;
-        double t = 0.0;
-#pragma unroll
-        for (int w2 = 0; w2 < kQWarps; ++w2) t += q.part[w2 * 64 + c];
-        q.red[c] = t;
-        q.cn[c] = fma(q.rowk[c], q.rowk[c], t);
-      }
-      __syncthreads();
-      double best = -1.0;
-      int p = k;
-      for (int c = k + l; c < s; c += 32) {
-        const double v = q.cn[c];
-        if (v > best) {
-          best = v;
-          p = c;
-        }
-      }
-#pragma unroll
-      for (int msk = 16; msk >= 1; msk >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, msk);
-        const int op = __shfl_xor_sync(0xffffffffu, p, msk);
-        if (ob > best || (ob == best && op < p)) {
-          best = ob;
-          p = op;
-        }
-      }
-      if (p != k) {  // exchange columns k and p in every warp's rows
-        swap_cols(a, k, p);
-        if (threadIdx.x == 0) {
-          const int t = q.piv[k];
-          q.piv[k] = q.piv[p];
-          q.piv[p] = t;
-        }
-      }
-      alpha = q.rowk[p];
-      ss = q.red[p];
-    } else {
-      if (l == ol) {
-        const double t = os ? col_norm_below(a[1], lo) : col_norm_below(a[0], lo);
-        if (lo >= 0 && lo < RPW) q.rowk[0] = os ? col_at(a[1], lo) : col_at(a[0], lo);
-        q.normp[w] = t;
-      }
-      __syncthreads();
-      // fixed-order tree over the 16 warp partials, identical in every warp
-      double t = l < kQWarps ? q.normp[l] : 0.0;
-      t += __shfl_xor_sync(0xffffffffu, t, 8);
-      t += __shfl_xor_sync(0xffffffffu, t, 4);
-      t += __shfl_xor_sync(0xffffffffu, t, 2);
-      t += __shfl_xor_sync(0xffffffffu, t, 1);
-      ss = __shfl_sync(0xffffffffu, t, 0);
-      alpha = q.rowk[0];
-    }
-    double beta = alpha, tk = 0.0, scale = 0.0;
-    if (ss != 0.0) {
-      beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-      tk = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
-    if (l == ol) {  // the owner lane forms v (in place below the diagonal) and publishes it
-      if (os)
-        make_reflector(a[1], lo, scale, beta, q.vbuf + row0);
-      else
-        make_reflector(a[0], lo, scale, beta, q.vbuf + row0);
-    }
-    if (threadIdx.x == 0) q.tau[k] = tk;
-    __syncthreads();
-    if (tk != 0.0) {
-      const bool done = lo >= RPW;  // all of this warp's rows are above row k: v is zero here
-      double vr[RPW];
-      if (!done) {
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) vr[i] = q.vbuf[row0 + i];
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = l + 32 * j;
-        if (c > k && c < s) {
-          double t = 0.0;
-          if (!done) {
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) t = fma(vr[i], a[j][i], t);
-          }
-          q.part[w * 64 + c] = t;
-        }
-      }
-      __syncthreads();
-      if ((int)threadIdx.x > k && (int)threadIdx.x < s) {
-        const int c = threadIdx.x;
-        double t = 0.0;
-#pragma unroll
-        for (int w2 = 0; w2 < kQWarps; ++w2) t += q.part[w2 * 64 + c];
-        q.fval[c] = tk * t;
-      }
-      __syncthreads();
-      if (!done) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int c = l + 32 * j;
-          if (c > k && c < s) {
-            const double f = q.fval[c];
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) a[j][i] = fma(-f, vr[i], a[j][i]);
-          }
-        }
-      }
-    }
-  }
-}
-
-// y <- H_{k_lo} H_{k_lo+1} ... H_{k_hi-1} y  (reflectors applied last to first).
-// Vs: the block's reflectors (v_k below row k of column k, ld ldv), rows >= m of Vs zero,
-// ldv >= 16 * RPW; tau in smem.
-template <int RPW>
-__device__ void reg_apply(double (&y)[2][RPW], int mu, const double* Vs, int ldv,
-                          const double* tau, int k_hi, int k_lo, const QSmem& q) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
-  for (int k = k_hi - 1; k >= k_lo; --k) {
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const int lo = k - row0;
-    const bool done = lo >= RPW;
-    double vr[RPW];
-    if (lo < 0) {
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) vr[i] = Vs[row0 + i + (size_t)ldv * k];
-    } else if (!done) {
-#pragma unroll
-      for (int i = 0; i < RPW; ++i)
-        vr[i] = i > lo ? Vs[row0 + i + (size_t)ldv * k] : (i == lo ? 1.0 : 0.0);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = l + 32 * j;
-      if (c < mu) {
-        double t = 0.0;
-        if (!done) {
-#pragma unroll
-          for (int i = 0; i < RPW; ++i) t = fma(vr[i], y[j][i], t);
-        }
-        q.part[w * 64 + c] = t;
-      }
-    }
-    __syncthreads();
-    if ((int)threadIdx.x < mu) {
-      const int c = threadIdx.x;
-      double t = 0.0;
-#pragma unroll
-      for (int w2 = 0; w2 < kQWarps; ++w2) t += q.part[w2 * 64 + c];
-      q.fval[c] = tk * t;
-    }
-    __syncthreads();
-    if (!done) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = l + 32 * j;
-        if (c < mu) {
-          const double f = q.fval[c];
-#pragma unroll
-          for (int i = 0; i < RPW; ++i) y[j][i] = fma(-f, vr[i], y[j][i]);
-        }
-      }
-    }
-  }
-}
-
-// Per-column argmax |y| over this CTA's rows with the reference's scan semantics (strict >,
-// first index wins): thread partials over its rows, combined in warp (= row) order by
-// threads c < mu into best[c] / bidx[c] (bidx = -1 if the column is all zero here).
-template <int RPW>
-__device__ void reg_argmax(const double (&y)[2][RPW], int m, int mu, const QSmem& q,
-                           double* best, int* bidx) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int c = l + 32 * j;
-    if (c < mu) {
-      double b = 0.0;
-      int bi = -1;
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const double v = fabs(y[j][i]);
-        if (row0 + i < m && v > b) {
-          b = v;
-          bi = row0 + i;
-        }
-      }
-      q.pval[w * 64 + c] = b;
-      q.pidx[w * 64 + c] = bi;
-    }
-  }
-  __syncthreads();
-  if ((int)threadIdx.x < mu) {
-    const int c = threadIdx.x;
-    double b = 0.0;
-    int bi = -1;
-    for (int w2 = 0; w2 < kQWarps; ++w2) {
-      const double v = q.pval[w2 * 64 + c];
-      if (v > b) {
-        b = v;
-        bi = q.pidx[w2 * 64 + c];
-      }
-    }
-    best[c] = b;
-    bidx[c] = bi;
-  }
-  __syncthreads();
-}
-
+// ---------------------------------------------------------------------------
+// column-by-warp panels <-> shared tiles
+// ---------------------------------------------------------------------------
 // coalesced global (rows x cols, ld lda) -> shared tile (ld ldt), rows [rows, prow) zeroed
 __device__ __forceinline__ void load_tile(const double* __restrict__ g, long long lda, int rows,
                                           int cols, double* t, int ldt, int prow) {
@@ -404,34 +145,277 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ g, long lon
   }
 }
 
-template <int RPW>
-__device__ __forceinline__ void tile_to_regs(const double* t, int ldt, int rows, int cols,
-                                             double (&a)[2][RPW]) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+template <int RPL>
+__device__ __forceinline__ void cw_load(const double* t, int ldt, int rows, int cols,
+                                        double (&a)[kCW][RPL]) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int c = l + 32 * j;
+  for (int j = 0; j < kCW; ++j) {
+    const int c = w + kQWarps * j;
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int r = row0 + i;
-      a[j][i] = (r < rows && c < cols) ? t[r + ldt * c] : 0.0;
+    for (int i = 0; i < RPL; ++i) {
+      const int r = l + 32 * i;
+      a[j][i] = (r < rows && c < cols) ? t[r + (size_t)ldt * c] : 0.0;
     }
   }
 }
 
-template <int RPW>
-__device__ __forceinline__ void regs_to_tile(const double (&a)[2][RPW], int rows, int cols,
-                                             double* t, int ldt) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
+template <int RPL>
+__device__ __forceinline__ void cw_store(const double (&a)[kCW][RPL], int rows, int cols,
+                                         double* t, int ldt) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int c = l + 32 * j;
+  for (int j = 0; j < kCW; ++j) {
+    const int c = w + kQWarps * j;
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int r = row0 + i;
-      if (r < rows && c < cols) t[r + ldt * c] = a[j][i];
+    for (int i = 0; i < RPL; ++i) {
+      const int r = l + 32 * i;
+      if (r < rows && c < cols) t[r + (size_t)ldt * c] = a[j][i];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Householder QR of the panel a (m x s; rows >= m and columns >= s zero).  LAPACK dlarfg
+// convention: H_k = I - tau v v^T, v_k = 1, beta = -sign(alpha) ||x||.  Columns are never
+// moved: logical column k lives in physical column q.piv[k] (identity without pivoting),
+// which on exit holds R(0..k, k) in rows <= k and v_k below; q.tau[k] the scalars.
+// Pivoting takes, at step k, the remaining column with the largest norm over rows >= k
+// (first logical position on ties; norms recomputed exactly every step) -- it only permutes
+// R's columns, so the left singular vectors are unaffected.
+// Barriers: one per step (the owner warp's v), plus one for the norms when pivoting.
+// ---------------------------------------------------------------------------
+template <int RPL>
+__device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool pivot) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int kmax = min(m, s);
+  int pA = l, pB = l + 32;  // physical column at logical positions l and l + 32
+  unsigned done = 0;        // slots of this warp already factored
+  if (pivot) {
+    double t[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      t[j] = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) t[j] = fma(a[j][i], a[j][i], t[j]);
+    }
+    warp_sum_cw(t);
+    if (l == 0)
+#pragma unroll
+      for (int j = 0; j < kCW; ++j)
+        if (w + kQWarps * j < s) q.cn[w + kQWarps * j] = t[j];
+    __syncthreads();
+  }
+  for (int k = 0; k < kmax; ++k) {
+    int pc = k;
+    if (pivot) {  // every warp: the same argmax over the remaining logical positions
+      double best = (l >= k && l < s) ? q.cn[pA] : -1.0;
+      int pos = l;
+      const double vb2 = (l + 32 >= k && l + 32 < s) ? q.cn[pB] : -1.0;
+      if (vb2 > best) {
+        best = vb2;
+        pos = l + 32;
+      }
+#pragma unroll
+      for (int msk = 16; msk >= 1; msk >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, msk);
+        const int op = __shfl_xor_sync(0xffffffffu, pos, msk);
+        if (ob > best || (ob == best && op < pos)) {
+          best = ob;
+          pos = op;
+        }
+      }
+      const int pk = __shfl_sync(0xffffffffu, k < 32 ? pA : pB, k & 31);
+      pc = __shfl_sync(0xffffffffu, pos < 32 ? pA : pB, pos & 31);
+      if (l == (k & 31)) {
+        if (k < 32)
+          pA = pc;
+        else
+          pB = pc;
+      }
+      if (pos != k && l == (pos & 31)) {
+        if (pos < 32)
+          pA = pk;
+        else
+          pB = pk;
+      }
+    }
+    double* vb = q.vbuf + (k & 1) * kMaxBlockRows;
+    if (w == pc % kQWarps) {  // owner warp: reflector of physical column pc
+      const int oj = pc / kQWarps;
+      done |= 1u << oj;
+      double col[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) col[i] = a[0][i];
+#pragma unroll
+      for (int j = 1; j < kCW; ++j)
+        if (j == oj)
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) col[i] = a[j][i];
+      double t0 = 0.0, t1 = 0.0, al = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = l + 32 * i;
+        if (r > k) {
+          if (i & 1)
+            t1 = fma(col[i], col[i], t1);
+          else
+            t0 = fma(col[i], col[i], t0);
+        }
+        if (r == k) al = col[i];
+      }
+      double ss = t0 + t1;
+#pragma unroll
+      for (int msk = 16; msk >= 1; msk >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, msk);
+        al += __shfl_xor_sync(0xffffffffu, al, msk);
+      }
+      double beta = al, tk = 0.0, scale = 0.0;
+      if (ss != 0.0) householder_scalars(al, ss, beta, tk, scale);
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = l + 32 * i;
+        if (r > k) {
+          col[i] *= scale;
+          vb[r] = col[i];
+        } else if (r == k) {
+          col[i] = beta;
+          vb[r] = 1.0;
+        } else {
+          vb[r] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCW; ++j)
+        if (j == oj)
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) a[j][i] = col[i];
+      if (l == 0) q.tau[k] = tk;
+    }
+    __syncthreads();
+    const double tk = q.tau[k];
+    bool act[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) act[j] = (w + kQWarps * j < s) && !((done >> j) & 1u);
+    if (tk != 0.0) {
+      double vr[RPL], t[kCW];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) vr[i] = vb[l + 32 * i];
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        t[j] = 0.0;
+        if (act[j])
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) t[j] = fma(vr[i], a[j][i], t[j]);
+      }
+      warp_sum_cw(t);
+#pragma unroll
+      for (int j = 0; j < kCW; ++j)
+        if (act[j]) {
+          const double f = tk * t[j];
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) a[j][i] = fma(-f, vr[i], a[j][i]);
+        }
+    }
+    if (pivot && k + 1 < kmax) {  // norms over rows > k of the remaining columns
+      double t[kCW];
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        t[j] = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+          if (l + 32 * i > k) t[j] = fma(a[j][i], a[j][i], t[j]);
+      }
+      warp_sum_cw(t);
+      if (l == 0)
+#pragma unroll
+        for (int j = 0; j < kCW; ++j)
+          if (act[j]) q.cn[w + kQWarps * j] = t[j];
+      __syncthreads();
+    }
+  }
+  if (w == 0) {
+    q.piv[l] = pivot ? pA : l;
+    q.piv[l + 32] = pivot ? pB : l + 32;
+  }
+  __syncthreads();
+}
+
+// y <- H_{k_lo} H_{k_lo+1} ... H_{k_hi-1} y  (reflectors applied last to first).
+// Vs: logical column k holds v_k below row k (ld ldv >= 32 * RPL, rows >= m zero); tau in
+// smem.  Each warp applies every reflector to its own columns: no block barrier.
+template <int RPL>
+__device__ void reg_apply(double (&y)[kCW][RPL], int mu, const double* Vs, int ldv,
+                          const double* tau, int k_hi, int k_lo) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (w >= mu) return;
+  bool act[kCW];
+#pragma unroll
+  for (int j = 0; j < kCW; ++j) act[j] = w + kQWarps * j < mu;
+  for (int k = k_hi - 1; k >= k_lo; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    double vr[RPL], t[kCW];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = l + 32 * i;
+      vr[i] = r > k ? Vs[r + (size_t)ldv * k] : (r == k ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      t[j] = 0.0;
+      if (act[j])
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) t[j] = fma(vr[i], y[j][i], t[j]);
+    }
+    warp_sum_cw(t);
+#pragma unroll
+    for (int j = 0; j < kCW; ++j)
+      if (act[j]) {
+        const double f = tk * t[j];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) y[j][i] = fma(-f, vr[i], y[j][i]);
+      }
+  }
+}
+
+// Per-column argmax |y| over rows < m with the reference's scan semantics (strict >, first
+// index wins) -> best[c], bidx[c] (bidx = -1 if the column is all zero here).  Ends with a
+// block barrier.
+template <int RPL>
+__device__ void reg_argmax(const double (&y)[kCW][RPL], int m, int mu, double* best, int* bidx) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kCW; ++j) {
+    const int c = w + kQWarps * j;
+    if (c < mu) {
+      double b = 0.0;
+      int bi = -1;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const double v = fabs(y[j][i]);
+        const int r = l + 32 * i;
+        if (r < m && v > b) {
+          b = v;
+          bi = r;
+        }
+      }
+#pragma unroll
+      for (int msk = 16; msk >= 1; msk >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b, msk);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, msk);
+        if (ob > b || (ob == b && oi >= 0 && (bi < 0 || oi < bi))) {
+          b = ob;
+          bi = oi;
+        }
+      }
+      if (l == 0) {
+        best[c] = b;
+        bidx[c] = bi;
+      }
+    }
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -457,18 +441,6 @@ __device__ unsigned long long g_jclk[8];  // microbenchmark only: per-phase cycl
 
 __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// 1/sqrt(x) for normal positive x: the hardware approximation plus two Newton steps
-// (full double precision within an ulp or two) -- a short dependent chain, where the
-// library rsqrt/sqrt carry special-case branches on the Jacobi's critical path.
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
 }
 
 // Rotation for the pair (top, bottom) with squared norms a, b and inner product c: the
@@ -662,11 +634,12 @@ done:
   return flags[63] != 0;
 }
 
+
 // ---------------------------------------------------------------------------
 // Leaf QR: block b of A (m x s, lda) -> reflectors into V (same rows), tau[b*s + k],
 // R_b into rows [b*s, b*s+s) of S (ld lds), zeros below the diagonal.
 // ---------------------------------------------------------------------------
-template <int RPW>
+template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
     const double* __restrict__ A, long long m, int s, int lda, int nb, double* __restrict__ V,
     double* __restrict__ tau, double* __restrict__ S, int lds) {
@@ -678,10 +651,10 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
   const int rows = (int)(r1 - r0), ldt = rows | 1;
   load_tile(A + r0, lda, rows, s, tile, ldt, rows);
   __syncthreads();
-  double a[2][RPW];
-  tile_to_regs(tile, ldt, rows, s, a);
+  double a[kCW][RPL];
+  cw_load(tile, ldt, rows, s, a);
   reg_qr(a, rows, s, q, false);
-  regs_to_tile(a, rows, s, tile, ldt);
+  cw_store(a, rows, s, tile, ldt);
   __syncthreads();
   for (int e = threadIdx.x; e < rows * s; e += kQThreads) {
     const int i = e % rows, c = e / rows;
@@ -698,14 +671,14 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
 // Core: one CTA.  S (m x s, lds) -> pivoted QR -> Jacobi on R^T -> Y = Q [U_R(:, :mu); 0].
 // final != 0: sign-fix Y and write it to out (ld ldo); else write Y to out unsigned.
 // ---------------------------------------------------------------------------
-template <int RPW>
+template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
     int ldo, int final_level, int* status, double jacobi_tol) {
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
   const int n = 64;  // Jacobi column slots (zero columns beyond s)
-  const int ldv = (kQWarps * RPW) | 1;
+  const int ldv = (32 * RPL) | 1;
   double* Vs = sm + kQScratchBytes / 8;        // m x s (ld ldv): input, then reflectors, then Y
   double* G = Vs + (size_t)ldv * s;            // s x s   (R^T)
   double* J = G + (size_t)s * s;               // n x n   (accumulated rotations)
@@ -713,24 +686,24 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
   int* perm = reinterpret_cast<int*>(sig + n); // n
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 
-  load_tile(S, lds, m, s, Vs, ldv, kQWarps * RPW);
+  load_tile(S, lds, m, s, Vs, ldv, 32 * RPL);
   __syncthreads();
-  double a[2][RPW];
-  tile_to_regs(Vs, ldv, m, s, a);
+  double a[kCW][RPL];
+  cw_load(Vs, ldv, m, s, a);
   reg_qr(a, m, s, q, true);
-  // G = R^T (lower triangle) with a zero pad column, reflectors back to Vs, J = I
-  {
-    const int row0 = w * RPW;
+  if ((int)threadIdx.x < s) q.ipiv[q.piv[threadIdx.x]] = threadIdx.x;
+  __syncthreads();
+  // G = R^T (lower triangle), reflectors to Vs in logical column order
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = l + 32 * j;
-      if (c >= s) continue;
+  for (int j = 0; j < kCW; ++j) {
+    const int c = w + kQWarps * j;
+    if (c >= s) continue;
+    const int k = q.ipiv[c];
 #pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int r = row0 + i;
-        if (r < s) G[c + (size_t)s * r] = r <= c && r < m ? a[j][i] : 0.0;
-        if (r > c && r < m) Vs[r + (size_t)ldv * c] = a[j][i];
-      }
+    for (int i = 0; i < RPL; ++i) {
+      const int r = l + 32 * i;
+      if (r < s) G[k + (size_t)s * r] = r <= k && r < m ? a[j][i] : 0.0;
+      if (r > k && r < m) Vs[r + (size_t)ldv * k] = a[j][i];
     }
   }
   __syncthreads();
@@ -770,24 +743,20 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
   }
   __syncthreads();
   // Y = [U_R(:, :mu) ; 0] with U_R = J(0:s, perm), then the reflectors
-  double y[2][RPW];
-  {
-    const int row0 = w * RPW;
+  double y[kCW][RPL];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = l + 32 * j;
+  for (int j = 0; j < kCW; ++j) {
+    const int c = w + kQWarps * j;
 #pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const int r = row0 + i;
-        y[j][i] = (c < mu && r < s && r < m) ? J[r + (size_t)n * perm[c]] : 0.0;
-      }
+    for (int i = 0; i < RPL; ++i) {
+      const int r = l + 32 * i;
+      y[j][i] = (c < mu && r < s && r < m) ? J[r + (size_t)n * perm[c]] : 0.0;
     }
   }
-  reg_apply(y, mu, Vs, ldv, q.tau, min(m, s), 0, q);
-  __syncthreads();
+  reg_apply(y, mu, Vs, ldv, q.tau, min(m, s), 0);
   if (final_level) {
-    reg_argmax(y, m, mu, q, q.red, q.piv);  // best |.| per column in q.red, row in q.piv
-    regs_to_tile(y, m, mu, Vs, ldv);
+    reg_argmax(y, m, mu, q.red, q.piv);  // best |.| per column in q.red, row in q.piv
+    cw_store(y, m, mu, Vs, ldv);
     __syncthreads();
     if ((int)threadIdx.x < mu) {
       const int c = threadIdx.x, im = q.piv[c];
@@ -799,7 +768,8 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
       out[i + (size_t)ldo * c] = q.fval[c] * Vs[i + (size_t)ldv * c];
     }
   } else {
-    regs_to_tile(y, m, mu, Vs, ldv);
+    __syncthreads();  // every warp is done reading the reflectors
+    cw_store(y, m, mu, Vs, ldv);
     __syncthreads();
     for (int e = threadIdx.x; e < m * mu; e += kQThreads) {
       const int i = e % m, c = e / m;
@@ -813,7 +783,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
 // Leaf apply: block b: Y_b = Q_b [W(b*s : b*s+s, :) ; 0] -> out rows [r0, r1) (ld ldo).
 // With pbest also records per-block column argmax partials for the sign fix.
 // ---------------------------------------------------------------------------
-template <int RPW>
+template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
     const double* __restrict__ V, long long m, int s, int ldv, int nb,
     const double* __restrict__ tau, const double* __restrict__ W, int ldw, int mu,
@@ -823,32 +793,32 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
   double* tile = sm + kQScratchBytes / 8;
   const int b = blockIdx.x;
   const long long r0 = (m * b) / nb, r1 = (m * (b + 1)) / nb;
-  const int rows = (int)(r1 - r0), ldt = (kQWarps * RPW) | 1;
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, row0 = w * RPW;
-  load_tile(V + r0, ldv, rows, s, tile, ldt, kQWarps * RPW);
+  const int rows = (int)(r1 - r0), ldt = (32 * RPL) | 1;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  load_tile(V + r0, ldv, rows, s, tile, ldt, 32 * RPL);
   for (int k = threadIdx.x; k < s; k += kQThreads) q.tau[k] = tau[(size_t)b * s + k];
-  double y[2][RPW];
+  double y[kCW][RPL];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int c = l + 32 * j;
+  for (int j = 0; j < kCW; ++j) {
+    const int c = w + kQWarps * j;
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int r = row0 + i;
+    for (int i = 0; i < RPL; ++i) {
+      const int r = l + 32 * i;
       y[j][i] = (c < mu && r < s && r < rows) ? W[(size_t)b * s + r + (size_t)ldw * c] : 0.0;
     }
   }
   __syncthreads();
-  reg_apply(y, mu, tile, ldt, q.tau, min(rows, s), 0, q);
-  __syncthreads();
+  reg_apply(y, mu, tile, ldt, q.tau, min(rows, s), 0);
   if (pbest) {
-    reg_argmax(y, rows, mu, q, q.red, q.piv);
+    reg_argmax(y, rows, mu, q.red, q.piv);
     if ((int)threadIdx.x < mu) {
       const int c = threadIdx.x, im = q.piv[c];
       pbest[(size_t)b * mu + c] = q.red[c];
       pidx[(size_t)b * mu + c] = im >= 0 ? (int)(r0 + im) : 0;
     }
   }
-  regs_to_tile(y, rows, mu, tile, ldt);
+  __syncthreads();  // every warp is done reading the reflectors
+  cw_store(y, rows, mu, tile, ldt);
   __syncthreads();
   for (int e = threadIdx.x; e < rows * mu; e += kQThreads) {
     const int i = e % rows, c = e / rows;
@@ -888,21 +858,19 @@ struct OrthLevel {
   size_t v_off, tau_off, w_off;  // workspace offsets (doubles)
 };
 
-static int rpw_for(long long rows) {
-  const long long r = (rows + kQWarps - 1) / kQWarps;
-  return r <= 4 ? 4 : r <= 8 ? 8 : r <= 12 ? 12 : 16;
-}
+// rows per lane of the column-by-warp panels
+static int rpl_for(long long rows) { return rows <= 64 ? 2 : rows <= 128 ? 4 : 8; }
 
-// shared tiles hold 16 * RPW rows (ld (16 * RPW) | 1) so reflector columns can be read
+// shared tiles hold 32 * RPL rows (ld (32 * RPL) | 1) so reflector columns can be read
 // without row guards
 static size_t leaf_smem(long long rows, int s) {
-  return kQScratchBytes + sizeof(double) * (size_t)((kQWarps * rpw_for(rows)) | 1) * s + 64;
+  return kQScratchBytes + sizeof(double) * (size_t)((32 * rpl_for(rows)) | 1) * s + 64;
 }
 
 static size_t core_smem(long long m, int s) {
   const int n = 64;
   return kQScratchBytes +
-         sizeof(double) * ((size_t)((kQWarps * rpw_for(m)) | 1) * s + (size_t)s * s + (size_t)n * n + n) +
+         sizeof(double) * ((size_t)((32 * rpl_for(m)) | 1) * s + (size_t)s * s + (size_t)n * n + n) +
          sizeof(int) * n + 64;
 }
 
@@ -947,45 +915,44 @@ namespace {
 // the attribute is set once per kernel (and device) to the largest size any call can use
 constexpr size_t kOrthSmemMax = 227 * 1024;
 
-template <int RPW>
+template <int RPL>
 cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, double* tau,
                     double* S, int lds, cudaStream_t st) {
   static unsigned long long done = 0;
   const long long rows = (m + nb - 1) / nb;
   const size_t smem = leaf_smem(rows, s);
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_qr_kernel<RPW>), kOrthSmemMax, done);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_qr_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_leaf_qr_kernel<RPW><<<nb, kQThreads, smem, st>>>(A, m, s, (int)m, nb, V, tau, S, lds);
+  orth_leaf_qr_kernel<RPL><<<nb, kQThreads, smem, st>>>(A, m, s, (int)m, nb, V, tau, S, lds);
   return cudaGetLastError();
 }
 
-template <int RPW>
+template <int RPL>
 cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, int final_level,
                  int* status, double tol, cudaStream_t st) {
   static unsigned long long done = 0;
   const size_t smem = core_smem(m, s);
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPW>), kOrthSmemMax, done);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_core_kernel<RPW><<<1, kQThreads, smem, st>>>(S, m, s, m, mu, out, ldo, final_level, status, tol);
+  orth_core_kernel<RPL><<<1, kQThreads, smem, st>>>(S, m, s, m, mu, out, ldo, final_level, status, tol);
   return cudaGetLastError();
 }
 
-template <int RPW>
+template <int RPL>
 cudaError_t leaf_apply(const double* V, long long m, int s, int nb, const double* tau,
                        const double* W, int ldw, int mu, double* out, double* pbest, int* pidx,
                        cudaStream_t st) {
   static unsigned long long done = 0;
   const long long rows = (m + nb - 1) / nb;
   const size_t smem = leaf_smem(rows, s);
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_apply_kernel<RPW>), kOrthSmemMax, done);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_apply_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_leaf_apply_kernel<RPW><<<nb, kQThreads, smem, st>>>(V, m, s, (int)m, nb, tau, W, ldw, mu,
+  orth_leaf_apply_kernel<RPL><<<nb, kQThreads, smem, st>>>(V, m, s, (int)m, nb, tau, W, ldw, mu,
                                                           out, (int)m, pbest, pidx);
   return cudaGetLastError();
 }
 
-#define LMRA_RPW_DISPATCH(rpw, call) \
-  ((rpw) == 4 ? call<4> : (rpw) == 8 ? call<8> : (rpw) == 12 ? call<12> : call<16>)
+#define LMRA_RPL_DISPATCH(rpl, call) ((rpl) == 2 ? call<2> : (rpl) == 4 ? call<4> : call<8>)
 
 }  // namespace
 
@@ -1001,7 +968,7 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   std::vector<OrthLevel> lv = plan_levels(I, s, &used);
   cudaError_t e;
   if (lv.empty())
-    return LMRA_RPW_DISPATCH(rpw_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st);
+    return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st);
   std::vector<size_t> wbuf(lv.size());
   for (size_t l = 0; l < lv.size(); ++l) {
     wbuf[l] = used;
@@ -1013,23 +980,23 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   for (size_t l = 0; l < lv.size(); ++l) {
     const OrthLevel& L = lv[l];
     const double* A = l == 0 ? c : work + lv[l - 1].w_off;
-    const int rpw = rpw_for((L.m + L.nb - 1) / L.nb);
-    e = LMRA_RPW_DISPATCH(rpw, leaf_qr)(A, L.m, s, L.nb, work + L.v_off, work + L.tau_off,
+    const int rpl = rpl_for((L.m + L.nb - 1) / L.nb);
+    e = LMRA_RPL_DISPATCH(rpl, leaf_qr)(A, L.m, s, L.nb, work + L.v_off, work + L.tau_off,
                                         work + L.w_off, L.nb * s, st);
     if (e != cudaSuccess) return e;
   }
   // core on the last stacked R
   const OrthLevel& last = lv.back();
   const int mB = last.nb * s;
-  e = LMRA_RPW_DISPATCH(rpw_for(mB), core)(work + last.w_off, mB, s, mu, work + wbuf.back(), mB, 0,
+  e = LMRA_RPL_DISPATCH(rpl_for(mB), core)(work + last.w_off, mB, s, mu, work + wbuf.back(), mB, 0,
                                           status, tol, st);
   if (e != cudaSuccess) return e;
   // back down
   for (int l = (int)lv.size() - 1; l >= 0; --l) {
     const OrthLevel& L = lv[l];
     double* out = l == 0 ? u : work + wbuf[l - 1];
-    const int rpw = rpw_for((L.m + L.nb - 1) / L.nb);
-    e = LMRA_RPW_DISPATCH(rpw, leaf_apply)(work + L.v_off, L.m, s, L.nb, work + L.tau_off,
+    const int rpl = rpl_for((L.m + L.nb - 1) / L.nb);
+    e = LMRA_RPL_DISPATCH(rpl, leaf_apply)(work + L.v_off, L.m, s, L.nb, work + L.tau_off,
                                            work + wbuf[l], L.nb * s, mu, out,
                                            l == 0 ? pbest : nullptr, l == 0 ? pidx : nullptr, st);
     if (e != cudaSuccess) return e;

@@ -37,13 +37,17 @@ struct TtmCfg {
 template <int M8, bool RCONTIG, int KC_, int ST_>
 __global__ void __launch_bounds__(kThreads, 2)
     ttm_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ bt, int m,
-               int mtot, int koff, double* __restrict__ y) {
+               int mtot, int koff, double* __restrict__ y, long long kper) {
   using C = TtmCfg<M8, RCONTIG, KC_, ST_>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const long long J = v.inner * v.outer, I = v.I;
+  const long long J = v.inner * v.outer;
   const long long j0 = (long long)blockIdx.x * C::JT;
-  const int nk = (int)((I + C::KC - 1) / C::KC);
+  // split-K (blockIdx.y): this CTA sums r in [kbeg, I) and writes partial blockIdx.y
+  const long long kbeg = (long long)blockIdx.y * kper;
+  const long long I = min(v.I, kbeg + kper);
+  const int nk = (int)((I - kbeg + C::KC - 1) / C::KC);
+  y += (size_t)blockIdx.y * (size_t)J * mtot;
   const bool vec16 = RCONTIG ? (I % 2 == 0) : (v.inner % 2 == 0);
 
   // per-thread fixed column(s) for the JCONTIG loader
@@ -60,13 +64,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     long long j = j0 + jl;
     jvalid = j < J;
-    jbase = jvalid ? col_base(j, v.inner, I) : 0;
+    jbase = jvalid ? col_base(j, v.inner, v.I) : 0;
   }
 
   auto load = [&](int stage, int kt) {
     double* As = smem + stage * C::STAGE_ELEMS;
     double* Bs = As + C::A_ELEMS;
-    const long long k0 = (long long)kt * C::KC;
+    const long long k0 = kbeg + (long long)kt * C::KC;
     // B chunk from the packed row-major bk[r][M8] (zero padded): rows r0..r0+15 are
     // contiguous, 16-byte copies, conflict-free row-major stores
     for (int e = tid; e < C::KC * (M8 / 2); e += kThreads) {
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           int rp = e % (C::KC / 2), jj = e / (C::KC / 2);
           long long j = j0 + jj, r = k0 + 2 * rp;
           bool ok = (j < J) && (r < I);
-          cp_async16(As + jj * C::LDA + 2 * rp, ok ? x + I * j + r : x, ok);
+          cp_async16(As + jj * C::LDA + 2 * rp, ok ? x + v.I * j + r : x, ok);
         }
       } else {
 #pragma unroll
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           int rl = e % C::KC, jj = e / C::KC;
           long long j = j0 + jj, r = k0 + rl;
           bool ok = (j < J) && (r < I);
-          cp_async8(As + jj * C::LDA + rl, ok ? x + I * j + r : x, ok);
+          cp_async8(As + jj * C::LDA + rl, ok ? x + v.I * j + r : x, ok);
         }
       }
     } else {  // X(r, j) = x[base_j + inner*r]  ->  As[r][j]
@@ -347,7 +351,7 @@ __global__ void gather_strided_kernel(const double* __restrict__ x, ModeView v,
     base = col_base(idx[tcol], v.inner, v.I);
     sc = scale[tcol];
   }
-  for (long long r0 = 0; r0 < v.I; r0 += 32) {
+  for (long long r0 = 32LL * blockIdx.y; r0 < v.I; r0 += 32LL * gridDim.y) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       int rl = ty + 8 * q;
@@ -380,15 +384,16 @@ __global__ void pack_b_kernel(const double* __restrict__ bt, long long I, int m,
 
 template <int M8, bool RC>
 static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_colmajor, int m,
-                                int mtot, int koff, double* y, cudaStream_t st) {
+                                int mtot, int koff, double* y, int ksplit, long long kper,
+                                cudaStream_t st) {
   double* bt = nullptr;  // packed copy, stream-ordered scratch
-  cudaError_t pe = cudaMallocAsync(reinterpret_cast<void**>(&bt), sizeof(double) * v.I * M8, st);
+  cudaError_t pe = scratch_alloc(reinterpret_cast<void**>(&bt), sizeof(double) * v.I * M8, st);
   if (pe != cudaSuccess) return pe;
   pack_b_kernel<<<(unsigned)((v.I * M8 + 255) / 256), 256, 0, st>>>(bt_colmajor, v.I, m, M8, bt);
   struct FreeGuard {
     double* p;
     cudaStream_t s;
-    ~FreeGuard() { cudaFreeAsync(p, s); }
+    ~FreeGuard() { scratch_free(p, s); }
   } free_guard{bt, st};
   // K chunk 16 x 3 stages: measured best overall against (32,2), (16,4), (32,3) on the
   // BASELINE widths (tools/ttm_variants.sh, round 1)
@@ -400,8 +405,8 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
                                      C::SMEM, attr_done);
     if (e != cudaSuccess) return e;
     long long J = v.inner * v.outer;
-    dim3 grid((unsigned)((J + C::JT - 1) / C::JT));
-    ttm_kernel<M8, RC, KC, ST><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y);
+    dim3 grid((unsigned)((J + C::JT - 1) / C::JT), (unsigned)ksplit);
+    ttm_kernel<M8, RC, KC, ST><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y, kper);
     return cudaGetLastError();
   };
   return go(std::integral_constant<int, 16>{}, std::integral_constant<int, 3>{});
@@ -409,33 +414,70 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
 
 template <bool RC>
 static cudaError_t launch_ttm_rc(const double* x, ModeView v, const double* bt, int m, int mtot,
-                                 int koff, double* y, cudaStream_t st) {
+                                 int koff, double* y, int ks, long long kper, cudaStream_t st) {
   switch ((m + 7) / 8) {
-    case 1: return launch_ttm_t<8, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 2: return launch_ttm_t<16, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 3: return launch_ttm_t<24, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 4: return launch_ttm_t<32, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 5: return launch_ttm_t<40, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 6: return launch_ttm_t<48, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 7: return launch_ttm_t<56, RC>(x, v, bt, m, mtot, koff, y, st);
-    case 8: return launch_ttm_t<64, RC>(x, v, bt, m, mtot, koff, y, st);
+    case 1: return launch_ttm_t<8, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 2: return launch_ttm_t<16, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 3: return launch_ttm_t<24, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 4: return launch_ttm_t<32, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 5: return launch_ttm_t<40, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 6: return launch_ttm_t<48, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 7: return launch_ttm_t<56, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 8: return launch_ttm_t<64, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
   }
   return cudaErrorInvalidValue;
+}
+
+static int device_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+      sms = 148;
+  }
+  return sms;
 }
 
 cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
                        cudaStream_t st) {
   if (m < 1) return cudaErrorInvalidValue;
-  if (v.inner * v.outer == 0) return cudaSuccess;
+  const long long J = v.inner * v.outer;
+  if (J == 0) return cudaSuccess;
+  // Narrow outputs (few 128-column tiles, e.g. the power scheme on sampled columns or the
+  // core's last contraction) leave most SMs idle over a long K: split K across CTAs into
+  // fixed-order partials (deterministic), >= 64 rows of K per split.
+  const long long jt = (J + 127) / 128;
+  int ks = 1;
+  const int sms = device_sms();
+  if (jt * 2 <= sms && v.I >= 256)
+    ks = (int)std::max<long long>(1, std::min<long long>(sms / jt, v.I / 64));
+  long long kper = (v.I + ks - 1) / ks;
+  kper = ((kper + 15) / 16) * 16;
+  ks = (int)((v.I + kper - 1) / kper);
+  double* part = y;
+  if (ks > 1) {
+    cudaError_t pe =
+        scratch_alloc(reinterpret_cast<void**>(&part), sizeof(double) * (size_t)J * m * ks, st);
+    if (pe != cudaSuccess) return pe;
+  }
+  cudaError_t e = cudaSuccess;
   // widths above one DMMA tile are done as column blocks of <= kMaxWidth output rows
-  for (int k0 = 0; k0 < m; k0 += kMaxWidth) {
+  for (int k0 = 0; k0 < m && e == cudaSuccess; k0 += kMaxWidth) {
     int mb = std::min(kMaxWidth, m - k0);
     const double* btb = bt + (size_t)v.I * k0;
-    cudaError_t e = v.inner == 1 ? launch_ttm_rc<true>(x, v, btb, mb, m, k0, y, st)
-                                 : launch_ttm_rc<false>(x, v, btb, mb, m, k0, y, st);
-    if (e != cudaSuccess) return e;
+    e = v.inner == 1 ? launch_ttm_rc<true>(x, v, btb, mb, m, k0, part, ks, kper, st)
+                     : launch_ttm_rc<false>(x, v, btb, mb, m, k0, part, ks, kper, st);
   }
-  return cudaSuccess;
+  if (ks > 1) {
+    if (e == cudaSuccess) {
+      const long long n = J * m;
+      reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ks, n, y);
+      e = cudaGetLastError();
+    }
+    scratch_free(part, st);
+  }
+  return e;
 }
 
 template <int M8, bool RC>
@@ -475,8 +517,8 @@ GramPlan plan_gram(ModeView v, int num_sms) {
   const long long rtiles = (v.I + 63) / 64;
   long long target = (long long)num_sms * 4;
   long long ns = std::max<long long>(1, target / std::max<long long>(1, rtiles));
-  // at least 256 columns per split so each CTA amortises its prologue
-  ns = std::min<long long>(ns, std::max<long long>(1, J / 256));
+  // at least 32 columns per split (two K chunks) so each CTA amortises its prologue
+  ns = std::min<long long>(ns, std::max<long long>(1, J / 32));
   ns = std::min<long long>(ns, 1024);
   long long jper = (J + ns - 1) / ns;
   jper = ((jper + 15) / 16) * 16;
@@ -508,7 +550,11 @@ cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, con
   if (v.inner == 1) {
     gather_contig_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(x, v.I, idx, scale, T, out);
   } else {
-    gather_strided_kernel<<<(unsigned)((T + 31) / 32), 256, 0, st>>>(x, v, idx, scale, T, out);
+    // rows split over grid.y: each sampled fiber is strided (one sector per element), so the
+    // gather is latency-bound and wants every SM issuing
+    const long long tb = (T + 31) / 32, rb = (v.I + 31) / 32;
+    const long long ry = std::max<long long>(1, std::min<long long>(rb, (4LL * device_sms() + tb - 1) / tb));
+    gather_strided_kernel<<<dim3((unsigned)tb, (unsigned)ry), 256, 0, st>>>(x, v, idx, scale, T, out);
   }
   return cudaGetLastError();
 }

@@ -19,6 +19,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
@@ -165,6 +166,47 @@ void ThreadComm::allreduce_sum(double* buf, size_t n, cudaStream_t st) {
 }  // namespace
 
 // ------------------------------------------------------------------ context
+// Device blocks handed to results (core, factors), recycled instead of cudaMalloc/cudaFree
+// per run (each of those costs ~0.1 ms and cudaFree synchronises the device).  Shared by the
+// context and its results, so a result may outlive the context.
+struct ResultBlocks {
+  int device = 0;
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;  // capacity -> block
+  std::map<void*, size_t> cap;
+  void* get(size_t bytes) {
+    size_t c = 256;
+    while (c < bytes) c <<= 1;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.find(c);
+      if (it != free_blocks.end()) {
+        void* p = it->second;
+        free_blocks.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, c) != cudaSuccess) throw std::runtime_error("cudaMalloc (result) failed");
+    std::lock_guard<std::mutex> lk(mu);
+    cap[p] = c;
+    return p;
+  }
+  void put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cap.find(p);
+    if (it != cap.end()) free_blocks.emplace(it->second, p);
+  }
+  ~ResultBlocks() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != device) cudaSetDevice(device);
+    for (auto& kv : cap) cudaFree(kv.first);
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  }
+};
+
 struct lmra_context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -181,6 +223,11 @@ struct lmra_context {
   std::vector<cudaStream_t> aux;   // per-mode streams (T-HOSVD modes run concurrently)
   double* pinned = nullptr;        // pinned staging for Omega (async H2D, no pageable sync)
   size_t pinned_doubles = 0;
+  // Per-run device arena (see ArenaScope): one cudaMalloc'd block, bump-allocated during a
+  // run, reset when the run has synchronised, grown between runs to what the last run asked.
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_off = 0, arena_want = 0;
+  std::shared_ptr<ResultBlocks> results = std::make_shared<ResultBlocks>();
   cudaStream_t aux_stream(size_t i) {
     while (aux.size() <= i) {
       cudaStream_t s;
@@ -225,12 +272,82 @@ struct DeviceGuard {
   }
 };
 
+// Device memory of a run.  The stream-ordered pool (cudaMallocAsync) stalled the host for
+// 1-700 ms at random steps of an otherwise steady-state loop (measured on cfg5 with
+// LMRA_TIMELINE: 6 MB / 60 MB requests remapping memory), so every buffer of a run comes
+// from a per-context arena instead: bump allocation, no frees, reset once the run has
+// synchronised.  A request that does not fit falls back to the pool and the arena is grown
+// to the run's total before the next run (the first run of a shape warms it).
+static thread_local lmra_context* t_arena_ctx = nullptr;
+
+static void* arena_take(size_t bytes) {
+  lmra_context* c = t_arena_ctx;
+  if (!c) return nullptr;
+  const size_t b = (bytes + 255) & ~size_t(255);
+  c->arena_want += b;
+  if (c->arena_off + b > c->arena_cap) return nullptr;
+  void* p = c->arena + c->arena_off;
+  c->arena_off += b;
+  return p;
+}
+
+static bool in_arena(const void* p) {
+  const lmra_context* c = t_arena_ctx;
+  return c && c->arena && p >= c->arena && p < c->arena + c->arena_cap;
+}
+
+class ArenaScope {
+ public:
+  explicit ArenaScope(lmra_context* ctx) : ctx_(ctx), prev_(t_arena_ctx) {
+    ctx_->arena_off = 0;
+    ctx_->arena_want = 0;
+    t_arena_ctx = ctx_;
+  }
+  ~ArenaScope() {
+    // every stream of the run is drained before its memory is handed out again
+    cudaStreamSynchronize(ctx_->stream);
+    for (cudaStream_t s : ctx_->aux) cudaStreamSynchronize(s);
+    t_arena_ctx = prev_;
+    if (ctx_->arena_want > ctx_->arena_cap) {
+      if (ctx_->arena) cudaFree(ctx_->arena);
+      ctx_->arena = nullptr;
+      ctx_->arena_cap = 0;
+      const size_t cap = ctx_->arena_want + ctx_->arena_want / 8 + (64u << 20);
+      if (cudaMalloc(reinterpret_cast<void**>(&ctx_->arena), cap) == cudaSuccess)
+        ctx_->arena_cap = cap;
+      else
+        cudaGetLastError();  // no room: later runs keep using the pool
+    }
+    ctx_->arena_off = 0;
+    ctx_->arena_want = 0;
+  }
+
+ private:
+  lmra_context* ctx_;
+  lmra_context* prev_;
+};
+
+// diagnostics (LMRA_TIMELINE=1): phase timeline and slow host calls on stderr
+static bool diag_timing() {
+  static const bool on = getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1';
+  return on;
+}
+
 // Stream-ordered device buffer from the device's (retained) memory pool.
 class DevBuf {
  public:
   DevBuf() = default;
   DevBuf(size_t n, cudaStream_t st) : st_(st), n_(n) {
-    if (n) ck(cudaMallocAsync(reinterpret_cast<void**>(&p_), std::max<size_t>(n, 2) * sizeof(double), st), "cudaMallocAsync");
+    if (!n) return;
+    const size_t bytes = std::max<size_t>(n, 2) * sizeof(double);
+    if ((p_ = static_cast<double*>(arena_take(bytes)))) {
+      arena_ = true;
+      return;
+    }
+    const double t0 = diag_timing() ? now_ms() : 0.0;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&p_), bytes, st), "cudaMallocAsync");
+    if (diag_timing() && now_ms() - t0 > 0.5)
+      fprintf(stderr, "hostslow cudaMallocAsync %zu MB %.3f ms\n", n * 8 >> 20, now_ms() - t0);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -240,6 +357,7 @@ class DevBuf {
     p_ = o.p_;
     st_ = o.st_;
     n_ = o.n_;
+    arena_ = o.arena_;
     o.p_ = nullptr;
     o.n_ = 0;
     return *this;
@@ -247,21 +365,28 @@ class DevBuf {
   ~DevBuf() { release(); }
   double* get() const { return p_; }
   size_t size() const { return n_; }
+  // ownership to the caller (results outlive the run): a copy in a recycled result block,
+  // returned to the context's ResultBlocks by ~lmra_result
   double* detach() {
-    double* p = p_;
-    p_ = nullptr;
+    if (!p_) return nullptr;
+    if (!t_arena_ctx) throw std::logic_error("DevBuf::detach outside a run");
+    double* d = static_cast<double*>(t_arena_ctx->results->get(std::max<size_t>(n_, 2) * sizeof(double)));
+    ck(cudaMemcpyAsync(d, p_, n_ * sizeof(double), cudaMemcpyDeviceToDevice, st_), "D2D result");
+    release();
     n_ = 0;
-    return p;
+    return d;
   }
 
  private:
   void release() {
-    if (p_) cudaFreeAsync(p_, st_);
+    if (p_ && !arena_) cudaFreeAsync(p_, st_);
     p_ = nullptr;
+    arena_ = false;
   }
   double* p_ = nullptr;
   cudaStream_t st_ = nullptr;
   size_t n_ = 0;
+  bool arena_ = false;
 };
 
 ModeView view_of(const std::vector<size_t>& dims, size_t mode) {
@@ -285,6 +410,7 @@ size_t prod(const std::vector<size_t>& d) {
 // ------------------------------------------------------------------ result
 struct lmra_result {
   int device = 0;
+  std::shared_ptr<ResultBlocks> blocks;  // owner of core / factors
   std::vector<size_t> core_dims;
   double* core = nullptr;
   std::vector<size_t> f_rows, f_cols;
@@ -306,9 +432,14 @@ struct lmra_result {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != device) cudaSetDevice(device);
-    if (core) cudaFree(core);
-    for (double* f : factors)
-      if (f) cudaFree(f);
+    if (blocks) {  // stream order: the run that produced them has synchronised
+      blocks->put(core);
+      for (double* f : factors) blocks->put(f);
+    } else {
+      if (core) cudaFree(core);
+      for (double* f : factors)
+        if (f) cudaFree(f);
+    }
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
   }
 };
@@ -336,7 +467,10 @@ class Engine {
       a = ctx_->event();
       ck(cudaEventRecord(a, st_), "event");
     }
+    const double t0 = diag_timing() ? now_ms() : 0.0;
     ck(f(), phase.c_str());
+    if (diag_timing() && now_ms() - t0 > 0.5)
+      fprintf(stderr, "hostslow launch %s %.3f ms\n", phase.c_str(), now_ms() - t0);
     ++ctx_->launches;
     if (prof_) {
       b = ctx_->event();
@@ -719,6 +853,15 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
   res->t_device = dev_ms;
   res->launches = (double)(ctx->launches - launches0);
+  static const bool timeline = getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1';
+  if (timeline && !prof.empty()) {  // diagnostics: phase start/end relative to the first phase
+    for (const PhaseRec& p : prof) {
+      float a = 0, b = 0;
+      ck(cudaEventElapsedTime(&a, prof[0].a, p.a), "event time");
+      ck(cudaEventElapsedTime(&b, prof[0].a, p.b), "event time");
+      fprintf(stderr, "timeline %-16s %9.4f %9.4f\n", p.name.c_str(), a, b);
+    }
+  }
   for (const PhaseRec& p : prof) {
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, p.a, p.b), "event time");
@@ -1079,6 +1222,15 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
   res->t_device = dev_ms;
   res->launches = (double)(ctx->launches - launches0);
+  static const bool timeline = getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1';
+  if (timeline && !prof.empty()) {  // diagnostics: phase start/end relative to the first phase
+    for (const PhaseRec& p : prof) {
+      float a = 0, b = 0;
+      ck(cudaEventElapsedTime(&a, prof[0].a, p.a), "event time");
+      ck(cudaEventElapsedTime(&b, prof[0].a, p.b), "event time");
+      fprintf(stderr, "timeline %-16s %9.4f %9.4f\n", p.name.c_str(), a, b);
+    }
+  }
   for (const PhaseRec& p : prof) {
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, p.a, p.b), "event time");
@@ -1136,6 +1288,7 @@ int lmra_context_create(int device, void* stream, lmra_context** out) {
   return guard([&] {
     auto c = std::make_unique<lmra_context>();
     c->device = device;
+    c->results->device = device;
     DeviceGuard dg(device);
     ck(cudaFree(nullptr), "cuda init");
     ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
@@ -1162,6 +1315,7 @@ void lmra_context_destroy(lmra_context* ctx) {
     for (cudaStream_t s : ctx->aux) cudaStreamDestroy(s);
     for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   }
   delete ctx;
@@ -1254,6 +1408,7 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
     const bool sharded = ctx->comm && ctx->nranks > 1;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard dg(ctx->device);
+    ArenaScope arena(ctx);  // every device buffer of the run (after the device guard)
     RunInputs in;
     in.alg = algorithm;
     in.dims.assign(dims, dims + order);
@@ -1261,6 +1416,7 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
     in.ov = overrides;
     auto res = std::make_unique<lmra_result>();
     res->device = ctx->device;
+    res->blocks = ctx->results;
     DevBuf staged;
     if (x_location == LMRA_HOST) {
       size_t n = prod(in.dims);
@@ -1657,3 +1813,13 @@ int lmra_memcpy(lmra_context* ctx, void* dst, const void* src, size_t bytes, int
 }  // extern "C"
 
 extern "C" int lmra_debug_jacobi_sweeps(void) { return lmra_dev::last_jacobi_sweeps(); }
+
+namespace lmra_dev {  // scratch of the launchers (kernels.hpp)
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  if ((*p = arena_take(bytes))) return cudaSuccess;
+  return cudaMallocAsync(p, bytes, st);
+}
+void scratch_free(void* p, cudaStream_t st) {
+  if (p && !in_arena(p)) cudaFreeAsync(p, st);
+}
+}  // namespace lmra_dev
