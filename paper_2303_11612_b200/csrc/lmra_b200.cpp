@@ -365,6 +365,8 @@ class DevBuf {
   ~DevBuf() { release(); }
   double* get() const { return p_; }
   size_t size() const { return n_; }
+  // the stream of the buffer's last use (its free is ordered after that stream's work)
+  void rebind(cudaStream_t st) { st_ = st; }
   // ownership to the caller (results outlive the run): a copy in a recycled result block,
   // returned to the context's ResultBlocks by ~lmra_result
   double* detach() {
@@ -694,14 +696,41 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
 
   // phase 2 of a mode: Omega -> power scheme (on the unfolding or the sampled columns)
   // -> orthonormalised factor.  Omega must be drawn (omega_thread joined) before this.
+  // Omega uploads: every mode's draw goes up in one copy on its own stream as soon as the
+  // host thread is done (during the norm pass), instead of in stream order behind each
+  // mode's sampling chain, where the copy sat on the critical path.
+  std::vector<DevBuf> d_om(N);
+  cudaEvent_t om_ready = nullptr;
+  auto upload_omegas = [&] {
+    if (omega_thread.joinable()) omega_thread.join();
+    if (om_ready) return;
+    cudaStream_t cs = ctx->aux_stream(N);
+    ck(cudaStreamWaitEvent(cs, ev0, 0), "wait");  // the run's start (stream-ordered arena)
+    for (size_t n = 0; n < N; ++n) {
+      const size_t cnt = om_off[n + 1] - om_off[n];
+      d_om[n] = DevBuf(cnt, cs);
+      ck(cudaMemcpyAsync(d_om[n].get(), om_pin + om_off[n], cnt * sizeof(double),
+                         cudaMemcpyHostToDevice, cs), "H2D omega");
+    }
+    ck(cudaEventCreateWithFlags(&om_ready, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(om_ready, cs), "event");
+  };
+  struct EventGuard {
+    cudaEvent_t& e;
+    ~EventGuard() {
+      if (e) cudaEventDestroy(e);
+    }
+  } om_guard{om_ready};
+
   auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
                          size_t n) -> DevBuf {
     cudaStream_t s_ = e.st_;
     const ModeView v = view_of(dims, n);
     const size_t I = dims[n], s = r.sketch[n];
-    DevBuf c(I * s, s_);
-    ck(cudaMemcpyAsync(c.get(), om_pin + om_off[n], I * s * sizeof(double), cudaMemcpyHostToDevice, s_),
-       "H2D omega");
+    upload_omegas();
+    ck(cudaStreamWaitEvent(s_, om_ready, 0), "wait omega");
+    DevBuf c = std::move(d_om[n]);  // the sketch is formed in place
+    c.rebind(s_);
     if (!amm) {
       e.gram_power(x, v, c, s, cfg.power, cfg.strategy);
     } else {
@@ -750,7 +779,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       engs.emplace_back(ctx, sn, ctx->profile ? &prof : nullptr);
     }
     for (size_t n = 0; n < N; ++n) sample_mode(engs[n], in.x, in.dims, n, amm ? t_flat[n] : 0);
-    omega_thread.join();
+    upload_omegas();
     for (size_t n = 0; n < N; ++n) factors[n] = factor_mode(engs[n], in.x, in.dims, n);
     for (size_t n = 0; n < N; ++n) {
       cudaEvent_t done;
@@ -792,7 +821,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
         if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
       }
       sample_mode(eng, src, cur, n, t_n);
-      if (omega_thread.joinable()) omega_thread.join();
+      upload_omegas();
       factors[n] = factor_mode(eng, src, cur, n);
       const double* w0 =
           (amm && cfg.regime != kUniform && src == in.x && d_w[n].get() && !(in.ov && in.ov->sample_idx))
