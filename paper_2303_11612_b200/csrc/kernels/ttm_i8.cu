@@ -66,8 +66,8 @@ constexpr int kI8ProdWarp = 8, kI8MmaWarp = 9, kI8QWarp = 10, kI8EpiWarp0 = 11;
 constexpr int kI8EpiWarps = 8;
 constexpr int kI8MaxN = 64;  // N = mu rounded up to 16 (M = 128 needs N % 16 == 0)
 constexpr int kI8ABufs = 2;
-constexpr int kI8TmemDigits = 6;  // all A digits in TMEM (the smem-digit path is compiled out)
-constexpr int kI8ABytes = kI8Tile * kI8Kstep;  // one digit of one K-step in smem, 4 KB
+constexpr int kI8StageLd = 9;  // epilogue output staging: 32 columns x 8 outputs, row pad 1
+constexpr int kI8StageBytes = kI8EpiWarps * 32 * kI8StageLd * 8;
 
 __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr) {
   // K-major, no swizzle: 8-row x 16-byte core matrices, LBO 128 B (K chunk), SBO 256 B (rows)
@@ -135,6 +135,28 @@ __global__ void q_digits_kernel(const double* __restrict__ q, int K, int mu, int
   }
 }
 
+#ifdef LMRA_I8_CLOCKS  // microbenchmark only (tools/microbench/i8_clocks.cu): CTA 0 wait cycles,
+                       // summed in registers and flushed once at the end of the kernel
+__device__ unsigned long long g_i8clk[20];
+#define I8_WAIT(idx, call)                   \
+  do {                                       \
+    const long long _t0 = clock64();         \
+    call;                                    \
+    i8acc[idx] += clock64() - _t0;           \
+  } while (0)
+#define I8_T0(v) const long long v = clock64()
+#define I8_ACC(idx, v) i8acc[idx] += clock64() - (v)
+#else
+#define I8_WAIT(idx, call) call
+#define I8_T0(v)
+#define I8_ACC(idx, v)
+#endif
+
+// exact int32 -> fp64 without the conversion unit: 2^52 + 2^31 + x has x in its low word
+__device__ __forceinline__ double i32_to_f64(uint32_t x) {
+  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
+}
+
 __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
@@ -152,7 +174,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     const double* __restrict__ w, long long J, int K, int mu, double* __restrict__ y) {
   constexpr int kQBytes = kI8Digits * N * kI8Kstep;
   constexpr uint32_t kAccCols = kI8Levels * N;
-  constexpr uint32_t kACols = kI8TmemDigits * 8;  // TMEM digits x 32 bytes per lane
+  constexpr uint32_t kACols = kI8Digits * 8;  // 6 digits x 32 bytes per lane
   constexpr int kAB = kI8ABufs;
   static_assert(kI8Stages % 2 == 0 && kAB == 2, "stages and A buffers are partitioned by slicer group");
   static_assert(kAccCols + kAB * kACols <= 512, "TMEM budget");
@@ -160,8 +182,8 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
   unsigned char* base = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
   double* xs = reinterpret_cast<double*>(base);                          // stages x 32 KB
   uint8_t* qs = base + kI8Stages * kI8XBytes;                            // qstages x kQBytes
-  uint8_t* as = qs + kI8QStages * kQBytes;  // [buffer][digit 4..5] x 4 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(as + kAB * 2 * kI8ABytes);
+  double* ostage = reinterpret_cast<double*>(qs + kI8QStages * kQBytes);  // epilogue staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ostage) + kI8StageBytes);
   uint64_t* full = bars;                       // [stages] X landed
   uint64_t* empty = full + kI8Stages;          // [stages] X converted (4 slicer warps)
   uint64_t* qfull = empty + kI8Stages;         // [qstages] Q digits landed
@@ -171,11 +193,15 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
   uint64_t* accfull = aempty + kAB;            // [1]
   uint64_t* accempty = accfull + 1;            // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
-  int* eq = reinterpret_cast<int*>(tmem_slot + 4);  // [N]
+  double* qsc = reinterpret_cast<double*>(tmem_slot + 4);  // [N] 2^eq_m
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nks = (K + kI8Kstep - 1) / kI8Kstep;
   const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
+#ifdef LMRA_I8_CLOCKS
+  long long i8acc[20] = {0};
+  const long long i8start = clock64();
+#endif
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
       mbar_init(&full[s], 1);
@@ -193,7 +219,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     mbar_init(accempty, kI8EpiWarps);
     mbar_fence_init();
   }
-  if (tid < N) eq[tid] = tid < mu ? eqg[tid] : 0;
+  if (tid < N) qsc[tid] = ldexp(1.0, tid < mu ? eqg[tid] : 0);  // 2^eq_m
   if (warp == kI8MmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
@@ -210,7 +236,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int ks = 0; ks < nks; ++ks, ++g) {
           const int st = (int)(g % kI8Stages);
-          mbar_wait(&empty[st], (unsigned)((g / kI8Stages) & 1) ^ 1u);
+          I8_WAIT(0, mbar_wait(&empty[st], (unsigned)((g / kI8Stages) & 1) ^ 1u));
           mbar_arrive_expect_tx(&full[st], kI8XBytes);
           double* dst = xs + (size_t)st * (kI8XBytes / 8);
           tma_load_2d(dst, &xmap, &full[st], ks * kI8Kstep, (int)(t * kI8Tile));
@@ -225,7 +251,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int ks = 0; ks < nks; ++ks, ++g) {
           const int qsi = (int)(g % kI8QStages);
-          mbar_wait(&qempty[qsi], (unsigned)((g / kI8QStages) & 1) ^ 1u);
+          I8_WAIT(1, mbar_wait(&qempty[qsi], (unsigned)((g / kI8QStages) & 1) ^ 1u));
           mbar_arrive_expect_tx(&qfull[qsi], kQBytes);
           bulk_load(qs + (size_t)qsi * kQBytes, qd + (size_t)ks * kQBytes, kQBytes, &qfull[qsi]);
         }
@@ -235,16 +261,16 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     if (lane == 0) {
       long long g = 0, tcount = 0;
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
-        mbar_wait(accempty, (unsigned)(tcount & 1) ^ 1u);  // previous tile drained
+        I8_WAIT(2, mbar_wait(accempty, (unsigned)(tcount & 1) ^ 1u));  // previous tile drained
         tc_fence_after();
         for (int ks = 0; ks < nks; ++ks, ++g) {
           const int qsi = (int)(g % kI8QStages), b = (int)(g % kAB);
-          mbar_wait(&afull[b], (unsigned)((g / kAB) & 1));
-          mbar_wait(&qfull[qsi], (unsigned)((g / kI8QStages) & 1));
+          I8_WAIT(3, mbar_wait(&afull[b], (unsigned)((g / kAB) & 1)));
+          I8_WAIT(4, mbar_wait(&qfull[qsi], (unsigned)((g / kI8QStages) & 1)));
           tc_fence_after();
+          I8_T0(tm0);
           const uint32_t qbase = smem_u32(qs + (size_t)qsi * kQBytes);
           const uint32_t abase = tmem + kAccCols + (uint32_t)b * kACols;
-          const uint32_t asbase = smem_u32(as + (size_t)b * 2 * kI8ABytes);
           // (t, first s, number of s) groups covering s in [max(0, 5 - t), 5]
           constexpr int kSched[9][3] = {{5, 0, 3}, {5, 3, 3}, {4, 1, 2}, {4, 3, 3}, {3, 2, 2},
                                         {3, 4, 2}, {2, 3, 3}, {1, 4, 2}, {0, 5, 1}};
@@ -257,21 +283,14 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
             // the first two groups (t = 5) cover all six levels: at a tile's first K-step they
             // overwrite, everything after accumulates (no zeroing pass)
             const uint32_t acc = (ks == 0 && gi < 2) ? 0u : 1u;
-            if (dt < kI8TmemDigits) {
-              asm volatile(
-                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                  " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
-                  "r"(abase + (uint32_t)dt * 8), "l"(bdesc), "r"(idesc), "r"(acc));
-            } else {
-              const uint64_t adesc = umma_smem_desc(asbase + (uint32_t)((dt - kI8TmemDigits) * kI8ABytes));
-              asm volatile(
-                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                  " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
-                  "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-            }
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)L * N),
+                "r"(abase + (uint32_t)dt * 8), "l"(bdesc), "r"(idesc), "r"(acc));
           }
           tc_commit(&qempty[qsi]);  // the Q digits are consumed
           tc_commit(&aempty[b]);  // the A digit buffer is consumed
+          I8_ACC(13, tm0);
         }
         tc_commit(accfull);
       }
@@ -280,22 +299,28 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     // a warp reaches only the TMEM sub-partition (32 lanes) of its warp index mod 4
     const int jl = 32 * (warp & 3) + lane;  // column within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    double* ost = ostage + (warp - kI8EpiWarp0) * 32 * kI8StageLd;
     long long tcount = 0;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
       const long long j = t * kI8Tile + jl;
+      const long long jw0 = t * kI8Tile + 32 * (warp & 3);  // first column of this warp
       int ex = 0;
       if (j < J) {
         const double nrm = sqrt(w[j]);
         ex = nrm > 0.0 ? ilogb(nrm) + 2 : 0;
       }
-      mbar_wait(accfull, (unsigned)(tcount & 1));
+      const double sj = ldexp(1.0, ex - 94 + 8 * kI8MinLevel);  // column part of the scale
+      I8_WAIT(7, mbar_wait(accfull, (unsigned)(tcount & 1)));
       tc_fence_after();
+      I8_T0(te0);
       // recombine the 6 level accumulators of column j, scale by 2^(ex + eq_m - 94 + 40); the
       // accumulators are released as soon as the last chunk is in registers
       const int half = (warp - kI8EpiWarp0) >> 2;  // two warps per sub-partition split the chunks
 #pragma unroll 1
       for (int m0 = 8 * half; m0 < N; m0 += 16) {
+        if (m0 >= mu && m0 + 16 < N) continue;  // no output here (the last chunk still releases)
         uint32_t v[kI8Levels][8];
+        I8_T0(tld);
 #pragma unroll
         for (int L = 0; L < kI8Levels; ++L)
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
@@ -303,28 +328,41 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
                          "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
                        : "r"(tmem + lane_base + (uint32_t)(L * N + m0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        I8_ACC(17, tld);
+        I8_T0(tcp);
         if (m0 + 16 >= N) {  // this warp's last chunk is in registers
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(accempty);
+          I8_ACC(8, te0);
         }
-        if (j < J) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int m = m0 + u;
-            if (m >= mu) break;
-            // sum_L S_L 2^(8L) < 2^71: levels 0-3 and 4-5 combined exactly in int64, then two
-            // conversions (the fp64 conversion throughput, not the arithmetic, bounds this loop)
-            const long long lo = (long long)(int)v[0][u] + ((long long)(int)v[1][u] << 8) +
-                                 ((long long)(int)v[2][u] << 16) + ((long long)(int)v[3][u] << 24);
-            const long long hi = (long long)(int)v[4][u] + ((long long)(int)v[5][u] << 8);
-            const double sacc = fma((double)hi, 4294967296.0, (double)lo);
-            const int e = ex + eq[m] - 94 + 8 * kI8MinLevel;
-            y[m + (size_t)mu * j] =
-                (e > -1000 && e < 1000) ? sacc * pow2(e) : ldexp(sacc, e);  // pow2: exact 2^e
-          }
+        for (int u = 0; u < 8; ++u) {
+          const int m = m0 + u;
+          // sum_L S_L 2^(8L): each int32 level to fp64 exactly with the magic-number trick
+          // (one LOP + one DADD: the 64-bit integer conversions ran on a slow pipe and held
+          // the accumulator drain), then a Horner chain from the top level down
+          double sacc = i32_to_f64(v[kI8Levels - 1][u]);
+#pragma unroll
+          for (int L = kI8Levels - 2; L >= 0; --L) sacc = fma(sacc, 256.0, i32_to_f64(v[L][u]));
+          // scale 2^(ex + eq_m - 94 + 40) as two exact power-of-two products (branch-free, so
+          // the 8 outputs' chains interleave)
+          ost[lane * kI8StageLd + u] = (sacc * sj) * qsc[m];
         }
+        __syncwarp();
+        I8_ACC(18, tcp);
+        I8_T0(tst);
+        // coalesced-ish stores: 4 columns x 8 outputs per instruction (64-byte runs of Y)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int jj = 4 * i + (lane >> 3), mm = lane & 7;
+          const long long jo = jw0 + jj;
+          if (m0 + mm < mu && jo < J) y[(m0 + mm) + (size_t)mu * jo] = ost[jj * kI8StageLd + mm];
+        }
+        __syncwarp();  // the staging rows are rewritten by the next chunk
+        I8_ACC(16, tst);
       }
+      I8_ACC(14, te0);
     }
   } else {  // ---------------- warps 0-7: digit split (group = K-step parity)
     const int grp = warp >> 2;
@@ -347,8 +385,9 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       for (int ks = 0; ks < nks; ++ks, ++g) {
         if ((int)(g & 1) != grp) continue;  // the other group's K-step
         const int st = (int)(g % kI8Stages), b = (int)(g % kAB);
-        mbar_wait(&full[st], (unsigned)((g / kI8Stages) & 1));
+        I8_WAIT(5 + grp * 4, mbar_wait(&full[st], (unsigned)((g / kI8Stages) & 1)));
         const double* stage = xs + (size_t)st * (kI8XBytes / 8);
+        I8_T0(ts0);
         uint32_t dw[kI8Digits][8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // k = 4c .. 4c+3: two 16-byte chunks of one swizzled row
@@ -377,30 +416,31 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the X stage
-        mbar_wait(&aempty[b], (unsigned)((g / kAB) & 1) ^ 1u);
+        I8_ACC(11, ts0);
+        I8_WAIT(6 + grp * 4, mbar_wait(&aempty[b], (unsigned)((g / kAB) & 1) ^ 1u));
         tc_fence_after();
         const uint32_t abase = tmem + lane_base + kAccCols + (uint32_t)b * kACols;
+        I8_T0(ts1);
 #pragma unroll
-        for (int s = 0; s < kI8TmemDigits; ++s)
+        for (int s = 0; s < kI8Digits; ++s)
           asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(
                            abase + (uint32_t)s * 8),
                        "r"(dw[s][0]), "r"(dw[s][1]), "r"(dw[s][2]), "r"(dw[s][3]), "r"(dw[s][4]),
                        "r"(dw[s][5]), "r"(dw[s][6]), "r"(dw[s][7]));
-#pragma unroll
-        for (int s = kI8TmemDigits; s < kI8Digits; ++s) {  // canonical K-major rows in smem
-          uint8_t* row = as + (size_t)b * 2 * kI8ABytes + (size_t)(s - kI8TmemDigits) * kI8ABytes +
-                         (jl >> 3) * 256 + (jl & 7) * 16;
-          *reinterpret_cast<uint4*>(row) = make_uint4(dw[s][0], dw[s][1], dw[s][2], dw[s][3]);
-          *reinterpret_cast<uint4*>(row + 128) = make_uint4(dw[s][4], dw[s][5], dw[s][6], dw[s][7]);
-        }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem digits -> tensor core
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[b]);
+        I8_ACC(12, ts1);
       }
     }
   }
+#ifdef LMRA_I8_CLOCKS
+  if (warp == kI8MmaWarp) i8acc[15] = clock64() - i8start;  // CTA 0's own span (SM clocks)
+  if (blockIdx.x == 0 && lane == 0)
+    for (int i = 0; i < 20; ++i)
+      if (i8acc[i]) atomicAdd(&g_i8clk[i], (unsigned long long)i8acc[i]);
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == kI8MmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
@@ -425,7 +465,7 @@ cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, c
                      int K, int mu, double* y, cudaStream_t st) {
   static unsigned long long done = 0;
   const size_t smem = kI8Stages * (size_t)kI8XBytes + kI8QStages * (size_t)kI8Digits * N * kI8Kstep +
-                      kI8ABufs * 2 * (size_t)kI8ABytes + 512 + 1024 + 4 * N;
+                      kI8StageBytes + 512 + 1024 + 8 * N;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_i8_kernel<N>), smem, done);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;

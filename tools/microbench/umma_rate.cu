@@ -61,6 +61,6 @@ void run() {
   cudaFree(d);
 }
 int main() {
-  run<64, true>(); run<64, false>(); run<128, true>(); run<128, false>(); run<256, true>(); run<256, false>(); run<32, true>(); run<16, true>();
+  run<64, true>(); run<64, false>(); run<128, true>(); run<128, false>(); run<192, true>(); run<192, false>(); run<256, true>(); run<256, false>(); run<32, true>(); run<16, true>();
   return 0;
 }
