@@ -189,7 +189,7 @@ def phase_cost(bc, phase: str, dims_local=None):
     return None
 
 
-def roofline(bc, phases, steps, dims_local=None):
+def roofline(bc, phases, steps, dims_local=None, ms_per_step=None):
     hbm, src = measured_peaks()
     # dominant kernel = the phase with the largest device time among the launches that run
     # alone on the main stream (core / shrink contractions, the fused norms pass); the
@@ -225,7 +225,10 @@ def roofline(bc, phases, steps, dims_local=None):
         out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                "frac": round(achieved / hbm, 4), "peak_source": src}
     out.update({"kernel": name, "launch_ms": round(per_launch_ms, 4),
-                "share_of_step": round(ms / max(1e-9, sum(v[0] for v in phases.values())), 3),
+                # per-launch device time over the step's device time (the per-mode phases run
+                # concurrently, so a sum of phase times would overstate the step)
+                "share_of_step": round(per_launch_ms * cnt / steps / ms_per_step, 3) if ms_per_step
+                else None,
                 "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": byts,
                 "traffic": traffic_from_profiles(name)})
     return out
@@ -397,7 +400,7 @@ def bench_gpu(args, rank, world, local_rank):
 
     if rank != 0:
         return 0
-    roof = roofline(bc, phases, args.steps, local_dims if world > 1 else None)
+    roof = roofline(bc, phases, args.steps, local_dims if world > 1 else None, ms_per_step)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         sbc = cpu_sample_workload()

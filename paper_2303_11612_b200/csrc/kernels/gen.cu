@@ -158,7 +158,7 @@ cudaError_t launch_transpose(const double* a, long long rows, long long cols, do
                              cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(a, rows, cols, at);
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(a, rows, cols, at); note_launch();
   return cudaGetLastError();
 }
 
@@ -174,7 +174,7 @@ __global__ void localize_idx_kernel(const long long* __restrict__ g, long long T
 cudaError_t launch_localize_idx(const long long* g, long long T, long long off, long long cnt,
                                 long long* l, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  localize_idx_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(g, T, off, cnt, l);
+  localize_idx_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(g, T, off, cnt, l); note_launch();
   return cudaGetLastError();
 }
 
@@ -192,7 +192,7 @@ __global__ void sum_ranks_kernel(const double* const* __restrict__ in, int nrank
 cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long n, double* out,
                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  sum_ranks_kernel<<<148 * 4, 256, 0, st>>>(in_dev, nranks, n, out);
+  sum_ranks_kernel<<<148 * 4, 256, 0, st>>>(in_dev, nranks, n, out); note_launch();
   return cudaGetLastError();
 }
 
@@ -200,7 +200,7 @@ cudaError_t launch_gen_normals(double* out, long long n, uint64_t seed, uint64_t
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   long long threads = ((n + 1) / 2 + kPairsPerThread - 1) / kPairsPerThread;
-  gen_normals_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(out, n, seed, stream);
+  gen_normals_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(out, n, seed, stream); note_launch();
   return cudaGetLastError();
 }
 
@@ -209,7 +209,7 @@ cudaError_t launch_gen_uniform_add(double* out, long long n, double scale, uint6
   if (n <= 0) return cudaSuccess;
   long long threads = (n + kPairsPerThread - 1) / kPairsPerThread;
   gen_uniform_add_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(out, n, scale, seed,
-                                                                            stream);
+                                                                            stream); note_launch();
   return cudaGetLastError();
 }
 
@@ -221,7 +221,7 @@ cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, cu
     d.d[k] = dims[k];
     n *= dims[k];
   }
-  gen_hilbert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, d, order);
+  gen_hilbert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, d, order); note_launch();
   return cudaGetLastError();
 }
 
@@ -235,20 +235,20 @@ cudaError_t launch_gen_cp(double* out, const long long* dims, int order, const d
     n *= dims[k];
   }
   gen_cp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, d, order, profiles, weights,
-                                                            n_terms);
+                                                            n_terms); note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_axpby(const double* a, const double* b, double coef, double* out, long long n,
                          cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  axpby_kernel<<<148 * 8, 256, 0, st>>>(a, b, coef, out, n);
+  axpby_kernel<<<148 * 8, 256, 0, st>>>(a, b, coef, out, n); note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_sumsq(const double* a, long long n, double* partials, int nparts,
                          cudaStream_t st) {
-  sumsq_kernel<<<nparts, 256, 0, st>>>(a, n, partials);
+  sumsq_kernel<<<nparts, 256, 0, st>>>(a, n, partials); note_launch();
   return cudaGetLastError();
 }
 

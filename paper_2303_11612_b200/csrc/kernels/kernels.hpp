@@ -14,6 +14,11 @@ struct ModeView {
 // widest factor / sketch the DMMA tiles take (N of m16n8k4 padded to 8)
 constexpr int kMaxWidth = 64;
 
+// Kernel launches issued by this library from the calling thread (every launch site calls
+// note_launch): the results' launch counts -- and so the bench's gpu_launches -- come from here.
+inline thread_local long long g_kernel_launches = 0;
+inline void note_launch() { ++g_kernel_launches; }
+
 // Stream-ordered scratch for the launchers: served from the run's device arena when the host
 // has one installed (lmra_b200.cpp ArenaScope), else from the stream-ordered pool.
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);

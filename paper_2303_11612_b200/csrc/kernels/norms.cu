@@ -82,9 +82,9 @@ cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaSt
   const long long J = v.inner * v.outer;
   if (J == 0) return cudaSuccess;
   if (v.inner == 1) {
-    sqnorm_contig_kernel<<<(unsigned)((J + 127) / 128), 128, 0, st>>>(x, v.I, J, w);
+    sqnorm_contig_kernel<<<(unsigned)((J + 127) / 128), 128, 0, st>>>(x, v.I, J, w); note_launch();
   } else {
-    sqnorm_strided_kernel<<<(unsigned)((J + 255) / 256), 256, 0, st>>>(x, v, w);
+    sqnorm_strided_kernel<<<(unsigned)((J + 255) / 256), 256, 0, st>>>(x, v, w); note_launch();
   }
   return cudaGetLastError();
 }

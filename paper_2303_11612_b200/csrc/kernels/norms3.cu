@@ -330,16 +330,18 @@ cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long
     const size_t smem = kTStages * kTStageBytes + 2 * kTStages * sizeof(uint64_t) + 1024;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(norms3_tma_kernel), smem, attr_done);
     if (e != cudaSuccess) return e;
-    norms3_tma_kernel<<<grid, kTThreads, smem, st>>>(tmap, I0, I1, I2, P0, P1, w2, P2, seg);
+    norms3_tma_kernel<<<grid, kTThreads, smem, st>>>(tmap, I0, I1, I2, P0, P1, w2, P2, seg); note_launch();
   } else {
-    norms3_chunks_kernel<<<grid, kN3Threads, 0, st>>>(x, I0, I1, I2, P0, P1, w2, P2, seg);
+    norms3_chunks_kernel<<<grid, kN3Threads, 0, st>>>(x, I0, I1, I2, P0, P1, w2, P2, seg); note_launch();
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  chunk_combine_kernel<<<(unsigned)((I1 * I2 + 255) / 256), 256, 0, st>>>(P0, I1 * I2, (int)c0, w0);
-  chunk_combine_kernel<<<(unsigned)((I0 * I2 + 255) / 256), 256, 0, st>>>(P1, I0 * I2, (int)c1, w1);
-  if (P2)
+  chunk_combine_kernel<<<(unsigned)((I1 * I2 + 255) / 256), 256, 0, st>>>(P0, I1 * I2, (int)c0, w0); note_launch();
+  chunk_combine_kernel<<<(unsigned)((I0 * I2 + 255) / 256), 256, 0, st>>>(P1, I0 * I2, (int)c1, w1); note_launch();
+  if (P2) {
     chunk_combine_kernel<<<(unsigned)((I0 * I1 + 255) / 256), 256, 0, st>>>(P2, I0 * I1, (int)c2, w2);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -945,7 +945,7 @@ cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, doub
   const size_t smem = leaf_smem(rows, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_qr_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_leaf_qr_kernel<RPL><<<nb, kQThreads, smem, st>>>(A, m, s, (int)m, nb, V, tau, S, lds);
+  orth_leaf_qr_kernel<RPL><<<nb, kQThreads, smem, st>>>(A, m, s, (int)m, nb, V, tau, S, lds); note_launch();
   return cudaGetLastError();
 }
 
@@ -956,7 +956,7 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
   const size_t smem = core_smem(m, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_core_kernel<RPL><<<1, kQThreads, smem, st>>>(S, m, s, m, mu, out, ldo, final_level, status, tol);
+  orth_core_kernel<RPL><<<1, kQThreads, smem, st>>>(S, m, s, m, mu, out, ldo, final_level, status, tol); note_launch();
   return cudaGetLastError();
 }
 
@@ -970,7 +970,7 @@ cudaError_t leaf_apply(const double* V, long long m, int s, int nb, const double
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_apply_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
   orth_leaf_apply_kernel<RPL><<<nb, kQThreads, smem, st>>>(V, m, s, (int)m, nb, tau, W, ldw, mu,
-                                                          out, (int)m, pbest, pidx);
+                                                          out, (int)m, pbest, pidx); note_launch();
   return cudaGetLastError();
 }
 
@@ -1023,7 +1023,7 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
                                            l == 0 ? pbest : nullptr, l == 0 ? pidx : nullptr, st);
     if (e != cudaSuccess) return e;
   }
-  orth_signfix_kernel<<<mu, 256, 0, st>>>(u, I, (int)I, mu, lv[0].nb, pbest, pidx);
+  orth_signfix_kernel<<<mu, 256, 0, st>>>(u, I, (int)I, mu, lv[0].nb, pbest, pidx); note_launch();
   return cudaGetLastError();
 }
 

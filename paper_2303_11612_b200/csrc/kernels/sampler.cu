@@ -1242,12 +1242,15 @@ struct ScanBufs {
 static cudaError_t exact_scan(const double* x, long long n, double* out, double* total,
                               int* status, int bad_flag, const ScanBufs& b, cudaStream_t st) {
   const int nc = nchunks_of(n);
-  chunk_sums_kernel<<<nc, kThr, 0, st>>>(x, n, b.csum);
-  chunk_plan_kernel<<<1, 1024, 0, st>>>(b.csum, nc, n, b.assumed, b.assumed2);
-  chunk_agg_kernel<<<nc, kThr, 0, st>>>(x, n, b.assumed, b.assumed2, b.agg, b.subagg);
+  chunk_sums_kernel<<<nc, kThr, 0, st>>>(x, n, b.csum); note_launch();
+  chunk_plan_kernel<<<1, 1024, 0, st>>>(b.csum, nc, n, b.assumed, b.assumed2); note_launch();
+  chunk_agg_kernel<<<nc, kThr, 0, st>>>(x, n, b.assumed, b.assumed2, b.agg, b.subagg); note_launch();
   chunk_walk_kernel<<<1, kCThr, 0, st>>>(x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
-                                         total, status, bad_flag);
-  if (out) chunk_write_kernel<<<nc, kThr, 0, st>>>(x, n, b.starts, b.substarts, out);
+                                         total, status, bad_flag); note_launch();
+  if (out) {
+    chunk_write_kernel<<<nc, kThr, 0, st>>>(x, n, b.starts, b.substarts, out);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 
@@ -1276,23 +1279,23 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   const int eg = 148 * 8;
   cudaError_t e;
   if (regime == 2) {  // uniform(n): p = 1/n each (sketching.cpp:50-53)
-    fill_kernel<<<eg, 256, 0, st>>>(p, n, 1.0 / (double)n);
+    fill_kernel<<<eg, 256, 0, st>>>(p, n, 1.0 / (double)n); note_launch();
   } else {
     // total = naive sum of w; x1 = w / total (+ beta mix); s = Neumaier(x1); p = x1 / s
     if ((e = exact_scan(w, n, nullptr, scal + 0, status, kBadWeight, b, st)) != cudaSuccess) return e;
-    normalize_mix_kernel<<<eg, 256, 0, st>>>(w, n, scal + 0, regime, beta, p, uni, status);
+    normalize_mix_kernel<<<eg, 256, 0, st>>>(w, n, scal + 0, regime, beta, p, uni, status); note_launch();
     if ((e = exact_scan(p, n, S, scal + 1, status, kBadWeight, b, st)) != cudaSuccess) return e;
-    neumaier_terms_kernel<<<nc, kThr, 0, st>>>(p, S, n, npart);
-    neumaier_final_kernel<<<1, kRedThr, 0, st>>>(p, n, scal + 1, npart, nc, scal + 1, status, uni);
-    divide_kernel<<<eg, 256, 0, st>>>(p, n, scal + 1, uni, status);
+    neumaier_terms_kernel<<<nc, kThr, 0, st>>>(p, S, n, npart); note_launch();
+    neumaier_final_kernel<<<1, kRedThr, 0, st>>>(p, n, scal + 1, npart, nc, scal + 1, status, uni); note_launch();
+    divide_kernel<<<eg, 256, 0, st>>>(p, n, scal + 1, uni, status); note_launch();
   }
-  check_last_kernel<<<nc, kThr, 0, st>>>(p, n, cpart, lastpos);
-  check_final_kernel<<<1, kRedThr, 0, st>>>(cpart, lastpos, nc, last, status);
+  check_last_kernel<<<nc, kThr, 0, st>>>(p, n, cpart, lastpos); note_launch();
+  check_final_kernel<<<1, kRedThr, 0, st>>>(cpart, lastpos, nc, last, status); note_launch();
   // cum = naive prefix of p; acc = cum[n-1]
   if ((e = exact_scan(p, n, S, scal + 2, status, kBadWeight, b, st)) != cudaSuccess) return e;
   const long long threads = (L + kDrawsPerThread - 1) / kDrawsPerThread;
   draw_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(S, p, n, scal + 2, last, L, seed,
-                                                                  stream, idx, scales, status);
+                                                                  stream, idx, scales, status); note_launch();
   return cudaGetLastError();
 }
 

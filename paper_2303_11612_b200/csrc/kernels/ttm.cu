@@ -389,7 +389,7 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
   double* bt = nullptr;  // packed copy, stream-ordered scratch
   cudaError_t pe = scratch_alloc(reinterpret_cast<void**>(&bt), sizeof(double) * v.I * M8, st);
   if (pe != cudaSuccess) return pe;
-  pack_b_kernel<<<(unsigned)((v.I * M8 + 255) / 256), 256, 0, st>>>(bt_colmajor, v.I, m, M8, bt);
+  pack_b_kernel<<<(unsigned)((v.I * M8 + 255) / 256), 256, 0, st>>>(bt_colmajor, v.I, m, M8, bt); note_launch();
   struct FreeGuard {
     double* p;
     cudaStream_t s;
@@ -406,7 +406,7 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
     if (e != cudaSuccess) return e;
     long long J = v.inner * v.outer;
     dim3 grid((unsigned)((J + C::JT - 1) / C::JT), (unsigned)ksplit);
-    ttm_kernel<M8, RC, KC, ST><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y, kper);
+    ttm_kernel<M8, RC, KC, ST><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y, kper); note_launch();
     return cudaGetLastError();
   };
   return go(std::integral_constant<int, 16>{}, std::integral_constant<int, 3>{});
@@ -472,7 +472,7 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
   if (ks > 1) {
     if (e == cudaSuccess) {
       const long long n = J * m;
-      reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ks, n, y);
+      reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ks, n, y); note_launch();
       e = cudaGetLastError();
     }
     scratch_free(part, st);
@@ -490,7 +490,7 @@ static cudaError_t launch_gram_t(const double* x, ModeView v, const double* h, i
                                    attr_done);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((v.I + C::RT - 1) / C::RT), (unsigned)nsplit);
-  gram_kernel<M8, RC><<<grid, kGramThreads, C::SMEM, st>>>(x, v, h, s, stot, koff, zpart, jper);
+  gram_kernel<M8, RC><<<grid, kGramThreads, C::SMEM, st>>>(x, v, h, s, stot, koff, zpart, jper); note_launch();
   return cudaGetLastError();
 }
 
@@ -540,7 +540,7 @@ cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, dou
     if (e != cudaSuccess) return e;
   }
   long long n = v.I * s;
-  reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(zpart, plan.nsplit, n, z);
+  reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(zpart, plan.nsplit, n, z); note_launch();
   return cudaGetLastError();
 }
 
@@ -548,13 +548,13 @@ cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, con
                           long long T, double* out, cudaStream_t st) {
   if (T == 0) return cudaSuccess;
   if (v.inner == 1) {
-    gather_contig_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(x, v.I, idx, scale, T, out);
+    gather_contig_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(x, v.I, idx, scale, T, out); note_launch();
   } else {
     // rows split over grid.y: each sampled fiber is strided (one sector per element), so the
     // gather is latency-bound and wants every SM issuing
     const long long tb = (T + 31) / 32, rb = (v.I + 31) / 32;
     const long long ry = std::max<long long>(1, std::min<long long>(rb, (4LL * device_sms() + tb - 1) / tb));
-    gather_strided_kernel<<<dim3((unsigned)tb, (unsigned)ry), 256, 0, st>>>(x, v, idx, scale, T, out);
+    gather_strided_kernel<<<dim3((unsigned)tb, (unsigned)ry), 256, 0, st>>>(x, v, idx, scale, T, out); note_launch();
   }
   return cudaGetLastError();
 }

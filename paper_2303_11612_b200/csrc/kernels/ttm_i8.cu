@@ -313,6 +313,11 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       I8_WAIT(7, mbar_wait(accfull, (unsigned)(tcount & 1)));
       tc_fence_after();
       I8_T0(te0);
+#ifdef LMRA_I8_NO_EPILOGUE  // microbenchmark only: release at once, no output (upper bound)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty);
+      continue;
+#endif
       // recombine the 6 level accumulators of column j, scale by 2^(ex + eq_m - 94 + 40); the
       // accumulators are released as soon as the last chunk is in registers
       const int half = (warp - kI8EpiWarp0) >> 2;  // two warps per sub-partition split the chunks
@@ -473,7 +478,7 @@ cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, c
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
   const int grid = (int)(ntiles < sms ? ntiles : sms);
-  ttm_i8_kernel<N><<<grid, kI8Threads, smem, st>>>(map, qd, eq, w, J, K, mu, y);
+  ttm_i8_kernel<N><<<grid, kI8Threads, smem, st>>>(map, qd, eq, w, J, K, mu, y); note_launch();
   return cudaGetLastError();
 }
 
@@ -497,7 +502,7 @@ cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const doubl
   const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
   uint8_t* qd = static_cast<uint8_t*>(work);
   int* eq = reinterpret_cast<int*>(qd + ((size_t)nks * kI8Digits * N * kI8Kstep + 255) / 256 * 256);
-  q_digits_kernel<<<N, 256, 0, st>>>(q, (int)K, mu, N, qd, eq);
+  q_digits_kernel<<<N, 256, 0, st>>>(q, (int)K, mu, N, qd, eq); note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap map;

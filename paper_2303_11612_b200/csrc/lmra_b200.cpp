@@ -612,7 +612,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   ck(cudaEventCreate(&ev0), "event");
   ck(cudaEventCreate(&ev1), "event");
   ck(cudaEventRecord(ev0, st), "event");
-  const long long launches0 = ctx->launches;
+  const long long launches0 = lmra_dev::g_kernel_launches;
 
   // Omega for every mode (gaussian_stream = {seed, n+1}, sketching.cpp:164-173) is data
   // independent: a host thread draws it into pinned memory while the GPU already runs
@@ -881,7 +881,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   for (size_t n = 0; n < N; ++n)
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
   res->t_device = dev_ms;
-  res->launches = (double)(ctx->launches - launches0);
+  res->launches = (double)(lmra_dev::g_kernel_launches - launches0);
   static const bool timeline = getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1';
   if (timeline && !prof.empty()) {  // diagnostics: phase start/end relative to the first phase
     for (const PhaseRec& p : prof) {
@@ -966,7 +966,7 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   ck(cudaEventCreate(&ev0), "event");
   ck(cudaEventCreate(&ev1), "event");
   ck(cudaEventRecord(ev0, st), "event");
-  const long long launches0 = ctx->launches;
+  const long long launches0 = lmra_dev::g_kernel_launches;
 
   std::vector<size_t> om_off(N + 1, 0);
   for (size_t n = 0; n < N; ++n) {
@@ -1250,7 +1250,7 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   for (size_t n = 0; n < N; ++n)
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
   res->t_device = dev_ms;
-  res->launches = (double)(ctx->launches - launches0);
+  res->launches = (double)(lmra_dev::g_kernel_launches - launches0);
   static const bool timeline = getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1';
   if (timeline && !prof.empty()) {  // diagnostics: phase start/end relative to the first phase
     for (const PhaseRec& p : prof) {
