@@ -153,7 +153,6 @@ void lmra_result_free(lmra_result* r);
 /* y = x x_mode b, b is b_rows x dims[mode] column-major (tensor.cpp:118-139) */
 int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
                         int mode, const double* b, uint64_t b_rows, double* y);
-/* c = (A A^T)^q G  (linalg.cpp:62-80), A rows x cols, G rows x s */
 /* y (mu x J) = q^T x for the mode-0 view of a tensor (x: K x J, column j contiguous; q: K x mu
  * column-major; w[j] = canonical squared norm of column j), computed on the int8 tensor cores
  * with exact digit products (~1e-13 relative).  Replaces, for the core's first contraction,
@@ -162,6 +161,7 @@ int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims
 int lmra_mode0_product_i8(lmra_context* ctx, const double* x, uint64_t K, uint64_t J, const double* q,
                           int mu, const double* w, double* y);
 
+/* c = (A A^T)^q G  (linalg.cpp:62-80), A rows x cols, G rows x s */
 int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uint64_t cols,
                           const double* g, uint64_t s, int q, int strategy, double* c);
 /* u = top-mu left singular vectors of c with the reference's sign rule (linalg.cpp:82-87) */
