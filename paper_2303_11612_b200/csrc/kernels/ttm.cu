@@ -9,6 +9,7 @@
 // dimension is j; the short dimension (factor / sketch width, <= 64) lives in
 // the N of m16n8k4 and is padded to a multiple of 8.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
@@ -450,8 +451,19 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
   const long long jt = (J + 127) / 128;
   int ks = 1;
   const int sms = device_sms();
-  if (jt * 2 <= sms && v.I >= 256)
+  if (jt * 2 <= sms && v.I >= 256) {
     ks = (int)std::max<long long>(1, std::min<long long>(sms / jt, v.I / 64));
+  } else if (v.I >= 512 && jt < 8LL * sms) {
+    // a few waves of a long-K contraction: fill the last wave (two CTAs per SM) by splitting
+    // K, each extra split charged ~3 % for its partials' round trip
+    const double slots = 2.0 * sms;
+    auto fill = [&](int k) {
+      const double n = (double)(jt * k);
+      return n / (std::ceil(n / slots) * slots) - 0.03 * (k - 1);
+    };
+    for (int k = 2; k <= 4 && v.I / k >= 128; ++k)
+      if (fill(k) > fill(ks) + 1e-9) ks = k;
+  }
   long long kper = (v.I + ks - 1) / ks;
   kper = ((kper + 15) / 16) * 16;
   ks = (int)((v.I + kper - 1) / kper);
