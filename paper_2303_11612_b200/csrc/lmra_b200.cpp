@@ -216,7 +216,8 @@ struct lmra_context {
   int nranks = 1, rank = 0;
   std::mutex mu;
   long long launches = 0;
-  bool profile = false;  // per-launch CUDA events (lmra_context_set_profiling)
+  int profile = 0;  // per-launch CUDA events (lmra_context_set_profiling): 1 every phase,
+                    // 2 only the phases on the context's own stream (light)
   bool keep_trace = true;  // copy drawn samples / norms back to the host (lmra_context_set_trace)
   std::vector<cudaEvent_t> events;
   size_t next_event = 0;
@@ -776,7 +777,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     for (size_t n = 0; n < N; ++n) {
       cudaStream_t sn = ctx->aux_stream(n);
       ck(cudaStreamWaitEvent(sn, fork, 0), "wait");
-      engs.emplace_back(ctx, sn, ctx->profile ? &prof : nullptr);
+      engs.emplace_back(ctx, sn, ctx->profile == 1 ? &prof : nullptr);
     }
     for (size_t n = 0; n < N; ++n) sample_mode(engs[n], in.x, in.dims, n, amm ? t_flat[n] : 0);
     upload_omegas();
@@ -1548,7 +1549,7 @@ int lmra_result_phase(const lmra_result* r, int i, char* name, size_t name_len, 
 }
 
 int lmra_context_set_profiling(lmra_context* ctx, int on) {
-  return guard([&] { ctx->profile = on != 0; });
+  return guard([&] { ctx->profile = on < 0 ? 0 : (on > 2 ? 1 : on); });
 }
 
 int lmra_context_set_trace(lmra_context* ctx, int on) {

@@ -178,9 +178,11 @@ class Context:
         """Keep host copies of drawn samples / column norms in results (default on)."""
         check(lib.lmra_context_set_trace(self.handle, int(bool(on))))
 
-    def set_profiling(self, on: bool):
-        """Per-launch CUDA events on the context stream -> _Result.phases()."""
-        check(lib.lmra_context_set_profiling(self.handle, int(bool(on))))
+    def set_profiling(self, on):
+        """Per-launch CUDA events -> _Result.phases(): True / 1 every phase, 2 only the
+        phases on the context's own stream (light), False / 0 none."""
+        level = on if isinstance(on, int) and not isinstance(on, bool) else int(bool(on))
+        check(lib.lmra_context_set_profiling(self.handle, level))
 
     def set_comm(self, unique_id: bytes, nranks: int, rank: int):
         """NCCL communicator (one process per GPU): later runs on this context are sharded
