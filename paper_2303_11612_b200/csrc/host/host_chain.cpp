@@ -6,6 +6,9 @@
 #include <iostream>
 #include <numeric>
 #include <stdexcept>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <thread>
 
 namespace lmra_host {
@@ -66,31 +69,108 @@ int host_threads() {
   return h ? static_cast<int>(std::min(h, 64u)) : 1;
 }
 
-void fill_normals(uint64_t seed, uint64_t stream, double* out, size_t n, int threads) {
-  auto work = [&](size_t b, size_t e) {
-    if (b >= e) return;
-    Rng g(seed, stream);
-    g.advance(4 * (b / 2));
-    size_t i = b;
-    if (i & 1) {
-      g.next_normal();
-      out[i++] = g.next_normal();
+void fill_normals_range(uint64_t seed, uint64_t stream, double* out, size_t b, size_t e) {
+  if (b >= e) return;
+  Rng g(seed, stream);
+  g.advance(4 * (b / 2));
+  size_t i = b;
+  if (i & 1) {
+    g.next_normal();
+    out[i++] = g.next_normal();
+  }
+  for (; i < e; ++i) out[i] = g.next_normal();
+}
+
+// ---------------------------------------------------------------- worker pool
+namespace {
+class Pool {
+ public:
+  explicit Pool(int n) {
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
     }
-    for (; i < e; ++i) out[i] = g.next_normal();
-  };
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void push(std::function<void()> f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push_back(std::move(f));
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+        if (stop_ && q_.empty()) return;
+        f = std::move(q_.front());
+        q_.pop_front();
+      }
+      f();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::deque<std::function<void()>> q_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+};
+
+Pool& pool() {
+  static Pool p(std::max(1, host_threads()));
+  return p;
+}
+}  // namespace
+
+struct TaskGroup::State {
+  std::mutex mu;
+  std::condition_variable cv;
+  long pending = 0;
+};
+
+TaskGroup::TaskGroup() : st_(std::make_shared<State>()) {}
+TaskGroup::~TaskGroup() { wait(); }
+
+void TaskGroup::run(std::function<void()> f) {
+  {
+    std::lock_guard<std::mutex> lk(st_->mu);
+    ++st_->pending;
+  }
+  std::shared_ptr<State> st = st_;
+  pool().push([st, f = std::move(f)] {
+    f();
+    std::lock_guard<std::mutex> lk(st->mu);
+    if (--st->pending == 0) st->cv.notify_all();
+  });
+}
+
+void TaskGroup::wait() {
+  std::unique_lock<std::mutex> lk(st_->mu);
+  st_->cv.wait(lk, [this] { return st_->pending == 0; });
+}
+
+void fill_normals(uint64_t seed, uint64_t stream, double* out, size_t n, int threads) {
   if (threads <= 1 || n < 8192) {
-    work(0, n);
+    fill_normals_range(seed, stream, out, 0, n);
     return;
   }
-  threads = (int)std::min<size_t>((size_t)threads, n / 4096);
-  std::vector<std::thread> pool;
-  size_t chunk = ((n + threads - 1) / threads + 1) & ~size_t(1);
-  for (int t = 1; t < threads; ++t) {
-    size_t b = std::min(n, t * chunk), e = std::min(n, b + chunk);
-    pool.emplace_back(work, b, e);
+  // chunks on the persistent pool (jump-ahead per chunk: bit-identical to the sequential loop)
+  const size_t chunk = std::max<size_t>(4096, ((n / (4 * (size_t)threads)) + 1) & ~size_t(1));
+  TaskGroup tg;
+  for (size_t b = 0; b < n; b += chunk) {
+    const size_t e = std::min(n, b + chunk);
+    tg.run([=] { fill_normals_range(seed, stream, out, b, e); });
   }
-  work(0, std::min(n, chunk));
-  for (auto& t : pool) t.join();
+  tg.wait();
 }
 
 // ---------------------------------------------------------------- sketching.cpp:13-53

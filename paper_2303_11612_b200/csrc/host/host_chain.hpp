@@ -5,6 +5,8 @@
 // two roundings, as in the reference sources.
 #pragma once
 #include <cstdint>
+#include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -29,6 +31,25 @@ class Rng {
 // normals [0, n) of stream (seed, stream) in generation order; threads split the
 // sequence with jump-ahead (bit-identical to the sequential loop).
 void fill_normals(uint64_t seed, uint64_t stream, double* out, size_t n, int threads);
+
+// normals [b, e) of stream (seed, stream) (b even), written to out[b..e)
+void fill_normals_range(uint64_t seed, uint64_t stream, double* out, size_t b, size_t e);
+
+// A set of host tasks run by a persistent process-wide worker pool (threads are started
+// once; spawning threads per run cost more than the Omega draw of the small configs).
+class TaskGroup {
+ public:
+  TaskGroup();
+  ~TaskGroup();  // waits
+  TaskGroup(const TaskGroup&) = delete;
+  TaskGroup& operator=(const TaskGroup&) = delete;
+  void run(std::function<void()> f);
+  void wait();
+
+ private:
+  struct State;
+  std::shared_ptr<State> st_;
+};
 
 double stable_sum(const double* v, size_t n);
 void check_distribution(const std::vector<double>& w);

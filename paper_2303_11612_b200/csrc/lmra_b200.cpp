@@ -625,23 +625,32 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     om_off[n + 1] = om_off[n] + in.dims[n] * r.sketch[n];
   }
   double* om_pin = ctx->pinned_buffer(om_off[N]);
-  std::thread omega_thread([&] {
-    const double tr0 = now_ms();
-    for (size_t n = 0; n < N; ++n) {
-      const size_t cnt = om_off[n + 1] - om_off[n];
-      if (in.ov && in.ov->omega && in.ov->omega[n])
-        std::memcpy(om_pin + om_off[n], in.ov->omega[n], sizeof(double) * cnt);
-      else
-        fill_normals(cfg.seed, n + 1, om_pin + om_off[n], cnt, host_threads());
+  // drawn in chunks by the persistent host worker pool (jump-ahead: bit-identical to the
+  // sequential stream), overlapping the device's norm pass / sampling chains
+  lmra_host::TaskGroup omega_tasks;
+  const double tr0 = now_ms();
+  bool rng_done = false;
+  for (size_t n = 0; n < N; ++n) {
+    const size_t cnt = om_off[n + 1] - om_off[n];
+    double* dst = om_pin + om_off[n];
+    if (in.ov && in.ov->omega && in.ov->omega[n]) {
+      std::memcpy(dst, in.ov->omega[n], sizeof(double) * cnt);
+      continue;
     }
-    res->t_rng = now_ms() - tr0;
-  });
-  struct JoinGuard {
-    std::thread& t;
-    ~JoinGuard() {
-      if (t.joinable()) t.join();
+    constexpr size_t kChunk = 4096;  // even: chunks start on a Box-Muller pair
+    const uint64_t seed = cfg.seed, stream = n + 1;
+    for (size_t b0 = 0; b0 < cnt; b0 += kChunk) {
+      const size_t e0 = std::min(cnt, b0 + kChunk);
+      omega_tasks.run([=] { fill_normals_range(seed, stream, dst, b0, e0); });
     }
-  } join_guard{omega_thread};
+  }
+  auto omega_ready = [&] {
+    omega_tasks.wait();
+    if (!rng_done) {
+      res->t_rng = now_ms() - tr0;
+      rng_done = true;
+    }
+  };
 
   // per-mode device status words: [0, N) orth convergence, [N, 2N) sampler flags
   DevBuf status(N, st);
@@ -696,14 +705,14 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   };
 
   // phase 2 of a mode: Omega -> power scheme (on the unfolding or the sampled columns)
-  // -> orthonormalised factor.  Omega must be drawn (omega_thread joined) before this.
+  // -> orthonormalised factor.  Omega must be drawn (omega_ready) before this.
   // Omega uploads: every mode's draw goes up in one copy on its own stream as soon as the
   // host thread is done (during the norm pass), instead of in stream order behind each
   // mode's sampling chain, where the copy sat on the critical path.
   std::vector<DevBuf> d_om(N);
   cudaEvent_t om_ready = nullptr;
   auto upload_omegas = [&] {
-    if (omega_thread.joinable()) omega_thread.join();
+    omega_ready();
     if (om_ready) return;
     cudaStream_t cs = ctx->aux_stream(N);
     ck(cudaStreamWaitEvent(cs, ev0, 0), "wait");  // the run's start (stream-ordered arena)
