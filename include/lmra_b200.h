@@ -162,6 +162,12 @@ int lmra_mode_n_product(lmra_context* ctx, const double* x, const uint64_t* dims
  * ST-HOSVD shrink (tucker.cpp:397-420).  Device pointers; K even <= 4096, mu <= 64. */
 int lmra_mode0_product_i8(lmra_context* ctx, const double* x, uint64_t K, uint64_t J, const double* q,
                           int mu, const double* w, double* y);
+/* y (R x mu x O) = x x_1 q^T for x (R x K x O, R fastest) on the int8 tensor cores: the mode-1
+ * product (tensor.hpp:56-57) of a tensor whose first mode has R <= 64 (even) entries, as in the
+ * core's second contraction (tucker.cpp:81-92).  Column scales from the columns' maximum
+ * exponents (computed here; run_algorithm takes them from the preceding mode-0 contraction). */
+int lmra_mode1_product_i8(lmra_context* ctx, const double* x, uint64_t R, uint64_t K, uint64_t O,
+                          const double* q, int mu, double* y);
 
 /* c = (A A^T)^q G  (linalg.cpp:62-80), A rows x cols, G rows x s */
 int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uint64_t cols,

@@ -91,6 +91,7 @@ def _load():
                                         C.POINTER(C.c_int)]),
         "lmra_mode_n_product": (C.c_int, [vp, vp, u64p, C.c_int, C.c_int, vp, C.c_uint64, vp]),
         "lmra_mode0_product_i8": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp, C.c_int, vp, vp]),
+        "lmra_mode1_product_i8": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_int, vp]),
         "lmra_gram_power_apply": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp, C.c_uint64,
                                             C.c_int, C.c_int, vp]),
         "lmra_leading_left_singular_vectors": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64,
@@ -131,7 +132,7 @@ EXPORTED = [
     "lmra_result_copy_norms", "lmra_result_timings", "lmra_result_free",
     "lmra_context_set_profiling", "lmra_result_num_phases", "lmra_result_phase",
     "lmra_context_set_trace", "lmra_sample_columns_device",
-    "lmra_mode_n_product", "lmra_mode0_product_i8",
+    "lmra_mode_n_product", "lmra_mode0_product_i8", "lmra_mode1_product_i8",
     "lmra_gram_power_apply", "lmra_leading_left_singular_vectors", "lmra_column_sqnorms",
     "lmra_gaussian_matrix", "lmra_probabilities", "lmra_randsample", "lmra_amm_sample_counts",
     "lmra_gen_tucker_noise", "lmra_gen_hilbert", "lmra_gen_video", "lmra_device_alloc",

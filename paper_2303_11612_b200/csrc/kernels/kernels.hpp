@@ -72,8 +72,21 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
 // K <= 4096, mu <= 64, x 16-byte aligned.
 bool ttm_i8_supported(long long K, long long J, int mu, const double* x);
 size_t ttm_i8_workspace_bytes(long long K, int mu);
+// fexp_out (optional, mu x O ints, preset to INT_MIN): receives the max binary exponent of
+// every mode-1 fibre (m, o) of Y, with column j = i1 + I1 o -- the scales of a following
+// launch_ttm_i8_inner over i1.
 cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const double* q, int mu,
-                          const double* w, double* y, void* work, cudaStream_t st);
+                          const double* w, double* y, void* work, cudaStream_t st,
+                          int* fexp_out = nullptr, long long I1 = 0);
+// The same contraction over the middle index of X(r, k, o) = x[r + R (k + K o)] (R <= 64, even):
+// Y(r, m, o) = sum_k q[k, m] X(r, k, o), i.e. the mode-1 product of a tensor whose mode 0 has
+// R entries.  fexp_in[r + R o] = max binary exponent of column (r, o) (INT_MIN: all zero).
+bool ttm_i8_inner_supported(long long R, long long K, long long O, int mu, const double* x);
+cudaError_t launch_ttm_i8_inner(const double* x, long long R, long long K, long long O, const double* q,
+                                int mu, const int* fexp_in, double* y, void* work, cudaStream_t st);
+// fexp[r + R o] = max binary exponent over k of X(r, k, o) (INT_MIN: all zero)
+cudaError_t launch_column_exponents(const double* x, long long R, long long K, long long O, int* fexp,
+                                    cudaStream_t st);
 
 // ---- synthetic generators (device) ----
 // element e of the normal sequence of PCG32 stream (seed, stream), Box-Muller pairs as in rng.hpp

@@ -36,7 +36,9 @@
 // cost ~45 cycles regardless of N (measured, tools/microbench/umma_rate.cu) while N >= 128 runs
 // at the full 8192 MAC/clk, so 9 grouped MMAs (~690 cycles per K-step) replace 21 (~955).
 // Accumulators are zeroed by the epilogue warps (every MMA accumulates).
+#include <climits>
 #include <cmath>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -168,10 +170,36 @@ __device__ __forceinline__ const double* xs_elem(const double* stage, int j, int
 }
 
 
-template <int N>
+// Geometry of one contraction.  Mode-0 form (kInner = false): X is K x J with column j
+// contiguous, scales from the canonical squared column norms w.  Inner form (kInner = true):
+// X(r, k, o) = x[r + R (k + K o)] with R <= 64 (the mode-1 view of a tensor whose first mode
+// has already been contracted to R), contracted over k; a tile is 2 o-slices x 64 rows r
+// (rows r >= R are the TMA's zero fill), scales from per-column maximum exponents fexp_in.
+struct I8Geom {
+  long long J;          // mode-0: columns
+  int K;
+  int R;                // inner: rows per o-slice (<= 64)
+  long long O;          // inner: o-slices
+  const double* w;      // mode-0: canonical squared column norms
+  const int* fexp_in;   // inner: max binary exponent of column (r, o) at r + R o
+  int* fexp_out;        // mode-0, optional: max exponent of Y's mode-1 fibres (m, o), m + mu o,
+  long long I1;         //   with j = i1 + I1 o (the next contraction's columns)
+};
+
+// binary exponent e with |v| < 2^(e+1) (an upper bound for subnormals), INT_MIN for 0
+__device__ __forceinline__ int exp_bound(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v) << 1;
+  if (b == 0) return -2147483647 - 1;
+  const int e = (int)(b >> 53);
+  return e == 0 ? -1023 : e - 1023;
+}
+
+template <int N, bool kInner>
 __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     const __grid_constant__ CUtensorMap xmap, const uint8_t* __restrict__ qd, const int* __restrict__ eqg,
-    const double* __restrict__ w, long long J, int K, int mu, double* __restrict__ y) {
+    const I8Geom geo, int mu, double* __restrict__ y) {
+  const long long J = geo.J;
+  const int K = geo.K;
   constexpr int kQBytes = kI8Digits * N * kI8Kstep;
   constexpr uint32_t kAccCols = kI8Levels * N;
   constexpr uint32_t kACols = kI8Digits * 8;  // 6 digits x 32 bytes per lane
@@ -197,7 +225,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nks = (K + kI8Kstep - 1) / kI8Kstep;
-  const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
+  const long long ntiles = kInner ? (geo.O + 1) / 2 : (J + kI8Tile - 1) / kI8Tile;
 #ifdef LMRA_I8_CLOCKS
   long long i8acc[20] = {0};
   const long long i8start = clock64();
@@ -239,8 +267,12 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
           I8_WAIT(0, mbar_wait(&empty[st], (unsigned)((g / kI8Stages) & 1) ^ 1u));
           mbar_arrive_expect_tx(&full[st], kI8XBytes);
           double* dst = xs + (size_t)st * (kI8XBytes / 8);
-          tma_load_2d(dst, &xmap, &full[st], ks * kI8Kstep, (int)(t * kI8Tile));
-          tma_load_2d(dst + kI8Tile * 16, &xmap, &full[st], ks * kI8Kstep + 16, (int)(t * kI8Tile));
+          if (kInner) {  // one box: 64 rows r x 32 k x 2 o-slices, [o][k][r] in smem
+            tma_load_3d(dst, &xmap, &full[st], 0, ks * kI8Kstep, (int)(2 * t));
+          } else {
+            tma_load_2d(dst, &xmap, &full[st], ks * kI8Kstep, (int)(t * kI8Tile));
+            tma_load_2d(dst + kI8Tile * 16, &xmap, &full[st], ks * kI8Kstep + 16, (int)(t * kI8Tile));
+          }
         }
       }
     }
@@ -304,12 +336,31 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
       const long long j = t * kI8Tile + jl;
       const long long jw0 = t * kI8Tile + 32 * (warp & 3);  // first column of this warp
+      const int rrow = jl & 63;                                // inner form: row r, slice o
+      const long long ocol = 2 * t + (jl >> 6);
       int ex = 0;
-      if (j < J) {
-        const double nrm = sqrt(w[j]);
-        ex = nrm > 0.0 ? ilogb(nrm) + 2 : 0;
+      bool valid;
+      if (kInner) {
+        valid = rrow < geo.R && ocol < geo.O;
+        const int fe = valid ? geo.fexp_in[rrow + (long long)geo.R * ocol] : INT_MIN;
+        ex = fe > -1100 ? fe + 2 : 0;
+      } else {
+        valid = j < J;
+        if (valid) {
+          const double nrm = sqrt(geo.w[j]);
+          ex = nrm > 0.0 ? ilogb(nrm) + 2 : 0;
+        }
       }
       const double sj = ldexp(1.0, ex - 94 + 8 * kI8MinLevel);  // column part of the scale
+      // mode-0 with fexp_out: the warp's 32 columns lie in one o-slice of the next contraction
+      // unless they straddle a multiple of I1
+      long long o_lo = 0;
+      bool o_uniform = true;
+      if (!kInner && geo.fexp_out) {
+        const long long jhi = min(jw0 + 31, J - 1);
+        o_lo = jw0 / geo.I1;
+        o_uniform = o_lo == jhi / geo.I1;
+      }
       I8_WAIT(7, mbar_wait(accfull, (unsigned)(tcount & 1)));
       tc_fence_after();
       I8_T0(te0);
@@ -352,20 +403,45 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
           for (int L = kI8Levels - 2; L >= 0; --L) sacc = fma(sacc, 256.0, i32_to_f64(v[L][u]));
           // scale 2^(ex + eq_m - 94 + 40) as two exact power-of-two products (branch-free, so
           // the 8 outputs' chains interleave)
-          ost[lane * kI8StageLd + u] = (sacc * sj) * qsc[m];
+          const double val = (sacc * sj) * qsc[m];
+          if (kInner) {  // Y(r, m, o): rows r of one slice are consecutive -- coalesced as is
+            if (valid && m < mu) y[rrow + (long long)geo.R * (m + (long long)mu * ocol)] = val;
+          } else {
+            ost[lane * kI8StageLd + u] = val;
+          }
         }
-        __syncwarp();
-        I8_ACC(18, tcp);
-        I8_T0(tst);
-        // coalesced-ish stores: 4 columns x 8 outputs per instruction (64-byte runs of Y)
+        if (!kInner) {
+          __syncwarp();
+          I8_ACC(18, tcp);
+          I8_T0(tst);
+          // coalesced-ish stores: 4 columns x 8 outputs per instruction (64-byte runs of Y)
+          unsigned hmax = 0u;  // fexp_out: |v|'s high word orders like |v| (exponent on top)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int jj = 4 * i + (lane >> 3), mm = lane & 7;
-          const long long jo = jw0 + jj;
-          if (m0 + mm < mu && jo < J) y[(m0 + mm) + (size_t)mu * jo] = ost[jj * kI8StageLd + mm];
+          for (int i = 0; i < 8; ++i) {
+            const int jj = 4 * i + (lane >> 3), mm = lane & 7;
+            const long long jo = jw0 + jj;
+            const double v = ost[jj * kI8StageLd + mm];
+            if (m0 + mm < mu && jo < J) {
+              y[(m0 + mm) + (size_t)mu * jo] = v;
+              const unsigned hw = (unsigned)__double2hiint(v) & 0x7fffffffu;
+              if (o_uniform)
+                hmax = max(hmax, hw);
+              else if (geo.fexp_out && hw != 0u)  // columns straddle two o-slices: one by one
+                atomicMax(&geo.fexp_out[(m0 + mm) + (long long)mu * (jo / geo.I1)],
+                          (hw >> 20) == 0 ? -1023 : (int)(hw >> 20) - 1023);
+            }
+          }
+          if (geo.fexp_out && o_uniform) {  // max exponent of Y's mode-1 fibre (m, o): each lane
+                                            // holds 8 of the warp's 32 columns of output m0 + mm
+            hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, 8));
+            hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, 16));
+            if (lane < 8 && m0 + lane < mu && hmax != 0u)
+              atomicMax(&geo.fexp_out[(m0 + lane) + (long long)mu * o_lo],
+                        (hmax >> 20) == 0 ? -1023 : (int)(hmax >> 20) - 1023);
+          }
+          __syncwarp();  // the staging rows are rewritten by the next chunk
+          I8_ACC(16, tst);
         }
-        __syncwarp();  // the staging rows are rewritten by the next chunk
-        I8_ACC(16, tst);
       }
       I8_ACC(14, te0);
     }
@@ -376,13 +452,36 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     long long g = 0, tcount = 0;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
       const long long j = t * kI8Tile + jl;
+      const int rrow = jl & 63;
+      const long long ocol = 2 * t + (jl >> 6);
+      bool has = false;
       int ex = 0;
-      double scale = 0.0;
-      if (j < J) {
-        const double nrm = sqrt(w[j]);
-        ex = nrm > 0.0 ? ilogb(nrm) + 2 : 0;
-        scale = nrm > 0.0 ? ldexp(1.0, 47 - ex) : 0.0;
+      if (kInner) {
+        const int fe = (rrow < geo.R && ocol < geo.O) ? geo.fexp_in[rrow + (long long)geo.R * ocol] : INT_MIN;
+        if (fe > -1100) {
+          ex = fe + 2;
+          has = true;
+        }
+      } else if (j < J) {
+        const double nrm = sqrt(geo.w[j]);
+        if (nrm > 0.0) {
+          ex = ilogb(nrm) + 2;
+          has = true;
+        }
       }
+      // 2^(47 - ex) as s1 * s2 (s2 = 1 unless the column is below ~2^-950, where one power
+      // of two would overflow); x * s1 is exact, so fma(x s1, s2, M) rounds once like
+      // fma(x, 2^(47-ex), M)
+      double s1 = 0.0, s2 = 1.0;
+      bool big = false;
+      if (has) {
+        const int sh = 47 - ex, a = sh > 1000 ? 1000 : sh;
+        s1 = ldexp(1.0, a);
+        s2 = ldexp(1.0, sh - a);
+        big = sh > 1000;
+      }
+      const bool warp_big = __any_sync(0xffffffffu, big);  // uniform: the two-step path only
+                                                           // when a column of the warp needs it
       // V = round(x 2^(47-ex)) read off the bits of fma(x, 2^(47-ex), 1.5 2^52): for |V| < 2^51
       // the sum is exact up to the final rounding (= round-to-nearest-even of x 2^(47-ex)) and
       // its low 51 bits are V's two's complement bits, i.e. bytes 0..5 are V's digits
@@ -394,31 +493,49 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
         const double* stage = xs + (size_t)st * (kI8XBytes / 8);
         I8_T0(ts0);
         uint32_t dw[kI8Digits][8];
+        // the conversion, instantiated with and without the two-step scale (warp-uniform
+        // choice outside the loop: a branch inside it cost the slicers ~50 %)
+        auto convert = [&](auto two_step) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // k = 4c .. 4c+3: two 16-byte chunks of one swizzled row
-          const double* rowp = stage + (c >> 2) * (kI8Tile * 16) + jl * 16;
-          const int c2 = 2 * (c & 3);
-          const double2 p0 = *reinterpret_cast<const double2*>(rowp + ((c2 ^ (jl & 7)) << 1));
-          const double2 p1 = *reinterpret_cast<const double2*>(rowp + (((c2 + 1) ^ (jl & 7)) << 1));
-          const double xv[4] = {p0.x, p0.y, p1.x, p1.y};
-          uint32_t lo[4], hi[4];
+          for (int c = 0; c < 8; ++c) {  // k = 4c .. 4c+3
+            double xv[4];
+            if (kInner) {  // stage [o][k][r]: this row's k values at stride 64 (conflict-free)
+              const double* colp = stage + (size_t)(jl >> 6) * (32 * 64) + rrow + (4 * c) * 64;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double d = fma(xv[u], scale, kMagic);
-            lo[u] = (uint32_t)__double2loint(d);
-            hi[u] = (uint32_t)__double2hiint(d);
+              for (int u = 0; u < 4; ++u) xv[u] = colp[u * 64];
+            } else {  // two 16-byte chunks of one swizzled row
+              const double* rowp = stage + (c >> 2) * (kI8Tile * 16) + jl * 16;
+              const int c2 = 2 * (c & 3);
+              const double2 p0 = *reinterpret_cast<const double2*>(rowp + ((c2 ^ (jl & 7)) << 1));
+              const double2 p1 = *reinterpret_cast<const double2*>(rowp + (((c2 + 1) ^ (jl & 7)) << 1));
+              xv[0] = p0.x;
+              xv[1] = p0.y;
+              xv[2] = p1.x;
+              xv[3] = p1.y;
+            }
+            uint32_t lo[4], hi[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double d = decltype(two_step)::value ? fma(xv[u] * s1, s2, kMagic) : fma(xv[u], s1, kMagic);
+              lo[u] = (uint32_t)__double2loint(d);
+              hi[u] = (uint32_t)__double2hiint(d);
+            }
+            // digit s of the 4 values = byte s of each V, packed little-endian
+            const uint32_t l01 = __byte_perm(lo[0], lo[1], 0x5140), l23 = __byte_perm(lo[2], lo[3], 0x5140);
+            const uint32_t l01b = __byte_perm(lo[0], lo[1], 0x7362), l23b = __byte_perm(lo[2], lo[3], 0x7362);
+            dw[0][c] = __byte_perm(l01, l23, 0x5410) ^ 0x80808080u;    // bytes 0
+            dw[1][c] = __byte_perm(l01, l23, 0x7632) ^ 0x80808080u;    // bytes 1
+            dw[2][c] = __byte_perm(l01b, l23b, 0x5410) ^ 0x80808080u;  // bytes 2
+            dw[3][c] = __byte_perm(l01b, l23b, 0x7632) ^ 0x80808080u;  // bytes 3
+            const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
+            dw[4][c] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;    // bytes 4
+            dw[5][c] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;    // bytes 5
           }
-          // digit s of the 4 values = byte s of each V, packed little-endian
-          const uint32_t l01 = __byte_perm(lo[0], lo[1], 0x5140), l23 = __byte_perm(lo[2], lo[3], 0x5140);
-          const uint32_t l01b = __byte_perm(lo[0], lo[1], 0x7362), l23b = __byte_perm(lo[2], lo[3], 0x7362);
-          dw[0][c] = __byte_perm(l01, l23, 0x5410) ^ 0x80808080u;    // bytes 0
-          dw[1][c] = __byte_perm(l01, l23, 0x7632) ^ 0x80808080u;    // bytes 1
-          dw[2][c] = __byte_perm(l01b, l23b, 0x5410) ^ 0x80808080u;  // bytes 2
-          dw[3][c] = __byte_perm(l01b, l23b, 0x7632) ^ 0x80808080u;  // bytes 3
-          const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
-          dw[4][c] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;    // bytes 4
-          dw[5][c] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;    // bytes 5
-        }
+        };
+        if (warp_big)
+          convert(std::true_type{});
+        else
+          convert(std::false_type{});
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the X stage
         I8_ACC(11, ts0);
@@ -465,21 +582,55 @@ PFN_cuTensorMapEncodeTiled_v12000 i8_tensor_map_encoder() {
   return fn;
 }
 
-template <int N>
-cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, const double* w, long long J,
-                     int K, int mu, double* y, cudaStream_t st) {
+// fexp[r + R o] = max_k exp_bound(x[r + R (k + K o)]) (INT_MIN for an all-zero column)
+__global__ void column_exponents_kernel(const double* __restrict__ x, long long R, long long K, long long O,
+                                        int* __restrict__ fexp) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // c = r + R o
+  if (c >= R * O) return;
+  const long long r = c % R, o = c / R;
+  const double* col = x + r + R * K * o;
+  int e = INT_MIN;
+  for (long long k = 0; k < K; ++k) e = max(e, exp_bound(col[R * k]));
+  fexp[c] = e;
+}
+
+template <int N, bool kInner>
+cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, const I8Geom& geo, int mu,
+                     double* y, cudaStream_t st) {
   static unsigned long long done = 0;
   const size_t smem = kI8Stages * (size_t)kI8XBytes + kI8QStages * (size_t)kI8Digits * N * kI8Kstep +
                       kI8StageBytes + 512 + 1024 + 8 * N;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_i8_kernel<N>), smem, done);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(ttm_i8_kernel<N, kInner>), smem, done);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long ntiles = (J + kI8Tile - 1) / kI8Tile;
+  const long long ntiles = kInner ? (geo.O + 1) / 2 : (geo.J + kI8Tile - 1) / kI8Tile;
   const int grid = (int)(ntiles < sms ? ntiles : sms);
-  ttm_i8_kernel<N><<<grid, kI8Threads, smem, st>>>(map, qd, eq, w, J, K, mu, y); note_launch();
+  ttm_i8_kernel<N, kInner><<<grid, kI8Threads, smem, st>>>(map, qd, eq, geo, mu, y); note_launch();
   return cudaGetLastError();
+}
+
+// Q digits + eq into the workspace (one small kernel), returns the digit / eq pointers
+cudaError_t prepare_q(const double* q, long long K, int mu, void* work, uint8_t** qd, int** eq,
+                      cudaStream_t st) {
+  const int N = ((mu + 15) / 16) * 16;
+  const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
+  *qd = static_cast<uint8_t*>(work);
+  *eq = reinterpret_cast<int*>(*qd + ((size_t)nks * kI8Digits * N * kI8Kstep + 255) / 256 * 256);
+  q_digits_kernel<<<N, 256, 0, st>>>(q, (int)K, mu, N, *qd, *eq); note_launch();
+  return cudaGetLastError();
+}
+
+template <bool kInner>
+cudaError_t dispatch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, const I8Geom& geo, int mu,
+                       double* y, cudaStream_t st) {
+  switch (((mu + 15) / 16) * 16) {
+    case 16: return launch_n<16, kInner>(map, qd, eq, geo, mu, y, st);
+    case 32: return launch_n<32, kInner>(map, qd, eq, geo, mu, y, st);
+    case 48: return launch_n<48, kInner>(map, qd, eq, geo, mu, y, st);
+    default: return launch_n<64, kInner>(map, qd, eq, geo, mu, y, st);
+  }
 }
 
 }  // namespace
@@ -489,6 +640,12 @@ bool ttm_i8_supported(long long K, long long J, int mu, const double* x) {
          mu <= kI8MaxN && J >= 1 && J < (1ll << 31) && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 }
 
+bool ttm_i8_inner_supported(long long R, long long K, long long O, int mu, const double* x) {
+  return i8_tensor_map_encoder() != nullptr && R >= 2 && R <= 64 && R % 2 == 0 && K >= 1 &&
+         K <= 4096 && O >= 1 && O < (1ll << 31) && mu >= 1 && mu <= kI8MaxN &&
+         (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+}
+
 size_t ttm_i8_workspace_bytes(long long K, int mu) {
   const int N = ((mu + 15) / 16) * 16;
   const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
@@ -496,14 +653,12 @@ size_t ttm_i8_workspace_bytes(long long K, int mu) {
 }
 
 cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const double* q, int mu,
-                          const double* w, double* y, void* work, cudaStream_t st) {
-  if (!ttm_i8_supported(K, J, mu, x)) return cudaErrorInvalidValue;
-  const int N = ((mu + 15) / 16) * 16;
-  const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
-  uint8_t* qd = static_cast<uint8_t*>(work);
-  int* eq = reinterpret_cast<int*>(qd + ((size_t)nks * kI8Digits * N * kI8Kstep + 255) / 256 * 256);
-  q_digits_kernel<<<N, 256, 0, st>>>(q, (int)K, mu, N, qd, eq); note_launch();
-  cudaError_t e = cudaGetLastError();
+                          const double* w, double* y, void* work, cudaStream_t st, int* fexp_out,
+                          long long I1) {
+  if (!ttm_i8_supported(K, J, mu, x) || (fexp_out && I1 < 1)) return cudaErrorInvalidValue;
+  uint8_t* qd;
+  int* eq;
+  cudaError_t e = prepare_q(q, K, mu, work, &qd, &eq, st);
   if (e != cudaSuccess) return e;
   CUtensorMap map;
   const cuuint64_t gdim[2] = {(cuuint64_t)K, (cuuint64_t)J};
@@ -513,12 +668,35 @@ cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const doubl
                               box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  switch (N) {
-    case 16: return launch_n<16>(map, qd, eq, w, J, (int)K, mu, y, st);
-    case 32: return launch_n<32>(map, qd, eq, w, J, (int)K, mu, y, st);
-    case 48: return launch_n<48>(map, qd, eq, w, J, (int)K, mu, y, st);
-    default: return launch_n<64>(map, qd, eq, w, J, (int)K, mu, y, st);
-  }
+  I8Geom geo{J, (int)K, 0, 0, w, nullptr, fexp_out, I1};
+  return dispatch_n<false>(map, qd, eq, geo, mu, y, st);
+}
+
+cudaError_t launch_column_exponents(const double* x, long long R, long long K, long long O, int* fexp,
+                                    cudaStream_t st) {
+  if (R < 1 || K < 1 || O < 1) return cudaErrorInvalidValue;
+  const long long n = R * O;
+  column_exponents_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, R, K, O, fexp); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ttm_i8_inner(const double* x, long long R, long long K, long long O, const double* q,
+                                int mu, const int* fexp_in, double* y, void* work, cudaStream_t st) {
+  if (!ttm_i8_inner_supported(R, K, O, mu, x)) return cudaErrorInvalidValue;
+  uint8_t* qd;
+  int* eq;
+  cudaError_t e = prepare_q(q, K, mu, work, &qd, &eq, st);
+  if (e != cudaSuccess) return e;
+  CUtensorMap map;  // (r, k, o), box 64 x 32 x 2, rows r >= R zero-filled, no swizzle
+  const cuuint64_t gdim[3] = {(cuuint64_t)R, (cuuint64_t)K, (cuuint64_t)O};
+  const cuuint64_t gstride[2] = {(cuuint64_t)R * 8, (cuuint64_t)(R * K) * 8};
+  const cuuint32_t box[3] = {64, (cuuint32_t)kI8Kstep, 2}, estride[3] = {1, 1, 1};
+  if (i8_tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), gdim, gstride,
+                              box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  I8Geom geo{0, (int)K, (int)R, O, nullptr, fexp_in, nullptr, 0};
+  return dispatch_n<true>(map, qd, eq, geo, mu, y, st);
 }
 
 }  // namespace lmra_dev

@@ -495,19 +495,58 @@ class Engine {
   // Mode-0 contraction of a tensor whose canonical mode-0 column norms w are known: on the
   // int8 tensor cores (ttm_i8.cu, ~1e-13 relative) when the shape allows, else the DMMA TTM.
   // LMRA_TTM_I8=0 forces the DMMA path.
+  // Per-column exponents handed from one int8 contraction to the next: after a mode-0
+  // contraction that wrote them, fexp holds the max exponent of every mode-1 fibre of its
+  // output, which a following mode-1 contraction uses as its fixed-point scales.
+  struct I8Chain {
+    DevBuf fexp;
+    bool ready = false;
+  };
+
+  // Y = X x_mode Q^T.  On the int8 tensor cores when the scales are known: mode 0 with the
+  // canonical column norms w, or mode 1 right after such a contraction (chain); the fp64 DMMA
+  // product otherwise.  next_mode1: the following contraction is mode 1 of the result.
   DevBuf ttm_mode0(const double* x, const std::vector<size_t>& dims, size_t mode, const double* q,
-                   size_t m, const double* w, const std::string& phase) {
+                   size_t m, const double* w, const std::string& phase, I8Chain* chain = nullptr,
+                   bool next_mode1 = false) {
     static const bool enabled = !(getenv("LMRA_TTM_I8") && std::string(getenv("LMRA_TTM_I8")) == "0");
-    const size_t K = dims[0], J = prod(dims) / K;
+    const size_t total = prod(dims);
+    std::vector<size_t> od = dims;
+    od[mode] = m;
+    if (enabled && mode == 1 && chain && chain->ready && dims.size() >= 2) {
+      chain->ready = false;
+      const size_t R = dims[0], K = dims[1], O = total / (R * K);
+      if (lmra_dev::ttm_i8_inner_supported((long long)R, (long long)K, (long long)O, (int)m, x)) {
+        DevBuf y(prod(od), st_);
+        DevBuf work((lmra_dev::ttm_i8_workspace_bytes((long long)K, (int)m) + 7) / 8, st_);
+        const int* fe = reinterpret_cast<const int*>(chain->fexp.get());
+        launch(phase + "_i8", [&] {
+          return lmra_dev::launch_ttm_i8_inner(x, (long long)R, (long long)K, (long long)O, q, (int)m, fe,
+                                               y.get(), work.get(), st_);
+        });
+        return y;
+      }
+    }
+    if (chain) chain->ready = false;
+    const size_t K = dims[0], J = total / K;
     if (mode != 0 || !w || !enabled || !lmra_dev::ttm_i8_supported((long long)K, (long long)J, (int)m, x))
       return ttm(x, dims, mode, q, m, phase);
-    std::vector<size_t> od = dims;
-    od[0] = m;
     DevBuf y(prod(od), st_);
     DevBuf work((lmra_dev::ttm_i8_workspace_bytes((long long)K, (int)m) + 7) / 8, st_);
+    int* fexp = nullptr;
+    long long I1 = 0;
+    if (chain && next_mode1 && dims.size() >= 2 && dims[1] > 0) {
+      I1 = (long long)dims[1];
+      const size_t n = m * (J / dims[1]);
+      chain->fexp = DevBuf((n + 1) / 2, st_);
+      fexp = reinterpret_cast<int*>(chain->fexp.get());
+      ck(cudaMemsetAsync(fexp, 0x80, n * sizeof(int), st_), "memset");  // INT_MIN-like
+    }
     launch(phase + "_i8", [&] {
-      return lmra_dev::launch_ttm_i8(x, (long long)K, (long long)J, q, (int)m, w, y.get(), work.get(), st_);
+      return lmra_dev::launch_ttm_i8(x, (long long)K, (long long)J, q, (int)m, w, y.get(), work.get(), st_,
+                                     fexp, I1);
     });
+    if (fexp) chain->ready = true;
     return y;
   }
 
@@ -810,9 +849,12 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     int step = 0;
     // the first contraction reads the input, whose mode-0 norms the sampler already has
     const double* w0 = (amm && cfg.regime != kUniform && d_w[0].get()) ? d_w[0].get() : nullptr;
-    for (size_t n : idx) {
+    Engine::I8Chain chain;
+    for (size_t k = 0; k < idx.size(); ++k) {
+      const size_t n = idx[k];
+      const bool next1 = k + 1 < idx.size() && idx[k + 1] == 1;
       DevBuf y = eng.ttm_mode0(src, cur, n, factors[n].get(), res->f_cols[n], src == in.x ? w0 : nullptr,
-                               "core_ttm" + std::to_string(step++));
+                               "core_ttm" + std::to_string(step++), &chain, next1);
       cur[n] = res->f_cols[n];
       t = std::move(y);
       src = t.get();
@@ -823,7 +865,10 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     std::vector<size_t> cur = in.dims;
     DevBuf work;
     const double* src = in.x;
-    for (size_t n : r.order) {
+    Engine::I8Chain chain;
+    for (size_t oi = 0; oi < r.order.size(); ++oi) {
+      const size_t n = r.order[oi];
+      const bool next1 = oi + 1 < r.order.size() && r.order[oi + 1] == 1;
       size_t t_n = 0;
       if (amm) {
         const size_t cols = prod(cur) / cur[n];
@@ -837,7 +882,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
           (amm && cfg.regime != kUniform && src == in.x && d_w[n].get() && !(in.ov && in.ov->sample_idx))
               ? d_w[n].get() : nullptr;
       DevBuf y = eng.ttm_mode0(src, cur, n, factors[n].get(), res->f_cols[n], w0,
-                               "shrink_ttm_m" + std::to_string(n));
+                               "shrink_ttm_m" + std::to_string(n), &chain, next1);
       cur[n] = res->f_cols[n];
       work = std::move(y);
       src = work.get();
@@ -1596,6 +1641,27 @@ int lmra_mode0_product_i8(lmra_context* ctx, const double* x, uint64_t K, uint64
     Engine eng(ctx);
     eng.launch("ttm_i8", [&] {
       return lmra_dev::launch_ttm_i8(x, (long long)K, (long long)J, q, mu, w, y, work.get(), ctx->stream);
+    });
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_mode1_product_i8(lmra_context* ctx, const double* x, uint64_t R, uint64_t K, uint64_t O,
+                          const double* q, int mu, double* y) {
+  return guard([&] {
+    if (!lmra_dev::ttm_i8_inner_supported((long long)R, (long long)K, (long long)O, mu, x))
+      throw std::invalid_argument("mode1_product_i8: shape not supported (R even <= 64, K <= 4096, mu <= 64)");
+    DeviceGuard dg(ctx->device);
+    DevBuf work((lmra_dev::ttm_i8_workspace_bytes((long long)K, mu) + 7) / 8, ctx->stream);
+    DevBuf fexp((R * O + 1) / 2, ctx->stream);
+    int* fe = reinterpret_cast<int*>(fexp.get());
+    Engine eng(ctx);
+    eng.launch("column_exponents", [&] {
+      return lmra_dev::launch_column_exponents(x, (long long)R, (long long)K, (long long)O, fe, ctx->stream);
+    });
+    eng.launch("ttm_i8", [&] {
+      return lmra_dev::launch_ttm_i8_inner(x, (long long)R, (long long)K, (long long)O, q, mu, fe, y, work.get(),
+                                           ctx->stream);
     });
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });

@@ -62,6 +62,16 @@ def mode0_product_i8(x, K: int, J: int, q, mu: int, w, ctx: Context = None):
     return y
 
 
+def mode1_product_i8(x, R: int, K: int, O: int, q, mu: int, ctx: Context = None):
+    """y (R x mu x O, R fastest) = x x_1 q^T on the int8 tensor cores (lmra_mode1_product_i8);
+    x: R x K x O (R fastest), q: K x mu column-major."""
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    y = empty(R * mu * O, ctx.device)
+    check(lib.lmra_mode1_product_i8(ctx.handle, _ptr(x), R, K, O, _ptr(q), mu, _ptr(y)))
+    return y
+
+
 def gram_power_apply(a_colmajor, rows: int, cols: int, g_colmajor, s: int, q: int,
                      strategy: str = "A", ctx: Context = None):
     ctx = ctx or default_context()

@@ -23,7 +23,8 @@ __global__ void colnorm(const double* x, int K, long long J, double* w) {
   w[j] = s;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const bool with_fexp = argc > 1 && argv[1][0] == 'f';  // also hand exponents to a mode-1 pass
   const int K = 1000, mu = 50;
   const long long J = 1000000;
   double *x, *q, *w, *y;
@@ -33,6 +34,8 @@ int main() {
   cudaMalloc(&w, (size_t)J * 8);
   cudaMalloc(&y, (size_t)mu * J * 8);
   cudaMalloc(&work, ttm_i8_workspace_bytes(K, mu));
+  int* fexp = nullptr;
+  cudaMalloc(&fexp, (size_t)mu * 1000 * sizeof(int));
   fill<<<4096, 256>>>(x, (size_t)K * J, 1);
   fill<<<64, 256>>>(q, (size_t)K * mu, 2);
   colnorm<<<(J + 255) / 256, 256>>>(x, K, J, w);
@@ -42,8 +45,9 @@ int main() {
   for (int rep = 0; rep < 3; ++rep) {
     unsigned long long z[20] = {0};
     cudaMemcpyToSymbol(g_i8clk, z, sizeof(z));
+    if (with_fexp) cudaMemset(fexp, 0x80, (size_t)mu * 1000 * sizeof(int));
     cudaEventRecord(e0);
-    cudaError_t e = launch_ttm_i8(x, K, J, q, mu, w, y, work, 0);
+    cudaError_t e = launch_ttm_i8(x, K, J, q, mu, w, y, work, 0, with_fexp ? fexp : nullptr, 1000);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     float ms = 0;
