@@ -13,6 +13,33 @@
 
 namespace lmra_dev {
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may be scheduled while the
+// previous kernel in its stream drains (its launch latency overlaps that tail); it must call
+// pdl_wait() before touching anything the previous kernel wrote (griddepcontrol.wait returns
+// once the prerequisite grid has completed and its writes are visible; it is a no-op for a
+// normal launch).  pdl_trigger() lets the dependent grid launch once every CTA of this one
+// has started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+
 __device__ __forceinline__ long long col_base(long long j, long long inner, long long I) {
   if (inner == 1) return j * I;
   long long o = j / inner;

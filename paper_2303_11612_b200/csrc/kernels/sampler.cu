@@ -304,6 +304,8 @@ __device__ __forceinline__ void load_items(const double* __restrict__ x, long lo
 // ---------------------------------------------------------------- pass A: chunk sums
 __global__ void __launch_bounds__(kThr) chunk_sums_kernel(const double* __restrict__ x, long long n,
                                                           double* __restrict__ csum) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double sm[32];
   double xv[kItems];
   load_items(x, n, (long long)blockIdx.x * kChunk + threadIdx.x * kItems, xv);
@@ -321,6 +323,8 @@ __global__ void __launch_bounds__(1024) chunk_plan_kernel(const double* __restri
                                                           int nchunks, long long n,
                                                           int* __restrict__ assumed,
                                                           int* __restrict__ assumed2) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double smd[32];
   const double delta = 4.0 * ((double)n + 64.0) * 0x1.0p-53 + 1e-15;
   double carry = 0.0;
@@ -381,6 +385,8 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
                                                          const int* __restrict__ assumed2,
                                                          ChunkAgg* __restrict__ agg,
                                                          ChunkAgg* __restrict__ subagg) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double smd[32];
   __shared__ int smi[32];
   const int k = blockIdx.x;
@@ -766,6 +772,8 @@ __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restr
                                                            double* __restrict__ out,
                                                            double* __restrict__ total,
                                                            int* __restrict__ status, int bad_flag) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ ChunkAgg tile[kTile];
   __shared__ Tx stx[kTileWarps];
   __shared__ double smd[32];
@@ -892,6 +900,8 @@ __global__ void __launch_bounds__(kThr) chunk_write_kernel(const double* __restr
                                                            const ChunkStart* __restrict__ starts,
                                                            const ChunkStart* __restrict__ substarts,
                                                            double* __restrict__ out) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double smd[32];
   __shared__ int smi[32];
   const int k = blockIdx.x;
@@ -936,6 +946,8 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 __global__ void __launch_bounds__(kThr) neumaier_terms_kernel(const double* __restrict__ x,
                                                               const double* __restrict__ S, long long n,
                                                               double* __restrict__ part) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double hi_s[kThr], lo_s[kThr], ab_s[kThr];
   const long long base = (long long)blockIdx.x * kChunk + threadIdx.x * kItems;
   double hi = 0.0, lo = 0.0, ab = 0.0;
@@ -1025,6 +1037,8 @@ __global__ void __launch_bounds__(kRedThr) neumaier_final_kernel(
     const double* __restrict__ x, long long n, const double* __restrict__ Sfinal,
     const double* __restrict__ part, int nchunks, double* __restrict__ s_out,
     int* __restrict__ status, const int* __restrict__ skip) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   if (skip && *skip) return;
   double hi, lo, ab;
   dd_block_sum(part, 3, nchunks, hi, lo, ab);
@@ -1052,6 +1066,8 @@ __global__ void normalize_mix_kernel(const double* __restrict__ w, long long n,
                                      const double* __restrict__ total, int regime, double beta,
                                      double* __restrict__ x1, int* __restrict__ uni,
                                      int* __restrict__ status) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   const double tot = *total;
   const bool uniform = !(tot > 0.0);
   if (!uniform && regime == 1 && !(beta > 0.0 && beta <= 1.0)) {
@@ -1074,6 +1090,8 @@ __global__ void normalize_mix_kernel(const double* __restrict__ w, long long n,
 // p = x / s (sketching.cpp:46); uniform path keeps x (= 1/n); flags s <= 0
 __global__ void divide_kernel(double* __restrict__ x, long long n, const double* __restrict__ s,
                               const int* __restrict__ uni, int* __restrict__ status) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   if (*uni) return;
   const double sv = *s;
   if (!(sv > 0.0)) {
@@ -1086,6 +1104,8 @@ __global__ void divide_kernel(double* __restrict__ x, long long n, const double*
 }
 
 __global__ void fill_kernel(double* __restrict__ x, long long n, double v) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     x[i] = v;
@@ -1097,6 +1117,8 @@ __global__ void fill_kernel(double* __restrict__ x, long long n, double v) {
 __global__ void __launch_bounds__(kThr) check_last_kernel(const double* __restrict__ p, long long n,
                                                           double* __restrict__ part,
                                                           long long* __restrict__ lastpos) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double hi_s[kThr], lo_s[kThr];
   __shared__ long long sml[32];
   double hi = 0.0, lo = 0.0;
@@ -1135,6 +1157,8 @@ __global__ void __launch_bounds__(kRedThr) check_final_kernel(const double* __re
                                                                const long long* __restrict__ lastpos,
                                                                int nchunks, long long* __restrict__ last,
                                                                int* __restrict__ status) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ long long sml[32];
   long long lp = -1;
   for (int k = threadIdx.x; k < nchunks; k += kRedThr) lp = max(lp, lastpos[k]);
@@ -1188,6 +1212,8 @@ __global__ void draw_kernel(const double* __restrict__ cum, const double* __rest
                             long long L, unsigned long long seed, unsigned long long stream,
                             long long* __restrict__ idx, double* __restrict__ scales,
                             int* __restrict__ status) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   const double acc = *acc_p;
   const long long j0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kDrawsPerThread;
   if (j0 >= L) return;
@@ -1242,14 +1268,14 @@ struct ScanBufs {
 static cudaError_t exact_scan(const double* x, long long n, double* out, double* total,
                               int* status, int bad_flag, const ScanBufs& b, cudaStream_t st) {
   const int nc = nchunks_of(n);
-  chunk_sums_kernel<<<nc, kThr, 0, st>>>(x, n, b.csum); note_launch();
-  chunk_plan_kernel<<<1, 1024, 0, st>>>(b.csum, nc, n, b.assumed, b.assumed2); note_launch();
-  chunk_agg_kernel<<<nc, kThr, 0, st>>>(x, n, b.assumed, b.assumed2, b.agg, b.subagg); note_launch();
-  chunk_walk_kernel<<<1, kCThr, 0, st>>>(x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
-                                         total, status, bad_flag); note_launch();
+  cudaError_t e;
+  if ((e = launch_pdl(chunk_sums_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.csum)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), 0, st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
+                                         total, status, bad_flag)) != cudaSuccess) return e;
   if (out) {
-    chunk_write_kernel<<<nc, kThr, 0, st>>>(x, n, b.starts, b.substarts, out);
-    note_launch();
+    if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, out)) != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -1279,23 +1305,23 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   const int eg = 148 * 8;
   cudaError_t e;
   if (regime == 2) {  // uniform(n): p = 1/n each (sketching.cpp:50-53)
-    fill_kernel<<<eg, 256, 0, st>>>(p, n, 1.0 / (double)n); note_launch();
+    if ((e = launch_pdl(fill_kernel, dim3(eg), dim3(256), 0, st, p, n, 1.0 / (double)n)) != cudaSuccess) return e;
   } else {
     // total = naive sum of w; x1 = w / total (+ beta mix); s = Neumaier(x1); p = x1 / s
     if ((e = exact_scan(w, n, nullptr, scal + 0, status, kBadWeight, b, st)) != cudaSuccess) return e;
-    normalize_mix_kernel<<<eg, 256, 0, st>>>(w, n, scal + 0, regime, beta, p, uni, status); note_launch();
+    if ((e = launch_pdl(normalize_mix_kernel, dim3(eg), dim3(256), 0, st, w, n, scal + 0, regime, beta, p, uni, status)) != cudaSuccess) return e;
     if ((e = exact_scan(p, n, S, scal + 1, status, kBadWeight, b, st)) != cudaSuccess) return e;
-    neumaier_terms_kernel<<<nc, kThr, 0, st>>>(p, S, n, npart); note_launch();
-    neumaier_final_kernel<<<1, kRedThr, 0, st>>>(p, n, scal + 1, npart, nc, scal + 1, status, uni); note_launch();
-    divide_kernel<<<eg, 256, 0, st>>>(p, n, scal + 1, uni, status); note_launch();
+    if ((e = launch_pdl(neumaier_terms_kernel, dim3(nc), dim3(kThr), 0, st, p, S, n, npart)) != cudaSuccess) return e;
+    if ((e = launch_pdl(neumaier_final_kernel, dim3(1), dim3(kRedThr), 0, st, p, n, scal + 1, npart, nc, scal + 1, status, uni)) != cudaSuccess) return e;
+    if ((e = launch_pdl(divide_kernel, dim3(eg), dim3(256), 0, st, p, n, scal + 1, uni, status)) != cudaSuccess) return e;
   }
-  check_last_kernel<<<nc, kThr, 0, st>>>(p, n, cpart, lastpos); note_launch();
-  check_final_kernel<<<1, kRedThr, 0, st>>>(cpart, lastpos, nc, last, status); note_launch();
+  if ((e = launch_pdl(check_last_kernel, dim3(nc), dim3(kThr), 0, st, p, n, cpart, lastpos)) != cudaSuccess) return e;
+  if ((e = launch_pdl(check_final_kernel, dim3(1), dim3(kRedThr), 0, st, cpart, lastpos, nc, last, status)) != cudaSuccess) return e;
   // cum = naive prefix of p; acc = cum[n-1]
   if ((e = exact_scan(p, n, S, scal + 2, status, kBadWeight, b, st)) != cudaSuccess) return e;
   const long long threads = (L + kDrawsPerThread - 1) / kDrawsPerThread;
-  draw_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(S, p, n, scal + 2, last, L, seed,
-                                                                  stream, idx, scales, status); note_launch();
+  if ((e = launch_pdl(draw_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, st, S, p, n, scal + 2, last, L, seed,
+                                                                  stream, idx, scales, status)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
