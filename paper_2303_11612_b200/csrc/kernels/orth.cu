@@ -665,6 +665,8 @@ template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
     const double* __restrict__ A, long long m, int s, int lda, int nb, double* __restrict__ V,
     double* __restrict__ tau, double* __restrict__ S, int lds) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
   double* tile = sm + kQScratchBytes / 8;
@@ -697,6 +699,8 @@ template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
     int ldo, int final_level, int* status, double jacobi_tol) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
   const int n = 64;  // Jacobi column slots (zero columns beyond s)
@@ -810,6 +814,8 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
     const double* __restrict__ V, long long m, int s, int ldv, int nb,
     const double* __restrict__ tau, const double* __restrict__ W, int ldw, int mu,
     double* __restrict__ out, int ldo, double* __restrict__ pbest, int* __restrict__ pidx) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
   double* tile = sm + kQScratchBytes / 8;
@@ -852,6 +858,8 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
 __global__ void orth_signfix_kernel(double* __restrict__ U, long long m, int ldu, int mu, int nb,
                                     const double* __restrict__ pbest,
                                     const int* __restrict__ pidx) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   const int c = blockIdx.x;
   __shared__ int flip;
   if (threadIdx.x == 0) {
@@ -945,7 +953,10 @@ cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, doub
   const size_t smem = leaf_smem(rows, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_qr_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_leaf_qr_kernel<RPL><<<nb, kQThreads, smem, st>>>(A, m, s, (int)m, nb, V, tau, S, lds); note_launch();
+  {
+    const cudaError_t le = launch_pdl(orth_leaf_qr_kernel<RPL>, dim3(nb), dim3(kQThreads), smem, st, A, m, s, (int)m, nb, V, tau, S, lds);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
@@ -956,7 +967,10 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
   const size_t smem = core_smem(m, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_core_kernel<RPL><<<1, kQThreads, smem, st>>>(S, m, s, m, mu, out, ldo, final_level, status, tol); note_launch();
+  {
+    const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu, out, ldo, final_level, status, tol);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
@@ -969,8 +983,11 @@ cudaError_t leaf_apply(const double* V, long long m, int s, int nb, const double
   const size_t smem = leaf_smem(rows, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_apply_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  orth_leaf_apply_kernel<RPL><<<nb, kQThreads, smem, st>>>(V, m, s, (int)m, nb, tau, W, ldw, mu,
-                                                          out, (int)m, pbest, pidx); note_launch();
+  {
+    const cudaError_t le = launch_pdl(orth_leaf_apply_kernel<RPL>, dim3(nb), dim3(kQThreads), smem, st, V, m, s, (int)m, nb, tau, W, ldw, mu,
+                                                          out, (int)m, pbest, pidx);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
@@ -1023,7 +1040,10 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
                                            l == 0 ? pbest : nullptr, l == 0 ? pidx : nullptr, st);
     if (e != cudaSuccess) return e;
   }
-  orth_signfix_kernel<<<mu, 256, 0, st>>>(u, I, (int)I, mu, lv[0].nb, pbest, pidx); note_launch();
+  {
+    const cudaError_t le = launch_pdl(orth_signfix_kernel, dim3(mu), dim3(256), 0, st, u, I, (int)I, mu, lv[0].nb, pbest, pidx);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 

@@ -39,6 +39,8 @@ template <int M8, bool RCONTIG, int KC_, int ST_>
 __global__ void __launch_bounds__(kThreads, 2)
     ttm_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ bt, int m,
                int mtot, int koff, double* __restrict__ y, long long kper) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   using C = TtmCfg<M8, RCONTIG, KC_, ST_>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -203,6 +205,8 @@ template <int M8, bool RCONTIG>
 __global__ void __launch_bounds__(kGramThreads)
     gram_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ h, int s,
                 int stot, int koff, double* __restrict__ zpart, long long jper) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   using C = GramCfg<M8, RCONTIG>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -310,6 +314,8 @@ __global__ void __launch_bounds__(kGramThreads)
 // z[e] = sum_{p < nsplit} zpart[p][e], fixed order (deterministic).
 __global__ void reduce_splits_kernel(const double* __restrict__ zpart, int nsplit, long long n,
                                      double* __restrict__ z) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   double acc = zpart[e];
@@ -323,6 +329,8 @@ __global__ void gather_contig_kernel(const double* __restrict__ x, long long I,
                                      const long long* __restrict__ idx,
                                      const double* __restrict__ scale, long long T,
                                      double* __restrict__ out) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   long long tcol = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (tcol >= T) return;
   const int lane = threadIdx.x & 31;
@@ -341,6 +349,8 @@ __global__ void gather_strided_kernel(const double* __restrict__ x, ModeView v,
                                       const long long* __restrict__ idx,
                                       const double* __restrict__ scale, long long T,
                                       double* __restrict__ out) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   __shared__ double tile[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const long long t0 = (long long)blockIdx.x * 32;
@@ -376,6 +386,8 @@ __global__ void gather_strided_kernel(const double* __restrict__ x, ModeView v,
 // bk[r * M8 + k] = bt[r + I * k] for k < m, 0 for m <= k < M8 (row-major, zero padded)
 __global__ void pack_b_kernel(const double* __restrict__ bt, long long I, int m, int M8,
                               double* __restrict__ bk) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= I * M8) return;
   const long long r = e / M8;
@@ -390,7 +402,10 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
   double* bt = nullptr;  // packed copy, stream-ordered scratch
   cudaError_t pe = scratch_alloc(reinterpret_cast<void**>(&bt), sizeof(double) * v.I * M8, st);
   if (pe != cudaSuccess) return pe;
-  pack_b_kernel<<<(unsigned)((v.I * M8 + 255) / 256), 256, 0, st>>>(bt_colmajor, v.I, m, M8, bt); note_launch();
+  {
+    const cudaError_t le = launch_pdl(pack_b_kernel, dim3((unsigned)((v.I * M8 + 255) / 256)), dim3(256), 0, st, bt_colmajor, v.I, m, M8, bt);
+    if (le != cudaSuccess) return le;
+  }
   struct FreeGuard {
     double* p;
     cudaStream_t s;
@@ -407,7 +422,10 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
     if (e != cudaSuccess) return e;
     long long J = v.inner * v.outer;
     dim3 grid((unsigned)((J + C::JT - 1) / C::JT), (unsigned)ksplit);
-    ttm_kernel<M8, RC, KC, ST><<<grid, kThreads, C::SMEM, st>>>(x, v, bt, m, mtot, koff, y, kper); note_launch();
+    {
+    const cudaError_t le = launch_pdl(ttm_kernel<M8, RC, KC, ST>, dim3(grid), dim3(kThreads), C::SMEM, st, x, v, bt, m, mtot, koff, y, kper);
+    if (le != cudaSuccess) return le;
+  }
     return cudaGetLastError();
   };
   return go(std::integral_constant<int, 16>{}, std::integral_constant<int, 3>{});
@@ -484,7 +502,10 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
   if (ks > 1) {
     if (e == cudaSuccess) {
       const long long n = J * m;
-      reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ks, n, y); note_launch();
+      {
+    const cudaError_t le = launch_pdl(reduce_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, part, ks, n, y);
+    if (le != cudaSuccess) return le;
+  }
       e = cudaGetLastError();
     }
     scratch_free(part, st);
@@ -502,7 +523,10 @@ static cudaError_t launch_gram_t(const double* x, ModeView v, const double* h, i
                                    attr_done);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((v.I + C::RT - 1) / C::RT), (unsigned)nsplit);
-  gram_kernel<M8, RC><<<grid, kGramThreads, C::SMEM, st>>>(x, v, h, s, stot, koff, zpart, jper); note_launch();
+  {
+    const cudaError_t le = launch_pdl(gram_kernel<M8, RC>, dim3(grid), dim3(kGramThreads), C::SMEM, st, x, v, h, s, stot, koff, zpart, jper);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
@@ -552,7 +576,10 @@ cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, dou
     if (e != cudaSuccess) return e;
   }
   long long n = v.I * s;
-  reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(zpart, plan.nsplit, n, z); note_launch();
+  {
+    const cudaError_t le = launch_pdl(reduce_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, zpart, plan.nsplit, n, z);
+    if (le != cudaSuccess) return le;
+  }
   return cudaGetLastError();
 }
 
@@ -560,13 +587,19 @@ cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, con
                           long long T, double* out, cudaStream_t st) {
   if (T == 0) return cudaSuccess;
   if (v.inner == 1) {
-    gather_contig_kernel<<<(unsigned)((T + 7) / 8), 256, 0, st>>>(x, v.I, idx, scale, T, out); note_launch();
+    {
+    const cudaError_t le = launch_pdl(gather_contig_kernel, dim3((unsigned)((T + 7) / 8)), dim3(256), 0, st, x, v.I, idx, scale, T, out);
+    if (le != cudaSuccess) return le;
+  }
   } else {
     // rows split over grid.y: each sampled fiber is strided (one sector per element), so the
     // gather is latency-bound and wants every SM issuing
     const long long tb = (T + 31) / 32, rb = (v.I + 31) / 32;
     const long long ry = std::max<long long>(1, std::min<long long>(rb, (4LL * device_sms() + tb - 1) / tb));
-    gather_strided_kernel<<<dim3((unsigned)tb, (unsigned)ry), 256, 0, st>>>(x, v, idx, scale, T, out); note_launch();
+    {
+    const cudaError_t le = launch_pdl(gather_strided_kernel, dim3(dim3((unsigned)tb, (unsigned)ry)), dim3(256), 0, st, x, v, idx, scale, T, out);
+    if (le != cudaSuccess) return le;
+  }
   }
   return cudaGetLastError();
 }
