@@ -103,6 +103,13 @@ class Pool {
     }
     cv_.notify_one();
   }
+  void push_batch(std::vector<std::function<void()>>& fs) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (auto& f : fs) q_.push_back(std::move(f));
+    }
+    cv_.notify_all();
+  }
 
  private:
   void loop() {
@@ -153,6 +160,24 @@ void TaskGroup::run(std::function<void()> f) {
   });
 }
 
+void TaskGroup::run_batch(std::vector<std::function<void()>> fs) {
+  if (fs.empty()) return;
+  {
+    std::lock_guard<std::mutex> lk(st_->mu);
+    st_->pending += (long)fs.size();
+  }
+  std::shared_ptr<State> st = st_;
+  std::vector<std::function<void()>> wrapped;
+  wrapped.reserve(fs.size());
+  for (auto& f : fs)
+    wrapped.emplace_back([st, f = std::move(f)] {
+      f();
+      std::lock_guard<std::mutex> lk(st->mu);
+      if (--st->pending == 0) st->cv.notify_all();
+    });
+  pool().push_batch(wrapped);
+}
+
 void TaskGroup::wait() {
   std::unique_lock<std::mutex> lk(st_->mu);
   st_->cv.wait(lk, [this] { return st_->pending == 0; });
@@ -166,10 +191,12 @@ void fill_normals(uint64_t seed, uint64_t stream, double* out, size_t n, int thr
   // chunks on the persistent pool (jump-ahead per chunk: bit-identical to the sequential loop)
   const size_t chunk = std::max<size_t>(4096, ((n / (4 * (size_t)threads)) + 1) & ~size_t(1));
   TaskGroup tg;
+  std::vector<std::function<void()>> tasks;
   for (size_t b = 0; b < n; b += chunk) {
     const size_t e = std::min(n, b + chunk);
-    tg.run([=] { fill_normals_range(seed, stream, out, b, e); });
+    tasks.emplace_back([=] { fill_normals_range(seed, stream, out, b, e); });
   }
+  tg.run_batch(std::move(tasks));
   tg.wait();
 }
 

@@ -44,6 +44,7 @@ class TaskGroup {
   TaskGroup(const TaskGroup&) = delete;
   TaskGroup& operator=(const TaskGroup&) = delete;
   void run(std::function<void()> f);
+  void run_batch(std::vector<std::function<void()>> fs);  // one queue lock, one wake-up
   void wait();
 
  private:

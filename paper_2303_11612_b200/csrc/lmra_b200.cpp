@@ -669,6 +669,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   lmra_host::TaskGroup omega_tasks;
   const double tr0 = now_ms();
   bool rng_done = false;
+  std::vector<std::function<void()>> omega_jobs;
   for (size_t n = 0; n < N; ++n) {
     const size_t cnt = om_off[n + 1] - om_off[n];
     double* dst = om_pin + om_off[n];
@@ -680,9 +681,10 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     const uint64_t seed = cfg.seed, stream = n + 1;
     for (size_t b0 = 0; b0 < cnt; b0 += kChunk) {
       const size_t e0 = std::min(cnt, b0 + kChunk);
-      omega_tasks.run([=] { fill_normals_range(seed, stream, dst, b0, e0); });
+      omega_jobs.emplace_back([=] { fill_normals_range(seed, stream, dst, b0, e0); });
     }
   }
+  omega_tasks.run_batch(std::move(omega_jobs));
   auto omega_ready = [&] {
     omega_tasks.wait();
     if (!rng_done) {
