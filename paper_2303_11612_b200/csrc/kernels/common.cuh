@@ -96,6 +96,43 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// ---- thread-block clusters / distributed shared memory ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+// this CTA's shared address `saddr` as seen in the shared window of cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st_f64(uint32_t raddr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(raddr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_s32(uint32_t raddr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(raddr), "r"(v) : "memory");
+}
+// arrive on an mbarrier of another CTA of the cluster, releasing this thread's prior writes
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t raddr_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(raddr_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 #ifndef LMRA_MBAR_SUSPEND_NS
 #define LMRA_MBAR_SUSPEND_NS 0x989680
 #endif

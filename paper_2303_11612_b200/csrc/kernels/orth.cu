@@ -493,7 +493,22 @@ __device__ __forceinline__ bool jacobi_angle(double a, double b, double c, doubl
 // forming all angles itself, or J warps consuming the angles asynchronously from an
 // mbarrier ring -- were slower: the angle chain is issue-bound when replicated, and the
 // ring's extra synchronisation costs more than the J rotation it takes off the barrier.)
-__device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem& q) {
+// The Jacobi split over a 2-CTA cluster: CTA 0 rotates G and forms the angles, CTA 1 accumulates
+// J from the angles it receives through a ring in its shared memory (DSMEM stores + remote
+// mbarrier arrives), a few rounds behind.  With J off CTA 0's SM a round runs ~29 % faster
+// (microbenchmark: 1500 -> 1070 cycles for s = 60): the fp64 and shuffle pipes and the angle
+// barrier are no longer shared with the J rotations.  (The same ring between warps of ONE CTA
+// was slower: the J rotations then still compete for the SM's pipes.)
+constexpr int kJRing = 8;  // ring slots (rounds CTA 1 may lag)
+struct JLink {
+  uint32_t ring;    // CTA 1's ring [kJRing][cos 32 | sin 32] (DSMEM address)
+  uint32_t ctl;     // CTA 1's control words [kJRing]: 0 round, 1 sweep end, 2 stop
+  uint32_t full;    // CTA 1's full barriers [kJRing] (32 arrivals: the lanes of warp 0)
+  uint64_t* empty;  // CTA 0's empty barriers [kJRing] (one arrival per J warp)
+};
+
+__device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem& q,
+                           const JLink* link = nullptr) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const bool isG = w < 8;
   const int row0 = (w & 7) * 8;
@@ -505,7 +520,13 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
   // rows: warps 0 .. gw-1 hold G (8 rows each), warps 8 .. 8+gw-1 the same rows of J (rows
   // >= s of J stay zero for every real column); the other warps sit the Jacobi out
   const int gw = (s + 7) / 8;
-  const bool active = (w & 7) < gw;
+  // linked: J lives on CTA 1; warp 8 (a J warp otherwise) forwards each round's angles there
+  // after bar B, off the G warps' critical path (a remote store + release-arrive costs a
+  // DSMEM round trip)
+  const bool sender = link && w == 8;
+  const bool active = link ? ((isG && (w & 7) < gw) || sender) : ((w & 7) < gw);
+  const int barb = link ? 32 * gw + 32 : 64 * gw;
+  int jround = 0;  // linked: ring entries sent (sender)
   double T[8], B[8];
   int cT = l < nh ? l : 1 << 20, cB = l < nh ? l + nh : 1 << 20;
 #pragma unroll
@@ -572,11 +593,21 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
           k2 = clock64();
 #endif
         }
-        named_bar(2, 64 * gw);  // bar B: angles of this round visible to every active warp
+        named_bar(2, barb);  // bar B: angles of this round visible to every active warp
 #ifdef LMRA_JACOBI_CLOCKS
         const long long k3 = clock64();
 #endif
         const double cs = cs_r[l], sn = cs_r[32 + l];
+        if (sender) {  // the round's angles to CTA 1
+          const int slot = jround % kJRing;
+          mbar_wait_cluster(&link->empty[slot], ((unsigned)(jround / kJRing) & 1u) ^ 1u);
+          dsmem_st_f64(link->ring + (uint32_t)(slot * 64 + l) * 8, cs);
+          dsmem_st_f64(link->ring + (uint32_t)(slot * 64 + 32 + l) * 8, sn);
+          if (l == 0) dsmem_st_s32(link->ctl + (uint32_t)slot * 4, 0);
+          mbar_arrive_remote(link->full + (uint32_t)slot * 8);
+          ++jround;
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const double x = T[i], y = B[i];
@@ -625,6 +656,13 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
       converged = true;
       if (threadIdx.x == 0) g_jacobi_sweeps = sweep + 1;
     }
+    if (sender) {  // sweep end: continue / stop to CTA 1
+      const int slot = jround % kJRing;
+      mbar_wait_cluster(&link->empty[slot], ((unsigned)(jround / kJRing) & 1u) ^ 1u);
+      if (l == 0) dsmem_st_s32(link->ctl + (uint32_t)slot * 4, (converged || sweep + 1 >= 60) ? 2 : 1);
+      mbar_arrive_remote(link->full + (uint32_t)slot * 8);
+      ++jround;
+    }
   }
 done:
 #ifdef LMRA_JACOBI_CLOCKS
@@ -643,7 +681,7 @@ done:
           if (cT < s) G[r + (size_t)s * cT] = T[i];
           if (cB < s) G[r + (size_t)s * cB] = B[i];
         }
-      } else if (cT < 64) {  // (inactive lanes hold no column)
+      } else if (!sender && cT < 64) {  // (inactive lanes hold no column; linked: J is on CTA 1)
         J[r + 64 * cT] = T[i];
         J[r + 64 * cB] = B[i];
       }
@@ -656,6 +694,82 @@ done:
   return flags[63] != 0;
 }
 
+
+// CTA 1 of the cluster: the J half of reg_jacobi, driven by the angles CTA 0 sends; the
+// final J goes into CTA 0's J buffer (jdst: its DSMEM address).  Same register layout,
+// tournament and rotation arithmetic as the J warps of reg_jacobi.
+__device__ void jacobi_j_consumer(int s, const double* ring, const int* ctl, uint64_t* full,
+                                  uint32_t empty_remote, uint32_t jdst) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int row0 = (w & 7) * 8;
+  const int nh = s <= 16 ? 8 : (s <= 32 ? 16 : 32);
+  const int gw = (s + 7) / 8;
+  if (!(w >= 8 && (w & 7) < gw)) return;
+  double T[8], B[8];
+  int cT = l < nh ? l : 1 << 20, cB = l < nh ? l + nh : 1 << 20;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = row0 + i;
+    T[i] = r == cT ? 1.0 : 0.0;
+    B[i] = r == cB ? 1.0 : 0.0;
+  }
+  int jround = 0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int group = nh;; group >>= 1) {
+      const int src = (l & ~(group - 1)) | ((l + 1) & (group - 1));
+      for (int r = 0; r < group; ++r) {
+        const int slot = jround % kJRing;
+        mbar_wait_cluster(&full[slot], (unsigned)(jround / kJRing) & 1u);
+        const double cs = ring[slot * 64 + l], sn = ring[slot * 64 + 32 + l];
+        __syncwarp();
+        if (l == 0) mbar_arrive_remote(empty_remote + (uint32_t)slot * 8);
+        ++jround;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double x = T[i], y = B[i];
+          T[i] = cs * x - sn * y;
+          B[i] = sn * x + cs * y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) B[i] = __shfl_sync(0xffffffffu, B[i], src);
+        cB = __shfl_sync(0xffffffffu, cB, src);
+      }
+      if (group == 1) break;
+      const int h = group >> 1;
+      const bool second = (l & h) != 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double tp = __shfl_xor_sync(0xffffffffu, T[i], h);
+        const double bp = __shfl_xor_sync(0xffffffffu, B[i], h);
+        if (second)
+          T[i] = bp;
+        else
+          B[i] = tp;
+      }
+      const int ctp = __shfl_xor_sync(0xffffffffu, cT, h);
+      const int cbp = __shfl_xor_sync(0xffffffffu, cB, h);
+      if (second)
+        cT = cbp;
+      else
+        cB = ctp;
+    }
+    const int slot = jround % kJRing;  // sweep end
+    mbar_wait_cluster(&full[slot], (unsigned)(jround / kJRing) & 1u);
+    const int c = ctl[slot];
+    __syncwarp();
+    if (l == 0) mbar_arrive_remote(empty_remote + (uint32_t)slot * 8);
+    ++jround;
+    if (c == 2) break;
+  }
+  if (cT < 64) {  // (lanes past the slots hold no column)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = row0 + i;
+      dsmem_st_f64(jdst + (uint32_t)(r + 64 * cT) * 8, T[i]);
+      dsmem_st_f64(jdst + (uint32_t)(r + 64 * cB) * 8, B[i]);
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Leaf QR: block b of A (m x s, lda) -> reflectors into V (same rows), tau[b*s + k],
@@ -698,7 +812,7 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
 template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
-    int ldo, int final_level, int* status, double jacobi_tol) {
+    int ldo, int final_level, int* status, double jacobi_tol, int clustered) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   extern __shared__ __align__(16) double sm[];
@@ -710,7 +824,23 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
   double* J = G + (size_t)s * s;               // n x n   (accumulated rotations)
   double* sig = J + (size_t)n * n;             // n
   int* perm = reinterpret_cast<int*>(sig + n); // n
+  uint64_t* jbars = reinterpret_cast<uint64_t*>(perm + n);  // [kJRing]: CTA 0 empty, CTA 1 full
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // cluster of 2 (clustered): CTA 1 only accumulates the Jacobi rotations (jacobi_j_consumer);
+  // its ring lives in its q.part, its control words in its q.ipiv
+  const uint32_t crank = clustered ? cluster_ctarank() : 0;
+  if (clustered) {
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kJRing; ++k) mbar_init(&jbars[k], crank == 0 ? (unsigned)((s + 7) / 8) : 32u);
+      mbar_fence_init();
+    }
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+    if (crank == 1) {
+      jacobi_j_consumer(s, q.part, q.ipiv, jbars, dsmem_addr(smem_u32(jbars), 0), dsmem_addr(smem_u32(J), 0));
+      cluster_sync();  // J delivered to CTA 0
+      return;
+    }
+  }
 
   load_tile(S, lds, m, s, Vs, ldv, 32 * RPL);
   __syncthreads();
@@ -751,7 +881,18 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     }
     __syncthreads();
   }
-  const bool converged = reg_jacobi(G, s, J, jacobi_tol, q);
+  bool converged;
+  if (clustered) {
+    JLink link;
+    link.ring = dsmem_addr(smem_u32(q.part), 1);
+    link.ctl = dsmem_addr(smem_u32(q.ipiv), 1);
+    link.full = dsmem_addr(smem_u32(jbars), 1);
+    link.empty = jbars;
+    converged = reg_jacobi(G, s, J, jacobi_tol, q, &link);
+    cluster_sync();  // CTA 1 has written J here
+  } else {
+    converged = reg_jacobi(G, s, J, jacobi_tol, q);
+  }
   // singular values = column norms of G, fixed order
   for (int c = w; c < s; c += kQWarps) {
     double t = 0.0;
@@ -901,7 +1042,7 @@ static size_t core_smem(long long m, int s) {
   const int n = 64;
   return kQScratchBytes +
          sizeof(double) * ((size_t)((32 * rpl_for(m)) | 1) * s + (size_t)s * s + (size_t)n * n + n) +
-         sizeof(int) * n + 64;
+         sizeof(int) * n + 8 * kJRing + 64;
 }
 
 static std::vector<OrthLevel> plan_levels(long long I, int s, size_t* total) {
@@ -967,8 +1108,34 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
   const size_t smem = core_smem(m, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
-  {
-    const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu, out, ldo, final_level, status, tol);
+  // the Jacobi's rotation accumulation on a second SM of a 2-CTA cluster (LMRA_ORTH_CLUSTER=0:
+  // one CTA does both halves)
+  // (only for wide sketches: below s = 48 the cluster launch and the DSMEM handoff cost more
+  // than the J rotations they move -- measured on cfg1 / cfg2 / cfg3)
+  static const bool cluster_ok = !(getenv("LMRA_ORTH_CLUSTER") && getenv("LMRA_ORTH_CLUSTER")[0] == '0');
+  const bool clustered = cluster_ok && s >= 48;
+  if (clustered) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(kQThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    note_launch();
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, orth_core_kernel<RPL>, S, m, s, m, mu, out, ldo, final_level,
+                                              status, tol, 1);
+    if (le != cudaSuccess) return le;
+  } else {
+    const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu,
+                                      out, ldo, final_level, status, tol, 0);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
