@@ -189,6 +189,23 @@ __global__ void sum_ranks_kernel(const double* const* __restrict__ in, int nrank
   }
 }
 
+// out[i] = sum_r in[r n + i] in rank order (the all-gathered form of sum_ranks)
+__global__ void sum_ranks_strided_kernel(const double* __restrict__ in, int nranks, long long n,
+                                         double* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = in[i];
+    for (int r = 1; r < nranks; ++r) s += in[(long long)r * n + i];
+    out[i] = s;
+  }
+}
+
+cudaError_t launch_sum_ranks_strided(const double* in, int nranks, long long n, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  sum_ranks_strided_kernel<<<148 * 4, 256, 0, st>>>(in, nranks, n, out); note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long n, double* out,
                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

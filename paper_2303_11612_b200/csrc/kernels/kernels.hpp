@@ -101,6 +101,8 @@ cudaError_t launch_gen_cp(double* out, const long long* dims, int order, const d
 cudaError_t launch_localize_idx(const long long* g, long long T, long long off, long long cnt,
                                 long long* l, cudaStream_t st);
 // out[i] = sum over ranks in order of in_dev[r][i] (in_dev: device array of device pointers)
+// out[i] = sum_r in[r n + i], r = 0, 1, ... (fixed order)
+cudaError_t launch_sum_ranks_strided(const double* in, int nranks, long long n, double* out, cudaStream_t st);
 cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long n, double* out,
                              cudaStream_t st);
 // at (cols x rows) = a^T

@@ -91,8 +91,16 @@ struct NcclComm : Comm {
   ~NcclComm() override {
     if (c) lmra_host::nccl().CommDestroy(c);
   }
+  // all-gather + a fixed-order (rank order) sum instead of ncclAllReduce: every rank gets
+  // the same bits, identical to ThreadComm's sum (the path the GPU tests check rank for rank)
+  // and independent of the reduction algorithm NCCL picks (ring / tree / NVLS)
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
-    ckn(lmra_host::nccl().AllReduce(buf, buf, n, ncclDouble, ncclSum, c, st), "ncclAllReduce");
+    if (n == 0) return;
+    double* tmp = nullptr;
+    ck(lmra_dev::scratch_alloc(reinterpret_cast<void**>(&tmp), n * nranks * sizeof(double), st), "alloc");
+    ckn(lmra_host::nccl().AllGather(buf, tmp, n, ncclDouble, c, st), "ncclAllGather");
+    ck(lmra_dev::launch_sum_ranks_strided(tmp, nranks, (long long)n, buf, st), "sum_ranks");
+    lmra_dev::scratch_free(tmp, st);
   }
   void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
     ckn(lmra_host::nccl().AllGather(send, recv, n, ncclDouble, c, st), "ncclAllGather");
