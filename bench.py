@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--algorithm", default=None,
+                    help="run the config's tensor and AlgoConfig through another algorithm (e.g. alg6/alg7)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -170,12 +172,16 @@ def phase_cost(bc, phase: str, dims_local=None):
         if bc.alg == "alg4" and len(dims) == 3:  # fused all-modes pass: one read, N outputs
             return 2.0 * size * 3, (size + sum(size / d for d in dims)) * 8
         return 2.0 * size, size * 8 + size / dims[0] * 8
+    qr = bc.alg in ("alg6", "alg7")  # the first core / every shrink contraction reads P (s rows)
+    sk = [min(m + cfg.oversampling, d) for m, d in zip(mu, dims)]
     if phase.startswith("core_ttm"):
         k = int(phase[len("core_ttm"):])
         cur = list(dims)
         for n in sorted(range(N), key=lambda n: mu[n])[:k]:
             cur[n] = mu[n]
         n = sorted(range(N), key=lambda n: mu[n])[k]
+        if qr and k == 0:
+            cur[n] = sk[n]
         inp = float(np.prod(cur))
         return 2.0 * inp * mu[n], (inp + inp / cur[n] * mu[n] + cur[n] * mu[n]) * 8
     if phase.startswith("shrink_ttm_m"):
@@ -184,6 +190,8 @@ def phase_cost(bc, phase: str, dims_local=None):
         cur = list(dims)
         for m in order[:order.index(n)]:
             cur[m] = mu[m]
+        if qr:
+            cur[n] = sk[n]
         inp = float(np.prod(cur))
         return 2.0 * inp * mu[n], (inp + inp / cur[n] * mu[n] + cur[n] * mu[n]) * 8
     return None
@@ -309,6 +317,11 @@ def bench_gpu(args, rank, world, local_rank):
     timed_prof = int(os.environ.get("LMRA_BENCH_PROFILE", "2"))
     ctx.set_profiling(timed_prof)
     bc = CONFIGS[args.config]
+    if args.algorithm:
+        import copy
+        bc = copy.deepcopy(bc)
+        bc.alg = args.algorithm
+        bc.name = f"{bc.name}/{args.algorithm}"
     dist = None
     if world > 1:
         import torch.distributed as dist

@@ -17,6 +17,8 @@
  *   mode_n_product      (tensor.hpp:56-57)          ->  lmra_mode_n_product
  *   gram_power_apply    (linalg.hpp:37-38)          ->  lmra_gram_power_apply
  *   leading_left_singular_vectors (linalg.hpp:41)   ->  lmra_leading_left_singular_vectors
+ *   thin_qr             (linalg.hpp:35)             ->  lmra_thin_qr_q
+ *   qr_project_extract  (linalg.hpp:43-46)          ->  lmra_qr_project_extract
  *   gaussian_matrix     (sketching.hpp:69)          ->  lmra_gaussian_matrix
  *   randsample          (sketching.hpp:56)          ->  lmra_randsample
  *   gram_sampling_probabilities (tucker.cpp:110-130)->  lmra_column_sqnorms + lmra_probabilities
@@ -43,8 +45,11 @@ extern "C" {
 #endif
 
 enum lmra_status { LMRA_OK = 0, LMRA_EINVAL = 1, LMRA_ERUNTIME = 2, LMRA_ECUDA = 3 };
-/* Algorithm ids (tucker.hpp:47-57). Only the randomized power/AMM family is on this path. */
-enum lmra_algorithm { LMRA_ALG1 = 1, LMRA_ALG2 = 2, LMRA_ALG4 = 4, LMRA_ALG5 = 5 };
+/* Algorithm ids (tucker.hpp:47-57). The randomized family: power scheme (alg1/alg2), AMM
+ * (alg4/alg5) and the QR-proxy extraction (alg6/alg7, tucker.cpp:422-454). */
+enum lmra_algorithm {
+  LMRA_ALG1 = 1, LMRA_ALG2 = 2, LMRA_ALG4 = 4, LMRA_ALG5 = 5, LMRA_ALG6 = 6, LMRA_ALG7 = 7
+};
 /* ProbRegime (sketching.hpp:31) */
 enum lmra_regime { LMRA_OPTIMAL = 0, LMRA_NEARLY_OPTIMAL = 1, LMRA_UNIFORM = 2 };
 /* GramStrategy (linalg.hpp:26) */
@@ -175,6 +180,14 @@ int lmra_gram_power_apply(lmra_context* ctx, const double* a, uint64_t rows, uin
 /* u = top-mu left singular vectors of c with the reference's sign rule (linalg.cpp:82-87) */
 int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint64_t rows,
                                        uint64_t cols, uint64_t mu, double* u);
+/* q (rows x cols) = thin Q of c (linalg.cpp:52-60), Householder TSQR; device pointers.
+ * rows <= 256: LAPACK/Eigen HouseholderQR sign convention; above: same span, column signs
+ * of the tree factorisation. */
+int lmra_thin_qr_q(lmra_context* ctx, const double* c, uint64_t rows, uint64_t cols, double* q);
+/* out (rows x mu) = Q U1 with Q = thin_qr(c).Q, U1 = top-mu left singular vectors of Q^T a
+ * (linalg.cpp:89-99); c rows x cols, a rows x a_cols (column-major); device pointers. */
+int lmra_qr_project_extract(lmra_context* ctx, const double* c, uint64_t rows, uint64_t cols,
+                            const double* a, uint64_t a_cols, uint64_t mu, double* out);
 /* the sampling chain on the device, bit-exact with the reference's host loops:
  * p = gram_sampling_probabilities from squared norms w (tucker.cpp:110-130), then
  * randsample(L, p, {seed, stream}) (sketching.cpp:96-131).  w, idx, scales, p: device. */

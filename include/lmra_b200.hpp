@@ -188,15 +188,24 @@ inline TuckerDecomposition rand_thosvd_amm(const DenseTensor& a, const AlgoConfi
 inline TuckerDecomposition rand_sthosvd_amm(const DenseTensor& a, const AlgoConfig& cfg) {
   return detail::run(LMRA_ALG5, a, cfg);
 }
+// tucker.hpp:107-108 (QR-proxy extraction)
+inline TuckerDecomposition rand_thosvd_power_qr(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_ALG6, a, cfg);
+}
+inline TuckerDecomposition rand_sthosvd_power_qr(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_ALG7, a, cfg);
+}
 
-// tucker.hpp:110-111 (the B200 path carries the randomized power / AMM family)
+// tucker.hpp:110-111 (the B200 path carries the randomized family: power, AMM, QR-proxy)
 inline TuckerDecomposition run_algorithm(Algorithm alg, const DenseTensor& a, const AlgoConfig& cfg) {
   switch (alg) {
     case Algorithm::RandThosvdPower: return rand_thosvd_power(a, cfg);
     case Algorithm::RandSthosvdPower: return rand_sthosvd_power(a, cfg);
     case Algorithm::RandThosvdAmm: return rand_thosvd_amm(a, cfg);
     case Algorithm::RandSthosvdAmm: return rand_sthosvd_amm(a, cfg);
-    default: throw std::invalid_argument("algorithm is outside the B200 hot path (alg1/2/4/5)");
+    case Algorithm::RandThosvdPowerQr: return rand_thosvd_power_qr(a, cfg);
+    case Algorithm::RandSthosvdPowerQr: return rand_sthosvd_power_qr(a, cfg);
+    default: throw std::invalid_argument("algorithm is outside the B200 hot path (randomized alg1-alg7)");
   }
 }
 

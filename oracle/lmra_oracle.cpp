@@ -354,6 +354,15 @@ Mat leading_left_singular_vectors(const Mat& c, size_t mu) {  // linalg.cpp:82-8
   return u;
 }
 
+Mat qr_project_extract(const Mat& c, const Mat& a_unfold, size_t mu) {  // linalg.cpp:89-99
+  if (c.r != a_unfold.r) throw std::invalid_argument("qr_project_extract: row counts differ");
+  if (mu < 1 || mu > c.c) throw std::invalid_argument("qr_project_extract: mu out of range");
+  Mat q = thin_qr_q(c);
+  Mat projected = matmul(q, true, a_unfold, false);
+  Mat u1 = leading_left_singular_vectors(projected, mu);
+  return matmul(q, false, u1, false);
+}
+
 // ---------------------------------------------------------------- sketching.cpp
 double stable_sum(const double* v, size_t n) {  // sketching.cpp:13-24
   double s = 0.0, c = 0.0;
@@ -680,7 +689,6 @@ void alg_power(const Tensor& a, const Config& cfg, bool sequential, orc_result& 
       Mat c = gram_power_apply(a_n, g, cfg.power, cfg.strategy);
       res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
       if (cfg.keep_trace) res.trace[n].sketch = c;
-    if (cfg.keep_trace) res.trace[n].sketch = c;
       if (cfg.keep_trace) res.trace[n].omega = std::move(g);
     });
     res.core = core_from_factors(a, res.factors);
@@ -694,6 +702,37 @@ void alg_power(const Tensor& a, const Config& cfg, bool sequential, orc_result& 
     res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
     if (cfg.keep_trace) res.trace[n].sketch = c;
     if (cfg.keep_trace) res.trace[n].omega = std::move(g);
+    work = mode_n_product(work, transpose(res.factors[n]), n);
+  }
+  res.core = std::move(work);
+}
+
+// tucker.cpp:422-454: the QR-proxy variants (alg6 / alg7).  mu is capped at the numerical
+// rank limit min(sketch width, unfolding columns) (rank_cap, tucker.cpp:65-71).
+void alg_power_qr(const Tensor& a, const Config& cfg, bool sequential, orc_result& res) {
+  Resolved r = resolve(a, cfg);
+  const size_t nm = a.dims.size();
+  res.factors.assign(nm, Mat());
+  res.trace.assign(nm, Trace());
+  auto one = [&](const Tensor& t, size_t n) {
+    Mat a_n = unfold(t, n);
+    Mat g = gaussian_matrix(t.dims[n], r.sketch[n], cfg.seed, n + 1);
+    Mat c = gram_power_apply(a_n, g, cfg.power, cfg.strategy);
+    const size_t mu = std::min(r.mu[n], std::min(r.sketch[n], a_n.c));
+    res.factors[n] = qr_project_extract(c, a_n, mu);
+    if (cfg.keep_trace) {
+      res.trace[n].sketch = c;
+      res.trace[n].omega = std::move(g);
+    }
+  };
+  if (!sequential) {
+    run_modes(nm, cfg.mode_threads, [&](size_t n) { one(a, n); });
+    res.core = core_from_factors(a, res.factors);
+    return;
+  }
+  Tensor work = a;
+  for (size_t n : r.order) {
+    one(work, n);
     work = mode_n_product(work, transpose(res.factors[n]), n);
   }
   res.core = std::move(work);
@@ -716,7 +755,6 @@ void alg_amm(const Tensor& a, const Config& cfg, bool sequential, orc_result& re
       Mat c = gram_power_apply(sampled, g, cfg.power, cfg.strategy);
       res.factors[n] = top_left_vectors_clamped(c, r.mu[n]);
       if (cfg.keep_trace) res.trace[n].sketch = c;
-    if (cfg.keep_trace) res.trace[n].sketch = c;
       if (cfg.keep_trace) {
         res.trace[n].omega = std::move(g);
         res.trace[n].samples = std::move(s);
@@ -902,6 +940,17 @@ int orc_thin_qr_q(const double* m, uint64_t rows, uint64_t cols, double* q) {
   });
 }
 
+int orc_qr_project_extract(const double* c, uint64_t rows, uint64_t cols, const double* a,
+                           uint64_t a_cols, uint64_t mu, double* out) {
+  return guard([&] {
+    Mat cm(rows, cols), am(rows, a_cols);
+    std::memcpy(cm.d.data(), c, sizeof(double) * rows * cols);
+    std::memcpy(am.d.data(), a, sizeof(double) * rows * a_cols);
+    Mat f = qr_project_extract(cm, am, mu);
+    std::memcpy(out, f.d.data(), sizeof(double) * rows * mu);
+  });
+}
+
 int orc_run(int alg, const double* x, const uint64_t* dims, int order, const orc_config* cfg,
             orc_result** out) {
   *out = nullptr;
@@ -917,6 +966,8 @@ int orc_run(int alg, const double* x, const uint64_t* dims, int order, const orc
         case ORC_ALG2: alg_power(a, k, true, *res); break;
         case ORC_ALG4: alg_amm(a, k, false, *res); break;
         case ORC_ALG5: alg_amm(a, k, true, *res); break;
+        case ORC_ALG6: alg_power_qr(a, k, false, *res); break;
+        case ORC_ALG7: alg_power_qr(a, k, true, *res); break;
         default: throw std::invalid_argument("unknown algorithm");
       }
       auto t1 = std::chrono::steady_clock::now();

@@ -37,7 +37,7 @@ extern "C" {
 #endif
 
 /* algorithm ids follow tucker.hpp:47-57 */
-enum { ORC_ALG1 = 1, ORC_ALG2 = 2, ORC_ALG4 = 4, ORC_ALG5 = 5 };
+enum { ORC_ALG1 = 1, ORC_ALG2 = 2, ORC_ALG4 = 4, ORC_ALG5 = 5, ORC_ALG6 = 6, ORC_ALG7 = 7 };
 /* ProbRegime, sketching.hpp:24 */
 enum { ORC_OPTIMAL = 0, ORC_NEARLY_OPTIMAL = 1, ORC_UNIFORM = 2 };
 
@@ -85,6 +85,9 @@ int orc_gram_power_apply(const double* a, uint64_t rows, uint64_t cols, const do
 int orc_leading_left_singular_vectors(const double* c, uint64_t rows, uint64_t cols, uint64_t mu,
                                       double* u);
 int orc_thin_qr_q(const double* m, uint64_t rows, uint64_t cols, double* q);
+/* linalg.cpp:89-99 */
+int orc_qr_project_extract(const double* c, uint64_t rows, uint64_t cols, const double* a,
+                           uint64_t a_cols, uint64_t mu, double* out);
 
 /* algorithms */
 int orc_run(int alg, const double* x, const uint64_t* dims, int order, const orc_config* cfg,

@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "liblmra_oracle.so")
 
-ALG = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5}
+ALG = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5, "alg6": 6, "alg7": 7}
 REGIME = {"optimal": 0, "nearly_optimal": 1, "uniform": 2}
 
 u64p = C.POINTER(C.c_uint64)
@@ -310,6 +310,17 @@ def thin_qr_q(m: np.ndarray) -> np.ndarray:
     _check(lib().orc_thin_qr_q(m.ctypes.data_as(dblp), C.c_uint64(m.shape[0]), C.c_uint64(m.shape[1]),
                                q.ctypes.data_as(dblp)))
     return q
+
+
+def qr_project_extract(c: np.ndarray, a: np.ndarray, mu: int) -> np.ndarray:
+    """linalg.cpp:89-99."""
+    c = np.asfortranarray(c, dtype=np.float64)
+    a = np.asfortranarray(a, dtype=np.float64)
+    out = np.empty((c.shape[0], mu), order="F")
+    _check(lib().orc_qr_project_extract(c.ctypes.data_as(dblp), C.c_uint64(c.shape[0]), C.c_uint64(c.shape[1]),
+                                        a.ctypes.data_as(dblp), C.c_uint64(a.shape[1]), C.c_uint64(mu),
+                                        out.ctypes.data_as(dblp)))
+    return out
 
 
 def relative_error(x: np.ndarray, dims: Sequence[int], dec: Decomposition) -> float:

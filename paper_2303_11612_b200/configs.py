@@ -107,8 +107,9 @@ def algorithmic_cost(bc: BaselineConfig) -> dict:
     B = 0.0
     F = 0.0
     size = float(np.prod(dims))
-    seq = bc.alg in ("alg2", "alg5")
+    seq = bc.alg in ("alg2", "alg5", "alg7")
     amm = bc.alg in ("alg4", "alg5")
+    qr = bc.alg in ("alg6", "alg7")  # QR-proxy: + projection P = Q^T A_(n), SVD via P's R factor
     order = list(cfg.order) if cfg.order else list(range(N))
 
     def power_cost(I, J, s_):
@@ -138,10 +139,24 @@ def algorithmic_cost(bc: BaselineConfig) -> dict:
         if not amm:
             # R2: the N modes' half-products share reads of X in each of the 2q phases
             B -= (N - 1) * 2 * q * size * 8
+        if qr:
+            # projections P_n = Q_n^T A_(n) share one read of X (R2); each P_n is written once
+            # and read once by its R factor
+            B += size * 8
+            for n in range(N):
+                J = size / dims[n]
+                B += (2 * J * s[n] + dims[n] * s[n]) * 8
+                F += 2.0 * size * s[n]
         # core: ascending width
         cur = list(dims)
         idx = sorted(range(N), key=lambda n: mu[n])
-        for n in idx:
+        for k, n in enumerate(idx):
+            if qr and k == 0:  # the first contraction reads P (s rows) instead of X
+                J = size / dims[n]
+                B += (J * s[n] + J * mu[n] + s[n] * mu[n]) * 8
+                F += 2.0 * J * s[n] * mu[n]
+                cur[n] = mu[n]
+                continue
             inp = float(np.prod(cur))
             out = inp / cur[n] * mu[n]
             B += (inp + out + cur[n] * mu[n]) * 8
@@ -164,7 +179,11 @@ def algorithmic_cost(bc: BaselineConfig) -> dict:
             B += b
             F += f
             out = sz / I * mu[n]
-            B += (sz + out + I * mu[n]) * 8
-            F += 2.0 * sz * mu[n]
+            if qr:  # projection (read A, write P), R factor (read P), shrink from P
+                B += (sz + 3 * J * s[n] + I * s[n] + out + s[n] * mu[n]) * 8
+                F += 2.0 * sz * s[n] + 2.0 * J * s[n] * mu[n]
+            else:
+                B += (sz + out + I * mu[n]) * 8
+                F += 2.0 * sz * mu[n]
             cur[n] = mu[n]
     return {"bytes": B, "flops": F, "tensor_bytes": size * 8}

@@ -66,6 +66,18 @@ size_t orth_workspace_doubles(long long I, int s);
 cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, double* work,
                         int* status, cudaStream_t st);
 
+// qr_project_extract (linalg.cpp:89-99) building blocks (orth.cu):
+// R (s x s, column-major) of a tall m x s matrix (m >= s) by Householder TSQR.
+size_t r_factor_workspace_doubles(long long m, int s);
+cudaError_t launch_r_factor(const double* a, long long m, int s, double* r, double* work,
+                            cudaStream_t st);
+// thin Q (I x s) of C (thin_qr, linalg.cpp:52-60) by Householder TSQR.
+size_t thin_q_workspace_doubles(long long I, int s);
+cudaError_t launch_thin_q(const double* c, long long I, int s, double* q, double* work, cudaStream_t st);
+// out (J x I column-major) = transposed mode unfolding of x (ModeView inner, I, outer).
+cudaError_t launch_unfold_t(const double* x, long long inner, long long I, long long outer, double* out,
+                            cudaStream_t st);
+
 // Mode-0 contraction on the int8 tensor cores (ttm_i8.cu): y (mu x J) = q^T x with x K x J
 // (column j contiguous), q K x mu column-major, w[j] the canonical squared norm of column j
 // (sets the column's fixed-point scale).  ~1e-13 relative accuracy; supported for K even,

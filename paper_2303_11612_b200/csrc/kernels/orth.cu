@@ -1214,4 +1214,125 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// QR-proxy extraction (qr_project_extract, linalg.cpp:89-99) building blocks
+// ---------------------------------------------------------------------------
+__global__ void eye_kernel(double* __restrict__ e, int s) {
+  pdl_wait();  // the chain's earlier kernels must be complete before the next one may rely on it
+  pdl_trigger();
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < s * s; k += gridDim.x * blockDim.x)
+    e[k] = (k % s == k / s) ? 1.0 : 0.0;
+}
+
+// workspace of the R-only tree: the leaf levels plus the top block's reflectors and tau
+static size_t r_tree_doubles(long long m, int s, std::vector<OrthLevel>* lv_out, size_t* top_off) {
+  size_t used = 0;
+  std::vector<OrthLevel> lv = plan_levels(m, s, &used);
+  const long long mt = lv.empty() ? m : (long long)lv.back().nb * s;
+  *top_off = used;
+  used += (size_t)mt * s + s;  // top reflectors (mt x s), tau (s)
+  if (lv_out) *lv_out = lv;
+  return used;
+}
+
+size_t r_factor_workspace_doubles(long long m, int s) {
+  size_t top = 0;
+  return r_tree_doubles(m, s, nullptr, &top) + 64;
+}
+
+// R (s x s, column-major, zeros below the diagonal) of the tall m x s matrix a: Householder
+// TSQR leaves level by level, then one Householder QR of the last stacked block.  Row signs
+// of R follow the dlarfg convention per block (only |R| and R^T R are tree-independent).
+cudaError_t launch_r_factor(const double* a, long long m, int s, double* r, double* work,
+                            cudaStream_t st) {
+  if (s < 1 || s > kOrthMaxS || m < s) return cudaErrorInvalidValue;
+  std::vector<OrthLevel> lv;
+  size_t top = 0;
+  r_tree_doubles(m, s, &lv, &top);
+  cudaError_t e;
+  for (size_t l = 0; l < lv.size(); ++l) {
+    const OrthLevel& L = lv[l];
+    const double* A = l == 0 ? a : work + lv[l - 1].w_off;
+    e = LMRA_RPL_DISPATCH(rpl_for((L.m + L.nb - 1) / L.nb), leaf_qr)(A, L.m, s, L.nb, work + L.v_off,
+                                                                      work + L.tau_off, work + L.w_off,
+                                                                      L.nb * s, st);
+    if (e != cudaSuccess) return e;
+  }
+  const long long mt = lv.empty() ? m : (long long)lv.back().nb * s;
+  const double* At = lv.empty() ? a : work + lv.back().w_off;
+  return LMRA_RPL_DISPATCH(rpl_for(mt), leaf_qr)(At, mt, s, 1, work + top, work + top + (size_t)mt * s, r, s,
+                                                 st);
+}
+
+size_t thin_q_workspace_doubles(long long I, int s) {
+  std::vector<OrthLevel> lv;
+  size_t top = 0;
+  size_t used = r_tree_doubles(I, s, &lv, &top);
+  used += (size_t)s * s * 2;                                // R of the top block, identity
+  for (auto& L : lv) used += (size_t)L.nb * s * s;          // W per level
+  return used + 64;
+}
+
+// Thin Q (I x s) of C (thin_qr, linalg.cpp:52-60): the reflectors of the R tree applied to
+// [I_s; 0] back down the tree.  One block (I <= 256) is exactly Householder QR with LAPACK's
+// (dgeqrf/dorgqr, = Eigen HouseholderQR) sign convention; above that the TSQR Q spans the
+// same column space with per-column signs that may differ.
+cudaError_t launch_thin_q(const double* c, long long I, int s, double* q, double* work, cudaStream_t st) {
+  if (s < 1 || s > kOrthMaxS || I < s) return cudaErrorInvalidValue;
+  std::vector<OrthLevel> lv;
+  size_t top = 0;
+  size_t used = r_tree_doubles(I, s, &lv, &top);
+  double* R = work + used;
+  double* E = R + (size_t)s * s;
+  used += (size_t)s * s * 2;
+  std::vector<size_t> wbuf(lv.size());
+  for (size_t l = 0; l < lv.size(); ++l) {
+    wbuf[l] = used;
+    used += (size_t)lv[l].nb * s * s;
+  }
+  cudaError_t e = launch_r_factor(c, I, s, R, work, st);
+  if (e != cudaSuccess) return e;
+  {
+    const cudaError_t le = launch_pdl(eye_kernel, dim3(1), dim3(256), 0, st, E, s);
+    if (le != cudaSuccess) return le;
+  }
+  const long long mt = lv.empty() ? I : (long long)lv.back().nb * s;
+  double* out_top = lv.empty() ? q : work + wbuf.back();
+  e = LMRA_RPL_DISPATCH(rpl_for(mt), leaf_apply)(work + top, mt, s, 1, work + top + (size_t)mt * s, E, s, s,
+                                                 out_top, nullptr, nullptr, st);
+  if (e != cudaSuccess) return e;
+  for (int l = (int)lv.size() - 1; l >= 0; --l) {
+    const OrthLevel& L = lv[l];
+    double* out = l == 0 ? q : work + wbuf[l - 1];
+    e = LMRA_RPL_DISPATCH(rpl_for((L.m + L.nb - 1) / L.nb), leaf_apply)(
+        work + L.v_off, L.m, s, L.nb, work + L.tau_off, work + wbuf[l], L.nb * s, s, out, nullptr, nullptr, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// out (J x I, column-major) = the transposed mode unfolding of x: out[j + J r] = X3[i, r, o],
+// j = i + inner o.  Each (r, o) fibre segment of `inner` contiguous values is a contiguous
+// run in out as well, so this is a strided copy (coalesced both ways for inner >= 32); the
+// mode-0 case (inner = 1) is a plain transpose.
+__global__ void unfold_t_kernel(const double* __restrict__ x, long long inner, long long I, long long outer,
+                                double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const long long n = inner * I * outer, J = inner * outer;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e % inner, ro = e / inner, r = ro % I, o = ro / I;
+    out[i + inner * o + J * r] = x[e];
+  }
+}
+
+cudaError_t launch_unfold_t(const double* x, long long inner, long long I, long long outer, double* out,
+                            cudaStream_t st) {
+  if (inner == 1) return launch_transpose(x, I, outer, out, st);
+  const long long n = inner * I * outer;
+  const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
+  return launch_pdl(unfold_t_kernel, dim3(blocks), dim3(256), 0, st, x, inner, I, outer, out);
+}
+
 }  // namespace lmra_dev

@@ -600,6 +600,52 @@ class Engine {
     return u;
   }
 
+  // qr_project_extract (linalg.cpp:89-99) for mode n of the tensor x: Q = thin_qr(C).Q,
+  // P = X x_n Q^T (the projected unfolding Q^T A_(n), formed in place on the mode view),
+  // U1 = top-mu left singular vectors of P_(n) (s x J) with the sign rule -- through the R
+  // factor of P_(n)^T when J >= s (P_(n) = R^T Q2^T, so U of R^T = U of P_(n)) -- and the
+  // factor Q U1.  P and U1 are kept: X x_n (Q U1)^T = P x_n U1^T, so the following shrink /
+  // core contraction of this mode reads P (s rows) instead of the tensor.
+  struct QrProxy {
+    DevBuf f, p, u1;
+  };
+  QrProxy qr_extract(const double* x, const std::vector<size_t>& dims, size_t n, const double* c, size_t s,
+                     size_t mu, int* status) {
+    const size_t I = dims[n];
+    const ModeView v = view_of(dims, n);
+    const size_t J = (size_t)(v.inner * v.outer);
+    QrProxy out;
+    DevBuf q(I * s, st_);
+    {
+      DevBuf w(lmra_dev::thin_q_workspace_doubles((long long)I, (int)s), st_);
+      launch("qr_thin_q", [&] { return lmra_dev::launch_thin_q(c, (long long)I, (int)s, q.get(), w.get(), st_); });
+    }
+    out.p = ttm(x, dims, n, q.get(), s, "qr_project");
+    DevBuf pt(J * s, st_);
+    launch("qr_unfold", [&] {
+      return lmra_dev::launch_unfold_t(out.p.get(), v.inner, (long long)s, v.outer, pt.get(), st_);
+    });
+    if (J >= s) {
+      DevBuf rr(s * s, st_), l(s * s, st_);
+      DevBuf w(lmra_dev::r_factor_workspace_doubles((long long)J, (int)s), st_);
+      launch("qr_r_factor", [&] {
+        return lmra_dev::launch_r_factor(pt.get(), (long long)J, (int)s, rr.get(), w.get(), st_);
+      });
+      launch("transpose", [&] { return lmra_dev::launch_transpose(rr.get(), (long long)s, (long long)s, l.get(), st_); });
+      out.u1 = orth(l.get(), s, s, mu, status);
+    } else {  // P_(n) is itself tall (s x J, J < s)
+      DevBuf pn(s * J, st_);
+      launch("transpose", [&] { return lmra_dev::launch_transpose(pt.get(), (long long)J, (long long)s, pn.get(), st_); });
+      out.u1 = orth(pn.get(), s, J, mu, status);
+    }
+    out.f = DevBuf(I * mu, st_);
+    launch("qr_factor", [&] {
+      return lmra_dev::launch_ttm(q.get(), ModeView{(long long)I, (long long)s, 1}, out.u1.get(), (int)mu,
+                                  out.f.get(), st_);
+    });
+    return out;
+  }
+
   DevBuf upload(const double* h, size_t n) {
     DevBuf d(n, st_);
     ck(cudaMemcpyAsync(d.get(), h, n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D");
@@ -637,7 +683,8 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     if (d == 0) throw std::invalid_argument("tensor dimension must be positive");
   Resolved r = resolve(in.dims, cfg);
   const bool amm = in.alg == LMRA_ALG4 || in.alg == LMRA_ALG5;
-  const bool sequential = in.alg == LMRA_ALG2 || in.alg == LMRA_ALG5;
+  const bool qr = in.alg == LMRA_ALG6 || in.alg == LMRA_ALG7;
+  const bool sequential = in.alg == LMRA_ALG2 || in.alg == LMRA_ALG5 || in.alg == LMRA_ALG7;
   std::vector<size_t> t_flat;
   if (amm && !sequential) t_flat = amm_sample_counts(in.dims, cfg, false);
   if (amm && sequential && !cfg.t_samples.empty() && cfg.t_samples.size() != N)
@@ -781,6 +828,8 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     }
   } om_guard{om_ready};
 
+  // QR-proxy (alg6/alg7): the projected tensor P and U1 of a mode whose contraction reads P
+  std::vector<Engine::QrProxy> qrp(N);
   auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
                          size_t n) -> DevBuf {
     cudaStream_t s_ = e.st_;
@@ -801,6 +850,16 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       });
       const ModeView cv{1, (long long)I, (long long)T};
       e.gram_power(cp.get(), cv, c, s, cfg.power, cfg.strategy);
+    }
+    if (qr) {  // tucker.cpp:431-434 / 447-450: mu capped at min(sketch width, unfolding columns)
+      const size_t J = (size_t)(v.inner * v.outer);
+      const size_t mu = std::min(r.mu[n], std::min(s, J));
+      if (mu < r.mu[n])
+        fprintf(stderr, "lmra: requested rank %zu exceeds matrix rank limit %zu, clamping\n", r.mu[n], mu);
+      res->f_rows[n] = I;
+      res->f_cols[n] = mu;
+      qrp[n] = e.qr_extract(x, dims, n, c.get(), s, mu, status_i + n);
+      return std::move(qrp[n].f);
     }
     const size_t mu = std::min(r.mu[n], std::min(I, s));  // top_left_vectors_clamped
     if (mu < r.mu[n])
@@ -853,6 +912,8 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     std::iota(idx.begin(), idx.end(), size_t{0});
     std::stable_sort(idx.begin(), idx.end(),
                      [&](size_t a, size_t b) { return res->f_cols[a] < res->f_cols[b]; });
+    if (qr)  // only the first contraction reads a projected tensor
+      for (size_t k = 1; k < idx.size(); ++k) qrp[idx[k]] = Engine::QrProxy{};
     std::vector<size_t> cur = in.dims;
     DevBuf t;
     const double* src = in.x;
@@ -863,6 +924,14 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     for (size_t k = 0; k < idx.size(); ++k) {
       const size_t n = idx[k];
       const bool next1 = k + 1 < idx.size() && idx[k + 1] == 1;
+      if (qr && k == 0) {  // X x_n (Q U1)^T = P x_n U1^T: read the projected tensor
+        std::vector<size_t> pd = cur;
+        pd[n] = r.sketch[n];
+        t = eng.ttm(qrp[n].p.get(), pd, n, qrp[n].u1.get(), res->f_cols[n], "core_ttm" + std::to_string(step++));
+        cur[n] = res->f_cols[n];
+        src = t.get();
+        continue;
+      }
       DevBuf y = eng.ttm_mode0(src, cur, n, factors[n].get(), res->f_cols[n], src == in.x ? w0 : nullptr,
                                "core_ttm" + std::to_string(step++), &chain, next1);
       cur[n] = res->f_cols[n];
@@ -888,6 +957,16 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       sample_mode(eng, src, cur, n, t_n);
       upload_omegas();
       factors[n] = factor_mode(eng, src, cur, n);
+      if (qr) {  // shrink through the projected tensor: P x_n U1^T
+        std::vector<size_t> pd = cur;
+        pd[n] = r.sketch[n];
+        DevBuf y = eng.ttm(qrp[n].p.get(), pd, n, qrp[n].u1.get(), res->f_cols[n], "shrink_ttm_m" + std::to_string(n));
+        qrp[n] = Engine::QrProxy{};
+        cur[n] = res->f_cols[n];
+        work = std::move(y);
+        src = work.get();
+        continue;
+      }
       const double* w0 =
           (amm && cfg.regime != kUniform && src == in.x && d_w[n].get() && !(in.ov && in.ov->sample_idx))
               ? d_w[n].get() : nullptr;
@@ -1496,10 +1575,12 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null context");
     if (algorithm != LMRA_ALG1 && algorithm != LMRA_ALG2 && algorithm != LMRA_ALG4 &&
-        algorithm != LMRA_ALG5)
+        algorithm != LMRA_ALG5 && algorithm != LMRA_ALG6 && algorithm != LMRA_ALG7)
       throw std::invalid_argument("unknown algorithm");
     if (order < 1) throw std::invalid_argument("cannot decompose an order-0 tensor");
     const bool sharded = ctx->comm && ctx->nranks > 1;
+    if (sharded && (algorithm == LMRA_ALG6 || algorithm == LMRA_ALG7))
+      throw std::invalid_argument("alg6/alg7 run on one device (no sharded QR-proxy path)");
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard dg(ctx->device);
     ArenaScope arena(ctx);  // every device buffer of the run (after the device guard)
@@ -1707,6 +1788,44 @@ int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint6
     ck(cudaMemsetAsync(status.get(), 0, sizeof(double), ctx->stream), "memset");
     DevBuf out = eng.orth(c, rows, cols, mu, reinterpret_cast<int*>(status.get()));
     ck(cudaMemcpyAsync(u, out.get(), rows * mu * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream),
+       "copy");
+    int st = 0;
+    ck(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    if (st) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  });
+}
+
+int lmra_thin_qr_q(lmra_context* ctx, const double* c, uint64_t rows, uint64_t cols, double* q) {
+  return guard([&] {
+    if (rows < cols) throw std::invalid_argument("thin_qr: requires rows >= cols");
+    if (cols < 1 || cols > (uint64_t)lmra_dev::kMaxWidth)
+      throw std::invalid_argument("thin_qr: 1 to 64 columns");
+    DeviceGuard dg(ctx->device);
+    Engine eng(ctx);
+    DevBuf w(lmra_dev::thin_q_workspace_doubles((long long)rows, (int)cols), ctx->stream);
+    eng.launch("qr_thin_q", [&] {
+      return lmra_dev::launch_thin_q(c, (long long)rows, (int)cols, q, w.get(), ctx->stream);
+    });
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_qr_project_extract(lmra_context* ctx, const double* c, uint64_t rows, uint64_t cols,
+                            const double* a, uint64_t a_cols, uint64_t mu, double* out) {
+  return guard([&] {
+    if (mu < 1 || mu > cols) throw std::invalid_argument("qr_project_extract: mu out of range");
+    if (rows < cols) throw std::invalid_argument("thin_qr: requires rows >= cols");
+    if (cols > (uint64_t)lmra_dev::kMaxWidth) throw std::invalid_argument("qr_project_extract: more than 64 columns");
+    if (mu > std::min(cols, a_cols))
+      throw std::invalid_argument("leading_left_singular_vectors: mu out of range");
+    DeviceGuard dg(ctx->device);
+    Engine eng(ctx);
+    DevBuf status(1, ctx->stream);
+    ck(cudaMemsetAsync(status.get(), 0, sizeof(double), ctx->stream), "memset");
+    Engine::QrProxy r = eng.qr_extract(a, {(size_t)rows, (size_t)a_cols}, 0, c, cols, mu,
+                                       reinterpret_cast<int*>(status.get()));
+    ck(cudaMemcpyAsync(out, r.f.get(), rows * mu * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream),
        "copy");
     int st = 0;
     ck(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");

@@ -90,6 +90,27 @@ def leading_left_singular_vectors(c_colmajor, rows: int, cols: int, mu: int, ctx
     return u
 
 
+def thin_qr_q(c_colmajor, rows: int, cols: int, ctx: Context = None):
+    """linalg.cpp:52-60 thin_qr(c).Q on the device (Householder TSQR)."""
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    q = empty(rows * cols, ctx.device)
+    check(lib.lmra_thin_qr_q(ctx.handle, _ptr(c_colmajor), rows, cols, _ptr(q)))
+    return q
+
+
+def qr_project_extract(c_colmajor, rows: int, cols: int, a_colmajor, a_cols: int, mu: int,
+                       ctx: Context = None):
+    """linalg.cpp:89-99: Q U1 with Q = thin_qr(c).Q and U1 the top-mu left singular vectors
+    of Q^T a (c: rows x cols, a: rows x a_cols, column-major device buffers)."""
+    ctx = ctx or default_context()
+    _torch().cuda.current_stream().synchronize()
+    out = empty(rows * mu, ctx.device)
+    check(lib.lmra_qr_project_extract(ctx.handle, _ptr(c_colmajor), rows, cols, _ptr(a_colmajor), a_cols,
+                                      mu, _ptr(out)))
+    return out
+
+
 def column_sqnorms(x, dims: Sequence[int], mode: int, ctx: Context = None):
     ctx = ctx or default_context()
     _torch().cuda.current_stream().synchronize()

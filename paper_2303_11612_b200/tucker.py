@@ -34,7 +34,7 @@ from . import _lib
 from ._lib import LmraError, LmraInvalidArgument, check, lib
 
 ALGORITHM_IDS = ["thosvd", "sthosvd", "hooi", "alg1", "alg2", "alg4", "alg5", "alg6", "alg7"]
-_ALG_CODE = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5}
+_ALG_CODE = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5, "alg6": 6, "alg7": 7}
 _REGIME = {"optimal": 0, "nearly_optimal": 1, "uniform": 2}
 _STRATEGY = {"A": 0, "B": 1}
 
@@ -387,7 +387,7 @@ def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omeg
     global_dims the whole tensor's dims (default: a's own dims, i.e. unsharded)."""
     if alg not in _ALG_CODE:
         if alg in ALGORITHM_IDS:
-            raise LmraInvalidArgument(f"{alg} is outside the B200 hot path (alg1/alg2/alg4/alg5)")
+            raise LmraInvalidArgument(f"{alg} is outside the B200 hot path (randomized alg1-alg7)")
         raise LmraInvalidArgument("unknown algorithm")
     t = _as_tensor(a)
     ctx = ctx or default_context()
@@ -439,6 +439,16 @@ def rand_thosvd_amm(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
 
 def rand_sthosvd_amm(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
     return run_algorithm("alg5", a, cfg, **kw)
+
+
+def rand_thosvd_power_qr(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    """tucker.cpp:422-436 (alg6): power-scheme sketch, QR-proxy extraction."""
+    return run_algorithm("alg6", a, cfg, **kw)
+
+
+def rand_sthosvd_power_qr(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    """tucker.cpp:438-454 (alg7): sequential modes, QR-proxy extraction."""
+    return run_algorithm("alg7", a, cfg, **kw)
 
 
 def amm_sample_counts(dims: Sequence[int], cfg: AlgoConfig, sequential: bool) -> List[int]:

@@ -5,7 +5,7 @@ import pytest
 
 from conftest import relative_error
 
-ALGS = ["alg1", "alg2", "alg4", "alg5"]
+ALGS = ["alg1", "alg2", "alg4", "alg5", "alg6", "alg7"]
 
 
 # ---------------------------------------------------------------- linalg (test_linalg.cpp)
@@ -167,10 +167,37 @@ def test_bit_identical_reruns(orc, alg):
     assert all(np.array_equal(p, q) for p, q in zip(a.factors, b.factors))
 
 
+def test_qr_proxy_tracks_power_variants(orc):
+    # :267-299: on the desk tensor alg6 / alg7 stay within 5 % of alg1 / alg2 on >= 16 of 20 seeds
+    dims = [60, 60, 60]
+    x = orc.gen_tucker_noise(dims, [10, 10, 10], 0.001, 31)
+    a = x.reshape(dims, order="F")
+    ok6 = ok7 = 0
+    for s in range(1, 21):
+        cfg = orc.AlgoConfig(rank=[10, 10, 10], seed=s)
+        re = {alg: relative_error(a, d.core, d.factors)
+              for alg in ("alg1", "alg2", "alg6", "alg7") for d in [orc.run(alg, x, dims, cfg)]}
+        ok6 += re["alg6"] <= 1.05 * re["alg1"]
+        ok7 += re["alg7"] <= 1.05 * re["alg2"]
+    assert ok6 >= 16 and ok7 >= 16, (ok6, ok7)
+
+
+def test_qr_project_extract_is_range_projection(orc):
+    # linalg.cpp:89-99: Q U1 = top left singular vectors of the projection of a onto range(c)
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((30, 200)) * np.logspace(0, -3, 30)[:, None]
+    c = a @ (a.T @ rng.standard_normal((30, 8)))
+    f = orc.qr_project_extract(c, a, 5)
+    q, _ = np.linalg.qr(c)
+    u = np.linalg.svd(q @ (q.T @ a))[0][:, :5]
+    assert np.abs(f.T @ f - np.eye(5)).max() <= 1e-13
+    assert np.linalg.norm(f - u @ (u.T @ f), 2) <= 1e-10
+
+
 def test_order4_exact_rank(orc):
     dims = [12, 12, 12, 12]                                                                 # :399-421
     x = orc.gen_tucker_noise(dims, [3, 3, 3, 3], 0.0, 47)
-    for alg in ["alg1", "alg2"]:
+    for alg in ["alg1", "alg2", "alg7"]:
         d = orc.run(alg, x, dims, orc.AlgoConfig(rank=[3, 3, 3, 3], seed=2))
         assert relative_error(x.reshape(dims, order="F"), d.core, d.factors) <= 1e-8
     d = orc.run("alg4", x, dims, orc.AlgoConfig(rank=[3, 3, 3, 3], seed=2, t_samples=[1728] * 4))
@@ -184,7 +211,8 @@ def test_degenerate_shapes(orc):
         d = orc.run(alg, x, dims, orc.AlgoConfig(rank=[10, 2, 2], seed=3, t_samples=[4, 80, 80]))
         for q in d.factors:
             assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-10
-        assert d.factors[0].shape == (40, 10)
+        # the QR-proxy variants cap mu at the unfolding's 4 columns (rank_cap, tucker.cpp:65-71)
+        assert d.factors[0].shape == ((40, 4) if alg in ("alg6", "alg7") else (40, 10))
 
 
 def test_baseline_generators(orc):
