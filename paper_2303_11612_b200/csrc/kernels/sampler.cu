@@ -21,8 +21,10 @@
 //    both binades.  One CTA walks the chunks in order with the exact state (pass C): runs
 //    of certified chunks are taken at once (a block scan of the 2-state parity transducer
 //    M -> M + R_parity(M)); a split chunk is walked sub-chunk by sub-chunk, stepping only
-//    the sub-chunk that holds the crossing; chunk 0 (dense crossings from S = 0) is
-//    processed element-exactly.  Pass D writes every S_i of the certified (sub-)chunks.
+//    the sub-chunk that holds the crossing (one warp: a warp scan of the sub-chunk
+//    transducers, the crossing sub-chunk stepped by one lane from shared memory); chunk 0
+//    (dense crossings from S = 0) is processed element-exactly.
+//    Pass D writes every S_i of the certified (sub-)chunks.
 //  * Neumaier's stable_sum (sketching.cpp:13-24) = fl(S + c): S is the naive sum (above);
 //    c is the naive sum of the exact two-sum errors e_i (computable from S_{i-1}, x_i,
 //    S_i).  c is accumulated exactly (double-double, fixed tree) and the final rounding
@@ -702,65 +704,133 @@ __device__ __forceinline__ int block_min_int(int v, int* sm) {
   return r;
 }
 
-// A split chunk: thread 0 takes certified sub-chunks (under whichever hypothesis matches the
-// current binade); the sub-chunk that is not certified (the crossing) is stepped exactly.
-__device__ double split_walk(const double* __restrict__ x, long long n, int k, double S,
-                             const ChunkAgg* __restrict__ subagg, ChunkStart* __restrict__ substarts,
-                             double* __restrict__ out, double* smd, int* smi, long long* sml,
-                             unsigned long long* st) {
+// ---------------------------------------------------------------- warp-level split walk
+// exclusive warp scan of parity transducers (lanes past the active range pass the identity)
+__device__ __forceinline__ Tx warp_excl_tx(Tx t) {
+  const int lane = threadIdx.x & 31;
+  Tx inc = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Tx u = tx_shfl_up(inc, o);
+    if (lane >= o) inc = tx_compose(u, inc);
+  }
+  Tx prev = tx_shfl_up(inc, 1);
+  if (lane == 0) prev = tx_identity();
+  return prev;
+}
+
+// The reference's recurrence S_i = fl(S_{i-1} + x_i) over cnt <= kSub elements staged in
+// shared memory, stepped by lane 0 of the walking warp (loads batched ahead of the dependent
+// adds; the prefixes overwrite xs), then written out by the warp.  Measured against a
+// warp-parallel variant (classify / scan / find the crossing, one iteration per binade
+// crossing): a single warp's ~25 dependent instructions per element slot made that 3x slower
+// than 256 plain dependent adds.
+__device__ double warp_seq_segment(double* xs, long long c0, int cnt, double S, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    double s = S;
+    int j = 0;
+    for (; j + 8 <= cnt; j += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = xs[j + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        s = __dadd_rn(s, v[k]);
+        v[k] = s;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xs[j + k] = v[k];
+    }
+    for (; j < cnt; ++j) {
+      s = __dadd_rn(s, xs[j]);
+      xs[j] = s;
+    }
+    S = s;
+  }
+  S = __shfl_sync(0xffffffffu, S, 0);
+  __syncwarp();
+  if (out)
+    for (int i = lane; i < cnt; i += 32) out[c0 + i] = xs[i];
+  return S;
+}
+
+// A split chunk, walked by warp 0: the chunk's elements are staged in shared memory by the
+// whole block first (xs, kChunk doubles); runs of certified sub-chunks (under whichever binade
+// hypothesis matches the exact state) are one warp scan of their parity transducers, the
+// sub-chunk holding a crossing is stepped (warp_seq_segment).  Replaces a thread-0 loop over
+// the 16 sub-chunks with block barriers around every stepped sub-chunk.
+__device__ double split_walk_warp(const double* __restrict__ x, long long n, int k, double S,
+                                  const ChunkAgg* __restrict__ subagg, ChunkStart* __restrict__ substarts,
+                                  double* __restrict__ out, double* xs, unsigned long long* st) {
   __shared__ double s_S;
-  __shared__ int s_g;
-  __shared__ ChunkAgg sub[2 * kNSub];  // this chunk's sub-aggregates, both hypotheses
-  if (threadIdx.x < 2 * kNSub) sub[threadIdx.x] = subagg[(size_t)k * 2 * kNSub + threadIdx.x];
+  const long long base = (long long)k * kChunk;
+  __syncthreads();  // xs / s_S may still be read from the previous split chunk
+  for (int i = threadIdx.x; i < kChunk; i += kCThr) xs[i] = base + i < n ? x[base + i] : 0.0;
+  ChunkAgg h0{}, h1{};
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < kNSub) {
+    h0 = subagg[(size_t)k * 2 * kNSub + lane];
+    h1 = subagg[(size_t)k * 2 * kNSub + kNSub + lane];
+  }
   __syncthreads();
-  int g = 0;
-  while (g < kNSub) {
-    if (threadIdx.x == 0) {
-      double s = S;
-      int gg = g;
-      if (s > 0.0) {
+  if (threadIdx.x < 32) {
+    int g = 0;
+    while (g < kNSub) {
+      if (S > 0.0) {
         int ue, be;
-        binade_of(s, ue, be);
-        double M = ldexp(s, -ue);
+        binade_of(S, ue, be);
+        const double M = ldexp(S, -ue);
         const double capU = ldexp(1.0, be - ue);
-        for (; gg < kNSub; ++gg) {
-          const ChunkAgg* h0 = sub + gg;
-          const ChunkAgg* h1 = sub + kNSub + gg;
-          const ChunkAgg* a = h0->ulp_exp == ue ? h0 : (h1->ulp_exp == ue ? h1 : nullptr);
-          if (!a) break;
-          const int P = parity_of(M);
-          if (!(M + (P ? a->Z1 : a->Z0) < capU - 1.0)) break;
+        const int P0 = parity_of(M);
+        bool valid = lane >= g && lane < kNSub;
+        ChunkAgg a{};
+        if (valid) {
+          if (h0.ulp_exp == ue) a = h0;
+          else if (h1.ulp_exp == ue) a = h1;
+          else valid = false;
+        }
+        Tx t = tx_identity();
+        if (valid) {
+          t.d0 = a.R0;
+          t.q0 = parity_of(a.R0);
+          t.d1 = a.R1;
+          t.q1 = 1 ^ parity_of(a.R1);
+        }
+        const Tx ex = warp_excl_tx(t);
+        const double Mi = M + (P0 ? ex.d1 : ex.d0);
+        const int Pi = P0 ? ex.q1 : ex.q0;
+        const bool cert = valid && (Mi + (Pi ? a.Z1 : a.Z0) < capU - 1.0);
+        const unsigned nc = __ballot_sync(0xffffffffu, !cert && lane >= g && lane < kNSub);
+        const int f = nc ? __ffs(nc) - 1 : kNSub;
+        if (lane >= g && lane < f) {
           ChunkStart cs;
-          cs.M = M;
-          cs.parity = P;
+          cs.M = Mi;
+          cs.parity = Pi;
           cs.ulp_exp = ue;
           cs.fast = 1;
           cs.pad = 0;
-          substarts[(size_t)k * kNSub + gg] = cs;
-          M += P ? a->R1 : a->R0;
+          substarts[(size_t)k * kNSub + lane] = cs;
         }
-        s = ldexp(M, ue);
+        if (f > g) S = ldexp(__shfl_sync(0xffffffffu, Mi + (Pi ? a.R1 : a.R0), f - 1), ue);
+        g = f;
       }
-      s_S = s;
-      s_g = gg;
-    }
-    __syncthreads();
-    S = s_S;
-    g = s_g;
-    __syncthreads();
-    if (g < kNSub) {  // the crossing sub-chunk, element-exact (one sequential batch)
-      const long long c0 = (long long)k * kChunk + (long long)g * kSub, c1 = min(n, c0 + kSub);
-      if (threadIdx.x == 0) {
-        ChunkStart cs{};
-        cs.fast = 0;
-        substarts[(size_t)k * kNSub + g] = cs;
-        st[3] += 1;
+      if (g < kNSub) {  // the crossing sub-chunk (or the start of the whole sum), element-exact
+        const long long c0 = base + (long long)g * kSub;
+        if (lane == 0) {
+          ChunkStart cs{};
+          cs.fast = 0;
+          substarts[(size_t)k * kNSub + g] = cs;
+          st[3] += 1;
+        }
+        if (c0 < n) S = warp_seq_segment(xs + g * kSub, c0, (int)(n - c0 < kSub ? n - c0 : kSub), S, out);
+        ++g;
       }
-      if (c0 < n) S = exact_segment(x, c0, c1, S, out, smd, smi, sml, st, true);
-      ++g;
     }
+    if (lane == 0) s_S = S;
   }
-  return S;
+  __syncthreads();
+  return s_S;
 }
 
 __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restrict__ x, long long n,
@@ -774,6 +844,7 @@ __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restr
                                                            int* __restrict__ status, int bad_flag) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  extern __shared__ __align__(16) double xs_dyn[];  // kChunk: a split chunk's elements
   __shared__ ChunkAgg tile[kTile];
   __shared__ Tx stx[kTileWarps];
   __shared__ double smd[32];
@@ -852,7 +923,7 @@ __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restr
           starts[k] = cs;
           st[2] += 1;
         }
-        S = split_walk(x, n, k, S, subagg, substarts, out, smd, smi, sml, st);
+        S = split_walk_warp(x, n, k, S, subagg, substarts, out, xs_dyn, st);
         if (threadIdx.x == 0) st[6] += (unsigned long long)(clock64() - tq0);
       } else {
         if (threadIdx.x == 0) {
@@ -1272,7 +1343,11 @@ static cudaError_t exact_scan(const double* x, long long n, double* out, double*
   if ((e = launch_pdl(chunk_sums_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.csum)) != cudaSuccess) return e;
   if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2)) != cudaSuccess) return e;
   if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg)) != cudaSuccess) return e;
-  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), 0, st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
+  static unsigned long long walk_attr = 0;
+  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(chunk_walk_kernel), kChunk * sizeof(double), walk_attr)) !=
+      cudaSuccess)
+    return e;
+  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), kChunk * sizeof(double), st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
                                          total, status, bad_flag)) != cudaSuccess) return e;
   if (out) {
     if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, out)) != cudaSuccess) return e;
