@@ -899,13 +899,20 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     for (size_t n = 0; n < N; ++n) sample_mode(engs[n], in.x, in.dims, n, amm ? t_flat[n] : 0);
     upload_omegas();
     for (size_t n = 0; n < N; ++n) factors[n] = factor_mode(engs[n], in.x, in.dims, n);
+    // each contraction of the core waits only for its own mode's factor: the first one
+    // (the long int8 / DMMA pass over the tensor) starts as soon as that mode's chain is done,
+    // while the other modes' orthonormalisations finish under it
+    std::vector<cudaEvent_t> mode_done(N);
     for (size_t n = 0; n < N; ++n) {
-      cudaEvent_t done;
-      ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
-      ck(cudaEventRecord(done, ctx->aux_stream(n)), "event");
-      ck(cudaStreamWaitEvent(st, done, 0), "wait");
-      cudaEventDestroy(done);
+      ck(cudaEventCreateWithFlags(&mode_done[n], cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(mode_done[n], ctx->aux_stream(n)), "event");
     }
+    struct EventsGuard {
+      std::vector<cudaEvent_t>& v;
+      ~EventsGuard() {
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+      }
+    } mode_done_guard{mode_done};
     cudaEventDestroy(fork);
     // core_from_factors (tucker.cpp:81-92): ascending factor width, stable
     std::vector<size_t> idx(N);
@@ -924,6 +931,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     for (size_t k = 0; k < idx.size(); ++k) {
       const size_t n = idx[k];
       const bool next1 = k + 1 < idx.size() && idx[k + 1] == 1;
+      ck(cudaStreamWaitEvent(st, mode_done[n], 0), "wait");
       if (qr && k == 0) {  // X x_n (Q U1)^T = P x_n U1^T: read the projected tensor
         std::vector<size_t> pd = cur;
         pd[n] = r.sketch[n];
@@ -979,7 +987,10 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     res->core_dims = cur;
     res->core = work.detach();
   }
-  for (size_t n = 0; n < N; ++n) res->factors[n] = factors[n].detach();
+  for (size_t n = 0; n < N; ++n) {  // copies on the main stream (ordered after every mode's join)
+    factors[n].rebind(st);
+    res->factors[n] = factors[n].detach();
+  }
 
   ck(cudaEventRecord(ev1, st), "event");
   std::vector<int> stat(2 * N);
@@ -1359,7 +1370,10 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   res->core_dims = gdims;
   if (curbuf.get() == nullptr) throw std::runtime_error("sharded run produced no core");
   res->core = curbuf.detach();
-  for (size_t n = 0; n < N; ++n) res->factors[n] = factors[n].detach();
+  for (size_t n = 0; n < N; ++n) {  // copies on the main stream (ordered after every mode's join)
+    factors[n].rebind(st);
+    res->factors[n] = factors[n].detach();
+  }
 
   ck(cudaEventRecord(ev1, st), "event");
   std::vector<int> stat(2 * N);
