@@ -19,6 +19,7 @@
  *   leading_left_singular_vectors (linalg.hpp:41)   ->  lmra_leading_left_singular_vectors
  *   thin_qr             (linalg.hpp:35)             ->  lmra_thin_qr_q
  *   qr_project_extract  (linalg.hpp:43-46)          ->  lmra_qr_project_extract
+ *   load_tensor / save_tensor (tensor_io.hpp:12-13) ->  lmra_tnsr_load / lmra_tnsr_save
  *   gaussian_matrix     (sketching.hpp:69)          ->  lmra_gaussian_matrix
  *   randsample          (sketching.hpp:56)          ->  lmra_randsample
  *   gram_sampling_probabilities (tucker.cpp:110-130)->  lmra_column_sqnorms + lmra_probabilities
@@ -194,6 +195,16 @@ int lmra_qr_project_extract(lmra_context* ctx, const double* c, uint64_t rows, u
 int lmra_sample_columns_device(lmra_context* ctx, const double* w, uint64_t n, int regime,
                                double beta, uint64_t L, uint64_t seed, uint64_t stream,
                                int64_t* idx, double* scales, double* p);
+/* TNSR files (tensor_io.hpp:9-13): "TNSR", u32 version 1, u32 order, u64 dims, float64
+ * values in storage order, little-endian.  Errors carry the reference's messages.
+ * lmra_tnsr_read_header: order and dims (up to max_order of them).
+ * lmra_tnsr_load: the values into dst (LMRA_HOST, or LMRA_DEVICE -- then streamed through
+ * pinned staging, file reads overlapping the copies; ctx gives device and stream).
+ * lmra_tnsr_save: src (host, or device with ctx) written with its dims. */
+int lmra_tnsr_read_header(const char* path, int* order, uint64_t* dims, int max_order);
+int lmra_tnsr_load(lmra_context* ctx, const char* path, double* dst, int dst_location);
+int lmra_tnsr_save(lmra_context* ctx, const char* path, const double* src, int src_location,
+                   const uint64_t* dims, int order);
 /* canonical column squared norms of the mode-n unfolding (tucker.cpp:117-119) */
 int lmra_column_sqnorms(lmra_context* ctx, const double* x, const uint64_t* dims, int order,
                         int mode, double* w);

@@ -5,7 +5,7 @@ from .tucker import (  # noqa: F401
     amm_sample_counts, default_context, gaussian_matrix, nccl_unique_id, parse_algorithm,
     probabilities, rand_sthosvd_amm, rand_sthosvd_power, rand_sthosvd_power_qr, rand_thosvd_amm,
     rand_thosvd_power, rand_thosvd_power_qr,
-    randsample, run_algorithm, run_raw, shard_range, ThreadGroup,
+    randsample, run_algorithm, run_raw, shard_range, ThreadGroup, load_tensor, save_tensor,
 )
 from ._lib import LmraError, LmraInvalidArgument, LIB_PATH  # noqa: F401
 from . import device  # noqa: F401

@@ -97,6 +97,9 @@ def _load():
         "lmra_leading_left_singular_vectors": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64,
                                                          C.c_uint64, vp]),
         "lmra_thin_qr_q": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp]),
+        "lmra_tnsr_read_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), u64p, C.c_int]),
+        "lmra_tnsr_load": (C.c_int, [vp, C.c_char_p, vp, C.c_int]),
+        "lmra_tnsr_save": (C.c_int, [vp, C.c_char_p, vp, C.c_int, u64p, C.c_int]),
         "lmra_qr_project_extract": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp, C.c_uint64,
                                               C.c_uint64, vp]),
         "lmra_column_sqnorms": (C.c_int, [vp, vp, u64p, C.c_int, C.c_int, vp]),
@@ -137,7 +140,8 @@ EXPORTED = [
     "lmra_context_set_trace", "lmra_sample_columns_device",
     "lmra_mode_n_product", "lmra_mode0_product_i8", "lmra_mode1_product_i8",
     "lmra_gram_power_apply", "lmra_leading_left_singular_vectors", "lmra_column_sqnorms",
-    "lmra_thin_qr_q", "lmra_qr_project_extract",
+    "lmra_thin_qr_q", "lmra_qr_project_extract", "lmra_tnsr_read_header", "lmra_tnsr_load",
+    "lmra_tnsr_save",
     "lmra_gaussian_matrix", "lmra_probabilities", "lmra_randsample", "lmra_amm_sample_counts",
     "lmra_gen_tucker_noise", "lmra_gen_hilbert", "lmra_gen_video", "lmra_device_alloc",
     "lmra_device_free", "lmra_memcpy",

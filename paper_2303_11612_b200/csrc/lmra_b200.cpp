@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "host/host_chain.hpp"
+#include "host/tnsr.hpp"
 #include "kernels/kernels.hpp"
 
 using lmra_dev::ModeView;
@@ -1807,6 +1808,41 @@ int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint6
     ck(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     if (st) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  });
+}
+
+int lmra_tnsr_read_header(const char* path, int* order, uint64_t* dims, int max_order) {
+  return guard([&] {
+    const lmra_host::TnsrHeader h = lmra_host::tnsr_read_header(path);
+    *order = (int)h.dims.size();
+    for (int k = 0; k < std::min(max_order, *order); ++k) dims[k] = h.dims[k];
+  });
+}
+
+int lmra_tnsr_load(lmra_context* ctx, const char* path, double* dst, int dst_location) {
+  return guard([&] {
+    if (dst_location == LMRA_HOST) {
+      lmra_host::tnsr_load_host(path, dst);
+      return;
+    }
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard dg(ctx->device);
+    lmra_host::tnsr_load_device(path, dst, ctx->stream);
+  });
+}
+
+int lmra_tnsr_save(lmra_context* ctx, const char* path, const double* src, int src_location,
+                   const uint64_t* dims, int order) {
+  return guard([&] {
+    if (order < 0) throw std::invalid_argument("negative tensor order");
+    std::vector<uint64_t> d(dims, dims + order);
+    if (src_location == LMRA_HOST) {
+      lmra_host::tnsr_save(path, d, src, false, nullptr);
+      return;
+    }
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard dg(ctx->device);
+    lmra_host::tnsr_save(path, d, src, true, ctx->stream);
   });
 }
 

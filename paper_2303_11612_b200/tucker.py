@@ -24,6 +24,7 @@ flattening); device data is passed as DenseTensor.on_device(ptr_or_torch, dims).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -146,6 +147,49 @@ class DenseTensor:
         if self.on_device:
             raise LmraError("device tensor: copy it to the host first")
         return self.data.reshape(self.dims, order="F")
+
+
+def _tnsr_header(path: str) -> List[int]:
+    order = C.c_int()
+    dims = np.zeros(64, dtype=np.uint64)
+    check(lib.lmra_tnsr_read_header(os.fsencode(path), C.byref(order), dims.ctypes.data_as(_lib.u64p), 64))
+    return [int(d) for d in dims[:order.value]]
+
+
+def load_tensor(path: str, device: bool = False, ctx: Optional["Context"] = None) -> DenseTensor:
+    """tensor_io.hpp:13 load_tensor.  device=True streams the values straight into HBM (a
+    float64 CUDA torch tensor owned by the returned DenseTensor)."""
+    dims = _tnsr_header(path)
+    n = int(np.prod(dims)) if dims else 1
+    if not device:
+        out = np.empty(n, dtype=np.float64)
+        check(lib.lmra_tnsr_load(None, os.fsencode(path), out.ctypes.data_as(C.c_void_p), 0))
+        return DenseTensor(dims, out)
+    import torch
+    ctx = ctx or default_context()
+    t = torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}")
+    torch.cuda.current_stream().synchronize()
+    check(lib.lmra_tnsr_load(ctx.handle, os.fsencode(path), C.c_void_p(t.data_ptr()), 1))
+    return DenseTensor(dims, None, t.data_ptr(), owner=t)
+
+
+def save_tensor(path: str, t: DenseTensor, ctx: Optional["Context"] = None) -> None:
+    """tensor_io.hpp:12 save_tensor (host or device tensor)."""
+    dims = np.asarray(t.dims, dtype=np.uint64)
+    if t.on_device:
+        ctx = ctx or default_context()
+        _torch_sync()
+        check(lib.lmra_tnsr_save(ctx.handle, os.fsencode(path), C.c_void_p(t.ptr), 1,
+                                 dims.ctypes.data_as(_lib.u64p), len(t.dims)))
+    else:
+        flat = np.ascontiguousarray(t.data, dtype=np.float64)
+        check(lib.lmra_tnsr_save(None, os.fsencode(path), flat.ctypes.data_as(C.c_void_p), 0,
+                                 dims.ctypes.data_as(_lib.u64p), len(t.dims)))
+
+
+def _torch_sync():
+    import torch
+    torch.cuda.current_stream().synchronize()
 
 
 @dataclass
