@@ -24,9 +24,18 @@ inline void note_launch() { ++g_kernel_launches; }
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 void scratch_free(void* p, cudaStream_t st);
 
+// Gathered columns for the power scheme on sampled columns (mode-0 views only): column j of
+// the view is x column idx[j] (< 0: a zero column) scaled by scale[j] -- C' of
+// sample_columns (sketching.cpp:133-141) without materialising it.  The TTM then writes
+// h_j = scale_j^2 (x_idx[j]^T b) and the Gram sums x_idx[j] h_j^T, i.e. C' C'^T b.
+struct Gather {
+  const long long* idx = nullptr;
+  const double* scale = nullptr;
+};
+
 // Y = X x_mode B, with B given transposed: bt[r + I*k] = B[k, r] (I x m column-major).
 cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
-                       cudaStream_t st);
+                       cudaStream_t st, Gather ga = Gather{});
 
 struct GramPlan {
   int nsplit = 1;
@@ -35,7 +44,7 @@ struct GramPlan {
 GramPlan plan_gram(ModeView v, int num_sms);
 // z (I x s, column-major) = sum_j X(:, j) H(:, j)^T; zpart holds nsplit * I * s doubles.
 cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, double* zpart,
-                        const GramPlan& plan, double* z, cudaStream_t st);
+                        const GramPlan& plan, double* z, cudaStream_t st, Gather ga = Gather{});
 
 // C' = A_(n)(:, idx) * diag(scale), I x T column-major.
 cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, const double* scale,

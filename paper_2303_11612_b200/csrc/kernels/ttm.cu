@@ -38,7 +38,7 @@ struct TtmCfg {
 template <int M8, bool RCONTIG, int KC_, int ST_>
 __global__ void __launch_bounds__(kThreads, 2)
     ttm_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ bt, int m,
-               int mtot, int koff, double* __restrict__ y, long long kper) {
+               int mtot, int koff, double* __restrict__ y, long long kper, Gather ga) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   using C = TtmCfg<M8, RCONTIG, KC_, ST_>;
@@ -70,6 +70,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     jbase = jvalid ? col_base(j, v.inner, v.I) : 0;
   }
 
+  // gathered columns (mode-0 views only): column j of X is x column ga.idx[j] (< 0: zero,
+  // another rank's column); this thread's columns are fixed over the K loop
+  constexpr int NQ = RCONTIG ? (C::JT * C::KC / 2) / kThreads : 1;
+  long long gcol[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const long long j = j0 + (tid + q * kThreads) / (C::KC / 2);
+    gcol[q] = j < J ? (ga.idx ? __ldg(ga.idx + j) : j) : -1;
+  }
+
   auto load = [&](int stage, int kt) {
     double* As = smem + stage * C::STAGE_ELEMS;
     double* Bs = As + C::A_ELEMS;
@@ -87,9 +97,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int q = 0; q < (C::JT * C::KC / 2) / kThreads; ++q) {
           int e = tid + q * kThreads;
           int rp = e % (C::KC / 2), jj = e / (C::KC / 2);
-          long long j = j0 + jj, r = k0 + 2 * rp;
-          bool ok = (j < J) && (r < I);
-          cp_async16(As + jj * C::LDA + 2 * rp, ok ? x + v.I * j + r : x, ok);
+          long long r = k0 + 2 * rp;
+          bool ok = (gcol[q] >= 0) && (r < I);
+          cp_async16(As + jj * C::LDA + 2 * rp, ok ? x + v.I * gcol[q] + r : x, ok);
         }
       } else {
 #pragma unroll
@@ -97,8 +107,9 @@ __global__ void __launch_bounds__(kThreads, 2)
           int e = tid + q * kThreads;
           int rl = e % C::KC, jj = e / C::KC;
           long long j = j0 + jj, r = k0 + rl;
-          bool ok = (j < J) && (r < I);
-          cp_async8(As + jj * C::LDA + rl, ok ? x + v.I * j + r : x, ok);
+          const long long cj = j < J ? (ga.idx ? __ldg(ga.idx + j) : j) : -1;
+          bool ok = (cj >= 0) && (r < I);
+          cp_async8(As + jj * C::LDA + rl, ok ? x + v.I * cj + r : x, ok);
         }
       }
     } else {  // X(r, j) = x[base_j + inner*r]  ->  As[r][j]
@@ -175,11 +186,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       ybase = i + v.inner * ((long long)mtot * o + koff);
       ystride = v.inner;
     }
+    // gathered: h_t = scale_t^2 (a_t^T c), so that the Gram pass sums a_t h_t^T
+    // (= C' C'^T c with C'(:, t) = scale_t a_t, sketching.cpp:133-141, never materialised)
+    double sc2 = 1.0;
+    if (ga.scale) {
+      const double sc = ga.scale[j];
+      sc2 = sc * sc;
+    }
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int k = f * 8 + 2 * t;
-      if (k < m) y[ybase + ystride * k] = acc[f][2 * half];
-      if (k + 1 < m) y[ybase + ystride * (k + 1)] = acc[f][2 * half + 1];
+      if (k < m) y[ybase + ystride * k] = ga.scale ? acc[f][2 * half] * sc2 : acc[f][2 * half];
+      if (k + 1 < m) y[ybase + ystride * (k + 1)] = ga.scale ? acc[f][2 * half + 1] * sc2 : acc[f][2 * half + 1];
     }
   }
 }
@@ -204,7 +222,7 @@ struct GramCfg {
 template <int M8, bool RCONTIG>
 __global__ void __launch_bounds__(kGramThreads)
     gram_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ h, int s,
-                int stot, int koff, double* __restrict__ zpart, long long jper) {
+                int stot, int koff, double* __restrict__ zpart, long long jper, Gather ga) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   using C = GramCfg<M8, RCONTIG>;
@@ -226,8 +244,9 @@ __global__ void __launch_bounds__(kGramThreads)
         int e = tid + q * kGramThreads;
         int rl = e % C::RT, jl = e / C::RT;
         long long j = jc0 + jl, r = r0 + rl;
-        bool ok = (j < jend) && (r < I);
-        cp_async8(As + jl * C::LDA + rl, ok ? x + I * j + r : x, ok);
+        const long long cj = j < jend ? (ga.idx ? __ldg(ga.idx + j) : j) : -1;
+        bool ok = (cj >= 0) && (r < I);
+        cp_async8(As + jl * C::LDA + rl, ok ? x + I * cj + r : x, ok);
       }
       for (int e = tid; e < C::JC * M8; e += kGramThreads) {
         int k = e % M8, jl = e / M8;
@@ -398,7 +417,7 @@ __global__ void pack_b_kernel(const double* __restrict__ bt, long long I, int m,
 template <int M8, bool RC>
 static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_colmajor, int m,
                                 int mtot, int koff, double* y, int ksplit, long long kper,
-                                cudaStream_t st) {
+                                cudaStream_t st, Gather ga) {
   double* bt = nullptr;  // packed copy, stream-ordered scratch
   cudaError_t pe = scratch_alloc(reinterpret_cast<void**>(&bt), sizeof(double) * v.I * M8, st);
   if (pe != cudaSuccess) return pe;
@@ -423,7 +442,7 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
     long long J = v.inner * v.outer;
     dim3 grid((unsigned)((J + C::JT - 1) / C::JT), (unsigned)ksplit);
     {
-    const cudaError_t le = launch_pdl(ttm_kernel<M8, RC, KC, ST>, dim3(grid), dim3(kThreads), C::SMEM, st, x, v, bt, m, mtot, koff, y, kper);
+    const cudaError_t le = launch_pdl(ttm_kernel<M8, RC, KC, ST>, dim3(grid), dim3(kThreads), C::SMEM, st, x, v, bt, m, mtot, koff, y, kper, ga);
     if (le != cudaSuccess) return le;
   }
     return cudaGetLastError();
@@ -433,16 +452,16 @@ static cudaError_t launch_ttm_t(const double* x, ModeView v, const double* bt_co
 
 template <bool RC>
 static cudaError_t launch_ttm_rc(const double* x, ModeView v, const double* bt, int m, int mtot,
-                                 int koff, double* y, int ks, long long kper, cudaStream_t st) {
+                                 int koff, double* y, int ks, long long kper, cudaStream_t st, Gather ga) {
   switch ((m + 7) / 8) {
-    case 1: return launch_ttm_t<8, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 2: return launch_ttm_t<16, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 3: return launch_ttm_t<24, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 4: return launch_ttm_t<32, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 5: return launch_ttm_t<40, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 6: return launch_ttm_t<48, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 7: return launch_ttm_t<56, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
-    case 8: return launch_ttm_t<64, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st);
+    case 1: return launch_ttm_t<8, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 2: return launch_ttm_t<16, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 3: return launch_ttm_t<24, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 4: return launch_ttm_t<32, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 5: return launch_ttm_t<40, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 6: return launch_ttm_t<48, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 7: return launch_ttm_t<56, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
+    case 8: return launch_ttm_t<64, RC>(x, v, bt, m, mtot, koff, y, ks, kper, st, ga);
   }
   return cudaErrorInvalidValue;
 }
@@ -459,7 +478,8 @@ static int device_sms() {
 }
 
 cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
-                       cudaStream_t st) {
+                       cudaStream_t st, Gather ga) {
+  if (ga.idx && v.inner != 1) return cudaErrorInvalidValue;  // gathered: mode-0 views only
   if (m < 1) return cudaErrorInvalidValue;
   const long long J = v.inner * v.outer;
   if (J == 0) return cudaSuccess;
@@ -496,8 +516,8 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
   for (int k0 = 0; k0 < m && e == cudaSuccess; k0 += kMaxWidth) {
     int mb = std::min(kMaxWidth, m - k0);
     const double* btb = bt + (size_t)v.I * k0;
-    e = v.inner == 1 ? launch_ttm_rc<true>(x, v, btb, mb, m, k0, part, ks, kper, st)
-                     : launch_ttm_rc<false>(x, v, btb, mb, m, k0, part, ks, kper, st);
+    e = v.inner == 1 ? launch_ttm_rc<true>(x, v, btb, mb, m, k0, part, ks, kper, st, ga)
+                     : launch_ttm_rc<false>(x, v, btb, mb, m, k0, part, ks, kper, st, ga);
   }
   if (ks > 1) {
     if (e == cudaSuccess) {
@@ -516,7 +536,7 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
 template <int M8, bool RC>
 static cudaError_t launch_gram_t(const double* x, ModeView v, const double* h, int s, int stot,
                                  int koff, double* zpart, int nsplit, long long jper,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, Gather ga) {
   using C = GramCfg<M8, RC>;
   static unsigned long long attr_done = 0;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_kernel<M8, RC>), C::SMEM,
@@ -524,7 +544,7 @@ static cudaError_t launch_gram_t(const double* x, ModeView v, const double* h, i
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((v.I + C::RT - 1) / C::RT), (unsigned)nsplit);
   {
-    const cudaError_t le = launch_pdl(gram_kernel<M8, RC>, dim3(grid), dim3(kGramThreads), C::SMEM, st, x, v, h, s, stot, koff, zpart, jper);
+    const cudaError_t le = launch_pdl(gram_kernel<M8, RC>, dim3(grid), dim3(kGramThreads), C::SMEM, st, x, v, h, s, stot, koff, zpart, jper, ga);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
@@ -533,16 +553,16 @@ static cudaError_t launch_gram_t(const double* x, ModeView v, const double* h, i
 template <bool RC>
 static cudaError_t launch_gram_rc(const double* x, ModeView v, const double* h, int s, int stot,
                                   int koff, double* zpart, int nsplit, long long jper,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, Gather ga) {
   switch ((s + 7) / 8) {
-    case 1: return launch_gram_t<8, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 2: return launch_gram_t<16, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 3: return launch_gram_t<24, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 4: return launch_gram_t<32, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 5: return launch_gram_t<40, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 6: return launch_gram_t<48, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 7: return launch_gram_t<56, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
-    case 8: return launch_gram_t<64, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st);
+    case 1: return launch_gram_t<8, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 2: return launch_gram_t<16, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 3: return launch_gram_t<24, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 4: return launch_gram_t<32, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 5: return launch_gram_t<40, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 6: return launch_gram_t<48, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 7: return launch_gram_t<56, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
+    case 8: return launch_gram_t<64, RC>(x, v, h, s, stot, koff, zpart, nsplit, jper, st, ga);
   }
   return cudaErrorInvalidValue;
 }
@@ -565,14 +585,15 @@ GramPlan plan_gram(ModeView v, int num_sms) {
 }
 
 cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, double* zpart,
-                        const GramPlan& plan, double* z, cudaStream_t st) {
+                        const GramPlan& plan, double* z, cudaStream_t st, Gather ga) {
   if (s < 1) return cudaErrorInvalidValue;
+  if (ga.idx && v.inner != 1) return cudaErrorInvalidValue;
   for (int k0 = 0; k0 < s; k0 += kMaxWidth) {
     int sb = std::min(kMaxWidth, s - k0);
     cudaError_t e =
         v.inner == 1
-            ? launch_gram_rc<true>(x, v, h, sb, s, k0, zpart, plan.nsplit, plan.jper, st)
-            : launch_gram_rc<false>(x, v, h, sb, s, k0, zpart, plan.nsplit, plan.jper, st);
+            ? launch_gram_rc<true>(x, v, h, sb, s, k0, zpart, plan.nsplit, plan.jper, st, ga)
+            : launch_gram_rc<false>(x, v, h, sb, s, k0, zpart, plan.nsplit, plan.jper, st, ga);
     if (e != cudaSuccess) return e;
   }
   long long n = v.I * s;

@@ -401,6 +401,13 @@ class DevBuf {
   bool arena_ = false;
 };
 
+// sampled matrices of at least this many elements are read in place by the power scheme
+// (Gather) instead of being materialised; LMRA_FUSED_GATHER_MIN overrides (tests force it)
+size_t fused_gather_min() {
+  const char* e = getenv("LMRA_FUSED_GATHER_MIN");
+  return e ? (size_t)strtoull(e, nullptr, 10) : (size_t(1) << 22);
+}
+
 ModeView view_of(const std::vector<size_t>& dims, size_t mode) {
   ModeView v;
   v.inner = 1;
@@ -559,17 +566,19 @@ class Engine {
     return y;
   }
 
-  // c = (A A^T)^q G on the mode-`mode` unfolding view of a; c (I x s) in/out
-  void gram_power(const double* a, ModeView v, DevBuf& c, size_t s, int q, int strategy) {
+  // c = (A A^T)^q G on the mode-`mode` unfolding view of a; c (I x s) in/out.  ga: A is the
+  // gathered, scaled columns of a (AMM, Strategy A only), read in place
+  void gram_power(const double* a, ModeView v, DevBuf& c, size_t s, int q, int strategy,
+                  lmra_dev::Gather ga = lmra_dev::Gather{}) {
     const size_t I = (size_t)v.I, J = (size_t)(v.inner * v.outer);
     lmra_dev::GramPlan plan = lmra_dev::plan_gram(v, ctx_->num_sms);
     if (strategy == 0) {  // linalg.cpp:70-74, Strategy A
       DevBuf h(J * s, st_);
       DevBuf zpart((size_t)plan.nsplit * I * s, st_);
       for (int k = 0; k < q; ++k) {
-        launch("power_half", [&] { return lmra_dev::launch_ttm(a, v, c.get(), (int)s, h.get(), st_); });
+        launch("power_half", [&] { return lmra_dev::launch_ttm(a, v, c.get(), (int)s, h.get(), st_, ga); });
         launch("power_gram", [&] {
-          return lmra_dev::launch_gram(a, v, h.get(), (int)s, zpart.get(), plan, c.get(), st_);
+          return lmra_dev::launch_gram(a, v, h.get(), (int)s, zpart.get(), plan, c.get(), st_, ga);
         });
       }
     } else {  // linalg.cpp:76-77, Strategy B: gram = A A^T once, then c = gram * c
@@ -842,6 +851,13 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     c.rebind(s_);
     if (!amm) {
       e.gram_power(x, v, c, s, cfg.power, cfg.strategy);
+    } else if (v.inner == 1 && cfg.strategy == 0 && I * n_draws[n] >= fused_gather_min()) {
+      // large sampled matrix of contiguous fibres (cfg5 mode 0: 512 x 157287, 644 MB): the
+      // power scheme reads the sampled columns in place instead of materialising C'
+      // (saves C's write and one of its two reads per power step)
+      const size_t T = n_draws[n];
+      const lmra_dev::Gather ga{reinterpret_cast<const long long*>(d_idx[n].get()), d_sc[n].get()};
+      e.gram_power(x, ModeView{1, (long long)I, (long long)T}, c, s, cfg.power, cfg.strategy, ga);
     } else {
       const size_t T = n_draws[n];
       DevBuf cp(I * T, s_);

@@ -244,3 +244,21 @@ def test_oversized_rank_clamped(gpu_ctx, lmra):
     x = lmra.DenseTensor.from_flat(np.random.default_rng(43).standard_normal(120), [6, 5, 4])
     d = lmra.run_algorithm("alg1", x, lmra.AlgoConfig(rank=[10, 10, 10]))
     assert list(d.core.shape) == [6, 5, 4]
+
+
+@pytest.mark.parametrize("alg", ["alg4", "alg5"])
+@pytest.mark.parametrize("regime", ["uniform", "nearly_optimal"])
+def test_power_on_sampled_columns_in_place(gpu_ctx, lmra, orc, alg, regime, monkeypatch):
+    # the power scheme reading the sampled columns in place (Gather: C' = A_(0)(:, idx) diag(scale)
+    # never materialised; used for large C' such as cfg5's mode 0) -- forced at small size
+    monkeypatch.setenv("LMRA_FUSED_GATHER_MIN", "1")
+    dims = [40, 30, 20]
+    x = orc.gen_tucker_noise(dims, [5, 4, 3], 1e-2, 9)
+    kw = dict(rank=[5, 4, 3], seed=7, regime=regime, power=2, t_samples=[300, 200, 150])
+    cg, co = _cfgs(lmra, orc, **kw)
+    ref = orc.run(alg, x, dims, co)
+    t = lmra.DenseTensor.from_flat(x, dims)
+    own = lmra.run_algorithm(alg, t, cg)
+    check_own_draws(alg, own, ref, regime)
+    gpu = lmra.run_algorithm(alg, t, cg, omega=ref.omega, samples=ref.samples)
+    compare(gpu, ref, x.reshape(dims, order="F"))
