@@ -207,10 +207,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 // layout with width s.  CTA tile: 64 rows r (4 warps x 16) x all k, K = j in chunks of 16.
 // ----------------------------------------------------------------------------
 constexpr int kGramThreads = 128;
+#ifndef LMRA_GRAM_STAGES
+#define LMRA_GRAM_STAGES 3
+#endif
 
 template <int M8, bool RCONTIG>
 struct GramCfg {
-  static constexpr int RT = 64, JC = 16, STAGES = 4;
+  static constexpr int RT = 64, JC = 16, STAGES = LMRA_GRAM_STAGES;
   static constexpr int LDA = RCONTIG ? conflict_free_ld(RT) : conflict_free_ld(JC);
   static constexpr int A_ELEMS = RCONTIG ? JC * LDA : RT * LDA;
   static constexpr int LDH = conflict_free_ld(M8);
