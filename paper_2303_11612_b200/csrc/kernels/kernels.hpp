@@ -61,7 +61,7 @@ cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long
 // The reference's sampling chain on the device, bit-exact (sampler.cu):
 // probabilities from squared column norms w (regime 0 optimal, 1 nearly-optimal, 2 uniform)
 // then L multinomial draws from PCG32 stream (seed, stream): idx (int64), scales, p (n).
-// status bits: 1 bad weight, 2 zero normaliser, 4 sum != 1, 8 zero total, 16 fallback,
+// status bits: 1 bad weight, 2 zero normaliser, 4 sum != 1, 8 zero total, 16 fallback, 64 internal,
 // 32 bad beta.
 size_t sampler_workspace_doubles(long long n);
 void sampler_walk_stats(unsigned long long* out2, bool reset);  // diagnostics

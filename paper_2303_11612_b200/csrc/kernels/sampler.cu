@@ -55,6 +55,7 @@ enum SamplerStatus {
   kZeroAcc = 8,        // cum total <= 0          -> "randsample: all-zero distribution"
   kFallback = 16,      // informational: sequential Neumaier fallback was used
   kBadBeta = 32,       // nearly-optimal beta outside (0, 1] (checked only when total > 0)
+  kInternal = 64,      // uniform closed form: segment table overflow (unreachable)
 };
 
 // ---------------------------------------------------------------- parity maps
@@ -1315,6 +1316,121 @@ __global__ void draw_kernel(const double* __restrict__ cum, const double* __rest
   }
 }
 
+// ---------------------------------------------------------------- uniform(n): closed form
+// For p = uniform(n) (every p_i = v = 1.0 / n, sketching.cpp:50-53) the reference's cumulative
+// sum cum_i = fl(cum_{i-1} + v) (sketching.cpp:99-104) is an arithmetic progression inside a
+// binade: with u the binade's ulp and y = v / u (exact), every in-binade step adds the same
+// integer r = round(y) ulps -- for a tie (frac y = 1/2) the first step lands on an even
+// multiple and every later step adds the even choice q + (q odd), q = floor(y).  So the whole
+// prefix is a list of segments (i0, M, r, ue, K): cum_{i0 + k} = (M + k r) 2^ue for k <= K,
+// joined by single steps evaluated with an IEEE add (the first step in a binade and every
+// binade crossing).  Thread 0 of each CTA builds the list in O(#binades); the draws
+// (upper_bound, sketching.cpp:122-127) binary-search it.  Replaces the n-element exact scan
+// and the n-element prefix array for the uniform regime.
+struct USeg {
+  long long i0, K;  // first index, further in-binade steps (K = 0: a single value)
+  double M, r;      // value at i0 = M 2^ue, step r ulps
+  int ue, pad;
+};
+constexpr int kUSegMax = 512;  // cum climbs from 1/n to ~1: <= 64 binades, <= 2 segments each
+constexpr int kUThreads = 128;
+
+__device__ __forceinline__ double useg_value(const USeg& g, long long k) { return ldexp(g.M + (double)k * g.r, g.ue); }
+
+// builds the segment list (thread 0); returns the count, or -1 if it would overflow
+__device__ int uniform_segments(long long n, double v, USeg* segs) {
+  long long i = 0;
+  double S = v;  // cum_0 = 0 + v
+  int cnt = 0;
+  while (true) {  // S = cum_i exactly
+    if (cnt >= kUSegMax) return -1;
+    int ue, be;
+    binade_of(S, ue, be);
+    const double M = ldexp(S, -ue), capU = ldexp(1.0, be - ue), y = ldexp(v, -ue);
+    const double fy = floor(y), fr = y - fy;
+    const bool tie = fr == 0.5;
+    // in-binade step: non-tie r = round(y); tie from an even multiple: the even choice
+    const double r = tie ? fy + (double)parity_of(fy) : (fr > 0.5 ? fy + 1.0 : fy);
+    const double cstar = fr >= 0.5 ? fy + 1.0 : fy;  // a step from M' crosses iff capU - M' <= cstar
+    long long K = 0;
+    if (!(tie && parity_of(M))) {  // (an odd start under a tie takes one IEEE step first)
+      const double N = capU - M - cstar;          // the step from M + k r stays inside iff k r < N
+      if (N > 0.0) {
+        if (r == 0.0) {
+          K = n - 1 - i;  // stagnation: v below half an ulp
+        } else {
+          double k = ceil(N / r);
+          while (k > 1.0 && (k - 1.0) * r >= N) k -= 1.0;
+          while (k * r < N) k += 1.0;
+          K = (long long)k;
+        }
+      }
+      K = min(K, n - 1 - i);
+    }
+    segs[cnt++] = USeg{i, K, M, r, ue, 0};
+    i += K;
+    if (i >= n - 1) break;
+    S = __dadd_rn(useg_value(segs[cnt - 1], K), v);  // binade crossing (or tie start): IEEE step
+    ++i;
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(kUThreads) uniform_draw_kernel(long long n, long long L, unsigned long long seed,
+                                                                 unsigned long long stream, long long* __restrict__ idx,
+                                                                 double* __restrict__ scales, int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) unsigned char usm[];
+  USeg* segs = reinterpret_cast<USeg*>(usm);
+  __shared__ int s_cnt;
+  const double v = __ddiv_rn(1.0, (double)n);
+  if (threadIdx.x == 0) s_cnt = uniform_segments(n, v, segs);
+  __syncthreads();
+  const int cnt = s_cnt;
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cnt < 0) {  // cannot happen for n < 2^63 (see kUSegMax); surfaced, never silent
+    if (j == 0) atomicOr(status, kInternal);
+    return;
+  }
+  if (j >= L) return;
+  const USeg& lastg = segs[cnt - 1];
+  const double acc = useg_value(lastg, lastg.K);  // cum_{n-1}
+  const double scale_base = __ddiv_rn(1.0, __dsqrt_rn((double)L));
+  Pcg32 g(seed, stream);
+  g.advance(2ull * (unsigned long long)j);
+  const unsigned long long hi = g.next(), lo = g.next();
+  const double u = __dmul_rn((double)(((hi << 32) | lo) >> 11) * 0x1.0p-53, acc);
+  // first segment whose last value exceeds u
+  int a = 0, b = cnt;
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if (useg_value(segs[mid], segs[mid].K) > u)
+      b = mid;
+    else
+      a = mid + 1;
+  }
+  long long id;
+  if (a == cnt) {
+    id = n - 1;  // "last": every uniform weight is positive
+  } else {
+    const USeg& sg = segs[a];
+    long long k = 0;
+    if (sg.K > 0 && sg.r > 0.0) {  // first k with M + k r > w  (w = u / 2^ue, exact)
+      const double w = ldexp(u, -sg.ue);
+      double kk = floor((w - sg.M) / sg.r) + 1.0;
+      if (kk < 0.0) kk = 0.0;
+      if (kk > (double)sg.K) kk = (double)sg.K;
+      while (kk > 0.0 && sg.M + (kk - 1.0) * sg.r > w) kk -= 1.0;
+      while (kk < (double)sg.K && !(sg.M + kk * sg.r > w)) kk += 1.0;
+      k = (long long)kk;
+    }
+    id = sg.i0 + k;
+  }
+  idx[j] = id;
+  scales[j] = __ddiv_rn(scale_base, __dsqrt_rn(v));
+}
+
 // ---------------------------------------------------------------- orchestration
 static int nchunks_of(long long n) { return (int)((n + kChunk - 1) / kChunk); }
 
@@ -1381,6 +1497,18 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   cudaError_t e;
   if (regime == 2) {  // uniform(n): p = 1/n each (sketching.cpp:50-53)
     if ((e = launch_pdl(fill_kernel, dim3(eg), dim3(256), 0, st, p, n, 1.0 / (double)n)) != cudaSuccess) return e;
+    static const bool closed_form = !(getenv("LMRA_UNIFORM_SCAN") && getenv("LMRA_UNIFORM_SCAN")[0] == '1');
+    if (closed_form) {
+      // ctor check (never fails for uniform: n fl(1/n) = 1 + O(u)) and "last", then the
+      // closed-form cumulative sum and draws -- no n-element scan
+      if ((e = launch_pdl(check_last_kernel, dim3(nc), dim3(kThr), 0, st, p, n, cpart, lastpos)) != cudaSuccess) return e;
+      if ((e = launch_pdl(check_final_kernel, dim3(1), dim3(kRedThr), 0, st, cpart, lastpos, nc, last, status)) != cudaSuccess) return e;
+      static unsigned long long uattr = 0;
+      const size_t usmem = sizeof(USeg) * kUSegMax;
+      if ((e = ensure_smem_attr(reinterpret_cast<const void*>(uniform_draw_kernel), usmem, uattr)) != cudaSuccess) return e;
+      return launch_pdl(uniform_draw_kernel, dim3((unsigned)((L + kUThreads - 1) / kUThreads)), dim3(kUThreads), usmem, st,
+                        n, L, seed, stream, idx, scales, status);
+    }
   } else {
     // total = naive sum of w; x1 = w / total (+ beta mix); s = Neumaier(x1); p = x1 / s
     if ((e = exact_scan(w, n, nullptr, scal + 0, status, kBadWeight, b, st)) != cudaSuccess) return e;

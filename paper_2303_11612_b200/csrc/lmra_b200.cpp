@@ -1049,6 +1049,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     if (f & 4) throw std::invalid_argument("probability weights must sum to one");
     if (f & 8) throw std::invalid_argument("randsample: all-zero distribution");
     if (f & 16) ++res->sampler_fallbacks;
+    if (f & 64) throw std::runtime_error("sampler: uniform segment table overflow");
   }
   for (size_t n = 0; n < N; ++n)
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
@@ -1421,6 +1422,7 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     if (f & 4) throw std::invalid_argument("probability weights must sum to one");
     if (f & 8) throw std::invalid_argument("randsample: all-zero distribution");
     if (f & 16) ++res->sampler_fallbacks;
+    if (f & 64) throw std::runtime_error("sampler: uniform segment table overflow");
   }
   for (size_t n = 0; n < N; ++n)
     if (stat[n] != 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");

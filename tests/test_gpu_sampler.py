@@ -65,3 +65,24 @@ def test_sampler_error_surface(gpu_ctx, lmra):
     z = torch.zeros(10, dtype=torch.float64, device="cuda")
     idx, sc, p = device.sample_columns(z, "optimal", 0.5, 5, 1, 1, ctx=gpu_ctx)
     assert np.all(p.cpu().numpy() == 0.1)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 10, 100, 1000, 4096, 4097, 65535, 65536, 99991, 786432,
+                               1_000_000, 1_048_576, 3_000_001])
+def test_uniform_closed_form_bit_exact(gpu_ctx, orc, n):
+    # uniform(n): the cumulative sum as binade segments of an arithmetic progression (no scan);
+    # indices and scales against the oracle's sequential cum + upper_bound, many draws so the
+    # draws land in every segment, including the crossing steps
+    import torch
+    from paper_2303_11612_b200 import device
+    L = 50_000
+    p_ref = np.full(n, 1.0 / n)
+    for seed, stream in ((7, 13), (1, 4)):
+        idx_ref, sc_ref = orc.randsample(L, p_ref, seed, stream)
+        w = torch.ones(n, dtype=torch.float64, device="cuda")
+        idx, sc, p = device.sample_columns(w, "uniform", 0.5, L, seed, stream, ctx=gpu_ctx)
+        assert np.array_equal(p.cpu().numpy(), p_ref)
+        got = idx.cpu().numpy()
+        bad = np.flatnonzero(got != idx_ref)
+        assert bad.size == 0, f"n={n}: {bad.size} indices differ, first {bad[:3]}: {got[bad[:3]]} vs {idx_ref[bad[:3]]}"
+        assert np.array_equal(sc.cpu().numpy(), sc_ref)
