@@ -3,7 +3,8 @@
 //
 // Same names, argument meaning and exception surface as the reference:
 //   rand_thosvd_power / rand_sthosvd_power / rand_thosvd_amm / rand_sthosvd_amm,
-//   run_algorithm, amm_sample_counts, AlgoConfig, MultilinearRank, TuckerDecomposition.
+//   rand_thosvd_power_qr / rand_sthosvd_power_qr, run_algorithm, amm_sample_counts,
+//   AlgoConfig, MultilinearRank, TuckerDecomposition; load_tensor / save_tensor (TNSR).
 // std::invalid_argument / std::runtime_error are re-thrown from the ABI status codes.
 //
 // Deviation: Eigen3 is not a dependency, so TuckerDecomposition::factors is a
@@ -229,6 +230,25 @@ inline std::vector<std::size_t> amm_sample_counts(const std::vector<std::size_t>
   std::vector<uint64_t> d(dims.begin(), dims.end()), out(dims.size());
   detail::check(lmra_amm_sample_counts(d.data(), (int)d.size(), &cc.c, sequential ? 1 : 0, out.data()));
   return std::vector<std::size_t>(out.begin(), out.end());
+}
+
+// tensor_io.hpp:12-13 -- TNSR files (host tensors; lmra_tnsr_load with LMRA_DEVICE streams a
+// file straight into HBM instead)
+inline void save_tensor(const std::string& path, const DenseTensor& t) {
+  std::vector<uint64_t> d(t.dims().begin(), t.dims().end());
+  detail::check(lmra_tnsr_save(nullptr, path.c_str(), t.data(), LMRA_HOST, d.data(), (int)d.size()));
+}
+inline DenseTensor load_tensor(const std::string& path) {
+  int order = 0;
+  std::vector<uint64_t> d(64);
+  detail::check(lmra_tnsr_read_header(path.c_str(), &order, d.data(), (int)d.size()));
+  if (order > (int)d.size()) {
+    d.resize((size_t)order);
+    detail::check(lmra_tnsr_read_header(path.c_str(), &order, d.data(), order));
+  }
+  DenseTensor t(std::vector<std::size_t>(d.begin(), d.begin() + order));
+  detail::check(lmra_tnsr_load(nullptr, path.c_str(), t.data(), LMRA_HOST));
+  return t;
 }
 
 }  // namespace lmra

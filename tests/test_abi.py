@@ -54,7 +54,13 @@ def test_cpp_dropin_header_compiles_and_links(tmp_path):
         "int main() {\n"
         "  lmra::AlgoConfig cfg; cfg.rank = lmra::MultilinearRank({2, 2, 2});\n"
         "  auto c = lmra::amm_sample_counts({6, 6, 6}, cfg, true);\n"
-        "  return c.size() == 3 ? 0 : 1;\n"
+        "  if (c.size() != 3) return 1;\n"
+        "  lmra::DenseTensor t({2, 3}, {1, 2, 3, 4, 5, 6.5});\n"
+        f"  lmra::save_tensor(\"{tmp_path}/t.tnsr\", t);\n"
+        f"  lmra::DenseTensor u = lmra::load_tensor(\"{tmp_path}/t.tnsr\");\n"
+        "  if (u.dims() != t.dims() || u.data()[5] != 6.5) return 2;\n"
+        "  try { lmra::load_tensor(\"/nonexistent.tnsr\"); return 3; }\n"
+        "  catch (const std::runtime_error& e) { return std::string(e.what()).find(\"cannot open\") == 0 ? 0 : 4; }\n"
         "}\n")
     exe = tmp_path / "use"
     lib_dir = os.path.join(ROOT, "paper_2303_11612_b200", "lib")
