@@ -236,20 +236,33 @@ __global__ void __launch_bounds__(kGramThreads)
   const long long jbeg = (long long)blockIdx.y * jper;
   const long long jend = min(J, jbeg + jper);
   const int nk = (int)((jend - jbeg + C::JC - 1) / C::JC);
+  const bool vec16 = RCONTIG && (I % 2 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 
   auto load = [&](int stage, int kt) {
     double* As = smem + stage * C::STAGE_ELEMS;
     double* Hs = As + C::A_ELEMS;
     const long long jc0 = jbeg + (long long)kt * C::JC;
     if (RCONTIG) {  // X(r, j) = x[I*j + r] -> As[j][r]
+      if (vec16) {  // row pairs: 16-byte copies (half the LSU work of 8-byte ones)
 #pragma unroll
-      for (int q = 0; q < (C::RT * C::JC) / kGramThreads; ++q) {
-        int e = tid + q * kGramThreads;
-        int rl = e % C::RT, jl = e / C::RT;
-        long long j = jc0 + jl, r = r0 + rl;
-        const long long cj = j < jend ? (ga.idx ? __ldg(ga.idx + j) : j) : -1;
-        bool ok = (cj >= 0) && (r < I);
-        cp_async8(As + jl * C::LDA + rl, ok ? x + I * cj + r : x, ok);
+        for (int q = 0; q < (C::RT / 2 * C::JC) / kGramThreads; ++q) {
+          int e = tid + q * kGramThreads;
+          int rp = e % (C::RT / 2), jl = e / (C::RT / 2);
+          long long j = jc0 + jl, r = r0 + 2 * rp;
+          const long long cj = j < jend ? (ga.idx ? __ldg(ga.idx + j) : j) : -1;
+          bool ok = (cj >= 0) && (r < I);
+          cp_async16(As + jl * C::LDA + 2 * rp, ok ? x + I * cj + r : x, ok);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < (C::RT * C::JC) / kGramThreads; ++q) {
+          int e = tid + q * kGramThreads;
+          int rl = e % C::RT, jl = e / C::RT;
+          long long j = jc0 + jl, r = r0 + rl;
+          const long long cj = j < jend ? (ga.idx ? __ldg(ga.idx + j) : j) : -1;
+          bool ok = (cj >= 0) && (r < I);
+          cp_async8(As + jl * C::LDA + rl, ok ? x + I * cj + r : x, ok);
+        }
       }
       for (int e = tid; e < C::JC * M8; e += kGramThreads) {
         int k = e % M8, jl = e / M8;
