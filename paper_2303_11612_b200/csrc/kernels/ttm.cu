@@ -210,10 +210,17 @@ constexpr int kGramThreads = 128;
 #ifndef LMRA_GRAM_STAGES
 #define LMRA_GRAM_STAGES 3
 #endif
+// m16 tiles per warp: two independent accumulator sets per H fragment (ncu on cfg2's mode-0
+// Gram at one tile: "wait" stalls on the DMMA accumulator chains dominated)
+#ifndef LMRA_GRAM_MT
+#define LMRA_GRAM_MT 2
+#endif
+constexpr int kGramMT = LMRA_GRAM_MT;
+constexpr int kGramRT = 64 * kGramMT;  // rows per CTA (4 warps x 16 x MT)
 
 template <int M8, bool RCONTIG>
 struct GramCfg {
-  static constexpr int RT = 64, JC = 16, STAGES = LMRA_GRAM_STAGES;
+  static constexpr int RT = kGramRT, JC = 16, STAGES = LMRA_GRAM_STAGES;
   static constexpr int LDA = RCONTIG ? conflict_free_ld(RT) : conflict_free_ld(JC);
   static constexpr int A_ELEMS = RCONTIG ? JC * LDA : RT * LDA;
   static constexpr int LDH = conflict_free_ld(M8);
@@ -295,18 +302,20 @@ __global__ void __launch_bounds__(kGramThreads)
   };
 
   constexpr int NF = M8 / 8;
-  double acc[NF][4];
+  double acc[kGramMT][NF][4];
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
+  for (int mt = 0; mt < kGramMT; ++mt)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[f][e] = 0.0;
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mt][f][e] = 0.0;
 
 #pragma unroll
   for (int st = 0; st < C::STAGES - 1; ++st) {
     if (st < nk) load(st, st);
     cp_async_commit();
   }
-  const int rw = warp * 16;
+  const int rw = warp * 16 * kGramMT;
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<C::STAGES - 2>();
     __syncthreads();
@@ -315,16 +324,24 @@ __global__ void __launch_bounds__(kGramThreads)
 #pragma unroll
     for (int kk = 0; kk < C::JC / 4; ++kk) {
       const int jj = kk * 4 + t;
-      double a0, a1;
-      if (RCONTIG) {
-        a0 = As[jj * C::LDA + rw + g];
-        a1 = As[jj * C::LDA + rw + g + 8];
-      } else {
-        a0 = As[(rw + g) * C::LDA + jj];
-        a1 = As[(rw + g + 8) * C::LDA + jj];
+      double a0[kGramMT], a1[kGramMT];
+#pragma unroll
+      for (int mt = 0; mt < kGramMT; ++mt) {
+        const int rr = rw + 16 * mt + g;
+        if (RCONTIG) {
+          a0[mt] = As[jj * C::LDA + rr];
+          a1[mt] = As[jj * C::LDA + rr + 8];
+        } else {
+          a0[mt] = As[rr * C::LDA + jj];
+          a1[mt] = As[(rr + 8) * C::LDA + jj];
+        }
       }
 #pragma unroll
-      for (int f = 0; f < NF; ++f) dmma16x8x4(acc[f], a0, a1, Hs[jj * C::LDH + f * 8 + g]);
+      for (int f = 0; f < NF; ++f) {
+        const double b = Hs[jj * C::LDH + f * 8 + g];
+#pragma unroll
+        for (int mt = 0; mt < kGramMT; ++mt) dmma16x8x4(acc[mt][f], a0[mt], a1[mt], b);
+      }
     }
     const int nt = kt + C::STAGES - 1;
     if (nt < nk) load(nt % C::STAGES, nt);
@@ -334,16 +351,18 @@ __global__ void __launch_bounds__(kGramThreads)
 
   double* zp = zpart + (size_t)blockIdx.y * I * stot + (size_t)I * koff;
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const long long r = r0 + rw + g + 8 * half;
-    if (r >= I) continue;
+  for (int mt = 0; mt < kGramMT; ++mt)
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      const int k = f * 8 + 2 * t;
-      if (k < s) zp[r + I * k] = acc[f][2 * half];
-      if (k + 1 < s) zp[r + I * (k + 1)] = acc[f][2 * half + 1];
+    for (int half = 0; half < 2; ++half) {
+      const long long r = r0 + rw + 16 * mt + g + 8 * half;
+      if (r >= I) continue;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const int k = f * 8 + 2 * t;
+        if (k < s) zp[r + I * k] = acc[mt][f][2 * half];
+        if (k + 1 < s) zp[r + I * (k + 1)] = acc[mt][f][2 * half + 1];
+      }
     }
-  }
 }
 
 // z[e] = sum_{p < nsplit} zpart[p][e], fixed order (deterministic).
@@ -586,8 +605,8 @@ static cudaError_t launch_gram_rc(const double* x, ModeView v, const double* h, 
 GramPlan plan_gram(ModeView v, int num_sms) {
   GramPlan p;
   const long long J = v.inner * v.outer;
-  const long long rtiles = (v.I + 63) / 64;
-  long long target = (long long)num_sms * 4;
+  const long long rtiles = (v.I + kGramRT - 1) / kGramRT;
+  long long target = (long long)num_sms * (kGramMT == 1 ? 4 : 3);  // ~ resident CTAs (one wave)
   long long ns = std::max<long long>(1, target / std::max<long long>(1, rtiles));
   // at least 32 columns per split (two K chunks) so each CTA amortises its prologue
   ns = std::min<long long>(ns, std::max<long long>(1, J / 32));
