@@ -1195,41 +1195,87 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
                            cudaMemcpyDeviceToDevice, st),
          "unpack");
   };
-  auto run_sampler = [&](size_t n, const double* w, size_t J, size_t T) -> size_t {
+  // the sampling chain of mode n (no collectives) on engine e's stream
+  auto run_sampler = [&](Engine& e, size_t n, const double* w, size_t J, size_t T) -> size_t {
+    cudaStream_t ss = e.st_;
     if (in.ov && in.ov->sample_idx && in.ov->sample_idx[n]) {  // parity overrides (global idx)
       T = in.ov->n_samples[n];
       const int64_t* oi = in.ov->sample_idx[n];
       for (size_t j = 0; j < T; ++j)
         if (oi[j] < 0 || (size_t)oi[j] >= J) throw std::invalid_argument("sample index out of range");
-      d_idx[n] = DevBuf(T + 1, st);
-      d_sc[n] = DevBuf(T, st);
-      ck(cudaMemcpyAsync(d_idx[n].get(), oi, T * sizeof(int64_t), cudaMemcpyHostToDevice, st), "H2D idx");
+      d_idx[n] = DevBuf(T + 1, ss);
+      d_sc[n] = DevBuf(T, ss);
+      ck(cudaMemcpyAsync(d_idx[n].get(), oi, T * sizeof(int64_t), cudaMemcpyHostToDevice, ss), "H2D idx");
       ck(cudaMemcpyAsync(d_sc[n].get(), in.ov->sample_scale[n], T * sizeof(double),
-                         cudaMemcpyHostToDevice, st), "H2D scales");
-      ck(cudaStreamSynchronize(st), "sync");
+                         cudaMemcpyHostToDevice, ss), "H2D scales");
+      ck(cudaStreamSynchronize(ss), "sync");
       n_draws[n] = T;
       return T;
     }
     if (T < 1) throw std::invalid_argument("randsample: L must be positive");
-    d_idx[n] = DevBuf(T + 1, st);
-    d_sc[n] = DevBuf(T, st);
-    DevBuf p(J, st), work(lmra_dev::sampler_workspace_doubles((long long)J), st);
+    d_idx[n] = DevBuf(T + 1, ss);
+    d_sc[n] = DevBuf(T, ss);
+    DevBuf p(J, ss), work(lmra_dev::sampler_workspace_doubles((long long)J), ss);
     DevBuf dummy;
     if (!w) {  // uniform regime never reads w
-      dummy = DevBuf(J, st);
+      dummy = DevBuf(J, ss);
       w = dummy.get();
     }
-    eng.launch("sampler", [&] {
+    e.launch("sampler", [&] {
       return lmra_dev::launch_sampler(w, (long long)J, cfg.regime, cfg.beta, (long long)T,
                                       cfg.seed, N + n + 1,
                                       reinterpret_cast<long long*>(d_idx[n].get()), d_sc[n].get(),
-                                      p.get(), work.get(), status_i + N + n, st);
+                                      p.get(), work.get(), status_i + N + n, ss);
     });
     n_draws[n] = T;
     return T;
   };
 
-  auto factor = [&](size_t n, size_t t_n) -> DevBuf {
+  // A mode's factor in four pieces:
+  //   norms_for   sampling weights (+ their collectives)                       main stream
+  //   sample_for  the sampling chain (no collectives)                           engine's stream
+  //   power_for   Omega, gather, power scheme (+ collectives), sketch rows      main stream
+  //   orth_for    orthonormalisation (no collectives)                           engine's stream
+  // ST-HOSVD runs them back to back; T-HOSVD runs the collective-free pieces of all modes
+  // concurrently on per-mode streams while every collective stays on the main stream in mode
+  // order (the same issue order on every rank).
+  struct ModeState {
+    size_t J = 0, T = 0;
+    DevBuf c;
+  };
+  std::vector<ModeState> ms(N);
+  auto norms_for = [&](size_t n) {
+    const std::vector<size_t> ld = ldims();
+    const ModeView v = view_of(ld, n);
+    const bool rows_split = sharded && n == N - 1;
+    const size_t Jl = (size_t)(v.inner * v.outer);
+    if (!sharded || rows_split) {  // every column local (rows split for mode N-1)
+      ms[n].J = Jl;
+      if (amm && cfg.regime != kUniform) {
+        d_w[n] = DevBuf(Jl, st);
+        eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+        if (rows_split) comm.allreduce_sum(d_w[n].get(), Jl, st);
+      }
+    } else {  // n < N-1: rank-local column range
+      const size_t per = Jl / c0, Jg = per * L;
+      ms[n].J = Jg;
+      if (amm && cfg.regime != kUniform) {
+        DevBuf wl(per * cmax, st), all((size_t)P * per * cmax, st);
+        ck(cudaMemsetAsync(wl.get(), 0, per * cmax * sizeof(double), st), "memset");
+        eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, wl.get(), st); });
+        comm.allgather(wl.get(), all.get(), per * cmax, st);
+        d_w[n] = DevBuf(Jg, st);
+        for (int q = 0; q < P; ++q)
+          ck(cudaMemcpyAsync(d_w[n].get() + per * sh0[q], all.get() + (size_t)q * per * cmax,
+                             per * shc[q] * sizeof(double), cudaMemcpyDeviceToDevice, st),
+             "unpack norms");
+      }
+    }
+  };
+  auto sample_for = [&](Engine& e, size_t n, size_t t_n) {
+    if (amm) ms[n].T = run_sampler(e, n, d_w[n].get(), ms[n].J, t_n);
+  };
+  auto power_for = [&](size_t n) {
     const size_t I = gdims[n], s = r.sketch[n];
     const std::vector<size_t> ld = ldims();
     const ModeView v = view_of(ld, n);
@@ -1237,16 +1283,11 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     ck(cudaMemcpyAsync(c.get(), om_pin + om_off[n], I * s * sizeof(double), cudaMemcpyHostToDevice, st),
        "H2D omega");
     const bool rows_split = sharded && n == N - 1;
+    const size_t t_n = ms[n].T;
     if (!sharded) {  // replicated tensor: the single-GPU computation, identical on every rank
       if (!amm) {
         eng.gram_power(cur, v, c, s, cfg.power, cfg.strategy);
       } else {
-        const size_t J = (size_t)(v.inner * v.outer);
-        if (cfg.regime != kUniform) {
-          d_w[n] = DevBuf(J, st);
-          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
-        }
-        t_n = run_sampler(n, d_w[n].get(), J, t_n);
         DevBuf cp(I * t_n, st);
         eng.launch("gather", [&] {
           return lmra_dev::launch_gather(cur, v, reinterpret_cast<const long long*>(d_idx[n].get()),
@@ -1255,7 +1296,7 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
         eng.gram_power(cp.get(), ModeView{1, (long long)I, (long long)t_n}, c, s, cfg.power, cfg.strategy);
       }
     } else if (!rows_split) {  // n < N-1: rank-local column range
-      const size_t Jl = (size_t)(v.inner * v.outer), per = Jl / c0, Jg = per * L;
+      const size_t Jl = (size_t)(v.inner * v.outer);
       const lmra_dev::GramPlan plan = lmra_dev::plan_gram(v, ctx->num_sms);
       if (!amm) {
         DevBuf h(Jl * s, st), zpart((size_t)plan.nsplit * I * s, st);
@@ -1267,21 +1308,9 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
           comm.allreduce_sum(c.get(), I * s, st);
         }
       } else {
-        if (cfg.regime != kUniform) {
-          DevBuf wl(per * cmax, st), all((size_t)P * per * cmax, st);
-          ck(cudaMemsetAsync(wl.get(), 0, per * cmax * sizeof(double), st), "memset");
-          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, wl.get(), st); });
-          comm.allgather(wl.get(), all.get(), per * cmax, st);
-          d_w[n] = DevBuf(Jg, st);
-          for (int q = 0; q < P; ++q)
-            ck(cudaMemcpyAsync(d_w[n].get() + per * sh0[q], all.get() + (size_t)q * per * cmax,
-                               per * shc[q] * sizeof(double), cudaMemcpyDeviceToDevice, st),
-               "unpack norms");
-        }
-        t_n = run_sampler(n, d_w[n].get(), Jg, t_n);
         DevBuf lidx(t_n + 1, st), cp(I * t_n, st);
         ck(lmra_dev::launch_localize_idx(reinterpret_cast<const long long*>(d_idx[n].get()),
-                                         (long long)t_n, (long long)(per * s0), (long long)Jl,
+                                         (long long)t_n, (long long)(Jl / c0 * s0), (long long)Jl,
                                          reinterpret_cast<long long*>(lidx.get()), st),
            "localize");
         eng.launch("gather", [&] {
@@ -1313,12 +1342,6 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
           });
         }
       } else {
-        if (cfg.regime != kUniform) {
-          d_w[n] = DevBuf(J, st);
-          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
-          comm.allreduce_sum(d_w[n].get(), J, st);
-        }
-        t_n = run_sampler(n, d_w[n].get(), J, t_n);
         DevBuf cp(c0 * t_n, st);
         eng.launch("gather", [&] {
           return lmra_dev::launch_gather(cur, v, reinterpret_cast<const long long*>(d_idx[n].get()),
@@ -1337,13 +1360,25 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
       }
       gather_rows(cr.get(), s, c.get(), I);
     }
+    ms[n].c = std::move(c);
+  };
+  auto orth_for = [&](Engine& e, size_t n) -> DevBuf {
+    const size_t I = gdims[n], s = r.sketch[n];
     const size_t mu = std::min(r.mu[n], std::min(I, s));  // top_left_vectors_clamped
     if (mu < r.mu[n] && R == 0)
       fprintf(stderr, "lmra: requested rank %zu exceeds matrix rank limit %zu, clamping\n",
               r.mu[n], mu);
     res->f_rows[n] = I;
     res->f_cols[n] = mu;
-    return eng.orth(c.get(), I, s, mu, status_i + n);
+    ms[n].c.rebind(e.st_);
+    DevBuf f = e.orth(ms[n].c.get(), I, s, mu, status_i + n);
+    return f;
+  };
+  auto factor = [&](size_t n, size_t t_n) -> DevBuf {
+    norms_for(n);
+    sample_for(eng, n, t_n);
+    power_for(n);
+    return orth_for(eng, n);
   };
 
   auto contract = [&](size_t n, const double* q, size_t mu, const std::string& phase) {
@@ -1366,7 +1401,45 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
 
   std::vector<DevBuf> factors(N);
   if (!sequential) {
-    for (size_t n = 0; n < N; ++n) factors[n] = factor(n, amm ? t_flat[n] : 0);
+    // phases across modes: norms (main) | samplers (per-mode streams, concurrent) | power
+    // schemes with their collectives (main, mode order) | orthonormalisations (per-mode
+    // streams, each starting as soon as its sketch is reduced)
+    std::vector<cudaEvent_t> evs;
+    auto new_event = [&](cudaStream_t on) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      evs.push_back(e);
+      ck(cudaEventRecord(e, on), "event");
+      return e;
+    };
+    struct EvGuard {
+      std::vector<cudaEvent_t>& v;
+      ~EvGuard() {
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+      }
+    } ev_guard{evs};
+    for (size_t n = 0; n < N; ++n) norms_for(n);
+    const cudaEvent_t norms_done = new_event(st);
+    std::vector<Engine> engs;
+    engs.reserve(N);
+    for (size_t n = 0; n < N; ++n) {
+      cudaStream_t sn = ctx->aux_stream(n);
+      ck(cudaStreamWaitEvent(sn, norms_done, 0), "wait");
+      engs.emplace_back(ctx, sn, ctx->profile == 1 ? &prof : nullptr);
+    }
+    std::vector<cudaEvent_t> sampled(N);
+    for (size_t n = 0; n < N; ++n) {
+      sample_for(engs[n], n, amm ? t_flat[n] : 0);
+      sampled[n] = new_event(engs[n].st_);
+    }
+    for (size_t n = 0; n < N; ++n) {
+      ck(cudaStreamWaitEvent(st, sampled[n], 0), "wait");
+      power_for(n);
+      const cudaEvent_t sketched = new_event(st);
+      ck(cudaStreamWaitEvent(engs[n].st_, sketched, 0), "wait");
+      factors[n] = orth_for(engs[n], n);
+    }
+    for (size_t n = 0; n < N; ++n) ck(cudaStreamWaitEvent(st, new_event(engs[n].st_), 0), "wait");
     std::vector<size_t> idx(N);
     std::iota(idx.begin(), idx.end(), size_t{0});
     std::stable_sort(idx.begin(), idx.end(),
