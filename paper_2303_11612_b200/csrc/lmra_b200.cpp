@@ -1244,6 +1244,9 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     DevBuf c;
   };
   std::vector<ModeState> ms(N);
+  // local weights already produced by the fused 3-mode pass (T-HOSVD on a 3-way slab)
+  std::vector<DevBuf> pre_w(N);
+  bool pre_last = false;
   auto norms_for = [&](size_t n) {
     const std::vector<size_t> ld = ldims();
     const ModeView v = view_of(ld, n);
@@ -1252,17 +1255,24 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     if (!sharded || rows_split) {  // every column local (rows split for mode N-1)
       ms[n].J = Jl;
       if (amm && cfg.regime != kUniform) {
-        d_w[n] = DevBuf(Jl, st);
-        eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+        if (!(rows_split && pre_last)) {
+          d_w[n] = DevBuf(Jl, st);
+          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+        }
         if (rows_split) comm.allreduce_sum(d_w[n].get(), Jl, st);
       }
     } else {  // n < N-1: rank-local column range
       const size_t per = Jl / c0, Jg = per * L;
       ms[n].J = Jg;
       if (amm && cfg.regime != kUniform) {
-        DevBuf wl(per * cmax, st), all((size_t)P * per * cmax, st);
-        ck(cudaMemsetAsync(wl.get(), 0, per * cmax * sizeof(double), st), "memset");
-        eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, wl.get(), st); });
+        DevBuf wl, all((size_t)P * per * cmax, st);
+        if (pre_w[n].get()) {
+          wl = std::move(pre_w[n]);
+        } else {
+          wl = DevBuf(per * cmax, st);
+          ck(cudaMemsetAsync(wl.get(), 0, per * cmax * sizeof(double), st), "memset");
+          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, wl.get(), st); });
+        }
         comm.allgather(wl.get(), all.get(), per * cmax, st);
         d_w[n] = DevBuf(Jg, st);
         for (int q = 0; q < P; ++q)
@@ -1418,6 +1428,23 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
         for (cudaEvent_t e : v) cudaEventDestroy(e);
       }
     } ev_guard{evs};
+    if (amm && cfg.regime != kUniform && N == 3 && !(in.ov && in.ov->sample_idx)) {
+      // one read of the slab for all three modes' canonical norms (bit-identical to the
+      // per-mode passes: modes 0/1 are local columns, mode 2 the slab partials)
+      const long long I0 = (long long)gdims[0], I1 = (long long)gdims[1], I2 = (long long)c0;
+      const size_t per0 = (size_t)(I1 * I2) / c0, per1 = (size_t)(I0 * I2) / c0;
+      pre_w[0] = DevBuf(per0 * cmax, st);
+      pre_w[1] = DevBuf(per1 * cmax, st);
+      ck(cudaMemsetAsync(pre_w[0].get(), 0, per0 * cmax * sizeof(double), st), "memset");
+      ck(cudaMemsetAsync(pre_w[1].get(), 0, per1 * cmax * sizeof(double), st), "memset");
+      d_w[2] = DevBuf((size_t)(I0 * I1), st);
+      DevBuf nwork(lmra_dev::norms3_workspace_doubles(I0, I1, I2), st);
+      eng.launch("norms", [&] {
+        return lmra_dev::launch_norms3(cur, I0, I1, I2, pre_w[0].get(), pre_w[1].get(), d_w[2].get(),
+                                       nwork.get(), st);
+      });
+      pre_last = true;
+    }
     for (size_t n = 0; n < N; ++n) norms_for(n);
     const cudaEvent_t norms_done = new_event(st);
     std::vector<Engine> engs;
