@@ -1391,10 +1391,20 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     return orth_for(eng, n);
   };
 
-  auto contract = [&](size_t n, const double* q, size_t mu, const std::string& phase) {
+  Engine::I8Chain chain;
+  auto contract = [&](size_t n, const double* q, size_t mu, const std::string& phase, bool next1) {
     const std::vector<size_t> ld = ldims();
     if (!sharded || n != N - 1) {
-      DevBuf y = eng.ttm(cur, ld, n, q, mu, phase);
+      // the slab's mode-0 contraction runs on the int8 tensor cores when its canonical column
+      // norms are known (this rank's columns of the all-gathered weights), like the
+      // single-GPU path; a following mode-1 contraction takes the handed-over exponents
+      const double* w0 = nullptr;
+      if (n == 0 && cur == in.x && amm && cfg.regime != kUniform && d_w[0].get() &&
+          !(in.ov && in.ov->sample_idx)) {
+        const size_t per = prod(ld) / ld[0] / ld[N - 1];
+        w0 = d_w[0].get() + (sharded ? per * s0 : 0);
+      }
+      DevBuf y = eng.ttm_mode0(cur, ld, n, q, mu, w0, phase, &chain, next1);
       curbuf = std::move(y);
     } else {  // contraction over the sharded mode: local partial + all-reduce -> replicated
       DevBuf qr = rows_of(q, gdims[n], mu, s0, c0);
@@ -1472,7 +1482,11 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     std::stable_sort(idx.begin(), idx.end(),
                      [&](size_t a, size_t b) { return res->f_cols[a] < res->f_cols[b]; });
     int step = 0;
-    for (size_t n : idx) contract(n, factors[n].get(), res->f_cols[n], "core_ttm" + std::to_string(step++));
+    for (size_t k = 0; k < N; ++k) {
+      const size_t n = idx[k];
+      contract(n, factors[n].get(), res->f_cols[n], "core_ttm" + std::to_string(step++),
+               k + 1 < N && idx[k + 1] == 1);
+    }
   } else {
     for (size_t n : r.order) {
       size_t t_n = 0;
@@ -1482,7 +1496,9 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
         if (t_n < 1) throw std::invalid_argument("sample counts must be positive");
       }
       factors[n] = factor(n, t_n);
-      contract(n, factors[n].get(), res->f_cols[n], "shrink_ttm_m" + std::to_string(n));
+      const size_t oi = (size_t)(std::find(r.order.begin(), r.order.end(), n) - r.order.begin());
+      contract(n, factors[n].get(), res->f_cols[n], "shrink_ttm_m" + std::to_string(n),
+               oi + 1 < r.order.size() && r.order[oi + 1] == 1);
     }
   }
   res->core_dims = gdims;
