@@ -23,6 +23,8 @@
  *   gaussian_matrix     (sketching.hpp:69)          ->  lmra_gaussian_matrix
  *   randsample          (sketching.hpp:56)          ->  lmra_randsample
  *   gram_sampling_probabilities (tucker.cpp:110-130)->  lmra_column_sqnorms + lmra_probabilities
+ *   reconstruct         (tucker.hpp:63)             ->  lmra_reconstruct
+ *   relative_error      (tucker.hpp:66)             ->  lmra_relative_error / lmra_result_relative_error
  *
  * Tensors are dense fp64 with the reference's linearisation: first index fastest
  * (tensor.hpp:9-12).  Matrices are column-major (Eigen default).
@@ -218,12 +220,47 @@ int lmra_randsample(uint64_t L, const double* p, uint64_t n, uint64_t seed, uint
 int lmra_amm_sample_counts(const uint64_t* dims, int order, const lmra_algo_config* cfg,
                            int sequential, uint64_t* out);
 
-/* ---- synthetic BASELINE inputs, generated on the device (x is a device buffer) ---- */
+/* ---- verification (tucker.hpp:63-66, tucker.cpp:222-240), on the device ----
+ * lmra_reconstruct: out = core x_0 Q_0 x_1 Q_1 ... (reconstruct, mode order); core (core_dims),
+ *   factors[n] (factor_rows[n] x core_dims[n], column-major) all on the host (location =
+ *   LMRA_HOST) or all on the device; out (prod factor_rows) at out_location.
+ * lmra_relative_error: ||a - approx||_F / ||a||_F over two tensors of dims (relative_error);
+ *   LMRA_EINVAL "relative_error: zero reference tensor" when a is zero.
+ * lmra_result_relative_error: the same for a result against the tensor a it decomposed,
+ *   reconstructed into device scratch (shape mismatch -> "relative_error: shape mismatch"). */
+int lmra_reconstruct(lmra_context* ctx, const double* core, const uint64_t* core_dims, int order,
+                     const double* const* factors, const uint64_t* factor_rows, int location, double* out,
+                     int out_location);
+int lmra_relative_error(lmra_context* ctx, const double* a, const double* approx, const uint64_t* dims,
+                        int order, int location, double* re);
+int lmra_result_relative_error(lmra_context* ctx, const lmra_result* r, const double* a, const uint64_t* dims,
+                               int order, int location, double* re);
+
+/* ---- synthetic BASELINE inputs, generated on the device (x is a device buffer) ----
+ * Definitions in paper_2303_11612_b200/csrc/gen/portable_gen.hpp: explicit IEEE operations in
+ * fixed orders, so the oracle's host generators produce the same bits.  The _slab variants
+ * write only the slab [start, start + count) of the last mode (a multi-GPU rank's share);
+ * the Tucker-plus-noise tensor is then made in two steps around a host exchange:
+ *   lmra_gen_tucker_signal_slab  x = the signal B on the slab; slice_b / slice_e (host, count
+ *                                entries) = sums of squares of B and of the noise E per slice;
+ *   lmra_gen_noise_coef          coef = gamma ||B|| / ||E|| from ALL slices' sums, in order;
+ *   lmra_gen_add_noise_slab      x += coef * E on the slab. */
 int lmra_gen_tucker_noise(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims,
                           int order, double gamma, uint64_t seed, double* x);
+int lmra_gen_tucker_signal_slab(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims, int order,
+                                uint64_t seed, uint64_t start, uint64_t count, double* x, double* slice_b,
+                                double* slice_e);
+int lmra_gen_noise_coef(const double* slice_b, const double* slice_e, uint64_t nslices, double gamma,
+                        double* coef);
+int lmra_gen_add_noise_slab(lmra_context* ctx, const uint64_t* dims, int order, uint64_t seed, uint64_t start,
+                            uint64_t count, double coef, double* x);
 int lmra_gen_hilbert(lmra_context* ctx, const uint64_t* dims, int order, double* x);
+int lmra_gen_hilbert_slab(lmra_context* ctx, const uint64_t* dims, int order, uint64_t start, uint64_t count,
+                          double* x);
 int lmra_gen_video(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms,
                    double noise, uint64_t seed, double* x);
+int lmra_gen_video_slab(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms, double noise,
+                        uint64_t seed, uint64_t start, uint64_t count, double* x);
 
 /* device memory helpers (so callers without a CUDA runtime can stage data) */
 int lmra_device_alloc(lmra_context* ctx, size_t bytes, void** out);

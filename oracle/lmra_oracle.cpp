@@ -5,6 +5,7 @@
 // sources; the only fused operations are the explicit std::fma in the canonical
 // column-norm order.
 #include "lmra_oracle.h"
+#include "../paper_2303_11612_b200/csrc/gen/portable_gen.hpp"
 
 #include <dlfcn.h>
 
@@ -1036,28 +1037,141 @@ double orc_relative_error(const double* x, const uint64_t* dims, int order, cons
   return re;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------- BASELINE generators
-// Definitions: RandomStream stream ids follow the
-// reference's datagen.cpp:20-23 (core 100, factor 101+n, noise 200).
+// The definitions live in paper_2303_11612_b200/csrc/gen/portable_gen.hpp (input synthesis,
+// not the algorithm under test: explicit IEEE operations and fixed orders, so the host
+// loops below give the device generators' exact bits).  Threads split independent outputs
+// only; every sum keeps the definition's sequential order.
+namespace {
+template <class F>
+void parallel_for(size_t n, F&& f) {  // f(begin, end) over [0, n)
+  const int th = default_threads();
+  if (th <= 1 || n < 2) {
+    f(size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t chunk = (n + th - 1) / th;
+  for (int t = 0; t < th; ++t) {
+    const size_t b = std::min(n, t * chunk), e = std::min(n, b + chunk);
+    if (b < e) pool.emplace_back([&f, b, e] { f(b, e); });
+  }
+  for (auto& t : pool) t.join();
+}
+
+// y[a, i, o] = sum_k U[i, k] x[a, k, o] (fma chain over k), i < I.  Blocked over a so the
+// block's x(a, :, o) panel stays in cache while every i is formed from it.
+void gen_ttm_host(const double* x, size_t inner, size_t K, size_t I, size_t outer, const double* u, size_t ldu,
+                  double* y) {
+  constexpr size_t kBlock = 512;
+  const size_t nab = (inner + kBlock - 1) / kBlock;
+  parallel_for(outer * nab, [&](size_t b, size_t e) {
+    // the block's x(a, :, o) panel is copied to a contiguous buffer first: its K rows sit
+    // inner * 8 bytes apart, which for a large inner maps them all onto the same cache sets
+    std::vector<double> panel(K * kBlock), acc(kBlock);
+    for (size_t r = b; r < e; ++r) {
+      const size_t ab = r % nab, o = r / nab;
+      const size_t a0 = ab * kBlock, a1 = std::min(inner, a0 + kBlock), na = a1 - a0;
+      for (size_t k = 0; k < K; ++k)
+        std::memcpy(panel.data() + k * kBlock, x + inner * (k + K * o) + a0, na * sizeof(double));
+      for (size_t i = 0; i < I; ++i) {
+        for (size_t a = 0; a < na; ++a) acc[a] = 0.0;
+        for (size_t k = 0; k < K; ++k) {
+          const double uk = u[i + ldu * k];
+          const double* xk = panel.data() + k * kBlock;
+          for (size_t a = 0; a < na; ++a) acc[a] = lmra_gen::gp_fma(uk, xk[a], acc[a]);
+        }
+        std::memcpy(y + inner * (i + I * o) + a0, acc.data(), na * sizeof(double));
+      }
+    }
+  });
+}
+}  // namespace
+
+extern "C" {
+
 int orc_gen_tucker_noise(const uint64_t* dims, const uint64_t* core_dims, int order, double gamma,
                          uint64_t seed, double* out) {
   return guard([&] {
+    using namespace lmra_gen;
+    if (order < 1 || order > 8) throw std::invalid_argument("generator: order must be 1..8");
     std::vector<size_t> cd(core_dims, core_dims + order), d(dims, dims + order);
-    Tensor b(cd);
-    fill_normals(seed, 100, b.v.data(), b.size(), default_threads());
+    for (int n = 0; n < order; ++n)
+      if (cd[n] < 1 || cd[n] > d[n]) throw std::invalid_argument("core dimensions must lie in [1, I_n]");
+    size_t ncore = 1, total = 1;
     for (int n = 0; n < order; ++n) {
-      Mat u = thin_qr_q(gaussian_matrix(d[n], cd[n], seed, 101 + n));
-      b = mode_n_product(b, u, (size_t)n);
+      ncore *= cd[n];
+      total *= d[n];
     }
-    std::vector<double> e(b.size());
-    fill_normals(seed, 200, e.data(), e.size(), default_threads());
-    double nb = 0.0, ne = 0.0;
-    for (size_t i = 0; i < b.size(); ++i) {
-      nb += b.v[i] * b.v[i];
-      ne += e[i] * e[i];
+    auto tp = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!getenv("ORC_GEN_TIMING")) return;
+      auto t = std::chrono::steady_clock::now();
+      fprintf(stderr, "gen %s %.3f s\n", what, std::chrono::duration<double>(t - tp).count());
+      tp = t;
+    };
+    std::vector<double> cur(ncore);
+    gp_normals_range(seed, kStreamCore, cur.data(), 0, ncore);
+    std::vector<size_t> cdim = cd;
+    for (int n = 0; n < order; ++n) {
+      std::vector<double> u(d[n] * cd[n]);
+      gp_orthonormal_factor(d[n], cd[n], seed, (uint64_t)n, u.data());
+      size_t inner = 1, outer = 1;
+      for (int k = 0; k < n; ++k) inner *= cdim[k];
+      for (int k = n + 1; k < order; ++k) outer *= cdim[k];
+      const bool last = n == order - 1;
+      std::vector<double> y;
+      double* dst = out;
+      if (!last) {
+        y.resize(inner * d[n] * outer);
+        dst = y.data();
+      }
+      gen_ttm_host(cur.data(), inner, cd[n], d[n], outer, u.data(), d[n], dst);
+      cdim[n] = d[n];
+      if (!last) cur.swap(y);
+      lap("ttm");
     }
-    double coef = gamma * std::sqrt(nb) / std::sqrt(ne);
-    for (size_t i = 0; i < b.size(); ++i) out[i] = b.v[i] + coef * e[i];
+    // per-slice (last mode) sums of squares of B and of E: fibres of d0 (fma chain), slice =
+    // sequential sum of its fibres, total = sequential sum over slices
+    const size_t d0 = d[0], L = order == 1 ? 1 : d[order - 1];
+    const size_t nfib = total / d0, per = nfib / L;
+    std::vector<double> fb(nfib), fe(nfib);
+    parallel_for(nfib, [&](size_t b, size_t e) {
+      std::vector<double> z(d0 + 1);
+      for (size_t f = b; f < e; ++f) {
+        const double* p = out + f * d0;
+        double acc = 0.0;
+        for (size_t i = 0; i < d0; ++i) acc = gp_fma(p[i], p[i], acc);
+        fb[f] = acc;
+        gp_normals_range(seed, kStreamNoise, z.data(), f * d0, (f + 1) * d0);
+        acc = 0.0;
+        for (size_t i = 0; i < d0; ++i) acc = gp_fma(z[i], z[i], acc);
+        fe[f] = acc;
+      }
+    });
+    lap("fibre sums");
+    std::vector<double> sb(L), se(L);
+    for (size_t l = 0; l < L; ++l) {
+      double ab = 0.0, ae = 0.0;
+      for (size_t j = 0; j < per; ++j) {
+        ab = gp_add(ab, fb[l * per + j]);
+        ae = gp_add(ae, fe[l * per + j]);
+      }
+      sb[l] = ab;
+      se[l] = ae;
+    }
+    const double coef = gp_noise_coef(sb.data(), se.data(), L, gamma);
+    parallel_for((total + 63) / 64, [&](size_t b, size_t e) {
+      double z[64];
+      for (size_t r = b; r < e; ++r) {
+        const size_t e0 = r * 64, e1 = std::min(total, e0 + 64);
+        gp_normals_range(seed, kStreamNoise, z, e0, e1);
+        for (size_t i = e0; i < e1; ++i) out[i] = gp_add(out[i], gp_mul(coef, z[i - e0]));
+      }
+    });
+    lap("noise");
   });
 }
 
@@ -1081,42 +1195,34 @@ int orc_gen_hilbert(const uint64_t* dims, int order, double* out) {
 int orc_gen_video(const uint64_t* dims, int order, uint64_t n_terms, double noise, uint64_t seed,
                   double* out) {
   return guard([&] {
-    std::vector<size_t> d(dims, dims + order);
-    size_t total = 1;
-    for (size_t v : d) total *= v;
-    // profiles P_n (I_n x R) and weights
-    std::vector<Mat> P(order);
-    for (int n = 0; n < order; ++n) P[n] = Mat(d[n], n_terms);
-    std::vector<double> w(n_terms);
-    for (size_t t = 0; t < n_terms; ++t) {
-      Rng g(seed, 300 + t);
-      w[t] = g.next_double();
-      for (int n = 0; n < order; ++n) {
-        double f = 0.5 + 7.5 * g.next_double();
-        double ph = 6.283185307179586476925286766559 * g.next_double();
-        for (size_t i = 0; i < d[n]; ++i) {
-          double x = static_cast<double>(i) / static_cast<double>(d[n]);
-          P[n](i, t) = std::cos(6.283185307179586476925286766559 * f * x + ph);
+    using namespace lmra_gen;
+    if (order < 1 || order > 8) throw std::invalid_argument("generator: order must be 1..8");
+    if (n_terms < 1) throw std::invalid_argument("video generator: n_terms must be positive");
+    std::vector<long long> d(dims, dims + order);
+    size_t total = 1, tot = 0;
+    for (long long v : d) {
+      total *= (size_t)v;
+      tot += (size_t)v * n_terms;
+    }
+    std::vector<double> prof(tot), w(n_terms);
+    gp_video_profiles(dims, order, n_terms, seed, prof.data(), w.data());
+    parallel_for((total + 63) / 64, [&](size_t b, size_t e) {
+      for (size_t r = b; r < e; ++r) {
+        const size_t e0 = r * 64, e1 = std::min(total, e0 + 64);
+        Pcg g(seed, kStreamVideoNoise);
+        g.advance(2ull * e0);
+        for (size_t el = e0; el < e1; ++el) {
+          long long idx[8];
+          size_t rem = el;
+          for (int k = 0; k < order; ++k) {
+            idx[k] = (long long)(rem % (size_t)d[k]);
+            rem /= (size_t)d[k];
+          }
+          const double v = gp_video_element(idx, d.data(), order, prof.data(), w.data(), (int)n_terms);
+          out[el] = gp_add(v, gp_mul(noise, g.next_double()));
         }
       }
-    }
-    // Khatri-Rao of modes 1..N-1 (J x R), then X_(0) = P_0 diag(w) KR^T
-    size_t J = total / d[0];
-    Mat kr(J, n_terms);
-    for (size_t t = 0; t < n_terms; ++t) {
-      for (size_t j = 0; j < J; ++j) {
-        size_t rem = j;
-        double v = w[t];
-        for (int n = 1; n < order; ++n) {
-          v *= P[n](rem % d[n], t);
-          rem /= d[n];
-        }
-        kr(j, t) = v;
-      }
-    }
-    gemm(false, true, d[0], J, n_terms, P[0].d.data(), d[0], kr.d.data(), J, out, d[0]);
-    Rng g(seed, 400);
-    for (size_t e = 0; e < total; ++e) out[e] += noise * g.next_double();
+    });
   });
 }
 

@@ -112,6 +112,17 @@ def _load():
         "lmra_gen_tucker_noise": (C.c_int, [vp, u64p, u64p, C.c_int, C.c_double, C.c_uint64, vp]),
         "lmra_gen_hilbert": (C.c_int, [vp, u64p, C.c_int, vp]),
         "lmra_gen_video": (C.c_int, [vp, u64p, C.c_int, C.c_uint64, C.c_double, C.c_uint64, vp]),
+        "lmra_gen_tucker_signal_slab": (C.c_int, [vp, u64p, u64p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                  vp, dblp, dblp]),
+        "lmra_gen_noise_coef": (C.c_int, [dblp, dblp, C.c_uint64, C.c_double, dblp]),
+        "lmra_gen_add_noise_slab": (C.c_int, [vp, u64p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                              C.c_double, vp]),
+        "lmra_gen_hilbert_slab": (C.c_int, [vp, u64p, C.c_int, C.c_uint64, C.c_uint64, vp]),
+        "lmra_gen_video_slab": (C.c_int, [vp, u64p, C.c_int, C.c_uint64, C.c_double, C.c_uint64, C.c_uint64,
+                                          C.c_uint64, vp]),
+        "lmra_reconstruct": (C.c_int, [vp, vp, u64p, C.c_int, C.POINTER(vp), u64p, C.c_int, vp, C.c_int]),
+        "lmra_relative_error": (C.c_int, [vp, vp, vp, u64p, C.c_int, C.c_int, dblp]),
+        "lmra_result_relative_error": (C.c_int, [vp, vp, vp, u64p, C.c_int, C.c_int, dblp]),
         "lmra_device_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
         "lmra_device_free": (C.c_int, [vp, vp]),
         "lmra_memcpy": (C.c_int, [vp, vp, vp, C.c_size_t, C.c_int, C.c_int]),
@@ -144,6 +155,8 @@ EXPORTED = [
     "lmra_tnsr_save",
     "lmra_gaussian_matrix", "lmra_probabilities", "lmra_randsample", "lmra_amm_sample_counts",
     "lmra_gen_tucker_noise", "lmra_gen_hilbert", "lmra_gen_video", "lmra_device_alloc",
+    "lmra_gen_tucker_signal_slab", "lmra_gen_noise_coef", "lmra_gen_add_noise_slab", "lmra_gen_hilbert_slab",
+    "lmra_gen_video_slab", "lmra_reconstruct", "lmra_relative_error", "lmra_result_relative_error",
     "lmra_device_free", "lmra_memcpy",
 ]
 

@@ -1,141 +1,212 @@
-// gen.cu -- device generators for the BASELINE synthetic inputs (DESIGN.md "Synthetic
-// inputs").  The integer part (PCG32 with the reference's seeding, rng.hpp:20-36) is
-// bit-identical to the host stream; the Box-Muller transform uses CUDA's log/sincos,
-// so device normals may differ from glibc's in the last ulp -- the generated tensor
-// is defined as what this code produces and is fed bit-identically to the oracle.
+// gen.cu -- device generators for the BASELINE synthetic inputs and
+// small device utilities (transpose, rank sums, index localisation).
+//
+// The generators evaluate the definitions of gen/portable_gen.hpp element by element with
+// explicit IEEE operations (no contraction, fixed summation orders), so they produce the
+// same bits as the host generators (oracle/lmra_oracle.cpp) -- and any slab of the last mode
+// on its own (multi-GPU ranks generate only their slab).
 #include "common.cuh"
+#include "../gen/portable_gen.hpp"
 
 namespace lmra_dev {
 
-struct Pcg {
-  unsigned long long state, inc;
-  __device__ Pcg(unsigned long long seed, unsigned long long stream) {
-    inc = (stream << 1u) | 1u;
-    state = 0;
-    next();
-    state += seed;
-    next();
-  }
-  __device__ unsigned int next() {
-    unsigned long long old = state;
-    state = old * 6364136223846793005ULL + inc;
-    unsigned int xs = (unsigned int)(((old >> 18u) ^ old) >> 27u);
-    unsigned int rot = (unsigned int)(old >> 59u);
-    return (xs >> rot) | (xs << ((32u - rot) & 31u));
-  }
-  __device__ void advance(unsigned long long delta) {
-    unsigned long long cm = 6364136223846793005ULL, cp = inc, am = 1, ap = 0;
-    while (delta) {
-      if (delta & 1) {
-        am *= cm;
-        ap = ap * cm + cp;
-      }
-      cp = (cm + 1) * cp;
-      cm *= cm;
-      delta >>= 1;
-    }
-    state = am * state + ap;
-  }
-  __device__ double next_double() {
-    unsigned long long hi = next(), lo = next();
-    return (double)(((hi << 32) | lo) >> 11) * 0x1.0p-53;
-  }
-};
+using namespace lmra_gen;
 
-constexpr int kPairsPerThread = 64;
-
-__global__ void gen_normals_kernel(double* __restrict__ out, long long n, unsigned long long seed,
-                                   unsigned long long stream) {
-  const long long npairs = (n + 1) / 2;
-  const long long p0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kPairsPerThread;
-  if (p0 >= npairs) return;
-  Pcg g(seed, stream);
-  g.advance(4ull * (unsigned long long)p0);
-  const long long p1 = min(npairs, p0 + kPairsPerThread);
-  for (long long p = p0; p < p1; ++p) {
-    double u1 = 1.0 - g.next_double();
-    double u2 = g.next_double();
-    double r = sqrt(-2.0 * log(u1));
-    double s, c;
-    sincos(6.283185307179586476925286766559 * u2, &s, &c);
-    out[2 * p] = r * c;
-    if (2 * p + 1 < n) out[2 * p + 1] = r * s;
+// y[a, i, o] = sum_k U[r0 + i, k] x[a, k, o] (fma chain over k ascending): one output per thread
+__global__ void gen_ttm_kernel(const double* __restrict__ x, long long inner, long long K, long long I,
+                               long long outer, const double* __restrict__ u, long long ldu,
+                               double* __restrict__ y) {
+  const long long n = inner * I * outer;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long a = e % inner, r = e / inner, i = r % I, o = r / I;
+    y[e] = gp_ttm_element(x, inner, K, u, ldu, a, i, o);
   }
 }
 
-__global__ void gen_uniform_add_kernel(double* __restrict__ out, long long n, double scale,
-                                       unsigned long long seed, unsigned long long stream) {
-  const long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kPairsPerThread;
-  if (e0 >= n) return;
+// out[f] = sum_i x[f d0 + i]^2 (fma chain), one fibre per thread
+__global__ void gen_fiber_sumsq_kernel(const double* __restrict__ x, long long d0, long long nfib,
+                                       double* __restrict__ out) {
+  const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfib) return;
+  const double* p = x + f * d0;
+  double acc = 0.0;
+  for (long long i = 0; i < d0; ++i) acc = gp_fma(p[i], p[i], acc);
+  out[f] = acc;
+}
+
+// the same for the normal stream (seed, stream), elements e_base + f d0 + i, regenerated
+__global__ void gen_noise_fiber_sumsq_kernel(unsigned long long seed, unsigned long long stream,
+                                             long long e_base, long long d0, long long nfib,
+                                             double* __restrict__ out) {
+  const long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfib) return;
+  const unsigned long long b = (unsigned long long)(e_base + f * d0), e = b + (unsigned long long)d0;
   Pcg g(seed, stream);
-  g.advance(2ull * (unsigned long long)e0);
-  const long long e1 = min(n, e0 + kPairsPerThread);
-  for (long long e = e0; e < e1; ++e) out[e] += scale * g.next_double();
+  g.advance(4ull * (b / 2));
+  double acc = 0.0;
+  unsigned long long i = b;
+  if (i & 1) {
+    double z0, z1;
+    g.normal_pair(&z0, &z1);
+    acc = gp_fma(z1, z1, acc);
+    ++i;
+  }
+  for (; i < e; i += 2) {
+    double z0, z1;
+    g.normal_pair(&z0, &z1);
+    acc = gp_fma(z0, z0, acc);
+    if (i + 1 < e) acc = gp_fma(z1, z1, acc);
+  }
+  out[f] = acc;
+}
+
+// out[l] = sum_j fib[l per + j] (sequential adds), one slice per thread
+__global__ void gen_slice_sum_kernel(const double* __restrict__ fib, long long per, long long nslices,
+                                     double* __restrict__ out) {
+  const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nslices) return;
+  double acc = 0.0;
+  for (long long j = 0; j < per; ++j) acc = gp_add(acc, fib[l * per + j]);
+  out[l] = acc;
+}
+
+constexpr long long kRun = 64;  // elements per thread (one jump-ahead per run)
+
+// x[e] += coef * z_(e_base + e), z the normal stream (seed, stream)
+__global__ void gen_add_noise_kernel(double* __restrict__ x, long long n, long long e_base, double coef,
+                                     unsigned long long seed, unsigned long long stream) {
+  const long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
+  if (e0 >= n) return;
+  const long long e1 = min(n, e0 + kRun);
+  double z[kRun + 1];
+  gp_normals_range(seed, stream, z, (unsigned long long)(e_base + e0), (unsigned long long)(e_base + e1));
+  for (long long e = e0; e < e1; ++e) x[e] = gp_add(x[e], gp_mul(coef, z[e - e0]));
 }
 
 struct Dims8 {
   long long d[8];
 };
 
-__global__ void gen_hilbert_kernel(double* __restrict__ out, long long n, Dims8 dims, int order) {
+// Hilbert slab: a = 1 / (i_0 + ... + i_{N-1} + 1) (0-based), last index offset by start
+__global__ void gen_hilbert_kernel(double* __restrict__ out, long long n, Dims8 dims, int order,
+                                   long long start) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   long long rem = e, s = 0;
   for (int k = 0; k < order; ++k) {
+    if (k == order - 1) {
+      s += rem + start;
+      break;
+    }
     long long q = rem / dims.d[k];
     s += rem - q * dims.d[k];
     rem = q;
   }
-  out[e] = 1.0 / (double)(s + 1);
+  out[e] = gp_div(1.0, (double)(s + 1));
 }
 
-// out[e] = sum_t w_t prod_n P_n[i_n, t]; profiles packed mode after mode (I_n x R each).
-__global__ void gen_cp_kernel(double* __restrict__ out, long long n, Dims8 dims, int order,
-                              const double* __restrict__ profiles,
-                              const double* __restrict__ weights, int R) {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  long long idx[8];
-  long long rem = e;
-  for (int k = 0; k < order; ++k) {
-    long long q = rem / dims.d[k];
-    idx[k] = rem - q * dims.d[k];
-    rem = q;
-  }
-  double acc = 0.0;
-  for (int t = 0; t < R; ++t) {
-    double v = weights[t];
-    long long off = 0;
+// video slab: sum of separable cosine terms + noise * U[0,1) (stream 400, element e_base + e)
+__global__ void gen_video_kernel(double* __restrict__ out, long long n, Dims8 dims, int order, long long start,
+                                 long long e_base, const double* __restrict__ profiles,
+                                 const double* __restrict__ weights, int R, double noise,
+                                 unsigned long long seed, unsigned long long stream) {
+  const long long e0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kRun;
+  if (e0 >= n) return;
+  const long long e1 = min(n, e0 + kRun);
+  Pcg g(seed, stream);
+  g.advance(2ull * (unsigned long long)(e_base + e0));
+  for (long long e = e0; e < e1; ++e) {
+    long long idx[8];
+    long long rem = e;
     for (int k = 0; k < order; ++k) {
-      v *= profiles[off + idx[k] + dims.d[k] * t];
-      off += dims.d[k] * R;
+      if (k == order - 1) {
+        idx[k] = rem + start;
+        break;
+      }
+      long long q = rem / dims.d[k];
+      idx[k] = rem - q * dims.d[k];
+      rem = q;
     }
-    acc += v;
+    const double v = gp_video_element(idx, dims.d, order, profiles, weights, R);
+    out[e] = gp_add(v, gp_mul(noise, g.next_double()));
   }
-  out[e] = acc;
 }
 
-__global__ void axpby_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                             double coef, double* __restrict__ out, long long n) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x)
-    out[e] = a[e] + coef * b[e];
+static unsigned grid_for(long long n, int per_block) {
+  long long g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > 148LL * 64) g = 148LL * 64;
+  return (unsigned)g;
 }
 
-__global__ void sumsq_kernel(const double* __restrict__ a, long long n,
-                             double* __restrict__ partials) {
-  __shared__ double red[256];
-  double s = 0.0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x)
-    s += a[e] * a[e];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int w = 128; w >= 1; w >>= 1) {
-    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
+cudaError_t launch_gen_ttm(const double* x, long long inner, long long K, long long I, long long outer,
+                           const double* u, long long ldu, double* y, cudaStream_t st) {
+  if (inner * I * outer <= 0) return cudaSuccess;
+  gen_ttm_kernel<<<grid_for(inner * I * outer, 256), 256, 0, st>>>(x, inner, K, I, outer, u, ldu, y); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_fiber_sumsq(const double* x, long long d0, long long nfib, double* out, cudaStream_t st) {
+  if (nfib <= 0) return cudaSuccess;
+  gen_fiber_sumsq_kernel<<<(unsigned)((nfib + 127) / 128), 128, 0, st>>>(x, d0, nfib, out); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_noise_fiber_sumsq(uint64_t seed, uint64_t stream, long long e_base, long long d0,
+                                         long long nfib, double* out, cudaStream_t st) {
+  if (nfib <= 0) return cudaSuccess;
+  gen_noise_fiber_sumsq_kernel<<<(unsigned)((nfib + 127) / 128), 128, 0, st>>>(seed, stream, e_base, d0, nfib,
+                                                                             out); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_slice_sum(const double* fib, long long per, long long nslices, double* out,
+                                 cudaStream_t st) {
+  if (nslices <= 0) return cudaSuccess;
+  gen_slice_sum_kernel<<<(unsigned)((nslices + 127) / 128), 128, 0, st>>>(fib, per, nslices, out); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_add_noise(double* x, long long n, long long e_base, double coef, uint64_t seed,
+                                 uint64_t stream, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const long long threads = (n + kRun - 1) / kRun;
+  gen_add_noise_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(x, n, e_base, coef, seed, stream); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, long long start, long long count,
+                               cudaStream_t st) {
+  if (order < 1 || order > 8) return cudaErrorInvalidValue;
+  Dims8 d{};
+  long long n = 1;
+  for (int k = 0; k < order; ++k) {
+    d.d[k] = dims[k];
+    n *= k == order - 1 ? count : dims[k];
   }
-  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+  if (n <= 0) return cudaSuccess;
+  gen_hilbert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, d, order, start); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_video(double* out, const long long* dims, int order, long long start, long long count,
+                             const double* profiles, const double* weights, int n_terms, double noise,
+                             uint64_t seed, uint64_t stream, cudaStream_t st) {
+  if (order < 1 || order > 8) return cudaErrorInvalidValue;
+  Dims8 d{};
+  long long n = 1, slice = 1;
+  for (int k = 0; k < order; ++k) {
+    d.d[k] = dims[k];
+    n *= k == order - 1 ? count : dims[k];
+    if (k < order - 1) slice *= dims[k];
+  }
+  if (n <= 0) return cudaSuccess;
+  const long long threads = (n + kRun - 1) / kRun;
+  gen_video_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(out, n, d, order, start, start * slice,
+                                                                     profiles, weights, n_terms, noise, seed,
+                                                                     stream); note_launch();
+  return cudaGetLastError();
 }
 
 // at (cols x rows) = a^T, a rows x cols column-major
@@ -210,62 +281,6 @@ cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long 
                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   sum_ranks_kernel<<<148 * 4, 256, 0, st>>>(in_dev, nranks, n, out); note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gen_normals(double* out, long long n, uint64_t seed, uint64_t stream,
-                               cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  long long threads = ((n + 1) / 2 + kPairsPerThread - 1) / kPairsPerThread;
-  gen_normals_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(out, n, seed, stream); note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gen_uniform_add(double* out, long long n, double scale, uint64_t seed,
-                                   uint64_t stream, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  long long threads = (n + kPairsPerThread - 1) / kPairsPerThread;
-  gen_uniform_add_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(out, n, scale, seed,
-                                                                            stream); note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, cudaStream_t st) {
-  if (order < 1 || order > 8) return cudaErrorInvalidValue;
-  Dims8 d{};
-  long long n = 1;
-  for (int k = 0; k < order; ++k) {
-    d.d[k] = dims[k];
-    n *= dims[k];
-  }
-  gen_hilbert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, d, order); note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gen_cp(double* out, const long long* dims, int order, const double* profiles,
-                          const double* weights, int n_terms, cudaStream_t st) {
-  if (order < 1 || order > 8) return cudaErrorInvalidValue;
-  Dims8 d{};
-  long long n = 1;
-  for (int k = 0; k < order; ++k) {
-    d.d[k] = dims[k];
-    n *= dims[k];
-  }
-  gen_cp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, d, order, profiles, weights,
-                                                            n_terms); note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_axpby(const double* a, const double* b, double coef, double* out, long long n,
-                         cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  axpby_kernel<<<148 * 8, 256, 0, st>>>(a, b, coef, out, n); note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_sumsq(const double* a, long long n, double* partials, int nparts,
-                         cudaStream_t st) {
-  sumsq_kernel<<<nparts, 256, 0, st>>>(a, n, partials); note_launch();
   return cudaGetLastError();
 }
 

@@ -109,15 +109,33 @@ cudaError_t launch_ttm_i8_inner(const double* x, long long R, long long K, long 
 cudaError_t launch_column_exponents(const double* x, long long R, long long K, long long O, int* fexp,
                                     cudaStream_t st);
 
-// ---- synthetic generators (device) ----
-// element e of the normal sequence of PCG32 stream (seed, stream), Box-Muller pairs as in rng.hpp
-cudaError_t launch_gen_normals(double* out, long long n, uint64_t seed, uint64_t stream,
+// ---- synthetic generators (gen.cu; definitions in gen/portable_gen.hpp, bit-identical to the host) ----
+// y[a, i, o] = sum_k u[i + ldu k] x[a + inner (k + K o)], i < I (fma chain over k ascending)
+cudaError_t launch_gen_ttm(const double* x, long long inner, long long K, long long I, long long outer,
+                           const double* u, long long ldu, double* y, cudaStream_t st);
+// out[f] = sum_i x[f d0 + i]^2 (fma chain), f < nfib
+cudaError_t launch_gen_fiber_sumsq(const double* x, long long d0, long long nfib, double* out, cudaStream_t st);
+// the same over the normal stream (seed, stream), elements e_base + f d0 + i (regenerated)
+cudaError_t launch_gen_noise_fiber_sumsq(uint64_t seed, uint64_t stream, long long e_base, long long d0,
+                                         long long nfib, double* out, cudaStream_t st);
+// out[l] = sum_j fib[l per + j] (sequential), l < nslices
+cudaError_t launch_gen_slice_sum(const double* fib, long long per, long long nslices, double* out,
+                                 cudaStream_t st);
+// x[e] = x[e] + coef * z_(e_base + e), z the normal stream (seed, stream)
+cudaError_t launch_gen_add_noise(double* x, long long n, long long e_base, double coef, uint64_t seed,
+                                 uint64_t stream, cudaStream_t st);
+// slabs [start, start + count) of the last mode
+cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, long long start, long long count,
                                cudaStream_t st);
-cudaError_t launch_gen_uniform_add(double* out, long long n, double scale, uint64_t seed,
-                                   uint64_t stream, cudaStream_t st);
-cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, cudaStream_t st);
-cudaError_t launch_gen_cp(double* out, const long long* dims, int order, const double* profiles,
-                          const double* weights, int n_terms, cudaStream_t st);
+cudaError_t launch_gen_video(double* out, const long long* dims, int order, long long start, long long count,
+                             const double* profiles, const double* weights, int n_terms, double noise,
+                             uint64_t seed, uint64_t stream, cudaStream_t st);
+
+// ---- verification (verify.cu): out2 = {sum (a - r)^2, sum a^2}, deterministic ----
+size_t diff_sumsq_workspace_doubles();
+cudaError_t launch_diff_sumsq(const double* a, const double* r, long long n, double* work, double* out2,
+                              cudaStream_t st);
+
 // sharded runs: l[t] = g[t] - off if in [0, cnt) else -1
 cudaError_t launch_localize_idx(const long long* g, long long T, long long off, long long cnt,
                                 long long* l, cudaStream_t st);
@@ -129,13 +147,6 @@ cudaError_t launch_sum_ranks(const double* const* in_dev, int nranks, long long 
 // at (cols x rows) = a^T
 cudaError_t launch_transpose(const double* a, long long rows, long long cols, double* at,
                              cudaStream_t st);
-// out = a + coef * b
-cudaError_t launch_axpby(const double* a, const double* b, double coef, double* out, long long n,
-                         cudaStream_t st);
-// partial sums of squares (deterministic, fixed grid) -> host reduces
-cudaError_t launch_sumsq(const double* a, long long n, double* partials, int nparts,
-                         cudaStream_t st);
-
 }  // namespace lmra_dev
 
 namespace lmra_dev {

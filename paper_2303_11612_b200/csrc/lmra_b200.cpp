@@ -30,6 +30,7 @@
 #include "host/host_chain.hpp"
 #include "host/tnsr.hpp"
 #include "kernels/kernels.hpp"
+#include "gen/portable_gen.hpp"
 
 using lmra_dev::ModeView;
 
@@ -2109,96 +2110,284 @@ int lmra_amm_sample_counts(const uint64_t* dims, int order, const lmra_algo_conf
 }
 
 // ------------------------------------------------------------------ generators
-int lmra_gen_hilbert(lmra_context* ctx, const uint64_t* dims, int order, double* x) {
+// Definitions: gen/portable_gen.hpp (bit-identical to the host generators of the oracle).
+// Every generator writes the slab [start, start + count) of the last mode (the whole tensor
+// for start = 0, count = dims[N-1]); a multi-GPU rank generates only its own slab.
+namespace {
+struct GenShape {
+  std::vector<size_t> d;
+  size_t L = 0, slice = 1, start = 0, count = 0;
+};
+GenShape gen_shape(const uint64_t* dims, int order, uint64_t start, uint64_t count) {
+  if (order < 1 || order > 8) throw std::invalid_argument("generator: order must be 1..8");
+  GenShape g;
+  g.d.assign(dims, dims + order);
+  for (size_t v : g.d)
+    if (v == 0) throw std::invalid_argument("tensor dimension must be positive");
+  g.L = g.d.back();
+  for (int k = 0; k + 1 < order; ++k) g.slice *= g.d[k];
+  if (start > g.L || count > g.L - start) throw std::invalid_argument("generator: slab out of range");
+  g.start = start;
+  g.count = count;
+  return g;
+}
+}  // namespace
+
+int lmra_gen_hilbert_slab(lmra_context* ctx, const uint64_t* dims, int order, uint64_t start, uint64_t count,
+                          double* x) {
   return guard([&] {
+    const GenShape g = gen_shape(dims, order, start, count);
     DeviceGuard dg(ctx->device);
-    std::vector<long long> d(dims, dims + order);
-    ck(lmra_dev::launch_gen_hilbert(x, d.data(), order, ctx->stream), "gen_hilbert");
+    std::vector<long long> d(g.d.begin(), g.d.end());
+    ck(lmra_dev::launch_gen_hilbert(x, d.data(), order, (long long)start, (long long)count, ctx->stream),
+       "gen_hilbert");
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }
 
-int lmra_gen_tucker_noise(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims,
-                          int order, double gamma, uint64_t seed, double* x) {
+int lmra_gen_hilbert(lmra_context* ctx, const uint64_t* dims, int order, double* x) {
+  if (order < 1) return lmra_gen_hilbert_slab(ctx, dims, order, 0, 0, x);
+  return lmra_gen_hilbert_slab(ctx, dims, order, 0, dims[order - 1], x);
+}
+
+int lmra_gen_tucker_signal_slab(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims, int order,
+                                uint64_t seed, uint64_t start, uint64_t count, double* x, double* slice_b,
+                                double* slice_e) {
   return guard([&] {
+    using namespace lmra_gen;
+    const GenShape g = gen_shape(dims, order, start, count);
+    if (order == 1 && (start != 0 || count != g.L)) throw std::invalid_argument("generator: an order-1 slab is the whole tensor");
+    std::vector<size_t> cd(core_dims, core_dims + order);
+    for (int n = 0; n < order; ++n)
+      if (cd[n] < 1 || cd[n] > g.d[n]) throw std::invalid_argument("core dimensions must lie in [1, I_n]");
     DeviceGuard dg(ctx->device);
     cudaStream_t st = ctx->stream;
-    Engine eng(ctx);
-    std::vector<size_t> d(dims, dims + order), cd(core_dims, core_dims + order);
-    for (int n = 0; n < order; ++n)
-      if (cd[n] > d[n] || cd[n] < 1 || cd[n] > (size_t)lmra_dev::kMaxWidth)
-        throw std::invalid_argument("core dimensions must lie in [1, min(I_n, 64)]");
-    // G ~ N(0,1) (stream 100), U_n = orthonormal basis of N(0,1) I_n x mu_n (stream 101+n)
-    DevBuf b(prod(cd), st);
-    ck(lmra_dev::launch_gen_normals(b.get(), (long long)prod(cd), seed, 100, st), "normals");
-    std::vector<size_t> cur = cd;
+    // host halves: G (stream 100) and the orthonormal factors U_n (stream 101 + n)
+    std::vector<double> hg(prod(cd));
+    gp_normals_range(seed, kStreamCore, hg.data(), 0, hg.size());
+    std::vector<std::vector<double>> hu(order);
     for (int n = 0; n < order; ++n) {
-      DevBuf m(d[n] * cd[n], st), u(d[n] * cd[n], st), ut(d[n] * cd[n], st);
-      ck(lmra_dev::launch_gen_normals(m.get(), (long long)(d[n] * cd[n]), seed, 101 + n, st), "normals");
-      DevBuf status(1, st);
-      DevBuf uu = eng.orth(m.get(), d[n], cd[n], cd[n], reinterpret_cast<int*>(status.get()));
-      // B <- B x_n U  (U is I_n x mu_n; bt = U^T, mu_n x I_n)
-      ck(lmra_dev::launch_transpose(uu.get(), (long long)d[n], (long long)cd[n], ut.get(), st),
-         "transpose");
-      std::vector<size_t> od = cur;
-      od[n] = d[n];
-      DevBuf y(prod(od), st);
-      ck(lmra_dev::launch_ttm(b.get(), view_of(cur, n), ut.get(), (int)d[n], y.get(), st), "ttm");
-      b = std::move(y);
-      cur = od;
+      hu[n].resize(g.d[n] * cd[n]);
+      gp_orthonormal_factor(g.d[n], cd[n], seed, (uint64_t)n, hu[n].data());
     }
-    const size_t total = prod(d);
-    DevBuf e(total, st);
-    ck(lmra_dev::launch_gen_normals(e.get(), (long long)total, seed, 200, st), "normals");
-    const int parts = 1024;
-    DevBuf pb(parts, st), pe(parts, st);
-    ck(lmra_dev::launch_sumsq(b.get(), (long long)total, pb.get(), parts, st), "sumsq");
-    ck(lmra_dev::launch_sumsq(e.get(), (long long)total, pe.get(), parts, st), "sumsq");
-    std::vector<double> hb(parts), he(parts);
-    ck(cudaMemcpyAsync(hb.data(), pb.get(), parts * 8, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaMemcpyAsync(he.data(), pe.get(), parts * 8, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaStreamSynchronize(st), "sync");
-    double nb = 0, ne = 0;
-    for (int i = 0; i < parts; ++i) {
-      nb += hb[i];
-      ne += he[i];
+    // B = G x_0 U_0 x_1 U_1 ... (mode order), the last product only for the slab's rows
+    Engine eng(ctx);
+    DevBuf cur = eng.upload(hg.data(), hg.size());
+    std::vector<size_t> cdim = cd;
+    for (int n = 0; n < order; ++n) {
+      DevBuf u = eng.upload(hu[n].data(), hu[n].size());
+      const bool last = n == order - 1;
+      const size_t rows = last ? g.count : g.d[n];
+      long long inner = 1, outer = 1;
+      for (int k = 0; k < n; ++k) inner *= (long long)cdim[k];
+      for (int k = n + 1; k < order; ++k) outer *= (long long)cdim[k];
+      double* dst = nullptr;
+      DevBuf y;
+      if (last) {
+        dst = x;
+      } else {
+        y = DevBuf((size_t)inner * rows * (size_t)outer, st);
+        dst = y.get();
+      }
+      ck(lmra_dev::launch_gen_ttm(cur.get(), inner, (long long)cd[n], (long long)rows, outer,
+                                  u.get() + (last ? g.start : 0), (long long)g.d[n], dst, st),
+         "gen_ttm");
+      cdim[n] = g.d[n];
+      if (!last) cur = std::move(y);
+      ck(cudaStreamSynchronize(st), "sync");  // u / cur are released at the end of the iteration
     }
-    const double coef = gamma * std::sqrt(nb) / std::sqrt(ne);
-    ck(lmra_dev::launch_axpby(b.get(), e.get(), coef, x, (long long)total, st), "axpby");
+    // per-slice sums of squares of B and of the noise E (stream 200, regenerated)
+    const size_t d0 = g.d[0];
+    const size_t local = g.slice * g.count;
+    const size_t nfib = local / d0, per = g.slice / d0;
+    const size_t sl = order == 1 ? 1 : g.count;  // an order-1 tensor is one slice
+    const size_t perf = order == 1 ? nfib : per;
+    DevBuf fb(nfib, st), fe(nfib, st), sb(sl, st), se(sl, st);
+    ck(lmra_dev::launch_gen_fiber_sumsq(x, (long long)d0, (long long)nfib, fb.get(), st), "fiber sumsq");
+    ck(lmra_dev::launch_gen_noise_fiber_sumsq(seed, kStreamNoise, (long long)(g.start * g.slice), (long long)d0,
+                                              (long long)nfib, fe.get(), st),
+       "noise sumsq");
+    ck(lmra_dev::launch_gen_slice_sum(fb.get(), (long long)perf, (long long)sl, sb.get(), st), "slice sum");
+    ck(lmra_dev::launch_gen_slice_sum(fe.get(), (long long)perf, (long long)sl, se.get(), st), "slice sum");
+    ck(cudaMemcpyAsync(slice_b, sb.get(), sl * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(slice_e, se.get(), sl * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "sync");
   });
 }
 
-int lmra_gen_video(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms,
-                   double noise, uint64_t seed, double* x) {
+int lmra_gen_noise_coef(const double* slice_b, const double* slice_e, uint64_t nslices, double gamma,
+                        double* coef) {
+  return guard([&] { *coef = lmra_gen::gp_noise_coef(slice_b, slice_e, nslices, gamma); });
+}
+
+int lmra_gen_add_noise_slab(lmra_context* ctx, const uint64_t* dims, int order, uint64_t seed, uint64_t start,
+                            uint64_t count, double coef, double* x) {
   return guard([&] {
+    const GenShape g = gen_shape(dims, order, start, count);
+    DeviceGuard dg(ctx->device);
+    ck(lmra_dev::launch_gen_add_noise(x, (long long)(g.slice * g.count), (long long)(g.start * g.slice), coef,
+                                      seed, lmra_gen::kStreamNoise, ctx->stream),
+       "add noise");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_gen_tucker_noise(lmra_context* ctx, const uint64_t* dims, const uint64_t* core_dims, int order,
+                          double gamma, uint64_t seed, double* x) {
+  return guard([&] {
+    if (order < 1) throw std::invalid_argument("generator: order must be 1..8");
+    const uint64_t L = dims[order - 1];
+    const size_t sl = order == 1 ? 1 : L;
+    std::vector<double> sb(sl), se(sl);
+    if (lmra_gen_tucker_signal_slab(ctx, dims, core_dims, order, seed, 0, L, x, sb.data(), se.data()) != LMRA_OK)
+      throw std::runtime_error(g_err);
+    const double coef = lmra_gen::gp_noise_coef(sb.data(), se.data(), sl, gamma);
+    if (lmra_gen_add_noise_slab(ctx, dims, order, seed, 0, L, coef, x) != LMRA_OK) throw std::runtime_error(g_err);
+  });
+}
+
+int lmra_gen_video_slab(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms, double noise,
+                        uint64_t seed, uint64_t start, uint64_t count, double* x) {
+  return guard([&] {
+    const GenShape g = gen_shape(dims, order, start, count);
+    if (n_terms < 1) throw std::invalid_argument("video generator: n_terms must be positive");
     DeviceGuard dg(ctx->device);
     cudaStream_t st = ctx->stream;
-    std::vector<size_t> d(dims, dims + order);
-    // profiles on the host with glibc cos (bit-identical to the oracle's), packed per mode
     size_t tot = 0;
-    for (size_t v : d) tot += v * n_terms;
+    for (size_t v : g.d) tot += v * n_terms;
     std::vector<double> prof(tot), w(n_terms);
-    for (size_t t = 0; t < n_terms; ++t) {
-      lmra_host::Rng g(seed, 300 + t);
-      w[t] = g.next_double();
-      size_t off = 0;
-      for (int n = 0; n < order; ++n) {
-        double f = 0.5 + 7.5 * g.next_double();
-        double ph = 6.283185307179586476925286766559 * g.next_double();
-        for (size_t i = 0; i < d[n]; ++i) {
-          double xx = static_cast<double>(i) / static_cast<double>(d[n]);
-          prof[off + i + d[n] * t] = std::cos(6.283185307179586476925286766559 * f * xx + ph);
-        }
-        off += d[n] * n_terms;
-      }
-    }
+    lmra_gen::gp_video_profiles(dims, order, n_terms, seed, prof.data(), w.data());
     Engine eng(ctx);
     DevBuf dp = eng.upload(prof.data(), tot), dw = eng.upload(w.data(), n_terms);
-    std::vector<long long> dl(d.begin(), d.end());
-    ck(lmra_dev::launch_gen_cp(x, dl.data(), order, dp.get(), dw.get(), (int)n_terms, st), "gen_cp");
-    ck(lmra_dev::launch_gen_uniform_add(x, (long long)prod(d), noise, seed, 400, st), "uniform");
+    std::vector<long long> dl(g.d.begin(), g.d.end());
+    ck(lmra_dev::launch_gen_video(x, dl.data(), order, (long long)start, (long long)count, dp.get(), dw.get(),
+                                  (int)n_terms, noise, seed, lmra_gen::kStreamVideoNoise, st),
+       "gen_video");
     ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int lmra_gen_video(lmra_context* ctx, const uint64_t* dims, int order, uint64_t n_terms, double noise,
+                   uint64_t seed, double* x) {
+  if (order < 1) return lmra_gen_video_slab(ctx, dims, order, n_terms, noise, seed, 0, 0, x);
+  return lmra_gen_video_slab(ctx, dims, order, n_terms, noise, seed, 0, dims[order - 1], x);
+}
+
+// ------------------------------------------------------------------ verification
+// reconstruct (tucker.cpp:222-227): core x_0 Q_0 x_1 Q_1 ... (mode order), into out
+static void reconstruct_into(lmra_context* ctx, const double* core, const std::vector<size_t>& cdims,
+                             const std::vector<const double*>& factors, const std::vector<size_t>& rows,
+                             double* out) {
+  cudaStream_t st = ctx->stream;
+  Engine eng(ctx);
+  const size_t N = cdims.size();
+  std::vector<size_t> cur = cdims;
+  DevBuf t;
+  const double* src = core;
+  if (N == 0) {
+    ck(cudaMemcpyAsync(out, core, sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+    return;
+  }
+  for (size_t n = 0; n < N; ++n) {
+    const size_t mu = cur[n], I = rows[n];
+    DevBuf qt(I * mu, st);
+    eng.launch("transpose", [&] {
+      return lmra_dev::launch_transpose(factors[n], (long long)I, (long long)mu, qt.get(), st);
+    });
+    std::vector<size_t> od = cur;
+    od[n] = I;
+    const bool last = n + 1 == N;
+    DevBuf y;
+    double* dst = last ? out : nullptr;
+    if (!last) {
+      y = DevBuf(prod(od), st);
+      dst = y.get();
+    }
+    eng.launch("reconstruct", [&] { return lmra_dev::launch_ttm(src, view_of(cur, n), qt.get(), (int)I, dst, st); });
+    ck(cudaStreamSynchronize(st), "sync");
+    cur = od;
+    if (!last) {
+      t = std::move(y);
+      src = t.get();
+    }
+  }
+}
+
+static double relative_error_dev(lmra_context* ctx, const double* a, const double* r, size_t n) {
+  cudaStream_t st = ctx->stream;
+  DevBuf work(lmra_dev::diff_sumsq_workspace_doubles(), st), out(2, st);
+  ck(lmra_dev::launch_diff_sumsq(a, r, (long long)n, work.get(), out.get(), st), "diff_sumsq");
+  double h[2];
+  ck(cudaMemcpyAsync(h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  if (h[1] == 0.0) throw std::invalid_argument("relative_error: zero reference tensor");
+  return std::sqrt(h[0] / h[1]);
+}
+
+// stages a host buffer on the device (or returns the device pointer as is)
+static const double* staged(lmra_context* ctx, const double* p, size_t n, int loc, DevBuf& keep) {
+  if (loc == LMRA_DEVICE) return p;
+  keep = DevBuf(n, ctx->stream);
+  ck(cudaMemcpyAsync(keep.get(), p, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  return keep.get();
+}
+
+int lmra_reconstruct(lmra_context* ctx, const double* core, const uint64_t* core_dims, int order,
+                     const double* const* factors, const uint64_t* factor_rows, int location, double* out,
+                     int out_location) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (order < 0) throw std::invalid_argument("negative tensor order");
+    DeviceGuard dg(ctx->device);
+    std::vector<size_t> cd(core_dims, core_dims + order), rows(factor_rows, factor_rows + order);
+    std::vector<DevBuf> keep(order + 1);
+    const double* c = staged(ctx, core, prod(cd), location, keep[order]);
+    std::vector<const double*> f(order);
+    for (int n = 0; n < order; ++n) f[n] = staged(ctx, factors[n], rows[n] * cd[n], location, keep[n]);
+    const size_t total = prod(rows);
+    DevBuf tmp;
+    double* dst = out;
+    if (out_location == LMRA_HOST) {
+      tmp = DevBuf(total, ctx->stream);
+      dst = tmp.get();
+    }
+    reconstruct_into(ctx, c, cd, f, rows, dst);
+    if (out_location == LMRA_HOST)
+      ck(cudaMemcpyAsync(out, dst, total * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int lmra_relative_error(lmra_context* ctx, const double* a, const double* approx, const uint64_t* dims, int order,
+                        int location, double* re) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard dg(ctx->device);
+    std::vector<size_t> d(dims, dims + order);
+    const size_t n = prod(d);
+    DevBuf ka, kr;
+    const double* da = staged(ctx, a, n, location, ka);
+    const double* dr = staged(ctx, approx, n, location, kr);
+    *re = relative_error_dev(ctx, da, dr, n);
+  });
+}
+
+int lmra_result_relative_error(lmra_context* ctx, const lmra_result* r, const double* a, const uint64_t* dims,
+                               int order, int location, double* re) {
+  return guard([&] {
+    if (!ctx || !r) throw std::invalid_argument("null context or result");
+    if ((size_t)order != r->factors.size()) throw std::invalid_argument("relative_error: shape mismatch");
+    std::vector<size_t> d(dims, dims + order);
+    for (int n = 0; n < order; ++n)
+      if (r->f_rows[n] != d[n]) throw std::invalid_argument("relative_error: shape mismatch");
+    DeviceGuard dg(ctx->device);
+    const size_t n = prod(d);
+    DevBuf ka;
+    const double* da = staged(ctx, a, n, location, ka);
+    DevBuf rec(n, ctx->stream);
+    std::vector<const double*> f(r->factors.begin(), r->factors.end());
+    reconstruct_into(ctx, r->core, r->core_dims, f, r->f_rows, rec.get());
+    *re = relative_error_dev(ctx, da, rec.get(), n);
   });
 }
 

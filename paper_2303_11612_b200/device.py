@@ -140,6 +140,15 @@ def sample_columns(w, regime: str, beta: float, L: int, seed: int, stream: int, 
 
 
 # ---------------------------------------------------------------- BASELINE generators
+# (definitions: csrc/gen/portable_gen.hpp; the oracle's host generators give the same bits)
+def _slab(dims, start, count):
+    L = int(dims[-1])
+    if count is None:
+        start, count = 0, L
+    n = int(np.prod(dims[:-1])) * int(count)
+    return int(start), int(count), n
+
+
 def gen_tucker_noise(dims, core_dims, gamma: float, seed: int, ctx: Context = None):
     ctx = ctx or default_context()
     x = empty(int(np.prod(dims)), ctx.device)
@@ -150,18 +159,90 @@ def gen_tucker_noise(dims, core_dims, gamma: float, seed: int, ctx: Context = No
     return x
 
 
-def gen_hilbert(dims, ctx: Context = None):
+def gen_tucker_signal_slab(dims, core_dims, seed: int, start: int, count: int, ctx: Context = None):
+    """First half of a slab of the Tucker + noise tensor: (x = signal slab, slice sums of
+    squares of the signal and of the noise, host arrays of `count` entries)."""
     ctx = ctx or default_context()
-    x = empty(int(np.prod(dims)), ctx.device)
+    start, count, n = _slab(dims, start, count)
+    x = empty(n, ctx.device)
+    nsl = count if len(dims) > 1 else 1
+    sb, se = np.empty(nsl), np.empty(nsl)
     _torch().cuda.current_stream().synchronize()
-    check(lib.lmra_gen_hilbert(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims), _ptr(x)))
+    check(lib.lmra_gen_tucker_signal_slab(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p),
+                                          _u64(core_dims).ctypes.data_as(_lib.u64p), len(dims), C.c_uint64(seed),
+                                          start, count, _ptr(x), sb.ctypes.data_as(_lib.dblp),
+                                          se.ctypes.data_as(_lib.dblp)))
+    return x, sb, se
+
+
+def noise_coef(slice_b, slice_e, gamma: float) -> float:
+    sb, se = np.ascontiguousarray(slice_b, dtype=np.float64), np.ascontiguousarray(slice_e, dtype=np.float64)
+    out = C.c_double()
+    check(lib.lmra_gen_noise_coef(sb.ctypes.data_as(_lib.dblp), se.ctypes.data_as(_lib.dblp), sb.size,
+                                  C.c_double(gamma), C.byref(out)))
+    return out.value
+
+
+def gen_add_noise_slab(x, dims, seed: int, start: int, count: int, coef: float, ctx: Context = None):
+    ctx = ctx or default_context()
+    start, count, _ = _slab(dims, start, count)
+    _torch().cuda.current_stream().synchronize()
+    check(lib.lmra_gen_add_noise_slab(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims),
+                                      C.c_uint64(seed), start, count, C.c_double(coef), _ptr(x)))
     return x
 
 
-def gen_video(dims, n_terms: int = 30, noise: float = 0.05, seed: int = 1, ctx: Context = None):
+def gen_hilbert(dims, ctx: Context = None, start: int = 0, count: int = None):
     ctx = ctx or default_context()
-    x = empty(int(np.prod(dims)), ctx.device)
+    start, count, n = _slab(dims, start, count)
+    x = empty(n, ctx.device)
     _torch().cuda.current_stream().synchronize()
-    check(lib.lmra_gen_video(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims),
-                             C.c_uint64(n_terms), C.c_double(noise), C.c_uint64(seed), _ptr(x)))
+    check(lib.lmra_gen_hilbert_slab(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims), start, count,
+                                    _ptr(x)))
     return x
+
+
+def gen_video(dims, n_terms: int = 30, noise: float = 0.05, seed: int = 1, ctx: Context = None,
+              start: int = 0, count: int = None):
+    ctx = ctx or default_context()
+    start, count, n = _slab(dims, start, count)
+    x = empty(n, ctx.device)
+    _torch().cuda.current_stream().synchronize()
+    check(lib.lmra_gen_video_slab(ctx.handle, _u64(dims).ctypes.data_as(_lib.u64p), len(dims),
+                                  C.c_uint64(n_terms), C.c_double(noise), C.c_uint64(seed), start, count,
+                                  _ptr(x)))
+    return x
+
+
+# ---------------------------------------------------------------- verification
+def relative_error(x, dims, core, factors, ctx: Context = None) -> float:
+    """||x - reconstruct(core, factors)|| / ||x|| on the device (tucker.cpp:222-240).  x: flat
+    float64 CUDA tensor; core (numpy, reference layout) and factors (numpy I_n x mu_n) are
+    uploaded.  Used for both sides of the parity checks."""
+    ctx = ctx or default_context()
+    torch = _torch()
+    core = np.asarray(core)
+    cdims = list(core.shape)
+    rec = empty(int(np.prod(dims)), ctx.device)
+    cd = torch.from_numpy(np.ascontiguousarray(core.ravel(order="F"))).cuda(ctx.device)
+    fs = [torch.from_numpy(np.ascontiguousarray(np.asarray(f).ravel(order="F"))).cuda(ctx.device)
+          for f in factors]
+    ptrs = (C.c_void_p * len(fs))(*[f.data_ptr() for f in fs])
+    rows = _u64([np.asarray(f).shape[0] for f in factors])
+    torch.cuda.current_stream().synchronize()
+    check(lib.lmra_reconstruct(ctx.handle, _ptr(cd), _u64(cdims).ctypes.data_as(_lib.u64p), len(cdims), ptrs,
+                               rows.ctypes.data_as(_lib.u64p), _lib.LMRA_DEVICE, _ptr(rec), _lib.LMRA_DEVICE))
+    out = C.c_double()
+    check(lib.lmra_relative_error(ctx.handle, _ptr(x), _ptr(rec), _u64(dims).ctypes.data_as(_lib.u64p), len(dims),
+                                  _lib.LMRA_DEVICE, C.byref(out)))
+    return out.value
+
+
+def result_relative_error(result, x, dims, ctx: Context = None) -> float:
+    """relative_error of a raw result (run_raw) against the device tensor x it decomposed."""
+    ctx = ctx or default_context()
+    out = C.c_double()
+    _torch().cuda.current_stream().synchronize()
+    check(lib.lmra_result_relative_error(ctx.handle, result.handle, _ptr(x), _u64(dims).ctypes.data_as(_lib.u64p),
+                                         len(dims), _lib.LMRA_DEVICE, C.byref(out)))
+    return out.value

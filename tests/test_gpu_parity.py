@@ -26,8 +26,9 @@ def _to_dev(a_flat):
     return torch.from_numpy(np.ascontiguousarray(a_flat)).cuda()
 
 
-def compare(gpu, ref, a, *, tol=TOL, check_core=True, check_columns=True, check_re=True):
-    """Returns a dict of metrics; asserts the parity contract."""
+def compare(gpu, ref, a, *, tol=TOL, check_core=True, check_columns=True, check_re=True, re_fn=None):
+    """Returns a dict of metrics; asserts the parity contract.  re_fn(core, factors) -> RE
+    replaces the numpy reconstruction (full-size tensors: device RE, lmra_relative_error)."""
     out = {"sines": [], "full_sines": []}
     for n, (qg, qo) in enumerate(zip(gpu.factors, ref.factors)):
         assert qg.shape == qo.shape, (n, qg.shape, qo.shape)
@@ -49,8 +50,12 @@ def compare(gpu, ref, a, *, tol=TOL, check_core=True, check_columns=True, check_
         cd = np.linalg.norm(gpu.core - ref.core) / np.linalg.norm(ref.core)
         out["core"] = cd
         assert cd <= tol, f"core rel diff {cd:.3g}"
-    re_g = relative_error(a, gpu.core, gpu.factors)
-    re_o = relative_error(a, ref.core, ref.factors)
+    if re_fn is None:
+        re_g = relative_error(a, gpu.core, gpu.factors)
+        re_o = relative_error(a, ref.core, ref.factors)
+    else:
+        re_g = re_fn(gpu.core, gpu.factors)
+        re_o = re_fn(ref.core, ref.factors)
     out["re"] = (re_g, re_o)
     if check_re:
         assert abs(re_g - re_o) <= tol * max(re_o, 1e-300), f"RE {re_g!r} vs {re_o!r}"
@@ -58,6 +63,28 @@ def compare(gpu, ref, a, *, tol=TOL, check_core=True, check_columns=True, check_
 
 
 # ---------------------------------------------------------------- primitives
+@pytest.mark.parametrize("dims,core", [((20, 18, 16), (4, 5, 3)), ((9, 7, 5, 3), (3, 3, 2, 2)), ((64, 33), (7, 5))])
+def test_device_relative_error_matches_oracle(gpu_ctx, orc, lmra, dims, core):
+    # reconstruct + relative_error (tucker.cpp:222-240) on the device vs the oracle's loop
+    from paper_2303_11612_b200 import device
+    x = orc.gen_tucker_noise(list(dims), list(core), 3e-2, 5)
+    cfg = dict(rank=list(core), seed=2)
+    ref = orc.run("alg1", x, list(dims), orc.AlgoConfig(**cfg))
+    want = orc.relative_error(x, list(dims), ref)
+    got = device.relative_error(_to_dev(x), list(dims), ref.core, ref.factors, ctx=gpu_ctx)
+    assert abs(got - want) <= 1e-13 * want, (got, want)
+    # the result-handle form (reconstructs the run's own device core / factors)
+    r = lmra.run_raw("alg1", lmra.DenseTensor.from_flat(x, list(dims)), lmra.AlgoConfig(**cfg), ctx=gpu_ctx)
+    dec = r.to_host()
+    got2 = device.result_relative_error(r, _to_dev(x), list(dims), ctx=gpu_ctx)
+    r.free()
+    assert abs(got2 - relative_error(x.reshape(dims, order="F"), dec.core, dec.factors)) <= 1e-13 * want
+    # the reference's error surface
+    with pytest.raises(lmra.LmraInvalidArgument, match="zero reference tensor"):
+        device.relative_error(_to_dev(np.zeros_like(x)), list(dims), ref.core, ref.factors, ctx=gpu_ctx)
+
+
+
 @pytest.mark.parametrize("dims,mode,m", [
     ((7, 5, 3), 0, 4), ((7, 5, 3), 1, 4), ((7, 5, 3), 2, 2),
     ((33, 40, 17), 0, 13), ((33, 40, 17), 1, 64), ((33, 40, 17), 2, 70),
