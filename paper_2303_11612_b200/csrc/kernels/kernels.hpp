@@ -75,6 +75,15 @@ size_t orth_workspace_doubles(long long I, int s);
 cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, double* work,
                         int* status, cudaStream_t st);
 
+// The same in two halves (orth.cu): launch_orth_basis writes Q_C (I x s), an orthonormal basis of
+// C's columns (pivoted Householder TSQR, no Jacobi); launch_orth_finish then runs the s x s Jacobi
+// and writes U = Q_C U_R(:, :mu) with the sign rule plus U_R' (s x mu) = U_R(:, :mu) with U's
+// column signs, so X x_n U^T = (X x_n Q_C^T) x_n U_R'^T.  Same workspace for both calls.
+size_t orth_split_workspace_doubles(long long I, int s);
+cudaError_t launch_orth_basis(const double* c, long long I, int s, double* qc, double* work, cudaStream_t st);
+cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, double* u, double* ur_signed,
+                               double* work, int* status, cudaStream_t st);
+
 // qr_project_extract (linalg.cpp:89-99) building blocks (orth.cu):
 // R (s x s, column-major) of a tall m x s matrix (m >= s) by Householder TSQR.
 size_t r_factor_workspace_doubles(long long m, int s);

@@ -809,10 +809,18 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
 // Core: one CTA.  S (m x s, lds) -> pivoted QR -> Jacobi on R^T -> Y = Q [U_R(:, :mu); 0].
 // final != 0: sign-fix Y and write it to out (ld ldo); else write Y to out unsigned.
 // ---------------------------------------------------------------------------
+// phase (the split used by the core / shrink contractions, launch_orth_basis + launch_orth_finish):
+//   kOrthFull   the whole chain above;
+//   kOrthBasis  pivoted QR only: G = R^T (unscaled) to gbuf (s x s) and Y = Q [I_s; 0] (m x s) to
+//               out -- the basis Q_C of the sketch, before any Jacobi;
+//   kOrthJacobi Jacobi on gbuf's G only: U_R(:, :mu) (singular values descending) to ur (s x mu).
+constexpr int kOrthFull = 0, kOrthBasis = 1, kOrthJacobi = 2;
+
 template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
-    int ldo, int final_level, int* status, double jacobi_tol, int clustered) {
+    int ldo, int final_level, int* status, double jacobi_tol, int clustered, int phase,
+    double* __restrict__ gbuf, double* __restrict__ ur) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   extern __shared__ __align__(16) double sm[];
@@ -842,27 +850,51 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     }
   }
 
-  load_tile(S, lds, m, s, Vs, ldv, 32 * RPL);
-  __syncthreads();
-  double a[kCW][RPL];
-  cw_load(Vs, ldv, m, s, a);
-  reg_qr(a, m, s, q, true);
-  if ((int)threadIdx.x < s) q.ipiv[q.piv[threadIdx.x]] = threadIdx.x;
-  __syncthreads();
-  // G = R^T (lower triangle), reflectors to Vs in logical column order
+  if (phase == kOrthJacobi) {  // G from the basis phase
+    for (int e = threadIdx.x; e < s * s; e += kQThreads) G[e] = gbuf[e];
+    __syncthreads();
+  } else {
+    load_tile(S, lds, m, s, Vs, ldv, 32 * RPL);
+    __syncthreads();
+    double a[kCW][RPL];
+    cw_load(Vs, ldv, m, s, a);
+    reg_qr(a, m, s, q, true);
+    if ((int)threadIdx.x < s) q.ipiv[q.piv[threadIdx.x]] = threadIdx.x;
+    __syncthreads();
+    // G = R^T (lower triangle), reflectors to Vs in logical column order
 #pragma unroll
-  for (int j = 0; j < kCW; ++j) {
-    const int c = w + kQWarps * j;
-    if (c >= s) continue;
-    const int k = q.ipiv[c];
+    for (int j = 0; j < kCW; ++j) {
+      const int c = w + kQWarps * j;
+      if (c >= s) continue;
+      const int k = q.ipiv[c];
 #pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = l + 32 * i;
-      if (r < s) G[k + (size_t)s * r] = r <= k && r < m ? a[j][i] : 0.0;
-      if (r > k && r < m) Vs[r + (size_t)ldv * k] = a[j][i];
+      for (int i = 0; i < RPL; ++i) {
+        const int r = l + 32 * i;
+        if (r < s) G[k + (size_t)s * r] = r <= k && r < m ? a[j][i] : 0.0;
+        if (r > k && r < m) Vs[r + (size_t)ldv * k] = a[j][i];
+      }
+    }
+    __syncthreads();
+    if (phase == kOrthBasis) {  // G out, Y = Q [I_s; 0] (logical column order) to out
+      for (int e = threadIdx.x; e < s * s; e += kQThreads) gbuf[e] = G[e];
+      double y[kCW][RPL];
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        const int c = w + kQWarps * j;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) y[j][i] = (c < s && l + 32 * i == c) ? 1.0 : 0.0;
+      }
+      reg_apply(y, s, Vs, ldv, q.tau, min(m, s), 0);
+      __syncthreads();  // every warp is done reading the reflectors
+      cw_store(y, m, s, Vs, ldv);
+      __syncthreads();
+      for (int e = threadIdx.x; e < m * s; e += kQThreads) {
+        const int i = e % m, c = e / m;
+        out[i + (size_t)ldo * c] = Vs[i + (size_t)ldv * c];
+      }
+      return;
     }
   }
-  __syncthreads();
   {  // G *= 2^-e with max |G| in [1, 2) (exact; only J and the singular values' order are used)
     double mx = 0.0;
     for (int e = threadIdx.x; e < s * s; e += kQThreads) mx = fmax(mx, fabs(G[e]));
@@ -909,6 +941,14 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     perm[rank] = c;
   }
   __syncthreads();
+  if (phase == kOrthJacobi) {  // U_R(:, :mu) in descending singular-value order
+    for (int e = threadIdx.x; e < s * mu; e += kQThreads) {
+      const int r = e % s, c = e / s;
+      ur[r + (size_t)s * c] = J[r + (size_t)n * perm[c]];
+    }
+    if (threadIdx.x == 0 && status) *status = converged ? 0 : 1;
+    return;
+  }
   // Y = [U_R(:, :mu) ; 0] with U_R = J(0:s, perm), then the reflectors
   double y[kCW][RPL];
 #pragma unroll
@@ -1103,7 +1143,8 @@ cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, doub
 
 template <int RPL>
 cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, int final_level,
-                 int* status, double tol, cudaStream_t st) {
+                 int* status, double tol, cudaStream_t st, int phase = kOrthFull, double* gbuf = nullptr,
+                 double* ur = nullptr) {
   static unsigned long long done = 0;
   const size_t smem = core_smem(m, s);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_core_kernel<RPL>), kOrthSmemMax, done);
@@ -1113,7 +1154,7 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
   // (only for wide sketches: below s = 48 the cluster launch and the DSMEM handoff cost more
   // than the J rotations they move -- measured on cfg1 / cfg2 / cfg3)
   static const bool cluster_ok = !(getenv("LMRA_ORTH_CLUSTER") && getenv("LMRA_ORTH_CLUSTER")[0] == '0');
-  const bool clustered = cluster_ok && s >= 48;
+  const bool clustered = cluster_ok && s >= 48 && phase != kOrthBasis;
   if (clustered) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2);
@@ -1131,11 +1172,11 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
     cfg.numAttrs = 2;
     note_launch();
     const cudaError_t le = cudaLaunchKernelEx(&cfg, orth_core_kernel<RPL>, S, m, s, m, mu, out, ldo, final_level,
-                                              status, tol, 1);
+                                              status, tol, 1, phase, gbuf, ur);
     if (le != cudaSuccess) return le;
   } else {
     const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu,
-                                      out, ldo, final_level, status, tol, 0);
+                                      out, ldo, final_level, status, tol, 0, phase, gbuf, ur);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
@@ -1174,7 +1215,8 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   std::vector<OrthLevel> lv = plan_levels(I, s, &used);
   cudaError_t e;
   if (lv.empty())
-    return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st);
+    return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st, kOrthFull, nullptr,
+                                               nullptr);
   std::vector<size_t> wbuf(lv.size());
   for (size_t l = 0; l < lv.size(); ++l) {
     wbuf[l] = used;
@@ -1195,7 +1237,7 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   const OrthLevel& last = lv.back();
   const int mB = last.nb * s;
   e = LMRA_RPL_DISPATCH(rpl_for(mB), core)(work + last.w_off, mB, s, mu, work + wbuf.back(), mB, 0,
-                                          status, tol, st);
+                                          status, tol, st, kOrthFull, nullptr, nullptr);
   if (e != cudaSuccess) return e;
   // back down
   for (int l = (int)lv.size() - 1; l >= 0; --l) {
@@ -1214,6 +1256,126 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// The split orthonormalisation: the basis Q_C (I x s) of the sketch first, the s x s Jacobi
+// after it (the big contraction that follows runs on Q_C while the Jacobi finishes), then
+// U = Q_C U_R(:, :mu) with the sign rule; U_R' = U_R(:, :mu) D carries the same column signs D
+// so that X x_n U^T = (X x_n Q_C^T) x_n U_R'^T.
+// ---------------------------------------------------------------------------
+// one CTA per column c: u(:, c) = Q_C U_R(:, c) (fma over k in order), then the sign rule of
+// fix_signs (linalg.cpp:13-29): the largest |u| (first index on ties) made >= 0, and the same
+// sign applied to U_R(:, c).
+__global__ void __launch_bounds__(256) orth_rotate_signfix_kernel(const double* __restrict__ qc, long long I, int s,
+                                                                  const double* __restrict__ ur, int mu,
+                                                                  double* __restrict__ u, double* __restrict__ ur_s) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x;
+  __shared__ double urc[64];
+  __shared__ double bv[8];
+  __shared__ long long bi[8];
+  __shared__ double sgn;
+  for (int k = threadIdx.x; k < s; k += blockDim.x) urc[k] = ur[k + (size_t)s * c];
+  __syncthreads();
+  double best = 0.0;
+  long long bidx = -1;
+  for (long long i = threadIdx.x; i < I; i += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < s; ++k) acc = fma(qc[i + I * k], urc[k], acc);
+    u[i + I * c] = acc;
+    const double a = fabs(acc);
+    if (a > best) {  // rows visited in increasing order per thread: strict > keeps the first
+      best = a;
+      bidx = i;
+    }
+  }
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int msk = 16; msk >= 1; msk >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, msk);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bidx, msk);
+    if (ob > best || (ob == best && oi >= 0 && (bidx < 0 || oi < bidx))) {
+      best = ob;
+      bidx = oi;
+    }
+  }
+  if (l == 0) {
+    bv[w] = best;
+    bi[w] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    long long ix = -1;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k)
+      if (bv[k] > b || (bv[k] == b && bi[k] >= 0 && (ix < 0 || bi[k] < ix))) {
+        b = bv[k];
+        ix = bi[k];
+      }
+    sgn = (ix >= 0 && u[ix + I * c] < 0.0) ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  const double sg = sgn;
+  for (int k = threadIdx.x; k < s; k += blockDim.x) ur_s[k + (size_t)s * c] = sg * urc[k];
+  if (sg < 0.0)
+    for (long long i = threadIdx.x; i < I; i += blockDim.x) u[i + I * c] = -u[i + I * c];
+}
+
+size_t orth_split_workspace_doubles(long long I, int s) {
+  return orth_workspace_doubles(I, s) + 2 * (size_t)s * s + 64;
+}
+
+// workspace: [orth tree | G (s x s) | U_R (s x s)]
+cudaError_t launch_orth_basis(const double* c, long long I, int s, double* qc, double* work, cudaStream_t st) {
+  if (s < 1 || s > kOrthMaxS || I < s) return cudaErrorInvalidValue;
+  size_t used = 0;
+  std::vector<OrthLevel> lv = plan_levels(I, s, &used);
+  double* gbuf = work + orth_workspace_doubles(I, s);
+  cudaError_t e;
+  if (lv.empty())
+    return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, s, qc, (int)I, 0, nullptr, 0.0, st, kOrthBasis, gbuf,
+                                               nullptr);
+  std::vector<size_t> wbuf(lv.size());
+  for (size_t l = 0; l < lv.size(); ++l) {
+    wbuf[l] = used;
+    used += (size_t)lv[l].nb * s * s;
+  }
+  for (size_t l = 0; l < lv.size(); ++l) {
+    const OrthLevel& L = lv[l];
+    const double* A = l == 0 ? c : work + lv[l - 1].w_off;
+    e = LMRA_RPL_DISPATCH(rpl_for((L.m + L.nb - 1) / L.nb), leaf_qr)(A, L.m, s, L.nb, work + L.v_off,
+                                                                      work + L.tau_off, work + L.w_off, L.nb * s, st);
+    if (e != cudaSuccess) return e;
+  }
+  const OrthLevel& last = lv.back();
+  const int mB = last.nb * s;
+  e = LMRA_RPL_DISPATCH(rpl_for(mB), core)(work + last.w_off, mB, s, s, work + wbuf.back(), mB, 0, nullptr, 0.0, st,
+                                          kOrthBasis, gbuf, nullptr);
+  if (e != cudaSuccess) return e;
+  for (int l = (int)lv.size() - 1; l >= 0; --l) {
+    const OrthLevel& L = lv[l];
+    double* out = l == 0 ? qc : work + wbuf[l - 1];
+    e = LMRA_RPL_DISPATCH(rpl_for((L.m + L.nb - 1) / L.nb), leaf_apply)(
+        work + L.v_off, L.m, s, L.nb, work + L.tau_off, work + wbuf[l], L.nb * s, s, out, nullptr, nullptr, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, double* u, double* ur_signed,
+                               double* work, int* status, cudaStream_t st) {
+  if (s < 1 || s > kOrthMaxS || mu < 1 || mu > s || I < s) return cudaErrorInvalidValue;
+  double tol = 8.0 * s * 0x1.0p-53;
+  if (const char* env = getenv("LMRA_JACOBI_TOL")) tol = atof(env);
+  double* gbuf = work + orth_workspace_doubles(I, s);
+  double* ur = gbuf + (size_t)s * s;
+  cudaError_t e = LMRA_RPL_DISPATCH(rpl_for(s), core)(nullptr, s, s, mu, nullptr, s, 0, status, tol, st,
+                                                      kOrthJacobi, gbuf, ur);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(orth_rotate_signfix_kernel, dim3(mu), dim3(256), 0, st, qc, I, s, (const double*)ur, mu, u,
+                    ur_signed);
+}
 
 // ---------------------------------------------------------------------------
 // QR-proxy extraction (qr_project_extract, linalg.cpp:89-99) building blocks

@@ -841,6 +841,24 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
 
   // QR-proxy (alg6/alg7): the projected tensor P and U1 of a mode whose contraction reads P
   std::vector<Engine::QrProxy> qrp(N);
+  // Split orthonormalisation (T-HOSVD on large tensors): each mode publishes its sketch basis
+  // Q_C (I x s) before the s x s Jacobi, the core's long contractions run on Q_C while the
+  // Jacobis finish, and the small rotations U_R'^T are applied to the s_0 x s_1 x ... core at
+  // the end (X x_n Q^T = (X x_n Q_C^T) x_n U_R'^T, modes commute).  LMRA_ORTH_SPLIT=0/1 forces.
+  struct SplitOrth {
+    DevBuf qc, urs, work;
+    cudaEvent_t basis = nullptr;
+  };
+  std::vector<SplitOrth> split(N);
+  struct SplitGuard {
+    std::vector<SplitOrth>& v;
+    ~SplitGuard() {
+      for (auto& so : v)
+        if (so.basis) cudaEventDestroy(so.basis);
+    }
+  } split_guard{split};
+  bool split_orth = !sequential && !qr && prod(in.dims) >= (size_t(1) << 25);
+  if (const char* e = getenv("LMRA_ORTH_SPLIT")) split_orth = !sequential && !qr && e[0] == '1';
   auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
                          size_t n) -> DevBuf {
     cudaStream_t s_ = e.st_;
@@ -885,6 +903,23 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
               r.mu[n], mu);
     res->f_rows[n] = I;
     res->f_cols[n] = mu;
+    if (split_orth) {
+      SplitOrth& so = split[n];
+      so.work = DevBuf(lmra_dev::orth_split_workspace_doubles((long long)I, (int)s), s_);
+      so.qc = DevBuf(I * s, s_);
+      e.launch("orth_basis", [&] {
+        return lmra_dev::launch_orth_basis(c.get(), (long long)I, (int)s, so.qc.get(), so.work.get(), s_);
+      });
+      ck(cudaEventCreateWithFlags(&so.basis, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(so.basis, s_), "event");
+      DevBuf u(I * mu, s_);
+      so.urs = DevBuf(s * mu, s_);
+      e.launch("orth_jacobi", [&] {
+        return lmra_dev::launch_orth_finish(so.qc.get(), (long long)I, (int)s, (int)mu, u.get(), so.urs.get(),
+                                            so.work.get(), status_i + n, s_);
+      });
+      return u;
+    }
     return e.orth(c.get(), I, s, mu, status_i + n);
   };
 
@@ -949,6 +984,16 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     for (size_t k = 0; k < idx.size(); ++k) {
       const size_t n = idx[k];
       const bool next1 = k + 1 < idx.size() && idx[k + 1] == 1;
+      if (split_orth) {  // the contraction with the basis Q_C, as soon as it exists
+        ck(cudaStreamWaitEvent(st, split[n].basis, 0), "wait");
+        const size_t sn = r.sketch[n];
+        DevBuf y = eng.ttm_mode0(src, cur, n, split[n].qc.get(), sn, src == in.x ? w0 : nullptr,
+                                 "core_ttm" + std::to_string(step++), &chain, next1);
+        cur[n] = sn;
+        t = std::move(y);
+        src = t.get();
+        continue;
+      }
       ck(cudaStreamWaitEvent(st, mode_done[n], 0), "wait");
       if (qr && k == 0) {  // X x_n (Q U1)^T = P x_n U1^T: read the projected tensor
         std::vector<size_t> pd = cur;
@@ -964,6 +1009,15 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       t = std::move(y);
       src = t.get();
     }
+    if (split_orth)  // the rotations U_R'^T on the s_0 x s_1 x ... core, each after its Jacobi
+      for (size_t k = 0; k < idx.size(); ++k) {
+        const size_t n = idx[k];
+        ck(cudaStreamWaitEvent(st, mode_done[n], 0), "wait");
+        DevBuf y = eng.ttm(src, cur, n, split[n].urs.get(), res->f_cols[n], "core_rot");
+        cur[n] = res->f_cols[n];
+        t = std::move(y);
+        src = t.get();
+      }
     res->core_dims = cur;
     res->core = t.detach();
   } else {
@@ -2239,10 +2293,14 @@ int lmra_gen_tucker_noise(lmra_context* ctx, const uint64_t* dims, const uint64_
     const uint64_t L = dims[order - 1];
     const size_t sl = order == 1 ? 1 : L;
     std::vector<double> sb(sl), se(sl);
-    if (lmra_gen_tucker_signal_slab(ctx, dims, core_dims, order, seed, 0, L, x, sb.data(), se.data()) != LMRA_OK)
-      throw std::runtime_error(g_err);
+    auto rethrow = [](int rc) {  // keep the error class of the step that failed
+      if (rc == LMRA_EINVAL) throw std::invalid_argument(g_err);
+      if (rc == LMRA_ECUDA) throw CudaError(g_err);
+      if (rc != LMRA_OK) throw std::runtime_error(g_err);
+    };
+    rethrow(lmra_gen_tucker_signal_slab(ctx, dims, core_dims, order, seed, 0, L, x, sb.data(), se.data()));
     const double coef = lmra_gen::gp_noise_coef(sb.data(), se.data(), sl, gamma);
-    if (lmra_gen_add_noise_slab(ctx, dims, order, seed, 0, L, coef, x) != LMRA_OK) throw std::runtime_error(g_err);
+    rethrow(lmra_gen_add_noise_slab(ctx, dims, order, seed, 0, L, coef, x));
   });
 }
 
