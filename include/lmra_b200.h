@@ -11,7 +11,9 @@
  *   rand_sthosvd_amm    (tucker.hpp:102)      alg5  ->  lmra_run_algorithm(LMRA_ALG5, ...)
  *   run_algorithm       (tucker.hpp:110-111)        ->  lmra_run_algorithm
  *   amm_sample_counts   (tucker.hpp:116-117)        ->  lmra_amm_sample_counts
- *   thread_cap          (tucker.hpp:121)            ->  (device count knob: env LMRA_NUM_GPUS)
+ *   thread_cap          (tucker.hpp:121)            ->  lmra_thread_cap (+ lmra_device_cap: LMRA_NUM_GPUS)
+ *   parse_algorithm / algorithm_id / all_algorithm_ids (tucker.hpp:59-61) -> lmra_parse_algorithm, ...
+ *   t_hosvd / st_hosvd / hooi (tucker.hpp:70-89)    ->  lmra_run_algorithm(LMRA_THOSVD / STHOSVD / HOOI)
  *   AlgoConfig          (tucker.hpp:32-45)          ->  lmra_algo_config
  *   TuckerDecomposition (tucker.hpp:27-30)          ->  lmra_result (core + factors)
  *   mode_n_product      (tensor.hpp:56-57)          ->  lmra_mode_n_product
@@ -51,7 +53,9 @@ enum lmra_status { LMRA_OK = 0, LMRA_EINVAL = 1, LMRA_ERUNTIME = 2, LMRA_ECUDA =
 /* Algorithm ids (tucker.hpp:47-57). The randomized family: power scheme (alg1/alg2), AMM
  * (alg4/alg5) and the QR-proxy extraction (alg6/alg7, tucker.cpp:422-454). */
 enum lmra_algorithm {
-  LMRA_ALG1 = 1, LMRA_ALG2 = 2, LMRA_ALG4 = 4, LMRA_ALG5 = 5, LMRA_ALG6 = 6, LMRA_ALG7 = 7
+  LMRA_ALG1 = 1, LMRA_ALG2 = 2, LMRA_ALG4 = 4, LMRA_ALG5 = 5, LMRA_ALG6 = 6, LMRA_ALG7 = 7,
+  /* the deterministic baselines (tucker.cpp:242-316): factors from the full unfoldings */
+  LMRA_THOSVD = 10, LMRA_STHOSVD = 11, LMRA_HOOI = 12
 };
 /* ProbRegime (sketching.hpp:31) */
 enum lmra_regime { LMRA_OPTIMAL = 0, LMRA_NEARLY_OPTIMAL = 1, LMRA_UNIFORM = 2 };
@@ -75,10 +79,25 @@ typedef struct {
   uint64_t n_order;
   uint64_t seed;              /* default 0 */
   int32_t strategy;           /* lmra_strategy, default A */
+  int32_t hooi_max_sweeps;    /* default 50 */
+  double hooi_tol;            /* default 1e-8 */
 } lmra_algo_config;
 
 /* Fills the reference's defaults (tucker.hpp:32-45). */
 void lmra_algo_config_init(lmra_algo_config* cfg);
+
+/* parse_algorithm / algorithm_id / all_algorithm_ids (tucker.hpp:59-61, tucker.cpp:190-220):
+ * lmra_parse_algorithm returns 1 and sets *algorithm for a known id ("thosvd", "sthosvd",
+ * "hooi", "alg1" ... "alg7"), else 0; lmra_algorithm_id returns "?" for an unknown code;
+ * lmra_all_algorithm_ids fills up to max_ids ids in the reference's order and returns 9. */
+int lmra_parse_algorithm(const char* id, int* algorithm);
+const char* lmra_algorithm_id(int algorithm);
+int lmra_all_algorithm_ids(const char** ids, int max_ids);
+/* thread_cap (tucker.hpp:121, tucker.cpp:164-172): LMRA_NUM_THREADS, default 1, in [1, 64].
+ * lmra_device_cap: the same idiom for devices, LMRA_NUM_GPUS, default 1, clamped to the
+ * visible device count -- the C++ drop-in (lmra_b200.hpp) runs on that many GPUs. */
+int lmra_thread_cap(void);
+int lmra_device_cap(void);
 
 /* Parity overrides: per-mode Omega (I_n x s, column-major, host) and per-mode sampled
  * columns (indices + scales, host).  NULL arrays / NULL entries mean "draw them from
@@ -118,14 +137,25 @@ int lmra_context_set_thread_comm(lmra_context* ctx, void* group, int rank);
 /* Shard plan: contiguous balanced slabs, rank r owns [start, start + count). */
 int lmra_shard_range(uint64_t extent, int nranks, int rank, uint64_t* start, uint64_t* count);
 
-/* run_algorithm (tucker.cpp:456-470) for alg1/alg2/alg4/alg5. x: dense tensor on the host
+/* run_algorithm (tucker.cpp:456-470) for every algorithm id. x: dense tensor on the host
  * (x_location = LMRA_HOST, copied in) or device (LMRA_DEVICE, read in place, never
  * mutated).  The call returns once the result is complete on the device. */
 int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const uint64_t* dims,
                        int order, int x_location, const lmra_algo_config* cfg,
                        const lmra_overrides* overrides, lmra_result** out);
 
+/* The same on ndev devices from ONE process (one host thread and context per device, the
+ * tensor split along its last mode as with one process per GPU; NCCL between distinct
+ * devices, else the in-process communicator).  x: the whole tensor on the host, or on
+ * devices[0] (x_location = LMRA_DEVICE; each rank's slab is copied peer to peer).  The
+ * result lives on devices[0]. */
+int lmra_run_algorithm_multigpu(int ndev, const int* devices, int algorithm, const double* x, const uint64_t* dims,
+                                int order, int x_location, const lmra_algo_config* cfg,
+                                const lmra_overrides* overrides, lmra_result** out);
+
 int lmra_result_order(const lmra_result* r);
+/* HooiStats (tucker.hpp:73-76) of a hooi run: converged flag and sweeps taken (0, 0 otherwise) */
+void lmra_result_hooi_stats(const lmra_result* r, int* converged, int* sweeps);
 void lmra_result_core_dims(const lmra_result* r, uint64_t* dims);
 int lmra_result_copy_core(const lmra_result* r, double* dst, int dst_location);
 void lmra_result_factor_dims(const lmra_result* r, int mode, uint64_t* rows, uint64_t* cols);

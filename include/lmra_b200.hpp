@@ -7,15 +7,23 @@
 //   AlgoConfig, MultilinearRank, TuckerDecomposition; load_tensor / save_tensor (TNSR).
 // std::invalid_argument / std::runtime_error are re-thrown from the ABI status codes.
 //
+// Also: t_hosvd / st_hosvd / hooi (the deterministic baselines), reconstruct /
+// relative_error, parse_algorithm / algorithm_id / all_algorithm_ids, thread_cap,
+// MultilinearRank::clamped_for.
+//
 // Deviation: Eigen3 is not a dependency, so TuckerDecomposition::factors is a
 // std::vector<lmra::Matrix> -- a column-major rows() x cols() matrix with data() and
 // operator()(i, j); with Eigen available, `Eigen::Map<const Eigen::MatrixXd>(m.data(),
-// m.rows(), m.cols())` views it without a copy.  Multi-GPU follows the thread_cap()
-// idiom: LMRA_NUM_GPUS (tucker.cpp:164-172 reads LMRA_NUM_THREADS the same way); one
-// process per GPU passes its slab of the last mode after lmra_context_set_comm.
+// m.rows(), m.cols())` views it without a copy.  hooi() starts from st_hosvd (the reference's
+// two-argument overload); the overload taking an explicit init is not provided.
+// Multi-GPU follows the thread_cap() idiom: LMRA_NUM_GPUS=N (tucker.cpp:164-172 reads
+// LMRA_NUM_THREADS the same way) makes every randomized T-HOSVD / ST-HOSVD call run on devices
+// 0..N-1 from this process (lmra_run_algorithm_multigpu); one process per GPU instead passes
+// its slab of the last mode through the C ABI after lmra_context_set_comm.
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -98,6 +106,19 @@ struct MultilinearRank {  // tucker.hpp:17-24
   std::vector<std::size_t> mu;
   MultilinearRank() = default;
   explicit MultilinearRank(std::vector<std::size_t> m) : mu(std::move(m)) {}
+  // tucker.cpp:174-188
+  std::vector<std::size_t> clamped_for(const std::vector<std::size_t>& dims) const {
+    if (mu.size() != dims.size()) throw std::invalid_argument("rank vector length must equal tensor order");
+    std::vector<std::size_t> out(mu.size());
+    bool clamped = false;
+    for (std::size_t n = 0; n < mu.size(); ++n) {
+      if (mu[n] < 1) throw std::invalid_argument("rank entries must be positive");
+      out[n] = mu[n] < dims[n] ? mu[n] : dims[n];
+      clamped |= out[n] != mu[n];
+    }
+    if (clamped) std::fputs("lmra: target rank exceeds tensor dimensions, clamping\n", stderr);
+    return out;
+  }
 };
 
 struct TuckerDecomposition {  // tucker.hpp:27-30
@@ -116,8 +137,13 @@ struct AlgoConfig {  // tucker.hpp:32-45
   std::vector<std::size_t> order;
   std::uint64_t seed = 0;
   GramStrategy strategy = GramStrategy::A;
-  int hooi_max_sweeps = 50;  // accepted for layout compatibility; HOOI is off this path
+  int hooi_max_sweeps = 50;
   double hooi_tol = 1e-8;
+};
+
+struct HooiStats {  // tucker.hpp:73-76
+  bool converged = false;
+  int sweeps = 0;
 };
 
 enum class Algorithm {  // tucker.hpp:47-57
@@ -149,15 +175,26 @@ struct CConfig {
     c.n_order = order.size();
     c.seed = cfg.seed;
     c.strategy = cfg.strategy == GramStrategy::A ? LMRA_STRATEGY_A : LMRA_STRATEGY_B;
+    c.hooi_max_sweeps = cfg.hooi_max_sweeps;
+    c.hooi_tol = cfg.hooi_tol;
   }
 };
 
-inline TuckerDecomposition run(int alg, const DenseTensor& a, const AlgoConfig& cfg) {
+inline TuckerDecomposition run(int alg, const DenseTensor& a, const AlgoConfig& cfg, HooiStats* stats = nullptr) {
   CConfig cc(cfg);
   std::vector<uint64_t> dims(a.dims().begin(), a.dims().end());
   lmra_result* r = nullptr;
-  check(lmra_run_algorithm(default_context(), alg, a.data(), dims.data(), (int)dims.size(),
-                           LMRA_HOST, &cc.c, nullptr, &r));
+  const int ngpu = lmra_device_cap();  // LMRA_NUM_GPUS
+  if (ngpu > 1 && alg != LMRA_ALG6 && alg != LMRA_ALG7 && alg != LMRA_THOSVD && alg != LMRA_STHOSVD &&
+      alg != LMRA_HOOI) {
+    std::vector<int> devs(ngpu);
+    for (int d = 0; d < ngpu; ++d) devs[d] = d;
+    check(lmra_run_algorithm_multigpu(ngpu, devs.data(), alg, a.data(), dims.data(), (int)dims.size(), LMRA_HOST,
+                                      &cc.c, nullptr, &r));
+  } else {
+    check(lmra_run_algorithm(default_context(), alg, a.data(), dims.data(), (int)dims.size(), LMRA_HOST, &cc.c,
+                             nullptr, &r));
+  }
   std::unique_ptr<lmra_result, void (*)(lmra_result*)> guard(r, lmra_result_free);
   const int N = lmra_result_order(r);
   std::vector<uint64_t> cd(N);
@@ -171,6 +208,12 @@ inline TuckerDecomposition run(int alg, const DenseTensor& a, const AlgoConfig& 
     Matrix m(rows, cols);
     check(lmra_result_copy_factor(r, n, m.data(), LMRA_HOST));
     out.factors.push_back(std::move(m));
+  }
+  if (stats) {
+    int conv = 0, sw = 0;
+    lmra_result_hooi_stats(r, &conv, &sw);
+    stats->converged = conv != 0;
+    stats->sweeps = sw;
   }
   return out;
 }
@@ -197,17 +240,31 @@ inline TuckerDecomposition rand_sthosvd_power_qr(const DenseTensor& a, const Alg
   return detail::run(LMRA_ALG7, a, cfg);
 }
 
-// tucker.hpp:110-111 (the B200 path carries the randomized family: power, AMM, QR-proxy)
+// tucker.hpp:70-89 (the deterministic baselines)
+inline TuckerDecomposition t_hosvd(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_THOSVD, a, cfg);
+}
+inline TuckerDecomposition st_hosvd(const DenseTensor& a, const AlgoConfig& cfg) {
+  return detail::run(LMRA_STHOSVD, a, cfg);
+}
+inline TuckerDecomposition hooi(const DenseTensor& a, const AlgoConfig& cfg, HooiStats* stats = nullptr) {
+  return detail::run(LMRA_HOOI, a, cfg, stats);
+}
+
+// tucker.hpp:110-111
 inline TuckerDecomposition run_algorithm(Algorithm alg, const DenseTensor& a, const AlgoConfig& cfg) {
   switch (alg) {
+    case Algorithm::Thosvd: return t_hosvd(a, cfg);
+    case Algorithm::Sthosvd: return st_hosvd(a, cfg);
+    case Algorithm::Hooi: return hooi(a, cfg);
     case Algorithm::RandThosvdPower: return rand_thosvd_power(a, cfg);
     case Algorithm::RandSthosvdPower: return rand_sthosvd_power(a, cfg);
     case Algorithm::RandThosvdAmm: return rand_thosvd_amm(a, cfg);
     case Algorithm::RandSthosvdAmm: return rand_sthosvd_amm(a, cfg);
     case Algorithm::RandThosvdPowerQr: return rand_thosvd_power_qr(a, cfg);
     case Algorithm::RandSthosvdPowerQr: return rand_sthosvd_power_qr(a, cfg);
-    default: throw std::invalid_argument("algorithm is outside the B200 hot path (randomized alg1-alg7)");
   }
+  throw std::invalid_argument("unknown algorithm");
 }
 
 inline std::optional<Algorithm> parse_algorithm(const std::string& id) {  // tucker.cpp:190-201
@@ -221,6 +278,54 @@ inline std::optional<Algorithm> parse_algorithm(const std::string& id) {  // tuc
   if (id == "alg6") return Algorithm::RandThosvdPowerQr;
   if (id == "alg7") return Algorithm::RandSthosvdPowerQr;
   return std::nullopt;
+}
+
+inline std::string algorithm_id(Algorithm a) {  // tucker.cpp:203-215
+  switch (a) {
+    case Algorithm::Thosvd: return "thosvd";
+    case Algorithm::Sthosvd: return "sthosvd";
+    case Algorithm::Hooi: return "hooi";
+    case Algorithm::RandThosvdPower: return "alg1";
+    case Algorithm::RandSthosvdPower: return "alg2";
+    case Algorithm::RandThosvdAmm: return "alg4";
+    case Algorithm::RandSthosvdAmm: return "alg5";
+    case Algorithm::RandThosvdPowerQr: return "alg6";
+    case Algorithm::RandSthosvdPowerQr: return "alg7";
+  }
+  return "?";
+}
+
+inline std::vector<std::string> all_algorithm_ids() {  // tucker.cpp:217-220
+  const char* ids[16];
+  const int n = lmra_all_algorithm_ids(ids, 16);
+  return std::vector<std::string>(ids, ids + n);
+}
+
+inline int thread_cap() { return lmra_thread_cap(); }  // tucker.hpp:121
+
+// tucker.hpp:63-66: reconstruct (core x_n Q_n) and relative_error, evaluated on the device
+inline DenseTensor reconstruct(const TuckerDecomposition& d) {
+  const int N = (int)d.factors.size();
+  std::vector<uint64_t> cd(d.core.dims().begin(), d.core.dims().end()), rows(N);
+  std::vector<const double*> f(N);
+  std::vector<std::size_t> od(N);
+  for (int n = 0; n < N; ++n) {
+    f[n] = d.factors[n].data();
+    rows[n] = d.factors[n].rows();
+    od[n] = d.factors[n].rows();
+  }
+  DenseTensor out(od);
+  detail::check(lmra_reconstruct(detail::default_context(), d.core.data(), cd.data(), N, f.data(), rows.data(),
+                                 LMRA_HOST, out.data(), LMRA_HOST));
+  return out;
+}
+inline double relative_error(const DenseTensor& a, const DenseTensor& approx) {
+  if (a.dims() != approx.dims()) throw std::invalid_argument("relative_error: shape mismatch");
+  std::vector<uint64_t> d(a.dims().begin(), a.dims().end());
+  double re = 0.0;
+  detail::check(lmra_relative_error(detail::default_context(), a.data(), approx.data(), d.data(), (int)d.size(),
+                                    LMRA_HOST, &re));
+  return re;
 }
 
 // tucker.hpp:116-117

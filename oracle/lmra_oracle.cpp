@@ -507,6 +507,8 @@ struct Config {
   int strategy = 0;
   int mode_threads = 1;
   bool keep_trace = false;
+  int hooi_max_sweeps = 50;
+  double hooi_tol = 1e-8;
 };
 
 Config to_config(const orc_config* c, int order) {
@@ -523,6 +525,8 @@ Config to_config(const orc_config* c, int order) {
   k.strategy = c->strategy;
   k.mode_threads = std::max(1, c->mode_threads);
   k.keep_trace = c->keep_trace != 0;
+  k.hooi_max_sweeps = c->hooi_max_sweeps;
+  k.hooi_tol = c->hooi_tol;
   return k;
 }
 
@@ -675,6 +679,79 @@ std::vector<double> mode_probabilities(const Mat& a_n, const Config& cfg, Trace*
   std::vector<double> w = gram_sampling_norms(a_n);
   if (tr && cfg.keep_trace) tr->norms = w;
   return probabilities_from_norms(std::move(w), cfg.regime, cfg.beta);
+}
+
+// ---------------------------------------------------------------- deterministic baselines
+double frobenius_norm(const Tensor& t) {  // tensor.cpp (sequential sum of squares)
+  double s = 0.0;
+  for (double v : t.v) s += v * v;
+  return std::sqrt(s);
+}
+
+void alg_thosvd(const Tensor& a, const Config& cfg, orc_result& res) {  // tucker.cpp:242-248
+  Resolved r = resolve(a, cfg);
+  const size_t nm = a.dims.size();
+  res.factors.assign(nm, Mat());
+  res.trace.assign(nm, Trace());
+  for (size_t n = 0; n < nm; ++n) {
+    Mat a_n = unfold(a, n);
+    res.factors[n] = top_left_vectors_clamped(a_n, r.mu[n]);
+    if (cfg.keep_trace) res.trace[n].sketch = std::move(a_n);
+  }
+  res.core = core_from_factors(a, res.factors);
+}
+
+void alg_sthosvd(const Tensor& a, const Config& cfg, orc_result& res) {  // tucker.cpp:250-259
+  Resolved r = resolve(a, cfg);
+  const size_t nm = a.dims.size();
+  res.factors.assign(nm, Mat());
+  res.trace.assign(nm, Trace());
+  Tensor work = a;
+  for (size_t n : r.order) {
+    Mat a_n = unfold(work, n);
+    res.factors[n] = top_left_vectors_clamped(a_n, r.mu[n]);
+    if (cfg.keep_trace) res.trace[n].sketch = std::move(a_n);
+    work = mode_n_product(work, transpose(res.factors[n]), n);
+  }
+  res.core = std::move(work);
+}
+
+void alg_hooi(const Tensor& a, const Config& cfg, orc_result& res) {  // tucker.cpp:261-316
+  Resolved r = resolve(a, cfg);
+  const size_t nm = a.dims.size();
+  alg_sthosvd(a, cfg, res);  // init = st_hosvd (tucker.cpp:314-316)
+  std::vector<Mat>& factors = res.factors;
+  Tensor core = core_from_factors(a, factors);
+  const double norm_a = frobenius_norm(a);
+  if (norm_a == 0.0) {
+    res.core = std::move(core);
+    return;
+  }
+  double prev = frobenius_norm(core);
+  bool converged = false;
+  int sweep = 0;
+  const size_t last = r.order.back();
+  while (sweep < cfg.hooi_max_sweeps) {
+    ++sweep;
+    for (size_t n : r.order) {
+      Tensor y = a;
+      for (size_t m = 0; m < nm; ++m)
+        if (m != n) y = mode_n_product(y, transpose(factors[m]), m);
+      Mat y_n = unfold(y, n);
+      factors[n] = top_left_vectors_clamped(y_n, r.mu[n]);
+      if (cfg.keep_trace) res.trace[n].sketch = std::move(y_n);
+      if (n == last) core = mode_n_product(y, transpose(factors[n]), n);
+    }
+    const double cur = frobenius_norm(core);
+    if (std::abs(cur - prev) / norm_a < cfg.hooi_tol) {
+      converged = true;
+      break;
+    }
+    prev = cur;
+  }
+  if (!converged)
+    std::fprintf(stderr, "lmra: hooi stopped after %d sweeps without meeting the tolerance\n", sweep);
+  res.core = std::move(core);
 }
 
 void alg_power(const Tensor& a, const Config& cfg, bool sequential, orc_result& res) {
@@ -969,6 +1046,9 @@ int orc_run(int alg, const double* x, const uint64_t* dims, int order, const orc
         case ORC_ALG5: alg_amm(a, k, true, *res); break;
         case ORC_ALG6: alg_power_qr(a, k, false, *res); break;
         case ORC_ALG7: alg_power_qr(a, k, true, *res); break;
+        case ORC_THOSVD: alg_thosvd(a, k, *res); break;
+        case ORC_STHOSVD: alg_sthosvd(a, k, *res); break;
+        case ORC_HOOI: alg_hooi(a, k, *res); break;
         default: throw std::invalid_argument("unknown algorithm");
       }
       auto t1 = std::chrono::steady_clock::now();
@@ -1002,6 +1082,10 @@ void orc_result_omega_dims(const orc_result* r, int n, uint64_t* rows, uint64_t*
 }
 void orc_result_omega(const orc_result* r, int n, double* out) {
   std::memcpy(out, r->trace[n].omega.d.data(), sizeof(double) * r->trace[n].omega.d.size());
+}
+void orc_result_sketch_dims(const orc_result* r, int n, uint64_t* rows, uint64_t* cols) {
+  *rows = r->trace[n].sketch.r;
+  *cols = r->trace[n].sketch.c;
 }
 void orc_result_sketch(const orc_result* r, int n, double* out) {
   std::memcpy(out, r->trace[n].sketch.d.data(), sizeof(double) * r->trace[n].sketch.d.size());

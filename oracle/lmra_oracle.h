@@ -37,7 +37,8 @@ extern "C" {
 #endif
 
 /* algorithm ids follow tucker.hpp:47-57 */
-enum { ORC_ALG1 = 1, ORC_ALG2 = 2, ORC_ALG4 = 4, ORC_ALG5 = 5, ORC_ALG6 = 6, ORC_ALG7 = 7 };
+enum { ORC_ALG1 = 1, ORC_ALG2 = 2, ORC_ALG4 = 4, ORC_ALG5 = 5, ORC_ALG6 = 6, ORC_ALG7 = 7,
+       ORC_THOSVD = 10, ORC_STHOSVD = 11, ORC_HOOI = 12 };
 /* ProbRegime, sketching.hpp:24 */
 enum { ORC_OPTIMAL = 0, ORC_NEARLY_OPTIMAL = 1, ORC_UNIFORM = 2 };
 
@@ -54,6 +55,8 @@ typedef struct {
   int32_t strategy;          /* 0 = A, 1 = B (GramStrategy) */
   int32_t mode_threads;      /* LMRA_NUM_THREADS analogue for alg1/alg4 */
   int32_t keep_trace;        /* store per-mode Omega / samples / norms */
+  int32_t hooi_max_sweeps;   /* default 50 */
+  double hooi_tol;           /* default 1e-8 */
 } orc_config;
 
 typedef struct orc_result orc_result;
@@ -101,6 +104,7 @@ double orc_result_seconds(const orc_result* r);
 /* trace (keep_trace != 0) */
 void orc_result_omega_dims(const orc_result* r, int n, uint64_t* rows, uint64_t* cols);
 void orc_result_omega(const orc_result* r, int n, double* out);
+void orc_result_sketch_dims(const orc_result* r, int n, uint64_t* rows, uint64_t* cols);
 void orc_result_sketch(const orc_result* r, int n, double* out); /* same dims as omega */
 uint64_t orc_result_num_samples(const orc_result* r, int n);
 void orc_result_samples(const orc_result* r, int n, int64_t* idx, double* scales);

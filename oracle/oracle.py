@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "liblmra_oracle.so")
 
-ALG = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5, "alg6": 6, "alg7": 7}
+ALG = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5, "alg6": 6, "alg7": 7, "thosvd": 10, "sthosvd": 11, "hooi": 12}
 REGIME = {"optimal": 0, "nearly_optimal": 1, "uniform": 2}
 
 u64p = C.POINTER(C.c_uint64)
@@ -30,7 +30,7 @@ class OrcConfig(C.Structure):
         ("rank", u64p), ("oversampling", C.c_uint64), ("power", C.c_int32), ("alpha", C.c_double),
         ("regime", C.c_int32), ("regime_beta", C.c_double), ("t_samples", u64p), ("order", u64p),
         ("seed", C.c_uint64), ("strategy", C.c_int32), ("mode_threads", C.c_int32),
-        ("keep_trace", C.c_int32),
+        ("keep_trace", C.c_int32), ("hooi_max_sweeps", C.c_int32), ("hooi_tol", C.c_double),
     ]
 
 
@@ -179,6 +179,8 @@ class AlgoConfig:
     strategy: str = "A"
     mode_threads: int = 1
     keep_trace: bool = True
+    hooi_max_sweeps: int = 50
+    hooi_tol: float = 1e-8
     _keep: list = field(default_factory=list, repr=False)
 
     def to_c(self, n_modes: int) -> OrcConfig:
@@ -196,7 +198,7 @@ class AlgoConfig:
             _p(rank, u64p), self.oversampling, self.power, self.alpha, REGIME[self.regime],
             self.regime_beta, _p(ts, u64p) if ts is not None else None,
             _p(od, u64p) if od is not None else None, self.seed, 0 if self.strategy == "A" else 1,
-            self.mode_threads, 1 if self.keep_trace else 0)
+            self.mode_threads, 1 if self.keep_trace else 0, self.hooi_max_sweeps, self.hooi_tol)
 
 
 @dataclass
@@ -245,6 +247,7 @@ def run(alg: str, x: np.ndarray, dims: Sequence[int], cfg: AlgoConfig) -> Decomp
                 if g.size:
                     L.orc_result_omega(h, n, _p(g, dblp))
                 omegas.append(g.reshape((r.value, k.value), order="F"))
+                L.orc_result_sketch_dims(h, n, C.byref(r), C.byref(k))
                 c = np.empty(r.value * k.value)
                 if c.size:
                     L.orc_result_sketch(h, n, _p(c, dblp))

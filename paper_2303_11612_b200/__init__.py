@@ -6,6 +6,7 @@ from .tucker import (  # noqa: F401
     probabilities, rand_sthosvd_amm, rand_sthosvd_power, rand_sthosvd_power_qr, rand_thosvd_amm,
     rand_thosvd_power, rand_thosvd_power_qr,
     randsample, run_algorithm, run_raw, shard_range, ThreadGroup, load_tensor, save_tensor,
+    t_hosvd, st_hosvd, hooi, thread_cap, device_cap, run_raw_multigpu,
 )
 from ._lib import LmraError, LmraInvalidArgument, LIB_PATH  # noqa: F401
 from . import device  # noqa: F401

@@ -25,7 +25,7 @@ class LmraAlgoConfig(C.Structure):
         ("rank", u64p), ("n_rank", C.c_uint64), ("oversampling", C.c_uint64), ("power", C.c_int32),
         ("alpha", C.c_double), ("regime", C.c_int32), ("regime_beta", C.c_double),
         ("t_samples", u64p), ("n_t_samples", C.c_uint64), ("order", u64p), ("n_order", C.c_uint64),
-        ("seed", C.c_uint64), ("strategy", C.c_int32),
+        ("seed", C.c_uint64), ("strategy", C.c_int32), ("hooi_max_sweeps", C.c_int32), ("hooi_tol", C.c_double),
     ]
 
 
@@ -68,6 +68,7 @@ def _load():
                                          C.POINTER(LmraAlgoConfig), C.POINTER(LmraOverrides),
                                          C.POINTER(vp)]),
         "lmra_result_order": (C.c_int, [vp]),
+        "lmra_result_hooi_stats": (None, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "lmra_result_core_dims": (None, [vp, u64p]),
         "lmra_result_copy_core": (C.c_int, [vp, vp, C.c_int]),
         "lmra_result_factor_dims": (None, [vp, C.c_int, u64p, u64p]),
@@ -123,6 +124,14 @@ def _load():
         "lmra_reconstruct": (C.c_int, [vp, vp, u64p, C.c_int, C.POINTER(vp), u64p, C.c_int, vp, C.c_int]),
         "lmra_relative_error": (C.c_int, [vp, vp, vp, u64p, C.c_int, C.c_int, dblp]),
         "lmra_result_relative_error": (C.c_int, [vp, vp, vp, u64p, C.c_int, C.c_int, dblp]),
+        "lmra_parse_algorithm": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
+        "lmra_algorithm_id": (C.c_char_p, [C.c_int]),
+        "lmra_all_algorithm_ids": (C.c_int, [C.POINTER(C.c_char_p), C.c_int]),
+        "lmra_thread_cap": (C.c_int, []),
+        "lmra_device_cap": (C.c_int, []),
+        "lmra_run_algorithm_multigpu": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, vp, u64p, C.c_int, C.c_int,
+                                                  C.POINTER(LmraAlgoConfig), C.POINTER(LmraOverrides),
+                                                  C.POINTER(vp)]),
         "lmra_device_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
         "lmra_device_free": (C.c_int, [vp, vp]),
         "lmra_memcpy": (C.c_int, [vp, vp, vp, C.c_size_t, C.c_int, C.c_int]),
@@ -157,6 +166,8 @@ EXPORTED = [
     "lmra_gen_tucker_noise", "lmra_gen_hilbert", "lmra_gen_video", "lmra_device_alloc",
     "lmra_gen_tucker_signal_slab", "lmra_gen_noise_coef", "lmra_gen_add_noise_slab", "lmra_gen_hilbert_slab",
     "lmra_gen_video_slab", "lmra_reconstruct", "lmra_relative_error", "lmra_result_relative_error",
+    "lmra_parse_algorithm", "lmra_algorithm_id", "lmra_all_algorithm_ids", "lmra_thread_cap", "lmra_device_cap",
+    "lmra_run_algorithm_multigpu", "lmra_result_hooi_stats",
     "lmra_device_free", "lmra_memcpy",
 ]
 

@@ -76,6 +76,8 @@ struct Config {
   std::vector<size_t> order;
   uint64_t seed = 0;
   int strategy = 0;
+  int hooi_max_sweeps = 50;
+  double hooi_tol = 1e-8;
 };
 
 struct Resolved {

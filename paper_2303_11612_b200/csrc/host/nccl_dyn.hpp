@@ -18,6 +18,8 @@ struct NcclApi {
   decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
   decltype(&ncclCommInitRank) CommInitRank = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclCommAbort) CommAbort = nullptr;
+  decltype(&ncclCommInitAll) CommInitAll = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclBroadcast) Broadcast = nullptr;
@@ -41,6 +43,8 @@ inline const NcclApi& nccl() {
     LMRA_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
     LMRA_NCCL_SYM(CommInitRank, "ncclCommInitRank");
     LMRA_NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    LMRA_NCCL_SYM(CommAbort, "ncclCommAbort");
+    LMRA_NCCL_SYM(CommInitAll, "ncclCommInitAll");
     LMRA_NCCL_SYM(AllReduce, "ncclAllReduce");
     LMRA_NCCL_SYM(AllGather, "ncclAllGather");
     LMRA_NCCL_SYM(Broadcast, "ncclBroadcast");

@@ -19,6 +19,12 @@ constexpr int kMaxWidth = 64;
 inline thread_local long long g_kernel_launches = 0;
 inline void note_launch() { ++g_kernel_launches; }
 
+// SMs the persistent int8 contraction leaves free (set by the host around a launch that runs
+// beside other kernels -- the split orthonormalisation's Jacobis -- so both make progress:
+// the contraction's tiles are assigned statically to its CTAs, and one CTA that cannot start
+// delays the whole kernel by the duration of whatever holds its SM)
+inline thread_local int g_i8_reserved_sms = 0;
+
 // Stream-ordered scratch for the launchers: served from the run's device arena when the host
 // has one installed (lmra_b200.cpp ArenaScope), else from the stream-ordered pool.
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
@@ -139,6 +145,14 @@ cudaError_t launch_gen_hilbert(double* out, const long long* dims, int order, lo
 cudaError_t launch_gen_video(double* out, const long long* dims, int order, long long start, long long count,
                              const double* profiles, const double* weights, int n_terms, double noise,
                              uint64_t seed, uint64_t stream, cudaStream_t st);
+
+// ---- deterministic baselines (dense.cu) ----
+// r (n x n) = upper triangle of a (ld lda), zeros below
+cudaError_t launch_copy_upper(const double* a, long long lda, int n, double* r, cudaStream_t st);
+// q (n x mu) = transpose of the first mu rows of vt (n x n)
+cudaError_t launch_rows_to_cols(const double* vt, int n, int mu, double* q, cudaStream_t st);
+// fix_signs (linalg.cpp:13-29) on the mu columns of u (m rows, ld ldu)
+cudaError_t launch_signfix_columns(double* u, long long m, int ldu, int mu, cudaStream_t st);
 
 // ---- verification (verify.cu): out2 = {sum (a - r)^2, sum a^2}, deterministic ----
 size_t diff_sumsq_workspace_doubles();

@@ -820,7 +820,7 @@ template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
     int ldo, int final_level, int* status, double jacobi_tol, int clustered, int phase,
-    double* __restrict__ gbuf, double* __restrict__ ur) {
+    double* __restrict__ gbuf, double* __restrict__ ur, int basis_pivot) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   extern __shared__ __align__(16) double sm[];
@@ -858,7 +858,9 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     __syncthreads();
     double a[kCW][RPL];
     cw_load(Vs, ldv, m, s, a);
-    reg_qr(a, m, s, q, true);
+    // the basis phase skips the column pivoting: it only preconditions the Jacobi (graded R,
+    // fewer sweeps), and in the split form the Jacobi runs off the critical path
+    reg_qr(a, m, s, q, phase != kOrthBasis || basis_pivot);
     if ((int)threadIdx.x < s) q.ipiv[q.piv[threadIdx.x]] = threadIdx.x;
     __syncthreads();
     // G = R^T (lower triangle), reflectors to Vs in logical column order
@@ -1141,6 +1143,12 @@ cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, doub
   return cudaGetLastError();
 }
 
+// LMRA_ORTH_BASIS_PIVOT=1: pivot in the basis phase too
+static int basis_pivot() {
+  static const int on = getenv("LMRA_ORTH_BASIS_PIVOT") && getenv("LMRA_ORTH_BASIS_PIVOT")[0] == '1';
+  return on;
+}
+
 template <int RPL>
 cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, int final_level,
                  int* status, double tol, cudaStream_t st, int phase = kOrthFull, double* gbuf = nullptr,
@@ -1172,11 +1180,11 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
     cfg.numAttrs = 2;
     note_launch();
     const cudaError_t le = cudaLaunchKernelEx(&cfg, orth_core_kernel<RPL>, S, m, s, m, mu, out, ldo, final_level,
-                                              status, tol, 1, phase, gbuf, ur);
+                                              status, tol, 1, phase, gbuf, ur, basis_pivot());
     if (le != cudaSuccess) return le;
   } else {
     const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu,
-                                      out, ldo, final_level, status, tol, 0, phase, gbuf, ur);
+                                      out, ldo, final_level, status, tol, 0, phase, gbuf, ur, basis_pivot());
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();

@@ -45,6 +45,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace lmra_dev {
@@ -606,7 +608,8 @@ cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long ntiles = kInner ? (geo.O + 1) / 2 : (geo.J + kI8Tile - 1) / kI8Tile;
-  const int grid = (int)(ntiles < sms ? ntiles : sms);
+  const int avail = std::max(1, sms - std::max(0, g_i8_reserved_sms));
+  const int grid = (int)(ntiles < avail ? ntiles : avail);
   ttm_i8_kernel<N, kInner><<<grid, kI8Threads, smem, st>>>(map, qd, eq, geo, mu, y); note_launch();
   return cudaGetLastError();
 }

@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 #include "host/nccl_dyn.hpp"
+#include "host/cusolver_dyn.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -22,6 +23,7 @@
 #include <map>
 #include <mutex>
 #include <numeric>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -93,11 +95,21 @@ struct NcclComm : Comm {
   ~NcclComm() override {
     if (c) lmra_host::nccl().CommDestroy(c);
   }
+  // a rank failed mid-run: abort the communicator so peers blocked in a collective return with
+  // an error instead of hanging; the communicator is unusable afterwards (a new one must be set)
+  void abort() override {
+    if (c && lmra_host::nccl().CommAbort) lmra_host::nccl().CommAbort(c);
+    c = nullptr;
+  }
+  void usable() const {
+    if (!c) throw std::runtime_error("NCCL communicator was aborted by an earlier failed run");
+  }
   // all-gather + a fixed-order (rank order) sum instead of ncclAllReduce: every rank gets
   // the same bits, identical to ThreadComm's sum (the path the GPU tests check rank for rank)
   // and independent of the reduction algorithm NCCL picks (ring / tree / NVLS)
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
     if (n == 0) return;
+    usable();
     double* tmp = nullptr;
     ck(lmra_dev::scratch_alloc(reinterpret_cast<void**>(&tmp), n * nranks * sizeof(double), st), "alloc");
     ckn(lmra_host::nccl().AllGather(buf, tmp, n, ncclDouble, c, st), "ncclAllGather");
@@ -105,6 +117,7 @@ struct NcclComm : Comm {
     lmra_dev::scratch_free(tmp, st);
   }
   void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    usable();
     ckn(lmra_host::nccl().AllGather(send, recv, n, ncclDouble, c, st), "ncclAllGather");
   }
 };
@@ -239,6 +252,7 @@ struct lmra_context {
   char* arena = nullptr;
   size_t arena_cap = 0, arena_off = 0, arena_want = 0;
   std::shared_ptr<ResultBlocks> results = std::make_shared<ResultBlocks>();
+  cusolverDnHandle_t cusolver = nullptr;  // deterministic baselines only (lazily created)
   cudaStream_t aux_stream(size_t i) {
     while (aux.size() <= i) {
       cudaStream_t s;
@@ -442,6 +456,7 @@ struct lmra_result {
   std::vector<std::vector<double>> norms;
   double t_total = 0, t_rng = 0, t_sampling = 0, t_device = 0, launches = 0;
   int sampler_fallbacks = 0;  // uncertified Neumaier roundings resolved sequentially
+  int hooi_converged = 0, hooi_sweeps = 0;  // HooiStats (tucker.hpp:73-76), hooi runs only
   struct Phase {
     std::string name;
     double ms;
@@ -981,6 +996,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     // the first contraction reads the input, whose mode-0 norms the sampler already has
     const double* w0 = (amm && cfg.regime != kUniform && d_w[0].get()) ? d_w[0].get() : nullptr;
     Engine::I8Chain chain;
+    if (split_orth) {  // SMs for the Jacobis that run beside the first contraction
+      int jac = 0;
+      for (size_t n = 0; n < N; ++n) jac += r.sketch[n] >= 48 ? 2 : 1;
+      lmra_dev::g_i8_reserved_sms = jac;
+    }
     for (size_t k = 0; k < idx.size(); ++k) {
       const size_t n = idx[k];
       const bool next1 = k + 1 < idx.size() && idx[k + 1] == 1;
@@ -1009,6 +1029,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       t = std::move(y);
       src = t.get();
     }
+    lmra_dev::g_i8_reserved_sms = 0;
     if (split_orth)  // the rotations U_R'^T on the s_0 x s_1 x ... core, each after its Jacobi
       for (size_t k = 0; k < idx.size(); ++k) {
         const size_t n = idx[k];
@@ -1623,6 +1644,211 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   res->t_total = now_ms() - t0;
 }
 
+// ------------------------------------------------------------------ deterministic baselines
+// t_hosvd / st_hosvd / hooi (tucker.cpp:242-316).  Their factors are the leading left singular
+// vectors of FULL unfoldings (top_left_vectors_clamped(unfold(x, n), mu), tucker.cpp:65-77):
+// A_(n)^T = Q R by Householder QR (cuSOLVER dgeqrf on the transposed unfolding, written by
+// unfold_t), then the SVD of the I_n x I_n R (dgesvd): A_(n) = V_R S (Q U_R)^T, so the factor is
+// V_R(:, :mu) with the sign rule of fix_signs (linalg.cpp:13-29).  Wide-and-short unfoldings
+// (J < I) take the SVD of A_(n) itself.  The mode products are the DMMA TTM.
+static void cusolver_check(cusolverStatus_t s, const char* what) {
+  if (s != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string(what) + ": cuSOLVER status " + std::to_string((int)s));
+}
+
+static DevBuf dense_lsv(lmra_context* ctx, const double* x, const std::vector<size_t>& dims, size_t n,
+                        size_t mu_req, size_t* mu_out) {
+  const auto& cs = lmra_host::cusolver();
+  cudaStream_t st = ctx->stream;
+  if (!ctx->cusolver) {
+    cusolver_check(cs.Create(&ctx->cusolver), "cusolverDnCreate");
+    if (cs.SetDeterministicMode) cs.SetDeterministicMode(ctx->cusolver, CUSOLVER_DETERMINISTIC_RESULTS);
+  }
+  cusolver_check(cs.SetStream(ctx->cusolver, st), "cusolverDnSetStream");
+  const ModeView v = view_of(dims, n);
+  const size_t I = dims[n], J = (size_t)(v.inner * v.outer);
+  const size_t mu = std::min(mu_req, std::min(I, J));  // rank_cap (tucker.cpp:65-71)
+  if (mu < mu_req)
+    fprintf(stderr, "lmra: requested rank %zu exceeds matrix rank limit %zu, clamping\n", mu_req, mu);
+  *mu_out = mu;
+  if (I > (size_t)INT32_MAX || J > (size_t)INT32_MAX) throw std::invalid_argument("unfolding too large for dgesvd");
+  Engine eng(ctx);
+  DevBuf at(J * I, st), info(1, st), q(I * mu, st), sv(std::min(I, J), st);
+  ck(cudaMemsetAsync(info.get(), 0, sizeof(double), st), "memset");
+  int* dinfo = reinterpret_cast<int*>(info.get());
+  eng.launch("dense_unfold", [&] { return lmra_dev::launch_unfold_t(x, v.inner, (long long)I, v.outer, at.get(), st); });
+  const int iI = (int)I, iJ = (int)J;
+  if (J >= I) {
+    int lw = 0;
+    cusolver_check(cs.Dgeqrf_bufferSize(ctx->cusolver, iJ, iI, at.get(), iJ, &lw), "dgeqrf_bufferSize");
+    DevBuf tau(I, st), w((size_t)std::max(lw, 1), st);
+    cusolver_check(cs.Dgeqrf(ctx->cusolver, iJ, iI, at.get(), iJ, tau.get(), w.get(), lw, dinfo), "dgeqrf");
+    DevBuf r(I * I, st), vt(I * I, st), rw(I, st);
+    eng.launch("dense_r", [&] { return lmra_dev::launch_copy_upper(at.get(), (long long)J, iI, r.get(), st); });
+    int lw2 = 0;
+    cusolver_check(cs.Dgesvd_bufferSize(ctx->cusolver, iI, iI, &lw2), "dgesvd_bufferSize");
+    DevBuf w2((size_t)std::max(lw2, 1), st);
+    cusolver_check(cs.Dgesvd(ctx->cusolver, 'N', 'A', iI, iI, r.get(), iI, sv.get(), nullptr, 1, vt.get(), iI,
+                             w2.get(), lw2, rw.get(), dinfo),
+                   "dgesvd");
+    eng.launch("dense_factor", [&] { return lmra_dev::launch_rows_to_cols(vt.get(), iI, (int)mu, q.get(), st); });
+  } else {
+    DevBuf a(I * J, st), u(I * J, st), rw(J, st);
+    eng.launch("transpose", [&] { return lmra_dev::launch_transpose(at.get(), (long long)J, (long long)I, a.get(), st); });
+    int lw2 = 0;
+    cusolver_check(cs.Dgesvd_bufferSize(ctx->cusolver, iI, iJ, &lw2), "dgesvd_bufferSize");
+    DevBuf w2((size_t)std::max(lw2, 1), st);
+    cusolver_check(cs.Dgesvd(ctx->cusolver, 'S', 'N', iI, iJ, a.get(), iI, sv.get(), u.get(), iI, nullptr, 1,
+                             w2.get(), lw2, rw.get(), dinfo),
+                   "dgesvd");
+    ck(cudaMemcpyAsync(q.get(), u.get(), I * mu * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+  }
+  eng.launch("dense_signs", [&] { return lmra_dev::launch_signfix_columns(q.get(), (long long)I, (int)I, (int)mu, st); });
+  int hinfo = 0;
+  ck(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");  // the locals above are released after this
+  if (hinfo > 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+  if (hinfo < 0) throw CudaError("cuSOLVER: illegal argument " + std::to_string(-hinfo));
+  return q;
+}
+
+static double frobenius_dev(lmra_context* ctx, const double* t, size_t n) {
+  cudaStream_t st = ctx->stream;
+  DevBuf work(lmra_dev::diff_sumsq_workspace_doubles(), st), out(2, st);
+  ck(lmra_dev::launch_diff_sumsq(t, t, (long long)n, work.get(), out.get(), st), "sumsq");
+  double h[2];
+  ck(cudaMemcpyAsync(h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  return std::sqrt(h[1]);
+}
+
+void run_deterministic_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) {
+  using namespace lmra_host;
+  const double t0 = now_ms();
+  // the per-run arena would grow to every intermediate of every HOOI sweep: stream-ordered
+  // pool allocations instead (each buffer freed when its scope ends)
+  lmra_context* arena_prev = t_arena_ctx;
+  t_arena_ctx = nullptr;
+  struct Restore {
+    lmra_context* p;
+    ~Restore() { t_arena_ctx = p; }
+  } restore{arena_prev};
+  const long long launches0 = lmra_dev::g_kernel_launches;
+  cudaStream_t st = ctx->stream;
+  Engine eng(ctx);
+  const auto& cfg = in.cfg;
+  const size_t N = in.dims.size();
+  for (size_t d : in.dims)
+    if (d == 0) throw std::invalid_argument("tensor dimension must be positive");
+  Resolved r = resolve(in.dims, cfg);
+  res->omega.assign(N, {});
+  res->om_rows.assign(N, 0);
+  res->om_cols.assign(N, 0);
+  res->idx.assign(N, {});
+  res->scales.assign(N, {});
+  res->norms.assign(N, {});
+  res->factors.assign(N, nullptr);
+  res->f_rows.assign(N, 0);
+  res->f_cols.assign(N, 0);
+  std::vector<DevBuf> factors(N);
+  std::vector<size_t> width(N, 0);
+  auto factor = [&](const double* t, const std::vector<size_t>& d, size_t n) {
+    factors[n] = dense_lsv(ctx, t, d, n, r.mu[n], &width[n]);
+  };
+  // core_from_factors (tucker.cpp:81-92): ascending factor width, stable
+  auto core_from = [&](std::vector<size_t>& cur) {
+    std::vector<size_t> idx(N);
+    std::iota(idx.begin(), idx.end(), size_t{0});
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return width[a] < width[b]; });
+    DevBuf t;
+    const double* src = in.x;
+    cur = in.dims;
+    for (size_t n : idx) {
+      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), width[n], "core_ttm");
+      cur[n] = width[n];
+      t = std::move(y);
+      src = t.get();
+    }
+    return t;
+  };
+  std::vector<size_t> cdims;
+  DevBuf core;
+  auto st_hosvd = [&] {
+    DevBuf work;
+    const double* src = in.x;
+    std::vector<size_t> cur = in.dims;
+    for (size_t n : r.order) {
+      factor(src, cur, n);
+      DevBuf y = eng.ttm(src, cur, n, factors[n].get(), width[n], "shrink_ttm");
+      cur[n] = width[n];
+      work = std::move(y);
+      src = work.get();
+    }
+    cdims = cur;
+    core = std::move(work);
+  };
+  if (in.alg == LMRA_THOSVD) {  // tucker.cpp:242-248
+    for (size_t n = 0; n < N; ++n) factor(in.x, in.dims, n);
+    core = core_from(cdims);
+  } else if (in.alg == LMRA_STHOSVD) {  // tucker.cpp:250-259
+    st_hosvd();
+  } else {  // LMRA_HOOI, tucker.cpp:261-316 with init = st_hosvd
+    st_hosvd();
+    core = core_from(cdims);
+    const double norm_a = frobenius_dev(ctx, in.x, prod(in.dims));
+    if (norm_a != 0.0) {
+      double prev = frobenius_dev(ctx, core.get(), prod(cdims));
+      bool converged = false;
+      int sweep = 0;
+      const size_t last = r.order.back();
+      while (sweep < cfg.hooi_max_sweeps) {
+        ++sweep;
+        for (size_t n : r.order) {
+          DevBuf y;
+          const double* src = in.x;
+          std::vector<size_t> cur = in.dims;
+          for (size_t m = 0; m < N; ++m) {
+            if (m == n) continue;
+            DevBuf z = eng.ttm(src, cur, m, factors[m].get(), width[m], "hooi_ttm");
+            cur[m] = width[m];
+            y = std::move(z);
+            src = y.get();
+          }
+          factor(src, cur, n);
+          if (n == last) {
+            DevBuf z = eng.ttm(src, cur, n, factors[n].get(), width[n], "hooi_ttm");
+            cur[n] = width[n];
+            cdims = cur;
+            core = std::move(z);
+          }
+        }
+        const double curn = frobenius_dev(ctx, core.get(), prod(cdims));
+        if (std::abs(curn - prev) / norm_a < cfg.hooi_tol) {
+          converged = true;
+          break;
+        }
+        prev = curn;
+      }
+      if (!converged)
+        fprintf(stderr, "lmra: hooi stopped after %d sweeps without meeting the tolerance\n", sweep);
+      res->hooi_converged = converged ? 1 : 0;
+      res->hooi_sweeps = sweep;
+    }
+  }
+  res->core_dims = cdims;
+  // result blocks (ResultBlocks) -- detach() needs an active arena context for the block cache
+  t_arena_ctx = ctx;
+  res->core = core.detach();
+  for (size_t n = 0; n < N; ++n) {
+    res->f_rows[n] = in.dims[n];
+    res->f_cols[n] = width[n];
+    res->factors[n] = factors[n].detach();
+  }
+  ck(cudaStreamSynchronize(st), "sync");
+  res->launches = (double)(lmra_dev::g_kernel_launches - launches0);
+  res->t_total = now_ms() - t0;
+  res->t_device = res->t_total;
+}
+
 lmra_host::Config to_config(const lmra_algo_config* c) {
   lmra_host::Config k;
   if (!c) throw std::invalid_argument("null config");
@@ -1637,6 +1863,8 @@ lmra_host::Config to_config(const lmra_algo_config* c) {
   if (c->n_order) k.order.assign(c->order, c->order + c->n_order);
   k.seed = c->seed;
   k.strategy = c->strategy;
+  k.hooi_max_sweeps = c->hooi_max_sweeps;
+  k.hooi_tol = c->hooi_tol;
   if (k.regime < 0 || k.regime > 2) throw std::invalid_argument("unknown probability regime");
   if (k.strategy != 0 && k.strategy != 1) throw std::invalid_argument("unknown Gram strategy");
   return k;
@@ -1658,6 +1886,8 @@ void lmra_algo_config_init(lmra_algo_config* cfg) {
   cfg->regime = LMRA_UNIFORM;
   cfg->regime_beta = 0.5;
   cfg->strategy = LMRA_STRATEGY_A;
+  cfg->hooi_max_sweeps = 50;
+  cfg->hooi_tol = 1e-8;
 }
 
 int lmra_context_create(int device, void* stream, lmra_context** out) {
@@ -1693,6 +1923,7 @@ void lmra_context_destroy(lmra_context* ctx) {
     for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->cusolver) lmra_host::cusolver().Destroy(ctx->cusolver);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   }
   delete ctx;
@@ -1772,19 +2003,75 @@ int lmra_shard_range(uint64_t extent, int nranks, int rank, uint64_t* start, uin
   });
 }
 
+// ------------------------------------------------------------------ algorithm ids, knobs
+// tucker.cpp:190-220 (parse_algorithm / algorithm_id / all_algorithm_ids)
+static const struct {
+  int code;
+  const char* id;
+} kAlgIds[] = {{LMRA_THOSVD, "thosvd"}, {LMRA_STHOSVD, "sthosvd"}, {LMRA_HOOI, "hooi"}, {LMRA_ALG1, "alg1"},
+               {LMRA_ALG2, "alg2"},     {LMRA_ALG4, "alg4"},       {LMRA_ALG5, "alg5"}, {LMRA_ALG6, "alg6"},
+               {LMRA_ALG7, "alg7"}};
+
+const char* lmra_algorithm_id(int algorithm) {
+  for (const auto& a : kAlgIds)
+    if (a.code == algorithm) return a.id;
+  return "?";
+}
+
+int lmra_parse_algorithm(const char* id, int* algorithm) {
+  if (!id) return 0;
+  for (const auto& a : kAlgIds)
+    if (std::strcmp(a.id, id) == 0) {
+      if (algorithm) *algorithm = a.code;
+      return 1;
+    }
+  return 0;
+}
+
+int lmra_all_algorithm_ids(const char** ids, int max_ids) {
+  const int n = (int)(sizeof(kAlgIds) / sizeof(kAlgIds[0]));
+  for (int k = 0; k < n && k < max_ids; ++k) ids[k] = kAlgIds[k].id;
+  return n;
+}
+
+// tucker.cpp:164-172: LMRA_NUM_THREADS, default 1, clamped to [1, 64]
+int lmra_thread_cap(void) {
+  static const int cap = [] {
+    const char* env = std::getenv("LMRA_NUM_THREADS");
+    if (!env) return 1;
+    return std::clamp(std::atoi(env), 1, 64);
+  }();
+  return cap;
+}
+
+// the same idiom for devices: LMRA_NUM_GPUS, default 1, clamped to [1, visible devices]
+int lmra_device_cap(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) {
+    cudaGetLastError();
+    return 1;
+  }
+  const char* env = std::getenv("LMRA_NUM_GPUS");
+  if (!env) return 1;
+  return std::clamp(std::atoi(env), 1, count);
+}
+
 int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const uint64_t* dims,
                        int order, int x_location, const lmra_algo_config* cfg,
                        const lmra_overrides* overrides, lmra_result** out) {
   *out = nullptr;
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null context");
+    const bool deterministic = algorithm == LMRA_THOSVD || algorithm == LMRA_STHOSVD || algorithm == LMRA_HOOI;
     if (algorithm != LMRA_ALG1 && algorithm != LMRA_ALG2 && algorithm != LMRA_ALG4 &&
-        algorithm != LMRA_ALG5 && algorithm != LMRA_ALG6 && algorithm != LMRA_ALG7)
+        algorithm != LMRA_ALG5 && algorithm != LMRA_ALG6 && algorithm != LMRA_ALG7 && !deterministic)
       throw std::invalid_argument("unknown algorithm");
     if (order < 1) throw std::invalid_argument("cannot decompose an order-0 tensor");
     const bool sharded = ctx->comm && ctx->nranks > 1;
     if (sharded && (algorithm == LMRA_ALG6 || algorithm == LMRA_ALG7))
       throw std::invalid_argument("alg6/alg7 run on one device (no sharded QR-proxy path)");
+    if (sharded && deterministic)
+      throw std::invalid_argument("the deterministic baselines (thosvd / sthosvd / hooi) run on one device");
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard dg(ctx->device);
     ArenaScope arena(ctx);  // every device buffer of the run (after the device guard)
@@ -1820,13 +2107,164 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
         ctx->comm->abort();
         throw;
       }
-    } else
+    } else if (deterministic) {
+      run_deterministic_impl(ctx, in, res.get());
+    } else {
       run_algorithm_impl(ctx, in, res.get());
+    }
     *out = res.release();
   });
 }
 
+// ------------------------------------------------------------------ in-process multi-GPU
+// One process drives ndev devices (the C++ drop-in's LMRA_NUM_GPUS): one context and one
+// host thread per device, the tensor split along its last mode exactly as with one process
+// per GPU.  Communicator: NCCL (ncclCommInitAll) when the devices are distinct, else the
+// in-process ThreadComm (device copies, peer access enabled).  Groups are cached per device
+// list; a group's runs are serialised.
+namespace {
+struct DeviceGroup {
+  std::vector<int> devs;
+  std::vector<lmra_context*> ctx;
+  std::shared_ptr<ThreadGroup> tg;
+  bool nccl = false;
+  std::mutex run_mu;
+  ~DeviceGroup() {
+    for (lmra_context* c : ctx) lmra_context_destroy(c);
+  }
+};
+std::mutex g_groups_mu;
+std::map<std::vector<int>, std::shared_ptr<DeviceGroup>> g_groups;
+
+std::shared_ptr<DeviceGroup> device_group(const std::vector<int>& devs) {
+  std::lock_guard<std::mutex> lk(g_groups_mu);
+  auto it = g_groups.find(devs);
+  if (it != g_groups.end()) return it->second;
+  auto g = std::make_shared<DeviceGroup>();
+  g->devs = devs;
+  const int n = (int)devs.size();
+  for (int d : devs) {
+    lmra_context* c = nullptr;
+    if (lmra_context_create(d, nullptr, &c) != LMRA_OK) throw CudaError(g_err);
+    g->ctx.push_back(c);
+  }
+  std::vector<int> sorted = devs;
+  std::sort(sorted.begin(), sorted.end());
+  const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+  if (n > 1 && distinct) {
+    try {
+      const auto& api = lmra_host::nccl();
+      if (api.CommInitAll) {
+        std::vector<ncclComm_t> comms(n);
+        ckn(api.CommInitAll(comms.data(), n, devs.data()), "ncclCommInitAll");
+        for (int r = 0; r < n; ++r) {
+          auto c = std::make_shared<NcclComm>();
+          c->c = comms[r];
+          c->nranks = n;
+          c->rank = r;
+          g->ctx[r]->comm = c;
+          g->ctx[r]->nranks = n;
+          g->ctx[r]->rank = r;
+        }
+        g->nccl = true;
+      }
+    } catch (const std::exception&) {
+      g->nccl = false;  // no NCCL in this process: the in-process communicator below
+    }
+  }
+  if (n > 1 && !g->nccl) {
+    for (int a : devs)
+      for (int b : devs)
+        if (a != b) {
+          int ok = 0;
+          cudaDeviceCanAccessPeer(&ok, a, b);
+          if (ok) {
+            DeviceGuard dg(a);
+            if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();  // already enabled
+          }
+        }
+    g->tg = std::make_shared<ThreadGroup>(n);
+    for (int r = 0; r < n; ++r) {
+      auto c = std::make_shared<ThreadComm>();
+      c->g = g->tg;
+      c->nranks = n;
+      c->rank = r;
+      g->ctx[r]->comm = c;
+      g->ctx[r]->nranks = n;
+      g->ctx[r]->rank = r;
+    }
+  }
+  g_groups[devs] = g;
+  return g;
+}
+}  // namespace
+
+int lmra_run_algorithm_multigpu(int ndev, const int* devices, int algorithm, const double* x, const uint64_t* dims,
+                                int order, int x_location, const lmra_algo_config* cfg,
+                                const lmra_overrides* overrides, lmra_result** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (ndev < 1 || !devices) throw std::invalid_argument("bad device list");
+    if (order < 1) throw std::invalid_argument("cannot decompose an order-0 tensor");
+    std::vector<int> devs(devices, devices + ndev);
+    auto g = device_group(devs);
+    std::lock_guard<std::mutex> lk(g->run_mu);
+    size_t slice = 1;
+    for (int k = 0; k + 1 < order; ++k) slice *= dims[k];
+    const uint64_t L = dims[order - 1];
+    std::vector<int> rc(ndev, LMRA_OK);
+    std::vector<std::string> err(ndev);
+    std::vector<lmra_result*> res(ndev, nullptr);
+    std::vector<std::thread> th;
+    for (int r = 0; r < ndev; ++r)
+      th.emplace_back([&, r] {
+        uint64_t st = 0, cnt = 0;
+        lmra_shard_range(L, ndev, r, &st, &cnt);
+        const double* xr = x ? x + st * slice : nullptr;
+        void* slab = nullptr;
+        if (x_location == LMRA_DEVICE && ndev > 1 && devs[r] != devs[0]) {  // x lives on devices[0]
+          DeviceGuard dg(devs[r]);
+          const size_t bytes = cnt * slice * sizeof(double);
+          if (cudaMalloc(&slab, std::max<size_t>(bytes, 16)) != cudaSuccess ||
+              cudaMemcpyPeer(slab, devs[r], xr, devs[0], bytes) != cudaSuccess) {
+            rc[r] = LMRA_ECUDA;
+            err[r] = "slab copy to device " + std::to_string(devs[r]) + " failed";
+            if (g->ctx[r]->comm) g->ctx[r]->comm->abort();
+            if (slab) cudaFree(slab);
+            return;
+          }
+          xr = static_cast<const double*>(slab);
+        }
+        rc[r] = lmra_run_algorithm(g->ctx[r], algorithm, xr, dims, order, x_location, cfg, overrides, &res[r]);
+        if (rc[r] != LMRA_OK) err[r] = lmra_last_error();
+        if (slab) {
+          DeviceGuard dg(devs[r]);
+          cudaFree(slab);
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int r = 1; r < ndev; ++r)
+      if (res[r]) lmra_result_free(res[r]);
+    for (int r = 0; r < ndev; ++r)
+      if (rc[r] != LMRA_OK) {
+        if (res[0]) lmra_result_free(res[0]);
+        {  // the communicator was aborted: the next call builds a fresh group
+          std::lock_guard<std::mutex> lk2(g_groups_mu);
+          g_groups.erase(devs);
+        }
+        if (rc[r] == LMRA_EINVAL) throw std::invalid_argument(err[r]);
+        if (rc[r] == LMRA_ECUDA) throw CudaError(err[r]);
+        throw std::runtime_error(err[r]);
+      }
+    *out = res[0];
+  });
+}
+
 int lmra_result_order(const lmra_result* r) { return (int)r->factors.size(); }
+void lmra_result_hooi_stats(const lmra_result* r, int* converged, int* sweeps) {
+  *converged = r->hooi_converged;
+  *sweeps = r->hooi_sweeps;
+}
 void lmra_result_core_dims(const lmra_result* r, uint64_t* dims) {
   for (size_t n = 0; n < r->core_dims.size(); ++n) dims[n] = r->core_dims[n];
 }

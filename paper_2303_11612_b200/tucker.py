@@ -35,22 +35,39 @@ from . import _lib
 from ._lib import LmraError, LmraInvalidArgument, check, lib
 
 ALGORITHM_IDS = ["thosvd", "sthosvd", "hooi", "alg1", "alg2", "alg4", "alg5", "alg6", "alg7"]
-_ALG_CODE = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5, "alg6": 6, "alg7": 7}
+_ALG_CODE = {"alg1": 1, "alg2": 2, "alg4": 4, "alg5": 5, "alg6": 6, "alg7": 7,
+             "thosvd": 10, "sthosvd": 11, "hooi": 12}
 _REGIME = {"optimal": 0, "nearly_optimal": 1, "uniform": 2}
 _STRATEGY = {"A": 0, "B": 1}
 
 
 def parse_algorithm(name: str) -> Optional[str]:
-    """tucker.cpp:190-201: returns the id if known, else None."""
-    return name if name in ALGORITHM_IDS else None
+    """tucker.cpp:190-201 (lmra_parse_algorithm): the id if known, else None."""
+    code = C.c_int()
+    return name if lib.lmra_parse_algorithm(name.encode(), C.byref(code)) else None
 
 
-def algorithm_id(a: str) -> str:
-    return a
+def algorithm_id(a) -> str:
+    """tucker.cpp:203-215 (lmra_algorithm_id): id of an algorithm (name or ABI code); "?" if unknown."""
+    code = _ALG_CODE.get(a, -1) if isinstance(a, str) else int(a)
+    return lib.lmra_algorithm_id(code).decode()
 
 
 def all_algorithm_ids() -> List[str]:
-    return list(ALGORITHM_IDS)
+    """tucker.cpp:217-220 (lmra_all_algorithm_ids), in the reference's order."""
+    buf = (C.c_char_p * 16)()
+    n = lib.lmra_all_algorithm_ids(buf, 16)
+    return [buf[k].decode() for k in range(n)]
+
+
+def thread_cap() -> int:
+    """tucker.cpp:164-172: LMRA_NUM_THREADS, default 1, clamped to [1, 64]."""
+    return int(lib.lmra_thread_cap())
+
+
+def device_cap() -> int:
+    """LMRA_NUM_GPUS, default 1, clamped to the visible devices (the multi-GPU knob)."""
+    return int(lib.lmra_device_cap())
 
 
 @dataclass
@@ -66,6 +83,8 @@ class AlgoConfig:
     order: Optional[Sequence[int]] = None
     seed: int = 0
     strategy: str = "A"              # GramStrategy
+    hooi_max_sweeps: int = 50
+    hooi_tol: float = 1e-8
 
     def _to_c(self):
         if self.regime not in _REGIME:
@@ -96,6 +115,8 @@ class AlgoConfig:
         c.order, c.n_order = arr(self.order)
         c.seed = int(self.seed)
         c.strategy = _STRATEGY[self.strategy]
+        c.hooi_max_sweeps = int(self.hooi_max_sweeps)
+        c.hooi_tol = float(self.hooi_tol)
         return c, keep
 
 
@@ -430,8 +451,6 @@ def run_raw(alg: str, a, cfg: AlgoConfig, *, ctx: Optional[Context] = None, omeg
     global_dims: on a sharded context `a` is this rank's slab of the last mode and
     global_dims the whole tensor's dims (default: a's own dims, i.e. unsharded)."""
     if alg not in _ALG_CODE:
-        if alg in ALGORITHM_IDS:
-            raise LmraInvalidArgument(f"{alg} is outside the B200 hot path (randomized alg1-alg7)")
         raise LmraInvalidArgument("unknown algorithm")
     t = _as_tensor(a)
     ctx = ctx or default_context()
@@ -493,6 +512,45 @@ def rand_thosvd_power_qr(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
 def rand_sthosvd_power_qr(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
     """tucker.cpp:438-454 (alg7): sequential modes, QR-proxy extraction."""
     return run_algorithm("alg7", a, cfg, **kw)
+
+
+def t_hosvd(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    """tucker.cpp:242-248: factors from the full unfoldings (deterministic baseline)."""
+    return run_algorithm("thosvd", a, cfg, **kw)
+
+
+def st_hosvd(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    """tucker.cpp:250-259: sequentially truncated HOSVD (deterministic baseline)."""
+    return run_algorithm("sthosvd", a, cfg, **kw)
+
+
+def hooi(a, cfg: AlgoConfig, **kw) -> TuckerDecomposition:
+    """tucker.cpp:261-316: higher-order orthogonal iteration from the st_hosvd start; stops when
+    |delta ||core||| / ||a|| < cfg.hooi_tol or after cfg.hooi_max_sweeps sweeps."""
+    return run_algorithm("hooi", a, cfg, **kw)
+
+
+def run_raw_multigpu(alg: str, a, cfg: AlgoConfig, devices: Sequence[int]) -> "_Result":
+    """run_algorithm on several devices from this process (lmra_run_algorithm_multigpu): one
+    host thread and context per device, the tensor split along its last mode.  `a`: host
+    DenseTensor / ndarray, or a device tensor on devices[0]."""
+    if alg not in _ALG_CODE:
+        raise LmraInvalidArgument("unknown algorithm")
+    t = _as_tensor(a)
+    dims = np.asarray(t.dims, dtype=np.uint64)
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    c, keep = cfg._to_c()
+    h = C.c_void_p()
+    if t.on_device:
+        xp, loc = C.c_void_p(t.ptr), _lib.LMRA_DEVICE
+    else:
+        xp, loc = C.c_void_p(t.data.ctypes.data), _lib.LMRA_HOST
+    _torch_sync()
+    rc = lib.lmra_run_algorithm_multigpu(len(devices), devs, _ALG_CODE[alg], xp, dims.ctypes.data_as(_lib.u64p),
+                                         len(t.dims), loc, C.byref(c), None, C.byref(h))
+    del keep
+    check(rc)
+    return _Result(h, len(t.dims))
 
 
 def amm_sample_counts(dims: Sequence[int], cfg: AlgoConfig, sequential: bool) -> List[int]:

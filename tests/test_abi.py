@@ -59,6 +59,11 @@ def test_cpp_dropin_header_compiles_and_links(tmp_path):
         f"  lmra::save_tensor(\"{tmp_path}/t.tnsr\", t);\n"
         f"  lmra::DenseTensor u = lmra::load_tensor(\"{tmp_path}/t.tnsr\");\n"
         "  if (u.dims() != t.dims() || u.data()[5] != 6.5) return 2;\n"
+        "  if (lmra::all_algorithm_ids().size() != 9 || lmra::algorithm_id(lmra::Algorithm::Hooi) != \"hooi\") return 5;\n"
+        "  if (!lmra::parse_algorithm(\"alg5\") || lmra::parse_algorithm(\"alg3\")) return 6;\n"
+        "  if (lmra::thread_cap() < 1) return 7;\n"
+        "  if (cfg.rank.clamped_for({1, 5, 5}) != std::vector<std::size_t>({1, 2, 2})) return 8;\n"
+        "  try { cfg.rank.clamped_for({1, 5}); return 9; } catch (const std::invalid_argument&) {}\n"
         "  try { lmra::load_tensor(\"/nonexistent.tnsr\"); return 3; }\n"
         "  catch (const std::runtime_error& e) { return std::string(e.what()).find(\"cannot open\") == 0 ? 0 : 4; }\n"
         "}\n")

@@ -249,7 +249,7 @@ def test_config_validation(gpu_ctx, lmra):
         with pytest.raises(lmra.LmraInvalidArgument):
             lmra.run_algorithm(alg, x, lmra.AlgoConfig(**kw))
     with pytest.raises(lmra.LmraInvalidArgument):
-        lmra.run_algorithm("hooi", x, lmra.AlgoConfig(rank=[2, 2, 2]))
+        lmra.run_algorithm("alg3", x, lmra.AlgoConfig(rank=[2, 2, 2]))
 
 
 def test_degenerate_shapes(gpu_ctx, lmra, orc):

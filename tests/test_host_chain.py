@@ -1,8 +1,12 @@
 """The product's host-side restatements (csrc/host/host_chain.cpp), reached through the C ABI
 without a GPU, against the oracle: the sampling chain and the config rules must be bit-exact.
 (On the device path the same chain runs in sampler.cu -- tests/test_gpu_sampler.py.)"""
+import os
+
 import numpy as np
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("regime", ["optimal", "nearly_optimal", "uniform"])
@@ -44,4 +48,31 @@ def test_error_surface(lmra):
     with pytest.raises(lmra.LmraInvalidArgument):
         lmra.randsample(0, np.array([1.0]), 1, 1)
     with pytest.raises(lmra.LmraInvalidArgument):
-        lmra.run_algorithm("thosvd", np.zeros((2, 2)), lmra.AlgoConfig(rank=[1, 1]))
+        lmra.run_algorithm("alg3", np.zeros((2, 2)), lmra.AlgoConfig(rank=[1, 1]))
+
+
+def test_algorithm_ids_and_knobs(lmra, monkeypatch):
+    # tucker.cpp:164-220: ids in the reference's order, parse / id round trips, thread_cap
+    ids = lmra.all_algorithm_ids()
+    assert ids == ["thosvd", "sthosvd", "hooi", "alg1", "alg2", "alg4", "alg5", "alg6", "alg7"]
+    for a in ids:
+        assert lmra.parse_algorithm(a) == a
+        assert lmra.algorithm_id(a) == a
+    assert lmra.parse_algorithm("alg3") is None and lmra.parse_algorithm("") is None
+    assert lmra.algorithm_id(99) == "?"
+    assert lmra.thread_cap() >= 1
+    assert lmra.device_cap() == 1  # no device visible here (or LMRA_NUM_GPUS unset)
+
+
+def test_knob_semantics_in_fresh_process():
+    # the caps are read once per process (static, as tucker.cpp:164-172): check the env idiom
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_2303_11612_b200 as P; "
+            "print(P.thread_cap())" % ROOT)
+    for env, want in (({"LMRA_NUM_THREADS": "7"}, "7"), ({"LMRA_NUM_THREADS": "500"}, "64"),
+                      ({"LMRA_NUM_THREADS": "0"}, "1"), ({}, "1")):
+        e = {k: v for k, v in os.environ.items() if k != "LMRA_NUM_THREADS"}
+        e.update(env)
+        out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, check=True)
+        assert out.stdout.strip() == want, (env, out.stdout, out.stderr)
