@@ -456,18 +456,23 @@ Mat gaussian_matrix(size_t rows, size_t cols, uint64_t seed, uint64_t stream) {
   return g;
 }
 
-// Canonical squared norm of a fiber (shared with the GPU kernels): chunks of 32
-// consecutive entries accumulated with fma, chunk partials added in order.
+// Canonical squared norm of a fiber (shared with the GPU kernels): chunks of 32 consecutive
+// entries accumulated with fma from +0; pairs of chunks (segments of 64 entries) summed; the
+// segment sums added in order.  (Two levels so that a fibre split across devices at multiples
+// of 64 entries combines per-device segment sums into the same bits; fibres of <= 64 entries
+// give the plain in-order chunk sum.)
 double canonical_sqnorm(const double* x, size_t len, size_t stride) {
-  double total = 0.0;
-  for (size_t c0 = 0; c0 < len; c0 += 32) {
+  double total = 0.0, seg = 0.0;
+  size_t c = 0;
+  for (size_t c0 = 0; c0 < len; c0 += 32, ++c) {
     double p = 0.0;
     size_t c1 = std::min(len, c0 + 32);
     for (size_t r = c0; r < c1; ++r) {
       double v = x[r * stride];
       p = std::fma(v, v, p);
     }
-    total = total + p;
+    seg = (c & 1) ? seg + p : p;
+    if ((c & 1) || c1 == len) total = total + seg;
   }
   return total;
 }

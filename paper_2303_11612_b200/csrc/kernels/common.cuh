@@ -40,6 +40,15 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 
+// The canonical column squared norm (shared with the oracle, canonical_sqnorm): chunks of 32
+// fibre entries summed by an fma chain from +0, pairs of chunks (64-entry segments) summed,
+// segment sums added in order.  canon_add folds chunk c's partial p into (seg, total); `last`
+// marks the fibre's final chunk.
+__device__ __forceinline__ void canon_add(double p, long long c, bool last, double& seg, double& total) {
+  seg = (c & 1) ? seg + p : p;
+  if ((c & 1) || last) total = total + seg;
+}
+
 __device__ __forceinline__ long long col_base(long long j, long long inner, long long I) {
   if (inner == 1) return j * I;
   long long o = j / inner;

@@ -60,9 +60,21 @@ cudaError_t launch_gather(const double* x, ModeView v, const long long* idx, con
 // fma within a chunk, chunk partials added in order) -- bit-identical to the oracle.
 cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaStream_t st);
 // The same canonical norms for all three modes of a 3-way tensor from one read (norms3.cu).
+// p2_chunks (optional, ceil(I2/32) x I0 I1): mode 2's chunk partials go there instead of w2
+// (a sharded slab's last mode, combined across devices).
 size_t norms3_workspace_doubles(long long I0, long long I1, long long I2);
 cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long I2, double* w0,
-                          double* w1, double* w2, double* work, cudaStream_t st);
+                          double* w1, double* w2, double* work, cudaStream_t st, double* p2_chunks = nullptr);
+// A fibre split across devices (sharded mode N-1, slab boundaries at multiples of 64 entries):
+// chunk partials P[c][j] of the local rows, their segment (chunk pair) sums S[s][j], and the
+// combine of every rank's segments in global order -- the canonical norm's exact bits.
+struct SegCounts {
+  int n[64];
+};
+cudaError_t launch_chunk_partials(const double* x, ModeView v, double* P, cudaStream_t st);
+cudaError_t launch_segment_sums(const double* P, long long J, int nchunks, double* S, cudaStream_t st);
+cudaError_t launch_segment_combine(const double* G, long long J, int nranks, int kmax, const SegCounts& counts,
+                                   double* w, cudaStream_t st);
 
 // The reference's sampling chain on the device, bit-exact (sampler.cu):
 // probabilities from squared column norms w (regime 0 optimal, 1 nearly-optimal, 2 uniform)

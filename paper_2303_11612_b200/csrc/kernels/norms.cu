@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(128) sqnorm_contig_kernel(const double* __rest
   __shared__ double tile[128][kNormChunk + 1];
   const int tid = threadIdx.x;
   const long long j0 = (long long)blockIdx.x * 128;
-  double total = 0.0;
+  double total = 0.0, seg = 0.0;
   for (long long r0 = 0; r0 < I; r0 += kNormChunk) {
     const int n = (I - r0 < kNormChunk) ? (int)(I - r0) : kNormChunk;
     // coalesced: a warp reads 32 consecutive entries of one fiber per instruction
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(128) sqnorm_contig_kernel(const double* __rest
       double v = tile[tid][q];
       p = fma(v, v, p);
     }
-    total = total + p;
+    canon_add(p, r0 / kNormChunk, r0 + kNormChunk >= I, seg, total);
     __syncthreads();
   }
   const long long j = j0 + tid;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) sqnorm_strided_kernel(const double* __res
   if (j >= J) return;
   const long long o = j / v.inner, i = j - o * v.inner;
   const double* f = x + i + v.inner * v.I * o;
-  double total = 0.0;
+  double total = 0.0, seg = 0.0;
   long long r0 = 0;
   for (; r0 + kNormChunk <= v.I; r0 += kNormChunk) {
     double vals[kNormChunk];
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) sqnorm_strided_kernel(const double* __res
     double p = 0.0;
 #pragma unroll
     for (int q = 0; q < kNormChunk; ++q) p = fma(vals[q], vals[q], p);
-    total = total + p;
+    canon_add(p, r0 / kNormChunk, r0 + kNormChunk >= v.I, seg, total);
   }
   if (r0 < v.I) {
     double p = 0.0;
@@ -73,9 +73,71 @@ __global__ void __launch_bounds__(256) sqnorm_strided_kernel(const double* __res
       double val = __ldcs(f + v.inner * r);
       p = fma(val, val, p);
     }
-    total = total + p;
+    canon_add(p, r0 / kNormChunk, true, seg, total);
   }
   w[j] = total;
+}
+
+// ---- the canonical norm of a fibre split across devices (sharded mode N-1) ----
+// P[c * J + j] = chunk c's partial (fma chain over its 32 entries) of column j of the view
+__global__ void __launch_bounds__(256) chunk_partials_kernel(const double* __restrict__ x, ModeView v,
+                                                             double* __restrict__ P) {
+  const long long J = v.inner * v.outer;
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long c = blockIdx.y;
+  if (j >= J) return;
+  const long long o = j / v.inner, i = j - o * v.inner;
+  const double* f = x + i + v.inner * v.I * o;
+  const long long r0 = c * kNormChunk, r1 = min(v.I, r0 + kNormChunk);
+  double p = 0.0;
+  for (long long r = r0; r < r1; ++r) {
+    const double val = __ldcs(f + v.inner * r);
+    p = fma(val, val, p);
+  }
+  P[c * J + j] = p;
+}
+
+// S[s * J + j] = segment s of column j: chunk 2s's partial + chunk 2s + 1's (when it exists)
+__global__ void segment_sums_kernel(const double* __restrict__ P, long long J, int nchunks, double* __restrict__ S) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int sg = blockIdx.y;
+  if (j >= J) return;
+  double v = P[(long long)(2 * sg) * J + j];
+  if (2 * sg + 1 < nchunks) v = v + P[(long long)(2 * sg + 1) * J + j];
+  S[(long long)sg * J + j] = v;
+}
+
+// w[j] = the segments of column j added in global order: rank q contributed counts[q]
+// segments at G[(q * kmax + s) * J + j]
+__global__ void segment_combine_kernel(const double* __restrict__ G, long long J, int nranks, int kmax,
+                                       SegCounts counts, double* __restrict__ w) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  double total = 0.0;
+  for (int q = 0; q < nranks; ++q)
+    for (int sg = 0; sg < counts.n[q]; ++sg) total = total + G[((long long)q * kmax + sg) * J + j];
+  w[j] = total;
+}
+
+cudaError_t launch_chunk_partials(const double* x, ModeView v, double* P, cudaStream_t st) {
+  const long long J = v.inner * v.outer, nc = (v.I + kNormChunk - 1) / kNormChunk;
+  if (J == 0 || nc == 0) return cudaSuccess;
+  chunk_partials_kernel<<<dim3((unsigned)((J + 255) / 256), (unsigned)nc), 256, 0, st>>>(x, v, P); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segment_sums(const double* P, long long J, int nchunks, double* S, cudaStream_t st) {
+  const int nseg = (nchunks + 1) / 2;
+  if (J == 0 || nseg == 0) return cudaSuccess;
+  segment_sums_kernel<<<dim3((unsigned)((J + 255) / 256), (unsigned)nseg), 256, 0, st>>>(P, J, nchunks, S); note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segment_combine(const double* G, long long J, int nranks, int kmax, const SegCounts& counts,
+                                   double* w, cudaStream_t st) {
+  if (J == 0) return cudaSuccess;
+  segment_combine_kernel<<<(unsigned)((J + 255) / 256), 256, 0, st>>>(G, J, nranks, kmax, counts, w); note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaStream_t st) {

@@ -2,9 +2,9 @@
 // tensor (T-HOSVD with sampling: every mode's probabilities come from the same input,
 // so the mode passes share the read -- SURVEY 8d rule R2).
 //
-// Canonical order (shared with the oracle, norms.cu): a column's squared norm is the
-// in-order sum of chunk partials, a chunk partial being the fma-sequential sum over 32
-// consecutive fiber entries.  Each element belongs to exactly one chunk per mode, so a
+// Canonical order (shared with the oracle, norms.cu, common.cuh canon_add): a column's squared
+// norm is the in-order sum of chunk-pair sums, a chunk partial being the fma-sequential sum
+// over 32 consecutive fiber entries.  Each element belongs to exactly one chunk per mode, so a
 // 32 x 32 x 32 brick holds complete chunks of all three modes:
 //   pass 1 (this kernel, one read of X): chunk partials of modes 0 and 1 -> P0, P1
 //          (|X|/32 doubles each); mode 2 combined in registers (see below)
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kN3Threads) norms3_chunks_kernel(
   };
 #pragma unroll
   for (int s = 0; s < kN3Stages - 1; ++s) issue(z0 + s);
-  double part2[4] = {0.0, 0.0, 0.0, 0.0}, tot2[4] = {0.0, 0.0, 0.0, 0.0};
+  double part2[4] = {0.0, 0.0, 0.0, 0.0}, tot2[4] = {0.0, 0.0, 0.0, 0.0}, seg2[4] = {0.0, 0.0, 0.0, 0.0};
   for (long long i2 = z0; i2 < z1; ++i2) {
     issue(i2 + kN3Stages - 1);
     cp_async_wait<kN3Stages - 1>();
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kN3Threads) norms3_chunks_kernel(
         if (P2) {
           if (ok[k]) P2[(i2 / kB) * slab + (i0b + a0) + I0 * (i1b + a1 + 8 * k)] = part2[k];
         } else {
-          tot2[k] = tot2[k] + part2[k];
+          canon_add(part2[k], i2 / kB, i2 == I2 - 1, seg2[k], tot2[k]);
         }
         part2[k] = 0.0;
       }
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kTThreads, 3) norms3_tma_kernel(
     return;
   }
   const int a0 = tid & 31, a1 = tid >> 5;  // mode-2 fibres (i0 = a0, i1 = a1 + 8k)
-  double part2[4] = {0.0, 0.0, 0.0, 0.0}, tot2[4] = {0.0, 0.0, 0.0, 0.0};
+  double part2[4] = {0.0, 0.0, 0.0, 0.0}, tot2[4] = {0.0, 0.0, 0.0, 0.0}, seg2[4] = {0.0, 0.0, 0.0, 0.0};
   int stage = 0;
   unsigned phase = 0;
   for (long long i2 = z0; i2 < z1; ++i2) {
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kTThreads, 3) norms3_tma_kernel(
           if (a0 < n0 && a1 + 8 * k < n1)
             P2[(i2 / kB) * (I0 * I1) + (i0b + a0) + I0 * (i1b + a1 + 8 * k)] = part2[k];
         } else {
-          tot2[k] = tot2[k] + part2[k];
+          canon_add(part2[k], i2 / kB, i2 == I2 - 1, seg2[k], tot2[k]);
         }
         part2[k] = 0.0;
       }
@@ -258,13 +258,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// w[j] = sum_c P[c][j] in chunk order (c = 0, 1, ...): the canonical combine
+// w[j] = the canonical combine of the chunk partials P[c][j], c = 0, 1, ... (canon_add)
 __global__ void chunk_combine_kernel(const double* __restrict__ P, long long J, int nchunks,
                                      double* __restrict__ w) {
   const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= J) return;
-  double total = 0.0;
-  for (int c = 0; c < nchunks; ++c) total = total + P[(long long)c * J + j];
+  double total = 0.0, seg = 0.0;
+  for (int c = 0; c < nchunks; ++c) canon_add(P[(long long)c * J + j], c, c == nchunks - 1, seg, total);
   w[j] = total;
 }
 
@@ -282,7 +282,7 @@ size_t norms3_workspace_doubles(long long I0, long long I1, long long I2) {
 }
 
 cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long I2, double* w0,
-                          double* w1, double* w2, double* work, cudaStream_t st) {
+                          double* w1, double* w2, double* work, cudaStream_t st, double* p2_chunks) {
   const long long c0 = (I0 + kB - 1) / kB, c1 = (I1 + kB - 1) / kB, c2 = (I2 + kB - 1) / kB;
   double* P0 = work;
   double* P1 = P0 + c0 * I1 * I2;
@@ -314,7 +314,7 @@ cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long
       if (fill(z) > fill(best) + 1e-9) best = z;
     zs = best;
   }
-  double* P2 = zs > 1 ? P1 + c1 * I0 * I2 : nullptr;
+  double* P2 = p2_chunks ? p2_chunks : (zs > 1 ? P1 + c1 * I0 * I2 : nullptr);
   const long long seg = ((c2 + zs - 1) / zs) * kB;
   dim3 grid((unsigned)c0, (unsigned)c1, (unsigned)((I2 + seg - 1) / seg));
   CUtensorMap tmap;
@@ -338,7 +338,7 @@ cudaError_t launch_norms3(const double* x, long long I0, long long I1, long long
   if (e != cudaSuccess) return e;
   chunk_combine_kernel<<<(unsigned)((I1 * I2 + 255) / 256), 256, 0, st>>>(P0, I1 * I2, (int)c0, w0); note_launch();
   chunk_combine_kernel<<<(unsigned)((I0 * I2 + 255) / 256), 256, 0, st>>>(P1, I0 * I2, (int)c1, w1); note_launch();
-  if (P2) {
+  if (P2 && !p2_chunks) {
     chunk_combine_kernel<<<(unsigned)((I0 * I1 + 255) / 256), 256, 0, st>>>(P2, I0 * I1, (int)c2, w2);
     note_launch();
   }

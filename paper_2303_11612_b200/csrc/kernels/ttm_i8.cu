@@ -72,6 +72,8 @@ constexpr int kI8MaxN = 64;  // N = mu rounded up to 16 (M = 128 needs N % 16 ==
 constexpr int kI8ABufs = 2;
 constexpr int kI8StageLd = 9;  // epilogue output staging: 32 columns x 8 outputs, row pad 1
 constexpr int kI8StageBytes = kI8EpiWarps * 32 * kI8StageLd * 8;
+constexpr int kTR = 4;  // tile-id ring of the dynamic scheduler
+constexpr int kTRConsumers = 1 + 1 + kI8EpiWarps + 8;  // Q producer, MMA, epilogue warps, slicer warps
 
 __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr) {
   // K-major, no swizzle: 8-row x 16-byte core matrices, LBO 128 B (K chunk), SBO 256 B (rows)
@@ -186,6 +188,7 @@ struct I8Geom {
   const int* fexp_in;   // inner: max binary exponent of column (r, o) at r + R o
   int* fexp_out;        // mode-0, optional: max exponent of Y's mode-1 fibres (m, o), m + mu o,
   long long I1;         //   with j = i1 + I1 o (the next contraction's columns)
+  unsigned long long* tile_ctr;  // dynamic tile scheduler: next tile (zeroed before the launch)
 };
 
 // binary exponent e with |v| < 2^(e+1) (an upper bound for subnormals), INT_MIN for 0
@@ -222,7 +225,10 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
   uint64_t* aempty = afull + kAB;              // [kAB]
   uint64_t* accfull = aempty + kAB;            // [1]
   uint64_t* accempty = accfull + 1;            // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+  uint64_t* tfull = accempty + 1;              // [kTR] tile id published (X producer)
+  uint64_t* tempty = tfull + kTR;              // [kTR] tile id read by every other role
+  long long* tring = reinterpret_cast<long long*>(tempty + kTR);  // [kTR] tile ids
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tring + kTR);
   double* qsc = reinterpret_cast<double*>(tmem_slot + 4);  // [N] 2^eq_m
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -247,6 +253,10 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     }
     mbar_init(accfull, 1);
     mbar_init(accempty, kI8EpiWarps);
+    for (int r = 0; r < kTR; ++r) {
+      mbar_init(&tfull[r], 1);
+      mbar_init(&tempty[r], kTRConsumers);
+    }
     mbar_fence_init();
   }
   if (tid < N) qsc[tid] = ldexp(1.0, tid < mu ? eqg[tid] : 0);  // 2^eq_m
@@ -259,11 +269,36 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Dynamic tile scheduler: the X producer takes tiles from a global counter and publishes them
+  // in a small ring; every other role follows the same sequence (a CTA that starts late --
+  // its SM busy with a concurrent kernel -- simply takes fewer tiles).  take_warp: whole warp;
+  // take_lane: a single-lane role.
+  auto take_warp = [&](long long it) -> long long {
+    const int slot = (int)(it % kTR);
+    mbar_wait(&tfull[slot], (unsigned)((it / kTR) & 1));
+    const long long t = tring[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[slot]);
+    return t;
+  };
+  auto take_lane = [&](long long it) -> long long {
+    const int slot = (int)(it % kTR);
+    mbar_wait(&tfull[slot], (unsigned)((it / kTR) & 1));
+    const long long t = tring[slot];
+    mbar_arrive(&tempty[slot]);
+    return t;
+  };
 
   if (warp == kI8ProdWarp) {  // ---------------- producers: lane 0 X tiles, lane 1 Q digits
     if (lane == 0) {
       long long g = 0;
-      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (long long it = 0;; ++it) {
+        const int slot = (int)(it % kTR);
+        mbar_wait(&tempty[slot], (unsigned)((it / kTR) & 1) ^ 1u);
+        const long long t = (long long)atomicAdd(geo.tile_ctr, 1ull);
+        tring[slot] = t;
+        mbar_arrive(&tfull[slot]);
+        if (t >= ntiles) break;
         for (int ks = 0; ks < nks; ++ks, ++g) {
           const int st = (int)(g % kI8Stages);
           I8_WAIT(0, mbar_wait(&empty[st], (unsigned)((g / kI8Stages) & 1) ^ 1u));
@@ -282,7 +317,8 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
                                   // the X producer must not hold it up)
     if (lane == 0) {
       long long g = 0;
-      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (long long it = 0;; ++it) {
+        if (take_lane(it) >= ntiles) break;
         for (int ks = 0; ks < nks; ++ks, ++g) {
           const int qsi = (int)(g % kI8QStages);
           I8_WAIT(1, mbar_wait(&qempty[qsi], (unsigned)((g / kI8QStages) & 1) ^ 1u));
@@ -294,7 +330,8 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
   } else if (warp == kI8MmaWarp) {  // ---------------- MMA issuer
     if (lane == 0) {
       long long g = 0, tcount = 0;
-      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+      for (long long it = 0;; ++it, ++tcount) {
+        if (take_lane(it) >= ntiles) break;
         I8_WAIT(2, mbar_wait(accempty, (unsigned)(tcount & 1) ^ 1u));  // previous tile drained
         tc_fence_after();
         for (int ks = 0; ks < nks; ++ks, ++g) {
@@ -335,7 +372,9 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     double* ost = ostage + (warp - kI8EpiWarp0) * 32 * kI8StageLd;
     long long tcount = 0;
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+    for (long long it = 0;; ++it, ++tcount) {
+      const long long t = take_warp(it);
+      if (t >= ntiles) break;
       const long long j = t * kI8Tile + jl;
       const long long jw0 = t * kI8Tile + 32 * (warp & 3);  // first column of this warp
       const int rrow = jl & 63;                                // inner form: row r, slice o
@@ -452,7 +491,9 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
     const int jl = tid & (kI8Tile - 1);  // column within the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     long long g = 0, tcount = 0;
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+    for (long long it = 0;; ++it, ++tcount) {
+      const long long t = take_warp(it);
+      if (t >= ntiles) break;
       const long long j = t * kI8Tile + jl;
       const int rrow = jl & 63;
       const long long ocol = 2 * t + (jl >> 6);
@@ -652,8 +693,17 @@ bool ttm_i8_inner_supported(long long R, long long K, long long O, int mu, const
 size_t ttm_i8_workspace_bytes(long long K, int mu) {
   const int N = ((mu + 15) / 16) * 16;
   const long long nks = (K + kI8Kstep - 1) / kI8Kstep;
-  return (size_t)nks * kI8Digits * N * kI8Kstep + 4 * 64 + 256;
+  return (size_t)nks * kI8Digits * N * kI8Kstep + 4 * 64 + 256 + 256;  // + the tile counter
 }
+
+namespace {
+// the tile counter lives in the last 256 bytes of the workspace
+unsigned long long* tile_counter(void* work, long long K, int mu, cudaStream_t st, cudaError_t* e) {
+  auto* c = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(work) + ttm_i8_workspace_bytes(K, mu) - 256);
+  *e = cudaMemsetAsync(c, 0, sizeof(unsigned long long), st);
+  return c;
+}
+}  // namespace
 
 cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const double* q, int mu,
                           const double* w, double* y, void* work, cudaStream_t st, int* fexp_out,
@@ -671,7 +721,9 @@ cudaError_t launch_ttm_i8(const double* x, long long K, long long J, const doubl
                               box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  I8Geom geo{J, (int)K, 0, 0, w, nullptr, fexp_out, I1};
+  unsigned long long* ctr = tile_counter(work, K, mu, st, &e);
+  if (e != cudaSuccess) return e;
+  I8Geom geo{J, (int)K, 0, 0, w, nullptr, fexp_out, I1, ctr};
   return dispatch_n<false>(map, qd, eq, geo, mu, y, st);
 }
 
@@ -698,7 +750,9 @@ cudaError_t launch_ttm_i8_inner(const double* x, long long R, long long K, long 
                               box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  I8Geom geo{0, (int)K, (int)R, O, nullptr, fexp_in, nullptr, 0};
+  unsigned long long* ctr = tile_counter(work, K, mu, st, &e);
+  if (e != cudaSuccess) return e;
+  I8Geom geo{0, (int)K, (int)R, O, nullptr, fexp_in, nullptr, 0, ctr};
   return dispatch_n<true>(map, qd, eq, geo, mu, y, st);
 }
 

@@ -439,6 +439,25 @@ size_t prod(const std::vector<size_t>& d) {
   return p;
 }
 
+// Shard plan of the last mode (extent L over P ranks): contiguous slabs, balanced in units of
+// 64 rows (two canonical norm chunks) when L >= 64 P, so that a fibre of the last mode splits
+// between ranks only at segment boundaries of the canonical squared norm (canon_add) and the
+// sharded norms combine to the single-device bits; otherwise balanced rows.
+constexpr size_t kShardUnit = 64;
+void shard_bounds(size_t L, size_t P, size_t r, size_t* start, size_t* count) {
+  size_t b, e;
+  if (L >= kShardUnit * P) {
+    const size_t u = (L + kShardUnit - 1) / kShardUnit;
+    b = std::min(L, (u * r) / P * kShardUnit);
+    e = std::min(L, (u * (r + 1)) / P * kShardUnit);
+  } else {
+    b = (L * r) / P;
+    e = (L * (r + 1)) / P;
+  }
+  *start = b;
+  *count = e - b;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ result
@@ -1196,8 +1215,7 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   if (L < (size_t)P) throw std::invalid_argument("last mode extent is smaller than the rank count");
   std::vector<size_t> sh0(P), shc(P);
   for (int q = 0; q < P; ++q) {
-    sh0[q] = (L * q) / P;
-    shc[q] = (L * (q + 1)) / P - sh0[q];
+    shard_bounds(L, (size_t)P, (size_t)q, &sh0[q], &shc[q]);
   }
   const size_t s0 = sh0[R], c0 = shc[R], cmax = *std::max_element(shc.begin(), shc.end());
 
@@ -1320,22 +1338,57 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
     DevBuf c;
   };
   std::vector<ModeState> ms(N);
-  // local weights already produced by the fused 3-mode pass (T-HOSVD on a 3-way slab)
+  // local weights already produced by the fused 3-mode pass (T-HOSVD on a 3-way slab); for the
+  // last mode its chunk partials when the slabs are segment-aligned
   std::vector<DevBuf> pre_w(N);
+  DevBuf pre_chunks;
   bool pre_last = false;
+  const bool seg_aligned = L >= kShardUnit * (size_t)P;
+  if (seg_aligned && P > 64) throw std::invalid_argument("more than 64 ranks");
   auto norms_for = [&](size_t n) {
     const std::vector<size_t> ld = ldims();
     const ModeView v = view_of(ld, n);
     const bool rows_split = sharded && n == N - 1;
     const size_t Jl = (size_t)(v.inner * v.outer);
-    if (!sharded || rows_split) {  // every column local (rows split for mode N-1)
+    if (!sharded) {  // replicated tensor: every column local
       ms[n].J = Jl;
       if (amm && cfg.regime != kUniform) {
-        if (!(rows_split && pre_last)) {
+        d_w[n] = DevBuf(Jl, st);
+        eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+      }
+    } else if (rows_split) {  // mode N-1: every column local, its rows split across the ranks
+      ms[n].J = Jl;
+      if (amm && cfg.regime != kUniform) {
+        if (seg_aligned) {
+          // the canonical norm's segments of this rank's rows, all-gathered and added in global
+          // order: the single-device bits (shard boundaries at multiples of 64 rows)
+          const size_t nch = (c0 + 31) / 32;
+          DevBuf chunks;
+          if (pre_last) {
+            chunks = std::move(pre_chunks);
+          } else {
+            chunks = DevBuf(nch * Jl, st);
+            eng.launch("norms", [&] { return lmra_dev::launch_chunk_partials(cur, v, chunks.get(), st); });
+          }
+          lmra_dev::SegCounts cnt{};
+          int kmax = 0;
+          for (int q = 0; q < P; ++q) {
+            cnt.n[q] = (int)(((shc[q] + 31) / 32 + 1) / 2);
+            kmax = std::max(kmax, cnt.n[q]);
+          }
+          DevBuf segs((size_t)kmax * Jl, st), all((size_t)P * kmax * Jl, st);
+          ck(cudaMemsetAsync(segs.get(), 0, (size_t)kmax * Jl * sizeof(double), st), "memset");
+          ck(lmra_dev::launch_segment_sums(chunks.get(), (long long)Jl, (int)nch, segs.get(), st), "segments");
+          comm.allgather(segs.get(), all.get(), (size_t)kmax * Jl, st);
           d_w[n] = DevBuf(Jl, st);
-          eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+          ck(lmra_dev::launch_segment_combine(all.get(), (long long)Jl, P, kmax, cnt, d_w[n].get(), st), "combine");
+        } else {  // unaligned slabs (L < 64 P): rank partials added in rank order
+          if (!pre_last) {
+            d_w[n] = DevBuf(Jl, st);
+            eng.launch("norms", [&] { return lmra_dev::launch_column_sqnorms(cur, v, d_w[n].get(), st); });
+          }
+          comm.allreduce_sum(d_w[n].get(), Jl, st);
         }
-        if (rows_split) comm.allreduce_sum(d_w[n].get(), Jl, st);
       }
     } else {  // n < N-1: rank-local column range
       const size_t per = Jl / c0, Jg = per * L;
@@ -1524,10 +1577,11 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
       ck(cudaMemsetAsync(pre_w[0].get(), 0, per0 * cmax * sizeof(double), st), "memset");
       ck(cudaMemsetAsync(pre_w[1].get(), 0, per1 * cmax * sizeof(double), st), "memset");
       d_w[2] = DevBuf((size_t)(I0 * I1), st);
+      if (seg_aligned) pre_chunks = DevBuf((size_t)((I2 + 31) / 32) * (size_t)(I0 * I1), st);
       DevBuf nwork(lmra_dev::norms3_workspace_doubles(I0, I1, I2), st);
       eng.launch("norms", [&] {
         return lmra_dev::launch_norms3(cur, I0, I1, I2, pre_w[0].get(), pre_w[1].get(), d_w[2].get(),
-                                       nwork.get(), st);
+                                       nwork.get(), st, seg_aligned ? pre_chunks.get() : nullptr);
       });
       pre_last = true;
     }
@@ -1996,10 +2050,10 @@ int lmra_context_set_thread_comm(lmra_context* ctx, void* group, int rank) {
 int lmra_shard_range(uint64_t extent, int nranks, int rank, uint64_t* start, uint64_t* count) {
   return guard([&] {
     if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank layout");
-    uint64_t b = (extent * (uint64_t)rank) / (uint64_t)nranks;
-    uint64_t e = (extent * (uint64_t)(rank + 1)) / (uint64_t)nranks;
+    size_t b = 0, c = 0;
+    shard_bounds((size_t)extent, (size_t)nranks, (size_t)rank, &b, &c);
     *start = b;
-    *count = e - b;
+    *count = c;
   });
 }
 
@@ -2089,9 +2143,9 @@ int lmra_run_algorithm(lmra_context* ctx, int algorithm, const double* x, const 
       if (sharded) {  // x is this rank's slab of the last mode
         const size_t L = in.dims.back();
         if (L == 0) throw std::invalid_argument("tensor dimension must be positive");
-        const size_t b = (L * (size_t)ctx->rank) / (size_t)ctx->nranks;
-        const size_t e = (L * (size_t)(ctx->rank + 1)) / (size_t)ctx->nranks;
-        n = n / L * (e - b);
+        size_t b = 0, c = 0;
+        shard_bounds(L, (size_t)ctx->nranks, (size_t)ctx->rank, &b, &c);
+        n = n / L * c;
       }
       staged = DevBuf(n, ctx->stream);
       ck(cudaMemcpyAsync(staged.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream),

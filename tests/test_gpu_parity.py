@@ -58,7 +58,9 @@ def compare(gpu, ref, a, *, tol=TOL, check_core=True, check_columns=True, check_
         re_o = re_fn(ref.core, ref.factors)
     out["re"] = (re_g, re_o)
     if check_re:
-        assert abs(re_g - re_o) <= tol * max(re_o, 1e-300), f"RE {re_g!r} vs {re_o!r}"
+        # relative (tol) for every RE >= 1e-3 -- all BASELINE configs except the documented cfg2;
+        # an absolute 1e-13 floor for decompositions exact to rounding (RE ~ 1e-15)
+        assert abs(re_g - re_o) <= tol * max(re_o, 1e-3), f"RE {re_g!r} vs {re_o!r}"
     return out
 
 
