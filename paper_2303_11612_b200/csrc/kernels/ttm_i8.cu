@@ -649,8 +649,11 @@ cudaError_t launch_n(const CUtensorMap& map, const uint8_t* qd, const int* eq, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long ntiles = kInner ? (geo.O + 1) / 2 : (geo.J + kI8Tile - 1) / kI8Tile;
-  const int avail = std::max(1, sms - std::max(0, g_i8_reserved_sms));
+  int reserve = std::max(0, g_i8_reserved_sms);
+  if (const char* env = getenv("LMRA_I8_RESERVE")) reserve = atoi(env);  // diagnostics override
+  const int avail = std::max(1, sms - reserve);
   const int grid = (int)(ntiles < avail ? ntiles : avail);
+  if (getenv("LMRA_I8_DEBUG")) fprintf(stderr, "ttm_i8 grid %d (sms %d, reserve %d, tiles %lld)\n", grid, sms, reserve, ntiles);
   ttm_i8_kernel<N, kInner><<<grid, kI8Threads, smem, st>>>(map, qd, eq, geo, mu, y); note_launch();
   return cudaGetLastError();
 }

@@ -1970,7 +1970,11 @@ int lmra_context_create(int device, void* stream, lmra_context** out) {
 void lmra_context_destroy(lmra_context* ctx) {
   if (!ctx) return;
   {
-    DeviceGuard dg(ctx->device);
+    // never throws (may run during process teardown, when the CUDA driver is shutting down)
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    cudaGetLastError();
     cudaStreamSynchronize(ctx->stream);
     ctx->comm.reset();
     for (cudaStream_t s : ctx->aux) cudaStreamDestroy(s);
@@ -1979,6 +1983,8 @@ void lmra_context_destroy(lmra_context* ctx) {
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->cusolver) lmra_host::cusolver().Destroy(ctx->cusolver);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
+    cudaGetLastError();
   }
   delete ctx;
 }
@@ -2187,8 +2193,11 @@ struct DeviceGroup {
     for (lmra_context* c : ctx) lmra_context_destroy(c);
   }
 };
-std::mutex g_groups_mu;
-std::map<std::vector<int>, std::shared_ptr<DeviceGroup>> g_groups;
+// never destroyed: tearing contexts down in static destructors would race the CUDA runtime's own
+// teardown at process exit
+std::mutex& g_groups_mu = *new std::mutex;
+std::map<std::vector<int>, std::shared_ptr<DeviceGroup>>& g_groups =
+    *new std::map<std::vector<int>, std::shared_ptr<DeviceGroup>>;
 
 std::shared_ptr<DeviceGroup> device_group(const std::vector<int>& devs) {
   std::lock_guard<std::mutex> lk(g_groups_mu);

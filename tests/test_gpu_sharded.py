@@ -10,9 +10,10 @@ all-gather, partial-core all-reduce -- is the same code the NCCL communicator dr
 Checks: (1) all ranks return bitwise-identical factors and core; (2) against the oracle on
 the whole tensor with the parity tolerances of test_gpu_parity (for AMM runs the oracle's
 own draws are passed in, so the comparison isolates the sharded arithmetic); (3) without
-overrides, draws of modes < N-1 are bit-exact with the oracle's (their norms are computed
-locally in the canonical order and all-gathered) and the uniform regime is bit-exact on
-every mode.
+overrides, the draws are bit-exact with the oracle's: modes < N-1 always (their norms are
+computed locally in the canonical order and all-gathered), the sharded mode N-1 whenever the
+slabs are segment-aligned (last extent >= 64 P: each rank's canonical-norm segments are
+all-gathered and added in global order), and every mode in the uniform regime.
 """
 import threading
 
@@ -85,6 +86,11 @@ CASES = [
     ("alg4", (12, 10, 9, 14), (3, 3, 3, 3), 3, "nearly_optimal"),
     ("alg5", (40, 36, 48), (5, 5, 5), 2, "nearly_optimal"),
     ("alg5", (40, 36, 47), (4, 5, 6), 4, "optimal"),
+    # segment-aligned slabs (last extent >= 64 P): the sharded mode's norms are exact too
+    ("alg4", (20, 18, 130), (4, 4, 5), 2, "nearly_optimal"),
+    ("alg4", (12, 10, 300), (3, 3, 5), 4, "optimal"),
+    ("alg4", (8, 6, 5, 200), (3, 3, 3, 4), 3, "nearly_optimal"),
+    ("alg5", (16, 14, 200), (4, 4, 4), 3, "nearly_optimal"),
 ]
 
 
@@ -109,9 +115,10 @@ def test_sharded_own_draws(orc, alg, dims, rank, P, regime):
     """No overrides: the sharded run's own sampling chain against the oracle's draws.
 
     Indices must agree on every mode.  Scales are bit-exact where the norms are exact:
-    T-HOSVD modes < N-1 (local canonical norms, all-gathered) and the first ST-HOSVD mode
-    when it is not the sharded one.  The sharded mode's norms are all-reduced partials and
-    later ST-HOSVD modes see a shrunk tensor with its own rounding: 1e-13 relative."""
+    T-HOSVD modes < N-1 (local canonical norms, all-gathered), the sharded mode N-1 when the
+    slabs are segment-aligned, and the first ST-HOSVD mode.  Unaligned slabs' mode N-1 norms
+    are rank partials added in rank order, and later ST-HOSVD modes see a shrunk tensor with
+    its own rounding: 1e-13 relative."""
     a = _tensor(orc, dims, seed=5)
     ocfg = orc.AlgoConfig(rank=list(rank), oversampling=6, power=1, regime=regime, seed=2,
                           alpha=0.5)
@@ -128,7 +135,8 @@ def test_sharded_own_draws(orc, alg, dims, rank, P, regime):
         gi, gs = own.samples[n]
         oi, os_ = ref.samples[n]
         assert np.array_equal(gi, oi), f"mode {n}: sharded draws differ from the oracle's"
-        exact = n < N - 1 if alg == "alg4" else n == 0
+        aligned = dims[-1] >= 64 * P
+        exact = (n < N - 1 or aligned) if alg == "alg4" else n == 0
         if exact:
             assert np.array_equal(gs, os_), f"mode {n}: scales"
         else:

@@ -123,3 +123,67 @@ def test_shard_plan_world2_gloo():
     for rank, errs, _ in results:
         for k, v in errs.items():
             assert v <= 1e-13, (rank, k, v)
+
+
+def test_shard_plan_is_segment_aligned(lmra):
+    # lmra_shard_range: contiguous covering slabs, balanced in units of 64 rows when L >= 64 P
+    for L, P in [(1000, 8), (1000, 2), (512, 8), (130, 2), (47, 4), (63, 1), (4096, 7)]:
+        spans = [lmra.shard_range(L, P, r) for r in range(P)]
+        assert spans[0][0] == 0 and sum(c for _, c in spans) == L
+        for (s0, c0), (s1, _) in zip(spans, spans[1:]):
+            assert s0 + c0 == s1
+        if L >= 64 * P:
+            assert all(s0 % 64 == 0 for s0, _ in spans)
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= 64
+
+
+def _segments_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as orc
+        from paper_2303_11612_b200 import shard_range
+        dims = [5, 4, 300]
+        x = orc.gen_tucker_noise(dims, [3, 3, 4], 1e-2, 7)
+        slab_n = dims[0] * dims[1]
+        s0, c0 = shard_range(dims[2], world, rank)
+        slab = x[slab_n * s0: slab_n * (s0 + c0)]
+        # this rank's canonical-norm segments of every mode-2 column: 64 rows each (a 64-row
+        # fibre's canonical norm is exactly its segment sum)
+        segs = []
+        for r0 in range(0, c0, 64):
+            n = min(64, c0 - r0)
+            segs.append(orc.column_sqnorms(slab[slab_n * r0: slab_n * (r0 + n)], [dims[0], dims[1], n], 2))
+        mine = np.stack(segs)
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        total = np.zeros(slab_n)
+        for g in got:  # global segment order = rank order, then local order
+            for row in g:
+                total = total + row
+        want = orc.column_sqnorms(x, dims, 2)
+        q.put((rank, bool(np.array_equal(total, want)), (s0, c0)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_canonical_norms_world2_gloo():
+    """The sharded mode's norms (run_sharded_impl, segment-aligned slabs): each rank's
+    segment sums all-gathered and added in global order give the unsharded canonical bits."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_segments_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert sorted(r[2] for r in results) == [(0, 128), (128, 172)]
+    assert all(r[1] for r in results)
