@@ -875,10 +875,12 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
 
   // QR-proxy (alg6/alg7): the projected tensor P and U1 of a mode whose contraction reads P
   std::vector<Engine::QrProxy> qrp(N);
-  // Split orthonormalisation (T-HOSVD on large tensors): each mode publishes its sketch basis
-  // Q_C (I x s) before the s x s Jacobi, the core's long contractions run on Q_C while the
-  // Jacobis finish, and the small rotations U_R'^T are applied to the s_0 x s_1 x ... core at
-  // the end (X x_n Q^T = (X x_n Q_C^T) x_n U_R'^T, modes commute).  LMRA_ORTH_SPLIT=0/1 forces.
+  // Split orthonormalisation (T-HOSVD, opt-in with LMRA_ORTH_SPLIT=1): each mode publishes its
+  // sketch basis Q_C (I x s) before the s x s Jacobi, the core's long contractions run on Q_C
+  // while the Jacobis finish, and the small rotations U_R'^T are applied to the s_0 x s_1 x ...
+  // core at the end (X x_n Q^T = (X x_n Q_C^T) x_n U_R'^T, modes commute).  Parity-tested, but
+  // measured slower on cfg4 (4.66-4.78 vs 4.61 ms): the int8 contraction runs power-capped, and
+  // Jacobis beside it both slow it (1.48 -> 1.72-1.85 ms) and run ~2x slower themselves.
   struct SplitOrth {
     DevBuf qc, urs, work;
     cudaEvent_t basis = nullptr;
@@ -891,7 +893,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
         if (so.basis) cudaEventDestroy(so.basis);
     }
   } split_guard{split};
-  bool split_orth = !sequential && !qr && prod(in.dims) >= (size_t(1) << 25);
+  bool split_orth = false;
   if (const char* e = getenv("LMRA_ORTH_SPLIT")) split_orth = !sequential && !qr && e[0] == '1';
   auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
                          size_t n) -> DevBuf {

@@ -275,6 +275,21 @@ def test_oversized_rank_clamped(gpu_ctx, lmra):
     assert list(d.core.shape) == [6, 5, 4]
 
 
+@pytest.mark.parametrize("alg", ["alg1", "alg4"])
+def test_split_orthonormalisation_path(gpu_ctx, lmra, orc, alg, monkeypatch):
+    # LMRA_ORTH_SPLIT=1: the core contracted with each sketch's basis Q_C, the Jacobi rotations
+    # U_R' applied to the small core at the end (opt-in path, lmra_b200.cpp)
+    monkeypatch.setenv("LMRA_ORTH_SPLIT", "1")
+    dims = [60, 50, 40]
+    x = orc.gen_tucker_noise(dims, [6, 5, 4], 1e-2, 13)
+    kw = dict(rank=[6, 5, 4], seed=3, power=2, regime="nearly_optimal", t_samples=[300, 300, 300])
+    cg, co = _cfgs(lmra, orc, **kw)
+    ref = orc.run(alg, x, dims, co)
+    t = lmra.DenseTensor.from_flat(x, dims)
+    gpu = lmra.run_algorithm(alg, t, cg, omega=ref.omega, samples=ref.samples if alg == "alg4" else None)
+    compare(gpu, ref, x.reshape(dims, order="F"))
+
+
 @pytest.mark.parametrize("alg", ["alg4", "alg5"])
 @pytest.mark.parametrize("regime", ["uniform", "nearly_optimal"])
 def test_power_on_sampled_columns_in_place(gpu_ctx, lmra, orc, alg, regime, monkeypatch):
