@@ -377,7 +377,8 @@ def traffic_from_profiles(config_key: str, kernel_phase: str):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(config_key, {}).get(kernel_phase)
+        v = d.get(config_key, {})
+        return v.get(kernel_phase) if isinstance(v, dict) else None
     except (OSError, ValueError, AttributeError):
         return None
 
