@@ -456,6 +456,25 @@ __device__ void reg_argmax(const double (&y)[kCW][RPL], int m, int mu, double* b
 // round).  Offline simulation on the cfg4 sketches: 7-8 sweeps, as with round-robin.
 // Sketches with s <= 16 / 32 use 16 / 32 slots (15 / 31 rounds a sweep).
 // ---------------------------------------------------------------------------
+// Circle-method move after a round: lane 0 keeps its top (the fixed player), every other top
+// moves one lane right (lane 1 takes lane 0's bottom), every bottom one lane left (lane P-1
+// takes its own top).  Two shuffles per register row.
+__device__ __forceinline__ void circle_shift(double (&T)[8], double (&B)[8], int& cT, int& cB, int l, int P) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double up = __shfl_up_sync(0xffffffffu, l == 0 ? B[i] : T[i], 1);
+    const double dn = __shfl_down_sync(0xffffffffu, B[i], 1);
+    const double t = T[i];
+    if (l != 0) T[i] = up;
+    B[i] = l == P - 1 ? t : dn;
+  }
+  const int up = __shfl_up_sync(0xffffffffu, l == 0 ? cB : cT, 1);
+  const int dn = __shfl_down_sync(0xffffffffu, cB, 1);
+  const int t = cT;
+  if (l != 0) cT = up;
+  cB = l == P - 1 ? t : dn;
+}
+
 __device__ int g_jacobi_sweeps;
 #ifdef LMRA_JACOBI_CLOCKS
 __device__ unsigned long long g_jclk[8];  // microbenchmark only: per-phase cycles, warp 0
@@ -515,8 +534,10 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
   double* part = q.part;  // [3][8 warps][32 lanes]
   double* csn = q.fval;   // [round parity][cos 32 | sin 32]: q.fval and q.rowk (128 doubles)
   int* flags = q.pidx;    // [0, 60) per-sweep "rotated", [63] result
-  // slots: the next power of two >= s (16, 32 or 64); lanes >= nh hold nothing
-  const int nh = s <= 16 ? 8 : (s <= 32 ? 16 : 32);
+  // circle-method round robin: lanes l < P hold the pair (top_l, bottom_l) of 2P >= s column
+  // slots; 2P - 1 rounds visit every pair once (s = 50: 49 rounds, not the 63 of a 64-slot
+  // power-of-two tournament)
+  const int nh = (s + 1) / 2;
   // rows: warps 0 .. gw-1 hold G (8 rows each), warps 8 .. 8+gw-1 the same rows of J (rows
   // >= s of J stay zero for every real column); the other warps sit the Jacobi out
   const int gw = (s + 7) / 8;
@@ -550,9 +571,8 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
 #endif
   if (!active) goto done;
   for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
-    for (int group = nh;; group >>= 1) {
-      const int src = (l & ~(group - 1)) | ((l + 1) & (group - 1));
-      for (int r = 0; r < group; ++r, ++round) {
+    {
+      for (int r = 0; r < 2 * nh - 1; ++r, ++round) {
         double* cs_r = csn + 64 * (round & 1);
 #ifdef LMRA_JACOBI_CLOCKS
         const long long k0 = clock64();
@@ -585,7 +605,12 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
             const double sb = ((pb[0] + pb[1]) + (pb[2] + pb[3])) + ((pb[4] + pb[5]) + (pb[6] + pb[7]));
             const double sc = ((pc[0] + pc[1]) + (pc[2] + pc[3])) + ((pc[4] + pc[5]) + (pc[6] + pc[7]));
             double cs, sn;
-            if (jacobi_angle(sa, sb, sc, tol2, cs, sn)) flags[sweep] = 1;
+            // lanes past the P pairs receive stale columns from the circle move: identity
+            if (l < nh && jacobi_angle(sa, sb, sc, tol2, cs, sn)) flags[sweep] = 1;
+            if (l >= nh) {
+              cs = 1.0;
+              sn = 0.0;
+            }
             cs_r[l] = cs;
             cs_r[32 + l] = sn;
           }
@@ -614,10 +639,7 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
           T[i] = cs * x - sn * y;
           B[i] = sn * x + cs * y;
         }
-        // bottoms move one lane down their group (cyclically)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) B[i] = __shfl_sync(0xffffffffu, B[i], src);
-        cB = __shfl_sync(0xffffffffu, cB, src);
+        circle_shift(T, B, cT, cB, l, nh);
 #ifdef LMRA_JACOBI_CLOCKS
         {  // k0->k1 partials + bar A, k1->k2 angles, k2->k3 bar B, k3->k4 rotate (registers)
           const long long k4 = clock64();
@@ -631,25 +653,6 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
         }
 #endif
       }
-      if (group == 1) break;
-      // split: first-half tops pair with second-half tops, bottoms with bottoms
-      const int h = group >> 1;
-      const bool second = (l & h) != 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double tp = __shfl_xor_sync(0xffffffffu, T[i], h);
-        const double bp = __shfl_xor_sync(0xffffffffu, B[i], h);
-        if (second)
-          T[i] = bp;
-        else
-          B[i] = tp;
-      }
-      const int ctp = __shfl_xor_sync(0xffffffffu, cT, h);
-      const int cbp = __shfl_xor_sync(0xffffffffu, cB, h);
-      if (second)
-        cT = cbp;
-      else
-        cB = ctp;
     }
     // flags[sweep] was written before the sweep's last bar B
     if (!flags[sweep]) {
@@ -678,10 +681,10 @@ done:
       const int r = row0 + i;
       if (isG) {
         if (r < s) {
-          if (cT < s) G[r + (size_t)s * cT] = T[i];
-          if (cB < s) G[r + (size_t)s * cB] = B[i];
+          if (l < nh && cT < s) G[r + (size_t)s * cT] = T[i];
+          if (l < nh && cB < s) G[r + (size_t)s * cB] = B[i];
         }
-      } else if (!sender && cT < 64) {  // (inactive lanes hold no column; linked: J is on CTA 1)
+      } else if (!sender && l < nh && cT < 64) {  // (lanes past the pairs hold stale columns; linked: J is on CTA 1)
         J[r + 64 * cT] = T[i];
         J[r + 64 * cB] = B[i];
       }
@@ -702,7 +705,10 @@ __device__ void jacobi_j_consumer(int s, const double* ring, const int* ctl, uin
                                   uint32_t empty_remote, uint32_t jdst) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int row0 = (w & 7) * 8;
-  const int nh = s <= 16 ? 8 : (s <= 32 ? 16 : 32);
+  // circle-method round robin: lanes l < P hold the pair (top_l, bottom_l) of 2P >= s column
+  // slots; 2P - 1 rounds visit every pair once (s = 50: 49 rounds, not the 63 of a 64-slot
+  // power-of-two tournament)
+  const int nh = (s + 1) / 2;
   const int gw = (s + 7) / 8;
   if (!(w >= 8 && (w & 7) < gw)) return;
   double T[8], B[8];
@@ -715,9 +721,8 @@ __device__ void jacobi_j_consumer(int s, const double* ring, const int* ctl, uin
   }
   int jround = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
-    for (int group = nh;; group >>= 1) {
-      const int src = (l & ~(group - 1)) | ((l + 1) & (group - 1));
-      for (int r = 0; r < group; ++r) {
+    {
+      for (int r = 0; r < 2 * nh - 1; ++r) {
         const int slot = jround % kJRing;
         mbar_wait_cluster(&full[slot], (unsigned)(jround / kJRing) & 1u);
         const double cs = ring[slot * 64 + l], sn = ring[slot * 64 + 32 + l];
@@ -730,28 +735,8 @@ __device__ void jacobi_j_consumer(int s, const double* ring, const int* ctl, uin
           T[i] = cs * x - sn * y;
           B[i] = sn * x + cs * y;
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) B[i] = __shfl_sync(0xffffffffu, B[i], src);
-        cB = __shfl_sync(0xffffffffu, cB, src);
+        circle_shift(T, B, cT, cB, l, nh);
       }
-      if (group == 1) break;
-      const int h = group >> 1;
-      const bool second = (l & h) != 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double tp = __shfl_xor_sync(0xffffffffu, T[i], h);
-        const double bp = __shfl_xor_sync(0xffffffffu, B[i], h);
-        if (second)
-          T[i] = bp;
-        else
-          B[i] = tp;
-      }
-      const int ctp = __shfl_xor_sync(0xffffffffu, cT, h);
-      const int cbp = __shfl_xor_sync(0xffffffffu, cB, h);
-      if (second)
-        cT = cbp;
-      else
-        cB = ctp;
     }
     const int slot = jround % kJRing;  // sweep end
     mbar_wait_cluster(&full[slot], (unsigned)(jround / kJRing) & 1u);
@@ -761,7 +746,7 @@ __device__ void jacobi_j_consumer(int s, const double* ring, const int* ctl, uin
     ++jround;
     if (c == 2) break;
   }
-  if (cT < 64) {  // (lanes past the slots hold no column)
+  if (l < nh && cT < 64) {  // (lanes past the pairs hold stale columns)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int r = row0 + i;
