@@ -460,6 +460,7 @@ __device__ void reg_argmax(const double (&y)[kCW][RPL], int m, int mu, double* b
 // moves one lane right (lane 1 takes lane 0's bottom), every bottom one lane left (lane P-1
 // takes its own top).  Two shuffles per register row.
 __device__ __forceinline__ void circle_shift(double (&T)[8], double (&B)[8], int& cT, int& cB, int l, int P) {
+  if (P == 1) return;  // one pair: nothing moves
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const double up = __shfl_up_sync(0xffffffffu, l == 0 ? B[i] : T[i], 1);
