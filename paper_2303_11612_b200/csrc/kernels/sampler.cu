@@ -306,9 +306,10 @@ __device__ __forceinline__ void load_items(const double* __restrict__ x, long lo
 
 // ---------------------------------------------------------------- pass A: chunk sums
 __global__ void __launch_bounds__(kThr) chunk_sums_kernel(const double* __restrict__ x, long long n,
-                                                          double* __restrict__ csum) {
+                                                          double* __restrict__ csum, const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  if (skip && *skip) return;
   __shared__ double sm[32];
   double xv[kItems];
   load_items(x, n, (long long)blockIdx.x * kChunk + threadIdx.x * kItems, xv);
@@ -325,9 +326,11 @@ __global__ void __launch_bounds__(kThr) chunk_sums_kernel(const double* __restri
 __global__ void __launch_bounds__(1024) chunk_plan_kernel(const double* __restrict__ csum,
                                                           int nchunks, long long n,
                                                           int* __restrict__ assumed,
-                                                          int* __restrict__ assumed2) {
+                                                          int* __restrict__ assumed2,
+                                                          const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  if (skip && *skip) return;
   __shared__ double smd[32];
   const double delta = 4.0 * ((double)n + 64.0) * 0x1.0p-53 + 1e-15;
   double carry = 0.0;
@@ -387,9 +390,11 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
                                                          const int* __restrict__ assumed,
                                                          const int* __restrict__ assumed2,
                                                          ChunkAgg* __restrict__ agg,
-                                                         ChunkAgg* __restrict__ subagg) {
+                                                         ChunkAgg* __restrict__ subagg,
+                                                         const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  if (skip && *skip) return;
   __shared__ double smd[32];
   __shared__ int smi[32];
   const int k = blockIdx.x;
@@ -842,9 +847,11 @@ __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restr
                                                            ChunkStart* __restrict__ substarts,
                                                            double* __restrict__ out,
                                                            double* __restrict__ total,
-                                                           int* __restrict__ status, int bad_flag) {
+                                                           int* __restrict__ status, int bad_flag,
+                                                           const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  if (skip && *skip) return;
   extern __shared__ __align__(16) double xs_dyn[];  // kChunk: a split chunk's elements
   __shared__ ChunkAgg tile[kTile];
   __shared__ Tx stx[kTileWarps];
@@ -971,9 +978,11 @@ __device__ __forceinline__ void items_write(const double (&xv)[kItems], int ue, 
 __global__ void __launch_bounds__(kThr) chunk_write_kernel(const double* __restrict__ x, long long n,
                                                            const ChunkStart* __restrict__ starts,
                                                            const ChunkStart* __restrict__ substarts,
-                                                           double* __restrict__ out) {
+                                                           double* __restrict__ out,
+                                                           const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  if (skip && *skip) return;
   __shared__ double smd[32];
   __shared__ int smi[32];
   const int k = blockIdx.x;
@@ -1017,9 +1026,11 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 
 __global__ void __launch_bounds__(kThr) neumaier_terms_kernel(const double* __restrict__ x,
                                                               const double* __restrict__ S, long long n,
-                                                              double* __restrict__ part) {
+                                                              double* __restrict__ part,
+                                                              const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
+  if (skip && *skip) return;
   __shared__ double hi_s[kThr], lo_s[kThr], ab_s[kThr];
   const long long base = (long long)blockIdx.x * kChunk + threadIdx.x * kItems;
   double hi = 0.0, lo = 0.0, ab = 0.0;
@@ -1131,6 +1142,177 @@ __global__ void __launch_bounds__(kRedThr) neumaier_final_kernel(
   }
 }
 
+// ---------------------------------------------------------------- Neumaier without the scan
+// Double-double accumulation with renormalisation (|lo| <= ulp(hi) / 2 after every step), so
+// each step's error is O(u^2 |hi|): n steps cost at most ~2 n u^2 sum x.
+__device__ __forceinline__ void dd_add_d(double& hi, double& lo, double x) {
+  double s, e;
+  two_sum(hi, x, s, e);
+  e = __dadd_rn(lo, e);
+  const double h2 = __dadd_rn(s, e);  // fast two-sum (|s| >= |e|)
+  lo = __dsub_rn(e, __dsub_rn(h2, s));
+  hi = h2;
+}
+__device__ __forceinline__ void dd_add_dd(double& hi, double& lo, double bh, double bl) {
+  double s, e;
+  two_sum(hi, bh, s, e);
+  e = __dadd_rn(e, __dadd_rn(lo, bl));
+  const double h2 = __dadd_rn(s, e);
+  lo = __dsub_rn(e, __dsub_rn(h2, s));
+  hi = h2;
+}
+// fixed-tree block reduction of (hi, lo) pairs; thread 0 gets the result
+template <int NT>
+__device__ void block_dd_reduce(double& hi, double& lo, double* hs, double* ls) {
+  hs[threadIdx.x] = hi;
+  ls[threadIdx.x] = lo;
+  __syncthreads();
+  for (int w = NT / 2; w >= 1; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      double h = hs[threadIdx.x], l = ls[threadIdx.x];
+      dd_add_dd(h, l, hs[threadIdx.x + w], ls[threadIdx.x + w]);
+      hs[threadIdx.x] = h;
+      ls[threadIdx.x] = l;
+    }
+    __syncthreads();
+  }
+  hi = hs[0];
+  lo = ls[0];
+}
+
+// x1 = w / total (+ beta mix) -- tucker.cpp:119-128, as normalize_mix_kernel -- fused with the
+// chunk's double-double sum of x1 (for the Neumaier certificate) and the weight check of
+// normalized() (sketching.cpp:42-44).  One CTA per 4096-element chunk.
+__global__ void __launch_bounds__(kThr) normalize_dd_kernel(const double* __restrict__ w, long long n,
+                                                            const double* __restrict__ total, int regime,
+                                                            double beta, double* __restrict__ x1,
+                                                            int* __restrict__ uni, double* __restrict__ part,
+                                                            int* __restrict__ status) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ double hs[kThr], ls[kThr];
+  const double tot = *total;
+  const bool uniform = !(tot > 0.0);
+  if (!uniform && regime == 1 && !(beta > 0.0 && beta <= 1.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, kBadBeta);
+  }
+  const double cmix = __ddiv_rn(__dsub_rn(1.0, beta), (double)n);
+  const double vu = __ddiv_rn(1.0, (double)n);
+  const long long base = (long long)blockIdx.x * kChunk + threadIdx.x * kItems;
+  double xv[kItems];
+  load_items(w, n, base, xv);
+  double hi = 0.0, lo = 0.0;
+  int bad = 0;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j) {
+    if (base + j >= n) break;
+    double v = vu;
+    if (!uniform) {
+      v = __ddiv_rn(xv[j], tot);
+      if (regime == 1) v = __dadd_rn(__dmul_rn(beta, v), cmix);
+    }
+    x1[base + j] = v;
+    if (!(v >= 0.0)) bad = 1;
+    else dd_add_d(hi, lo, v);
+  }
+  bad = __syncthreads_or(bad);
+  block_dd_reduce<kThr>(hi, lo, hs, ls);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = hi;
+    part[2 * blockIdx.x + 1] = lo;
+    if (bad) atomicOr(status, kBadWeight);
+    if (blockIdx.x == 0) *uni = uniform ? 1 : 0;
+  }
+}
+
+// stable_sum (sketching.cpp:13-24) certified from the exact total, without the naive prefix:
+// the reference returns fl(S + c) with S the naive sum and c the naive sum of the exact
+// two-sum errors e_i; S + sum e_i = T = sum x exactly, |e_i| <= u S_i <= u n T (x >= 0), and
+// c's own drift is <= (n - 1) u sum|e_i|, so S + c lies within B = n^2 u^2 T (1 + 3 n u) of T.
+// With T known to O(n u^2 T) in double-double, fl(S + c) is the rounding of every value in
+// [T - E, T + E] when that interval holds no rounding boundary (all but ~1e-4 of cases).
+// Certified: s -> *s_out and *skip = 1 (the scan-based path below is skipped); otherwise
+// *skip = 0 and the exact scan + neumaier_terms + neumaier_final run.  Uniform (uni): s is
+// never used (p = 1/n), *skip = 1.
+__global__ void __launch_bounds__(kRedThr) neumaier_cert_kernel(const double* __restrict__ part, int nchunks,
+                                                                long long n, const int* __restrict__ uni,
+                                                                double* __restrict__ s_out,
+                                                                int* __restrict__ skip, int force_fallback) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ double hs[kRedThr], ls[kRedThr];
+  if (*uni) {
+    if (threadIdx.x == 0) *skip = 1;
+    return;
+  }
+  double hi = 0.0, lo = 0.0;
+  for (int k = threadIdx.x; k < nchunks; k += kRedThr) dd_add_dd(hi, lo, part[2 * k], part[2 * k + 1]);
+  block_dd_reduce<kRedThr>(hi, lo, hs, ls);
+  if (threadIdx.x != 0) return;
+  const double nn = (double)n;
+  const double u = 0x1.0p-53;
+  // B (c drift, with slack) + the double-double error (<= 2 u^2 per step, n + 2 nchunks + 512 steps)
+  const double rel = __dmul_ru(__dmul_ru(nn, nn), u * u) * 1.0625 + (nn + 2.0 * nchunks + 1024.0) * 4.0 * u * u;
+  const double E = __dadd_ru(__dmul_ru(rel, fabs(hi)), 0x1.0p-1074);
+  const double r_lo = __dadd_rn(hi, __dsub_rd(lo, E));
+  const double r_hi = __dadd_rn(hi, __dadd_ru(lo, E));
+  if (r_lo == r_hi && isfinite(r_lo) && !force_fallback) {
+    *s_out = r_lo;
+    *skip = 1;
+  } else {
+    *skip = 0;
+  }
+}
+
+// p = x / s (sketching.cpp:46) fused with the ctor check's double-double partial sum, the
+// last positive index (sketching.cpp:109-111) and the approximate chunk sums that plan the
+// cumulative scan (pass A of exact_scan).  One CTA per chunk.
+__global__ void __launch_bounds__(kThr) divide_check_kernel(double* __restrict__ x, long long n,
+                                                            const double* __restrict__ s,
+                                                            const int* __restrict__ uni,
+                                                            int* __restrict__ status, double* __restrict__ cpart,
+                                                            long long* __restrict__ lastpos,
+                                                            double* __restrict__ csum) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ double hs[kThr], ls[kThr];
+  __shared__ long long sml[32];
+  __shared__ double smd[32];
+  const double sv = *s;
+  bool divide = !*uni;
+  if (divide && !(sv > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, kZeroNormalize);
+    divide = false;
+  }
+  const long long base = (long long)blockIdx.x * kChunk + threadIdx.x * kItems;
+  double xv[kItems];
+  load_items(x, n, base, xv);
+  double hi = 0.0, lo = 0.0, v = 0.0;
+  long long last = -1;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j) {
+    if (base + j >= n) break;
+    double pv = xv[j];
+    if (divide) {
+      pv = __ddiv_rn(pv, sv);
+      x[base + j] = pv;
+    }
+    dd_add_d(hi, lo, pv);
+    v += pv;
+    if (pv != 0.0) last = base + j;
+  }
+  double tot;
+  block_incl<kThr>(v, smd, tot);
+  last = -block_min_ll<kThr>(-last, sml);
+  block_dd_reduce<kThr>(hi, lo, hs, ls);
+  if (threadIdx.x == 0) {
+    cpart[2 * blockIdx.x] = hi;
+    cpart[2 * blockIdx.x + 1] = lo;
+    lastpos[blockIdx.x] = last;
+    csum[blockIdx.x] = tot;
+  }
+}
+
 // ---------------------------------------------------------------- elementwise steps
 // mode 0: total -> x1 = w / total (or uniform when total <= 0: sets *uni = 1)
 // tucker.cpp:119-128; the mix beta*x + (1-beta)/n is two roundings (no contraction)
@@ -1157,22 +1339,6 @@ __global__ void normalize_mix_kernel(const double* __restrict__ w, long long n,
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *uni = uniform ? 1 : 0;
-}
-
-// p = x / s (sketching.cpp:46); uniform path keeps x (= 1/n); flags s <= 0
-__global__ void divide_kernel(double* __restrict__ x, long long n, const double* __restrict__ s,
-                              const int* __restrict__ uni, int* __restrict__ status) {
-  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
-  pdl_trigger();
-  if (*uni) return;
-  const double sv = *s;
-  if (!(sv > 0.0)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, kZeroNormalize);
-    return;
-  }
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    x[i] = __ddiv_rn(x[i], sv);
 }
 
 __global__ void fill_kernel(double* __restrict__ x, long long n, double v) {
@@ -1453,20 +1619,22 @@ struct ScanBufs {
 };
 
 static cudaError_t exact_scan(const double* x, long long n, double* out, double* total,
-                              int* status, int bad_flag, const ScanBufs& b, cudaStream_t st) {
+                              int* status, int bad_flag, const ScanBufs& b, cudaStream_t st,
+                              const int* skip = nullptr, bool csum_ready = false) {
   const int nc = nchunks_of(n);
   cudaError_t e;
-  if ((e = launch_pdl(chunk_sums_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.csum)) != cudaSuccess) return e;
-  if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2)) != cudaSuccess) return e;
-  if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg)) != cudaSuccess) return e;
+  if (!csum_ready)
+    if ((e = launch_pdl(chunk_sums_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.csum, skip)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2, skip)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg, skip)) != cudaSuccess) return e;
   static unsigned long long walk_attr = 0;
   if ((e = ensure_smem_attr(reinterpret_cast<const void*>(chunk_walk_kernel), kChunk * sizeof(double), walk_attr)) !=
       cudaSuccess)
     return e;
   if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), kChunk * sizeof(double), st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
-                                         total, status, bad_flag)) != cudaSuccess) return e;
+                                         total, status, bad_flag, skip)) != cudaSuccess) return e;
   if (out) {
-    if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, out)) != cudaSuccess) return e;
+    if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, out, skip)) != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -1488,6 +1656,7 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   double* scal = csum + 17 * nc;  // [0] total [1] s [2] acc ; ints after
   int* uni = reinterpret_cast<int*>(scal + 8);
   long long* last = reinterpret_cast<long long*>(scal + 10);
+  int* skip = reinterpret_cast<int*>(scal + 12);  // 1: the Neumaier sum was certified without the scan
   double* ext = scal + 64;  // split-chunk buffers
   int* assumed2 = reinterpret_cast<int*>(ext);
   ChunkAgg* subagg = reinterpret_cast<ChunkAgg*>(ext + nc);
@@ -1513,16 +1682,35 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   } else {
     // total = naive sum of w; x1 = w / total (+ beta mix); s = Neumaier(x1); p = x1 / s
     if ((e = exact_scan(w, n, nullptr, scal + 0, status, kBadWeight, b, st)) != cudaSuccess) return e;
-    if ((e = launch_pdl(normalize_mix_kernel, dim3(eg), dim3(256), 0, st, w, n, scal + 0, regime, beta, p, uni, status)) != cudaSuccess) return e;
-    if ((e = exact_scan(p, n, S, scal + 1, status, kBadWeight, b, st)) != cudaSuccess) return e;
-    if ((e = launch_pdl(neumaier_terms_kernel, dim3(nc), dim3(kThr), 0, st, p, S, n, npart)) != cudaSuccess) return e;
-    if ((e = launch_pdl(neumaier_final_kernel, dim3(1), dim3(kRedThr), 0, st, p, n, scal + 1, npart, nc, scal + 1, status, uni)) != cudaSuccess) return e;
-    if ((e = launch_pdl(divide_kernel, dim3(eg), dim3(256), 0, st, p, n, scal + 1, uni, status)) != cudaSuccess) return e;
+    // diagnostics / tests (read per call): LMRA_NEUMAIER_SCAN=1 the prefix-based certificate
+    // only; =2 the certificate from the total is forced to fail (its fallback path runs)
+    const char* nm = getenv("LMRA_NEUMAIER_SCAN");
+    const bool scan_neumaier = nm && nm[0] == '1';
+    const int force_fallback = nm && nm[0] == '2';
+    if (scan_neumaier) {  // the prefix-based certificate only (kept for tests / comparison)
+      if ((e = launch_pdl(normalize_mix_kernel, dim3(eg), dim3(256), 0, st, w, n, scal + 0, regime, beta, p, uni, status)) != cudaSuccess) return e;
+      if ((e = exact_scan(p, n, S, scal + 1, status, kBadWeight, b, st)) != cudaSuccess) return e;
+      if ((e = launch_pdl(neumaier_terms_kernel, dim3(nc), dim3(kThr), 0, st, p, S, n, npart, (const int*)nullptr)) != cudaSuccess) return e;
+      if ((e = launch_pdl(neumaier_final_kernel, dim3(1), dim3(kRedThr), 0, st, p, n, scal + 1, npart, nc, scal + 1, status, uni)) != cudaSuccess) return e;
+    } else {
+      // x1 and its double-double chunk sums in one pass; s certified from the total; the
+      // prefix-based path (exact scan of x1 + two-sum terms) runs only when that fails
+      if ((e = launch_pdl(normalize_dd_kernel, dim3(nc), dim3(kThr), 0, st, w, n, scal + 0, regime, beta, p, uni, npart, status)) != cudaSuccess) return e;
+      if ((e = launch_pdl(neumaier_cert_kernel, dim3(1), dim3(kRedThr), 0, st, npart, nc, n, uni, scal + 1, skip, force_fallback)) != cudaSuccess) return e;
+      if ((e = exact_scan(p, n, S, scal + 1, status, kBadWeight, b, st, skip)) != cudaSuccess) return e;
+      if ((e = launch_pdl(neumaier_terms_kernel, dim3(nc), dim3(kThr), 0, st, p, S, n, npart, (const int*)skip)) != cudaSuccess) return e;
+      if ((e = launch_pdl(neumaier_final_kernel, dim3(1), dim3(kRedThr), 0, st, p, n, scal + 1, npart, nc, scal + 1, status, (const int*)skip)) != cudaSuccess) return e;
+    }
   }
-  if ((e = launch_pdl(check_last_kernel, dim3(nc), dim3(kThr), 0, st, p, n, cpart, lastpos)) != cudaSuccess) return e;
+  if (regime != 2) {
+    // p = x1 / s, the ctor check partials, last, and the cumulative scan's chunk sums: one pass
+    if ((e = launch_pdl(divide_check_kernel, dim3(nc), dim3(kThr), 0, st, p, n, scal + 1, uni, status, cpart, lastpos, csum)) != cudaSuccess) return e;
+  } else {
+    if ((e = launch_pdl(check_last_kernel, dim3(nc), dim3(kThr), 0, st, p, n, cpart, lastpos)) != cudaSuccess) return e;
+  }
   if ((e = launch_pdl(check_final_kernel, dim3(1), dim3(kRedThr), 0, st, cpart, lastpos, nc, last, status)) != cudaSuccess) return e;
   // cum = naive prefix of p; acc = cum[n-1]
-  if ((e = exact_scan(p, n, S, scal + 2, status, kBadWeight, b, st)) != cudaSuccess) return e;
+  if ((e = exact_scan(p, n, S, scal + 2, status, kBadWeight, b, st, nullptr, regime != 2)) != cudaSuccess) return e;
   const long long threads = (L + kDrawsPerThread - 1) / kDrawsPerThread;
   if ((e = launch_pdl(draw_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, st, S, p, n, scal + 2, last, L, seed,
                                                                   stream, idx, scales, status)) != cudaSuccess) return e;

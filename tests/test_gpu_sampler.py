@@ -49,6 +49,27 @@ def test_sampler_bit_exact(gpu_ctx, orc, name, regime):
     assert np.array_equal(sc.cpu().numpy(), sc_ref)
 
 
+@pytest.mark.parametrize("name", ["gauss_sq_1e5", "uniform01_333k", "constant_third_50k", "with_zeros_40k",
+                                  "wide_range_60k", "tiny_values_30k", "small_7", "half_ulp_ties_10k"])
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_sampler_neumaier_paths(gpu_ctx, orc, name, mode, monkeypatch):
+    # stable_sum is normally certified from the double-double total (no prefix scan); mode 1
+    # runs the prefix-based certificate instead, mode 2 forces the total-based certificate to
+    # fail so its fallback chain (exact scan of x1, two-sum terms, final rounding) runs
+    import torch
+    from paper_2303_11612_b200 import device
+    monkeypatch.setenv("LMRA_NEUMAIER_SCAN", mode)
+    w = np.ascontiguousarray(CASES[name], dtype=np.float64)
+    L = 4099 if w.size > 10 else 17
+    for regime in ("optimal", "nearly_optimal"):
+        p_ref = orc.probabilities(w, regime, 0.5)
+        idx_ref, sc_ref = orc.randsample(L, p_ref, 7, 13)
+        idx, sc, p = device.sample_columns(torch.from_numpy(w).cuda(), regime, 0.5, L, 7, 13, ctx=gpu_ctx)
+        assert np.array_equal(p.cpu().numpy(), p_ref)
+        assert np.array_equal(idx.cpu().numpy(), idx_ref)
+        assert np.array_equal(sc.cpu().numpy(), sc_ref)
+
+
 def test_sampler_error_surface(gpu_ctx, lmra):
     import torch
     from paper_2303_11612_b200 import device
