@@ -43,9 +43,9 @@ constexpr int kThr = 256;                 // grid passes: 16 items per thread
 constexpr int kItems = kChunk / kThr;
 constexpr int kCThr = 1024;               // pass C (single CTA): 4 items per thread
 constexpr int kCItems = kChunk / kCThr;
-constexpr int kSub = 256;                 // sub-chunk of a split chunk
-constexpr int kNSub = kChunk / kSub;      // 16 sub-chunks
-constexpr int kSubThr = kSub / kItems;    // 16 threads (a half-warp) per sub-chunk in passes B/D
+constexpr int kSub = 64;                  // sub-chunk of a split chunk (the stepped unit)
+constexpr int kNSub = kChunk / kSub;      // 64 sub-chunks (two per lane of the walking warp)
+constexpr int kSubThr = kSub / kItems;    // 4 threads per sub-chunk in passes B/D
 constexpr double kTwo53 = 9007199254740992.0;
 
 enum SamplerStatus {
@@ -218,37 +218,38 @@ struct ChunkStart {  // exact state at a certified chunk's start (pass C -> pass
   int pad;
 };
 
-// ---------------------------------------------------------------- half-warp segments
-// A split chunk's sub-chunk is 16 consecutive threads (16 items each) in passes B and D:
-// scans and reductions stay inside the 16-lane segment.
+// ---------------------------------------------------------------- sub-chunk segments
+// A split chunk's sub-chunk is kSubThr consecutive threads (16 items each) in passes B and D:
+// scans and reductions stay inside the kSubThr-lane segment.
 __device__ __forceinline__ unsigned seg_mask() {
-  return 0xffffu << (threadIdx.x & 16);
+  static_assert(kSubThr >= 2 && kSubThr <= 16 && (kSubThr & (kSubThr - 1)) == 0, "segment width");
+  return ((1u << kSubThr) - 1u) << ((threadIdx.x & 31) & ~(kSubThr - 1));
 }
 __device__ __forceinline__ int seg_excl_map(int m, unsigned mask, int& total) {
-  const int sl = threadIdx.x & 15;
+  const int sl = threadIdx.x & (kSubThr - 1);
   int inc = m;
 #pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const int t = __shfl_up_sync(mask, inc, o, 16);
+  for (int o = 1; o < kSubThr; o <<= 1) {
+    const int t = __shfl_up_sync(mask, inc, o, kSubThr);
     if (sl >= o) inc = map_compose(t, inc);
   }
-  total = __shfl_sync(mask, inc, 15, 16);
-  int prev = __shfl_up_sync(mask, inc, 1, 16);
+  total = __shfl_sync(mask, inc, kSubThr - 1, kSubThr);
+  int prev = __shfl_up_sync(mask, inc, 1, kSubThr);
   return sl == 0 ? 0 : prev;
 }
 __device__ __forceinline__ double seg_incl_sum(double v, unsigned mask, double& total) {
-  const int sl = threadIdx.x & 15;
+  const int sl = threadIdx.x & (kSubThr - 1);
 #pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const double t = __shfl_up_sync(mask, v, o, 16);
+  for (int o = 1; o < kSubThr; o <<= 1) {
+    const double t = __shfl_up_sync(mask, v, o, kSubThr);
     if (sl >= o) v += t;
   }
-  total = __shfl_sync(mask, v, 15, 16);
+  total = __shfl_sync(mask, v, kSubThr - 1, kSubThr);
   return v;
 }
 __device__ __forceinline__ double seg_max(double v, unsigned mask) {
 #pragma unroll
-  for (int o = 8; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(mask, v, o, 16));
+  for (int o = kSubThr / 2; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(mask, v, o, kSubThr));
   return v;
 }
 
@@ -372,7 +373,7 @@ __device__ void sub_aggregate(const double (&xv)[kItems], int ue, ChunkAgg* __re
   const double ex1 = seg_incl_sum(run1, mask, tot1) - run1;
   const double Z0 = seg_max(zl0 + ex0, mask) + 2.0;  // margin for the rounded additions
   const double Z1 = seg_max(zl1 + ex1, mask) + 2.0;
-  if ((threadIdx.x & 15) == 0) {
+  if ((threadIdx.x & (kSubThr - 1)) == 0) {
     ChunkAgg a;
     a.R0 = fmin(tot0, 2.0 * kTwo53);
     a.R1 = fmin(tot1, 2.0 * kTwo53);
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
     __shared__ double subsum[kNSub];
     double tot;
     seg_incl_sum(v, seg_mask(), tot);
-    if ((threadIdx.x & 15) == 0) subsum[g] = tot;
+    if ((threadIdx.x & (kSubThr - 1)) == 0) subsum[g] = tot;
     __syncthreads();
     double pre = 0.0;
     for (int h = 0; h < g; ++h) pre += subsum[h];
@@ -427,12 +428,12 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
     if (g > 0 && lo >= 0x1.0p-1022 && ilogb(lo) == ilogb(hi)) ug = ilogb(lo) - 52;
     if (ug != kNoBinade) {
       sub_aggregate(xv, ug, subagg + g);
-    } else if ((threadIdx.x & 15) == 0) {
+    } else if ((threadIdx.x & (kSubThr - 1)) == 0) {
       ChunkAgg a{};
       a.ulp_exp = kNoBinade;
       subagg[g] = a;
     }
-    if ((threadIdx.x & 15) == 0) {
+    if ((threadIdx.x & (kSubThr - 1)) == 0) {
       ChunkAgg a{};
       a.ulp_exp = kNoBinade;
       subagg[kNSub + g] = a;  // no second hypothesis
@@ -761,26 +762,38 @@ __device__ double warp_seq_segment(double* xs, long long c0, int cnt, double S, 
   return S;
 }
 
-// A split chunk, walked by warp 0: the chunk's elements are staged in shared memory by the
-// whole block first (xs, kChunk doubles); runs of certified sub-chunks (under whichever binade
-// hypothesis matches the exact state) are one warp scan of their parity transducers, the
-// sub-chunk holding a crossing is stepped (warp_seq_segment).  Replaces a thread-0 loop over
-// the 16 sub-chunks with block barriers around every stepped sub-chunk.
+// A split chunk, walked by warp 0: runs of certified sub-chunks (under whichever binade
+// hypothesis matches the exact state) are one warp scan of their parity transducers (lane l
+// holds sub-chunks 2l and 2l + 1), and only the 64-element sub-chunk holding a crossing is
+// stepped (loaded into shared memory by the warp, stepped by lane 0: warp_seq_segment).
+// (Round 1 used 256-element sub-chunks and staged the whole chunk first: ~12 k cycles per
+// split chunk, most of them the stepped 256 elements; 64-element sub-chunks cut the stepping
+// 4x and the staging to one 512-byte load.)
+__device__ __forceinline__ Tx tx_of(const ChunkAgg& a) {
+  Tx t;
+  t.d0 = a.R0;
+  t.q0 = parity_of(a.R0);
+  t.d1 = a.R1;
+  t.q1 = 1 ^ parity_of(a.R1);
+  return t;
+}
+
 __device__ double split_walk_warp(const double* __restrict__ x, long long n, int k, double S,
                                   const ChunkAgg* __restrict__ subagg, ChunkStart* __restrict__ substarts,
                                   double* __restrict__ out, double* xs, unsigned long long* st) {
+  static_assert(kNSub == 64, "two sub-chunks per lane");
   __shared__ double s_S;
   const long long base = (long long)k * kChunk;
   __syncthreads();  // xs / s_S may still be read from the previous split chunk
-  for (int i = threadIdx.x; i < kChunk; i += kCThr) xs[i] = base + i < n ? x[base + i] : 0.0;
-  ChunkAgg h0{}, h1{};
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x < kNSub) {
-    h0 = subagg[(size_t)k * 2 * kNSub + lane];
-    h1 = subagg[(size_t)k * 2 * kNSub + kNSub + lane];
-  }
-  __syncthreads();
   if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const ChunkAgg* h = subagg + (size_t)k * 2 * kNSub;
+    ChunkAgg h0[2], h1[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      h0[j] = h[2 * lane + j];
+      h1[j] = h[kNSub + 2 * lane + j];
+    }
     int g = 0;
     while (g < kNSub) {
       if (S > 0.0) {
@@ -789,36 +802,51 @@ __device__ double split_walk_warp(const double* __restrict__ x, long long n, int
         const double M = ldexp(S, -ue);
         const double capU = ldexp(1.0, be - ue);
         const int P0 = parity_of(M);
-        bool valid = lane >= g && lane < kNSub;
-        ChunkAgg a{};
-        if (valid) {
-          if (h0.ulp_exp == ue) a = h0;
-          else if (h1.ulp_exp == ue) a = h1;
-          else valid = false;
+        bool valid[2];
+        ChunkAgg a[2];
+        Tx t[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int idx = 2 * lane + j;
+          valid[j] = idx >= g;
+          a[j] = ChunkAgg{};
+          if (valid[j]) {
+            if (h0[j].ulp_exp == ue) a[j] = h0[j];
+            else if (h1[j].ulp_exp == ue) a[j] = h1[j];
+            else valid[j] = false;
+          }
+          t[j] = valid[j] ? tx_of(a[j]) : tx_identity();
         }
-        Tx t = tx_identity();
-        if (valid) {
-          t.d0 = a.R0;
-          t.q0 = parity_of(a.R0);
-          t.d1 = a.R1;
-          t.q1 = 1 ^ parity_of(a.R1);
+        const Tx ex = warp_excl_tx(tx_compose(t[0], t[1]));
+        // states at the lane's two sub-chunks
+        const double M0 = M + (P0 ? ex.d1 : ex.d0);
+        const int Q0 = P0 ? ex.q1 : ex.q0;
+        const bool c0 = valid[0] && (M0 + (Q0 ? a[0].Z1 : a[0].Z0) < capU - 1.0);
+        const double M1 = M0 + (Q0 ? t[0].d1 : t[0].d0);
+        const int Q1 = Q0 ? t[0].q1 : t[0].q0;
+        const bool c1 = valid[1] && (M1 + (Q1 ? a[1].Z1 : a[1].Z0) < capU - 1.0);
+        int fail = kNSub;
+        if (2 * lane + 1 >= g && !c1) fail = 2 * lane + 1;
+        if (2 * lane >= g && !c0) fail = 2 * lane;
+        const int f = __reduce_min_sync(0xffffffffu, fail);  // first sub-chunk not certified
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int idx = 2 * lane + j;
+          if (idx >= g && idx < f) {
+            ChunkStart cs;
+            cs.M = j ? M1 : M0;
+            cs.parity = j ? Q1 : Q0;
+            cs.ulp_exp = ue;
+            cs.fast = 1;
+            cs.pad = 0;
+            substarts[(size_t)k * kNSub + idx] = cs;
+          }
         }
-        const Tx ex = warp_excl_tx(t);
-        const double Mi = M + (P0 ? ex.d1 : ex.d0);
-        const int Pi = P0 ? ex.q1 : ex.q0;
-        const bool cert = valid && (Mi + (Pi ? a.Z1 : a.Z0) < capU - 1.0);
-        const unsigned nc = __ballot_sync(0xffffffffu, !cert && lane >= g && lane < kNSub);
-        const int f = nc ? __ffs(nc) - 1 : kNSub;
-        if (lane >= g && lane < f) {
-          ChunkStart cs;
-          cs.M = Mi;
-          cs.parity = Pi;
-          cs.ulp_exp = ue;
-          cs.fast = 1;
-          cs.pad = 0;
-          substarts[(size_t)k * kNSub + lane] = cs;
+        if (f > g) {  // state after sub-chunk f - 1
+          const int ol = (f - 1) >> 1, oj = (f - 1) & 1;
+          const double Mend = oj ? M1 + (Q1 ? t[1].d1 : t[1].d0) : M1;
+          S = ldexp(__shfl_sync(0xffffffffu, Mend, ol), ue);
         }
-        if (f > g) S = ldexp(__shfl_sync(0xffffffffu, Mi + (Pi ? a.R1 : a.R0), f - 1), ue);
         g = f;
       }
       if (g < kNSub) {  // the crossing sub-chunk (or the start of the whole sum), element-exact
@@ -829,7 +857,13 @@ __device__ double split_walk_warp(const double* __restrict__ x, long long n, int
           substarts[(size_t)k * kNSub + g] = cs;
           st[3] += 1;
         }
-        if (c0 < n) S = warp_seq_segment(xs + g * kSub, c0, (int)(n - c0 < kSub ? n - c0 : kSub), S, out);
+        if (c0 < n) {
+          const int cnt = (int)(n - c0 < kSub ? n - c0 : kSub);
+          for (int i = lane; i < cnt; i += 32) xs[i] = x[c0 + i];
+          __syncwarp();
+          S = warp_seq_segment(xs, c0, cnt, S, out);
+          __syncwarp();
+        }
         ++g;
       }
     }
@@ -852,7 +886,7 @@ __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restr
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   if (skip && *skip) return;
-  extern __shared__ __align__(16) double xs_dyn[];  // kChunk: a split chunk's elements
+  extern __shared__ __align__(16) double xs_dyn[];  // kSub: a stepped sub-chunk's elements
   __shared__ ChunkAgg tile[kTile];
   __shared__ Tx stx[kTileWarps];
   __shared__ double smd[32];
@@ -1604,8 +1638,8 @@ size_t sampler_workspace_doubles(long long n) {
   const size_t nc = (size_t)nchunks_of(n);
   // p / x1 (n), S (n), csum (nc), assumed (nc ints), agg (nc * 6), starts (nc * 3),
   // neumaier partials (3 nc), check partials (2 nc), lastpos (nc), scalars (16),
-  // assumed2 (nc ints), subagg (nc * 2 * 16 * 6), substarts (nc * 16 * 3)
-  return 2 * (size_t)n + nc * (1 + 1 + 6 + 3 + 3 + 2 + 1) + 64 + nc * (1 + 192 + 48);
+  // assumed2 (nc ints), subagg (nc * 2 * kNSub * 6), substarts (nc * kNSub * 3)
+  return 2 * (size_t)n + nc * (1 + 1 + 6 + 3 + 3 + 2 + 1) + 64 + nc * (1 + 2 * kNSub * 6 + kNSub * 3);
 }
 
 struct ScanBufs {
@@ -1628,10 +1662,10 @@ static cudaError_t exact_scan(const double* x, long long n, double* out, double*
   if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2, skip)) != cudaSuccess) return e;
   if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg, skip)) != cudaSuccess) return e;
   static unsigned long long walk_attr = 0;
-  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(chunk_walk_kernel), kChunk * sizeof(double), walk_attr)) !=
+  if ((e = ensure_smem_attr(reinterpret_cast<const void*>(chunk_walk_kernel), kSub * sizeof(double), walk_attr)) !=
       cudaSuccess)
     return e;
-  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), kChunk * sizeof(double), st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
+  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), kSub * sizeof(double), st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
                                          total, status, bad_flag, skip)) != cudaSuccess) return e;
   if (out) {
     if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, out, skip)) != cudaSuccess) return e;
@@ -1660,7 +1694,7 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   double* ext = scal + 64;  // split-chunk buffers
   int* assumed2 = reinterpret_cast<int*>(ext);
   ChunkAgg* subagg = reinterpret_cast<ChunkAgg*>(ext + nc);
-  ChunkStart* substarts = reinterpret_cast<ChunkStart*>(ext + nc + (size_t)nc * 192);
+  ChunkStart* substarts = reinterpret_cast<ChunkStart*>(ext + nc + (size_t)nc * 2 * kNSub * 6);
   ScanBufs b{csum, assumed, assumed2, agg, starts, subagg, substarts};
   const int eg = 148 * 8;
   cudaError_t e;
