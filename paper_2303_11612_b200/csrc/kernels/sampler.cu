@@ -210,12 +210,29 @@ struct ChunkAgg {
 };
 constexpr int kNoBinade = 1 << 30;
 
+// A split chunk holding one binade crossing, in O(1) for the walk (pass B): the approximate
+// per-element prefix places the crossing element in a short window [w0, w1]; the elements
+// before it form one segment under the lower binade (pre), those after it one under the upper
+// binade (post).  The walk applies pre, steps the window with IEEE adds, applies post.
+constexpr int kWin = 32;  // longest stepped window
+struct CrossAgg {
+  ChunkAgg pre, post;
+  long long w0, w1;  // absolute element indices, window inclusive
+  int ok;            // 0: no usable window (the sub-chunk walk handles the chunk)
+  int pad;
+};
+
 struct ChunkStart {  // exact state at a certified chunk's start (pass C -> pass D)
   double M;          // S / u (integer < 2^53)
   int parity;
   int ulp_exp;
   int fast;          // 1: pass D writes the chunk, 0: pass C already wrote it, 2: split
+                     // (sub-chunk starts), 3: crossing chunk (CrossStart)
   int pad;
+};
+struct CrossStart {  // pass C -> pass D for a crossing chunk written by the O(1) path
+  ChunkStart pre, post;
+  long long w0, w1;
 };
 
 // ---------------------------------------------------------------- sub-chunk segments
@@ -328,6 +345,7 @@ __global__ void __launch_bounds__(1024) chunk_plan_kernel(const double* __restri
                                                           int nchunks, long long n,
                                                           int* __restrict__ assumed,
                                                           int* __restrict__ assumed2,
+                                                          double* __restrict__ approx,
                                                           const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
@@ -355,6 +373,7 @@ __global__ void __launch_bounds__(1024) chunk_plan_kernel(const double* __restri
       }
       assumed[k] = ue;
       assumed2[k] = ue2;
+      approx[k] = acc;
     }
     carry += tot;
   }
@@ -387,11 +406,87 @@ __device__ void sub_aggregate(const double (&xv)[kItems], int ue, ChunkAgg* __re
   }
 }
 
+// whole-block aggregate of this thread's items under binade ue (thread 0's result is valid)
+__device__ ChunkAgg block_aggregate(const double (&xv)[kItems], int ue, double* smd, int* smi) {
+  int excl;
+  const int bmap = BlockScan<kThr>::excl_map(thread_map(xv, ue), excl, smi);
+  double run0, run1, zl0, zl1;
+  two_parity_pass(xv, ue, excl, run0, run1, zl0, zl1);
+  double tot0, tot1;
+  const double ex0 = block_incl<kThr>(run0, smd, tot0) - run0;
+  const double ex1 = block_incl<kThr>(run1, smd, tot1) - run1;
+  const double Z0 = block_max<kThr>(zl0 + ex0, smd) + 2.0;  // margin for the rounded additions
+  const double Z1 = block_max<kThr>(zl1 + ex1, smd) + 2.0;
+  ChunkAgg a;
+  a.R0 = fmin(tot0, 2.0 * kTwo53);
+  a.R1 = fmin(tot1, 2.0 * kTwo53);
+  a.Z0 = Z0;
+  a.Z1 = Z1;
+  a.map = bmap;
+  a.ulp_exp = ue;
+  a.bad = 0;
+  a.split = 0;
+  return a;
+}
+
+// The crossing window of split chunk k (one predicted boundary B = 2^(ue2 + 52)) and its pre /
+// post aggregates.  With S~_i the approximate prefix (plan's chunk start + a block scan) and
+// |S~_i - S_i| <= delta S_i: every i with S~_i (1 + delta) < B has S_i < B, and the first i with
+// S~_i (1 - delta) >= B has S_i >= B, so the exact crossing lies in [w0, w1].
+__device__ void cross_aggregate(const double (&xv)[kItems], long long base, long long n, int k, int ue,
+                                int ue2, double start, CrossAgg* __restrict__ out, double* smd, int* smi,
+                                long long* sml) {
+  double v = 0.0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) v += xv[j] >= 0.0 ? xv[j] : 0.0;
+  double tot;
+  const double incl = block_incl<kThr>(v, smd, tot);
+  double run = start + (incl - v);
+  const double delta = 4.0 * ((double)n + 64.0) * 0x1.0p-53 + 1e-15;
+  const double Bnd = ldexp(1.0, ue2 + 52);
+  const long long kNone = 0x7fffffffffffffffLL;
+  long long fh = kNone, fl = kNone;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    run += xv[j] >= 0.0 ? xv[j] : 0.0;
+    const long long i = base + j;
+    if (i < n) {
+      if (fh == kNone && run * (1.0 + delta) + 1e-300 >= Bnd) fh = i;
+      if (fl == kNone && run * (1.0 - delta) >= Bnd) fl = i;
+    }
+  }
+  fh = block_min_ll<kThr>(fh, sml);
+  fl = block_min_ll<kThr>(fl, sml);
+  const long long c0 = (long long)k * kChunk, ce = min(n, c0 + kChunk);
+  const long long w0 = fh == kNone ? ce : fh;
+  const long long w1 = fl == kNone ? ce - 1 : fl;
+  const bool ok = w0 < ce && w1 >= w0 && w1 - w0 + 1 <= kWin;
+  double xm[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) xm[j] = base + j < w0 ? xv[j] : 0.0;
+  const ChunkAgg pre = block_aggregate(xm, ue, smd, smi);
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) xm[j] = base + j > w1 ? xv[j] : 0.0;
+  const ChunkAgg post = block_aggregate(xm, ue2, smd, smi);
+  if (threadIdx.x == 0) {
+    CrossAgg c;
+    c.pre = pre;
+    c.post = post;
+    c.w0 = w0;
+    c.w1 = w1;
+    c.ok = ok ? 1 : 0;
+    c.pad = 0;
+    *out = c;
+  }
+}
+
 __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restrict__ x, long long n,
                                                          const int* __restrict__ assumed,
                                                          const int* __restrict__ assumed2,
                                                          ChunkAgg* __restrict__ agg,
                                                          ChunkAgg* __restrict__ subagg,
+                                                         const double* __restrict__ approx,
+                                                         CrossAgg* __restrict__ cross,
                                                          const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
@@ -451,6 +546,8 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
   if (assumed2[k] != kNoBinade) {  // split: [k][hypothesis][sub-chunk]
     sub_aggregate(xv, ue, subagg + ((size_t)k * 2 + 0) * kNSub + g);
     sub_aggregate(xv, assumed2[k], subagg + ((size_t)k * 2 + 1) * kNSub + g);
+    __shared__ long long sml[32];
+    cross_aggregate(xv, base, n, k, ue, assumed2[k], approx[k], cross + k, smd, smi, sml);
     bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
       ChunkAgg a{};
@@ -471,26 +568,10 @@ __global__ void __launch_bounds__(kThr) chunk_agg_kernel(const double* __restric
     }
     return;
   }
-  int excl;
-  const int bmap = BlockScan<kThr>::excl_map(thread_map(xv, ue), excl, smi);
-  double run0, run1, zl0, zl1;
-  two_parity_pass(xv, ue, excl, run0, run1, zl0, zl1);
-  double tot0, tot1;
-  const double ex0 = block_incl<kThr>(run0, smd, tot0) - run0;
-  const double ex1 = block_incl<kThr>(run1, smd, tot1) - run1;
-  const double Z0 = block_max<kThr>(zl0 + ex0, smd) + 2.0;  // margin for the rounded additions
-  const double Z1 = block_max<kThr>(zl1 + ex1, smd) + 2.0;
+  ChunkAgg a = block_aggregate(xv, ue, smd, smi);
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
-    ChunkAgg a;
-    a.R0 = fmin(tot0, 2.0 * kTwo53);
-    a.R1 = fmin(tot1, 2.0 * kTwo53);
-    a.Z0 = Z0;
-    a.Z1 = Z1;
-    a.map = bmap;
-    a.ulp_exp = ue;
     a.bad = bad;
-    a.split = 0;
     agg[k] = a;
   }
 }
@@ -873,12 +954,82 @@ __device__ double split_walk_warp(const double* __restrict__ x, long long n, int
   return s_S;
 }
 
+// A crossing chunk in O(1) (warp 0; every lane carries the same state): certify and apply the
+// pre segment, step the window [w0, w1] with IEEE adds (loaded by the warp in one go), check the
+// state reached the upper binade, certify and apply the post segment.  Returns false (state
+// untouched) when any check fails: the caller walks the chunk by sub-chunks instead.
+__device__ bool cross_walk_warp(const double* __restrict__ x, long long n, int k, double& S,
+                                const CrossAgg& c, CrossStart* __restrict__ cstarts,
+                                double* __restrict__ out, double* xs) {
+  const int lane = threadIdx.x & 31;
+  if (!c.ok || !(S > 0.0)) return false;
+  const long long c0 = (long long)k * kChunk;
+  int ue, be;
+  binade_of(S, ue, be);
+  if (ue != c.pre.ulp_exp) return false;
+  double M = ldexp(S, -ue);
+  double capU = ldexp(1.0, be - ue);
+  int P = parity_of(M);
+  CrossStart cs;
+  cs.pre.M = M;
+  cs.pre.parity = P;
+  cs.pre.ulp_exp = ue;
+  cs.pre.fast = 1;
+  cs.pre.pad = 0;
+  cs.w0 = c.w0;
+  cs.w1 = c.w1;
+  if (c.w0 > c0) {
+    if (!(M + (P ? c.pre.Z1 : c.pre.Z0) < capU - 1.0)) return false;
+    M += P ? c.pre.R1 : c.pre.R0;
+  }
+  double Sw = ldexp(M, ue);
+  const int cnt = (int)(c.w1 - c.w0 + 1);
+  if (lane < cnt) xs[lane] = x[c.w0 + lane];
+  __syncwarp();
+  if (lane == 0) {
+    double sv = Sw;
+    for (int j = 0; j < cnt; ++j) {
+      sv = __dadd_rn(sv, xs[j]);
+      xs[j] = sv;
+    }
+  }
+  __syncwarp();
+  Sw = xs[cnt - 1];
+  binade_of(Sw, ue, be);
+  const bool reached = ue == c.post.ulp_exp;
+  double Mp = ldexp(Sw, -ue);
+  capU = ldexp(1.0, be - ue);
+  P = parity_of(Mp);
+  cs.post.M = Mp;
+  cs.post.parity = P;
+  cs.post.ulp_exp = ue;
+  cs.post.fast = 1;
+  cs.post.pad = 0;
+  const long long ce = min(n, c0 + kChunk);
+  bool ok = reached;
+  if (ok && c.w1 + 1 < ce) {
+    ok = Mp + (P ? c.post.Z1 : c.post.Z0) < capU - 1.0;
+    Mp += P ? c.post.R1 : c.post.R0;
+  }
+  if (!ok) {
+    __syncwarp();
+    return false;
+  }
+  if (out && lane < cnt) out[c.w0 + lane] = xs[lane];
+  if (lane == 0) cstarts[k] = cs;
+  S = ldexp(Mp, ue);
+  __syncwarp();
+  return true;
+}
+
 __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restrict__ x, long long n,
                                                            int nchunks,
                                                            const ChunkAgg* __restrict__ agg,
                                                            const ChunkAgg* __restrict__ subagg,
                                                            ChunkStart* __restrict__ starts,
                                                            ChunkStart* __restrict__ substarts,
+                                                           const CrossAgg* __restrict__ cross,
+                                                           CrossStart* __restrict__ cstarts,
                                                            double* __restrict__ out,
                                                            double* __restrict__ total,
                                                            int* __restrict__ status, int bad_flag,
@@ -959,6 +1110,34 @@ __global__ void __launch_bounds__(kCThr) chunk_walk_kernel(const double* __restr
       const long long tq0 = clock64();
       const long long c0 = (long long)k * kChunk, c1 = min(n, c0 + kChunk);
       if (tile[k - t0].split) {  // (chunk 0 is split: its first sub-chunk starts at S = 0)
+        __shared__ int s_done;
+        __shared__ double s_cS;
+        if (threadIdx.x < 32) {  // one crossing: the O(1) path
+          double Sx = S;
+          bool done = false;
+          if (k > 0 && cross) {
+            const CrossAgg c = cross[k];
+            done = cross_walk_warp(x, n, k, Sx, c, cstarts, out, xs_dyn);
+          }
+          if (threadIdx.x == 0) {
+            s_done = done ? 1 : 0;
+            s_cS = Sx;
+          }
+        }
+        __syncthreads();
+        if (s_done) {
+          S = s_cS;
+          if (threadIdx.x == 0) {
+            ChunkStart cs{};
+            cs.fast = 3;
+            starts[k] = cs;
+            st[1] += 1;
+            st[5] += (unsigned long long)(clock64() - tq0);
+          }
+          ++k;
+          __syncthreads();
+          continue;
+        }
         if (threadIdx.x == 0) {
           ChunkStart cs{};
           cs.fast = 2;
@@ -1009,9 +1188,34 @@ __device__ __forceinline__ void items_write(const double (&xv)[kItems], int ue, 
   }
 }
 
+// S_i for the items of this block in [lo, hi) from the exact state cs at lo (the others are
+// masked to 0: identity parity maps, no ulps) -- one crossing chunk's pre or post segment
+__device__ void write_range(const double (&xv_in)[kItems], long long base, long long n, long long lo,
+                            long long hi, const ChunkStart& cs, double* __restrict__ out, double* smd,
+                            int* smi) {
+  double xv[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) xv[j] = (base + j >= lo && base + j < hi) ? xv_in[j] : 0.0;
+  int excl;
+  BlockScan<kThr>::excl_map(thread_map(xv, cs.ulp_exp), excl, smi);
+  const int par = map_apply(excl, cs.parity);
+  const double run = items_run(xv, cs.ulp_exp, par);
+  double tot;
+  const double ex = block_incl<kThr>(run, smd, tot) - run;
+  int p2 = par;
+  double local = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < kItems; ++j) {
+    local += step_r(classify(xv[j], cs.ulp_exp), p2);
+    const long long i = base + j;
+    if (i >= lo && i < hi && i < n) out[i] = ldexp(cs.M + ex + local, cs.ulp_exp);
+  }
+}
+
 __global__ void __launch_bounds__(kThr) chunk_write_kernel(const double* __restrict__ x, long long n,
                                                            const ChunkStart* __restrict__ starts,
                                                            const ChunkStart* __restrict__ substarts,
+                                                           const CrossStart* __restrict__ cstarts,
                                                            double* __restrict__ out,
                                                            const int* __restrict__ skip) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
@@ -1024,6 +1228,14 @@ __global__ void __launch_bounds__(kThr) chunk_write_kernel(const double* __restr
   if (cs0.fast == 0) return;
   const long long base = (long long)k * kChunk + threadIdx.x * kItems;
   double xv[kItems];
+  if (cs0.fast == 3) {  // crossing chunk: pre and post segments (the walk wrote the window)
+    const CrossStart c = cstarts[k];
+    load_items(x, n, base, xv);
+    const long long c0 = (long long)k * kChunk, ce = min(n, c0 + kChunk);
+    if (c.w0 > c0) write_range(xv, base, n, c0, c.w0, c.pre, out, smd, smi);
+    if (c.w1 + 1 < ce) write_range(xv, base, n, c.w1 + 1, ce, c.post, out, smd, smi);
+    return;
+  }
   if (cs0.fast == 2) {  // split chunk: one 16-lane segment per sub-chunk, own start state
     const ChunkStart cs = substarts[(size_t)k * kNSub + threadIdx.x / kSubThr];
     if (!cs.fast) return;  // stepped by the walk (whole segment leaves together)
@@ -1639,7 +1851,9 @@ size_t sampler_workspace_doubles(long long n) {
   // p / x1 (n), S (n), csum (nc), assumed (nc ints), agg (nc * 6), starts (nc * 3),
   // neumaier partials (3 nc), check partials (2 nc), lastpos (nc), scalars (16),
   // assumed2 (nc ints), subagg (nc * 2 * kNSub * 6), substarts (nc * kNSub * 3)
-  return 2 * (size_t)n + nc * (1 + 1 + 6 + 3 + 3 + 2 + 1) + 64 + nc * (1 + 2 * kNSub * 6 + kNSub * 3);
+  // + approx (nc), cross aggregates and starts (nc each)
+  return 2 * (size_t)n + nc * (1 + 1 + 6 + 3 + 3 + 2 + 1) + 64 + nc * (1 + 2 * kNSub * 6 + kNSub * 3) +
+         nc * (1 + (sizeof(CrossAgg) + 7) / 8 + (sizeof(CrossStart) + 7) / 8);
 }
 
 struct ScanBufs {
@@ -1650,6 +1864,9 @@ struct ScanBufs {
   ChunkStart* starts;
   ChunkAgg* subagg;
   ChunkStart* substarts;
+  double* approx;
+  CrossAgg* cross;
+  CrossStart* cstarts;
 };
 
 static cudaError_t exact_scan(const double* x, long long n, double* out, double* total,
@@ -1659,16 +1876,19 @@ static cudaError_t exact_scan(const double* x, long long n, double* out, double*
   cudaError_t e;
   if (!csum_ready)
     if ((e = launch_pdl(chunk_sums_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.csum, skip)) != cudaSuccess) return e;
-  if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2, skip)) != cudaSuccess) return e;
-  if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg, skip)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_plan_kernel, dim3(1), dim3(1024), 0, st, b.csum, nc, n, b.assumed, b.assumed2, b.approx, skip)) != cudaSuccess) return e;
+  if ((e = launch_pdl(chunk_agg_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.assumed, b.assumed2, b.agg, b.subagg, (const double*)b.approx, b.cross, skip)) != cudaSuccess) return e;
+  // LMRA_SAMPLER_CROSS=0 (tests): crossing chunks always take the sub-chunk walk
+  const char* cx = getenv("LMRA_SAMPLER_CROSS");
+  const bool cross_on = !(cx && cx[0] == '0');
   static unsigned long long walk_attr = 0;
   if ((e = ensure_smem_attr(reinterpret_cast<const void*>(chunk_walk_kernel), kSub * sizeof(double), walk_attr)) !=
       cudaSuccess)
     return e;
-  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), kSub * sizeof(double), st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, out,
+  if ((e = launch_pdl(chunk_walk_kernel, dim3(1), dim3(kCThr), kSub * sizeof(double), st, x, n, nc, b.agg, b.subagg, b.starts, b.substarts, cross_on ? (const CrossAgg*)b.cross : nullptr, b.cstarts, out,
                                          total, status, bad_flag, skip)) != cudaSuccess) return e;
   if (out) {
-    if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, out, skip)) != cudaSuccess) return e;
+    if ((e = launch_pdl(chunk_write_kernel, dim3(nc), dim3(kThr), 0, st, x, n, b.starts, b.substarts, (const CrossStart*)b.cstarts, out, skip)) != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -1695,7 +1915,10 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
   int* assumed2 = reinterpret_cast<int*>(ext);
   ChunkAgg* subagg = reinterpret_cast<ChunkAgg*>(ext + nc);
   ChunkStart* substarts = reinterpret_cast<ChunkStart*>(ext + nc + (size_t)nc * 2 * kNSub * 6);
-  ScanBufs b{csum, assumed, assumed2, agg, starts, subagg, substarts};
+  double* approx = ext + nc + (size_t)nc * (2 * kNSub * 6 + kNSub * 3);
+  CrossAgg* cross = reinterpret_cast<CrossAgg*>(approx + nc);
+  CrossStart* cstarts = reinterpret_cast<CrossStart*>(approx + nc + (size_t)nc * ((sizeof(CrossAgg) + 7) / 8));
+  ScanBufs b{csum, assumed, assumed2, agg, starts, subagg, substarts, approx, cross, cstarts};
   const int eg = 148 * 8;
   cudaError_t e;
   if (regime == 2) {  // uniform(n): p = 1/n each (sketching.cpp:50-53)

@@ -51,14 +51,19 @@ def test_sampler_bit_exact(gpu_ctx, orc, name, regime):
 
 @pytest.mark.parametrize("name", ["gauss_sq_1e5", "uniform01_333k", "constant_third_50k", "with_zeros_40k",
                                   "wide_range_60k", "tiny_values_30k", "small_7", "half_ulp_ties_10k"])
-@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("mode", ["1", "2", "nocross"])
 def test_sampler_neumaier_paths(gpu_ctx, orc, name, mode, monkeypatch):
     # stable_sum is normally certified from the double-double total (no prefix scan); mode 1
     # runs the prefix-based certificate instead, mode 2 forces the total-based certificate to
     # fail so its fallback chain (exact scan of x1, two-sum terms, final rounding) runs
     import torch
     from paper_2303_11612_b200 import device
-    monkeypatch.setenv("LMRA_NEUMAIER_SCAN", mode)
+    # nocross: the binade-crossing chunks of the exact scans take the sub-chunk walk instead of
+    # their O(1) pre / window / post path
+    if mode == "nocross":
+        monkeypatch.setenv("LMRA_SAMPLER_CROSS", "0")
+    else:
+        monkeypatch.setenv("LMRA_NEUMAIER_SCAN", mode)
     w = np.ascontiguousarray(CASES[name], dtype=np.float64)
     L = 4099 if w.size > 10 else 17
     for regime in ("optimal", "nearly_optimal"):
