@@ -37,6 +37,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+L2_FLUSH_BELOW = 256 << 20   # inputs below this may stay L2-resident (126 MB L2): flush per step
+L2_FLUSH_BYTES = 256 << 20
 P64_MEASURED_TFLOPS = 37.0   # DMMA m16n8k4 loop, profiles/fp64_peaks_r01.json (this pool's B200)
 
 
@@ -211,8 +213,8 @@ def workload_config(bc, cost):
             "rank": list(c.rank), "oversampling": c.oversampling, "power": c.power, "regime": c.regime,
             "t_samples": c.t_samples, "alpha": c.alpha, "order": c.order, "seed": c.seed,
             "generator": {"kind": bc.generator, **bc.gen_args},
-            "l2": "input >> 126 MB L2; no flush needed" if cost["tensor_bytes"] > 1e9
-                  else "input may be L2-resident between steps (no flush)",
+            "l2": ("input >> 126 MB L2; no flush needed" if cost["tensor_bytes"] >= L2_FLUSH_BELOW
+                   else "L2 flushed between timed steps (256 MB write outside the per-step CUDA events)"),
             "algorithmic_bytes_per_step": cost["bytes"], "algorithmic_flops_per_step": cost["flops"]}
 
 
@@ -451,12 +453,23 @@ def bench_gpu(args, rank, world, local_rank):
     phases = {}
     launches = 0
     host_split = {"host_rng_ms": 0.0, "host_sampling_ms": 0.0, "total_ms": 0.0, "device_ms": 0.0}
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    # inputs that fit the 126 MB L2 (cfg1) are timed step by step with the L2 flushed in between
+    # (a 256 MB write outside the per-step events); larger inputs stream from HBM anyway
+    flush = None
+    if cost["tensor_bytes"] < L2_FLUSH_BELOW:
+        flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps if flush is not None else 1)]
     with ClockSampler(local_rank) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
+        if flush is None:
+            evs[0][0].record(stream)
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+                evs[i][0].record(stream)
             r = P.run_raw(bc.alg, t, cfg, ctx=ctx, global_dims=dims)
+            if flush is not None:
+                evs[i][1].record(stream)
             for k, (ms, cnt) in r.phases().items():
                 a = phases.get(k, (0.0, 0))
                 phases[k] = (a[0] + ms, a[1] + cnt)
@@ -465,9 +478,10 @@ def bench_gpu(args, rank, world, local_rank):
             for k in host_split:
                 host_split[k] += tm[k]
             r.free()
-        ev1.record(stream)
+        if flush is None:
+            evs[0][1].record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
     barrier()
     if dist is not None:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
