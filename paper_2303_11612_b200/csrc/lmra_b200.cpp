@@ -637,12 +637,49 @@ class Engine {
   }
 
   DevBuf orth(const double* c, size_t I, size_t s, size_t mu, int* status) {
+    if (s > (size_t)lmra_dev::kMaxWidth) return orth_wide(c, I, s, mu);
     DevBuf u(I * mu, st_);
     DevBuf work(lmra_dev::orth_workspace_doubles((long long)I, (int)s), st_);
     launch("orth", [&] {
       return lmra_dev::launch_orth(c, (long long)I, (int)s, (int)mu, u.get(), work.get(), status, st_);
     });
     return u;
+  }
+
+  // Sketches wider than the register-resident orthonormalisation (s > 64: the reference accepts
+  // any s = min(mu + p, I_n), tucker.cpp:34-35): thin SVD of the I x s sketch by cuSOLVER dgesvd
+  // (U of C directly, I >= s) + the sign rule.  Off every BASELINE configuration (s <= 60);
+  // synchronous, so the shared cuSOLVER handle is idle before the next mode uses it.
+  DevBuf orth_wide(const double* c, size_t I, size_t s, size_t mu) {
+    const auto& cs = lmra_host::cusolver();
+    if (!ctx_->cusolver) {
+      cusolver_ok(cs.Create(&ctx_->cusolver), "cusolverDnCreate");
+      if (cs.SetDeterministicMode) cs.SetDeterministicMode(ctx_->cusolver, CUSOLVER_DETERMINISTIC_RESULTS);
+    }
+    cusolver_ok(cs.SetStream(ctx_->cusolver, st_), "cusolverDnSetStream");
+    if (I > (size_t)INT32_MAX) throw std::invalid_argument("sketch too tall for dgesvd");
+    const int iI = (int)I, is = (int)s;
+    DevBuf a(I * s, st_), uf(I * s, st_), sv(s, st_), rw(s, st_), info(1, st_), u(I * mu, st_);
+    ck(cudaMemcpyAsync(a.get(), c, I * s * sizeof(double), cudaMemcpyDeviceToDevice, st_), "copy");
+    ck(cudaMemsetAsync(info.get(), 0, sizeof(double), st_), "memset");
+    int lw = 0;
+    cusolver_ok(cs.Dgesvd_bufferSize(ctx_->cusolver, iI, is, &lw), "dgesvd_bufferSize");
+    DevBuf w((size_t)std::max(lw, 1), st_);
+    int* dinfo = reinterpret_cast<int*>(info.get());
+    cusolver_ok(cs.Dgesvd(ctx_->cusolver, 'S', 'N', iI, is, a.get(), iI, sv.get(), uf.get(), iI, nullptr, 1, w.get(),
+                          lw, rw.get(), dinfo),
+                "dgesvd");
+    ck(cudaMemcpyAsync(u.get(), uf.get(), I * mu * sizeof(double), cudaMemcpyDeviceToDevice, st_), "copy");
+    launch("orth", [&] { return lmra_dev::launch_signfix_columns(u.get(), (long long)I, (int)I, (int)mu, st_); });
+    int hinfo = 0;
+    ck(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st_), "D2H");
+    ck(cudaStreamSynchronize(st_), "sync");
+    if (hinfo > 0) throw std::runtime_error("thin_svd: SVD iteration did not converge");
+    if (hinfo < 0) throw CudaError("cuSOLVER: illegal argument " + std::to_string(-hinfo));
+    return u;
+  }
+  static void cusolver_ok(cusolverStatus_t st, const char* what) {
+    if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string(what) + ": cuSOLVER status " + std::to_string((int)st));
   }
 
   // qr_project_extract (linalg.cpp:89-99) for mode n of the tensor x: Q = thin_qr(C).Q,
@@ -734,9 +771,9 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   if (amm && !sequential) t_flat = amm_sample_counts(in.dims, cfg, false);
   if (amm && sequential && !cfg.t_samples.empty() && cfg.t_samples.size() != N)
     throw std::invalid_argument("sample count override length must equal tensor order");
-  for (size_t n = 0; n < N; ++n)
-    if (r.sketch[n] > (size_t)lmra_dev::kMaxWidth)
-      throw std::invalid_argument("sketch width mu_n + oversampling above 64 is not supported");
+  for (size_t n = 0; n < N; ++n)  // (alg1/2/4/5 take wide sketches through Engine::orth_wide)
+    if (qr && r.sketch[n] > (size_t)lmra_dev::kMaxWidth)
+      throw std::invalid_argument("sketch width mu_n + oversampling above 64 is not supported by the QR-proxy variants");
 
   res->omega.assign(N, {});
   res->om_rows.assign(N, 0);
@@ -1210,9 +1247,6 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   if (amm && !sequential) t_flat = amm_sample_counts(in.dims, cfg, false);
   if (amm && sequential && !cfg.t_samples.empty() && cfg.t_samples.size() != N)
     throw std::invalid_argument("sample count override length must equal tensor order");
-  for (size_t n = 0; n < N; ++n)
-    if (r.sketch[n] > (size_t)lmra_dev::kMaxWidth)
-      throw std::invalid_argument("sketch width mu_n + oversampling above 64 is not supported");
   const size_t L = in.dims[N - 1];
   if (L < (size_t)P) throw std::invalid_argument("last mode extent is smaller than the rank count");
   std::vector<size_t> sh0(P), shc(P);
@@ -2487,8 +2521,6 @@ int lmra_leading_left_singular_vectors(lmra_context* ctx, const double* c, uint6
     if (mu < 1 || mu > std::min(rows, cols))
       throw std::invalid_argument("leading_left_singular_vectors: mu out of range");
     if (rows < cols) throw std::invalid_argument("leading_left_singular_vectors: needs rows >= cols");
-    if (cols > (uint64_t)lmra_dev::kMaxWidth)
-      throw std::invalid_argument("leading_left_singular_vectors: more than 64 columns");
     DeviceGuard dg(ctx->device);
     Engine eng(ctx);
     DevBuf status(1, ctx->stream);

@@ -119,7 +119,7 @@ def test_column_sqnorms_bit_exact(gpu_ctx, orc, dims):
 
 @pytest.mark.parametrize("I,s,mu", [(5, 3, 2), (40, 20, 10), (200, 15, 10), (400, 30, 20),
                                     (100, 20, 15), (512, 50, 40), (1000, 60, 50), (3000, 64, 64),
-                                    (3, 3, 3), (64, 1, 1), (700, 33, 7)])
+                                    (3, 3, 3), (64, 1, 1), (700, 33, 7), (300, 80, 70), (1000, 128, 100)])
 def test_orth_matches_oracle_svd(gpu_ctx, orc, I, s, mu):
     from paper_2303_11612_b200 import device
     c = np.asfortranarray(np.random.default_rng(I + s).standard_normal((I, s)))
@@ -181,7 +181,25 @@ def test_small_random_tensor(gpu_ctx, lmra, orc, alg, regime):
     compare(gpu, ref, a)
 
 
-def check_own_draws(alg, own, ref, regime, order=None):
+@pytest.mark.parametrize("alg", ALGS)
+def test_wide_sketch_matches_oracle(gpu_ctx, lmra, orc, alg):
+    # sketch width mu + p above 64 (tucker.cpp:34-35 accepts any min(mu + p, I_n)): the
+    # orthonormalisation goes through the wide-sketch path; everything else is unchanged
+    dims = [90, 84, 12]
+    x = np.random.default_rng(61).standard_normal(int(np.prod(dims)))
+    kw = dict(rank=[60, 70, 6], oversampling=10, seed=9, regime="nearly_optimal",
+              t_samples=[400, 400, 400] if alg == "alg4" else None)
+    cg, co = _cfgs(lmra, orc, **kw)
+    ref = orc.run(alg, x, dims, co)
+    t = lmra.DenseTensor.from_flat(x, dims)
+    own = lmra.run_algorithm(alg, t, cg)
+    # (the shrunk tensor's small mode-2 fibres of this random input carry ~1e-12 relative
+    # differences into their norms; the indices are still bit-exact)
+    check_own_draws(alg, own, ref, "nearly_optimal", scale_tol=1e-10)
+    compare(own, ref, x.reshape(dims, order="F"), check_columns=False)
+
+
+def check_own_draws(alg, own, ref, regime, order=None, scale_tol=1e-12):
     """The GPU run's own Omega / sampled columns against the oracle's.
 
     Omega: bit-exact (same seeded host stream).  Samples: bit-exact whenever the
@@ -202,7 +220,7 @@ def check_own_draws(alg, own, ref, regime, order=None):
             assert np.array_equal(own.samples[n][1], ref.samples[n][1]), f"scales mode {n}"
         else:
             d = np.abs(own.samples[n][1] / ref.samples[n][1] - 1).max()
-            assert d <= 1e-12, f"scales mode {n}: {d:.3g}"
+            assert d <= scale_tol, f"scales mode {n}: {d:.3g}"
 
 
 @pytest.mark.parametrize("alg", ALGS)
