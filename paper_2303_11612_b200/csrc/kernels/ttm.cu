@@ -51,7 +51,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const long long I = min(v.I, kbeg + kper);
   const int nk = (int)((I - kbeg + C::KC - 1) / C::KC);
   y += (size_t)blockIdx.y * (size_t)J * mtot;
-  const bool vec16 = RCONTIG ? (I % 2 == 0) : (v.inner % 2 == 0);
+  // 16-byte fibre loads: every column start (stride v.I, not this split's end) and the base
+  // must be 16-byte aligned (a split-K CTA of an odd-I view once took the vector path)
+  const bool vec16 = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (RCONTIG ? (v.I % 2 == 0) : (v.inner % 2 == 0));
 
   // per-thread fixed column(s) for the JCONTIG loader
   long long jbase = 0;
@@ -524,8 +526,9 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
   const long long jt = (J + 127) / 128;
   int ks = 1;
   const int sms = device_sms();
+  const long long mink = getenv("LMRA_TTM_MINK") ? atoll(getenv("LMRA_TTM_MINK")) : 32;
   if (jt * 2 <= sms && v.I >= 256) {
-    ks = (int)std::max<long long>(1, std::min<long long>(sms / jt, v.I / 64));
+    ks = (int)std::max<long long>(1, std::min<long long>(sms / jt, v.I / mink));
   } else if (v.I >= 512 && jt < 8LL * sms) {
     // a few waves of a long-K contraction: fill the last wave (two CTAs per SM) by splitting
     // K, each extra split charged ~3 % for its partials' round trip
@@ -609,7 +612,8 @@ GramPlan plan_gram(ModeView v, int num_sms) {
   long long target = (long long)num_sms * (kGramMT == 1 ? 4 : 3);  // ~ resident CTAs (one wave)
   long long ns = std::max<long long>(1, target / std::max<long long>(1, rtiles));
   // at least 32 columns per split (two K chunks) so each CTA amortises its prologue
-  ns = std::min<long long>(ns, std::max<long long>(1, J / 32));
+  const long long minj = getenv("LMRA_GRAM_MINJ") ? atoll(getenv("LMRA_GRAM_MINJ")) : 16;
+  ns = std::min<long long>(ns, std::max<long long>(1, J / minj));
   ns = std::min<long long>(ns, 1024);
   long long jper = (J + ns - 1) / ns;
   jper = ((jper + 15) / 16) * 16;

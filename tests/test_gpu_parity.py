@@ -145,14 +145,18 @@ def test_orth_rank_deficient_still_orthonormal(gpu_ctx):
 
 
 @pytest.mark.parametrize("strategy", ["A", "B"])
-def test_gram_power_apply_matches_oracle(gpu_ctx, orc, strategy):
+@pytest.mark.parametrize("shape", [(37, 300, 9, 2), (1000, 400, 60, 2), (200, 5000, 15, 1), (3, 960, 3, 1),
+                                   (513, 77, 33, 3), (511, 1000, 7, 1)])
+def test_gram_power_apply_matches_oracle(gpu_ctx, orc, strategy, shape):
+    # split-K TTM / Gram launches on odd and even row counts (16-byte fibre loads need even I)
     from paper_2303_11612_b200 import device
-    rng = np.random.default_rng(3)
-    a = np.asfortranarray(rng.standard_normal((37, 300)))
-    g = np.asfortranarray(rng.standard_normal((37, 9)))
-    want = orc.gram_power_apply(a, g, 2, strategy)
-    got = device.gram_power_apply(_to_dev(a.ravel(order="F")), 37, 300, _to_dev(g.ravel(order="F")),
-                                  9, 2, strategy, ctx=gpu_ctx).cpu().numpy().reshape((37, 9), order="F")
+    I, J, s, q = shape
+    rng = np.random.default_rng(3 + I)
+    a = np.asfortranarray(rng.standard_normal((I, J)))
+    g = np.asfortranarray(rng.standard_normal((I, s)))
+    want = orc.gram_power_apply(a, g, q, strategy)
+    got = device.gram_power_apply(_to_dev(a.ravel(order="F")), I, J, _to_dev(g.ravel(order="F")),
+                                  s, q, strategy, ctx=gpu_ctx).cpu().numpy().reshape((I, s), order="F")
     assert np.abs(got - want).max() / np.abs(want).max() <= 1e-13
 
 
