@@ -808,7 +808,10 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     int ldo, int final_level, int* status, double jacobi_tol, int clustered, int phase,
     double* __restrict__ gbuf, double* __restrict__ ur, int basis_pivot) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
-  pdl_trigger();
+  // no early pdl_trigger(): a dependent launched now would park its CTAs (waiting in
+  // griddepcontrol.wait) on SMs for the whole Jacobi, and a big kernel of another stream (the
+  // core contraction beside a split orthonormalisation) could not use those SMs; the trigger
+  // comes once the Jacobi is done (CTA 1 of a cluster triggers by exiting)
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
   const int n = 64;  // Jacobi column slots (zero columns beyond s)
@@ -864,6 +867,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     }
     __syncthreads();
     if (phase == kOrthBasis) {  // G out, Y = Q [I_s; 0] (logical column order) to out
+      pdl_trigger();
       for (int e = threadIdx.x; e < s * s; e += kQThreads) gbuf[e] = G[e];
       double y[kCW][RPL];
 #pragma unroll
@@ -913,6 +917,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
   } else {
     converged = reg_jacobi(G, s, J, jacobi_tol, q);
   }
+  pdl_trigger();
   // singular values = column norms of G, fixed order
   for (int c = w; c < s; c += kQWarps) {
     double t = 0.0;
@@ -1148,7 +1153,9 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
   // (only for wide sketches: below s = 48 the cluster launch and the DSMEM handoff cost more
   // than the J rotations they move -- measured on cfg1 / cfg2 / cfg3)
   static const bool cluster_ok = !(getenv("LMRA_ORTH_CLUSTER") && getenv("LMRA_ORTH_CLUSTER")[0] == '0');
-  const bool clustered = cluster_ok && s >= 48 && phase != kOrthBasis;
+  // (the split form's Jacobi runs beside the core contraction, off the critical path: one CTA,
+  // so that it never waits for two co-scheduled SMs the contraction has taken)
+  const bool clustered = cluster_ok && s >= 48 && phase == kOrthFull;
   if (clustered) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2);

@@ -930,8 +930,20 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
         if (so.basis) cudaEventDestroy(so.basis);
     }
   } split_guard{split};
-  bool split_orth = false;
+  // default: on for T-HOSVD inputs of >= 2^27 elements (1 GB), whose first core contraction is
+  // long enough to hide the first mode's Jacobi; LMRA_ORTH_SPLIT=0/1 forces it off/on
+  bool split_orth = !sequential && !qr && prod(in.dims) >= (size_t(1) << 27);
   if (const char* e = getenv("LMRA_ORTH_SPLIT")) split_orth = !sequential && !qr && e[0] == '1';
+  // only the mode the core contracts first is split (core_from_factors: ascending factor width,
+  // stable); the later contractions wait for their modes' full factors, whose Jacobis finish
+  // under the first contraction
+  size_t split_mode = 0;
+  if (split_orth) {
+    std::vector<size_t> mus(N);
+    for (size_t n = 0; n < N; ++n) mus[n] = std::min(r.mu[n], std::min(in.dims[n], r.sketch[n]));
+    for (size_t n = 1; n < N; ++n)
+      if (mus[n] < mus[split_mode]) split_mode = n;
+  }
   auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
                          size_t n) -> DevBuf {
     cudaStream_t s_ = e.st_;
@@ -976,7 +988,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
               r.mu[n], mu);
     res->f_rows[n] = I;
     res->f_cols[n] = mu;
-    if (split_orth) {
+    if (split_orth && n == split_mode && dims == in.dims) {
       SplitOrth& so = split[n];
       so.work = DevBuf(lmra_dev::orth_split_workspace_doubles((long long)I, (int)s), s_);
       so.qc = DevBuf(I * s, s_);
@@ -1054,15 +1066,17 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     // the first contraction reads the input, whose mode-0 norms the sampler already has
     const double* w0 = (amm && cfg.regime != kUniform && d_w[0].get()) ? d_w[0].get() : nullptr;
     Engine::I8Chain chain;
-    if (split_orth) {  // SMs for the Jacobis that run beside the first contraction
-      int jac = 0;
-      for (size_t n = 0; n < N; ++n) jac += r.sketch[n] >= 48 ? 2 : 1;
-      lmra_dev::g_i8_reserved_sms = jac;
+    if (split_orth) {  // SMs for the orthonormalisations that run beside the first contraction
+      int jac = 1;  // the split mode's Jacobi (one CTA) + the other modes' (2-CTA clusters if s >= 48)
+      for (size_t n = 0; n < N; ++n)
+        if (n != split_mode) jac += r.sketch[n] >= 48 ? 2 : 1;
+      lmra_dev::g_i8_reserved_sms = jac + 1;
     }
     for (size_t k = 0; k < idx.size(); ++k) {
       const size_t n = idx[k];
       const bool next1 = k + 1 < idx.size() && idx[k + 1] == 1;
-      if (split_orth) {  // the contraction with the basis Q_C, as soon as it exists
+      if (split_orth && k == 0) {  // the contraction with the basis Q_C, as soon as it exists
+        if (n != split_mode) throw std::logic_error("split orthonormalisation: contraction order");
         ck(cudaStreamWaitEvent(st, split[n].basis, 0), "wait");
         const size_t sn = r.sketch[n];
         DevBuf y = eng.ttm_mode0(src, cur, n, split[n].qc.get(), sn, src == in.x ? w0 : nullptr,
@@ -1088,15 +1102,14 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       src = t.get();
     }
     lmra_dev::g_i8_reserved_sms = 0;
-    if (split_orth)  // the rotations U_R'^T on the s_0 x s_1 x ... core, each after its Jacobi
-      for (size_t k = 0; k < idx.size(); ++k) {
-        const size_t n = idx[k];
-        ck(cudaStreamWaitEvent(st, mode_done[n], 0), "wait");
-        DevBuf y = eng.ttm(src, cur, n, split[n].urs.get(), res->f_cols[n], "core_rot");
-        cur[n] = res->f_cols[n];
-        t = std::move(y);
-        src = t.get();
-      }
+    if (split_orth) {  // the rotation U_R'^T of the split mode, after its Jacobi
+      const size_t n = idx[0];
+      ck(cudaStreamWaitEvent(st, mode_done[n], 0), "wait");
+      DevBuf y = eng.ttm(src, cur, n, split[n].urs.get(), res->f_cols[n], "core_rot");
+      cur[n] = res->f_cols[n];
+      t = std::move(y);
+      src = t.get();
+    }
     res->core_dims = cur;
     res->core = t.detach();
   } else {
