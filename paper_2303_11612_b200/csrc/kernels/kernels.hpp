@@ -87,6 +87,14 @@ cudaError_t launch_sampler(const double* w, long long n, int regime, double beta
                            uint64_t seed, uint64_t stream, long long* idx, double* scales,
                            double* p_out, double* work, int* status, cudaStream_t st);
 
+// Shifted CholeskyQR3 basis of C (I x s, s <= 64) in one thread-block cluster (cholqr.cu):
+// Q_C (I x s) orthonormal and R (s x s, upper, column-major) with C = Q_C R; *fail = 1 when a
+// Cholesky pivot breaks down (numerically rank-deficient C): the caller then needs another path.
+bool cholqr_supported(long long I, int s);
+int cholqr_cluster_size(long long I);
+cudaError_t launch_cholqr(const double* c, long long I, int s, double* qc, double* r, int* fail,
+                          cudaStream_t st);
+
 // Top-mu left singular vectors of C (I x s, column-major) with the reference's sign
 // convention (linalg.cpp:13-43,82-87), written to U (I x mu).  Workspace: orth_workspace().
 size_t orth_workspace_doubles(long long I, int s);

@@ -764,8 +764,9 @@ __device__ void jacobi_j_consumer(int s, const double* ring, const int* ctl, uin
 template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_leaf_qr_kernel(
     const double* __restrict__ A, long long m, int s, int lda, int nb, double* __restrict__ V,
-    double* __restrict__ tau, double* __restrict__ S, int lds) {
+    double* __restrict__ tau, double* __restrict__ S, int lds, const int* __restrict__ gate, int run_if) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
   pdl_trigger();
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
@@ -806,8 +807,9 @@ template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
     int ldo, int final_level, int* status, double jacobi_tol, int clustered, int phase,
-    double* __restrict__ gbuf, double* __restrict__ ur, int basis_pivot) {
+    double* __restrict__ gbuf, double* __restrict__ ur, int basis_pivot, const int* __restrict__ gate, int run_if) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
   // no early pdl_trigger(): a dependent launched now would park its CTAs (waiting in
   // griddepcontrol.wait) on SMs for the whole Jacobi, and a big kernel of another stream (the
   // core contraction beside a split orthonormalisation) could not use those SMs; the trigger
@@ -987,8 +989,10 @@ template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
     const double* __restrict__ V, long long m, int s, int ldv, int nb,
     const double* __restrict__ tau, const double* __restrict__ W, int ldw, int mu,
-    double* __restrict__ out, int ldo, double* __restrict__ pbest, int* __restrict__ pidx) {
+    double* __restrict__ out, int ldo, double* __restrict__ pbest, int* __restrict__ pidx,
+    const int* __restrict__ gate, int run_if) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
   pdl_trigger();
   extern __shared__ __align__(16) double sm[];
   const QSmem q = carve_q(sm);
@@ -1031,8 +1035,9 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
 // Sign fix: per column, combine block partials in block order; flip if negative.
 __global__ void orth_signfix_kernel(double* __restrict__ U, long long m, int ldu, int mu, int nb,
                                     const double* __restrict__ pbest,
-                                    const int* __restrict__ pidx) {
+                                    const int* __restrict__ pidx, const int* __restrict__ gate, int run_if) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
   pdl_trigger();
   const int c = blockIdx.x;
   __shared__ int flip;
@@ -1099,12 +1104,31 @@ static std::vector<OrthLevel> plan_levels(long long I, int s, size_t* total) {
   return lv;
 }
 
-size_t orth_workspace_doubles(long long I, int s) {
+// Householder tree workspace (the fallback path's, and the whole of it without CholeskyQR)
+static size_t tree_workspace_doubles(long long I, int s) {
   size_t used = 0;
   std::vector<OrthLevel> lv = plan_levels(I, s, &used);
   for (auto& L : lv) used += (size_t)L.nb * s * s;  // W per level (mu <= s)
   if (!lv.empty()) used += (size_t)lv[0].nb * s * 2;
   return used + 64;
+}
+
+// CholeskyQR basis first (cholqr.cu) for sketches whose Householder tree has four or more
+// leaves (I > 768 rows) and that fit one cluster.  Measured (B200, whole decompositions): cfg4's
+// 1000 x 60 sketches 4.02 -> 3.87 ms; at cfg5's 512 x 50 even; at cfg2's 400 x 30 the tree is
+// cheaper (1.85 vs 2.11 ms) -- the CholeskyQR's three s-step Cholesky chains cost the same at
+// any I, the tree's leaf / stacked-R chains grow with I.  LMRA_ORTH_CHOLQR=0 / 1 forces it off /
+// on (any I > 256 the cluster takes).
+static bool use_cholqr(long long I, int s) {
+  const char* env = getenv("LMRA_ORTH_CHOLQR");
+  if (env && env[0] == '0') return false;
+  const long long min_rows = (env && env[0] == '1') ? kMaxBlockRows + 1 : 3 * kMaxBlockRows + 1;
+  return I >= min_rows && cholqr_supported(I, s);
+}
+
+// [tree | Q_C (I x s) | R (s x s) | Y (s x s) | gate]
+size_t orth_workspace_doubles(long long I, int s) {
+  return tree_workspace_doubles(I, s) + (use_cholqr(I, s) ? (size_t)I * s + 2 * (size_t)s * s + 64 : 0);
 }
 
 // sweeps taken by the most recent converged Jacobi (diagnostics only)
@@ -1119,6 +1143,19 @@ namespace {
 // the attribute is set once per kernel (and device) to the largest size any call can use
 constexpr size_t kOrthSmemMax = 227 * 1024;
 
+// Gate of the launches issued while a GateScope is alive: each kernel returns at once unless
+// *gate == run_if (the Householder fallback behind a CholeskyQR attempt runs only if it failed).
+struct Gate {
+  const int* p = nullptr;
+  int run_if = 0;
+};
+thread_local Gate g_gate;
+struct GateScope {
+  Gate saved;
+  GateScope(const int* p, int run_if) : saved(g_gate) { g_gate = Gate{p, run_if}; }
+  ~GateScope() { g_gate = saved; }
+};
+
 template <int RPL>
 cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, double* tau,
                     double* S, int lds, cudaStream_t st) {
@@ -1128,7 +1165,8 @@ cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, doub
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(orth_leaf_qr_kernel<RPL>), kOrthSmemMax, done);
   if (e != cudaSuccess) return e;
   {
-    const cudaError_t le = launch_pdl(orth_leaf_qr_kernel<RPL>, dim3(nb), dim3(kQThreads), smem, st, A, m, s, (int)m, nb, V, tau, S, lds);
+    const cudaError_t le = launch_pdl(orth_leaf_qr_kernel<RPL>, dim3(nb), dim3(kQThreads), smem, st, A, m, s, (int)m, nb, V, tau, S, lds,
+                                      g_gate.p, g_gate.run_if);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
@@ -1173,11 +1211,13 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
     cfg.numAttrs = 2;
     note_launch();
     const cudaError_t le = cudaLaunchKernelEx(&cfg, orth_core_kernel<RPL>, S, m, s, m, mu, out, ldo, final_level,
-                                              status, tol, 1, phase, gbuf, ur, basis_pivot());
+                                              status, tol, 1, phase, gbuf, ur, basis_pivot(), g_gate.p,
+                                              g_gate.run_if);
     if (le != cudaSuccess) return le;
   } else {
     const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu,
-                                      out, ldo, final_level, status, tol, 0, phase, gbuf, ur, basis_pivot());
+                                      out, ldo, final_level, status, tol, 0, phase, gbuf, ur, basis_pivot(), g_gate.p,
+                                      g_gate.run_if);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
@@ -1194,7 +1234,7 @@ cudaError_t leaf_apply(const double* V, long long m, int s, int nb, const double
   if (e != cudaSuccess) return e;
   {
     const cudaError_t le = launch_pdl(orth_leaf_apply_kernel<RPL>, dim3(nb), dim3(kQThreads), smem, st, V, m, s, (int)m, nb, tau, W, ldw, mu,
-                                                          out, (int)m, pbest, pidx);
+                                                          out, (int)m, pbest, pidx, g_gate.p, g_gate.run_if);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
@@ -1203,6 +1243,14 @@ cudaError_t leaf_apply(const double* V, long long m, int s, int nb, const double
 #define LMRA_RPL_DISPATCH(rpl, call) ((rpl) == 2 ? call<2> : (rpl) == 4 ? call<4> : call<8>)
 
 }  // namespace
+
+__global__ void __launch_bounds__(256) orth_rotate_signfix_kernel(const double* __restrict__ qc, long long I, int s,
+                                                                  const double* __restrict__ ur, int mu,
+                                                                  double* __restrict__ u, double* __restrict__ ur_s,
+                                                                  const int* __restrict__ gate, int run_if);
+static cudaError_t launch_orth_tree(const double* c, long long I, int s, int mu, double* u, double* work,
+                                    int* status, double tol, const std::vector<OrthLevel>& lv, size_t used,
+                                    cudaStream_t st);
 
 cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, double* work,
                         int* status, cudaStream_t st) {
@@ -1218,6 +1266,35 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   if (lv.empty())
     return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st, kOrthFull, nullptr,
                                                nullptr);
+  if (use_cholqr(I, s)) {
+    // C = Q_C R by CholeskyQR (cluster kernel), then the s x s chain on R: pivoted QR + Jacobi
+    // -> Y = left singular vectors of R (s x mu), U = Q_C Y with the sign rule.  If the
+    // CholeskyQR flags a failure, the same launches skip and the Householder tree below runs.
+    double* qcb = work + tree_workspace_doubles(I, s);
+    double* rm = qcb + (size_t)I * s;
+    double* y = rm + (size_t)s * s;
+    int* gate = reinterpret_cast<int*>(y + (size_t)s * s);
+    e = launch_cholqr(c, I, s, qcb, rm, gate, st);
+    if (e != cudaSuccess) return e;
+    {
+      GateScope gs(gate, 0);
+      e = LMRA_RPL_DISPATCH(rpl_for(s), core)(rm, s, s, mu, y, s, 0, status, tol, st, kOrthFull, nullptr, nullptr);
+      if (e != cudaSuccess) return e;
+    }
+    e = launch_pdl(orth_rotate_signfix_kernel, dim3(mu), dim3(256), 0, st, (const double*)qcb, I, s,
+                   (const double*)y, mu, u, (double*)nullptr, (const int*)gate, 0);
+    if (e != cudaSuccess) return e;
+    GateScope gs(gate, 1);
+    return launch_orth_tree(c, I, s, mu, u, work, status, tol, lv, used, st);
+  }
+  return launch_orth_tree(c, I, s, mu, u, work, status, tol, lv, used, st);
+}
+
+// the Householder tree path of launch_orth (leaves, pivoted core, back down, sign fix)
+static cudaError_t launch_orth_tree(const double* c, long long I, int s, int mu, double* u, double* work,
+                                    int* status, double tol, const std::vector<OrthLevel>& lv, size_t used,
+                                    cudaStream_t st) {
+  cudaError_t e;
   std::vector<size_t> wbuf(lv.size());
   for (size_t l = 0; l < lv.size(); ++l) {
     wbuf[l] = used;
@@ -1251,7 +1328,8 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
     if (e != cudaSuccess) return e;
   }
   {
-    const cudaError_t le = launch_pdl(orth_signfix_kernel, dim3(mu), dim3(256), 0, st, u, I, (int)I, mu, lv[0].nb, pbest, pidx);
+    const cudaError_t le = launch_pdl(orth_signfix_kernel, dim3(mu), dim3(256), 0, st, u, I, (int)I, mu, lv[0].nb, pbest, pidx,
+                                      g_gate.p, g_gate.run_if);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
@@ -1269,8 +1347,10 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
 // sign applied to U_R(:, c).
 __global__ void __launch_bounds__(256) orth_rotate_signfix_kernel(const double* __restrict__ qc, long long I, int s,
                                                                   const double* __restrict__ ur, int mu,
-                                                                  double* __restrict__ u, double* __restrict__ ur_s) {
+                                                                  double* __restrict__ u, double* __restrict__ ur_s,
+                                                                  const int* __restrict__ gate, int run_if) {
   pdl_wait();
+  if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
   pdl_trigger();
   const int c = blockIdx.x;
   __shared__ double urc[64];
@@ -1318,7 +1398,8 @@ __global__ void __launch_bounds__(256) orth_rotate_signfix_kernel(const double* 
   }
   __syncthreads();
   const double sg = sgn;
-  for (int k = threadIdx.x; k < s; k += blockDim.x) ur_s[k + (size_t)s * c] = sg * urc[k];
+  if (ur_s)
+    for (int k = threadIdx.x; k < s; k += blockDim.x) ur_s[k + (size_t)s * c] = sg * urc[k];
   if (sg < 0.0)
     for (long long i = threadIdx.x; i < I; i += blockDim.x) u[i + I * c] = -u[i + I * c];
 }
@@ -1337,6 +1418,15 @@ cudaError_t launch_orth_basis(const double* c, long long I, int s, double* qc, d
   if (lv.empty())
     return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, s, qc, (int)I, 0, nullptr, 0.0, st, kOrthBasis, gbuf,
                                                nullptr);
+  // CholeskyQR: Q_C and R (to gbuf; the finish runs pivoted QR + Jacobi on it); the Householder
+  // tree below (G = R^T to gbuf) runs only if it fails
+  int* gate = reinterpret_cast<int*>(gbuf + 2 * (size_t)s * s);
+  const bool cq = use_cholqr(I, s);
+  if (cq) {
+    e = launch_cholqr(c, I, s, qc, gbuf, gate, st);
+    if (e != cudaSuccess) return e;
+  }
+  GateScope gs(cq ? gate : nullptr, 1);
   std::vector<size_t> wbuf(lv.size());
   for (size_t l = 0; l < lv.size(); ++l) {
     wbuf[l] = used;
@@ -1371,11 +1461,21 @@ cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, dou
   if (const char* env = getenv("LMRA_JACOBI_TOL")) tol = atof(env);
   double* gbuf = work + orth_workspace_doubles(I, s);
   double* ur = gbuf + (size_t)s * s;
-  cudaError_t e = LMRA_RPL_DISPATCH(rpl_for(s), core)(nullptr, s, s, mu, nullptr, s, 0, status, tol, st,
-                                                      kOrthJacobi, gbuf, ur);
-  if (e != cudaSuccess) return e;
+  int* gate = reinterpret_cast<int*>(gbuf + 2 * (size_t)s * s);
+  const bool cq = use_cholqr(I, s);
+  cudaError_t e;
+  if (cq) {  // R from the CholeskyQR: pivoted QR + Jacobi -> U_R(:, :mu) = Y (s x mu)
+    GateScope gs(gate, 0);
+    e = LMRA_RPL_DISPATCH(rpl_for(s), core)(gbuf, s, s, mu, ur, s, 0, status, tol, st, kOrthFull, nullptr, nullptr);
+    if (e != cudaSuccess) return e;
+  }
+  {
+    GateScope gs(cq ? gate : nullptr, 1);
+    e = LMRA_RPL_DISPATCH(rpl_for(s), core)(nullptr, s, s, mu, nullptr, s, 0, status, tol, st, kOrthJacobi, gbuf, ur);
+    if (e != cudaSuccess) return e;
+  }
   return launch_pdl(orth_rotate_signfix_kernel, dim3(mu), dim3(256), 0, st, qc, I, s, (const double*)ur, mu, u,
-                    ur_signed);
+                    ur_signed, (const int*)nullptr, 0);
 }
 
 // ---------------------------------------------------------------------------

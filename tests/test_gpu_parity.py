@@ -144,6 +144,55 @@ def test_orth_rank_deficient_still_orthonormal(gpu_ctx):
     assert subspace_sine(u[:, :4], q) <= 1e-10
 
 
+def _graded_sketch(I, s, decades, seed):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((I, s)))
+    v, _ = np.linalg.qr(rng.standard_normal((s, s)))
+    sig = 10.0 ** (-decades * np.arange(s) / max(s - 1, 1))
+    return np.asfortranarray((u * sig) @ v.T), sig
+
+
+@pytest.mark.parametrize("I,s,mu,decades", [(1000, 60, 50, 10), (1000, 60, 50, 15), (800, 50, 40, 14),
+                                            (900, 30, 20, 8), (1280, 64, 64, 12), (1400, 64, 64, 12),
+                                            (769, 16, 16, 15)])
+def test_orth_cholqr_graded_sketches(gpu_ctx, orc, I, s, mu, decades, monkeypatch):
+    # sketches with kappa up to 1e15 (the BASELINE sketches reach 1e16) through the
+    # CholeskyQR basis (I > 768; 1400 rows exceed one cluster: Householder): leading vectors match the oracle's thin SVD where the spectrum
+    # determines them (sigma_k >= 1e-4 sigma_1), the whole factor is orthonormal, and the
+    # Householder-only path (LMRA_ORTH_CHOLQR=0) gives the same vectors
+    from paper_2303_11612_b200 import device
+    c, sig = _graded_sketch(I, s, decades, I + s + decades)
+    want = orc.leading_left_singular_vectors(c, mu)
+    outs = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("LMRA_ORTH_CHOLQR", env)
+        got = device.leading_left_singular_vectors(_to_dev(c.ravel(order="F")), I, s, mu,
+                                                   ctx=gpu_ctx).cpu().numpy().reshape((I, mu), order="F")
+        assert np.abs(got.T @ got - np.eye(mu)).max() <= 1e-13
+        k = int(np.sum(sig[:mu] >= 1e-4))
+        assert np.abs(got[:, :k] - want[:, :k]).max() <= 1e-10, np.abs(got[:, :k] - want[:, :k]).max()
+        outs.append(got)
+    k = int(np.sum(sig[:mu] >= 1e-4))
+    assert np.abs(outs[0][:, :k] - outs[1][:, :k]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("I,s,rank,mu", [(1000, 60, 20, 30), (900, 40, 1, 10), (800, 20, 19, 20)])
+def test_orth_cholqr_rank_deficient_falls_back(gpu_ctx, I, s, rank, mu):
+    # an exactly rank-deficient sketch has no C R^-1 basis: the CholeskyQR flags it and the
+    # gated Householder tree behind it produces the factor (orthonormal, leading block = range(C))
+    from paper_2303_11612_b200 import device
+    rng = np.random.default_rng(I + rank)
+    base = rng.standard_normal((I, rank))
+    c = np.asfortranarray(base @ rng.standard_normal((rank, s)))
+    c[:, s // 2] = 0.0
+    u = device.leading_left_singular_vectors(_to_dev(c.ravel(order="F")), I, s, mu,
+                                             ctx=gpu_ctx).cpu().numpy().reshape((I, mu), order="F")
+    assert np.all(np.isfinite(u))
+    assert np.abs(u.T @ u - np.eye(mu)).max() <= 1e-12
+    q, _ = np.linalg.qr(base)
+    assert subspace_sine(u[:, :rank], q) <= 1e-10
+
+
 @pytest.mark.parametrize("strategy", ["A", "B"])
 @pytest.mark.parametrize("shape", [(37, 300, 9, 2), (1000, 400, 60, 2), (200, 5000, 15, 1), (3, 960, 3, 1),
                                    (513, 77, 33, 3), (511, 1000, 7, 1)])
@@ -302,7 +351,19 @@ def test_split_orthonormalisation_path(gpu_ctx, lmra, orc, alg, monkeypatch):
     # LMRA_ORTH_SPLIT=1: the core contracted with each sketch's basis Q_C, the Jacobi rotations
     # U_R' applied to the small core at the end (opt-in path, lmra_b200.cpp)
     monkeypatch.setenv("LMRA_ORTH_SPLIT", "1")
-    dims = [60, 50, 40]
+    _split_case(lmra, orc, alg, [60, 50, 40])
+
+
+@pytest.mark.parametrize("alg", ["alg1", "alg4"])
+@pytest.mark.parametrize("cholqr", ["1", "0"])
+def test_split_orthonormalisation_cholqr_basis(gpu_ctx, lmra, orc, alg, cholqr, monkeypatch):
+    # the split form with a CholeskyQR basis (first mode > 768 rows) and with the Householder one
+    monkeypatch.setenv("LMRA_ORTH_SPLIT", "1")
+    monkeypatch.setenv("LMRA_ORTH_CHOLQR", cholqr)
+    _split_case(lmra, orc, alg, [40, 50, 800])  # mode 2 (rank 4) is contracted first
+
+
+def _split_case(lmra, orc, alg, dims):
     x = orc.gen_tucker_noise(dims, [6, 5, 4], 1e-2, 13)
     kw = dict(rank=[6, 5, 4], seed=3, power=2, regime="nearly_optimal", t_samples=[300, 300, 300])
     cg, co = _cfgs(lmra, orc, **kw)
