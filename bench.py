@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0, help="CPU arm threads (default: all host cores)")
+    ap.add_argument("--no-single-thread", action="store_true",
+                    help="reference arm: skip the extra 1-thread decomposition")
     return ap.parse_args()
 
 
@@ -255,6 +257,14 @@ def bench_reference(args, rank, world):
     times = run_cpu(bc, x, max(1, args.steps), args.warmup, threads)
     total = sum(times)
     v = round(cost["bytes"] * len(times) / total / 1e9, 4)
+    # BASELINE.md's second CPU row: the reference's default, one thread (LMRA_NUM_THREADS=1,
+    # BLAS single-threaded; README.md:132-135), one decomposition of the same workload
+    single = None
+    if threads > 1 and not args.no_single_thread:
+        t1 = run_cpu(bc, x, 1, 0, 1)[0]
+        single = {"value": round(cost["bytes"] / t1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                  "seconds_per_decomposition": round(t1, 3),
+                  "sample": "one decomposition of the same workload and input bits, 1 thread"}
     sample = (f"the full workload ({'x'.join(map(str, bc.dims))}, {bc.alg}): one decomposition per step, "
               f"{len(times)} timed after {args.warmup} warm-up; oracle C++ restatement of the reference + "
               f"OpenBLAS, {threads} threads; input bits identical to the GPU arm's (host generators), "
@@ -267,7 +277,8 @@ def bench_reference(args, rank, world):
         "parallelism": f"host CPU, {threads} threads",
         "config": workload_config(bc, cost),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
-                         "cpu_model": cpu_model(), "per_step_s": [round(t, 3) for t in times]},
+                         "cpu_model": cpu_model(), "per_step_s": [round(t, 3) for t in times],
+                         "single_thread": single},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
