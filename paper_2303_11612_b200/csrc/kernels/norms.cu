@@ -10,6 +10,8 @@
 // HBM-bound: 8 B read per element, 2 flop.  Contiguous fibers (mode 0) are staged
 // through shared memory so each thread walks its own fiber; strided fibers (modes
 // > 0) are read coalesced across threads (consecutive i), one thread per column.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace lmra_dev {
@@ -44,6 +46,56 @@ __global__ void __launch_bounds__(128) sqnorm_contig_kernel(const double* __rest
     canon_add(p, r0 / kNormChunk, r0 + kNormChunk >= I, seg, total);
     __syncthreads();
   }
+  const long long j = j0 + tid;
+  if (j < J) w[j] = total;
+}
+
+// mode 0, pipelined: the same canonical sums, with the 32-row x 128-column tiles streamed by
+// cp.async through a 3-stage ring (the one-tile kernel above alternates load and compute phases
+// and reached 4.9 TB/s on cfg5's 3.2 GB tensor, long-scoreboard bound).  Column c's 32 entries
+// land rotated by c (element q at (q + c) mod 32), so both the 8-byte async copies (a warp
+// writes 32 consecutive entries of one column) and the per-thread column reads (32 lanes, 32
+// columns, same q) hit distinct bank pairs.
+constexpr int kNCStages = 3;
+__global__ void __launch_bounds__(128) sqnorm_contig_pipe_kernel(const double* __restrict__ x,
+                                                                 long long I, long long J,
+                                                                 double* __restrict__ w) {
+  extern __shared__ __align__(16) double ring[];  // [stage][128 columns][32]
+  const int tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5;
+  const long long j0 = (long long)blockIdx.x * 128;
+  const long long nch = (I + kNormChunk - 1) / kNormChunk;
+  auto load = [&](long long ch) {
+    double* t = ring + (ch % kNCStages) * (128 * kNormChunk);
+    const long long r0 = ch * kNormChunk;
+    const bool rok = r0 + lane < I;
+#pragma unroll 8
+    for (int c = wrp; c < 128; c += 4) {
+      const long long j = j0 + c;
+      const bool ok = rok && j < J;
+      cp_async8(t + c * kNormChunk + ((lane + c) & (kNormChunk - 1)), ok ? x + I * j + r0 + lane : x, ok);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < kNCStages - 1; ++st) {
+    if (st < nch) load(st);
+    cp_async_commit();
+  }
+  double total = 0.0, seg = 0.0;
+  for (long long ch = 0; ch < nch; ++ch) {
+    cp_async_wait<kNCStages - 2>();
+    __syncthreads();  // stage ch landed for every thread; stage ch - 1 is free again
+    if (ch + kNCStages - 1 < nch) load(ch + kNCStages - 1);
+    cp_async_commit();
+    const double* t = ring + (ch % kNCStages) * (128 * kNormChunk) + tid * kNormChunk;
+    const int n = (I - ch * kNormChunk < kNormChunk) ? (int)(I - ch * kNormChunk) : kNormChunk;
+    double p = 0.0;
+    for (int q = 0; q < n; ++q) {
+      const double v = t[(q + tid) & (kNormChunk - 1)];
+      p = fma(v, v, p);
+    }
+    canon_add(p, ch, ch + 1 == nch, seg, total);
+  }
+  cp_async_wait<0>();
   const long long j = j0 + tid;
   if (j < J) w[j] = total;
 }
@@ -144,7 +196,17 @@ cudaError_t launch_column_sqnorms(const double* x, ModeView v, double* w, cudaSt
   const long long J = v.inner * v.outer;
   if (J == 0) return cudaSuccess;
   if (v.inner == 1) {
-    sqnorm_contig_kernel<<<(unsigned)((J + 127) / 128), 128, 0, st>>>(x, v.I, J, w); note_launch();
+    static const bool pipe = !(getenv("LMRA_NORMS_PIPE") && getenv("LMRA_NORMS_PIPE")[0] == '0');
+    if (pipe) {
+      static unsigned long long attr_done = 0;
+      const size_t smem = sizeof(double) * kNCStages * 128 * kNormChunk;
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(sqnorm_contig_pipe_kernel), smem, attr_done);
+      if (e != cudaSuccess) return e;
+      sqnorm_contig_pipe_kernel<<<(unsigned)((J + 127) / 128), 128, smem, st>>>(x, v.I, J, w);
+    } else {
+      sqnorm_contig_kernel<<<(unsigned)((J + 127) / 128), 128, 0, st>>>(x, v.I, J, w);
+    }
+    note_launch();
   } else {
     sqnorm_strided_kernel<<<(unsigned)((J + 255) / 256), 256, 0, st>>>(x, v, w); note_launch();
   }
