@@ -699,6 +699,179 @@ done:
 }
 
 
+// ---------------------------------------------------------------------------
+// Two-warp Jacobi for narrow sketches (s <= 32): the same one-sided Jacobi on G = R^T with the
+// rotations accumulated in J, the same circle-method pair order and angle formula as
+// reg_jacobi, but with no block barrier.  Warp 0 holds G, warp 1 holds J, both in registers:
+// lanes are grouped L per pair (L = 32 / P2, P2 = the power of two >= the P = ceil(s / 2)
+// pairs); lane (p, h) holds rows [h H, h H + H) of the pair's two columns.  A pair's dot
+// products are H-row partials combined by log2(L) xor-shuffles, every lane of the pair forms
+// the same angle, the rotation is lane-local, the circle move is two shuffles by L lanes.
+// Warp 0 hands each round's angles to warp 1 through a double-buffered slot and a 64-thread
+// named barrier (warp 1 rotates J and moves its columns one round behind).  reg_jacobi's round
+// (partials -> barrier -> warp 0 forms the angles -> barrier -> rotate) costs ~1-2 k cycles
+// whatever s is; at s = 15..30 that fixed cost dominated the sketch SVD.
+template <int L, int H>
+__device__ __forceinline__ void circle_move_rows(double (&T)[H], double (&B)[H], int p, int P) {
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const double up = __shfl_up_sync(0xffffffffu, p == 0 ? B[i] : T[i], L);
+    const double dn = __shfl_down_sync(0xffffffffu, B[i], L);
+    const double t = T[i];
+    if (p != 0) T[i] = up;
+    B[i] = p == P - 1 ? t : dn;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void circle_move_slots(int& cT, int& cB, int p, int P) {
+  const int up = __shfl_up_sync(0xffffffffu, p == 0 ? cB : cT, L);
+  const int dn = __shfl_down_sync(0xffffffffu, cB, L);
+  const int t = cT;
+  if (p != 0) cT = up;
+  cB = p == P - 1 ? t : dn;
+}
+
+// slots: [2][cos 32 | sin 32] doubles; ctl: [2] ints (0 round, 1 stop)
+template <int L, int H>
+__device__ bool narrow_jacobi_g(double* G, int s, double tol, double* slots, int* ctl) {
+  const int l = threadIdx.x & 31;
+  const int p = l / L, h = l % L;
+  const int P = (s + 1) / 2;
+  const bool live = p < P;
+  const double tol2 = tol * tol;
+  int cT = live ? p : 1 << 20, cB = live ? p + P : 1 << 20;
+  double T[H], B[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int r = h * H + i;
+    T[i] = (live && r < s && cT < s) ? G[r + (size_t)s * cT] : 0.0;
+    B[i] = (live && r < s && cB < s) ? G[r + (size_t)s * cB] : 0.0;
+  }
+  bool converged = false;
+  int round = 0;
+  for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
+    bool rotated = false;
+    for (int rd = 0; rd < 2 * P - 1; ++rd, ++round) {
+      double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+      for (int i = 0; i < H; ++i) {
+        a = fma(T[i], T[i], a);
+        b = fma(B[i], B[i], b);
+        c = fma(T[i], B[i], c);
+      }
+#pragma unroll
+      for (int m = 1; m < L; m <<= 1) {  // the pair's L lanes, fixed xor order: identical sums
+        a += __shfl_xor_sync(0xffffffffu, a, m);
+        b += __shfl_xor_sync(0xffffffffu, b, m);
+        c += __shfl_xor_sync(0xffffffffu, c, m);
+      }
+      double cs = 1.0, sn = 0.0;
+      if (live && jacobi_angle(a, b, c, tol2, cs, sn)) rotated = true;
+      double* sl = slots + 64 * (round & 1);
+      if (h == 0 && p < 32) {
+        sl[p] = cs;
+        sl[32 + p] = sn;
+      }
+      if (l == 0) ctl[round & 1] = 0;
+      named_bar(1, 64);  // the round's angles to warp 1
+#pragma unroll
+      for (int i = 0; i < H; ++i) {
+        const double x = T[i], y = B[i];
+        T[i] = cs * x - sn * y;
+        B[i] = sn * x + cs * y;
+      }
+      if (P > 1) {
+        circle_move_rows<L, H>(T, B, p, P);
+        circle_move_slots<L>(cT, cB, p, P);
+      }
+    }
+    if (!__any_sync(0xffffffffu, rotated)) {
+      converged = true;
+      if (l == 0) g_jacobi_sweeps = sweep + 1;
+    }
+  }
+  if (l == 0) ctl[round & 1] = 1;  // stop
+  named_bar(1, 64);
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const int r = h * H + i;
+      if (r < s) {
+        if (cT < s) G[r + (size_t)s * cT] = T[i];
+        if (cB < s) G[r + (size_t)s * cB] = B[i];
+      }
+    }
+  }
+  return converged;
+}
+
+template <int L, int H>
+__device__ void narrow_jacobi_j(double* J, int s, const double* slots, const int* ctl) {
+  const int l = threadIdx.x & 31;
+  const int p = l / L, h = l % L;
+  const int P = (s + 1) / 2;
+  const bool live = p < P;
+  int cT = live ? p : 1 << 20, cB = live ? p + P : 1 << 20;
+  double T[H], B[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int r = h * H + i;
+    T[i] = r == cT ? 1.0 : 0.0;
+    B[i] = r == cB ? 1.0 : 0.0;
+  }
+  for (int round = 0;; ++round) {
+    named_bar(1, 64);
+    if (ctl[round & 1]) break;
+    const double* sl = slots + 64 * (round & 1);
+    const double cs = live ? sl[p] : 1.0, sn = live ? sl[32 + p] : 0.0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double x = T[i], y = B[i];
+      T[i] = cs * x - sn * y;
+      B[i] = sn * x + cs * y;
+    }
+    if (P > 1) {
+      circle_move_rows<L, H>(T, B, p, P);
+      circle_move_slots<L>(cT, cB, p, P);
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const int r = h * H + i;
+      if (r < 64 && cT < 64) J[r + 64 * cT] = T[i];
+      if (r < 64 && cB < 64) J[r + 64 * cB] = B[i];
+    }
+  }
+}
+
+// the whole CTA: warps 0 / 1 run the G / J halves, the others wait; the flag goes through smem
+template <int L, int H>
+__device__ bool narrow_jacobi_lh(double* G, int s, double* J, double tol, const QSmem& q) {
+  const int w = threadIdx.x >> 5;
+  double* slots = q.fval;  // q.fval + q.rowk: 128 contiguous doubles
+  int* ctl = q.pidx;       // [0, 2) round control, [63] result
+  if (w == 0) {
+    const bool conv = narrow_jacobi_g<L, H>(G, s, tol, slots, ctl);
+    if ((threadIdx.x & 31) == 0) q.pidx[63] = conv ? 1 : 0;
+  } else if (w == 1) {
+    narrow_jacobi_j<L, H>(J, s, slots, ctl);
+  }
+  __syncthreads();
+  return q.pidx[63] != 0;
+}
+
+__device__ bool narrow_jacobi(double* G, int s, double* J, double tol, const QSmem& q) {
+  // J is read as 64 x 64 afterwards: identity first (the J warp writes the s real slots)
+  for (int e = threadIdx.x; e < 64 * 64; e += kQThreads) J[e] = (e % 65 == 0) ? 1.0 : 0.0;
+  __syncthreads();
+  if (s <= 8) return narrow_jacobi_lh<8, 2>(G, s, J, tol, q);
+  if (s <= 16) return narrow_jacobi_lh<4, 4>(G, s, J, tol, q);
+  if (s <= 24) return narrow_jacobi_lh<2, 12>(G, s, J, tol, q);
+  return narrow_jacobi_lh<2, 16>(G, s, J, tol, q);
+}
+
 // CTA 1 of the cluster: the J half of reg_jacobi, driven by the angles CTA 0 sends; the
 // final J goes into CTA 0's J buffer (jdst: its DSMEM address).  Same register layout,
 // tournament and rotation arithmetic as the J warps of reg_jacobi.
@@ -807,7 +980,8 @@ template <int RPL>
 __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     const double* __restrict__ S, int m, int s, int lds, int mu, double* __restrict__ out,
     int ldo, int final_level, int* status, double jacobi_tol, int clustered, int phase,
-    double* __restrict__ gbuf, double* __restrict__ ur, int basis_pivot, const int* __restrict__ gate, int run_if) {
+    double* __restrict__ gbuf, double* __restrict__ ur, int basis_pivot, const int* __restrict__ gate, int run_if,
+    int narrow_jacobi_on) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
   // no early pdl_trigger(): a dependent launched now would park its CTAs (waiting in
@@ -917,7 +1091,9 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     converged = reg_jacobi(G, s, J, jacobi_tol, q, &link);
     cluster_sync();  // CTA 1 has written J here
   } else {
-    converged = reg_jacobi(G, s, J, jacobi_tol, q);
+    // narrow sketches: the barrier-free one-warp Jacobi (LMRA_NARROW_JACOBI=0: the block one)
+    converged = (s <= 32 && narrow_jacobi_on) ? narrow_jacobi(G, s, J, jacobi_tol, q)
+                                              : reg_jacobi(G, s, J, jacobi_tol, q);
   }
   pdl_trigger();
   // singular values = column norms of G, fixed order
@@ -1172,6 +1348,12 @@ cudaError_t leaf_qr(const double* A, long long m, int s, int nb, double* V, doub
   return cudaGetLastError();
 }
 
+// LMRA_NARROW_JACOBI=0: sketches with s <= 32 take the block Jacobi too (comparison / tests)
+static int narrow_jacobi_on() {
+  const char* e = getenv("LMRA_NARROW_JACOBI");
+  return !(e && e[0] == '0');
+}
+
 // LMRA_ORTH_BASIS_PIVOT=1: pivot in the basis phase too
 static int basis_pivot() {
   static const int on = getenv("LMRA_ORTH_BASIS_PIVOT") && getenv("LMRA_ORTH_BASIS_PIVOT")[0] == '1';
@@ -1212,12 +1394,12 @@ cudaError_t core(const double* S, int m, int s, int mu, double* out, int ldo, in
     note_launch();
     const cudaError_t le = cudaLaunchKernelEx(&cfg, orth_core_kernel<RPL>, S, m, s, m, mu, out, ldo, final_level,
                                               status, tol, 1, phase, gbuf, ur, basis_pivot(), g_gate.p,
-                                              g_gate.run_if);
+                                              g_gate.run_if, narrow_jacobi_on());
     if (le != cudaSuccess) return le;
   } else {
     const cudaError_t le = launch_pdl(orth_core_kernel<RPL>, dim3(1), dim3(kQThreads), smem, st, S, m, s, m, mu,
                                       out, ldo, final_level, status, tol, 0, phase, gbuf, ur, basis_pivot(), g_gate.p,
-                                      g_gate.run_if);
+                                      g_gate.run_if, narrow_jacobi_on());
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();
