@@ -753,13 +753,25 @@ __device__ bool narrow_jacobi_g(double* G, int s, double tol, double* slots, int
   for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
     bool rotated = false;
     for (int rd = 0; rd < 2 * P - 1; ++rd, ++round) {
-      double a = 0.0, b = 0.0, c = 0.0;
+#ifdef LMRA_JACOBI_CLOCKS
+      const long long k0 = clock64();
+#endif
+      // two accumulators per sum (shorter fma chains), added once
+      double a = 0.0, b = 0.0, c = 0.0, a2 = 0.0, b2 = 0.0, c2 = 0.0;
 #pragma unroll
-      for (int i = 0; i < H; ++i) {
+      for (int i = 0; i < H; i += 2) {
         a = fma(T[i], T[i], a);
         b = fma(B[i], B[i], b);
         c = fma(T[i], B[i], c);
+        if (i + 1 < H) {
+          a2 = fma(T[i + 1], T[i + 1], a2);
+          b2 = fma(B[i + 1], B[i + 1], b2);
+          c2 = fma(T[i + 1], B[i + 1], c2);
+        }
       }
+      a += a2;
+      b += b2;
+      c += c2;
 #pragma unroll
       for (int m = 1; m < L; m <<= 1) {  // the pair's L lanes, fixed xor order: identical sums
         a += __shfl_xor_sync(0xffffffffu, a, m);
@@ -774,7 +786,13 @@ __device__ bool narrow_jacobi_g(double* G, int s, double tol, double* slots, int
         sl[32 + p] = sn;
       }
       if (l == 0) ctl[round & 1] = 0;
+#ifdef LMRA_JACOBI_CLOCKS
+      const long long k1 = clock64();
+#endif
       named_bar(1, 64);  // the round's angles to warp 1
+#ifdef LMRA_JACOBI_CLOCKS
+      const long long k2 = clock64();
+#endif
 #pragma unroll
       for (int i = 0; i < H; ++i) {
         const double x = T[i], y = B[i];
@@ -785,6 +803,15 @@ __device__ bool narrow_jacobi_g(double* G, int s, double tol, double* slots, int
         circle_move_rows<L, H>(T, B, p, P);
         circle_move_slots<L>(cT, cB, p, P);
       }
+#ifdef LMRA_JACOBI_CLOCKS
+      if (l == 0) {
+        const long long k3 = clock64();
+        g_jclk[0] += k1 - k0;
+        g_jclk[1] += k2 - k1;
+        g_jclk[2] += k3 - k2;
+        g_jclk[4] += 1;
+      }
+#endif
     }
     if (!__any_sync(0xffffffffu, rotated)) {
       converged = true;
@@ -1092,6 +1119,9 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     cluster_sync();  // CTA 1 has written J here
   } else {
     // narrow sketches: the barrier-free one-warp Jacobi (LMRA_NARROW_JACOBI=0: the block one)
+    // narrow sketches (s <= 32): the barrier-free two-warp Jacobi (LMRA_NARROW_JACOBI=0: the block one);
+    // wider ones keep the block form (a multi-warp register form with shared-memory edge exchange
+    // measured 1.6x slower per round at s = 40..60, tools/microbench/jacobi_variants.cu)
     converged = (s <= 32 && narrow_jacobi_on) ? narrow_jacobi(G, s, J, jacobi_tol, q)
                                               : reg_jacobi(G, s, J, jacobi_tol, q);
   }
