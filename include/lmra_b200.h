@@ -184,9 +184,10 @@ int lmra_result_num_phases(const lmra_result* r);
 int lmra_result_phase(const lmra_result* r, int i, char* name, size_t name_len, double* ms,
                       int* launches);
 /* Releases the result.  Its device core / factor buffers go back to the context's block
- * cache and are reused by later runs: device work still reading them (on another stream)
- * must be complete first -- the same contract as cudaFree, minus cudaFree's implicit
- * device synchronisation. */
+ * cache and are reused by later runs.  If their device pointers were handed out
+ * (lmra_result_core_device / lmra_result_factor_device), free synchronises the device first,
+ * so reads the caller queued on its own streams complete before the blocks are reused (the
+ * guarantee cudaFree gives); results only read through the copy calls skip that sync. */
 void lmra_result_free(lmra_result* r);
 
 /* ---- primitives (device pointers unless stated; all on the context's stream) ---- */

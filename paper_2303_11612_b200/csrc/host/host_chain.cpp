@@ -103,6 +103,19 @@ class Pool {
     }
     cv_.notify_one();
   }
+  // runs one queued job on the calling thread (false: queue empty) -- a waiter helps instead of
+  // sleeping while the workers wake up (small batches: the wake-up dominated)
+  bool try_run_one() {
+    std::function<void()> f;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (q_.empty()) return false;
+      f = std::move(q_.front());
+      q_.pop_front();
+    }
+    f();
+    return true;
+  }
   void push_batch(std::vector<std::function<void()>>& fs) {
     {
       std::lock_guard<std::mutex> lk(mu_);
@@ -179,6 +192,13 @@ void TaskGroup::run_batch(std::vector<std::function<void()>> fs) {
 }
 
 void TaskGroup::wait() {
+  for (;;) {
+    {
+      std::lock_guard<std::mutex> lk(st_->mu);
+      if (st_->pending == 0) return;
+    }
+    if (!pool().try_run_one()) break;
+  }
   std::unique_lock<std::mutex> lk(st_->mu);
   st_->cv.wait(lk, [this] { return st_->pending == 0; });
 }

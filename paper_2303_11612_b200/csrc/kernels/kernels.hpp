@@ -194,4 +194,5 @@ cudaError_t launch_transpose(const double* a, long long rows, long long cols, do
 
 namespace lmra_dev {
 int last_jacobi_sweeps();  // diagnostics: sweeps of the most recent converged Jacobi
+void last_orth_clocks(long long* out7);  // diagnostics: phase clocks of the last full orth core
 }

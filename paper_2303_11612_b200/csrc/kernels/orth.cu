@@ -477,6 +477,11 @@ __device__ __forceinline__ void circle_shift(double (&T)[8], double (&B)[8], int
 }
 
 __device__ int g_jacobi_sweeps;
+// phase clocks of the most recent orth_core_kernel (thread 0; diagnostics only): start, tile
+// loaded, QR done, G scaled, Jacobi done, order done, end
+__device__ long long g_orth_clk[8];
+#define ORTH_CLK(i) \
+  if (threadIdx.x == 0 && phase == kOrthFull) g_orth_clk[i] = clock64()
 #ifdef LMRA_JACOBI_CLOCKS
 __device__ unsigned long long g_jclk[8];  // microbenchmark only: per-phase cycles, warp 0
 #endif
@@ -1011,6 +1016,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     int narrow_jacobi_on) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   if (gate && *gate != run_if) return;  // the other branch of a gated pair of paths (cholqr fallback)
+  ORTH_CLK(0);
   // no early pdl_trigger(): a dependent launched now would park its CTAs (waiting in
   // griddepcontrol.wait) on SMs for the whole Jacobi, and a big kernel of another stream (the
   // core contraction beside a split orthonormalisation) could not use those SMs; the trigger
@@ -1048,6 +1054,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
   } else {
     load_tile(S, lds, m, s, Vs, ldv, 32 * RPL);
     __syncthreads();
+    ORTH_CLK(1);
     double a[kCW][RPL];
     cw_load(Vs, ldv, m, s, a);
     // the basis phase skips the column pivoting: it only preconditions the Jacobi (graded R,
@@ -1055,6 +1062,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     reg_qr(a, m, s, q, phase != kOrthBasis || basis_pivot);
     if ((int)threadIdx.x < s) q.ipiv[q.piv[threadIdx.x]] = threadIdx.x;
     __syncthreads();
+    ORTH_CLK(2);
     // G = R^T (lower triangle), reflectors to Vs in logical column order
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
@@ -1108,6 +1116,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     }
     __syncthreads();
   }
+  ORTH_CLK(3);
   bool converged;
   if (clustered) {
     JLink link;
@@ -1126,6 +1135,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
                                               : reg_jacobi(G, s, J, jacobi_tol, q);
   }
   pdl_trigger();
+  ORTH_CLK(4);
   // singular values = column norms of G, fixed order
   for (int c = w; c < s; c += kQWarps) {
     double t = 0.0;
@@ -1142,6 +1152,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     perm[rank] = c;
   }
   __syncthreads();
+  ORTH_CLK(5);
   if (phase == kOrthJacobi) {  // U_R(:, :mu) in descending singular-value order
     for (int e = threadIdx.x; e < s * mu; e += kQThreads) {
       const int r = e % s, c = e / s;
@@ -1185,6 +1196,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     }
   }
   if (threadIdx.x == 0 && status) *status = converged ? 0 : 1;
+  ORTH_CLK(6);
 }
 
 // ---------------------------------------------------------------------------
@@ -1338,6 +1350,8 @@ size_t orth_workspace_doubles(long long I, int s) {
 }
 
 // sweeps taken by the most recent converged Jacobi (diagnostics only)
+void last_orth_clocks(long long* out7) { cudaMemcpyFromSymbol(out7, g_orth_clk, 7 * sizeof(long long)); }
+
 int last_jacobi_sweeps() {
   int v = 0;
   cudaMemcpyFromSymbol(&v, g_jacobi_sweeps, sizeof(int));

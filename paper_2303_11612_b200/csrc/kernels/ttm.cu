@@ -367,6 +367,40 @@ __global__ void __launch_bounds__(kGramThreads)
     }
 }
 
+// Many splits (the Gram's split-J partials: ~200 on cfg1): 8 threads per output, thread g
+// summing the partials p = g (mod 8) with their loads independent, then the 8 sums added in
+// g order through shared memory -- fixed order (deterministic), 8x the loads in flight of the
+// one-thread-per-output loop, which was a ~200-long chain of L2 round trips.
+__global__ void __launch_bounds__(256) reduce_splits8_kernel(const double* __restrict__ zpart, int nsplit,
+                                                             long long n, double* __restrict__ z) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ double part[8][33];
+  const int lx = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const long long e = (long long)blockIdx.x * 32 + lx;
+  double acc = 0.0;
+  if (e < n) {
+    double a0 = 0.0, a1 = 0.0;
+    int p = g;
+    for (; p + 8 < nsplit; p += 16) {
+      a0 += zpart[(size_t)p * n + e];
+      a1 += zpart[(size_t)(p + 8) * n + e];
+    }
+    if (p < nsplit) a0 += zpart[(size_t)p * n + e];
+    acc = a0 + a1;
+  }
+  part[g][lx] = acc;
+  __syncthreads();
+  if (g == 0 && e < n) {
+    double t = part[0][lx];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += part[k][lx];
+    z[e] = t;
+  }
+}
+
+static cudaError_t launch_reduce_splits(const double* zpart, int nsplit, long long n, double* z, cudaStream_t st);
+
 // z[e] = sum_{p < nsplit} zpart[p][e], fixed order (deterministic).
 __global__ void reduce_splits_kernel(const double* __restrict__ zpart, int nsplit, long long n,
                                      double* __restrict__ z) {
@@ -377,6 +411,12 @@ __global__ void reduce_splits_kernel(const double* __restrict__ zpart, int nspli
   double acc = zpart[e];
   for (int p = 1; p < nsplit; ++p) acc += zpart[(size_t)p * n + e];
   z[e] = acc;
+}
+
+static cudaError_t launch_reduce_splits(const double* zpart, int nsplit, long long n, double* z, cudaStream_t st) {
+  if (nsplit >= 16)
+    return launch_pdl(reduce_splits8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, st, zpart, nsplit, n, z);
+  return launch_pdl(reduce_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, zpart, nsplit, n, z);
 }
 
 // C'(:, t) = X(:, idx[t]) * scale[t]  (sketching.cpp:133-141), C' is I x T column-major.
@@ -514,12 +554,75 @@ static int device_sms() {
   return sms;
 }
 
+// Short contractions (I <= 8: cfg5's mode of extent 3): a streaming kernel, one thread per
+// column j -- the I fibre values in registers, B^T (I x m) in shared memory, m outputs written
+// in Y's layout.  The DMMA kernel pads K to its 16-row chunk and runs one K stage per CTA, so
+// it was latency-bound (cfg5 shrink of the 3-extent mode: 43 us for 40 MB of traffic).
+// Same sum order as the DMMA path's single K chunk is not required: r ascending, fma chain.
+constexpr int kSmallI = 8;
+template <int IS>
+__global__ void __launch_bounds__(256) ttm_small_kernel(const double* __restrict__ x, ModeView v,
+                                                        const double* __restrict__ bt, int m, int mtot,
+                                                        int koff, double* __restrict__ y, Gather ga) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ double bs[kSmallI * kMaxWidth];
+  const int I = (int)v.I;
+  for (int e = threadIdx.x; e < I * m; e += blockDim.x) bs[e] = bt[e];  // bt[r + I * k]
+  __syncthreads();
+  const long long J = v.inner * v.outer;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (long long)gridDim.x * blockDim.x) {
+    double xr[IS];
+    long long ybase, ystride;
+    double sc2 = 1.0;
+    if (v.inner == 1) {
+      const long long cj = ga.idx ? __ldg(ga.idx + j) : j;
+#pragma unroll
+      for (int r = 0; r < IS; ++r) xr[r] = (r < I && cj >= 0) ? __ldg(x + I * cj + r) : 0.0;
+      if (ga.scale) {
+        const double sc = ga.scale[j];
+        sc2 = sc * sc;
+      }
+      ybase = j * mtot + koff;
+      ystride = 1;
+    } else {
+      const long long o = j / v.inner, i = j - o * v.inner;
+      const long long base = i + v.inner * (long long)I * o;
+#pragma unroll
+      for (int r = 0; r < IS; ++r) xr[r] = r < I ? __ldg(x + base + v.inner * r) : 0.0;
+      ybase = i + v.inner * ((long long)mtot * o + koff);
+      ystride = v.inner;
+    }
+    for (int k = 0; k < m; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < IS; ++r)
+        if (r < I) acc = fma(bs[r + I * k], xr[r], acc);
+      y[ybase + ystride * k] = ga.scale ? acc * sc2 : acc;
+    }
+  }
+}
+
+static cudaError_t launch_ttm_small(const double* x, ModeView v, const double* bt, int m, double* y,
+                                    cudaStream_t st, Gather ga) {
+  const long long J = v.inner * v.outer;
+  const long long blocks = std::min<long long>((J + 255) / 256, 8LL * device_sms());
+  auto go = [&](auto is) {
+    return launch_pdl(ttm_small_kernel<decltype(is)::value>, dim3((unsigned)blocks), dim3(256), 0, st, x, v, bt,
+                      m, m, 0, y, ga);
+  };
+  const cudaError_t e = v.I <= 4 ? go(std::integral_constant<int, 4>{}) : go(std::integral_constant<int, 8>{});
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, double* y,
                        cudaStream_t st, Gather ga) {
   if (ga.idx && v.inner != 1) return cudaErrorInvalidValue;  // gathered: mode-0 views only
   if (m < 1) return cudaErrorInvalidValue;
   const long long J = v.inner * v.outer;
   if (J == 0) return cudaSuccess;
+  if (v.I <= kSmallI && m <= kMaxWidth && !getenv("LMRA_TTM_NO_SMALL")) return launch_ttm_small(x, v, bt, m, y, st, ga);
   // Narrow outputs (few 128-column tiles, e.g. the power scheme on sampled columns or the
   // core's last contraction) leave most SMs idle over a long K: split K across CTAs into
   // fixed-order partials (deterministic), >= 64 rows of K per split.
@@ -527,8 +630,10 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
   int ks = 1;
   const int sms = device_sms();
   const long long mink = getenv("LMRA_TTM_MINK") ? atoll(getenv("LMRA_TTM_MINK")) : 32;
-  if (jt * 2 <= sms && v.I >= 256) {
-    ks = (int)std::max<long long>(1, std::min<long long>(sms / jt, v.I / mink));
+  if (jt * 2 <= sms && v.I >= 64) {
+    // (both resident CTAs of an SM: small contractions -- the core's later modes, the last
+    // shrinks -- were a ~10-stage K loop on a few CTAs, latency-bound at ~15 us)
+    ks = (int)std::max<long long>(1, std::min<long long>(2 * sms / jt, v.I / mink));
   } else if (v.I >= 512 && jt < 8LL * sms) {
     // a few waves of a long-K contraction: fill the last wave (two CTAs per SM) by splitting
     // K, each extra split charged ~3 % for its partials' round trip
@@ -561,7 +666,7 @@ cudaError_t launch_ttm(const double* x, ModeView v, const double* bt, int m, dou
     if (e == cudaSuccess) {
       const long long n = J * m;
       {
-    const cudaError_t le = launch_pdl(reduce_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, part, ks, n, y);
+    const cudaError_t le = launch_reduce_splits(part, ks, n, y, st);
     if (le != cudaSuccess) return le;
   }
       e = cudaGetLastError();
@@ -637,7 +742,7 @@ cudaError_t launch_gram(const double* x, ModeView v, const double* h, int s, dou
   }
   long long n = v.I * s;
   {
-    const cudaError_t le = launch_pdl(reduce_splits_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, zpart, plan.nsplit, n, z);
+    const cudaError_t le = launch_reduce_splits(zpart, plan.nsplit, n, z, st);
     if (le != cudaSuccess) return le;
   }
   return cudaGetLastError();

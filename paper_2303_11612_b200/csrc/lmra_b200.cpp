@@ -15,6 +15,7 @@
 #include "host/cusolver_dyn.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -482,11 +483,18 @@ struct lmra_result {
     int count;
   };
   std::vector<Phase> phases;  // device time per launch category (profiling contexts only)
+  // set once core / factor device pointers were handed out (lmra_result_*_device): the caller
+  // may have queued reads of them on streams of its own
+  mutable std::atomic<bool> exposed{false};
   ~lmra_result() {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != device) cudaSetDevice(device);
-    if (blocks) {  // stream order: the run that produced them has synchronised
+    if (blocks) {
+      // the run that produced the blocks has synchronised; reads the caller queued elsewhere
+      // through the device pointers must finish before the next run's detach() reuses the
+      // blocks on the context stream -- the guarantee cudaFree gave (it synchronises)
+      if (exposed.load()) cudaDeviceSynchronize();
       blocks->put(core);
       for (double* f : factors) blocks->put(f);
     } else {
@@ -807,6 +815,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   const double tr0 = now_ms();
   bool rng_done = false;
   std::vector<std::function<void()>> omega_jobs;
+  // chunk size: ~2 jobs per pool thread, 256..4096 normals (even: chunks start on a
+  // Box-Muller pair).  Small draws (cfg1: 3 x 3000 normals) split finely: at ~30 ns a normal,
+  // one 4096-normal job per mode kept the device idle ~0.09 ms before the first power step.
+  const size_t kChunk = std::min<size_t>(
+      4096, std::max<size_t>(256, (om_off[N] / (2 * (size_t)lmra_host::host_threads()) + 1) & ~size_t(1)));
   for (size_t n = 0; n < N; ++n) {
     const size_t cnt = om_off[n + 1] - om_off[n];
     double* dst = om_pin + om_off[n];
@@ -814,7 +827,6 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       std::memcpy(dst, in.ov->omega[n], sizeof(double) * cnt);
       continue;
     }
-    constexpr size_t kChunk = 4096;  // even: chunks start on a Box-Muller pair
     const uint64_t seed = cfg.seed, stream = n + 1;
     for (size_t b0 = 0; b0 < cnt; b0 += kChunk) {
       const size_t e0 = std::min(cnt, b0 + kChunk);
@@ -944,8 +956,9 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     for (size_t n = 1; n < N; ++n)
       if (mus[n] < mus[split_mode]) split_mode = n;
   }
-  auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
-                         size_t n) -> DevBuf {
+  // phase 2a: the sketch c (I x s) of mode n
+  auto factor_power = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
+                          size_t n) -> DevBuf {
     cudaStream_t s_ = e.st_;
     const ModeView v = view_of(dims, n);
     const size_t I = dims[n], s = r.sketch[n];
@@ -972,6 +985,14 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       const ModeView cv{1, (long long)I, (long long)T};
       e.gram_power(cp.get(), cv, c, s, cfg.power, cfg.strategy);
     }
+    return c;
+  };
+  // phase 2b: the factor of mode n from its sketch c
+  auto factor_orth = [&](Engine& e, const double* x, const std::vector<size_t>& dims, size_t n,
+                         DevBuf& c) -> DevBuf {
+    cudaStream_t s_ = e.st_;
+    const ModeView v = view_of(dims, n);
+    const size_t I = dims[n], s = r.sketch[n];
     if (qr) {  // tucker.cpp:431-434 / 447-450: mu capped at min(sketch width, unfolding columns)
       const size_t J = (size_t)(v.inner * v.outer);
       const size_t mu = std::min(r.mu[n], std::min(s, J));
@@ -1007,6 +1028,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     }
     return e.orth(c.get(), I, s, mu, status_i + n);
   };
+  auto factor_mode = [&](Engine& e, const double* x, const std::vector<size_t>& dims,
+                         size_t n) -> DevBuf {
+    DevBuf c = factor_power(e, x, dims, n);
+    return factor_orth(e, x, dims, n, c);
+  };
 
   std::vector<DevBuf> factors(N);
   if (!sequential) {
@@ -1036,7 +1062,12 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     }
     for (size_t n = 0; n < N; ++n) sample_mode(engs[n], in.x, in.dims, n, amm ? t_flat[n] : 0);
     upload_omegas();
-    for (size_t n = 0; n < N; ++n) factors[n] = factor_mode(engs[n], in.x, in.dims, n);
+    // launched phase by phase across the modes (every mode's power scheme, then every mode's
+    // orthonormalisation), so the modes' chains start together instead of one host launch
+    // sequence (~20 us) apart
+    std::vector<DevBuf> sketches(N);
+    for (size_t n = 0; n < N; ++n) sketches[n] = factor_power(engs[n], in.x, in.dims, n);
+    for (size_t n = 0; n < N; ++n) factors[n] = factor_orth(engs[n], in.x, in.dims, n, sketches[n]);
     // each contraction of the core waits only for its own mode's factor: the first one
     // (the long int8 / DMMA pass over the tensor) starts as soon as that mode's chain is done,
     // while the other modes' orthonormalisations finish under it
@@ -1185,6 +1216,11 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
   ck(cudaStreamSynchronize(st), "sync");
   float dev_ms = 0;
   ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event time");
+  if (getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1' && !prof.empty()) {
+    float lead = 0;  // run start -> first phase (host RNG, uploads, launch latency)
+    ck(cudaEventElapsedTime(&lead, ev0, prof[0].a), "event time");
+    fprintf(stderr, "timeline lead-in %9.4f ms, run %9.4f ms\n", lead, dev_ms);
+  }
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   // the reference's exception surface, in its order of checks (sketching.cpp / tucker.cpp)
@@ -1707,6 +1743,11 @@ void run_sharded_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res) 
   ck(cudaStreamSynchronize(st), "sync");
   float dev_ms = 0;
   ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event time");
+  if (getenv("LMRA_TIMELINE") && getenv("LMRA_TIMELINE")[0] == '1' && !prof.empty()) {
+    float lead = 0;  // run start -> first phase (host RNG, uploads, launch latency)
+    ck(cudaEventElapsedTime(&lead, ev0, prof[0].a), "event time");
+    fprintf(stderr, "timeline lead-in %9.4f ms, run %9.4f ms\n", lead, dev_ms);
+  }
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   for (size_t n = 0; n < N; ++n) {
@@ -2399,8 +2440,12 @@ int lmra_result_copy_factor(const lmra_result* r, int mode, double* dst, int dst
   return copy_out(r->device, dst, r->factors[mode], r->f_rows[mode] * r->f_cols[mode],
                   dst_location);
 }
-const double* lmra_result_core_device(const lmra_result* r) { return r->core; }
+const double* lmra_result_core_device(const lmra_result* r) {
+  r->exposed.store(true);
+  return r->core;
+}
 const double* lmra_result_factor_device(const lmra_result* r, int mode) {
+  r->exposed.store(true);
   return r->factors[mode];
 }
 void lmra_result_omega_dims(const lmra_result* r, int mode, uint64_t* rows, uint64_t* cols) {
@@ -3026,6 +3071,7 @@ int lmra_memcpy(lmra_context* ctx, void* dst, const void* src, size_t bytes, int
 }  // extern "C"
 
 extern "C" int lmra_debug_jacobi_sweeps(void) { return lmra_dev::last_jacobi_sweeps(); }
+extern "C" void lmra_debug_orth_clocks(long long* out7) { lmra_dev::last_orth_clocks(out7); }
 
 namespace lmra_dev {  // scratch of the launchers (kernels.hpp)
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {

@@ -92,6 +92,10 @@ def test_device_relative_error_matches_oracle(gpu_ctx, orc, lmra, dims, core):
     ((33, 40, 17), 0, 13), ((33, 40, 17), 1, 64), ((33, 40, 17), 2, 70),
     ((64, 30, 20), 1, 8), ((6, 200, 9), 1, 50), ((200, 10, 30), 0, 1), ((10, 20, 200), 2, 57),
     ((3, 4, 5, 6), 3, 5), ((2, 129, 3), 1, 33),
+    # the streaming kernel for short modes (I <= 8): contiguous and strided fibres, m up to 64
+    ((40, 40, 3, 64), 2, 3), ((8, 900, 5), 0, 64), ((300, 7, 20), 1, 7), ((50, 20, 1), 2, 1),
+    # small contractions split along K over both resident CTAs of an SM
+    ((10, 200, 200), 1, 10), ((10, 10, 200), 2, 10), ((40, 40, 3, 512), 3, 40),
 ])
 def test_ttm_matches_oracle(gpu_ctx, orc, dims, mode, m):
     from paper_2303_11612_b200 import device
@@ -195,7 +199,8 @@ def test_orth_cholqr_rank_deficient_falls_back(gpu_ctx, I, s, rank, mu):
 
 @pytest.mark.parametrize("strategy", ["A", "B"])
 @pytest.mark.parametrize("shape", [(37, 300, 9, 2), (1000, 400, 60, 2), (200, 5000, 15, 1), (3, 960, 3, 1),
-                                   (513, 77, 33, 3), (511, 1000, 7, 1)])
+                                   (513, 77, 33, 3), (511, 1000, 7, 1),
+                                   (3, 163840, 3, 1), (200, 40000, 15, 1)])
 def test_gram_power_apply_matches_oracle(gpu_ctx, orc, strategy, shape):
     # split-K TTM / Gram launches on odd and even row counts (16-byte fibre loads need even I)
     from paper_2303_11612_b200 import device
@@ -389,3 +394,42 @@ def test_power_on_sampled_columns_in_place(gpu_ctx, lmra, orc, alg, regime, monk
     check_own_draws(alg, own, ref, regime)
     gpu = lmra.run_algorithm(alg, t, cg, omega=ref.omega, samples=ref.samples)
     compare(gpu, ref, x.reshape(dims, order="F"))
+
+
+def _cudart():
+    import ctypes
+    for name in ("libcudart.so.12", "libcudart.so"):
+        try:
+            return ctypes.CDLL(name)
+        except OSError:
+            continue
+    pytest.skip("libcudart not loadable through ctypes")
+
+
+def test_result_free_after_device_pointer_read(gpu_ctx, lmra, orc):
+    """A result whose device pointers were handed out synchronises at free, so a copy the caller
+    queued on a stream of its own still reads the run's core after the blocks go back to the
+    pool and the next run reuses them (ResultBlocks reuse without stream order)."""
+    import ctypes
+    torch = _torch()
+    rt = _cudart()
+    dims, core = [40, 36, 32], [5, 5, 5]
+    cfg = lmra.AlgoConfig(rank=list(core), seed=4)
+    xa = orc.gen_tucker_noise(dims, core, 1e-2, 8)
+    xb = orc.gen_tucker_noise(dims, core, 1e-2, 9)
+    ra = lmra.run_raw("alg1", lmra.DenseTensor.from_flat(xa, dims), cfg, ctx=gpu_ctx)
+    want = ra.to_host(with_trace=False).core.ravel(order="F").copy()
+    dst = torch.zeros(want.size, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(50_000_000)  # the copy below starts well after free() returns
+    rc = rt.cudaMemcpyAsync(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(ra.core_device_ptr()),
+                            ctypes.c_size_t(want.size * 8), ctypes.c_int(3), ctypes.c_void_p(side.cuda_stream))
+    assert rc == 0
+    ra.free()
+    rb = lmra.run_raw("alg1", lmra.DenseTensor.from_flat(xb, dims), cfg, ctx=gpu_ctx)
+    other = rb.to_host(with_trace=False).core.ravel(order="F")
+    side.synchronize()
+    rb.free()
+    assert not np.array_equal(other, want)
+    assert np.array_equal(dst.cpu().numpy(), want)

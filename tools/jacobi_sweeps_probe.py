@@ -1,6 +1,6 @@
 """Jacobi sweeps and orthonormalisation time on the BASELINE sketches (oracle sketches of
 scaled-down configs), per mode: lmra_leading_left_singular_vectors, then
-lmra_debug_jacobi_sweeps."""
+lmra_debug_jacobi_sweeps and the orth core's phase clocks (lmra_debug_orth_clocks)."""
 import ctypes
 import os
 import sys
@@ -16,6 +16,8 @@ from paper_2303_11612_b200 import _lib, device  # noqa: E402
 
 lib = _lib.lib
 lib.lmra_debug_jacobi_sweeps.restype = ctypes.c_int
+lib.lmra_debug_orth_clocks.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
+clk = (ctypes.c_longlong * 7)()
 for name, dims in [("cfg1", None), ("cfg2", None), ("cfg3", None), ("cfg4", [1000, 200, 200]),
                    ("cfg5", [512, 128, 3, 128])]:
     bc = CONFIGS[name] if dims is None else scaled(name, dims)
@@ -37,6 +39,10 @@ for name, dims in [("cfg1", None), ("cfg2", None), ("cfg3", None), ("cfg4", [100
             t0 = time.perf_counter()
             device.leading_left_singular_vectors(cd, I, s, mu)
             ts.append((time.perf_counter() - t0) * 1e3)
+        lib.lmra_debug_orth_clocks(clk)
+        c7 = list(clk)
+        ph = ["load", "qr", "scale", "jacobi", "order", "apply+store"]
+        parts = ", ".join(f"{ph[i]} {(c7[i + 1] - c7[i]) / 1e3:.1f}k" for i in range(6))
         sv = np.linalg.svd(sk, compute_uv=False)
         print(f"{name} mode {n}: {I}x{s} mu {mu}: sweeps {sw}, {min(ts):.3f} ms (host-timed), "
-              f"kappa {sv[0] / max(sv[-1], 1e-300):.2e}", flush=True)
+              f"kappa {sv[0] / max(sv[-1], 1e-300):.2e}; core cycles: {parts}", flush=True)
