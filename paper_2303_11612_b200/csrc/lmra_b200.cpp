@@ -190,6 +190,12 @@ void ThreadComm::allreduce_sum(double* buf, size_t n, cudaStream_t st) {
 }  // namespace
 
 // ------------------------------------------------------------------ context
+// int8 tensor-core contractions on (default) or off (LMRA_TTM_I8=0: every contraction on DMMA)
+bool ttm_i8_on() {
+  static const bool on = !(getenv("LMRA_TTM_I8") && std::string(getenv("LMRA_TTM_I8")) == "0");
+  return on;
+}
+
 // Device blocks handed to results (core, factors), recycled instead of cudaMalloc/cudaFree
 // per run (each of those costs ~0.1 ms and cudaFree synchronises the device).  Shared by the
 // context and its results, so a result may outlive the context.
@@ -568,7 +574,7 @@ class Engine {
   DevBuf ttm_mode0(const double* x, const std::vector<size_t>& dims, size_t mode, const double* q,
                    size_t m, const double* w, const std::string& phase, I8Chain* chain = nullptr,
                    bool next_mode1 = false) {
-    static const bool enabled = !(getenv("LMRA_TTM_I8") && std::string(getenv("LMRA_TTM_I8")) == "0");
+    const bool enabled = ttm_i8_on();
     const size_t total = prod(dims);
     std::vector<size_t> od = dims;
     od[mode] = m;
@@ -1148,6 +1154,9 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     DevBuf work;
     const double* src = in.x;
     Engine::I8Chain chain;
+    // (no split orthonormalisation here: measured on cfg5, the first shrink with the sketch basis
+    // beside the Jacobi, then the s x mu rotation and the mode-1 column exponents, tied the plain
+    // order -- 5.37 vs 5.35 ms: the Jacobi beside the power-capped int8 shrink ran 0.35 -> 0.61 ms)
     for (size_t oi = 0; oi < r.order.size(); ++oi) {
       const size_t n = r.order[oi];
       const bool next1 = oi + 1 < r.order.size() && r.order[oi + 1] == 1;
