@@ -410,41 +410,55 @@ __global__ void __launch_bounds__(kI8Threads, 1) ttm_i8_kernel(
       if (lane == 0) mbar_arrive(accempty);
       continue;
 #endif
-      // recombine the 6 level accumulators of column j, scale by 2^(ex + eq_m - 94 + 40); the
-      // accumulators are released as soon as the last chunk is in registers
+      // recombine the 6 level accumulators of column j, scale by 2^(ex + eq_m - 94 + 40).  All of
+      // this warp's chunks are drained first -- TMEM -> registers, the 6 levels recombined into
+      // one double per output -- and the accumulators released before any output is scaled and
+      // stored: the MMA warp waits for that release before the next tile's first K-step (TMEM has
+      // no room for a second accumulator set), and with the stores inside the drain it waited
+      // ~18 % of the kernel (tools/microbench/i8_clocks.cu, mma_wait_accempty)
       const int half = (warp - kI8EpiWarp0) >> 2;  // two warps per sub-partition split the chunks
-#pragma unroll 1
-      for (int m0 = 8 * half; m0 < N; m0 += 16) {
-        if (m0 >= mu && m0 + 16 < N) continue;  // no output here (the last chunk still releases)
-        uint32_t v[kI8Levels][8];
-        I8_T0(tld);
+      constexpr int kCh = N / 16;                   // chunks of 8 outputs per warp
+      double sums[kCh][8];
+      I8_T0(tld);
 #pragma unroll
-        for (int L = 0; L < kI8Levels; ++L)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
-                         "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
-                       : "r"(tmem + lane_base + (uint32_t)(L * N + m0)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        I8_ACC(17, tld);
-        I8_T0(tcp);
-        if (m0 + 16 >= N) {  // this warp's last chunk is in registers
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(accempty);
-          I8_ACC(8, te0);
+      for (int c = 0; c < kCh; ++c) {
+        const int m0 = 8 * half + 16 * c;
+        if (m0 >= mu) continue;  // warp-uniform: no output in this chunk
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // 4 outputs at a time (register budget)
+          uint32_t v[kI8Levels][4];
+#pragma unroll
+          for (int L = 0; L < kI8Levels; ++L)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                         : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3])
+                         : "r"(tmem + lane_base + (uint32_t)(L * N + m0 + 4 * hh)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // sum_L S_L 2^(8L): each int32 level to fp64 exactly with the magic-number trick
+            // (one LOP + one DADD), then a Horner chain from the top level down
+            double sacc = i32_to_f64(v[kI8Levels - 1][u]);
+#pragma unroll
+            for (int L = kI8Levels - 2; L >= 0; --L) sacc = fma(sacc, 256.0, i32_to_f64(v[L][u]));
+            sums[c][4 * hh + u] = sacc;
+          }
         }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty);
+      I8_ACC(17, tld);
+      I8_ACC(8, te0);
+#pragma unroll
+      for (int c = 0; c < kCh; ++c) {
+        const int m0 = 8 * half + 16 * c;
+        if (m0 >= mu) continue;
+        I8_T0(tcp);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int m = m0 + u;
-          // sum_L S_L 2^(8L): each int32 level to fp64 exactly with the magic-number trick
-          // (one LOP + one DADD: the 64-bit integer conversions ran on a slow pipe and held
-          // the accumulator drain), then a Horner chain from the top level down
-          double sacc = i32_to_f64(v[kI8Levels - 1][u]);
-#pragma unroll
-          for (int L = kI8Levels - 2; L >= 0; --L) sacc = fma(sacc, 256.0, i32_to_f64(v[L][u]));
-          // scale 2^(ex + eq_m - 94 + 40) as two exact power-of-two products (branch-free, so
-          // the 8 outputs' chains interleave)
-          const double val = (sacc * sj) * qsc[m];
+          // scale 2^(ex + eq_m - 94 + 40) as two exact power-of-two products
+          const double val = (sums[c][u] * sj) * qsc[m];
           if (kInner) {  // Y(r, m, o): rows r of one slice are consecutive -- coalesced as is
             if (valid && m < mu) y[rrow + (long long)geo.R * (m + (long long)mu * ocol)] = val;
           } else {
