@@ -6,7 +6,13 @@
 #include <cstdlib>
 #include <vector>
 #include "../../paper_2303_11612_b200/csrc/kernels/orth.cu"
+#include "../../paper_2303_11612_b200/csrc/kernels/cholqr.cu"
 using namespace lmra_dev;
+namespace lmra_dev {  // host launchers orth.cu references but this benchmark never calls
+cudaError_t launch_transpose(const double*, long long, long long, double*, cudaStream_t) { return cudaErrorNotSupported; }
+cudaError_t scratch_alloc(void**, size_t, cudaStream_t) { return cudaErrorNotSupported; }
+void scratch_free(void*, cudaStream_t) {}
+}
 
 template <int RPL>
 __global__ void __launch_bounds__(512) qb(const double* A, int m, int s, int pivot, long long* out) {
@@ -67,6 +73,12 @@ void run(int m, int s, int pivot) {
 int main() {
   run<8>(250, 60, 0);
   run<8>(240, 60, 1);
+  run<8>(256, 50, 0);
+  run<4>(100, 50, 0);
+  run<4>(100, 50, 1);
+  run<4>(128, 50, 1);
+  run<2>(60, 30, 0);
+  run<2>(60, 30, 1);
   run<4>(120, 60, 0);
   run<2>(60, 60, 0);
   return 0;
