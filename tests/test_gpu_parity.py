@@ -110,7 +110,10 @@ def test_ttm_matches_oracle(gpu_ctx, orc, dims, mode, m):
 
 
 @pytest.mark.parametrize("dims", [(7, 5, 3), (33, 40, 17), (100, 3, 70), (1, 1000, 4), (65, 2, 2),
-                                  (512, 40, 3), (3, 3, 3, 3)])
+                                  (512, 40, 3), (3, 3, 3, 3),
+                                  # the TMA mode-0 pass: partial 32-row chunks, partial 128-column tiles,
+                                  # more tiles than SMs (a persistent CTA takes several)
+                                  (18, 77, 5), (1030, 129, 2), (64, 1000, 3), (200, 300, 1), (512, 256, 3, 2)])
 def test_column_sqnorms_bit_exact(gpu_ctx, orc, dims):
     from paper_2303_11612_b200 import device
     x = np.random.default_rng(2).standard_normal(int(np.prod(dims)))
