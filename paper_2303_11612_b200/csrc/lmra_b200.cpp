@@ -845,6 +845,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     if (!rng_done) {
       res->t_rng = now_ms() - tr0;
       rng_done = true;
+      if (diag_timing()) fprintf(stderr, "hostmark omega drawn %.4f ms (dispatched at %.4f)\n", now_ms() - t0, tr0 - t0);
     }
   };
 
@@ -920,6 +921,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     }
     ck(cudaEventCreateWithFlags(&om_ready, cudaEventDisableTiming), "event");
     ck(cudaEventRecord(om_ready, cs), "event");
+    if (diag_timing()) fprintf(stderr, "hostmark omega uploaded %.4f ms\n", now_ms() - t0);
   };
   struct EventGuard {
     cudaEvent_t& e;
@@ -1073,6 +1075,7 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     // sequence (~20 us) apart
     std::vector<DevBuf> sketches(N);
     for (size_t n = 0; n < N; ++n) sketches[n] = factor_power(engs[n], in.x, in.dims, n);
+    if (diag_timing()) fprintf(stderr, "hostmark power launched %.4f ms\n", now_ms() - t0);
     for (size_t n = 0; n < N; ++n) factors[n] = factor_orth(engs[n], in.x, in.dims, n, sketches[n]);
     // each contraction of the core waits only for its own mode's factor: the first one
     // (the long int8 / DMMA pass over the tensor) starts as soon as that mode's chain is done,
