@@ -580,6 +580,8 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
   if (threadIdx.x < 64) flags[threadIdx.x] = 0;
   if (threadIdx.x < 64) big[threadIdx.x] = 0;
   __syncthreads();
+  const bool early = tol > 0.0;  // a negative tol switches the early stop off (LMRA_JACOBI_EARLY=0)
+  tol = fabs(tol);
   const double tol2 = tol * tol;
   const double qthr2 = jacobi_quad_thr2(tol);
   bool converged = false;
@@ -674,7 +676,7 @@ __device__ bool reg_jacobi(double* G, int s, double* J, double tol, const QSmem&
       }
     }
     // flags[sweep] / big[sweep] were written before the sweep's last bar B
-    if (!flags[sweep] || !big[sweep]) {
+    if (!flags[sweep] || (early && !big[sweep])) {
       converged = true;
       if (threadIdx.x == 0) g_jacobi_sweeps = sweep + 1;
     }
@@ -757,6 +759,8 @@ __device__ bool narrow_jacobi_g(double* G, int s, double tol, double* slots, int
   const int p = l / L, h = l % L;
   const int P = (s + 1) / 2;
   const bool live = p < P;
+  const bool early = tol > 0.0;  // a negative tol switches the early stop off (LMRA_JACOBI_EARLY=0)
+  tol = fabs(tol);
   const double tol2 = tol * tol;
   int cT = live ? p : 1 << 20, cB = live ? p + P : 1 << 20;
   double T[H], B[H];
@@ -833,7 +837,7 @@ __device__ bool narrow_jacobi_g(double* G, int s, double tol, double* slots, int
       }
 #endif
     }
-    if (!__any_sync(0xffffffffu, rotated) || !__any_sync(0xffffffffu, big)) {
+    if (!__any_sync(0xffffffffu, rotated) || (early && !__any_sync(0xffffffffu, big))) {
       converged = true;
       if (l == 0) g_jacobi_sweeps = sweep + 1;
     }
@@ -1501,6 +1505,8 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   // product is rounding noise and further rotations cannot reduce it.
   double tol = 8.0 * s * 0x1.0p-53;
   if (const char* env = getenv("LMRA_JACOBI_TOL")) tol = atof(env);
+  if (const char* env = getenv("LMRA_JACOBI_EARLY"))  // =0: always run the verification sweep
+    if (env[0] == '0') tol = -tol;
   size_t used = 0;
   std::vector<OrthLevel> lv = plan_levels(I, s, &used);
   cudaError_t e;
@@ -1700,6 +1706,8 @@ cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, dou
   if (s < 1 || s > kOrthMaxS || mu < 1 || mu > s || I < s) return cudaErrorInvalidValue;
   double tol = 8.0 * s * 0x1.0p-53;
   if (const char* env = getenv("LMRA_JACOBI_TOL")) tol = atof(env);
+  if (const char* env = getenv("LMRA_JACOBI_EARLY"))  // =0: always run the verification sweep
+    if (env[0] == '0') tol = -tol;
   double* gbuf = work + orth_workspace_doubles(I, s);
   double* ur = gbuf + (size_t)s * s;
   int* gate = reinterpret_cast<int*>(gbuf + 2 * (size_t)s * s);
