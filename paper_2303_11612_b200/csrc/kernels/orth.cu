@@ -207,10 +207,22 @@ __device__ __forceinline__ void cw_store(const double (&a)[kCW][RPL], int rows, 
 // R's columns, so the left singular vectors are unaffected.
 // Barriers: one per step (the owner warp's v), plus one for the norms when pivoting.
 // ---------------------------------------------------------------------------
+#ifdef LMRA_QR_CLOCKS
+__device__ unsigned long long g_qrclk[8];  // microbenchmark only: warp-0 phase cycles per QR
+#define QR_T(v) const long long v = clock64()
+#define QR_ACC(i, a, b) \
+  if (threadIdx.x == 0) qacc[i] += (b) - (a)
+#else
+#define QR_T(v)
+#define QR_ACC(i, a, b)
+#endif
 template <int RPL>
 __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool pivot) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int kmax = min(m, s);
+#ifdef LMRA_QR_CLOCKS
+  long long qacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   int pA = l, pB = l + 32;  // physical column at logical positions l and l + 32
   unsigned done = 0;        // slots of this warp already factored
   if (pivot) {
@@ -225,28 +237,29 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
     if (l == 0)
 #pragma unroll
       for (int j = 0; j < kCW; ++j)
-        if (w + kQWarps * j < s) q.cn[w + kQWarps * j] = t[j];
+        if (w + kQWarps * j < s) {
+          q.cn[w + kQWarps * j] = t[j];
+          q.red[w + kQWarps * j] = t[j];  // the original norms (downdate safeguard; q.red is the sign fix's later)
+        }
     __syncthreads();
   }
   for (int k = 0; k < kmax; ++k) {
+    QR_T(c0);
     int pc = k;
     if (pivot) {  // every warp: the same argmax over the remaining logical positions
-      double best = (l >= k && l < s) ? q.cn[pA] : -1.0;
-      int pos = l;
-      const double vb2 = (l + 32 >= k && l + 32 < s) ? q.cn[pB] : -1.0;
-      if (vb2 > best) {
-        best = vb2;
-        pos = l + 32;
-      }
-#pragma unroll
-      for (int msk = 16; msk >= 1; msk >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, msk);
-        const int op = __shfl_xor_sync(0xffffffffu, pos, msk);
-        if (ob > best || (ob == best && op < pos)) {
-          best = ob;
-          pos = op;
-        }
-      }
+      // one warp max-reduction (REDUX) of 32-bit keys instead of a 5-level shuffle tree of
+      // (double, position) pairs (64-bit shuffles run at 0.5 per clock per SM, and all 16
+      // warps did this every step): key = the squared norm's top 25 bits (sign, exponent, 13
+      // mantissa bits -- non-negative doubles order like their bit patterns) above 127 - pos,
+      // so the largest norm wins and norms equal to ~1e-4 go to the first position
+      auto key = [](double v, int pos) -> unsigned {
+        const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(v) >> 32);
+        return (hi & ~0x7Fu) | (unsigned)(127 - pos);
+      };
+      const unsigned ka = (l >= k && l < s) ? key(q.cn[pA], l) : 0u;
+      const unsigned kb = (l + 32 >= k && l + 32 < s) ? key(q.cn[pB], l + 32) : 0u;
+      const unsigned best = __reduce_max_sync(0xffffffffu, ka > kb ? ka : kb);
+      const int pos = 127 - (int)(best & 0x7Fu);
       const int pk = __shfl_sync(0xffffffffu, k < 32 ? pA : pB, k & 31);
       pc = __shfl_sync(0xffffffffu, pos < 32 ? pA : pB, pos & 31);
       if (l == (k & 31)) {
@@ -262,6 +275,8 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
           pB = pk;
       }
     }
+    QR_T(c1);
+    QR_ACC(0, c0, c1);
     double* vb = q.vbuf + (k & 1) * kMaxBlockRows;
     if (w == pc % kQWarps) {  // owner warp: reflector of physical column pc
       const int oj = pc / kQWarps;
@@ -314,7 +329,11 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
           for (int i = 0; i < RPL; ++i) a[j][i] = col[i];
       if (l == 0) q.tau[k] = tk;
     }
+    QR_T(c2);
+    QR_ACC(1, c1, c2);
     __syncthreads();
+    QR_T(c3);
+    QR_ACC(2, c2, c3);
     const double tk = q.tau[k];
     bool act[kCW];
 #pragma unroll
@@ -339,23 +358,55 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
           for (int i = 0; i < RPL; ++i) a[j][i] = fma(-f, vr[i], a[j][i]);
         }
     }
+    QR_T(c4);
+    QR_ACC(3, c3, c4);
     if (pivot && k + 1 < kmax) {  // norms over rows > k of the remaining columns
-      double t[kCW];
+      // downdated (dgeqp3's rule): the reflector keeps each column's norm over rows >= k, so the
+      // norm over rows > k is the old one less the new row-k entry squared; lane k % 32 holds
+      // row k.  Recomputed (warp reduction) when the downdate cancelled below 1e-6 of the
+      // column's original squared norm.
+      const int ik = k >> 5;
+      int redo = 0;
 #pragma unroll
       for (int j = 0; j < kCW; ++j) {
-        t[j] = 0.0;
+        double rk = a[j][0];
 #pragma unroll
-        for (int i = 0; i < RPL; ++i)
-          if (l + 32 * i > k) t[j] = fma(a[j][i], a[j][i], t[j]);
+        for (int i = 1; i < RPL; ++i) rk = i == ik ? a[j][i] : rk;
+        if (act[j] && l == (k & 31)) {
+          const int c = w + kQWarps * j;
+          const double nv = q.cn[c] - rk * rk;
+          if (!(nv > 1e-6 * q.red[c])) redo = 1;
+          q.cn[c] = nv;
+        }
       }
-      warp_sum_cw(t);
-      if (l == 0)
+      if (__shfl_sync(0xffffffffu, redo, k & 31)) {
+        double t[kCW];
 #pragma unroll
-        for (int j = 0; j < kCW; ++j)
-          if (act[j]) q.cn[w + kQWarps * j] = t[j];
+        for (int j = 0; j < kCW; ++j) {
+          t[j] = 0.0;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i)
+            if (l + 32 * i > k) t[j] = fma(a[j][i], a[j][i], t[j]);
+        }
+        warp_sum_cw(t);
+        __syncwarp();
+        if (l == 0)
+#pragma unroll
+          for (int j = 0; j < kCW; ++j)
+            if (act[j]) {
+              q.cn[w + kQWarps * j] = t[j];
+              q.red[w + kQWarps * j] = t[j];
+            }
+      }
       __syncthreads();
     }
+    QR_T(c5);
+    QR_ACC(4, c4, c5);
   }
+#ifdef LMRA_QR_CLOCKS
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 5; ++i) g_qrclk[i] = qacc[i];
+#endif
   if (w == 0) {
     q.piv[l] = pivot ? pA : l;
     q.piv[l + 32] = pivot ? pB : l + 32;

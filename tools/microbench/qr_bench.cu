@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#define LMRA_QR_CLOCKS 1
 #include "../../paper_2303_11612_b200/csrc/kernels/orth.cu"
 #include "../../paper_2303_11612_b200/csrc/kernels/cholqr.cu"
 using namespace lmra_dev;
@@ -64,6 +65,10 @@ void run(int m, int s, int pivot) {
   cudaFuncSetAttribute(qb<RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int rep = 0; rep < 3; ++rep) qb<RPL><<<1, 512, smem>>>(d, m, s, pivot, out);
   cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long c[8];
+  cudaMemcpyFromSymbol(c, g_qrclk, sizeof(c));
+  printf("  per step (warp 0): pivot %.0f, reflector %.0f, barrier %.0f, update %.0f, norms %.0f\n", c[0] / (double)s,
+         c[1] / (double)s, c[2] / (double)s, c[3] / (double)s, c[4] / (double)s);
   printf("{\"rpl\": %d, \"m\": %d, \"s\": %d, \"pivot\": %d, \"qr_cycles\": %lld, \"qr_per_step\": %.0f, "
          "\"apply_cycles\": %lld, \"apply_per_step\": %.0f, \"err\": \"%s\"}\n",
          RPL, m, s, pivot, out[0], out[0] / (double)s, out[1], out[1] / (double)s, cudaGetErrorString(e));
