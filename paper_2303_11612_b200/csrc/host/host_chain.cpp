@@ -5,6 +5,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <iostream>
 #include <numeric>
 #include <stdexcept>
@@ -136,7 +137,10 @@ class Pool {
   // sleeping workers through the condition variable took ~50 us (cfg1's 3 x 3000 normals were
   // drawn in 60-85 us on 16 threads, ~17 us of work); decompositions issued back to back find
   // the workers still polling.  (OpenMP runtimes keep their workers spinning the same way.)
-  static constexpr double kSpinMs = 2.0;
+  static double spin_ms() {  // LMRA_POOL_SPIN_US overrides (0: sleep at once)
+    static const double v = getenv("LMRA_POOL_SPIN_US") ? atof(getenv("LMRA_POOL_SPIN_US")) / 1000.0 : 2.0;
+    return v;
+  }
   bool try_pop(std::function<void()>& f) {
     if (queued_.load(std::memory_order_acquire) == 0) return false;
     std::lock_guard<std::mutex> lk(mu_);
@@ -149,7 +153,7 @@ class Pool {
   void loop() {
     for (;;) {
       std::function<void()> f;
-      const auto spin_end = std::chrono::steady_clock::now() + std::chrono::microseconds((long)(kSpinMs * 1000));
+      const auto spin_end = std::chrono::steady_clock::now() + std::chrono::microseconds((long)(spin_ms() * 1000));
       while (!try_pop(f)) {
         if (stop_flag_.load(std::memory_order_acquire)) break;
         if (std::chrono::steady_clock::now() >= spin_end) break;
