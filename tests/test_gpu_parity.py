@@ -96,6 +96,8 @@ def test_device_relative_error_matches_oracle(gpu_ctx, orc, lmra, dims, core):
     ((40, 40, 3, 64), 2, 3), ((8, 900, 5), 0, 64), ((300, 7, 20), 1, 7), ((50, 20, 1), 2, 1),
     # small contractions split along K over both resident CTAs of an SM
     ((10, 200, 200), 1, 10), ((10, 10, 200), 2, 10), ((40, 40, 3, 512), 3, 40),
+    # the persistent streaming TTM (mode 0, m <= 32, >= 4 tiles per SM): even / odd K, every width
+    ((100, 400, 200), 0, 15), ((99, 400, 200), 0, 20), ((64, 300, 300), 0, 32), ((30, 700, 120), 0, 7),
 ])
 def test_ttm_matches_oracle(gpu_ctx, orc, dims, mode, m):
     from paper_2303_11612_b200 import device
@@ -203,7 +205,7 @@ def test_orth_cholqr_rank_deficient_falls_back(gpu_ctx, I, s, rank, mu):
 @pytest.mark.parametrize("strategy", ["A", "B"])
 @pytest.mark.parametrize("shape", [(37, 300, 9, 2), (1000, 400, 60, 2), (200, 5000, 15, 1), (3, 960, 3, 1),
                                    (513, 77, 33, 3), (511, 1000, 7, 1),
-                                   (3, 163840, 3, 1), (200, 40000, 15, 1)])
+                                   (3, 163840, 3, 1), (200, 40000, 15, 1), (120, 90001, 30, 1)])
 def test_gram_power_apply_matches_oracle(gpu_ctx, orc, strategy, shape):
     # split-K TTM / Gram launches on odd and even row counts (16-byte fibre loads need even I)
     from paper_2303_11612_b200 import device
