@@ -35,8 +35,13 @@ struct TtmCfg {
   static constexpr size_t SMEM = sizeof(double) * STAGE_ELEMS * STAGES;
 };
 
+// narrow outputs (M8 <= 24: the shrinks / core contractions of cfg1-3) hold few accumulators:
+// three CTAs per SM for more loads in flight (ncu, cfg3's first shrink: 24 % occupancy, DMMA
+// pipe and DRAM each ~half busy)
+template <int M8>
+constexpr int ttm_min_blocks() { return M8 <= 24 ? 3 : 2; }
 template <int M8, bool RCONTIG, int KC_, int ST_>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, ttm_min_blocks<M8>())
     ttm_kernel(const double* __restrict__ x, ModeView v, const double* __restrict__ bt, int m,
                int mtot, int koff, double* __restrict__ y, long long kper, Gather ga) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
