@@ -106,6 +106,10 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
 // and writes U = Q_C U_R(:, :mu) with the sign rule plus U_R' (s x mu) = U_R(:, :mu) with U's
 // column signs, so X x_n U^T = (X x_n Q_C^T) x_n U_R'^T.  Same workspace for both calls.
 size_t orth_split_workspace_doubles(long long I, int s);
+// urs (s x mu, column-major) = qc^T u for qc (I x s) and u (I x mu): a factor's coefficients in
+// the split form's basis (the factor itself from launch_orth)
+cudaError_t launch_basis_coeffs(const double* qc, long long I, int s, const double* u, int mu, double* urs,
+                                cudaStream_t st);
 cudaError_t launch_orth_basis(const double* c, long long I, int s, double* qc, double* work, cudaStream_t st);
 cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, double* u, double* ur_signed,
                                double* work, int* status, cudaStream_t st);

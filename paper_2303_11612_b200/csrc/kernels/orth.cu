@@ -1407,11 +1407,22 @@ static size_t tree_workspace_doubles(long long I, int s) {
 // cheaper (1.85 vs 2.11 ms) -- the CholeskyQR's three s-step Cholesky chains cost the same at
 // any I, the tree's leaf / stacked-R chains grow with I.  LMRA_ORTH_CHOLQR=0 / 1 forces it off /
 // on (any I > 256 the cluster takes).
-static bool use_cholqr(long long I, int s) {
+// CholeskyQR serves the split form's basis Q_C (an orthonormal basis of the sketch for the first
+// core contraction) above 768 rows.  The factors always come from the Householder path: the
+// CholeskyQR R loses the column-graded relative accuracy that column-pivoted Householder keeps,
+// and factors taken from it (pivoted QR + Jacobi on that R) missed the 1e-10 subspace contract on
+// some power-scheme sketches (sines 1.9e-10 / 7.8e-10 on 900 x 10 / 1000 x 10 sketches where the
+// Householder path gives 2e-14).  LMRA_ORTH_CHOLQR=0: no CholeskyQR at all; =1: CholeskyQR from
+// 257 rows, for the factors too (tests of that path).
+static bool use_cholqr(long long I, int s) {  // the basis phase
   const char* env = getenv("LMRA_ORTH_CHOLQR");
   if (env && env[0] == '0') return false;
   const long long min_rows = (env && env[0] == '1') ? kMaxBlockRows + 1 : 3 * kMaxBlockRows + 1;
   return I >= min_rows && cholqr_supported(I, s);
+}
+static bool use_cholqr_factor(long long I, int s) {  // the full orthonormalisation
+  const char* env = getenv("LMRA_ORTH_CHOLQR");
+  return env && env[0] == '1' && use_cholqr(I, s);
 }
 
 // [tree | Q_C (I x s) | R (s x s) | Y (s x s) | gate]
@@ -1564,7 +1575,7 @@ cudaError_t launch_orth(const double* c, long long I, int s, int mu, double* u, 
   if (lv.empty())
     return LMRA_RPL_DISPATCH(rpl_for(I), core)(c, (int)I, s, mu, u, (int)I, 1, status, tol, st, kOrthFull, nullptr,
                                                nullptr);
-  if (use_cholqr(I, s)) {
+  if (use_cholqr_factor(I, s)) {
     // C = Q_C R by CholeskyQR (cluster kernel), then the s x s chain on R: pivoted QR + Jacobi
     // -> Y = left singular vectors of R (s x mu), U = Q_C Y with the sign rule.  If the
     // CholeskyQR flags a failure, the same launches skip and the Householder tree below runs.
@@ -1750,6 +1761,35 @@ cudaError_t launch_orth_basis(const double* c, long long I, int s, double* qc, d
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// urs (s x mu) = Q_C^T U: the coefficients of the factor in the split form's basis, so that
+// X x_n U^T = (X x_n Q_C^T) x_n urs^T.  One CTA per factor column, a warp per basis column
+// (fixed-order lane partials + butterfly: deterministic).
+__global__ void __launch_bounds__(256) basis_coeffs_kernel(const double* __restrict__ qc, long long I, int s,
+                                                           const double* __restrict__ u, double* __restrict__ urs) {
+  pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
+  pdl_trigger();
+  const int b = blockIdx.x, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const double* ub = u + (size_t)I * b;
+  for (int a = w; a < s; a += 8) {
+    const double* qa = qc + (size_t)I * a;
+    double t0 = 0.0, t1 = 0.0;
+    long long i = l;
+    for (; i + 32 < I; i += 64) {
+      t0 = fma(qa[i], ub[i], t0);
+      t1 = fma(qa[i + 32], ub[i + 32], t1);
+    }
+    if (i < I) t0 = fma(qa[i], ub[i], t0);
+    double t = warp_sum(t0 + t1);
+    if (l == 0) urs[a + (size_t)s * b] = t;
+  }
+}
+
+cudaError_t launch_basis_coeffs(const double* qc, long long I, int s, const double* u, int mu, double* urs,
+                                cudaStream_t st) {
+  if (s < 1 || mu < 1 || I < 1) return cudaErrorInvalidValue;
+  return launch_pdl(basis_coeffs_kernel, dim3((unsigned)mu), dim3(256), 0, st, qc, I, s, u, urs);
 }
 
 cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, double* u, double* ur_signed,

@@ -1040,11 +1040,12 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
       });
       ck(cudaEventCreateWithFlags(&so.basis, cudaEventDisableTiming), "event");
       ck(cudaEventRecord(so.basis, s_), "event");
-      DevBuf u(I * mu, s_);
+      // the factor from the full Householder path (beside the contraction, off the critical path)
+      // and its coefficients in the basis: the CholeskyQR basis serves the contraction only
+      DevBuf u = e.orth(c.get(), I, s, mu, status_i + n);
       so.urs = DevBuf(s * mu, s_);
-      e.launch("orth_jacobi", [&] {
-        return lmra_dev::launch_orth_finish(so.qc.get(), (long long)I, (int)s, (int)mu, u.get(), so.urs.get(),
-                                            so.work.get(), status_i + n, s_);
+      e.launch("orth_coeffs", [&] {
+        return lmra_dev::launch_basis_coeffs(so.qc.get(), (long long)I, (int)s, u.get(), (int)mu, so.urs.get(), s_);
       });
       return u;
     }
@@ -1133,9 +1134,8 @@ void run_algorithm_impl(lmra_context* ctx, const RunInputs& in, lmra_result* res
     const double* w0 = (amm && cfg.regime != kUniform && d_w[0].get()) ? d_w[0].get() : nullptr;
     Engine::I8Chain chain;
     if (split_orth) {  // SMs for the orthonormalisations that run beside the first contraction
-      int jac = 1;  // the split mode's Jacobi (one CTA) + the other modes' (2-CTA clusters if s >= 48)
-      for (size_t n = 0; n < N; ++n)
-        if (n != split_mode) jac += r.sketch[n] >= 48 ? 2 : 1;
+      int jac = 0;  // every mode's Jacobi core (2-CTA clusters if s >= 48), the split mode's included
+      for (size_t n = 0; n < N; ++n) jac += r.sketch[n] >= 48 ? 2 : 1;
       lmra_dev::g_i8_reserved_sms = jac + 1;
     }
     for (size_t k = 0; k < idx.size(); ++k) {

@@ -383,6 +383,21 @@ def _split_case(lmra, orc, alg, dims):
     compare(gpu, ref, x.reshape(dims, order="F"))
 
 
+@pytest.mark.parametrize("dims,power", [([900, 30, 20], 1), ([1000, 40, 30], 2), ([800, 50, 20], 2)])
+@pytest.mark.parametrize("alg", ["alg1", "alg2"])
+def test_tall_sketch_factors_householder(gpu_ctx, lmra, orc, dims, power, alg):
+    # sketches above 768 rows: the factor comes from the Householder path even where CholeskyQR
+    # provides the split contraction's basis (CholeskyQR factors missed the contract on these:
+    # gap-aware sines 1.9e-10 / 7.8e-10)
+    rank = [5, 4, 3]
+    x = orc.gen_tucker_noise(dims, rank, 1e-2, 21)
+    kw = dict(rank=rank, seed=5, power=power)
+    ref = orc.run(alg, x, dims, orc.AlgoConfig(**kw))
+    out = compare(lmra.run_algorithm(alg, lmra.DenseTensor.from_flat(x, dims), lmra.AlgoConfig(**kw)), ref,
+                  x.reshape(dims, order="F"))
+    assert max(out["sines"]) <= 1e-12, out["sines"]
+
+
 @pytest.mark.parametrize("alg", ["alg4", "alg5"])
 @pytest.mark.parametrize("regime", ["uniform", "nearly_optimal"])
 def test_power_on_sampled_columns_in_place(gpu_ctx, lmra, orc, alg, regime, monkeypatch):
