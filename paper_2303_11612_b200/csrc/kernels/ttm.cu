@@ -563,7 +563,8 @@ static int device_sms() {
 // column j -- the I fibre values in registers, B^T (I x m) in shared memory, m outputs written
 // in Y's layout.  The DMMA kernel pads K to its 16-row chunk and runs one K stage per CTA, so
 // it was latency-bound (cfg5 shrink of the 3-extent mode: 43 us for 40 MB of traffic).
-// Same sum order as the DMMA path's single K chunk is not required: r ascending, fma chain.
+// Each output is an fma chain over r ascending (deterministic; the DMMA path sums in another
+// fixed order, both within the fp64 contract).
 constexpr int kSmallI = 8;
 template <int IS>
 __global__ void __launch_bounds__(256) ttm_small_kernel(const double* __restrict__ x, ModeView v,
