@@ -38,6 +38,10 @@ constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxBlockRows = 256;            // rows per CTA: 32 lanes x RPL (<= 8)
 constexpr int kOrthMaxS = 64;
 constexpr int kCW = kOrthMaxS / kQWarps;      // column slots per warp
+// Column c lives in warp c / kCW, slot c % kCW: narrow sketches occupy few warps and the others
+// skip every reduction (64-bit shuffles run at 0.5 per clock per SM: with columns dealt
+// round-robin, s = 15 kept all 16 warps reducing every Householder step).
+__device__ __forceinline__ int slot_col(int w, int j) { return w * kCW + j; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -173,7 +177,7 @@ __device__ __forceinline__ void cw_load(const double* t, int ldt, int rows, int 
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < kCW; ++j) {
-    const int c = w + kQWarps * j;
+    const int c = slot_col(w, j);
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = l + 32 * i;
@@ -188,7 +192,7 @@ __device__ __forceinline__ void cw_store(const double (&a)[kCW][RPL], int rows, 
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < kCW; ++j) {
-    const int c = w + kQWarps * j;
+    const int c = slot_col(w, j);
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = l + 32 * i;
@@ -237,9 +241,9 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
     if (l == 0)
 #pragma unroll
       for (int j = 0; j < kCW; ++j)
-        if (w + kQWarps * j < s) {
-          q.cn[w + kQWarps * j] = t[j];
-          q.red[w + kQWarps * j] = t[j];  // the original norms (downdate safeguard; q.red is the sign fix's later)
+        if (slot_col(w, j) < s) {
+          q.cn[slot_col(w, j)] = t[j];
+          q.red[slot_col(w, j)] = t[j];  // the original norms (downdate safeguard; q.red is the sign fix's later)
         }
     __syncthreads();
   }
@@ -278,8 +282,8 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
     QR_T(c1);
     QR_ACC(0, c0, c1);
     double* vb = q.vbuf + (k & 1) * kMaxBlockRows;
-    if (w == pc % kQWarps) {  // owner warp: reflector of physical column pc
-      const int oj = pc / kQWarps;
+    if (w == pc / kCW) {  // owner warp: reflector of physical column pc
+      const int oj = pc % kCW;
       done |= 1u << oj;
       double col[RPL];
 #pragma unroll
@@ -337,8 +341,11 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
     const double tk = q.tau[k];
     bool act[kCW];
 #pragma unroll
-    for (int j = 0; j < kCW; ++j) act[j] = (w + kQWarps * j < s) && !((done >> j) & 1u);
-    if (tk != 0.0) {
+    for (int j = 0; j < kCW; ++j) act[j] = (slot_col(w, j) < s) && !((done >> j) & 1u);
+    // warp-uniform: a warp whose columns are all factored (or past s) skips the reduction
+    const int nvalid = min(kCW, max(0, s - slot_col(w, 0)));
+    const bool any_act = (~done & ((1u << nvalid) - 1u)) != 0u;
+    if (tk != 0.0 && any_act) {
       double vr[RPL], t[kCW];
 #pragma unroll
       for (int i = 0; i < RPL; ++i) vr[i] = vb[l + 32 * i];
@@ -373,7 +380,7 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
 #pragma unroll
         for (int i = 1; i < RPL; ++i) rk = i == ik ? a[j][i] : rk;
         if (act[j] && l == (k & 31)) {
-          const int c = w + kQWarps * j;
+          const int c = slot_col(w, j);
           const double nv = q.cn[c] - rk * rk;
           if (!(nv > 1e-6 * q.red[c])) redo = 1;
           q.cn[c] = nv;
@@ -394,8 +401,8 @@ __device__ void reg_qr(double (&a)[kCW][RPL], int m, int s, const QSmem& q, bool
 #pragma unroll
           for (int j = 0; j < kCW; ++j)
             if (act[j]) {
-              q.cn[w + kQWarps * j] = t[j];
-              q.red[w + kQWarps * j] = t[j];
+              q.cn[slot_col(w, j)] = t[j];
+              q.red[slot_col(w, j)] = t[j];
             }
       }
       __syncthreads();
@@ -421,10 +428,10 @@ template <int RPL>
 __device__ void reg_apply(double (&y)[kCW][RPL], int mu, const double* Vs, int ldv,
                           const double* tau, int k_hi, int k_lo) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (w >= mu) return;
+  if (slot_col(w, 0) >= mu) return;
   bool act[kCW];
 #pragma unroll
-  for (int j = 0; j < kCW; ++j) act[j] = w + kQWarps * j < mu;
+  for (int j = 0; j < kCW; ++j) act[j] = slot_col(w, j) < mu;
   for (int k = k_hi - 1; k >= k_lo; --k) {
     const double tk = tau[k];
     if (tk == 0.0) continue;
@@ -460,7 +467,7 @@ __device__ void reg_argmax(const double (&y)[kCW][RPL], int m, int mu, double* b
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < kCW; ++j) {
-    const int c = w + kQWarps * j;
+    const int c = slot_col(w, j);
     if (c < mu) {
       double b = 0.0;
       int bi = -1;
@@ -1136,7 +1143,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
     // G = R^T (lower triangle), reflectors to Vs in logical column order
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
-      const int c = w + kQWarps * j;
+      const int c = slot_col(w, j);
       if (c >= s) continue;
       const int k = q.ipiv[c];
 #pragma unroll
@@ -1153,7 +1160,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
       double y[kCW][RPL];
 #pragma unroll
       for (int j = 0; j < kCW; ++j) {
-        const int c = w + kQWarps * j;
+        const int c = slot_col(w, j);
 #pragma unroll
         for (int i = 0; i < RPL; ++i) y[j][i] = (c < s && l + 32 * i == c) ? 1.0 : 0.0;
       }
@@ -1235,7 +1242,7 @@ __global__ void __launch_bounds__(kQThreads) orth_core_kernel(
   double y[kCW][RPL];
 #pragma unroll
   for (int j = 0; j < kCW; ++j) {
-    const int c = w + kQWarps * j;
+    const int c = slot_col(w, j);
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = l + 32 * i;
@@ -1294,7 +1301,7 @@ __global__ void __launch_bounds__(kQThreads) orth_leaf_apply_kernel(
   double y[kCW][RPL];
 #pragma unroll
   for (int j = 0; j < kCW; ++j) {
-    const int c = w + kQWarps * j;
+    const int c = slot_col(w, j);
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = l + 32 * i;
