@@ -1771,32 +1771,38 @@ cudaError_t launch_orth_basis(const double* c, long long I, int s, double* qc, d
 }
 
 // urs (s x mu) = Q_C^T U: the coefficients of the factor in the split form's basis, so that
-// X x_n U^T = (X x_n Q_C^T) x_n urs^T.  One CTA per factor column, a warp per basis column
-// (fixed-order lane partials + butterfly: deterministic).
+// X x_n U^T = (X x_n Q_C^T) x_n urs^T.  One warp per coefficient (grid mu x ceil(s / 8)), eight
+// independent loads per lane in flight (the loop over I was a latency chain: ~0.1 ms with a warp
+// walking eight dots), fixed-order sums (deterministic).
 __global__ void __launch_bounds__(256) basis_coeffs_kernel(const double* __restrict__ qc, long long I, int s,
                                                            const double* __restrict__ u, double* __restrict__ urs) {
   pdl_wait();  // the previous kernel's outputs (programmatic dependent launch)
   pdl_trigger();
   const int b = blockIdx.x, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int a = blockIdx.y * 8 + w;
+  if (a >= s) return;
   const double* ub = u + (size_t)I * b;
-  for (int a = w; a < s; a += 8) {
-    const double* qa = qc + (size_t)I * a;
-    double t0 = 0.0, t1 = 0.0;
-    long long i = l;
-    for (; i + 32 < I; i += 64) {
-      t0 = fma(qa[i], ub[i], t0);
-      t1 = fma(qa[i + 32], ub[i + 32], t1);
+  const double* qa = qc + (size_t)I * a;
+  double t = 0.0;
+  for (long long i0 = 0; i0 < I; i0 += 256) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long i = i0 + l + 32 * k;
+      v[k] = i < I ? qa[i] * ub[i] : 0.0;
     }
-    if (i < I) t0 = fma(qa[i], ub[i], t0);
-    double t = warp_sum(t0 + t1);
-    if (l == 0) urs[a + (size_t)s * b] = t;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += v[k];
   }
+  t = warp_sum(t);
+  if (l == 0) urs[a + (size_t)s * b] = t;
 }
 
 cudaError_t launch_basis_coeffs(const double* qc, long long I, int s, const double* u, int mu, double* urs,
                                 cudaStream_t st) {
   if (s < 1 || mu < 1 || I < 1) return cudaErrorInvalidValue;
-  return launch_pdl(basis_coeffs_kernel, dim3((unsigned)mu), dim3(256), 0, st, qc, I, s, u, urs);
+  return launch_pdl(basis_coeffs_kernel, dim3((unsigned)mu, (unsigned)((s + 7) / 8)), dim3(256), 0, st, qc, I, s, u,
+                    urs);
 }
 
 cudaError_t launch_orth_finish(const double* qc, long long I, int s, int mu, double* u, double* ur_signed,
