@@ -20,6 +20,7 @@ from conftest import gap_blocks, relative_error, subspace_sine  # noqa: E402
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 ALL_ALGS = len(sys.argv) > 3 and sys.argv[3] == "all"  # + the QR-proxy variants and the deterministic baselines
+LARGE = len(sys.argv) > 3 and sys.argv[3] == "large"  # 3-way tensors of >= 2^27 elements (the big-input paths)
 rng = np.random.default_rng(seed0)
 fails = 0
 
@@ -62,6 +63,11 @@ for case in range(n_cases):
     big = int(rng.integers(0, order))
     dims = [int(rng.integers(3, 40)) for _ in range(order)]
     dims[big] = int(rng.choice([int(rng.integers(40, 300)), int(rng.integers(770, 1100))]))
+    if LARGE:  # >= 2^27 elements: the split orthonormalisation, int8 contractions, CholeskyQR basis
+        order = 3
+        dims = [int(rng.integers(480, 1050)) for _ in range(3)]
+        while np.prod(dims) < (1 << 27):
+            dims[int(rng.integers(0, 3))] += 64
     rank = [max(1, min(d, int(rng.integers(1, 12)))) for d in dims]
     algs = ["alg1", "alg2", "alg4", "alg5"] + (["alg6", "alg7", "thosvd", "sthosvd", "hooi"] if ALL_ALGS else [])
     alg = str(rng.choice(algs))
