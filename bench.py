@@ -430,11 +430,11 @@ def bench_gpu(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.current_stream()
     ctx = P.Context(local_rank, stream.cuda_stream)
-    # light profiling in the timed region (events only around the streaming passes -- the norm
-    # pass and the contractions, what the roofline needs); the full per-phase
+    # light profiling in the timed region (events only around the mode-0 contraction, the
+    # roofline's dominant launch on the streaming configs); the full per-phase
     # breakdown comes from untimed profiled runs after it (per-phase event bookkeeping of the
     # per-mode chains costs host time between runs)
-    timed_prof = int(os.environ.get("LMRA_BENCH_PROFILE", "3"))  # 3: streaming passes only
+    timed_prof = int(os.environ.get("LMRA_BENCH_PROFILE", "3"))  # 3: the mode-0 contraction only
     ctx.set_profiling(timed_prof)
     bc = workload(args)
     cfg = algo_config(bc)

@@ -175,8 +175,7 @@ int lmra_result_timings(const lmra_result* r, double* out5);
 /* per-phase device time (CUDA events around each launch), only recorded when
  * lmra_context_set_profiling(ctx, 1) (every phase), (ctx, 2) (light: only the phases on the
  * context's own stream -- the norm pass and the contractions -- not the per-mode chains that
- * T-HOSVD runs on their own streams) or (ctx, 3) (streaming passes only: norms, core / shrink
- * contractions, on any algorithm).  Phases: norms, gather, power_half, power_gram, orth,
+ * T-HOSVD runs on their own streams) or (ctx, 3) (only the mode-0 core / shrink contraction).  Phases: norms, gather, power_half, power_gram, orth,
  * core_ttm<k> (k-th contraction of core_from_factors), shrink_ttm_m<n>. */
 int lmra_context_set_profiling(lmra_context* ctx, int on);
 /* keep host copies of the drawn samples / column norms in the result (default on) */

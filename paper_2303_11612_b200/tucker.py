@@ -245,8 +245,8 @@ class Context:
 
     def set_profiling(self, on):
         """Per-launch CUDA events -> _Result.phases(): True / 1 every phase, 2 only the
-        phases on the context's own stream (light), 3 only the streaming passes (norms,
-        core / shrink contractions), False / 0 none."""
+        phases on the context's own stream (light), 3 only the mode-0 core / shrink
+        contraction, False / 0 none."""
         level = on if isinstance(on, int) and not isinstance(on, bool) else int(bool(on))
         check(lib.lmra_context_set_profiling(self.handle, level))
 
